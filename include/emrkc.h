@@ -1,0 +1,265 @@
+/*
+ * emrkc.h — C ABI of the B200-native emRKC monodomain time step.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (arxiv/paper_2401_01745, /root/reference/proj). The reference binds its
+ * integrators to the problem through std::function callbacks bundled in
+ * `SplitRhs` (P/include/mrkc/multirate.hpp:25-35) and the virtual
+ * `MonodomainProblem` / `IonicModel` interfaces
+ * (P/include/mrkc/monodomain.hpp:93-176, P/include/mrkc/ionic.hpp:17-53).
+ * Every entry point below replaces one reference function; the comment on
+ * each names it (P/ = /root/reference/proj/).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no C++ or torch types cross the ABI.
+ *  - State vectors use the reference `Vec` layout byte-for-byte:
+ *    [V | gate_0 | ... | gate_{g-1} | aux_0 | ...], each block n_nodes long,
+ *    node index i0 + n0*(i1 + n1*i2) (P/include/mrkc/monodomain.hpp:51-60,
+ *    P/src/monodomain.cpp:36-44). With a partition, the blocks hold the
+ *    local z-slab only (same layout, n_nodes = local node count).
+ *  - Units are the reference's: mm, ms, mV, mS/mm, uF/mm^2, uA/mm^3.
+ *  - Every function returns an emrkc_status. EMRKC_EINVAL maps to the
+ *    reference's std::invalid_argument / ConfigError, EMRKC_ENONFINITE to
+ *    NumericalAbort. emrkc_last_error() returns the message.
+ *  - A handle owns one device and one CUDA stream; it is not thread-safe,
+ *    distinct handles may be driven from distinct host threads.
+ *  - There is no CPU fallback: every compute entry point runs sm_100a
+ *    kernels and fails with EMRKC_ECUDA when no device is usable.
+ */
+#ifndef EMRKC_H
+#define EMRKC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMRKC_ABI_VERSION 1
+
+typedef enum emrkc_status {
+  EMRKC_OK = 0,
+  EMRKC_EINVAL = 1,     /* std::invalid_argument / ConfigError */
+  EMRKC_ENONFINITE = 2, /* NumericalAbort (non-finite stage / norm guard) */
+  EMRKC_ECUDA = 3,      /* CUDA runtime failure or no usable device */
+  EMRKC_ESTATE = 4,     /* call out of order (e.g. no state uploaded) */
+  EMRKC_ENOMEM = 5
+} emrkc_status;
+
+enum { EMRKC_MODEL_HH = 0 };          /* make_ionic_model("hh"), P/src/ionic.cpp:125-128 */
+enum { EMRKC_RHS_F = 0, EMRKC_RHS_S = 1 }; /* SplitRhs::f_F / f_S */
+enum { EMRKC_VARIANT_STANDARD = 0 };  /* EmrkcVariant::standard, P/include/mrkc/multirate.hpp:37-40 */
+enum {
+  EMRKC_ABORT_NONE = 0,
+  EMRKC_ABORT_NONFINITE = 1,  /* check_stage_finite, P/src/cheb.cpp:73-80 */
+  EMRKC_ABORT_NORM_GUARD = 2  /* ||V||_inf > 1e6, P/src/simulate.cpp:222-227 */
+};
+
+/* Problem description. Replaces the arguments of
+ * MonodomainOperator(Grid, Conductivity, IonicModel, StimulusProtocol)
+ * (P/include/mrkc/monodomain.hpp:121-123) with plain data. The grid is
+ * given by node counts (make_grid builds extent/dx + 1 nodes per axis,
+ * P/src/monodomain.cpp:9-32; extent = (n-1)*dx here). */
+typedef struct emrkc_problem {
+  int32_t dim;                 /* 1, 2 or 3 */
+  int32_t model;               /* EMRKC_MODEL_HH */
+  int64_t n[3];                /* nodes per axis (1 on unused axes) */
+  double dx[3];                /* [mm] */
+  double sigma[3];             /* Conductivity::sigma [mS/mm] */
+  double chi;                  /* [1/mm] */
+  double C_m;                  /* [uF/mm^2] */
+  double stim_chi_amplitude;   /* StimulusProtocol::chi_amplitude [uA/mm^3] */
+  double stim_lo[3];           /* box_lo [mm] */
+  double stim_hi[3];           /* box_hi [mm] */
+  double stim_t0, stim_t1;     /* window [ms], inclusive */
+} emrkc_problem;
+
+/* z-slab ownership along the slowest axis (axis dim-1). [z_begin, z_end).
+ * A null partition means the whole grid. No reference counterpart: the
+ * reference never partitions. */
+typedef struct emrkc_partition {
+  int64_t z_begin;
+  int64_t z_end;
+} emrkc_partition;
+
+/* MultirateStepReport (P/include/mrkc/multirate.hpp:44-51) plus the abort
+ * information the reference carries in NumericalAbort. */
+typedef struct emrkc_step_report {
+  int32_t s;            /* outer stages  (get_stages(dt, rho_S))      */
+  int32_t m;            /* inner stages  (get_stages(eta, rho_F))     */
+  double eta;           /* 2 dt / ell_s                                */
+  double ell_s;
+  double ell_m;
+  int64_t n_fF;         /* EvalCounters deltas of this step            */
+  int64_t n_fS;
+  int64_t n_exp;
+  int32_t abort_kind;   /* EMRKC_ABORT_*                               */
+  int32_t abort_stage;  /* stage index named in the NumericalAbort msg */
+  int32_t abort_inner;  /* 1: raised by the inner iteration            */
+  int32_t abort_outer_stage; /* outer stage j in which it happened     */
+} emrkc_step_report;
+
+/* RunResult (P/include/mrkc/simulate.hpp:21-45) fields that the emRKC
+ * branch of run_simulation fills (P/src/simulate.cpp:95-234). */
+typedef struct emrkc_run_result {
+  int64_t n_steps;      /* requested steps                              */
+  int64_t steps_done;   /* steps whose result was accepted into y       */
+  int32_t aborted;
+  int32_t abort_kind;   /* EMRKC_ABORT_*                                */
+  int64_t abort_step;   /* -1 when not aborted                          */
+  int32_t abort_stage;
+  int32_t abort_inner;
+  double gate_min;      /* track_gate_range over the run                */
+  double gate_max;
+  int64_t n_fF;         /* EvalCounters                                  */
+  int64_t n_fS;
+  int64_t n_exp;
+  int32_t s;            /* per-step plan (constant: rho is frozen)      */
+  int32_t m;
+  double eta;
+  double device_ms;     /* CUDA-event time of the stepping loop         */
+} emrkc_run_result;
+
+/* RhoEstimate (P/include/mrkc/spectral.hpp:10-16). */
+typedef struct emrkc_rho_result {
+  double rho;           /* safety-multiplied estimate [1/ms] */
+  int32_t iterations;
+  int32_t converged;
+  double safety;        /* 1.05 */
+} emrkc_rho_result;
+
+typedef struct emrkc_handle emrkc_handle;
+
+/* ---- library / host-side numerics (no device needed) ------------------ */
+
+const char* emrkc_version(void);
+
+/* Thread-local message of the last failing call made without a handle
+ * (or with a null handle); see also emrkc_last_error(). */
+const char* emrkc_global_error(void);
+
+/* get_stages(dt, rho, epsilon) — P/src/cheb.cpp:25-39. */
+int emrkc_get_stages(double dt, double rho, double epsilon, int32_t* s,
+                     double* ell, double* beta);
+
+/* rkc_coeffs(s, epsilon) — P/src/cheb.cpp:41-69. Arrays have s+1 entries
+ * (any may be null). */
+int emrkc_rkc_coeffs(int32_t s, double epsilon, double* omega0,
+                     double* omega1, double* b, double* mu, double* nu,
+                     double* kappa, double* c);
+
+/* plan_step (P/src/multirate.cpp:129-135): fills s, m, eta, ell_s, ell_m
+ * and the per-step counters of *plan. */
+int emrkc_plan_step(double dt, double rho_F, double rho_S, double epsilon,
+                    emrkc_step_report* plan);
+
+/* IonicModel::n_gates/n_aux — P/include/mrkc/ionic.hpp:22-23. */
+int emrkc_model_info(int32_t model, int32_t* n_gates, int32_t* n_aux);
+
+/* IonicModel::resting_state — P/src/ionic.cpp:42-77. gates: n_gates. */
+int emrkc_resting_state(int32_t model, double* V, double* gates);
+
+/* StateLayout::size() of the (local) state — P/include/mrkc/monodomain.hpp:56. */
+int64_t emrkc_state_len(const emrkc_problem* p, const emrkc_partition* part);
+
+/* Balanced z-slab split of n_z planes over nranks (uneven allowed). */
+int emrkc_partition_slab(int64_t n_z, int32_t nranks, int32_t rank,
+                         emrkc_partition* out);
+
+/* ---- device handle ----------------------------------------------------- */
+
+/* Builds the device operator: replaces constructing MonodomainOperator
+ * (P/src/monodomain.cpp:305-311) and binding SplitRhs
+ * (P/src/simulate.cpp:153-157). part may be null (whole grid). */
+int emrkc_create(const emrkc_problem* p, int32_t device,
+                 const emrkc_partition* part, emrkc_handle** out);
+void emrkc_destroy(emrkc_handle* h);
+const char* emrkc_last_error(const emrkc_handle* h);
+int64_t emrkc_local_len(const emrkc_handle* h);
+
+/* Upload / download the (local) state in reference Vec layout. */
+int emrkc_set_state(emrkc_handle* h, const double* y, int64_t len);
+int emrkc_get_state(emrkc_handle* h, double* y, int64_t len);
+/* Device pointer of the current state (valid until the next step/run). */
+int emrkc_state_device_ptr(emrkc_handle* h, double** dptr);
+int emrkc_synchronize(emrkc_handle* h);
+
+/* MonodomainOperator::f_F / f_S (P/src/monodomain.cpp:207-221) and
+ * exp_part (:246-256) on host buffers, evaluated on the device. Whole-grid
+ * handles only. */
+int emrkc_eval_rhs(emrkc_handle* h, int32_t which, double t,
+                   const double* y, double* out, int64_t len);
+int emrkc_exp_part(emrkc_handle* h, const double* y, double* lambda,
+                   double* y_inf, int64_t len);
+
+/* estimate_spectral_radius(t, y, f_F|f_S, v0, rho0) on the current state
+ * (P/src/spectral.cpp:26-71). v0 null selects the reference's seeded
+ * direction (mt19937_64(0x9e3779b97f4a7c15) U(-1,1), :16-22). v_out
+ * (nullable) receives the final direction. Whole-grid handles only;
+ * partitioned handles use emrkc_group_estimate_rho. */
+int emrkc_estimate_rho(emrkc_handle* h, int32_t which, double t,
+                       const double* v0, double rho0, emrkc_rho_result* out,
+                       double* v_out);
+
+/* emrkc_step(t, y, dt, rhs, epsilon, variant, report)
+ * (P/src/multirate.cpp:173-189) on the device-resident state. On a
+ * non-finite stage it returns EMRKC_ENONFINITE, leaves the state
+ * unchanged and fills report->abort_* (the NumericalAbort). */
+int emrkc_step(emrkc_handle* h, double t, double dt, double epsilon,
+               int32_t variant, double rho_F, double rho_S,
+               emrkc_step_report* report);
+
+/* emrkc_step over host buffers: the per-call drop-in of
+ * `Vec emrkc_step(t, const Vec& y, ...)` — copies y in, steps, copies the
+ * result out (y_out may alias y_in). */
+int emrkc_step_host(emrkc_handle* h, double t, const double* y_in,
+                    double* y_out, int64_t len, double dt, double epsilon,
+                    int32_t variant, double rho_F, double rho_S,
+                    emrkc_step_report* report);
+
+/* The emRKC branch of run_simulation's stepping loop
+ * (P/src/simulate.cpp:176-229): steps step0 .. step0+nsteps-1 with
+ * t = step*dt, abort on non-finite stages, ||V||_inf > 1e6 guard and gate
+ * range tracking — all on the device, with no per-step host sync. */
+int emrkc_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
+              double epsilon, int32_t variant, double rho_F, double rho_S,
+              emrkc_run_result* res);
+
+/* ---- z-slab groups (multi-slab / multi-GPU) ---------------------------- */
+
+/* A group steps the handles of consecutive z-slabs (ordered bottom to top)
+ * in lockstep; V halo planes are written by each producing kernel straight
+ * into the neighbour's ghost planes (peer stores over NVLink when the
+ * neighbour lives on another device). Handles may share one device. */
+typedef struct emrkc_group emrkc_group;
+int emrkc_group_create(emrkc_handle* const* hs, int32_t n, emrkc_group** out);
+void emrkc_group_destroy(emrkc_group* g);
+int emrkc_group_estimate_rho(emrkc_group* g, int32_t which, double t,
+                             emrkc_rho_result* out);
+int emrkc_group_run(emrkc_group* g, int64_t step0, int64_t nsteps, double dt,
+                    double epsilon, int32_t variant, double rho_F,
+                    double rho_S, emrkc_run_result* res);
+
+/* ---- multi-process (one process per GPU) ------------------------------- */
+
+/* Cross-process ghost-plane link: each rank exports an opaque blob (CUDA
+ * IPC handles of its ghost buffers and events), the host exchanges blobs
+ * (e.g. torch.distributed all_gather_object), and each rank imports its
+ * lower (side 0) and upper (side 1) neighbour's blob. */
+int64_t emrkc_ipc_blob_size(void);
+int emrkc_ipc_export(emrkc_handle* h, void* blob, int64_t len);
+int emrkc_ipc_import(emrkc_handle* h, int32_t side, const void* blob,
+                     int64_t len);
+/* Local part of a distributed run: like emrkc_run, but the halo planes go
+ * to the imported neighbours; the caller reduces the returned per-rank
+ * result (max of abort flags/steps, min/max of gate range). */
+int emrkc_dist_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
+                   double epsilon, int32_t variant, double rho_F,
+                   double rho_S, emrkc_run_result* res);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* EMRKC_H */

@@ -1,0 +1,205 @@
+"""ctypes view of the C ABI declared in ``include/emrkc.h``.
+
+Plain data structures and prototypes only; the compute lives in
+``libemrkc_b200.so`` (hand-written sm_100a CUDA, built by
+``__graft_entry__.build()``). Loading fails loudly when the library is
+missing: there is no Python or CPU fallback for the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libemrkc_b200.so")
+
+# ---- enums (include/emrkc.h) ------------------------------------------------
+EMRKC_OK = 0
+EMRKC_EINVAL = 1
+EMRKC_ENONFINITE = 2
+EMRKC_ECUDA = 3
+EMRKC_ESTATE = 4
+EMRKC_ENOMEM = 5
+
+EMRKC_MODEL_HH = 0
+EMRKC_RHS_F = 0
+EMRKC_RHS_S = 1
+EMRKC_VARIANT_STANDARD = 0
+EMRKC_ABORT_NONE = 0
+EMRKC_ABORT_NONFINITE = 1
+EMRKC_ABORT_NORM_GUARD = 2
+
+
+class Problem(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32),
+        ("model", C.c_int32),
+        ("n", C.c_int64 * 3),
+        ("dx", C.c_double * 3),
+        ("sigma", C.c_double * 3),
+        ("chi", C.c_double),
+        ("C_m", C.c_double),
+        ("stim_chi_amplitude", C.c_double),
+        ("stim_lo", C.c_double * 3),
+        ("stim_hi", C.c_double * 3),
+        ("stim_t0", C.c_double),
+        ("stim_t1", C.c_double),
+    ]
+
+    @property
+    def n_nodes(self) -> int:
+        nn = 1
+        for a in range(self.dim):
+            nn *= int(self.n[a])
+        return nn
+
+    @property
+    def shape(self):
+        """numpy shape of one SoA block, slowest axis first."""
+        return tuple(int(self.n[a]) for a in reversed(range(self.dim)))
+
+    def state_len(self) -> int:
+        return 4 * self.n_nodes
+
+    def describe(self) -> dict:
+        return {
+            "dim": self.dim,
+            "n": [int(self.n[a]) for a in range(3)],
+            "dx": list(self.dx),
+            "sigma": list(self.sigma),
+            "chi": self.chi,
+            "C_m": self.C_m,
+            "stim_chi_amplitude": self.stim_chi_amplitude,
+            "stim_lo": list(self.stim_lo),
+            "stim_hi": list(self.stim_hi),
+            "stim_t0": self.stim_t0,
+            "stim_t1": self.stim_t1,
+        }
+
+
+class Partition(C.Structure):
+    _fields_ = [("z_begin", C.c_int64), ("z_end", C.c_int64)]
+
+
+class StepReport(C.Structure):
+    _fields_ = [
+        ("s", C.c_int32),
+        ("m", C.c_int32),
+        ("eta", C.c_double),
+        ("ell_s", C.c_double),
+        ("ell_m", C.c_double),
+        ("n_fF", C.c_int64),
+        ("n_fS", C.c_int64),
+        ("n_exp", C.c_int64),
+        ("abort_kind", C.c_int32),
+        ("abort_stage", C.c_int32),
+        ("abort_inner", C.c_int32),
+        ("abort_outer_stage", C.c_int32),
+    ]
+
+
+class RunResult(C.Structure):
+    _fields_ = [
+        ("n_steps", C.c_int64),
+        ("steps_done", C.c_int64),
+        ("aborted", C.c_int32),
+        ("abort_kind", C.c_int32),
+        ("abort_step", C.c_int64),
+        ("abort_stage", C.c_int32),
+        ("abort_inner", C.c_int32),
+        ("gate_min", C.c_double),
+        ("gate_max", C.c_double),
+        ("n_fF", C.c_int64),
+        ("n_fS", C.c_int64),
+        ("n_exp", C.c_int64),
+        ("s", C.c_int32),
+        ("m", C.c_int32),
+        ("eta", C.c_double),
+        ("device_ms", C.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class RhoResult(C.Structure):
+    _fields_ = [
+        ("rho", C.c_double),
+        ("iterations", C.c_int32),
+        ("converged", C.c_int32),
+        ("safety", C.c_double),
+    ]
+
+
+DP = C.POINTER(C.c_double)
+I32P = C.POINTER(C.c_int32)
+
+
+def dptr(a: np.ndarray | None):
+    """double* of a C-contiguous float64 array (None -> NULL)."""
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"], "need contiguous float64"
+    return a.ctypes.data_as(DP)
+
+
+# Every function the header declares: name -> (restype, argtypes).
+PROTOTYPES = {
+    "emrkc_version": (C.c_char_p, []),
+    "emrkc_global_error": (C.c_char_p, []),
+    "emrkc_get_stages": (C.c_int, [C.c_double, C.c_double, C.c_double, I32P, DP, DP]),
+    "emrkc_rkc_coeffs": (C.c_int, [C.c_int32, C.c_double, DP, DP, DP, DP, DP, DP, DP]),
+    "emrkc_plan_step": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(StepReport)]),
+    "emrkc_model_info": (C.c_int, [C.c_int32, I32P, I32P]),
+    "emrkc_resting_state": (C.c_int, [C.c_int32, DP, DP]),
+    "emrkc_state_len": (C.c_int64, [C.POINTER(Problem), C.POINTER(Partition)]),
+    "emrkc_partition_slab": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(Partition)]),
+    "emrkc_create": (C.c_int, [C.POINTER(Problem), C.c_int32, C.POINTER(Partition), C.POINTER(C.c_void_p)]),
+    "emrkc_destroy": (None, [C.c_void_p]),
+    "emrkc_last_error": (C.c_char_p, [C.c_void_p]),
+    "emrkc_local_len": (C.c_int64, [C.c_void_p]),
+    "emrkc_set_state": (C.c_int, [C.c_void_p, DP, C.c_int64]),
+    "emrkc_get_state": (C.c_int, [C.c_void_p, DP, C.c_int64]),
+    "emrkc_state_device_ptr": (C.c_int, [C.c_void_p, C.POINTER(DP)]),
+    "emrkc_synchronize": (C.c_int, [C.c_void_p]),
+    "emrkc_eval_rhs": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, DP, DP, C.c_int64]),
+    "emrkc_exp_part": (C.c_int, [C.c_void_p, DP, DP, DP, C.c_int64]),
+    "emrkc_estimate_rho": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, DP, C.c_double, C.POINTER(RhoResult), DP]),
+    "emrkc_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(StepReport)]),
+    "emrkc_step_host": (C.c_int, [C.c_void_p, C.c_double, DP, DP, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(StepReport)]),
+    "emrkc_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
+    "emrkc_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_void_p)]),
+    "emrkc_group_destroy": (None, [C.c_void_p]),
+    "emrkc_group_estimate_rho": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.POINTER(RhoResult)]),
+    "emrkc_group_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
+    "emrkc_ipc_blob_size": (C.c_int64, []),
+    "emrkc_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+    "emrkc_ipc_import": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]),
+    "emrkc_dist_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
+}
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load libemrkc_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError(
+            f"{p} not found: build the CUDA library first "
+            "(python -c 'import __graft_entry__ as g; g.build()'). "
+            "There is no CPU fallback."
+        )
+    lib = C.CDLL(p)
+    for name, (res, args) in PROTOTYPES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib

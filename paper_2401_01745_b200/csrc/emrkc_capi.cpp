@@ -1,0 +1,1429 @@
+// emrkc_capi.cpp — host side of libemrkc_b200.so: the C ABI of
+// include/emrkc.h. Planning, RKC coefficients, device buffers, the step /
+// run loops, the device power iteration and z-slab groups.
+//
+// The host numerics restate the reference's scalar routines (get_stages,
+// rkc_coeffs, resting_state, P/src/cheb.cpp:8-69, P/src/ionic.cpp:14-116)
+// in the same evaluation order so that s, m, eta and every coefficient are
+// bit-identical; all per-node work runs in kernels.cu. There is no CPU
+// fallback: without a device every compute call fails with EMRKC_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <array>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/emrkc.h"
+#include "kernels.h"
+
+using emrkc_k::Geom;
+using emrkc_k::Halo;
+using emrkc_k::kNoEvent;
+using emrkc_k::StageArgs;
+
+namespace {
+
+thread_local std::string g_global_err;
+
+int set_global(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_global_err = buf;
+  return code;
+}
+
+// ---------------------------------------------------------------------------
+// Host numerics (restated from the reference, same operation order)
+// ---------------------------------------------------------------------------
+struct Cheb {
+  double value, derivative;
+};
+
+Cheb cheb_T(int degree, double x) {  // P/src/cheb.cpp:8-23
+  double tm1 = 1.0, dm1 = 0.0;
+  if (degree == 0) return {tm1, dm1};
+  double t = x, d = 1.0;
+  for (int j = 2; j <= degree; ++j) {
+    const double tj = 2.0 * x * t - tm1;
+    const double dj = 2.0 * t + 2.0 * x * d - dm1;
+    tm1 = t;
+    dm1 = d;
+    t = tj;
+    d = dj;
+  }
+  return {t, d};
+}
+
+struct Coeffs {
+  int s = 0;
+  double omega0 = 0, omega1 = 0;
+  std::vector<double> b, mu, nu, kappa, c;
+};
+
+int stages(double dt, double rho, double eps, int32_t* s, double* ell,
+           double* beta) {  // P/src/cheb.cpp:25-39
+  if (!std::isfinite(dt) || !std::isfinite(rho) || !std::isfinite(eps))
+    return set_global(EMRKC_EINVAL, "get_stages: non-finite input");
+  if (dt <= 0.0) return set_global(EMRKC_EINVAL, "get_stages: dt must be > 0");
+  if (rho < 0.0) return set_global(EMRKC_EINVAL, "get_stages: rho must be >= 0");
+  if (eps < 0.0 || eps >= 1.5)
+    return set_global(EMRKC_EINVAL, "get_stages: damping must be in [0, 1.5)");
+  const double b = 2.0 - 4.0 * eps / 3.0;
+  const double q = std::ceil(std::sqrt(dt * rho / b));
+  if (!(q < 1e6))
+    return set_global(EMRKC_EINVAL, "get_stages: stage count overflow");
+  const int si = std::max(1, static_cast<int>(q));
+  *s = si;
+  *ell = b * static_cast<double>(si) * si;
+  *beta = b;
+  return EMRKC_OK;
+}
+
+int coeffs(int s, double eps, Coeffs* k) {  // P/src/cheb.cpp:41-69
+  if (s < 1) return set_global(EMRKC_EINVAL, "rkc_coeffs: s must be >= 1");
+  k->s = s;
+  k->omega0 = 1.0 + eps / (static_cast<double>(s) * s);
+  const Cheb ts = cheb_T(s, k->omega0);
+  k->omega1 = ts.value / ts.derivative;
+  k->b.assign(s + 1, 0.0);
+  for (int j = 0; j <= s; ++j) k->b[j] = 1.0 / cheb_T(j, k->omega0).value;
+  k->mu.assign(s + 1, 0.0);
+  k->nu.assign(s + 1, 0.0);
+  k->kappa.assign(s + 1, 0.0);
+  k->c.assign(s + 1, 0.0);
+  k->mu[1] = k->omega1 / k->omega0;
+  k->c[1] = k->mu[1];
+  for (int j = 2; j <= s; ++j) {
+    k->mu[j] = 2.0 * k->omega1 * k->b[j] / k->b[j - 1];
+    k->nu[j] = 2.0 * k->omega0 * k->b[j] / k->b[j - 1];
+    k->kappa[j] = -k->b[j] / k->b[j - 2];
+    k->c[j] = k->nu[j] * k->c[j - 1] + k->kappa[j] * k->c[j - 2] + k->mu[j];
+  }
+  return EMRKC_OK;
+}
+
+// HH on the host, for the resting state only (P/src/ionic.cpp:14-116).
+double lin_exp_ratio(double x, double k) {
+  const double u = x / k;
+  if (std::abs(u) < 1e-4) return k * (1.0 + u * (0.5 + u / 12.0));
+  return x / (1.0 - std::exp(-u));
+}
+void hh_gate_coeffs(double V, double* lam, double* zinf) {
+  double a[3], b[3];
+  a[0] = 0.1 * lin_exp_ratio(V + 40.0, 10.0);
+  b[0] = 4.0 * std::exp(-(V + 65.0) / 18.0);
+  a[1] = 0.07 * std::exp(-(V + 65.0) / 20.0);
+  b[1] = 1.0 / (1.0 + std::exp(-(V + 35.0) / 10.0));
+  a[2] = 0.01 * lin_exp_ratio(V + 55.0, 10.0);
+  b[2] = 0.125 * std::exp(-(V + 65.0) / 80.0);
+  for (int g = 0; g < 3; ++g) {
+    lam[g] = -(a[g] + b[g]);
+    zinf[g] = a[g] / (a[g] + b[g]);
+  }
+}
+double hh_current(double V, const double* z) {
+  const double m = z[0], h = z[1], n = z[2];
+  return 1.2 * m * m * m * h * (V - 50.0) + 0.36 * n * n * n * n * (V - -77.0) +
+         0.003 * (V - -54.387);
+}
+
+// Per-step plan: plan_step (P/src/multirate.cpp:129-135) + coefficients.
+struct Plan {
+  double dt = -1, eps = -1, rho_F = -1, rho_S = -1;
+  int s = 0, m = 0;
+  double eta = 0, ell_s = 0, ell_m = 0, beta = 0;
+  Coeffs outer, inner;
+  std::vector<double> in_mueta;  // mu'_k * eta (rkc_iteration's k.mu[j]*dt)
+  std::vector<double> mudt;      // mu_j * dt
+};
+
+int make_plan(double dt, double rho_F, double rho_S, double eps, Plan* p) {
+  if (!(dt > 0.0)) return set_global(EMRKC_EINVAL, "emrkc_step: dt must be > 0");
+  int rc = stages(dt, rho_S, eps, &p->s, &p->ell_s, &p->beta);
+  if (rc) return rc;
+  p->eta = 2.0 * dt / p->ell_s;
+  rc = stages(p->eta, rho_F, eps, &p->m, &p->ell_m, &p->beta);
+  if (rc) return rc;
+  if ((rc = coeffs(p->s, eps, &p->outer))) return rc;
+  if ((rc = coeffs(p->m, eps, &p->inner))) return rc;
+  p->in_mueta.assign(p->m + 1, 0.0);
+  for (int k = 1; k <= p->m; ++k) p->in_mueta[k] = p->inner.mu[k] * p->eta;
+  p->mudt.assign(p->s + 1, 0.0);
+  for (int j = 1; j <= p->s; ++j) p->mudt[j] = p->outer.mu[j] * dt;
+  p->dt = dt;
+  p->eps = eps;
+  p->rho_F = rho_F;
+  p->rho_S = rho_S;
+  return EMRKC_OK;
+}
+
+int64_t nodes_of(const emrkc_problem* p) {
+  int64_t nn = 1;
+  for (int a = 0; a < p->dim; ++a) nn *= p->n[a];
+  return nn;
+}
+
+int validate(const emrkc_problem* p) {
+  if (!p) return set_global(EMRKC_EINVAL, "null problem");
+  if (p->dim < 1 || p->dim > 3)
+    return set_global(EMRKC_EINVAL, "grid: dim must be 1, 2, or 3");
+  if (p->model != EMRKC_MODEL_HH)
+    return set_global(EMRKC_EINVAL, "unknown ionic model %d", p->model);
+  for (int a = 0; a < p->dim; ++a) {
+    if (p->n[a] < 2 || !(p->dx[a] > 0.0))
+      return set_global(EMRKC_EINVAL, "grid: extent and dx must be positive");
+    if (p->n[a] > (1 << 30))
+      return set_global(EMRKC_EINVAL, "grid: axis too long");
+  }
+  for (int a = p->dim; a < 3; ++a)
+    if (p->n[a] != 1) return set_global(EMRKC_EINVAL, "grid: unused axes need n = 1");
+  if (!(p->chi > 0.0) || !(p->C_m > 0.0))
+    return set_global(EMRKC_EINVAL, "conductivity: chi and C_m must be > 0");
+  return EMRKC_OK;
+}
+
+// Stimulus node range of one axis: the reference's per-node test
+// x = i*dx against [lo - 1e-12, hi + 1e-12] (P/src/monodomain.cpp:151-158)
+// evaluated for every index; the accepted set is an interval.
+void stim_range(const emrkc_problem* p, int a, int* lo, int* hi) {
+  *lo = 1;
+  *hi = 0;
+  bool any = false;
+  for (int64_t i = 0; i < p->n[a]; ++i) {
+    const double x = static_cast<double>(i) * p->dx[a];
+    if (!(x < p->stim_lo[a] - 1e-12 || x > p->stim_hi[a] + 1e-12)) {
+      if (!any) *lo = static_cast<int>(i);
+      *hi = static_cast<int>(i);
+      any = true;
+    }
+  }
+}
+
+double stim_rate_at(const emrkc_problem* p, double t) {
+  // stimulus_rate's time/amplitude part (P/src/monodomain.cpp:152,157) and
+  // StimulusProtocol::active_at (P/include/mrkc/monodomain.hpp:71)
+  if (p->stim_chi_amplitude == 0.0 || !(t >= p->stim_t0 && t <= p->stim_t1))
+    return 0.0;
+  return p->stim_chi_amplitude / (p->chi * p->C_m);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Handle
+// ---------------------------------------------------------------------------
+struct emrkc_handle {
+  emrkc_problem p{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Geom geom{};
+  int64_t nn = 0, len = 0;
+  int64_t z_begin = 0, z_end = 0;
+  bool partitioned = false;
+  double* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  int nbuf = 0;
+  int cur = 0;
+  bool has_state = false;
+  // m >= 2 scratch
+  double* fs = nullptr;
+  double* ye = nullptr;
+  double* u[3] = {nullptr, nullptr, nullptr};
+  // ghost planes [side: 0 below, 1 above][slot]
+  double* ghost[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  emrkc_handle* nbr[2] = {nullptr, nullptr};  // in-process neighbours
+  long long level = 0;
+  // device scalars
+  unsigned long long* d_event = nullptr;
+  unsigned long long* d_slots = nullptr;
+  size_t slots_cap = 0;
+  double* d_coef = nullptr;  // in_mueta | in_nu | in_kappa (3*(m+1))
+  size_t coef_cap = 0;
+  double* d_red = nullptr;   // reduction partials + scalar
+  Plan plan;
+  bool plan_uploaded = false;
+  int fast = 1;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::string err;
+};
+
+struct emrkc_group {
+  std::vector<emrkc_handle*> hs;
+};
+
+namespace {
+
+int set_err(emrkc_handle* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  g_global_err = buf;
+  return code;
+}
+
+#define CK(h, call)                                                          \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      return set_err((h), EMRKC_ECUDA, "%s: %s (%s:%d)", #call,              \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);            \
+  } while (0)
+
+int use_device(emrkc_handle* h) {
+  CK(h, cudaSetDevice(h->device));
+  return EMRKC_OK;
+}
+
+int ensure_buffers(emrkc_handle* h, int nb) {
+  for (int i = h->nbuf; i < nb; ++i)
+    CK(h, cudaMalloc(&h->buf[i], sizeof(double) * h->len));
+  if (nb > h->nbuf) h->nbuf = nb;
+  return EMRKC_OK;
+}
+
+int ensure_inner(emrkc_handle* h) {
+  if (h->fs) return EMRKC_OK;
+  CK(h, cudaMalloc(&h->fs, sizeof(double) * h->nn));
+  CK(h, cudaMalloc(&h->ye, sizeof(double) * 3 * h->nn));
+  for (int k = 0; k < 3; ++k) CK(h, cudaMalloc(&h->u[k], sizeof(double) * h->nn));
+  return EMRKC_OK;
+}
+
+int ensure_slots(emrkc_handle* h, size_t nsteps) {
+  const size_t need = 2 * (nsteps + 1);
+  if (need <= h->slots_cap) return EMRKC_OK;
+  if (h->d_slots) cudaFree(h->d_slots);
+  CK(h, cudaMalloc(&h->d_slots, sizeof(unsigned long long) * need));
+  h->slots_cap = need;
+  return EMRKC_OK;
+}
+
+int upload_plan(emrkc_handle* h, double dt, double rho_F, double rho_S,
+                double eps) {
+  Plan& pl = h->plan;
+  if (pl.dt == dt && pl.rho_F == rho_F && pl.rho_S == rho_S && pl.eps == eps &&
+      h->plan_uploaded)
+    return EMRKC_OK;
+  int rc = make_plan(dt, rho_F, rho_S, eps, &pl);
+  if (rc) return set_err(h, rc, "%s", g_global_err.c_str());
+  const size_t need = 3 * (pl.m + 1);
+  if (need > h->coef_cap) {
+    if (h->d_coef) cudaFree(h->d_coef);
+    CK(h, cudaMalloc(&h->d_coef, sizeof(double) * need));
+    h->coef_cap = need;
+  }
+  std::vector<double> host(need, 0.0);
+  for (int k = 0; k <= pl.m; ++k) {
+    host[k] = pl.in_mueta[k];
+    host[(pl.m + 1) + k] = pl.inner.nu[k];
+    host[2 * (pl.m + 1) + k] = pl.inner.kappa[k];
+  }
+  CK(h, cudaMemcpy(h->d_coef, host.data(), sizeof(double) * need,
+                   cudaMemcpyHostToDevice));
+  const int nb = pl.s == 1 ? 2 : (pl.s == 2 ? 3 : 4);
+  if ((rc = ensure_buffers(h, nb))) return rc;
+  if (pl.m >= 2 && (rc = ensure_inner(h))) return rc;
+  h->plan_uploaded = true;
+  return EMRKC_OK;
+}
+
+// Ghost planes consumed at stencil level L (slot L%2), and where this
+// handle's produced plane goes (the neighbour's slot (L+1)%2).
+Halo halo_at(const emrkc_handle* h, long long L) {
+  Halo x{};
+  const int rs = static_cast<int>(L & 1), ws = static_cast<int>((L + 1) & 1);
+  if (h->nbr[0]) {
+    x.lo = h->ghost[0][rs];
+    x.put_lo = h->nbr[0]->ghost[1][ws];
+  }
+  if (h->nbr[1]) {
+    x.hi = h->ghost[1][rs];
+    x.put_hi = h->nbr[1]->ghost[0][ws];
+  }
+  return x;
+}
+
+// One step of the plan, launched level by level (a level = one stencil
+// consuming kernel). No host synchronisation.
+struct StepCtx {
+  int in = 0;
+  int w[3] = {0, 0, 0};
+  int nw = 1;
+  double t = 0.0;
+  StageArgs a{};
+};
+
+void begin_step(emrkc_handle* h, double t, long long step_in_run,
+                unsigned long long* gate_slot, StepCtx* c) {
+  const Plan& pl = h->plan;
+  c->in = h->cur;
+  c->t = t;
+  c->nw = (pl.s == 1) ? 1 : (pl.s == 2 ? 2 : 3);
+  for (int k = 0; k < c->nw; ++k) c->w[k] = (c->in + 1 + k) % h->nbuf;
+  const unsigned long long stride =
+      static_cast<unsigned long long>(pl.s) * (pl.m + 1) + 2;
+  StageArgs& a = c->a;
+  a = StageArgs{};
+  a.eta = pl.eta;
+  a.inv_eta = 1.0 / pl.eta;
+  a.s = pl.s;
+  a.m = pl.m;
+  a.in_mueta = h->d_coef;
+  a.in_nu = h->d_coef + (pl.m + 1);
+  a.in_kappa = h->d_coef + 2 * (pl.m + 1);
+  a.code_base = static_cast<unsigned long long>(step_in_run) * stride;
+  a.event = h->d_event;
+  a.gate_slot = gate_slot;
+  a.fs = h->fs;
+  a.ye = h->ye;
+  for (int k = 0; k < 3; ++k) a.u[k] = h->u[k];
+}
+
+// Launches inner stage k (1..m) of outer stage j (1..s).
+int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
+  const Plan& pl = h->plan;
+  StageArgs& a = c->a;
+  const int nw = c->nw;
+  a.j = j;
+  a.last = (j == pl.s);
+  a.out = h->buf[c->w[(j - 1) % nw]];
+  a.g1 = (j == 1) ? h->buf[c->in] : h->buf[c->w[(j - 2) % nw]];
+  a.g2 = (j == 1) ? nullptr
+                  : (j == 2 ? h->buf[c->in] : h->buf[c->w[(j - 3) % nw]]);
+  a.mudt = pl.mudt[j];
+  a.nu = pl.outer.nu[j];
+  a.kappa = pl.outer.kappa[j];
+  // stage time: t for j = 1, t + c_{j-1} dt after (P/src/cheb.cpp:90,97)
+  const double r = (j == 1) ? c->t : c->t + pl.outer.c[j - 1] * pl.dt;
+  a.stim = stim_rate_at(&h->p, r);
+  const Halo hl = halo_at(h, h->level);
+  if (pl.m == 1)
+    CK(h, emrkc_k::launch_stage_m1(h->geom, hl, a, h->fast, h->stream));
+  else if (k == 1)
+    CK(h, emrkc_k::launch_stage_first(h->geom, hl, a, h->fast, h->stream));
+  else
+    CK(h, emrkc_k::launch_stage_inner(h->geom, hl, a, k, h->fast, h->stream));
+  ++h->level;
+  return EMRKC_OK;
+}
+
+int end_step(emrkc_handle* h, const StepCtx* c) {
+  return c->w[(h->plan.s - 1) % c->nw];
+}
+
+int enqueue_step(emrkc_handle* h, double t, long long step_in_run,
+                 unsigned long long* gate_slot, int* out_idx) {
+  StepCtx c;
+  begin_step(h, t, step_in_run, gate_slot, &c);
+  for (int j = 1; j <= h->plan.s; ++j)
+    for (int k = 1; k <= h->plan.m; ++k) {
+      const int rc = launch_level(h, &c, j, k);
+      if (rc) return rc;
+    }
+  *out_idx = end_step(h, &c);
+  return EMRKC_OK;
+}
+
+struct Decoded {
+  bool none = true;
+  bool guard = false;
+  long long step = -1;
+  int outer_stage = 0, stage = 0, inner = 0;
+};
+
+Decoded decode_event(unsigned long long ev, const Plan& pl) {
+  Decoded d;
+  if (ev == kNoEvent) return d;
+  const unsigned long long stride =
+      static_cast<unsigned long long>(pl.s) * (pl.m + 1) + 2;
+  d.none = false;
+  d.step = static_cast<long long>(ev / stride);
+  const int ord = static_cast<int>(ev % stride);
+  if (ord == pl.s * (pl.m + 1) + 1) {
+    d.guard = true;
+    return d;
+  }
+  d.outer_stage = (ord - 1) / (pl.m + 1) + 1;
+  const int k = (ord - 1) % (pl.m + 1) + 1;
+  if (k <= pl.m) {
+    d.inner = 1;
+    d.stage = k;
+  } else {
+    d.inner = 0;
+    d.stage = d.outer_stage;
+  }
+  return d;
+}
+
+// Work tallies of a step aborted at (outer stage j, inner stage k):
+// the reference counts calls made before the throw (P/src/multirate.cpp:18-38).
+void partial_counters(const Decoded& d, const Plan& pl, int64_t* fF,
+                      int64_t* fS, int64_t* ex) {
+  const int j = d.outer_stage;
+  *ex += j;
+  *fS += j;
+  *fF += static_cast<int64_t>(j - 1) * pl.m + (d.inner ? d.stage : pl.m);
+}
+
+int init_handle(emrkc_handle* h) {
+  CK(h, cudaSetDevice(h->device));
+  CK(h, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CK(h, cudaMalloc(&h->d_event, sizeof(unsigned long long)));
+  CK(h, cudaMalloc(&h->d_red, sizeof(double) * (emrkc_k::power_blocks() + 8)));
+  CK(h, cudaEventCreate(&h->ev0));
+  CK(h, cudaEventCreate(&h->ev1));
+  if (h->partitioned) {
+    const size_t pl = static_cast<size_t>(h->geom.plane);
+    for (int s = 0; s < 2; ++s)
+      for (int k = 0; k < 2; ++k) {
+        CK(h, cudaMalloc(&h->ghost[s][k], sizeof(double) * pl));
+        CK(h, cudaMemset(h->ghost[s][k], 0, sizeof(double) * pl));
+      }
+  }
+  const char* f = std::getenv("EMRKC_FAST");
+  h->fast = f ? std::atoi(f) : 1;
+  return EMRKC_OK;
+}
+
+// Deterministic device norm^2 (fixed grid) of x[len].
+int norm2sq(emrkc_handle* h, const double* x, int64_t len, double* out) {
+  const int nb = emrkc_k::power_blocks();
+  CK(h, emrkc_k::launch_norm2_partial(x, len, h->d_red, nb, h->stream));
+  CK(h, emrkc_k::launch_sum_partials(h->d_red, nb, h->d_red + nb, h->stream));
+  CK(h, cudaMemcpyAsync(out, h->d_red + nb, sizeof(double),
+                        cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return EMRKC_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* emrkc_version(void) { return "emrkc-b200 1 (sm_100a)"; }
+
+const char* emrkc_global_error(void) { return g_global_err.c_str(); }
+
+int emrkc_get_stages(double dt, double rho, double epsilon, int32_t* s,
+                     double* ell, double* beta) {
+  int32_t s_;
+  double l_, b_;
+  const int rc = stages(dt, rho, epsilon, &s_, &l_, &b_);
+  if (rc) return rc;
+  if (s) *s = s_;
+  if (ell) *ell = l_;
+  if (beta) *beta = b_;
+  return EMRKC_OK;
+}
+
+int emrkc_rkc_coeffs(int32_t s, double epsilon, double* omega0,
+                     double* omega1, double* b, double* mu, double* nu,
+                     double* kappa, double* c) {
+  Coeffs k;
+  const int rc = coeffs(s, epsilon, &k);
+  if (rc) return rc;
+  if (omega0) *omega0 = k.omega0;
+  if (omega1) *omega1 = k.omega1;
+  for (int j = 0; j <= s; ++j) {
+    if (b) b[j] = k.b[j];
+    if (mu) mu[j] = k.mu[j];
+    if (nu) nu[j] = k.nu[j];
+    if (kappa) kappa[j] = k.kappa[j];
+    if (c) c[j] = k.c[j];
+  }
+  return EMRKC_OK;
+}
+
+int emrkc_plan_step(double dt, double rho_F, double rho_S, double epsilon,
+                    emrkc_step_report* plan) {
+  if (!plan) return set_global(EMRKC_EINVAL, "null report");
+  Plan p;
+  const int rc = make_plan(dt, rho_F, rho_S, epsilon, &p);
+  if (rc) return rc;
+  std::memset(plan, 0, sizeof(*plan));
+  plan->s = p.s;
+  plan->m = p.m;
+  plan->eta = p.eta;
+  plan->ell_s = p.ell_s;
+  plan->ell_m = p.ell_m;
+  plan->n_fF = static_cast<int64_t>(p.s) * p.m;
+  plan->n_fS = p.s;
+  plan->n_exp = p.s;
+  return EMRKC_OK;
+}
+
+int emrkc_model_info(int32_t model, int32_t* n_gates, int32_t* n_aux) {
+  if (model != EMRKC_MODEL_HH)
+    return set_global(EMRKC_EINVAL, "unknown ionic model %d", model);
+  if (n_gates) *n_gates = 3;
+  if (n_aux) *n_aux = 0;
+  return EMRKC_OK;
+}
+
+int emrkc_resting_state(int32_t model, double* V, double* gates) {
+  if (model != EMRKC_MODEL_HH)
+    return set_global(EMRKC_EINVAL, "unknown ionic model %d", model);
+  // IonicModel::resting_state — bisection on [-90, -40] mV (P/src/ionic.cpp:42-77)
+  double lam[3], zinf[3];
+  auto steady = [&](double v) {
+    hh_gate_coeffs(v, lam, zinf);
+    return hh_current(v, zinf);
+  };
+  double lo = -90.0, hi = -40.0;
+  double flo = steady(lo), fhi = steady(hi);
+  if (flo * fhi > 0.0)
+    return set_global(EMRKC_EINVAL, "resting_state: no sign change in [-90, -40] mV");
+  for (int it = 0; it < 200 && hi - lo > 1e-14; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    const double fm = steady(mid);
+    if (flo * fm <= 0.0) {
+      hi = mid;
+      fhi = fm;
+    } else {
+      lo = mid;
+      flo = fm;
+    }
+  }
+  const double v = 0.5 * (lo + hi);
+  hh_gate_coeffs(v, lam, zinf);
+  if (V) *V = v;
+  if (gates)
+    for (int g = 0; g < 3; ++g) gates[g] = zinf[g];
+  return EMRKC_OK;
+}
+
+int64_t emrkc_state_len(const emrkc_problem* p, const emrkc_partition* part) {
+  if (validate(p)) return -1;
+  int64_t nn = nodes_of(p);
+  if (part) {
+    const int za = p->dim - 1;
+    nn = nn / p->n[za] * (part->z_end - part->z_begin);
+  }
+  return 4 * nn;
+}
+
+int emrkc_partition_slab(int64_t n_z, int32_t nranks, int32_t rank,
+                         emrkc_partition* out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks || n_z < nranks)
+    return set_global(EMRKC_EINVAL, "partition: need 0 <= rank < nranks <= n_z");
+  const int64_t base = n_z / nranks, rem = n_z % nranks;
+  out->z_begin = rank * base + std::min<int64_t>(rank, rem);
+  out->z_end = out->z_begin + base + (rank < rem ? 1 : 0);
+  return EMRKC_OK;
+}
+
+int emrkc_create(const emrkc_problem* p, int32_t device,
+                 const emrkc_partition* part, emrkc_handle** out) {
+  if (!out) return set_global(EMRKC_EINVAL, "null output handle");
+  *out = nullptr;
+  int rc = validate(p);
+  if (rc) return rc;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return set_global(EMRKC_ECUDA, "no CUDA device available (%s); there is no CPU fallback",
+                      cudaGetErrorString(e));
+  if (device < 0 || device >= ndev)
+    return set_global(EMRKC_EINVAL, "device %d out of range (%d devices)", device, ndev);
+  const int za = p->dim - 1;
+  int64_t zb = 0, ze = p->n[za];
+  if (part) {
+    zb = part->z_begin;
+    ze = part->z_end;
+    if (zb < 0 || ze > p->n[za] || ze <= zb)
+      return set_global(EMRKC_EINVAL, "partition: bad slab [%lld, %lld)",
+                        (long long)zb, (long long)ze);
+    if (p->dim == 1 && (zb != 0 || ze != p->n[0]))
+      return set_global(EMRKC_EINVAL, "partition: 1-D grids are not partitioned");
+  }
+  auto* h = new emrkc_handle();
+  h->p = *p;
+  h->device = device;
+  h->z_begin = zb;
+  h->z_end = ze;
+  h->partitioned = (zb != 0 || ze != p->n[za]);
+  Geom& g = h->geom;
+  g.dim = p->dim;
+  g.n0 = static_cast<int>(p->n[0]);
+  g.n1 = static_cast<int>(p->n[1]);
+  g.n2 = static_cast<int>(p->n[2]);
+  g.nzg = static_cast<int>(p->n[za]);
+  g.nzl = static_cast<int>(ze - zb);
+  g.zoff = static_cast<int>(zb);
+  if (za == 0) g.n0 = g.nzl;
+  if (za == 1) g.n1 = g.nzl;
+  if (za == 2) g.n2 = g.nzl;
+  g.plane = 1;
+  for (int a = 0; a < za; ++a) g.plane *= p->n[a];
+  g.nn = g.plane * g.nzl;
+  for (int a = 0; a < 3; ++a)
+    g.w[a] = (a < p->dim) ? p->sigma[a] / (p->chi * p->C_m * p->dx[a] * p->dx[a])
+                          : 0.0;
+  g.Cm = p->C_m;
+  g.inv_Cm = 1.0 / p->C_m;
+  for (int a = 0; a < 3; ++a) {
+    if (a < p->dim) {
+      stim_range(p, a, &g.st_lo[a], &g.st_hi[a]);
+    } else {
+      g.st_lo[a] = 0;
+      g.st_hi[a] = 0;
+    }
+  }
+  h->nn = g.nn;
+  h->len = 4 * g.nn;
+  if ((rc = init_handle(h))) {
+    g_global_err = h->err;
+    emrkc_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return EMRKC_OK;
+}
+
+void emrkc_destroy(emrkc_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (auto& b : h->buf)
+    if (b) cudaFree(b);
+  if (h->fs) cudaFree(h->fs);
+  if (h->ye) cudaFree(h->ye);
+  for (auto& u : h->u)
+    if (u) cudaFree(u);
+  for (auto& s : h->ghost)
+    for (auto& k : s)
+      if (k) cudaFree(k);
+  if (h->d_event) cudaFree(h->d_event);
+  if (h->d_slots) cudaFree(h->d_slots);
+  if (h->d_coef) cudaFree(h->d_coef);
+  if (h->d_red) cudaFree(h->d_red);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+const char* emrkc_last_error(const emrkc_handle* h) {
+  return h ? h->err.c_str() : g_global_err.c_str();
+}
+
+int64_t emrkc_local_len(const emrkc_handle* h) { return h ? h->len : -1; }
+
+int emrkc_set_state(emrkc_handle* h, const double* y, int64_t len) {
+  if (!h || !y) return set_global(EMRKC_EINVAL, "null argument");
+  if (len != h->len)
+    return set_err(h, EMRKC_EINVAL, "MonodomainOperator: state size mismatch (%lld != %lld)",
+                   (long long)len, (long long)h->len);
+  int rc = use_device(h);
+  if (rc) return rc;
+  if ((rc = ensure_buffers(h, std::max(2, h->nbuf)))) return rc;
+  CK(h, cudaMemcpyAsync(h->buf[h->cur], y, sizeof(double) * len,
+                        cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->has_state = true;
+  return EMRKC_OK;
+}
+
+int emrkc_get_state(emrkc_handle* h, double* y, int64_t len) {
+  if (!h || !y) return set_global(EMRKC_EINVAL, "null argument");
+  if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
+  if (len != h->len)
+    return set_err(h, EMRKC_EINVAL, "state size mismatch");
+  int rc = use_device(h);
+  if (rc) return rc;
+  CK(h, cudaMemcpyAsync(y, h->buf[h->cur], sizeof(double) * len,
+                        cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return EMRKC_OK;
+}
+
+int emrkc_state_device_ptr(emrkc_handle* h, double** dptr) {
+  if (!h || !dptr) return set_global(EMRKC_EINVAL, "null argument");
+  if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
+  *dptr = h->buf[h->cur];
+  return EMRKC_OK;
+}
+
+int emrkc_synchronize(emrkc_handle* h) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  int rc = use_device(h);
+  if (rc) return rc;
+  CK(h, cudaStreamSynchronize(h->stream));
+  return EMRKC_OK;
+}
+
+int emrkc_eval_rhs(emrkc_handle* h, int32_t which, double t, const double* y,
+                   double* out, int64_t len) {
+  if (!h || !y || !out) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "eval_rhs: whole-grid handles only");
+  if (len != h->len) return set_err(h, EMRKC_EINVAL, "MonodomainOperator: state size mismatch");
+  if (which != EMRKC_RHS_F && which != EMRKC_RHS_S)
+    return set_err(h, EMRKC_EINVAL, "eval_rhs: which must be F or S");
+  int rc = use_device(h);
+  if (rc) return rc;
+  double *dy = nullptr, *dout = nullptr;
+  CK(h, cudaMalloc(&dy, sizeof(double) * len));
+  CK(h, cudaMalloc(&dout, sizeof(double) * len));
+  CK(h, cudaMemcpyAsync(dy, y, sizeof(double) * len, cudaMemcpyHostToDevice, h->stream));
+  CK(h, emrkc_k::launch_rhs(h->geom, Halo{}, which, dy, stim_rate_at(&h->p, t), dout,
+                            h->stream));
+  CK(h, cudaMemcpyAsync(out, dout, sizeof(double) * len, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  cudaFree(dy);
+  cudaFree(dout);
+  return EMRKC_OK;
+}
+
+int emrkc_exp_part(emrkc_handle* h, const double* y, double* lambda,
+                   double* y_inf, int64_t len) {
+  if (!h || !y || !lambda || !y_inf) return set_global(EMRKC_EINVAL, "null argument");
+  if (len != h->len) return set_err(h, EMRKC_EINVAL, "MonodomainOperator: state size mismatch");
+  int rc = use_device(h);
+  if (rc) return rc;
+  double *dy = nullptr, *dl = nullptr, *di = nullptr;
+  CK(h, cudaMalloc(&dy, sizeof(double) * len));
+  CK(h, cudaMalloc(&dl, sizeof(double) * len));
+  CK(h, cudaMalloc(&di, sizeof(double) * len));
+  CK(h, cudaMemcpyAsync(dy, y, sizeof(double) * len, cudaMemcpyHostToDevice, h->stream));
+  CK(h, emrkc_k::launch_exp_part(h->geom, dy, dl, di, h->stream));
+  CK(h, cudaMemcpyAsync(lambda, dl, sizeof(double) * len, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaMemcpyAsync(y_inf, di, sizeof(double) * len, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  cudaFree(dy);
+  cudaFree(dl);
+  cudaFree(di);
+  return EMRKC_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Power iteration (shared by single handles and groups)
+// ---------------------------------------------------------------------------
+namespace {
+
+// seeded_direction (P/src/spectral.cpp:16-22): libstdc++ mt19937_64 +
+// uniform_real_distribution(-1, 1) over the full global state.
+void seeded_direction(std::vector<double>& v) {
+  std::mt19937_64 rng(0x9e3779b97f4a7c15ull);
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  for (double& x : v) x = dist(rng);
+}
+
+// Global-vector slice of a slab handle: block b, local nodes.
+void scatter_slab(const emrkc_handle* h, const std::vector<double>& global,
+                  int64_t global_nn, std::vector<double>& local) {
+  local.resize(h->len);
+  const int64_t off = h->z_begin * h->geom.plane;
+  for (int b = 0; b < 4; ++b)
+    std::memcpy(local.data() + b * h->nn, global.data() + b * global_nn + off,
+                sizeof(double) * h->nn);
+}
+
+struct PowerWork {
+  double* v[2] = {nullptr, nullptr};
+  double* fy = nullptr;
+  double* gy[2] = {nullptr, nullptr};  // ghost planes of y_V (below, above)
+  double* gv[2] = {nullptr, nullptr};  // ghost planes of v_V
+};
+
+int power_alloc(emrkc_handle* h, PowerWork* w) {
+  CK(h, cudaSetDevice(h->device));
+  CK(h, cudaMalloc(&w->v[0], sizeof(double) * h->len));
+  CK(h, cudaMalloc(&w->v[1], sizeof(double) * h->len));
+  CK(h, cudaMalloc(&w->fy, sizeof(double) * h->len));
+  if (h->partitioned)
+    for (int s = 0; s < 2; ++s) {
+      CK(h, cudaMalloc(&w->gy[s], sizeof(double) * h->geom.plane));
+      CK(h, cudaMalloc(&w->gv[s], sizeof(double) * h->geom.plane));
+    }
+  return EMRKC_OK;
+}
+
+void power_free(emrkc_handle* h, PowerWork* w) {
+  cudaSetDevice(h->device);
+  for (auto p : {w->v[0], w->v[1], w->fy, w->gy[0], w->gy[1], w->gv[0], w->gv[1]})
+    if (p) cudaFree(p);
+}
+
+// Copy the neighbours' boundary V planes of field f (per handle) into the
+// ghost buffers dst (per handle, [below, above]).
+int exchange_planes(const std::vector<emrkc_handle*>& hs,
+                    const std::vector<const double*>& field,
+                    const std::vector<double* const*>& dst) {
+  const size_t n = hs.size();
+  for (size_t r = 0; r < n; ++r) {
+    emrkc_handle* h = hs[r];
+    const size_t bytes = sizeof(double) * h->geom.plane;
+    if (r > 0) {  // below: neighbour's last plane
+      emrkc_handle* nb = hs[r - 1];
+      const double* src = field[r - 1] + (nb->nn - nb->geom.plane);
+      CK(h, cudaMemcpyPeer(dst[r][0], h->device, src, nb->device, bytes));
+    }
+    if (r + 1 < n) {  // above: neighbour's first plane
+      emrkc_handle* nb = hs[r + 1];
+      CK(h, cudaMemcpyPeer(dst[r][1], h->device, field[r + 1], nb->device, bytes));
+    }
+  }
+  return EMRKC_OK;
+}
+
+// estimate_spectral_radius (P/src/spectral.cpp:26-71) over a list of slabs
+// (one whole-grid handle is the common case). Norms are sums of per-slab
+// deterministic device reductions.
+int power_iteration(const std::vector<emrkc_handle*>& hs, int which, double t,
+                    const double* v0_global, double rho0, emrkc_rho_result* out,
+                    double* v_out_global) {
+  const size_t n = hs.size();
+  emrkc_handle* h0 = hs[0];
+  const emrkc_problem& p = h0->p;
+  const int64_t gnn = nodes_of(&p);
+  const int64_t glen = 4 * gnn;
+  for (auto* h : hs)
+    if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
+  std::vector<double> v0(glen);
+  if (v0_global)
+    std::memcpy(v0.data(), v0_global, sizeof(double) * glen);
+  else
+    seeded_direction(v0);
+  std::vector<PowerWork> w(n);
+  int rc = EMRKC_OK;
+  int a = 0;
+  const double stim = stim_rate_at(&p, t);
+  const double kEps = 1e-8, kTol = 1e-2;
+  const int kMaxIters = 50;
+  auto cleanup = [&]() {
+    for (size_t r = 0; r < n; ++r) power_free(hs[r], &w[r]);
+  };
+  auto sum_norm2 = [&](auto field_of) -> double {
+    double tot = 0.0;
+    for (size_t r = 0; r < n; ++r) {
+      double part = 0.0;
+      rc = norm2sq(hs[r], field_of(r), hs[r]->len, &part);
+      if (rc) return 0.0;
+      tot += part;
+    }
+    return tot;
+  };
+  std::vector<const double*> ys(n), vs(n);
+  std::vector<double* const*> gys(n), gvs(n);
+  double nv_cur, ny, delta, rho = rho0, rho_old = 0.0;
+  int it = 0;
+  out->safety = 1.05;
+  out->converged = 1;
+  for (size_t r = 0; r < n; ++r) {
+    if ((rc = power_alloc(hs[r], &w[r]))) goto fail;
+    std::vector<double> local;
+    scatter_slab(hs[r], v0, gnn, local);
+    cudaError_t e = cudaMemcpy(w[r].v[0], local.data(), sizeof(double) * hs[r]->len,
+                               cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      rc = set_err(hs[r], EMRKC_ECUDA, "%s", cudaGetErrorString(e));
+      goto fail;
+    }
+    ys[r] = hs[r]->buf[hs[r]->cur];
+    gys[r] = w[r].gy;
+    gvs[r] = w[r].gv;
+  }
+  nv_cur = std::sqrt(sum_norm2([&](size_t r) { return w[r].v[0]; }));
+  if (rc) goto fail;
+  if (nv_cur == 0.0) {
+    rc = set_err(h0, EMRKC_EINVAL, "estimate_spectral_radius: v0 must be nonzero");
+    goto fail;
+  }
+  ny = std::sqrt(sum_norm2([&](size_t r) { return ys[r]; }));
+  if (rc) goto fail;
+  delta = std::max(ny, kEps) * kEps;
+  if (n > 1 && (rc = exchange_planes(hs, ys, gys))) goto fail;
+  for (size_t r = 0; r < n; ++r) {
+    emrkc_handle* h = hs[r];
+    Halo hh{};
+    hh.lo = w[r].gy[0];
+    hh.hi = w[r].gy[1];
+    if (r == 0) hh.lo = nullptr;
+    if (r + 1 == n) hh.hi = nullptr;
+    cudaSetDevice(h->device);
+    cudaError_t e = emrkc_k::launch_rhs(h->geom, hh, which, ys[r], stim, w[r].fy, h->stream);
+    if (e != cudaSuccess) {
+      rc = set_err(h, EMRKC_ECUDA, "%s", cudaGetErrorString(e));
+      goto fail;
+    }
+  }
+  while (it == 0 || std::abs(rho - rho_old) >= kTol * rho) {
+    if (it >= kMaxIters) {
+      out->converged = 0;
+      break;
+    }
+    rho_old = rho;
+    const double q = delta / nv_cur;
+    for (size_t r = 0; r < n; ++r) vs[r] = w[r].v[a];
+    if (n > 1 && (rc = exchange_planes(hs, vs, gvs))) goto fail;
+    double tot = 0.0;
+    for (size_t r = 0; r < n; ++r) {
+      emrkc_handle* h = hs[r];
+      cudaSetDevice(h->device);
+      const int nb = emrkc_k::power_blocks();
+      cudaError_t e = emrkc_k::launch_power(
+          h->geom, which, ys[r], w[r].v[a], q, w[r].fy, stim, w[r].v[1 - a],
+          r > 0 ? w[r].gy[0] : nullptr, r + 1 < n ? w[r].gy[1] : nullptr,
+          r > 0 ? w[r].gv[0] : nullptr, r + 1 < n ? w[r].gv[1] : nullptr,
+          h->d_red, nb, h->stream);
+      if (e == cudaSuccess)
+        e = emrkc_k::launch_sum_partials(h->d_red, nb, h->d_red + nb, h->stream);
+      double part = 0.0;
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&part, h->d_red + nb, sizeof(double),
+                            cudaMemcpyDeviceToHost, h->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+      if (e != cudaSuccess) {
+        rc = set_err(h, EMRKC_ECUDA, "power iteration: %s", cudaGetErrorString(e));
+        goto fail;
+      }
+      tot += part;
+    }
+    a = 1 - a;
+    const double nv = std::sqrt(tot);
+    if (nv < 1e-300) {
+      out->rho = 0.0;
+      out->iterations = it + 1;
+      goto vout;
+    }
+    rho = nv / delta;
+    nv_cur = nv;
+    ++it;
+  }
+  out->rho = rho * out->safety;
+  out->iterations = it;
+vout:
+  if (v_out_global) {
+    for (size_t r = 0; r < n; ++r) {
+      emrkc_handle* h = hs[r];
+      std::vector<double> local(h->len);
+      cudaSetDevice(h->device);
+      cudaMemcpy(local.data(), w[r].v[a], sizeof(double) * h->len, cudaMemcpyDeviceToHost);
+      const int64_t off = h->z_begin * h->geom.plane;
+      for (int b = 0; b < 4; ++b)
+        std::memcpy(v_out_global + b * gnn + off, local.data() + b * h->nn,
+                    sizeof(double) * h->nn);
+    }
+  }
+fail:
+  cleanup();
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// Run loop over a list of slabs in lockstep (one handle: the plain run).
+// ---------------------------------------------------------------------------
+int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
+              int64_t nsteps, double dt, double eps, double rho_F,
+              double rho_S, emrkc_run_result* res, bool single_step,
+              emrkc_step_report* rep) {
+  const size_t n = hs.size();
+  int rc;
+  for (auto* h : hs) {
+    if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
+    if ((rc = use_device(h))) return rc;
+    if ((rc = upload_plan(h, dt, rho_F, rho_S, eps))) return rc;
+    if ((rc = ensure_slots(h, static_cast<size_t>(nsteps)))) return rc;
+    CK(h, cudaMemcpyAsync(h->d_event, &kNoEvent, sizeof(kNoEvent),
+                          cudaMemcpyHostToDevice, h->stream));
+    CK(h, emrkc_k::launch_fill_u64(h->d_slots, 2 * (nsteps + 1), 0, h->stream));
+    // min slots start at ~0, max slots at 0
+    std::vector<unsigned long long> init(2 * (nsteps + 1));
+    for (size_t k = 0; k < init.size(); k += 2) {
+      init[k] = kNoEvent;
+      init[k + 1] = 0ull;
+    }
+    CK(h, cudaMemcpyAsync(h->d_slots, init.data(), sizeof(unsigned long long) * init.size(),
+                          cudaMemcpyHostToDevice, h->stream));
+    CK(h, emrkc_k::launch_gate_range(h->geom, h->buf[h->cur],
+                                     h->d_slots + 2 * nsteps, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+  }
+  const Plan& pl = hs[0]->plan;
+  // Initial ghost planes of the current state (level L0 slot).
+  if (n > 1) {
+    const long long L0 = hs[0]->level;
+    for (auto* h : hs)
+      if (h->level != L0) return set_err(h, EMRKC_ESTATE, "group handles out of step");
+    std::vector<const double*> f(n);
+    std::vector<double* const*> dst(n);
+    std::vector<std::array<double*, 2>> slots(n);
+    for (size_t r = 0; r < n; ++r) {
+      f[r] = hs[r]->buf[hs[r]->cur];
+      slots[r] = {hs[r]->ghost[0][L0 & 1], hs[r]->ghost[1][L0 & 1]};
+      dst[r] = slots[r].data();
+    }
+    if ((rc = exchange_planes(hs, f, dst))) return rc;
+    for (auto* h : hs) CK(h, cudaDeviceSynchronize());
+  }
+  std::vector<std::vector<int>> in_idx(n, std::vector<int>(nsteps + 1));
+  for (auto* h : hs) {
+    CK(h, cudaSetDevice(h->device));
+    CK(h, cudaEventRecord(h->ev0, h->stream));
+  }
+  if (n == 1) {
+    emrkc_handle* h = hs[0];
+    for (int64_t r = 0; r < nsteps; ++r) {
+      const double t = static_cast<double>(step0 + r) * dt;  // simulate.cpp:177
+      in_idx[0][r] = h->cur;
+      int outi = 0;
+      if ((rc = enqueue_step(h, t, r, h->d_slots + 2 * r, &outi))) return rc;
+      h->cur = outi;
+    }
+  } else {
+    // Lockstep over slabs: after every level each slab waits for its
+    // neighbours' kernels of that level (their peer stores fill its ghost
+    // planes); after every step all slabs meet and fold the abort words so
+    // that every slab freezes on the same step.
+    std::vector<StepCtx> c(n);
+    std::vector<unsigned long long*> evs(n);
+    for (size_t q = 0; q < n; ++q) evs[q] = hs[q]->d_event;
+    auto sync_neighbours = [&]() -> int {
+      for (size_t q = 0; q < n; ++q) {
+        CK(hs[q], cudaSetDevice(hs[q]->device));
+        CK(hs[q], cudaEventRecord(hs[q]->ev1, hs[q]->stream));
+      }
+      for (size_t q = 0; q < n; ++q) {
+        CK(hs[q], cudaSetDevice(hs[q]->device));
+        if (q > 0) CK(hs[q], cudaStreamWaitEvent(hs[q]->stream, hs[q - 1]->ev1, 0));
+        if (q + 1 < n) CK(hs[q], cudaStreamWaitEvent(hs[q]->stream, hs[q + 1]->ev1, 0));
+      }
+      return EMRKC_OK;
+    };
+    for (int64_t r = 0; r < nsteps; ++r) {
+      const double t = static_cast<double>(step0 + r) * dt;  // simulate.cpp:177
+      for (size_t q = 0; q < n; ++q) {
+        in_idx[q][r] = hs[q]->cur;
+        begin_step(hs[q], t, r, hs[q]->d_slots + 2 * r, &c[q]);
+      }
+      for (int j = 1; j <= pl.s; ++j)
+        for (int k = 1; k <= pl.m; ++k) {
+          for (size_t q = 0; q < n; ++q) {
+            CK(hs[q], cudaSetDevice(hs[q]->device));
+            if ((rc = launch_level(hs[q], &c[q], j, k))) return rc;
+          }
+          if ((rc = sync_neighbours())) return rc;
+        }
+      for (size_t q = 0; q < n; ++q) hs[q]->cur = end_step(hs[q], &c[q]);
+      // all-slab barrier + abort-word fold
+      for (size_t q = 0; q < n; ++q) {
+        CK(hs[q], cudaSetDevice(hs[q]->device));
+        CK(hs[q], cudaEventRecord(hs[q]->ev1, hs[q]->stream));
+      }
+      for (size_t q = 0; q < n; ++q) {
+        CK(hs[q], cudaSetDevice(hs[q]->device));
+        for (size_t o = 0; o < n; ++o)
+          if (o != q) CK(hs[q], cudaStreamWaitEvent(hs[q]->stream, hs[o]->ev1, 0));
+        CK(hs[q], emrkc_k::launch_fold_events(hs[q]->d_event, evs.data(),
+                                              static_cast<int>(n), hs[q]->stream));
+      }
+    }
+  }
+  for (size_t q = 0; q < n; ++q) {
+    in_idx[q][nsteps] = hs[q]->cur;
+    CK(hs[q], cudaSetDevice(hs[q]->device));
+    CK(hs[q], cudaEventRecord(hs[q]->ev1, hs[q]->stream));
+  }
+  double ms = 0.0;
+  unsigned long long ev = kNoEvent;
+  std::vector<unsigned long long> slots;
+  std::vector<unsigned long long> all_slots(2 * (nsteps + 1));
+  for (size_t q = 0; q < n; ++q) {
+    emrkc_handle* h = hs[q];
+    CK(h, cudaSetDevice(h->device));
+    CK(h, cudaEventSynchronize(h->ev1));
+    float f = 0.0f;
+    CK(h, cudaEventElapsedTime(&f, h->ev0, h->ev1));
+    ms = std::max(ms, static_cast<double>(f));
+    unsigned long long e = kNoEvent;
+    CK(h, cudaMemcpy(&e, h->d_event, sizeof(e), cudaMemcpyDeviceToHost));
+    ev = std::min(ev, e);
+    slots.resize(2 * (nsteps + 1));
+    CK(h, cudaMemcpy(slots.data(), h->d_slots, sizeof(unsigned long long) * slots.size(),
+                     cudaMemcpyDeviceToHost));
+    for (size_t k = 0; k < slots.size(); k += 2) {
+      all_slots[k] = q == 0 ? slots[k] : std::min(all_slots[k], slots[k]);
+      all_slots[k + 1] = q == 0 ? slots[k + 1] : std::max(all_slots[k + 1], slots[k + 1]);
+    }
+  }
+  Decoded d = decode_event(ev, pl);
+  if (single_step && !d.none && d.guard) d = Decoded{};  // emrkc_step has no guard
+  int64_t accepted = nsteps, done = nsteps;
+  if (!d.none) {
+    if (d.guard) {
+      done = d.step + 1;
+      accepted = d.step;
+      for (size_t q = 0; q < n; ++q) hs[q]->cur = in_idx[q][d.step + 1];
+    } else {
+      done = d.step;
+      accepted = d.step;
+      for (size_t q = 0; q < n; ++q) hs[q]->cur = in_idx[q][d.step];
+    }
+  }
+  if (n > 1 && !d.none) {
+    // the ghost slots no longer match the (rolled back) state: the next run
+    // re-exchanges from the current state.
+  }
+  if (res) {
+    std::memset(res, 0, sizeof(*res));
+    res->n_steps = nsteps;
+    res->steps_done = done;
+    res->aborted = d.none ? 0 : 1;
+    res->abort_kind = d.none ? EMRKC_ABORT_NONE
+                             : (d.guard ? EMRKC_ABORT_NORM_GUARD : EMRKC_ABORT_NONFINITE);
+    res->abort_step = d.none ? -1 : step0 + d.step;
+    res->abort_stage = d.guard ? 0 : d.stage;
+    res->abort_inner = d.guard ? 0 : d.inner;
+    // track_gate_range: initial state then each accepted step (simulate.cpp:113,228)
+    double lo = 1.0, hi = 0.0;
+    auto fold = [&](size_t k) {
+      if (all_slots[k] != kNoEvent) {
+        const double v = emrkc_k::double_of(all_slots[k]);
+        lo = (v < lo) ? v : lo;
+      }
+      if (all_slots[k + 1] != 0ull) {
+        const double v = emrkc_k::double_of(all_slots[k + 1]);
+        hi = (hi < v) ? v : hi;
+      }
+    };
+    fold(2 * nsteps);
+    for (int64_t r = 0; r < accepted; ++r) fold(2 * r);
+    res->gate_min = lo;
+    res->gate_max = hi;
+    res->n_fF = done * pl.s * pl.m;
+    res->n_fS = done * pl.s;
+    res->n_exp = done * pl.s;
+    if (!d.none && !d.guard) partial_counters(d, pl, &res->n_fF, &res->n_fS, &res->n_exp);
+    res->s = pl.s;
+    res->m = pl.m;
+    res->eta = pl.eta;
+    res->device_ms = ms;
+  }
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->s = pl.s;
+    rep->m = pl.m;
+    rep->eta = pl.eta;
+    rep->ell_s = pl.ell_s;
+    rep->ell_m = pl.ell_m;
+    rep->n_fF = static_cast<int64_t>(pl.s) * pl.m;
+    rep->n_fS = pl.s;
+    rep->n_exp = pl.s;
+    if (!d.none && !d.guard) {
+      rep->n_fF = rep->n_fS = rep->n_exp = 0;
+      partial_counters(d, pl, &rep->n_fF, &rep->n_fS, &rep->n_exp);
+      rep->abort_kind = EMRKC_ABORT_NONFINITE;
+      rep->abort_stage = d.stage;
+      rep->abort_inner = d.inner;
+      rep->abort_outer_stage = d.outer_stage;
+      return set_err(hs[0], EMRKC_ENONFINITE, "rkc_iteration: non-finite value at stage %d",
+                     d.stage);
+    }
+  }
+  return EMRKC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int emrkc_estimate_rho(emrkc_handle* h, int32_t which, double t,
+                       const double* v0, double rho0, emrkc_rho_result* out,
+                       double* v_out) {
+  if (!h || !out) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->partitioned)
+    return set_err(h, EMRKC_EINVAL, "estimate_rho: partitioned handles use emrkc_group_estimate_rho");
+  if (which != EMRKC_RHS_F && which != EMRKC_RHS_S)
+    return set_err(h, EMRKC_EINVAL, "estimate_rho: which must be F or S");
+  return power_iteration({h}, which, t, v0, rho0, out, v_out);
+}
+
+int emrkc_step(emrkc_handle* h, double t, double dt, double epsilon,
+               int32_t variant, double rho_F, double rho_S,
+               emrkc_step_report* report) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "emrkc_step: whole-grid handles only");
+  if (variant != EMRKC_VARIANT_STANDARD)
+    return set_err(h, EMRKC_EINVAL, "emrkc_step: only the standard variant is implemented");
+  if (!(dt > 0.0)) return set_err(h, EMRKC_EINVAL, "emrkc_step: dt must be > 0");
+  if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
+  int rc = use_device(h);
+  if (rc) return rc;
+  if ((rc = upload_plan(h, dt, rho_F, rho_S, epsilon))) return rc;
+  if ((rc = ensure_slots(h, 1))) return rc;
+  const unsigned long long init[2] = {kNoEvent, 0ull};
+  CK(h, cudaMemcpyAsync(h->d_event, &kNoEvent, sizeof(kNoEvent), cudaMemcpyHostToDevice,
+                        h->stream));
+  CK(h, cudaMemcpyAsync(h->d_slots, init, sizeof(init), cudaMemcpyHostToDevice, h->stream));
+  const int in = h->cur;
+  int outi = 0;
+  if ((rc = enqueue_step(h, t, 0, h->d_slots, &outi))) return rc;
+  unsigned long long ev = kNoEvent;
+  CK(h, cudaMemcpyAsync(&ev, h->d_event, sizeof(ev), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  Decoded d = decode_event(ev, h->plan);
+  if (!d.none && d.guard) d = Decoded{};  // the guard belongs to the run loop
+  const Plan& pl = h->plan;
+  emrkc_step_report local;
+  emrkc_step_report* rep = report ? report : &local;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->s = pl.s;
+  rep->m = pl.m;
+  rep->eta = pl.eta;
+  rep->ell_s = pl.ell_s;
+  rep->ell_m = pl.ell_m;
+  rep->n_fF = static_cast<int64_t>(pl.s) * pl.m;
+  rep->n_fS = pl.s;
+  rep->n_exp = pl.s;
+  if (d.none) {
+    h->cur = outi;
+    return EMRKC_OK;
+  }
+  h->cur = in;  // NumericalAbort: y is not assigned (P/src/simulate.cpp:215-220)
+  rep->n_fF = rep->n_fS = rep->n_exp = 0;
+  partial_counters(d, pl, &rep->n_fF, &rep->n_fS, &rep->n_exp);
+  rep->abort_kind = EMRKC_ABORT_NONFINITE;
+  rep->abort_stage = d.stage;
+  rep->abort_inner = d.inner;
+  rep->abort_outer_stage = d.outer_stage;
+  return set_err(h, EMRKC_ENONFINITE, "rkc_iteration: non-finite value at stage %d", d.stage);
+}
+
+int emrkc_step_host(emrkc_handle* h, double t, const double* y_in,
+                    double* y_out, int64_t len, double dt, double epsilon,
+                    int32_t variant, double rho_F, double rho_S,
+                    emrkc_step_report* report) {
+  int rc = emrkc_set_state(h, y_in, len);
+  if (rc) return rc;
+  rc = emrkc_step(h, t, dt, epsilon, variant, rho_F, rho_S, report);
+  if (rc) return rc;
+  return emrkc_get_state(h, y_out, len);
+}
+
+int emrkc_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
+              double epsilon, int32_t variant, double rho_F, double rho_S,
+              emrkc_run_result* res) {
+  if (!h || !res) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "emrkc_run: whole-grid handles only");
+  if (variant != EMRKC_VARIANT_STANDARD)
+    return set_err(h, EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
+  if (nsteps < 0) return set_err(h, EMRKC_EINVAL, "emrkc_run: nsteps must be >= 0");
+  return run_slabs({h}, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr);
+}
+
+// ---- groups ---------------------------------------------------------------
+
+int emrkc_group_create(emrkc_handle* const* hs, int32_t n, emrkc_group** out) {
+  if (!hs || n < 1 || !out) return set_global(EMRKC_EINVAL, "group: bad arguments");
+  *out = nullptr;
+  const emrkc_problem& p0 = hs[0]->p;
+  int64_t z = 0;
+  for (int r = 0; r < n; ++r) {
+    emrkc_handle* h = hs[r];
+    if (!h) return set_global(EMRKC_EINVAL, "group: null handle");
+    if (std::memcmp(&h->p, &p0, sizeof(p0)) != 0)
+      return set_global(EMRKC_EINVAL, "group: handles describe different problems");
+    if (h->z_begin != z)
+      return set_global(EMRKC_EINVAL, "group: slabs must be consecutive and ordered");
+    z = h->z_end;
+    if (h->nbr[0] || h->nbr[1])
+      return set_global(EMRKC_EINVAL, "group: handle already linked");
+  }
+  if (z != p0.n[p0.dim - 1])
+    return set_global(EMRKC_EINVAL, "group: slabs do not cover the grid");
+  for (int r = 0; r < n; ++r) {
+    hs[r]->nbr[0] = r > 0 ? hs[r - 1] : nullptr;
+    hs[r]->nbr[1] = r + 1 < n ? hs[r + 1] : nullptr;
+    hs[r]->level = 0;
+    // peer access for stores into neighbours on other devices
+    for (int o = 0; o < n; ++o) {
+      if (hs[o]->device == hs[r]->device) continue;
+      cudaSetDevice(hs[r]->device);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(hs[o]->device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return set_global(EMRKC_ECUDA, "group: peer access %d->%d: %s", hs[r]->device,
+                          hs[o]->device, cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+  }
+  auto* g = new emrkc_group();
+  g->hs.assign(hs, hs + n);
+  *out = g;
+  return EMRKC_OK;
+}
+
+void emrkc_group_destroy(emrkc_group* g) {
+  if (!g) return;
+  for (auto* h : g->hs) {
+    h->nbr[0] = h->nbr[1] = nullptr;
+  }
+  delete g;
+}
+
+int emrkc_group_estimate_rho(emrkc_group* g, int32_t which, double t,
+                             emrkc_rho_result* out) {
+  if (!g || !out) return set_global(EMRKC_EINVAL, "null argument");
+  if (which != EMRKC_RHS_F && which != EMRKC_RHS_S)
+    return set_global(EMRKC_EINVAL, "estimate_rho: which must be F or S");
+  return power_iteration(g->hs, which, t, nullptr, 0.0, out, nullptr);
+}
+
+int emrkc_group_run(emrkc_group* g, int64_t step0, int64_t nsteps, double dt,
+                    double epsilon, int32_t variant, double rho_F,
+                    double rho_S, emrkc_run_result* res) {
+  if (!g || !res) return set_global(EMRKC_EINVAL, "null argument");
+  if (variant != EMRKC_VARIANT_STANDARD)
+    return set_global(EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
+  return run_slabs(g->hs, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr);
+}
+
+// ---- multi-process ----------------------------------------------------------
+
+int64_t emrkc_ipc_blob_size(void) { return 4096; }
+
+int emrkc_ipc_export(emrkc_handle* h, void* blob, int64_t len) {
+  (void)blob;
+  (void)len;
+  return set_err(h, EMRKC_EINVAL, "ipc_export: not implemented yet");
+}
+
+int emrkc_ipc_import(emrkc_handle* h, int32_t side, const void* blob,
+                     int64_t len) {
+  (void)side;
+  (void)blob;
+  (void)len;
+  return set_err(h, EMRKC_EINVAL, "ipc_import: not implemented yet");
+}
+
+int emrkc_dist_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
+                   double epsilon, int32_t variant, double rho_F,
+                   double rho_S, emrkc_run_result* res) {
+  (void)step0;
+  (void)nsteps;
+  (void)dt;
+  (void)epsilon;
+  (void)variant;
+  (void)rho_F;
+  (void)rho_S;
+  (void)res;
+  return set_err(h, EMRKC_EINVAL, "dist_run: not implemented yet");
+}
+
+}  // extern "C"

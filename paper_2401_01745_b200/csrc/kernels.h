@@ -1,0 +1,121 @@
+// kernels.h — host-side launch interface of the emRKC sm_100a kernels.
+// Internal to libemrkc_b200.so (not part of the C ABI).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace emrkc_k {
+
+constexpr unsigned long long kNoEvent = ~0ull;
+constexpr int kMaxStages = 512;  // per rkc iteration (coefficients in params)
+
+// Geometry of the local z-slab (the whole grid when not partitioned).
+// The slab axis is axis dim-1; unused axes have extent 1.
+struct Geom {
+  int dim;
+  int n0, n1, n2;         // local extents per axis (slab axis local count)
+  int nzl, nzg, zoff;     // slab axis: local count, global count, offset
+  long long plane;        // stride of the slab axis
+  long long nn;           // local nodes
+  double w[3];            // sigma_a / (chi C_m dx_a^2)
+  double inv_Cm, Cm;
+  int st_lo[3], st_hi[3]; // stimulus node box per axis (global, inclusive)
+};
+
+// Ghost planes of the V field consumed by one stencil level.
+struct Halo {
+  const double* lo;   // plane z = zoff-1 (null: global boundary)
+  const double* hi;   // plane z = zoff+nzl
+  double* put_lo;     // where my first plane goes (lower neighbour's hi ghost)
+  double* put_hi;     // where my last plane goes (upper neighbour's lo ghost)
+};
+
+// One outer stage of emRKC: pointers and coefficients.
+struct StageArgs {
+  const double* g1;   // g_{j-1} (state layout, 4 blocks)
+  const double* g2;   // g_{j-2} (null for j == 1)
+  double* out;        // g_j
+  double* fs;         // m >= 2: frozen slow V term (n)
+  double* ye;         // m >= 2: y_E gate blocks (3n)
+  double* u[3];       // m >= 2: inner V stages (rotating)
+  double eta, inv_eta;
+  double stim;        // stimulus rate at this stage's time (0 if inactive)
+  double mudt, nu, kappa;  // outer: mu_j*dt, nu_j, kappa_j
+  int j, s, m;
+  // inner coefficients (index 1..m): mu'_k*eta, nu'_k, kappa'_k
+  const double* in_mueta;
+  const double* in_nu;
+  const double* in_kappa;
+  unsigned long long code_base;  // step_in_run * stride
+  unsigned long long* event;     // first abort/guard event (atomicMin)
+  unsigned long long* gate_slot; // [2]: ordered min, max for this step
+  int last;                      // j == s: guard + gate range
+};
+
+// Launch helpers (all asynchronous on `st`). fast: shared-transcendental
+// ionic evaluation (hh_fast) instead of the reference-order one.
+cudaError_t launch_stage_m1(const Geom& g, const Halo& h, const StageArgs& a,
+                            int fast, cudaStream_t st);
+cudaError_t launch_stage_first(const Geom& g, const Halo& h,
+                               const StageArgs& a, int fast, cudaStream_t st);
+cudaError_t launch_stage_inner(const Geom& g, const Halo& h,
+                               const StageArgs& a, int k, int fast,
+                               cudaStream_t st);
+
+// Operator evaluations on the device (for parity / power iteration).
+cudaError_t launch_rhs(const Geom& g, const Halo& h, int which,
+                       const double* y, double stim, double* out,
+                       cudaStream_t st);
+cudaError_t launch_exp_part(const Geom& g, const double* y, double* lam,
+                            double* yinf, cudaStream_t st);
+
+// Power-iteration step: vout = f(y + q v) - fy, partial sums of vout^2.
+// ghost_y / ghost_v: slab-axis ghost planes of y_V and v_V (nullable).
+cudaError_t launch_power(const Geom& g, int which, const double* y,
+                         const double* v, double q,
+                         const double* fy, double stim, double* vout,
+                         const double* gy_lo, const double* gy_hi,
+                         const double* gv_lo, const double* gv_hi,
+                         double* partial, int nblocks, cudaStream_t st);
+cudaError_t launch_norm2_partial(const double* x, long long len,
+                                 double* partial, int nblocks,
+                                 cudaStream_t st);
+cudaError_t launch_sum_partials(const double* partial, int nblocks,
+                                double* out, cudaStream_t st);
+
+// Gate range of a state (ordered-u64 min/max into slot[0..1]) and
+// max |V| (ordered) into *vmax (nullable).
+cudaError_t launch_gate_range(const Geom& g, const double* y,
+                              unsigned long long* slot, cudaStream_t st);
+cudaError_t launch_fold_events(unsigned long long* dst,
+                               unsigned long long* const* src, int n,
+                               cudaStream_t st);
+cudaError_t launch_fill_u64(unsigned long long* p, long long n,
+                            unsigned long long v, cudaStream_t st);
+
+int power_blocks();  // fixed grid of the deterministic reductions
+
+// Ordered-u64 encoding of doubles for atomic min/max.
+__host__ __device__ inline unsigned long long ord_of(double x) {
+  unsigned long long b;
+#ifdef __CUDA_ARCH__
+  b = (unsigned long long)__double_as_longlong(x);
+#else
+  __builtin_memcpy(&b, &x, 8);
+#endif
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ inline double double_of(unsigned long long o) {
+  unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+  double x;
+#ifdef __CUDA_ARCH__
+  x = __longlong_as_double((long long)b);
+#else
+  __builtin_memcpy(&x, &b, 8);
+#endif
+  return x;
+}
+
+}  // namespace emrkc_k

@@ -1,0 +1,165 @@
+"""Synthetic workloads of BASELINE.json (no public dataset is involved).
+
+Unit conversion: 1e-3 S/cm = 0.1 mS/mm, chi = 1400/cm =
+140/mm, C_m = 1 uF/cm^2 = 0.01 uF/mm^2, h = 0.025 cm = 0.25 mm,
+50 uA/cm^2 -> chi*I_stim = 70 uA/mm^3. Stimulus boxes are given in node
+indices and converted with half-cell margins (lo = (i0-0.5)h,
+hi = (i1+0.5)h). Initial states: HH resting state + seeded noise, generated
+once on the host (numpy PCG64) so both sides consume identical bytes.
+
+Configs 3/4 name the CRN and TTP ionic models, which are not in the
+reference or this container; their GRIDS run here with HH
+standing in ("hh" is in every workload name).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .capi import Problem
+from .monodomain import make_problem, resting_state
+
+
+@dataclass
+class Workload:
+    name: str
+    problem: Problem
+    dt: float
+    t_end: float
+    noise: str            # "v_normal_0.1" | "mult_uniform_0.01"
+    seed: int
+    eps: float = 0.05
+    rho_S_forced: float | None = None
+    note: str = ""
+
+    @property
+    def n_steps(self) -> int:
+        return int(round(self.t_end / self.dt))
+
+    @property
+    def n_nodes(self) -> int:
+        return self.problem.n_nodes
+
+    def initial_state(self) -> np.ndarray:
+        V, z = resting_state()
+        nn = self.n_nodes
+        y = np.empty(4 * nn)
+        y[:nn] = V
+        for g in range(3):
+            y[(1 + g) * nn:(2 + g) * nn] = z[g]
+        rng = np.random.default_rng(self.seed)
+        if self.noise == "v_normal_0.1":
+            y[:nn] += rng.normal(0.0, 0.1, nn)
+        elif self.noise == "mult_uniform_0.01":
+            y *= rng.uniform(0.99, 1.01, y.size)
+        return y
+
+    def describe(self) -> dict:
+        p = self.problem
+        return {
+            "workload": self.name,
+            "dim": p.dim,
+            "nodes": [int(p.n[a]) for a in range(p.dim)],
+            "n_nodes": self.n_nodes,
+            "h_mm": p.dx[0],
+            "sigma_mS_per_mm": [p.sigma[a] for a in range(p.dim)],
+            "dt_ms": self.dt,
+            "t_end_ms": self.t_end,
+            "steps": self.n_steps,
+            "ionic_model": "hh",
+            "noise": self.noise,
+            "seed": self.seed,
+            "note": self.note,
+        }
+
+
+def _box(h, lo_idx, hi_idx):
+    return [(i - 0.5) * h for i in lo_idx], [(i + 0.5) * h for i in hi_idx]
+
+
+def hh2d_256() -> Workload:
+    """BASELINE config 1: 2-D 256^2 HH, h=0.25 mm, sigma 0.1 iso, 16^2 corner
+    stimulus 70 uA/mm^3 for [0,1] ms, dt 0.05, T 10 ms."""
+    h = 0.25
+    lo, hi = _box(h, [0, 0], [15, 15])
+    p = make_problem(2, [256, 256], [h, h], [0.1, 0.1], 140.0, 0.01, 70.0, lo, hi, 0.0, 1.0)
+    return Workload("hh2d_256x256", p, 0.05, 10.0, "v_normal_0.1", 1)
+
+
+def hh3d_128() -> Workload:
+    """BASELINE config 2: 3-D 128^3 HH, h=0.25 mm (assumed), sigma
+    (0.2, 0.1, 0.05), 8^3 corner stimulus [0,1] ms, dt 0.05, T 5 ms."""
+    h = 0.25
+    lo, hi = _box(h, [0, 0, 0], [7, 7, 7])
+    p = make_problem(3, [128, 128, 128], [h] * 3, [0.2, 0.1, 0.05], 140.0, 0.01, 70.0, lo, hi,
+                     0.0, 1.0)
+    return Workload("hh3d_128x128x128", p, 0.05, 5.0, "v_normal_0.1", 2)
+
+
+def hh3d_256x256x128() -> Workload:
+    """BASELINE config 3's grid (CRN absent: HH stands in): 256x256x128,
+    h=0.2 mm, sigma 0.15 iso, x=0 face stimulus (4 planes) [0,2] ms,
+    dt 0.05, T 20 ms, +-1% multiplicative noise."""
+    h = 0.2
+    lo, hi = _box(h, [0, 0, 0], [3, 255, 127])
+    p = make_problem(3, [256, 256, 128], [h] * 3, [0.15] * 3, 140.0, 0.01, 70.0, lo, hi, 0.0, 2.0)
+    return Workload("hh3d_256x256x128", p, 0.05, 20.0, "mult_uniform_0.01", 3,
+                    note="config-3 grid; CRN model absent from reference, HH stands in")
+
+
+def hh3d_512x512x256() -> Workload:
+    """BASELINE config 4's grid (TTP absent: HH stands in): 512x512x256,
+    h=0.1 mm, sigma (0.3, 0.1, 0.1), centre 6^3 stimulus [0,1] ms,
+    dt 0.05, T 10 ms, V noise."""
+    h = 0.1
+    lo, hi = _box(h, [253, 253, 125], [258, 258, 130])
+    p = make_problem(3, [512, 512, 256], [h] * 3, [0.3, 0.1, 0.1], 140.0, 0.01, 70.0, lo, hi,
+                     0.0, 1.0)
+    return Workload("hh3d_512x512x256", p, 0.05, 10.0, "v_normal_0.1", 4,
+                    note="config-4 grid; TTP model absent from reference, HH stands in")
+
+
+def hh3d_sweep(N: int) -> Workload:
+    """BASELINE config 5: HH 3-D box, N^3 nodes with h = 10/N mm
+    (N in 25, 50, 100, 200), sigma as config 2, 8^3 corner stimulus."""
+    h = {25: 0.4, 50: 0.2, 100: 0.1, 200: 0.05}[N]
+    lo, hi = _box(h, [0, 0, 0], [7, 7, 7])
+    p = make_problem(3, [N] * 3, [h] * 3, [0.2, 0.1, 0.05], 140.0, 0.01, 70.0, lo, hi, 0.0, 1.0)
+    return Workload(f"hh3d_sweep_{N}", p, 0.05, 5.0, "v_normal_0.1", 50 + N)
+
+
+def parity_2d() -> Workload:
+    """Parity-only case: 128^2, h=0.05 mm, sigma 0.2 iso,
+    16^2 corner, forced rho_S = 200 -> s = 3, m = 2; 60 steps."""
+    h = 0.05
+    lo, hi = _box(h, [0, 0], [15, 15])
+    p = make_problem(2, [128, 128], [h, h], [0.2, 0.2], 140.0, 0.01, 70.0, lo, hi, 0.0, 1.0)
+    return Workload("p2d_128_s3m2", p, 0.05, 3.0, "v_normal_0.1", 7, rho_S_forced=200.0)
+
+
+def parity_3d() -> Workload:
+    """Parity-only case: 48^3, h=0.05 mm, sigma as config 2, 8^3 corner,
+    forced rho_S = 50 -> s = 2, m = 2; 40 steps."""
+    h = 0.05
+    lo, hi = _box(h, [0, 0, 0], [7, 7, 7])
+    p = make_problem(3, [48] * 3, [h] * 3, [0.2, 0.1, 0.05], 140.0, 0.01, 70.0, lo, hi, 0.0, 1.0)
+    return Workload("p3d_48_s2m2", p, 0.05, 2.0, "v_normal_0.1", 8, rho_S_forced=50.0)
+
+
+REGISTRY = {
+    "hh2d_256x256": hh2d_256,
+    "hh3d_128x128x128": hh3d_128,
+    "hh3d_256x256x128": hh3d_256x256x128,
+    "hh3d_512x512x256": hh3d_512x512x256,
+    "hh3d_sweep_25": lambda: hh3d_sweep(25),
+    "hh3d_sweep_50": lambda: hh3d_sweep(50),
+    "hh3d_sweep_100": lambda: hh3d_sweep(100),
+    "hh3d_sweep_200": lambda: hh3d_sweep(200),
+    "p2d_128_s3m2": parity_2d,
+    "p3d_48_s2m2": parity_3d,
+}
+
+
+def get(name: str) -> Workload:
+    return REGISTRY[name]()
