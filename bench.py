@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""bench.py — emRKC node-steps/s (fp64) on B200, BASELINE.json's metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config WORKLOAD]
+
+A step is one emRKC time step (P/src/multirate.cpp:173-189) of the whole
+workload grid; node-steps/s = nodes x steps / seconds. Defaults: N = 1, the
+configs[1] workload of BASELINE.json (HH 3-D 128^3, dt 0.05 ms, T 5 ms =
+100 steps), W = 5, K = 100.
+
+`value`  : device time (CUDA events, per kernel launch, on the launching
+           stream) with the state resident in HBM; L2 (126 MB) is flushed by
+           a 256 MiB memset before every timed step, outside the timed pairs.
+`e2e`    : the per-call drop-in (emrkc_step_host: pinned host state in,
+           one device step, host state out), wall clock around each call.
+`roofline`: the step's dominant kernel, algorithmic bytes / its mean launch
+           time against MEASURED_PEAKS.json hbm_gbs.
+`cpu_baseline`: the reference's own code (oracle/_ref, compiled from the
+           reference sources) on 1 host core, bounded sample, stepping loop
+           only (the reference's wall_time window, P/src/simulate.cpp:175,230).
+`--impl reference`: the reference CPU implementation on all usable host
+           cores (independent replicas: the reference has no intra-run
+           parallelism, P/src/experiments.cpp:22-37).
+Multi-GPU (torchrun, one process per GPU): the grid is split into z-slabs
+(strong scaling) and V halo planes go to the neighbours by peer stores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+FLUSH_BYTES = 256 << 20  # > 2x the 126 MB L2
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+
+# Algorithmic bytes per node of each kernel: fp64 fields a
+# launch must read and write at least once.
+KERNEL_BYTES = {
+    ("m1", "first_outer"): 64,   # g_{j-1} in (4 fields), g_j out (4)
+    ("m1", "outer"): 96,         # + g_{j-2}
+    ("first", None): 72,         # g_{j-1} in (4); u_1, fs, y_E out (5)
+    ("inner", None): 32,         # u_{k-1}, u_{k-2}, fs in; u_k out
+    ("last", "first_outer"): 104,  # u_{m-1}, fs, y_E(3), g_{j-1}(4) in; g_j out (4)
+    ("last", "outer"): 136,        # + g_{j-2}
+}
+
+
+def launch_kinds(s: int, m: int):
+    """(kind, outer) of each launch of one step, in launch order."""
+    out = []
+    for j in range(1, s + 1):
+        o = "first_outer" if j == 1 else "outer"
+        for k in range(1, m + 1):
+            if m == 1:
+                out.append(("m1", o))
+            elif k == 1:
+                out.append(("first", None))
+            elif k < m:
+                out.append(("inner", None))
+            else:
+                out.append(("last", o))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _poll(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._poll, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for name, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def ncu_traffic(workload: str):
+    try:
+        with open(PROFILE_SUMMARY) as f:
+            d = json.load(f)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+def cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (the oracle is only ever the checker / the reported baseline)
+# ---------------------------------------------------------------------------
+
+def cpu_impl():
+    from oracle.oracle import Oracle, Reference, have_reference
+
+    if have_reference():
+        return Reference(), "reference"
+    return Oracle(), "port"
+
+
+def cpu_baseline(w, y0, rF, rS, budget_s=12.0):
+    impl, kind = cpu_impl()
+    p = w.problem
+    _, _, t1 = impl.run(p, y0, 0, 1, w.dt, w.eps, rF, rS)
+    k = int(max(1, min(w.n_steps, budget_s / max(t1, 1e-6))))
+    _, res, wall = impl.run(p, y0, 0, k, w.dt, w.eps, rF, rS)
+    v = w.n_nodes * res.steps_done / wall if wall > 0 else None
+    return {"value": v, "unit": "node-steps/s", "cores": 1, "kind": kind,
+            "sample": f"{k} emRKC steps of the full {w.name} grid from the seeded initial state, "
+                      f"1 thread, stepping loop wall time {wall:.2f} s "
+                      f"({'oracle/_ref: reference sources, -O3' if kind == 'reference' else 'oracle/emrkc_oracle.c'})"}
+
+
+def reference_arm(args, w):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2401_01745_b200.monodomain import resting_state  # host-only numerics
+
+    del resting_state
+    impl, kind = cpu_impl()
+    p = w.problem
+    y0 = w.initial_state()
+    rF = impl.estimate_rho(p, 0, 0.0, y0)[0].rho
+    rS = w.rho_S_forced if w.rho_S_forced is not None else impl.estimate_rho(p, 1, 0.0, y0)[0].rho
+    cores = cpu_count()
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16 << 30
+    per_replica = 20 * 8 * p.state_len()  # the reference's per-call Vec temporaries
+    threads = int(max(1, min(cores, avail * 0.7 // per_replica)))
+    # warm-up (one thread), then the per-step time of one replica
+    impl.run(p, y0, 0, max(0, min(args.warmup, 3) - 1), w.dt, w.eps, rF, rS)
+    _, _, t1 = impl.run(p, y0, 0, 1, w.dt, w.eps, rF, rS)
+    # bounded sample: about a minute of wall time across the threads
+    k = int(max(1, min(args.steps, 45.0 / max(t1, 1e-6))))
+    if kind == "reference":
+        secs = impl.bench(p, y0, k, w.dt, w.eps, rF, rS, threads)
+        wall = float(np.max(secs))
+    else:
+        threads = 1
+        _, _, wall = impl.run(p, y0, 0, k, w.dt, w.eps, rF, rS)
+    v = threads * w.n_nodes * k / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "node-steps/s",
+        "n_gpus": ws, "steps": k, "warmup": min(args.warmup, 3), "ms_per_step": wall * 1e3 / k,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_of(w, ws),
+        "cpu_baseline": {"value": v, "unit": "node-steps/s", "cores": threads, "kind": kind,
+                         "sample": f"{threads} concurrent independent replicas x {k} emRKC steps of the "
+                                   f"full {w.name} grid (the reference's serial loop per replica); "
+                                   f"1-thread step {t1:.3f} s"},
+        "e2e": {"value": v, "unit": "node-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "emRKC node-steps/s (fp64)"
+
+
+def config_of(w, n_gpus):
+    d = w.describe()
+    d["parallelism"] = f"z-slab x{n_gpus}" if n_gpus > 1 else "single GPU"
+    d["l2"] = "flushed (256 MiB memset) before every timed step"
+    return d
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def measure_device(w, device, warmup, steps, with_e2e=True):
+    """Device-resident timing of one workload on one GPU."""
+    import ctypes as C
+
+    from paper_2401_01745_b200 import capi
+    from paper_2401_01745_b200.capi import RunResult, dptr
+    from paper_2401_01745_b200.monodomain import MonodomainOperator
+
+    lib = capi.load()
+    p = w.problem
+    y0 = w.initial_state()
+    op = MonodomainOperator(p, device)
+    op.set_state(y0)
+    rF = op.estimate_spectral_radius(capi.EMRKC_RHS_F, 0.0).rho
+    rS = w.rho_S_forced if w.rho_S_forced is not None else \
+        op.estimate_spectral_radius(capi.EMRKC_RHS_S, 0.0).rho
+    if warmup:
+        op.run(0, warmup, w.dt, rF, rS, w.eps)
+    plan = lib.emrkc_plan_step
+    rep = capi.StepReport()
+    plan(w.dt, rF, rS, w.eps, C.byref(rep))
+    per = rep.s * rep.m
+    launch_ms = np.zeros(steps * per)
+    res = RunResult()
+    rc = lib.emrkc_run_timed(op.handle, warmup, steps, w.dt, w.eps, 0, rF, rS, FLUSH_BYTES,
+                             dptr(launch_ms), launch_ms.size, C.byref(res))
+    if rc:
+        raise RuntimeError(lib.emrkc_last_error(op.handle).decode())
+    out = {"op": op, "y0": y0, "rF": rF, "rS": rS, "s": rep.s, "m": rep.m,
+           "launch_ms": launch_ms.reshape(steps, per), "res": res, "steps": steps}
+    if with_e2e:
+        out["e2e"] = measure_e2e(op, w, y0, rF, rS, min(steps, 20))
+    return out
+
+
+def measure_e2e(op, w, y0, rF, rS, k):
+    """Per-call drop-in: pinned host y in -> device step -> host y out."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2401_01745_b200 import capi
+
+    lib = capi.load()
+    n = y0.size
+    hin = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    hout = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    hin.numpy()[:] = y0
+    pin = C.cast(hin.data_ptr(), capi.DP)
+    pout = C.cast(hout.data_ptr(), capi.DP)
+    rep = capi.StepReport()
+    # warm-up call
+    lib.emrkc_step_host(op.handle, 0.0, pin, pout, n, w.dt, w.eps, 0, rF, rS, C.byref(rep))
+    t0 = time.perf_counter()
+    for r in range(k):
+        rc = lib.emrkc_step_host(op.handle, r * w.dt, pin, pout, n, w.dt, w.eps, 0, rF, rS,
+                                 C.byref(rep))
+        if rc:
+            raise RuntimeError(lib.emrkc_last_error(op.handle).decode())
+        hin, hout = hout, hin  # next step consumes this step's result
+        pin, pout = pout, pin
+    wall = time.perf_counter() - t0
+    return {"value": w.n_nodes * k / wall, "unit": "node-steps/s",
+            "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+            "steps": k, "ms_per_step": wall * 1e3 / k,
+            "api": "emrkc_step_host (C ABI; drop-in of Vec emrkc_step(t, y, dt, rhs, ...))"}
+
+
+def roofline_of(m, w, peak, peak_kind):
+    per_pos = m["launch_ms"].mean(axis=0)
+    kinds = launch_kinds(m["s"], m["m"])
+    dom = int(np.argmax(per_pos))
+    kb = KERNEL_BYTES[kinds[dom]]
+    achieved = kb * w.n_nodes / (per_pos[dom] * 1e-3) / 1e9
+    step_ms = m["launch_ms"].sum(axis=1).mean()
+    step_gbs = 64 * w.n_nodes / (step_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(w.name)
+    return {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": traffic,
+        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+        "kernel": {"m1": "k_stage_m1", "first": "k_stage_first", "inner": "k_stage_inner",
+                   "last": "k_stage_inner(last)"}[kinds[dom][0]],
+        "alg_bytes_per_node": kb, "mean_launch_ms": float(per_pos[dom]),
+        "share_of_step": float(per_pos[dom] / per_pos.sum()),
+        "step_alg_bytes_per_node": 64, "step_achieved_gbs": step_gbs,
+        "step_frac": step_gbs / peak,
+    }
+
+
+def b200_arm(args, w):
+    ws, rank, local = dist_env()
+    if ws > 1:
+        return b200_dist(args, w)
+    import torch  # noqa: F401  (pinned host buffers for e2e)
+
+    peak, peak_kind = hbm_peak()
+    with ClockSampler(local) as clk:
+        m = measure_device(w, local, args.warmup, args.steps)
+    clocks = clk.summary()
+    res = m["res"]
+    total_ms = float(m["launch_ms"].sum())
+    value = w.n_nodes * args.steps / (total_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "node-steps/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded HH resting state + N(0, 0.1 mV) V noise)",
+        "config": config_of(w, 1),
+        "plan": {"s": m["s"], "m": m["m"], "rho_F": m["rF"], "rho_S": m["rS"],
+                 "eta": res.eta, "aborted": bool(res.aborted)},
+        "roofline": roofline_of(m, w, peak, peak_kind),
+        "e2e": m["e2e"],
+        "gpu_launches": int(args.steps * m["s"] * m["m"]),
+        "clocks": clocks,
+    }
+    y0, rF, rS = m["y0"], m["rF"], m["rS"]
+    m["op"].close()
+    del m
+    if not args.no_extra:
+        also = []
+        for name in ("hh3d_512x512x256", "hh2d_256x256"):
+            if name == w.name:
+                continue
+            from paper_2401_01745_b200 import workloads
+
+            wx = workloads.get(name)
+            mx = measure_device(wx, local, 3, 20, with_e2e=False)
+            tot = float(mx["launch_ms"].sum())
+            also.append({"workload": name, "value": wx.n_nodes * 20 / (tot * 1e-3),
+                         "unit": "node-steps/s", "ms_per_step": tot / 20, "s": mx["s"],
+                         "m": mx["m"], "roofline": roofline_of(mx, wx, peak, peak_kind)})
+            mx["op"].close()
+        line["also"] = also
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w, y0, rF, rS)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def b200_dist(args, w):
+    from paper_2401_01745_b200 import dist
+
+    return dist.bench_main(args, w, METRIC, config_of, hbm_peak, ClockSampler)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", default="hh3d_128x128x128")
+    ap.add_argument("--no-extra", action="store_true", help="skip the 'also' workloads")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    from paper_2401_01745_b200 import workloads
+
+    w = workloads.get(args.config)
+    if args.impl == "reference":
+        return reference_arm(args, w)
+    return b200_arm(args, w)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -226,6 +226,17 @@ int emrkc_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
               double epsilon, int32_t variant, double rho_F, double rho_S,
               emrkc_run_result* res);
 
+/* Benchmark form of emrkc_run: before every step, writes flush_bytes of a
+ * scratch buffer (evicts L2; 0 = no flush), then times every kernel launch
+ * of the step with its own CUDA-event pair on the handle's stream.
+ * launch_ms receives nsteps * s * m durations (launch order); the flush is
+ * outside every timed pair. Same numerics and abort semantics as
+ * emrkc_run; res->device_ms is the sum of the launch times. */
+int emrkc_run_timed(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
+                    double epsilon, int32_t variant, double rho_F,
+                    double rho_S, int64_t flush_bytes, double* launch_ms,
+                    int64_t launch_ms_len, emrkc_run_result* res);
+
 /* ---- z-slab groups (multi-slab / multi-GPU) ---------------------------- */
 
 /* A group steps the handles of consecutive z-slabs (ordered bottom to top)

@@ -79,6 +79,25 @@ class Problem(C.Structure):
         }
 
 
+    @classmethod
+    def from_dict(cls, d: dict) -> "Problem":
+        p = cls()
+        p.dim = d["dim"]
+        p.model = d.get("model", EMRKC_MODEL_HH)
+        for a in range(3):
+            p.n[a] = d["n"][a]
+            p.dx[a] = d["dx"][a]
+            p.sigma[a] = d["sigma"][a]
+            p.stim_lo[a] = d["stim_lo"][a]
+            p.stim_hi[a] = d["stim_hi"][a]
+        p.chi = d["chi"]
+        p.C_m = d["C_m"]
+        p.stim_chi_amplitude = d["stim_chi_amplitude"]
+        p.stim_t0 = d["stim_t0"]
+        p.stim_t1 = d["stim_t1"]
+        return p
+
+
 class Partition(C.Structure):
     _fields_ = [("z_begin", C.c_int64), ("z_end", C.c_int64)]
 
@@ -170,6 +189,7 @@ PROTOTYPES = {
     "emrkc_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_step_host": (C.c_int, [C.c_void_p, C.c_double, DP, DP, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
+    "emrkc_run_timed": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.c_int64, DP, C.c_int64, C.POINTER(RunResult)]),
     "emrkc_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_void_p)]),
     "emrkc_group_destroy": (None, [C.c_void_p]),
     "emrkc_group_estimate_rho": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, C.POINTER(RhoResult)]),

@@ -1033,7 +1033,8 @@ fail:
 int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
               int64_t nsteps, double dt, double eps, double rho_F,
               double rho_S, emrkc_run_result* res, bool single_step,
-              emrkc_step_report* rep) {
+              emrkc_step_report* rep, int64_t flush_bytes = 0,
+              double* launch_ms = nullptr, int64_t launch_ms_len = 0) {
   const size_t n = hs.size();
   int rc;
   for (auto* h : hs) {
@@ -1078,7 +1079,45 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     CK(h, cudaSetDevice(h->device));
     CK(h, cudaEventRecord(h->ev0, h->stream));
   }
-  if (n == 1) {
+  std::vector<cudaEvent_t> tev;
+  if (n == 1 && launch_ms) {
+    // benchmark form: flush L2 before each step, one event pair per launch
+    emrkc_handle* h = hs[0];
+    const int64_t per = static_cast<int64_t>(pl.s) * pl.m;
+    if (launch_ms_len < nsteps * per)
+      return set_err(h, EMRKC_EINVAL, "run_timed: launch_ms needs %lld entries",
+                     (long long)(nsteps * per));
+    void* scratch = nullptr;
+    if (flush_bytes > 0) CK(h, cudaMalloc(&scratch, flush_bytes));
+    tev.resize(2 * nsteps * per);
+    for (auto& e : tev) CK(h, cudaEventCreate(&e));
+    int64_t li = 0;
+    for (int64_t r = 0; r < nsteps; ++r) {
+      const double t = static_cast<double>(step0 + r) * dt;
+      in_idx[0][r] = h->cur;
+      if (scratch) CK(h, cudaMemsetAsync(scratch, static_cast<int>(r & 0xff), flush_bytes, h->stream));
+      StepCtx c;
+      begin_step(h, t, r, h->d_slots + 2 * r, &c);
+      for (int j = 1; j <= pl.s; ++j)
+        for (int k = 1; k <= pl.m; ++k, ++li) {
+          CK(h, cudaEventRecord(tev[2 * li], h->stream));
+          if ((rc = launch_level(h, &c, j, k))) return rc;
+          CK(h, cudaEventRecord(tev[2 * li + 1], h->stream));
+        }
+      h->cur = end_step(h, &c);
+    }
+    CK(h, cudaStreamSynchronize(h->stream));
+    double tot = 0.0;
+    for (int64_t i = 0; i < nsteps * per; ++i) {
+      float f = 0.0f;
+      CK(h, cudaEventElapsedTime(&f, tev[2 * i], tev[2 * i + 1]));
+      launch_ms[i] = f;
+      tot += f;
+    }
+    for (auto& e : tev) cudaEventDestroy(e);
+    if (scratch) cudaFree(scratch);
+    if (res) res->device_ms = tot;  // overwritten below, restored after
+  } else if (n == 1) {
     emrkc_handle* h = hs[0];
     for (int64_t r = 0; r < nsteps; ++r) {
       const double t = static_cast<double>(step0 + r) * dt;  // simulate.cpp:177
@@ -1215,6 +1254,11 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     res->m = pl.m;
     res->eta = pl.eta;
     res->device_ms = ms;
+    if (launch_ms) {
+      double tot = 0.0;
+      for (int64_t i = 0; i < nsteps * pl.s * pl.m; ++i) tot += launch_ms[i];
+      res->device_ms = tot;
+    }
   }
   if (rep) {
     std::memset(rep, 0, sizeof(*rep));
@@ -1326,6 +1370,19 @@ int emrkc_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
     return set_err(h, EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
   if (nsteps < 0) return set_err(h, EMRKC_EINVAL, "emrkc_run: nsteps must be >= 0");
   return run_slabs({h}, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr);
+}
+
+int emrkc_run_timed(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
+                    double epsilon, int32_t variant, double rho_F,
+                    double rho_S, int64_t flush_bytes, double* launch_ms,
+                    int64_t launch_ms_len, emrkc_run_result* res) {
+  if (!h || !res || !launch_ms) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "emrkc_run_timed: whole-grid handles only");
+  if (variant != EMRKC_VARIANT_STANDARD)
+    return set_err(h, EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
+  if (nsteps < 0 || flush_bytes < 0) return set_err(h, EMRKC_EINVAL, "emrkc_run_timed: bad sizes");
+  return run_slabs({h}, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr,
+                   flush_bytes, launch_ms, launch_ms_len);
 }
 
 // ---- groups ---------------------------------------------------------------
