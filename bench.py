@@ -7,7 +7,7 @@
 A step is one emRKC time step (P/src/multirate.cpp:173-189) of the whole
 workload grid; node-steps/s = nodes x steps / seconds. Defaults: N = 1, the
 configs[1] workload of BASELINE.json (HH 3-D 128^3, dt 0.05 ms, T 5 ms =
-100 steps), W = 5, K = 100.
+100 steps), W = 5, K = 1000 (ten back-to-back repeats of the 100-step run).
 
 `value`  : device time (CUDA events, per kernel launch, on the launching
            stream) with the state resident in HBM; L2 (126 MB) is flushed by
@@ -76,29 +76,53 @@ def launch_kinds(s: int, m: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled during the timed region (NVML,
+    every ~5 ms; nvidia-smi as a fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_s: float = 0.005):
         self.idx = gpu_index
-        self.samples = []
+        self.period = period_s
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._th = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+            self.max_mhz = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+            try:
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+            return (float(sm), float(self.max_mhz), int(rs))
+        out = subprocess.run(["nvidia-smi", "-i", str(self.idx),
+                              "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5)
+        a = [x.strip() for x in out.stdout.strip().split(",")]
+        return (float(a[0]), float(a[1]), int(a[2], 16))
 
     def _poll(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+                self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         self._th = threading.Thread(target=self._poll, daemon=True)
@@ -112,19 +136,17 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"],
                     "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        busy = [s for s in self.samples if not (s[2] & 0x1)] or self.samples  # drop GpuIdle
         reasons = set()
-        for s in self.samples:
-            for name, v in zip(names, s[4:8]):
-                if v.strip().lower() == "active":
+        for s in busy:
+            for bit, name in self.REASONS.items():
+                if s[2] & bit:
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(s[0] for s in busy),
+                "sm_max_mhz": max(s[1] for s in busy), "reasons": sorted(reasons),
+                "samples": len(busy), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def dist_env():
@@ -245,8 +267,16 @@ def config_of(w, n_gpus):
 # B200 arm
 # ---------------------------------------------------------------------------
 
-def measure_device(w, device, warmup, steps, with_e2e=True):
-    """Device-resident timing of one workload on one GPU."""
+def measure_device(w, device, warmup, steps, with_e2e=True, clocks=None, ramp_s=0.3):
+    """Device-resident timing of one workload on one GPU.
+
+    Warm-up: `warmup` steps, then untimed steps until `ramp_s` of GPU work
+    has passed (SM clock ramp). Timed: `steps` steps as back-to-back
+    repeats of the workload's own simulation (each repeat restarts from the
+    seeded initial state at t = 0 and runs at most the workload's step count),
+    every kernel launch timed by its own CUDA-event pair, L2 flushed before
+    every step outside the pairs. `clocks` (a ClockSampler) is active over
+    the timed loop only."""
     import ctypes as C
 
     from paper_2401_01745_b200 import capi
@@ -261,23 +291,49 @@ def measure_device(w, device, warmup, steps, with_e2e=True):
     rF = op.estimate_spectral_radius(capi.EMRKC_RHS_F, 0.0).rho
     rS = w.rho_S_forced if w.rho_S_forced is not None else \
         op.estimate_spectral_radius(capi.EMRKC_RHS_S, 0.0).rho
-    if warmup:
-        op.run(0, warmup, w.dt, rF, rS, w.eps)
-    plan = lib.emrkc_plan_step
     rep = capi.StepReport()
-    plan(w.dt, rF, rS, w.eps, C.byref(rep))
+    lib.emrkc_plan_step(w.dt, rF, rS, w.eps, C.byref(rep))
     per = rep.s * rep.m
+    op.run(0, warmup, w.dt, rF, rS, w.eps)
+    t0 = time.perf_counter()
+    ramp = 0
+    while time.perf_counter() - t0 < ramp_s:
+        op.run(0, max(1, min(50, w.n_steps)), w.dt, rF, rS, w.eps)
+        op.set_state(y0)
+        ramp += 1
+    chunks = []
+    left = steps
+    while left > 0:
+        chunks.append(min(left, w.n_steps))
+        left -= chunks[-1]
     launch_ms = np.zeros(steps * per)
-    res = RunResult()
-    rc = lib.emrkc_run_timed(op.handle, warmup, steps, w.dt, w.eps, 0, rF, rS, FLUSH_BYTES,
-                             dptr(launch_ms), launch_ms.size, C.byref(res))
-    if rc:
-        raise RuntimeError(lib.emrkc_last_error(op.handle).decode())
+    results = []
+    ctx = clocks if clocks is not None else _Null()
+    with ctx:
+        off = 0
+        for ck in chunks:
+            op.set_state(y0)
+            res = RunResult()
+            rc = lib.emrkc_run_timed(op.handle, 0, ck, w.dt, w.eps, 0, rF, rS, FLUSH_BYTES,
+                                     dptr(launch_ms[off:]), ck * per, C.byref(res))
+            if rc:
+                raise RuntimeError(lib.emrkc_last_error(op.handle).decode())
+            results.append(res)
+            off += ck * per
     out = {"op": op, "y0": y0, "rF": rF, "rS": rS, "s": rep.s, "m": rep.m,
-           "launch_ms": launch_ms.reshape(steps, per), "res": res, "steps": steps}
+           "launch_ms": launch_ms.reshape(steps, per), "res": results[-1], "steps": steps,
+           "repeats": len(chunks), "aborted": any(r.aborted for r in results)}
     if with_e2e:
         out["e2e"] = measure_e2e(op, w, y0, rF, rS, min(steps, 20))
     return out
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
 
 
 def measure_e2e(op, w, y0, rF, rS, k):
@@ -342,8 +398,8 @@ def b200_arm(args, w):
     import torch  # noqa: F401  (pinned host buffers for e2e)
 
     peak, peak_kind = hbm_peak()
-    with ClockSampler(local) as clk:
-        m = measure_device(w, local, args.warmup, args.steps)
+    clk = ClockSampler(local)
+    m = measure_device(w, local, args.warmup, args.steps, clocks=clk)
     clocks = clk.summary()
     res = m["res"]
     total_ms = float(m["launch_ms"].sum())
@@ -355,7 +411,10 @@ def b200_arm(args, w):
         "data": "synthetic (seeded HH resting state + N(0, 0.1 mV) V noise)",
         "config": config_of(w, 1),
         "plan": {"s": m["s"], "m": m["m"], "rho_F": m["rF"], "rho_S": m["rS"],
-                 "eta": res.eta, "aborted": bool(res.aborted)},
+                 "eta": res.eta, "aborted": bool(m["aborted"]),
+                 "timed_repeats": m["repeats"],
+                 "timed_note": f"{args.steps} timed steps = {m['repeats']} repeat(s) of the "
+                               f"workload's simulation from the seeded state (<= {w.n_steps} steps each)"},
         "roofline": roofline_of(m, w, peak, peak_kind),
         "e2e": m["e2e"],
         "gpu_launches": int(args.steps * m["s"] * m["m"]),
@@ -394,7 +453,7 @@ def b200_dist(args, w):
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", default="hh3d_128x128x128")

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libemrkc_b200.so")
+LIB_PATH = os.environ.get("EMRKC_LIB") or os.path.join(_HERE, "libemrkc_b200.so")
 
 # ---- enums (include/emrkc.h) ------------------------------------------------
 EMRKC_OK = 0

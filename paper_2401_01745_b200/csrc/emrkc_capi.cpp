@@ -252,6 +252,8 @@ struct emrkc_handle {
   Plan plan;
   bool plan_uploaded = false;
   int fast = 1;
+  int pipe = 1;
+  int zc = 1;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::string err;
 };
@@ -409,12 +411,66 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
   const double r = (j == 1) ? c->t : c->t + pl.outer.c[j - 1] * pl.dt;
   a.stim = stim_rate_at(&h->p, r);
   const Halo hl = halo_at(h, h->level);
-  if (pl.m == 1)
-    CK(h, emrkc_k::launch_stage_m1(h->geom, hl, a, h->fast, h->stream));
-  else if (k == 1)
-    CK(h, emrkc_k::launch_stage_first(h->geom, hl, a, h->fast, h->stream));
-  else
-    CK(h, emrkc_k::launch_stage_inner(h->geom, hl, a, k, h->fast, h->stream));
+  if (h->fast) {
+    const double cG = pl.mudt[j] / pl.eta;
+    if (k == 1) {
+      emrkc_k::FastArgs f{};
+      f.g1 = a.g1;
+      f.g2 = a.g2;
+      f.out = a.out;
+      f.fs = h->fs;
+      f.u1 = h->u[0];
+      f.eta = pl.eta;
+      f.stim = a.stim;
+      f.cG = cG;
+      f.cV = cG * pl.in_mueta[1];
+      f.mue1 = pl.in_mueta[1];
+      f.nu = a.nu;
+      f.kappa = a.kappa;
+      f.j = j;
+      f.m = pl.m;
+      f.s = pl.s;
+      f.last = a.last;
+      f.zc = h->zc;
+      f.code_base = a.code_base;
+      f.event = a.event;
+      f.gate_slot = a.gate_slot;
+      if (h->pipe)
+        CK(h, emrkc_k::launch_node_pipe(h->geom, hl, f, pl.m >= 2, h->stream));
+      else
+        CK(h, emrkc_k::launch_node_fast(h->geom, hl, f, pl.m >= 2, h->stream));
+    } else {
+      emrkc_k::FastInnerArgs f{};
+      f.um1 = h->u[(k - 2) % 3];
+      f.um2 = (k == 2) ? a.g1 : h->u[(k - 3) % 3];
+      f.fs = h->fs;
+      f.uk = h->u[(k - 1) % 3];
+      f.g1v = a.g1;
+      f.g2v = a.g2;
+      f.outv = a.out;
+      f.mueta = pl.in_mueta[k];
+      f.nu = pl.inner.nu[k];
+      f.kappa = pl.inner.kappa[k];
+      f.onu = a.nu;
+      f.okappa = a.kappa;
+      f.cG = cG;
+      f.j = j;
+      f.k = k;
+      f.m = pl.m;
+      f.s = pl.s;
+      f.last = a.last;
+      f.zc = h->zc;
+      f.code_base = a.code_base;
+      f.event = a.event;
+      CK(h, emrkc_k::launch_vin_fast(h->geom, hl, f, h->stream));
+    }
+  } else if (pl.m == 1) {
+    CK(h, emrkc_k::launch_stage_m1(h->geom, hl, a, 0, h->stream));
+  } else if (k == 1) {
+    CK(h, emrkc_k::launch_stage_first(h->geom, hl, a, 0, h->stream));
+  } else {
+    CK(h, emrkc_k::launch_stage_inner(h->geom, hl, a, k, 0, h->stream));
+  }
   ++h->level;
   return EMRKC_OK;
 }
@@ -494,6 +550,11 @@ int init_handle(emrkc_handle* h) {
   }
   const char* f = std::getenv("EMRKC_FAST");
   h->fast = f ? std::atoi(f) : 1;
+  h->zc = emrkc_k::fast_zc(h->geom);
+  const char* pp = std::getenv("EMRKC_PIPE");
+  h->pipe = (pp && *pp) ? std::atoi(pp) : 1;
+  if (const char* zc = std::getenv("EMRKC_ZC"))
+    if (*zc) h->zc = std::max(1, std::atoi(zc));
   return EMRKC_OK;
 }
 
@@ -674,6 +735,7 @@ int emrkc_create(const emrkc_problem* p, int32_t device,
   for (int a = 0; a < 3; ++a)
     g.w[a] = (a < p->dim) ? p->sigma[a] / (p->chi * p->C_m * p->dx[a] * p->dx[a])
                           : 0.0;
+  g.wc = -2.0 * (g.w[0] + g.w[1] + g.w[2]);
   g.Cm = p->C_m;
   g.inv_Cm = 1.0 / p->C_m;
   for (int a = 0; a < 3; ++a) {
@@ -1250,9 +1312,11 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     res->n_fS = done * pl.s;
     res->n_exp = done * pl.s;
     if (!d.none && !d.guard) partial_counters(d, pl, &res->n_fF, &res->n_fS, &res->n_exp);
-    res->s = pl.s;
-    res->m = pl.m;
-    res->eta = pl.eta;
+    // plan of the last accepted step (RunResult::steps.back(),
+    // P/src/simulate.cpp:205); none when no step was accepted
+    res->s = done > 0 ? pl.s : 0;
+    res->m = done > 0 ? pl.m : 0;
+    res->eta = done > 0 ? pl.eta : 0.0;
     res->device_ms = ms;
     if (launch_ms) {
       double tot = 0.0;

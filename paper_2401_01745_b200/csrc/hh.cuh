@@ -131,4 +131,20 @@ __device__ __forceinline__ void hh_gate_coeffs_fast(double V, double* lam,
   zinf[2] = nn * ipn;
 }
 
+// Reference-order exponential Euler of the gates (the fast kernels' path
+// for |V| > kFastVmax or non-finite V): d = expm1(eta*Lambda)(z - z_inf).
+struct Dgate {
+  double d0, d1, d2;
+};
+static __device__ __noinline__ Dgate hh_expeuler_ref(double V, double z0, double z1,
+                                                     double z2, double eta) {
+  double lam[3], zinf[3];
+  hh_gate_coeffs_ref(V, lam, zinf);
+  Dgate d;
+  d.d0 = expm1(eta * lam[0]) * (z0 - zinf[0]);
+  d.d1 = expm1(eta * lam[1]) * (z1 - zinf[1]);
+  d.d2 = expm1(eta * lam[2]) * (z2 - zinf[2]);
+  return d;
+}
+
 }  // namespace emrkc_dev

@@ -553,7 +553,9 @@ __global__ void __launch_bounds__(kThreads)
   if (n.valid) {
     const long long nn = g.nn;
     for (int q = 1; q <= 3; ++q) {
-      const unsigned long long o = ord_of(y[q * nn + n.i]);
+      const double v = y[q * nn + n.i];
+      if (v != v) continue;  // NaN never wins std::min / std::max (simulate.cpp:82-83)
+      const unsigned long long o = ord_of(v);
       lo = min(lo, o);
       hi = max(hi, o);
     }

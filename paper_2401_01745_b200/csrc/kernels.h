@@ -20,6 +20,7 @@ struct Geom {
   long long plane;        // stride of the slab axis
   long long nn;           // local nodes
   double w[3];            // sigma_a / (chi C_m dx_a^2)
+  double wc;              // -2 sum_a w_a (fast kernels)
   double inv_Cm, Cm;
   int st_lo[3], st_hi[3]; // stimulus node box per axis (global, inclusive)
 };
@@ -53,6 +54,48 @@ struct StageArgs {
   unsigned long long* gate_slot; // [2]: ordered min, max for this step
   int last;                      // j == s: guard + gate range
 };
+
+// Arguments of the fast kernels (kernels_fast.cu): one outer stage j.
+struct FastArgs {
+  const double* g1;   // g_{j-1}
+  const double* g2;   // g_{j-2} (j >= 2)
+  double* out;        // g_j (m == 1: all blocks; m >= 2: gate blocks)
+  double* fs;         // m >= 2: frozen slow V term
+  double* u1;         // m >= 2: inner stage 1 of V
+  double eta;
+  double stim;        // stimulus rate at the stage time (0 if inactive)
+  double cG;          // mu_j dt / eta   (gate rows: g_j = base + cG (y_E - z))
+  double cV;          // cG * mu'_1 eta  (m == 1: V of g_j = base + cV (f_F + f_S))
+  double mue1;        // mu'_1 eta       (m >= 2: u_1 = V + mue1 (f_F + f_S))
+  double nu, kappa;   // outer nu_j, kappa_j (j >= 2)
+  int j, m, s, last, zc;
+  unsigned long long code_base;
+  unsigned long long* event;
+  unsigned long long* gate_slot;
+};
+
+struct FastInnerArgs {
+  const double* um1;  // u_{k-1} (stencil field)
+  const double* um2;  // u_{k-2} (V block of g_{j-1} when k == 2)
+  const double* fs;
+  double* uk;         // k < m
+  const double* g1v;  // k == m: V of g_{j-1}, g_{j-2}
+  const double* g2v;
+  double* outv;       // k == m: V block of g_j
+  double mueta, nu, kappa;  // inner mu'_k eta, nu'_k, kappa'_k
+  double onu, okappa, cG;   // outer nu_j, kappa_j, mu_j dt / eta
+  int j, k, m, s, last, zc;
+  unsigned long long code_base;
+  unsigned long long* event;
+};
+
+int fast_zc(const Geom& g);
+cudaError_t launch_node_fast(const Geom& g, const Halo& h, const FastArgs& a,
+                             bool ion, cudaStream_t st);
+cudaError_t launch_node_pipe(const Geom& g, const Halo& h, const FastArgs& a,
+                             bool ion, cudaStream_t st);
+cudaError_t launch_vin_fast(const Geom& g, const Halo& h,
+                            const FastInnerArgs& a, cudaStream_t st);
 
 // Launch helpers (all asynchronous on `st`). fast: shared-transcendental
 // ionic evaluation (hh_fast) instead of the reference-order one.

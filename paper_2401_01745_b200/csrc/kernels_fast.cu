@@ -1,0 +1,702 @@
+// kernels_fast.cu — the default (fast) emRKC kernels for sm_100a.
+//
+// Same step as kernels.cu with the per-node arithmetic cut to
+// what the FP64 pipe can sustain at HBM speed:
+//  * z-marching (2.5-D): each thread owns one (x, y) column and walks `zc`
+//    consecutive planes of its slab, keeping V(z-1), V(z), V(z+1) in
+//    registers; x/y neighbours come from L1. Block prologue (abort-word
+//    check, 2 KiB exp table) and epilogue (gate range, norm guard) are
+//    amortised over the column.
+//  * ionic model through fast_math.cuh (3 + 3 table exps, one reciprocal).
+//  * recurrences in FMA form, and the algebra of SURVEY §8(a): f_F and f_S
+//    vanish on gate rows, so a gate's inner iterate is y_E (nu' + kappa' = 1)
+//    and its outer update is base + (mu_j dt / eta) (y_E - z); only V needs
+//    the stencil recurrence.
+// All of this moves results by rounding only; tests/test_gpu_parity.py holds
+// the default path to the reference within rel-L2 1e-9 (north_star).
+//
+// Kernels:
+//  k_m1_fast    m == 1: one HBM pass per outer stage (reads g_{j-1}[, g_{j-2}],
+//               writes g_j): the BASELINE configs 1-3 case.
+//  k_ion_fast   m >= 2, inner stage 1: ionic + gates of g_j (final), fs, u_1.
+//  k_vin_fast   m >= 2, inner stage k >= 2, V block only; the k == m launch
+//               forms V of g_j.
+#include <cstdio>
+
+#include "fast_math.cuh"
+#include "hh.cuh"
+#include "kernels.h"
+
+namespace emrkc_k {
+
+using namespace emrkc_dev;
+
+namespace {
+
+constexpr int FBX = 32;
+constexpr int FBY = 4;
+constexpr int kFThreads = FBX * FBY;
+
+template <int DIM>
+struct Col {
+  int c0, c1;
+  long long ip;
+  int z0, z1;
+  bool valid;
+};
+
+// Thread -> (column, z range). DIM 3: block = 32 x 8 columns, blockIdx.z
+// picks the z chunk. DIM 2: x from 32 lanes, (blockIdx.y, threadIdx.y) pick
+// the chunk of rows (the slab axis is axis 1). DIM 1: one node per thread.
+template <int DIM>
+__device__ __forceinline__ Col<DIM> col_here(const Geom& g, int zc) {
+  Col<DIM> c;
+  if (DIM == 3) {
+    c.c0 = blockIdx.x * FBX + threadIdx.x;
+    c.c1 = blockIdx.y * FBY + threadIdx.y;
+    c.z0 = blockIdx.z * zc;
+    c.valid = c.c0 < g.n0 && c.c1 < g.n1;
+    c.ip = (long long)c.c0 + (long long)g.n0 * c.c1;
+  } else if (DIM == 2) {
+    c.c0 = blockIdx.x * FBX + threadIdx.x;
+    c.c1 = 0;
+    c.z0 = (blockIdx.y * FBY + threadIdx.y) * zc;
+    c.valid = c.c0 < g.n0;
+    c.ip = c.c0;
+  } else {
+    c.c0 = c.c1 = 0;
+    c.z0 = (blockIdx.x * FBY + threadIdx.y) * FBX + threadIdx.x;
+    c.valid = true;
+    c.ip = 0;
+    zc = 1;
+  }
+  c.z1 = min(g.nzl, c.z0 + zc);
+  c.valid = c.valid && c.z0 < c.z1;
+  return c;
+}
+
+// Field value at local plane zz in [-1, nzl] of a column: interior, mirror
+// at the global boundary (P/src/monodomain.cpp:85-86), or ghost plane.
+__device__ __forceinline__ double zval(const double* __restrict__ f, const Geom& g,
+                                       long long ip, int zz, const double* glo,
+                                       const double* ghi) {
+  if (zz >= 0 && zz < g.nzl) return __ldg(f + ip + g.plane * zz);
+  int gz = zz + g.zoff;
+  gz = gz < 0 ? 1 : (gz >= g.nzg ? g.nzg - 2 : gz);
+  const int lz = gz - g.zoff;
+  if (lz >= 0 && lz < g.nzl) return __ldg(f + ip + g.plane * lz);
+  return lz < 0 ? __ldg(glo + ip) : __ldg(ghi + ip);
+}
+
+// In-plane neighbour offsets of a column (mirror at the boundaries).
+template <int DIM>
+struct Nbr {
+  long long xm, xp, ym, yp;
+};
+
+template <int DIM>
+__device__ __forceinline__ Nbr<DIM> nbr_of(const Geom& g, const Col<DIM>& c) {
+  Nbr<DIM> o{0, 0, 0, 0};
+  if (DIM >= 2) {
+    o.xm = c.c0 > 0 ? -1 : 1;
+    o.xp = c.c0 < g.n0 - 1 ? 1 : -1;
+  }
+  if (DIM == 3) {
+    o.ym = c.c1 > 0 ? -(long long)g.n0 : (long long)g.n0;
+    o.yp = c.c1 < g.n1 - 1 ? (long long)g.n0 : -(long long)g.n0;
+  }
+  return o;
+}
+
+// Scaled Laplacian with the column's z values in registers (FMA form;
+// wc = -2 sum_a w_a).
+template <int DIM>
+__device__ __forceinline__ double lap_fast(const Geom& g, const double* __restrict__ f,
+                                           long long i, const Nbr<DIM>& o, double vm,
+                                           double vc, double vp) {
+  double d = fma(g.wc, vc, g.w[DIM - 1] * (vp + vm));
+  if (DIM >= 2) d = fma(g.w[0], __ldg(f + i + o.xm) + __ldg(f + i + o.xp), d);
+  if (DIM == 3) d = fma(g.w[1], __ldg(f + i + o.ym) + __ldg(f + i + o.yp), d);
+  return d;
+}
+
+template <int DIM>
+__device__ __forceinline__ bool stim_col(const Geom& g, const Col<DIM>& c) {
+  if (DIM == 3)
+    return c.c0 >= g.st_lo[0] && c.c0 <= g.st_hi[0] && c.c1 >= g.st_lo[1] &&
+           c.c1 <= g.st_hi[1];
+  if (DIM == 2) return c.c0 >= g.st_lo[0] && c.c0 <= g.st_hi[0];
+  return true;
+}
+
+template <int DIM>
+__device__ __forceinline__ bool stim_col_xy(const Geom& g, int x, int y) {
+  if (DIM == 3)
+    return x >= g.st_lo[0] && x <= g.st_hi[0] && y >= g.st_lo[1] && y <= g.st_hi[1];
+  return x >= g.st_lo[0] && x <= g.st_hi[0];
+}
+
+template <int DIM>
+__device__ __forceinline__ bool stim_z(const Geom& g, int z) {
+  const int zg = z + g.zoff;
+  return zg >= g.st_lo[DIM - 1] && zg <= g.st_hi[DIM - 1];
+}
+
+// I_ion of HH (P/src/ionic.cpp:111-116), FMA form.
+__device__ __forceinline__ double current_fast(double V, double m, double h, double n) {
+  const double m2 = m * m;
+  const double n2 = n * n;
+  const double gna = kFC.gna * (m2 * m) * h;
+  const double gk = kFC.gk * (n2 * n2);
+  return fma(gna, V - kVNa, fma(gk, V - kVK, kFC.gl * (V - kFC.vl)));
+}
+
+__device__ __forceinline__ bool prologue(const unsigned long long* ev, double* tab) {
+  __shared__ int skip;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  if (tid == 0) skip = (*(volatile const unsigned long long*)ev) != kNoEvent;
+  if (tab) load_exp_table(tab, tid, blockDim.x * blockDim.y);
+  __syncthreads();
+  return skip != 0;
+}
+
+__device__ __forceinline__ void block_gate_range(unsigned long long* slot,
+                                                 unsigned long long lo,
+                                                 unsigned long long hi) {
+  __shared__ unsigned long long slo[kFThreads / 32], shi[kFThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  if ((tid & 31) == 0) {
+    slo[tid >> 5] = lo;
+    shi[tid >> 5] = hi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kFThreads / 32; ++w) {
+      lo = min(lo, slo[w]);
+      hi = max(hi, shi[w]);
+    }
+    if (lo != ~0ull) atomicMin(slot, lo);
+    if (hi != 0ull) atomicMax(slot + 1, hi);
+  }
+}
+
+// Block min/max of the gate outputs (P/src/simulate.cpp:76-85): per-thread
+// running min/max in double, one ordered-u64 atomic per block.
+__device__ __forceinline__ void block_gate_range_d(unsigned long long* slot, double lo,
+                                                   double hi, bool any) {
+  block_gate_range(slot, any ? ord_of(lo) : ~0ull, any ? ord_of(hi) : 0ull);
+}
+
+// Per-node body shared by the z loop: computes the outputs of one node.
+struct NodeOut {
+  double o0, o1, o2, o3;
+  double fs;
+};
+
+template <int DIM, int FIRST, int ION>
+__device__ __forceinline__ NodeOut node_update(const Geom& g, const FastArgs& a,
+                                               const double* __restrict__ tab, double vm,
+                                               double vc, double vp, double xs, double ys,
+                                               double z0, double z1, double z2, double stim,
+                                               const double* __restrict__ q2) {
+  double D = fma(g.wc, vc, g.w[DIM - 1] * (vp + vm));
+  if (DIM >= 2) D = fma(g.w[0], xs, D);
+  if (DIM == 3) D = fma(g.w[1], ys, D);
+  double d0, d1, d2;
+  if (fabs(vc) <= kFastVmax) {
+    hh_expeuler_fast(vc, z0, z1, z2, a.eta, tab, d0, d1, d2);
+  } else {
+    const Dgate dd = hh_expeuler_ref(vc, z0, z1, z2, a.eta);
+    d0 = dd.d0;
+    d1 = dd.d1;
+    d2 = dd.d2;
+  }
+  const double fs = fma(-current_fast(vc, z0 + d0, z1 + d1, z2 + d2), g.inv_Cm, stim);
+  const double fsum = D + fs;  // (f_F + f_S)(y_E) on V: inner stage 1
+  double b0 = vc, b1 = z0, b2 = z1, b3 = z2;
+  if (!FIRST) {
+    b0 = fma(a.nu, vc, a.kappa * __ldg(q2));
+    b1 = fma(a.nu, z0, a.kappa * __ldg(q2 + g.nn));
+    b2 = fma(a.nu, z1, a.kappa * __ldg(q2 + 2 * g.nn));
+    b3 = fma(a.nu, z2, a.kappa * __ldg(q2 + 3 * g.nn));
+  }
+  NodeOut r;
+  r.o1 = fma(a.cG, d0, b1);
+  r.o2 = fma(a.cG, d1, b2);
+  r.o3 = fma(a.cG, d2, b3);
+  r.o0 = ION ? fma(a.mue1, fsum, vc) : fma(a.cV, fsum, b0);
+  r.fs = fs;
+  return r;
+}
+
+template <int DIM, int FIRST, int ION>
+__device__ __forceinline__ NodeOut node_update_s(const Geom& g, const FastArgs& a,
+                                                 const double* __restrict__ tab, double vm,
+                                                 double vc, double vp, double xs, double ys,
+                                                 double z0, double z1, double z2, double stim,
+                                                 const double* q2s, int qstride) {
+  double D = fma(g.wc, vc, g.w[DIM - 1] * (vp + vm));
+  if (DIM >= 2) D = fma(g.w[0], xs, D);
+  if (DIM == 3) D = fma(g.w[1], ys, D);
+  double d0, d1, d2;
+  if (fabs(vc) <= kFastVmax) {
+    hh_expeuler_fast(vc, z0, z1, z2, a.eta, tab, d0, d1, d2);
+  } else {
+    const Dgate dd = hh_expeuler_ref(vc, z0, z1, z2, a.eta);
+    d0 = dd.d0;
+    d1 = dd.d1;
+    d2 = dd.d2;
+  }
+  const double fs = fma(-current_fast(vc, z0 + d0, z1 + d1, z2 + d2), g.inv_Cm, stim);
+  const double fsum = D + fs;
+  double b0 = vc, b1 = z0, b2 = z1, b3 = z2;
+  if (!FIRST) {
+    b0 = fma(a.nu, vc, a.kappa * q2s[0]);
+    b1 = fma(a.nu, z0, a.kappa * q2s[qstride]);
+    b2 = fma(a.nu, z1, a.kappa * q2s[2 * qstride]);
+    b3 = fma(a.nu, z2, a.kappa * q2s[3 * qstride]);
+  }
+  NodeOut r;
+  r.o1 = fma(a.cG, d0, b1);
+  r.o2 = fma(a.cG, d1, b2);
+  r.o3 = fma(a.cG, d2, b3);
+  r.o0 = ION ? fma(a.mue1, fsum, vc) : fma(a.cV, fsum, b0);
+  r.fs = fs;
+  return r;
+}
+
+// Exact abort ordinal of a column whose outputs went non-finite: the
+// reference checks inner stage 1 (y_E, f_F + f_S) before the outer stage
+// (P/src/cheb.cpp:73-80, multirate.cpp:100-104). Rare path.
+template <int DIM>
+__device__ __noinline__ bool inner_nonfinite(const Geom& g, const Halo& h, const double* G,
+                                             const Col<DIM>& c, const Nbr<DIM>& o, double eta) {
+  bool inner = false;
+  for (int z = c.z0; z < c.z1; ++z) {
+    const long long j = c.ip + g.plane * z;
+    const double V = zval(G, g, c.ip, z, h.lo, h.hi);
+    double D = fma(g.wc, V, g.w[DIM - 1] * (zval(G, g, c.ip, z - 1, h.lo, h.hi) +
+                                            zval(G, g, c.ip, z + 1, h.lo, h.hi)));
+    if (DIM >= 2) D = fma(g.w[0], __ldg(G + j + o.xm) + __ldg(G + j + o.xp), D);
+    if (DIM == 3) D = fma(g.w[1], __ldg(G + j + o.ym) + __ldg(G + j + o.yp), D);
+    const double z0 = __ldg(G + g.nn + j), z1 = __ldg(G + 2 * g.nn + j),
+                 z2 = __ldg(G + 3 * g.nn + j);
+    const Dgate d = hh_expeuler_ref(V, z0, z1, z2, eta);
+    const double y0 = z0 + d.d0, y1 = z1 + d.d1, y2 = z2 + d.d2;
+    const double fs = -current_fast(V, y0, y1, y2) * g.inv_Cm;
+    inner |= !(finite_hi(D + fs) && finite_hi(y0) && finite_hi(y1) && finite_hi(y2));
+  }
+  return inner;
+}
+
+// ---------------------------------------------------------------------------
+// k_node_fast: m == 1 (ION = 0, one HBM pass per outer stage) and the first
+// inner stage of m >= 2 (ION = 1: gate rows of g_j, fs, u_1).
+// ---------------------------------------------------------------------------
+#ifndef EMRKC_NODE_MINBLOCKS
+#define EMRKC_NODE_MINBLOCKS 1
+#endif
+#ifndef EMRKC_NODE_UNROLL
+#define EMRKC_NODE_UNROLL 2
+#endif
+constexpr int kNodeUnroll = EMRKC_NODE_UNROLL;
+template <int DIM, int FIRST, int ION>
+__global__ void __launch_bounds__(kFThreads, EMRKC_NODE_MINBLOCKS)
+    k_node_fast(const Geom g, const Halo h, const FastArgs a) {
+  __shared__ double tab[256];
+  if (prologue(a.event, tab)) return;
+  const Col<DIM> c = col_here<DIM>(g, a.zc);
+  bool bad = false, guard = false, any = false;
+  double glo = 2.0, ghi = -1.0;
+  if (c.valid) {
+    const Nbr<DIM> o = nbr_of<DIM>(g, c);
+    const bool scol = stim_col<DIM>(g, c);
+    const long long plane = g.plane, nn = g.nn;
+    const double* __restrict__ G = a.g1;
+    const long long i0 = c.ip + plane * c.z0;
+    const double* pv = G + i0;           // V of g_{j-1} at (column, z)
+    const double* pz = G + nn + i0;      // gate 0 (gates 1, 2 at +nn, +2nn)
+    double* po = a.out + i0;             // g_j
+    const double* q2 = FIRST ? nullptr : a.g2 + i0;
+    double* pu = ION ? a.u1 + i0 : nullptr;
+    double* pf = ION ? a.fs + i0 : nullptr;
+    double vm = zval(G, g, c.ip, c.z0 - 1, h.lo, h.hi);
+    double vc = __ldg(pv);
+#pragma unroll kNodeUnroll
+    for (int z = c.z0; z < c.z1; ++z) {
+      const double vp = (z + 1 < g.nzl) ? __ldg(pv + plane)
+                                        : zval(G, g, c.ip, z + 1, h.lo, h.hi);
+      double xs = 0.0, ys = 0.0;
+      if (DIM >= 2) xs = __ldg(pv + o.xm) + __ldg(pv + o.xp);
+      if (DIM == 3) ys = __ldg(pv + o.ym) + __ldg(pv + o.yp);
+      const double z0 = __ldg(pz), z1 = __ldg(pz + nn), z2 = __ldg(pz + 2 * nn);
+      const double stim = (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0;
+      const NodeOut r = node_update<DIM, FIRST, ION>(g, a, tab, vm, vc, vp, xs, ys, z0, z1,
+                                                     z2, stim, q2);
+      po[nn] = r.o1;
+      po[2 * nn] = r.o2;
+      po[3 * nn] = r.o3;
+      if (ION) {
+        *pu = r.o0;
+        *pf = r.fs;
+        pu += plane;
+        pf += plane;
+      } else {
+        *po = r.o0;
+        guard |= fabs(r.o0) > 1e6;
+      }
+      bad |= !(finite_hi(r.o0) && finite_hi(r.o1) && finite_hi(r.o2) && finite_hi(r.o3));
+      if (z == 0 && h.put_lo) h.put_lo[c.ip] = r.o0;
+      if (z == g.nzl - 1 && h.put_hi) h.put_hi[c.ip] = r.o0;
+      if (a.last) {
+        glo = fmin(glo, fmin(r.o1, fmin(r.o2, r.o3)));
+        ghi = fmax(ghi, fmax(r.o1, fmax(r.o2, r.o3)));
+        any = true;
+      }
+      vm = vc;
+      vc = vp;
+      pv += plane;
+      pz += plane;
+      po += plane;
+      if (!FIRST) q2 += plane;
+    }
+    if (bad) {
+      const bool inner = inner_nonfinite<DIM>(g, h, G, c, o, a.eta);
+      atomicMin(a.event, a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1)) +
+                             (inner ? 1 : a.m + 1));
+    }
+  }
+  if (!ION && a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+  if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, any);
+}
+
+// ---------------------------------------------------------------------------
+// k_node_pipe: the node kernel with its planes staged through shared memory
+// by cp.async (LDGSTS), two planes ahead of the compute. A block owns a
+// TX x TY column tile and walks zc planes; each plane stage holds the V tile
+// with a one-cell halo (mirror cells resolved at load time, so the compute
+// has no boundary logic) and the tile's gate values. Ring depths: V 5
+// (planes p-1, p, p+1 read while p+2 lands), gates 4 — each stage is
+// rewritten only after a __syncthreads separates it from its last reader.
+// ---------------------------------------------------------------------------
+template <int DIM>
+struct PipeTile {
+  static constexpr int TX = DIM == 3 ? 32 : 128;
+  static constexpr int TY = DIM == 3 ? 4 : 1;
+  static constexpr int HX = TX + 2;
+  static constexpr int HY = DIM == 3 ? TY + 2 : 1;
+  static constexpr int VT = HX * HY;  // V cells per stage
+  static constexpr int NT = TX * TY;  // threads = tile columns
+};
+constexpr int kRV = 5;
+constexpr int kRG = 4;
+
+template <int DIM, int FIRST>
+constexpr size_t pipe_smem_bytes() {
+  using T = PipeTile<DIM>;
+  return sizeof(double) * (256 + kRV * T::VT + kRG * 3 * T::NT + (FIRST ? 0 : kRG * 4 * T::NT));
+}
+
+__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Source of V for local plane zz in [-1, nzl]: state plane, mirror plane at
+// the global boundary (P/src/monodomain.cpp:85-86), or ghost plane.
+__device__ __forceinline__ const double* vplane(const Geom& g, const Halo& h,
+                                                const double* G, int zz) {
+  if (zz >= 0 && zz < g.nzl) return G + g.plane * zz;
+  int gz = zz + g.zoff;
+  gz = gz < 0 ? 1 : (gz >= g.nzg ? g.nzg - 2 : gz);
+  const int lz = gz - g.zoff;
+  if (lz >= 0 && lz < g.nzl) return G + g.plane * lz;
+  return lz < 0 ? h.lo : h.hi;
+}
+
+#ifndef EMRKC_PIPE_MINBLOCKS
+#define EMRKC_PIPE_MINBLOCKS 8
+#endif
+
+template <int DIM, int FIRST, int ION>
+__global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
+    k_node_pipe(const Geom g, const Halo h, const FastArgs a) {
+  using T = PipeTile<DIM>;
+  extern __shared__ double smem[];
+  double* tab = smem;
+  double* vst = smem + 256;                       // [kRV][VT]
+  double* gst = vst + kRV * T::VT;                // [kRG][3][NT]
+  double* g2s = gst + kRG * 3 * T::NT;            // [kRG][4][NT] (!FIRST)
+  const int t = threadIdx.x;
+  {
+    __shared__ int skip;
+    if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+    load_exp_table(tab, t, T::NT);
+    __syncthreads();
+    if (skip) return;
+  }
+  const int tx = t % T::TX, ty = t / T::TX;
+  const int x0 = blockIdx.x * T::TX;
+  const int y0 = DIM == 3 ? blockIdx.y * T::TY : 0;
+  const int zb = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
+  const int ze = min(g.nzl, zb + a.zc);
+  if (zb >= ze) return;  // uniform per block
+  const int cx = x0 + tx, cy = y0 + ty;
+  const bool valid = cx < g.n0 && (DIM == 2 || cy < g.n1);
+  const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
+  const long long nn = g.nn;
+  const double* G = a.g1;
+
+  // ---- plane loader: V tile + halo for zz in [zb-1, ze]; gates (and g2)
+  //      for zz in [zb, ze). Cells past the grid edge load a mirror / any
+  //      valid address; their values are never read.
+  auto load_plane = [&](int zz) {
+    const int sv = (zz - zb + 1) % kRV;
+    const double* vp = vplane(g, h, G, zz);
+    for (int c = t; c < T::VT; c += T::NT) {
+      const int hx = c % T::HX, hy = c / T::HX;
+      int gx = x0 + hx - 1;
+      gx = gx < 0 ? 1 : (gx >= g.n0 ? max(g.n0 - 2, 0) : gx);
+      int gy = 0;
+      if (DIM == 3) {
+        gy = y0 + hy - 1;
+        gy = gy < 0 ? 1 : (gy >= g.n1 ? max(g.n1 - 2, 0) : gy);
+      }
+      cp_async8(vst + sv * T::VT + c, vp + gx + (long long)g.n0 * gy);
+    }
+    if (zz >= zb && zz < ze) {
+      const int sg = (zz - zb) % kRG;
+      const double* gp = G + nn + ip + g.plane * zz;
+      cp_async8(gst + (sg * 3 + 0) * T::NT + t, gp);
+      cp_async8(gst + (sg * 3 + 1) * T::NT + t, gp + nn);
+      cp_async8(gst + (sg * 3 + 2) * T::NT + t, gp + 2 * nn);
+      if (!FIRST) {
+        const double* qp = a.g2 + ip + g.plane * zz;
+        for (int f = 0; f < 4; ++f) cp_async8(g2s + (sg * 4 + f) * T::NT + t, qp + f * nn);
+      }
+    }
+    cp_commit();
+  };
+
+  load_plane(zb - 1);
+  load_plane(zb);
+  load_plane(zb + 1);
+  const bool scol = valid && stim_col_xy<DIM>(g, cx, cy);
+  bool bad = false, guard = false;
+  double glo = 2.0, ghi = -1.0;
+  const int cell = (DIM == 3 ? (ty + 1) * T::HX : 0) + tx + 1;
+  for (int z = zb; z < ze; ++z) {
+    if (z + 2 <= ze) {
+      load_plane(z + 2);
+    } else {
+      cp_commit();  // keep the group count uniform
+    }
+    cp_wait<1>();
+    __syncthreads();
+    const int p = z - zb + 1;
+    const double* V0 = vst + (p % kRV) * T::VT;
+    const double vc = V0[cell];
+    const double vm = vst[((p - 1) % kRV) * T::VT + cell];
+    const double vp = vst[((p + 1) % kRV) * T::VT + cell];
+    double xs = 0.0, ys = 0.0;
+    if (DIM >= 2) xs = V0[cell - 1] + V0[cell + 1];
+    if (DIM == 3) ys = V0[cell - T::HX] + V0[cell + T::HX];
+    const int sg = (z - zb) % kRG;
+    const double z0 = gst[(sg * 3 + 0) * T::NT + t];
+    const double z1 = gst[(sg * 3 + 1) * T::NT + t];
+    const double z2 = gst[(sg * 3 + 2) * T::NT + t];
+    const double stim = (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0;
+    const NodeOut r = node_update_s<DIM, FIRST, ION>(g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2,
+                                                      stim, g2s + sg * 4 * T::NT + t, T::NT);
+    if (valid) {
+      const long long i = ip + g.plane * z;
+      a.out[nn + i] = r.o1;
+      a.out[2 * nn + i] = r.o2;
+      a.out[3 * nn + i] = r.o3;
+      if (ION) {
+        a.u1[i] = r.o0;
+        a.fs[i] = r.fs;
+      } else {
+        a.out[i] = r.o0;
+        guard |= fabs(r.o0) > 1e6;
+      }
+      bad |= !(finite_hi(r.o0) && finite_hi(r.o1) && finite_hi(r.o2) && finite_hi(r.o3));
+      if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
+      if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
+      if (a.last) {
+        glo = fmin(glo, fmin(r.o1, fmin(r.o2, r.o3)));
+        ghi = fmax(ghi, fmax(r.o1, fmax(r.o2, r.o3)));
+      }
+    }
+  }
+  cp_wait<0>();
+  if (bad) {
+    Col<DIM> c;
+    c.c0 = cx;
+    c.c1 = cy;
+    c.ip = ip;
+    c.z0 = zb;
+    c.z1 = ze;
+    c.valid = true;
+    const bool inner = inner_nonfinite<DIM>(g, h, G, c, nbr_of<DIM>(g, c), a.eta);
+    atomicMin(a.event, a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1)) +
+                           (inner ? 1 : a.m + 1));
+  }
+  if (!ION && a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+  if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, valid);
+}
+
+// ---------------------------------------------------------------------------
+// V-only inner stage k >= 2 (LAST: k == m, forms V of g_j).
+// ---------------------------------------------------------------------------
+template <int DIM, int LAST, int FIRST>
+__global__ void __launch_bounds__(kFThreads)
+    k_vin_fast(const Geom g, const Halo h, const FastInnerArgs a) {
+  if (prologue(a.event, nullptr)) return;
+  const Col<DIM> c = col_here<DIM>(g, a.zc);
+  bool bad_in = false, bad_out = false, guard = false;
+  if (c.valid) {
+    const double* __restrict__ U = a.um1;
+    const Nbr<DIM> o = nbr_of<DIM>(g, c);
+    double vm = zval(U, g, c.ip, c.z0 - 1, h.lo, h.hi);
+    double vc = zval(U, g, c.ip, c.z0, h.lo, h.hi);
+    for (int z = c.z0; z < c.z1; ++z) {
+      const double vp = zval(U, g, c.ip, z + 1, h.lo, h.hi);
+      const long long i = c.ip + g.plane * z;
+      const double D = lap_fast<DIM>(g, U, i, o, vm, vc, vp);
+      const double uk = fma(a.mueta, D + __ldg(a.fs + i),
+                            fma(a.nu, vc, a.kappa * __ldg(a.um2 + i)));
+      bad_in |= !finite_hi(uk);
+      double vput = uk;
+      if (!LAST) {
+        a.uk[i] = uk;
+      } else {
+        const double gv = __ldg(a.g1v + i);
+        const double b0 = FIRST ? gv : fma(a.onu, gv, a.okappa * __ldg(a.g2v + i));
+        const double o0 = fma(a.cG, uk - gv, b0);
+        a.outv[i] = o0;
+        bad_out |= !finite_hi(o0);
+        guard |= fabs(o0) > 1e6;
+        vput = o0;
+      }
+      if (z == 0 && h.put_lo) h.put_lo[c.ip] = vput;
+      if (z == g.nzl - 1 && h.put_hi) h.put_hi[c.ip] = vput;
+      vm = vc;
+      vc = vp;
+    }
+  }
+  const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
+  if (bad_in) atomicMin(a.event, base + a.k);
+  if (LAST && bad_out) atomicMin(a.event, base + a.m + 1);
+  if (LAST && a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+}
+
+template <int DIM>
+dim3 fgrid(const Geom& g, int zc) {
+  if (DIM == 3)
+    return dim3((g.n0 + FBX - 1) / FBX, (g.n1 + FBY - 1) / FBY, (g.nzl + zc - 1) / zc);
+  if (DIM == 2) {
+    const int chunks = (g.nzl + zc - 1) / zc;
+    return dim3((g.n0 + FBX - 1) / FBX, (chunks + FBY - 1) / FBY, 1);
+  }
+  return dim3((g.nzl + kFThreads - 1) / kFThreads, 1, 1);
+}
+
+}  // namespace
+
+// Planes per thread: enough columns x chunks to fill ~2 waves of 148 SMs
+// at 2048 threads, capped so the prologue stays amortised.
+int fast_zc(const Geom& g) {
+  if (g.dim == 1) return 1;
+  const long long cols = (g.dim == 3) ? (long long)g.n0 * g.n1 : g.n0;
+  const long long want = 148LL * 2048 * 2;
+  long long zc = (cols * g.nzl) / want;
+  if (zc < 1) zc = 1;
+  if (zc > 32) zc = 32;
+  if (zc > g.nzl) zc = g.nzl;
+  return (int)zc;
+}
+
+#define FDISPATCH(g, ...)                                   \
+  switch ((g).dim) {                                        \
+    case 1: { constexpr int D = 1; __VA_ARGS__; break; }    \
+    case 2: { constexpr int D = 2; __VA_ARGS__; break; }    \
+    default: { constexpr int D = 3; __VA_ARGS__; break; }   \
+  }
+
+cudaError_t launch_node_fast(const Geom& g, const Halo& h, const FastArgs& a,
+                             bool ion, cudaStream_t st) {
+  const dim3 blk(FBX, FBY);
+  const bool first = a.j == 1;
+  FDISPATCH(g, {
+    const dim3 grd = fgrid<D>(g, a.zc);
+    if (ion) {
+      if (first) k_node_fast<D, 1, 1><<<grd, blk, 0, st>>>(g, h, a);
+      else k_node_fast<D, 0, 1><<<grd, blk, 0, st>>>(g, h, a);
+    } else {
+      if (first) k_node_fast<D, 1, 0><<<grd, blk, 0, st>>>(g, h, a);
+      else k_node_fast<D, 0, 0><<<grd, blk, 0, st>>>(g, h, a);
+    }
+  });
+  return cudaGetLastError();
+}
+
+template <int D, int F, int I>
+static cudaError_t launch_pipe_t(const Geom& g, const Halo& h, const FastArgs& a,
+                                 cudaStream_t st) {
+  using T = PipeTile<D>;
+  constexpr size_t smem = pipe_smem_bytes<D, F>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_node_pipe<D, F, I>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  const int chunks = (g.nzl + a.zc - 1) / a.zc;
+  const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)
+                          : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
+  k_node_pipe<D, F, I><<<grd, T::NT, smem, st>>>(g, h, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_node_pipe(const Geom& g, const Halo& h, const FastArgs& a, bool ion,
+                             cudaStream_t st) {
+  const bool first = a.j == 1;
+  if (g.dim == 3) {
+    if (ion) return first ? launch_pipe_t<3, 1, 1>(g, h, a, st) : launch_pipe_t<3, 0, 1>(g, h, a, st);
+    return first ? launch_pipe_t<3, 1, 0>(g, h, a, st) : launch_pipe_t<3, 0, 0>(g, h, a, st);
+  }
+  if (g.dim == 2) {
+    if (ion) return first ? launch_pipe_t<2, 1, 1>(g, h, a, st) : launch_pipe_t<2, 0, 1>(g, h, a, st);
+    return first ? launch_pipe_t<2, 1, 0>(g, h, a, st) : launch_pipe_t<2, 0, 0>(g, h, a, st);
+  }
+  return launch_node_fast(g, h, a, ion, st);
+}
+
+cudaError_t launch_vin_fast(const Geom& g, const Halo& h, const FastInnerArgs& a,
+                            cudaStream_t st) {
+  const dim3 blk(FBX, FBY);
+  const bool last = a.k == a.m;
+  const bool first = a.j == 1;
+  FDISPATCH(g, {
+    const dim3 grd = fgrid<D>(g, a.zc);
+    if (!last) k_vin_fast<D, 0, 0><<<grd, blk, 0, st>>>(g, h, a);
+    else if (first) k_vin_fast<D, 1, 1><<<grd, blk, 0, st>>>(g, h, a);
+    else k_vin_fast<D, 1, 0><<<grd, blk, 0, st>>>(g, h, a);
+  });
+  return cudaGetLastError();
+}
+
+}  // namespace emrkc_k

@@ -24,7 +24,7 @@ SIG_DEF = 0.17 * 0.62 / 0.79
 
 
 def cases():
-    yield "g1d_201_dt0.1", make_problem(1, [201], [0.1], [SIG_DEF], 140.0, 0.01, 50.0, [0.0], [1.5], 0.0, 2.0), 0.1, 100, None, "rest"
+    yield "g1d_201_dt0.05", make_problem(1, [201], [0.1], [SIG_DEF], 140.0, 0.01, 50.0, [0.0], [1.5], 0.0, 2.0), 0.05, 100, None, "rest"
     yield "g2d_24x20", make_problem(2, [24, 20], [0.25, 0.25], [0.1, 0.1], 140.0, 0.01, 70.0, [-0.125, -0.125], [1.875, 1.875], 0.0, 1.0), 0.05, 40, None, "vnoise"
     yield "g3d_12x10x8", make_problem(3, [12, 10, 8], [0.25] * 3, [0.2, 0.1, 0.05], 140.0, 0.01, 70.0, [-0.125] * 3, [0.875] * 3, 0.0, 1.0), 0.05, 30, None, "vnoise"
     yield "g2d_32x24_s3m2", make_problem(2, [32, 24], [0.05, 0.05], [0.2, 0.2], 140.0, 0.01, 70.0, [-0.025, -0.025], [0.375, 0.375], 0.0, 1.0), 0.05, 15, 200.0, "vnoise"

@@ -20,5 +20,5 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   $CMD > gpurun_out/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
   $CMD > gpurun_out/plain2.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:k_stage -s 8 -c 2 -o gpurun_out/prof_${NCU_TAG:-m1} $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+  ncu --set full --clock-control none --import-source on -k regex:'k_node|k_stage|k_vin' -s 8 -c 2 -o gpurun_out/prof_${NCU_TAG:-m1} $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi

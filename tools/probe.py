@@ -8,7 +8,7 @@ from paper_2401_01745_b200 import workloads  # noqa: E402
 from paper_2401_01745_b200.monodomain import MonodomainOperator  # noqa: E402
 
 names = sys.argv[1:] or ["hh3d_128x128x128", "hh3d_512x512x256"]
-for fast in ("1", "0"):
+for fast in (("1",) if os.environ.get("EMRKC_PROBE_FAST_ONLY") else ("1", "0")):
     os.environ["EMRKC_FAST"] = fast
     for name in names:
         w = workloads.get(name)
