@@ -237,7 +237,7 @@ struct emrkc_handle {
   // m >= 2 scratch
   double* fs = nullptr;
   double* ye = nullptr;
-  double* u[3] = {nullptr, nullptr, nullptr};
+  double* u[4] = {nullptr, nullptr, nullptr, nullptr};
   // ghost planes [side: 0 below, 1 above][slot]
   double* ghost[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   emrkc_handle* nbr[2] = {nullptr, nullptr};  // in-process neighbours
@@ -299,7 +299,7 @@ int ensure_inner(emrkc_handle* h) {
   if (h->fs) return EMRKC_OK;
   CK(h, cudaMalloc(&h->fs, sizeof(double) * h->nn));
   CK(h, cudaMalloc(&h->ye, sizeof(double) * 3 * h->nn));
-  for (int k = 0; k < 3; ++k) CK(h, cudaMalloc(&h->u[k], sizeof(double) * h->nn));
+  for (int k = 0; k < 4; ++k) CK(h, cudaMalloc(&h->u[k], sizeof(double) * h->nn));
   return EMRKC_OK;
 }
 
@@ -419,7 +419,7 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.g2 = a.g2;
       f.out = a.out;
       f.fs = h->fs;
-      f.u1 = h->u[0];
+      f.u1 = h->u[3];
       f.eta = pl.eta;
       f.stim = a.stim;
       f.cG = cG;
@@ -427,6 +427,8 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.mue1 = pl.in_mueta[1];
       f.nu = a.nu;
       f.kappa = a.kappa;
+      // fast ionic path only where its range analysis holds (fast_math.cuh)
+      f.vfast = pl.eta <= 1.5 ? 150.0 : -1.0;
       f.j = j;
       f.m = pl.m;
       f.s = pl.s;
@@ -441,10 +443,14 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         CK(h, emrkc_k::launch_node_fast(h->geom, hl, f, pl.m >= 2, h->stream));
     } else {
       emrkc_k::FastInnerArgs f{};
-      f.um1 = h->u[(k - 2) % 3];
-      f.um2 = (k == 2) ? a.g1 : h->u[(k - 3) % 3];
-      f.fs = h->fs;
-      f.uk = h->u[(k - 1) % 3];
+      // increment form: d_1 stays in u[3] (it also gives a = d_1/(mu'_1 eta)),
+      // d_k (k >= 2) rotates through u[0..2]
+      auto dbuf = [&](int kk) { return kk == 1 ? h->u[3] : h->u[(kk - 2) % 3]; };
+      f.um1 = dbuf(k - 1);
+      f.um2 = (k == 2) ? nullptr : dbuf(k - 2);
+      f.d1 = h->u[3];
+      f.inv_mue1 = 1.0 / pl.in_mueta[1];
+      f.uk = dbuf(k);
       f.g1v = a.g1;
       f.g2v = a.g2;
       f.outv = a.out;

@@ -32,7 +32,13 @@ __constant__ FastConsts kFC = {
     kL2E256, kLn2_256_hi, kLn2_256_lo, 1.0 / 24.0, 1.0 / 6.0, 1.0 / 12.0,
     0.1, 0.1, 0.01, 0.07, 0.125, 1.0 / 18.0, 0.0125, 1.6487212707001282,
     0.22313016014842982, 1.2, 0.36, 0.003, -54.387};
-constexpr double kFastVmax = 500.0;            // hh_expeuler_fast validity (mV)
+// hh_expeuler_fast validity: |V| <= kFastVmax and eta <= kFastEtaMax. There
+// max(alpha + beta) ~ 450/ms (beta_m at V = -150 mV), so |eta Lambda| <= 700
+// and every exp_tab_nc argument stays in range; the batch product stays
+// < 1e140. Other nodes take the reference-order path (hh_expeuler_ref),
+// which also catches non-finite V.
+constexpr double kFastVmax = 150.0;
+constexpr double kFastEtaMax = 1.5;
 
 __device__ __forceinline__ double exp_tab(double x, const double* __restrict__ tab) {
   const int hi = __double2hiint(x);
@@ -88,11 +94,7 @@ __device__ __forceinline__ void load_exp_table(double* sh, int tid, int nthreads
 }
 
 // ---------------------------------------------------------------------------
-// Valid for |V| <= kFastVmax = 500 mV (callers branch to the reference-order
-// path otherwise, which also catches NaN): the rate arguments then stay
-// within |x| <= 55, the batch product below stays < 1e140, and the
-// eta*Lambda arguments are clamped at -700 (exp(-700) ~ 1e-304, so
-// expm1 = -1 exactly as for any smaller argument).
+// Valid for |V| <= kFastVmax, eta <= kFastEtaMax (see above).
 //
 // Exponential Euler of the three HH gates at one node, with the rates
 // evaluated through shared exponentials (hh.cuh, hh_gate_coeffs_fast) and
@@ -140,23 +142,22 @@ __device__ __forceinline__ void hh_expeuler_fast(double V, double z0, double z1,
   const double pm = fma(bm, dm, nm);   // (alpha_m + beta_m) dm
   const double pn = fma(bn, dn, nn);   // (alpha_n + beta_n) dn
   const double ph = ahdh + 1.0;        // (alpha_h + beta_h) dh
-  // one reciprocal for dm, dn, dh, pm, pn, ph (Montgomery batch inversion)
-  const double q1 = dm * dn;
-  const double q2 = q1 * dh;
-  const double q3 = q2 * pm;
-  const double q4 = q3 * pn;
-  double r = rcp_fast(q4 * ph);
-  const double iph = r * q4;  r *= ph;
-  const double ipn = r * q3;  r *= pn;
-  const double ipm = r * q2;  r *= pm;
-  const double idh = r * q1;  r *= dh;
-  const double idn = r * dm;
-  const double idm = r * dn;
+  // one reciprocal for dm, dn, dh, pm, pn, ph (batch inversion as a
+  // depth-3 tree: short dependency chain, 15 multiplies)
+  const double A = dm * dn, B = dh * pm, C = pn * ph;
+  const double AB = A * B;
+  const double r = rcp_fast(AB * C);
+  const double iAB = r * C, iC = r * AB;
+  const double iA = iAB * B, iB = iAB * A;
+  const double idm = iA * dn, idn = iA * dm;
+  const double idh = iB * pm, ipm = iB * dh;
+  const double ipn = iC * ph, iph = iC * pn;
   const double me = -eta;
-  // eta*Lambda_g = -eta (alpha+beta) = -eta p/d ; z_inf = numerator / p
-  const double em = exp_tab_nc(fmax(me * (pm * idm), -700.0), tab) - 1.0;
-  const double eh = exp_tab_nc(fmax(me * (ph * idh), -700.0), tab) - 1.0;
-  const double en = exp_tab_nc(fmax(me * (pn * idn), -700.0), tab) - 1.0;
+  // eta*Lambda_g = -eta (alpha+beta) = -eta p/d >= -700 for |V| <= kFastVmax
+  // and eta <= kFastEtaMax (host-checked), so exp_tab_nc needs no clamp.
+  const double em = exp_tab_nc(me * (pm * idm), tab) - 1.0;
+  const double eh = exp_tab_nc(me * (ph * idh), tab) - 1.0;
+  const double en = exp_tab_nc(me * (pn * idn), tab) - 1.0;
   d0 = em * (z0 - nm * ipm);
   d1 = eh * (z1 - ahdh * iph);
   d2 = en * (z2 - nn * ipn);

@@ -60,25 +60,31 @@ struct FastArgs {
   const double* g1;   // g_{j-1}
   const double* g2;   // g_{j-2} (j >= 2)
   double* out;        // g_j (m == 1: all blocks; m >= 2: gate blocks)
-  double* fs;         // m >= 2: frozen slow V term
-  double* u1;         // m >= 2: inner stage 1 of V
+  double* fs;         // unused (kept for layout stability)
+  double* u1;         // m >= 2: d_1 = u_1 - V (increment form, see FastInnerArgs)
   double eta;
   double stim;        // stimulus rate at the stage time (0 if inactive)
   double cG;          // mu_j dt / eta   (gate rows: g_j = base + cG (y_E - z))
   double cV;          // cG * mu'_1 eta  (m == 1: V of g_j = base + cV (f_F + f_S))
   double mue1;        // mu'_1 eta       (m >= 2: u_1 = V + mue1 (f_F + f_S))
   double nu, kappa;   // outer nu_j, kappa_j (j >= 2)
+  double vfast;       // |V| bound of the fast ionic path (0: never)
   int j, m, s, last, zc;
   unsigned long long code_base;
   unsigned long long* event;
   unsigned long long* gate_slot;
 };
 
+// Inner stages in increment form: d_k = u_k - V (V = y_E's V block), so
+// d_k = nu' d_{k-1} + kappa' d_{k-2} + mu'_k eta (a + f_F(d_{k-1})) with
+// a = (f_F + f_S)(y_E) = d_1 / (mu'_1 eta) and d_0 = 0 (f_F is linear and
+// nu' + kappa' = 1). Stage 1 stores only d_1; no fs field is needed.
 struct FastInnerArgs {
-  const double* um1;  // u_{k-1} (stencil field)
-  const double* um2;  // u_{k-2} (V block of g_{j-1} when k == 2)
-  const double* fs;
-  double* uk;         // k < m
+  const double* um1;  // d_{k-1} (stencil field)
+  const double* um2;  // d_{k-2} (null when k == 2: d_0 = 0)
+  const double* d1;   // d_1 (gives a)
+  double inv_mue1;    // 1 / (mu'_1 eta)
+  double* uk;         // k < m: d_k
   const double* g1v;  // k == m: V of g_{j-1}, g_{j-2}
   const double* g2v;
   double* outv;       // k == m: V block of g_j

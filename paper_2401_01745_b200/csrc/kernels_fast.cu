@@ -207,7 +207,7 @@ __device__ __forceinline__ NodeOut node_update(const Geom& g, const FastArgs& a,
   if (DIM >= 2) D = fma(g.w[0], xs, D);
   if (DIM == 3) D = fma(g.w[1], ys, D);
   double d0, d1, d2;
-  if (fabs(vc) <= kFastVmax) {
+  if (fabs(vc) <= a.vfast) {
     hh_expeuler_fast(vc, z0, z1, z2, a.eta, tab, d0, d1, d2);
   } else {
     const Dgate dd = hh_expeuler_ref(vc, z0, z1, z2, a.eta);
@@ -228,7 +228,7 @@ __device__ __forceinline__ NodeOut node_update(const Geom& g, const FastArgs& a,
   r.o1 = fma(a.cG, d0, b1);
   r.o2 = fma(a.cG, d1, b2);
   r.o3 = fma(a.cG, d2, b3);
-  r.o0 = ION ? fma(a.mue1, fsum, vc) : fma(a.cV, fsum, b0);
+  r.o0 = ION ? a.mue1 * fsum : fma(a.cV, fsum, b0);
   r.fs = fs;
   return r;
 }
@@ -243,7 +243,7 @@ __device__ __forceinline__ NodeOut node_update_s(const Geom& g, const FastArgs& 
   if (DIM >= 2) D = fma(g.w[0], xs, D);
   if (DIM == 3) D = fma(g.w[1], ys, D);
   double d0, d1, d2;
-  if (fabs(vc) <= kFastVmax) {
+  if (fabs(vc) <= a.vfast) {
     hh_expeuler_fast(vc, z0, z1, z2, a.eta, tab, d0, d1, d2);
   } else {
     const Dgate dd = hh_expeuler_ref(vc, z0, z1, z2, a.eta);
@@ -264,7 +264,7 @@ __device__ __forceinline__ NodeOut node_update_s(const Geom& g, const FastArgs& 
   r.o1 = fma(a.cG, d0, b1);
   r.o2 = fma(a.cG, d1, b2);
   r.o3 = fma(a.cG, d2, b3);
-  r.o0 = ION ? fma(a.mue1, fsum, vc) : fma(a.cV, fsum, b0);
+  r.o0 = ION ? a.mue1 * fsum : fma(a.cV, fsum, b0);
   r.fs = fs;
   return r;
 }
@@ -323,7 +323,6 @@ __global__ void __launch_bounds__(kFThreads, EMRKC_NODE_MINBLOCKS)
     double* po = a.out + i0;             // g_j
     const double* q2 = FIRST ? nullptr : a.g2 + i0;
     double* pu = ION ? a.u1 + i0 : nullptr;
-    double* pf = ION ? a.fs + i0 : nullptr;
     double vm = zval(G, g, c.ip, c.z0 - 1, h.lo, h.hi);
     double vc = __ldg(pv);
 #pragma unroll kNodeUnroll
@@ -341,10 +340,8 @@ __global__ void __launch_bounds__(kFThreads, EMRKC_NODE_MINBLOCKS)
       po[2 * nn] = r.o2;
       po[3 * nn] = r.o3;
       if (ION) {
-        *pu = r.o0;
-        *pf = r.fs;
+        *pu = r.o0;  // d_1
         pu += plane;
-        pf += plane;
       } else {
         *po = r.o0;
         guard |= fabs(r.o0) > 1e6;
@@ -393,7 +390,7 @@ struct PipeTile {
   static constexpr int VT = HX * HY;  // V cells per stage
   static constexpr int NT = TX * TY;  // threads = tile columns
 };
-constexpr int kRV = 5;
+constexpr int kRV = 8;  // power of two >= 5
 constexpr int kRG = 4;
 
 template <int DIM, int FIRST>
@@ -402,9 +399,8 @@ constexpr size_t pipe_smem_bytes() {
   return sizeof(double) * (256 + kRV * T::VT + kRG * 3 * T::NT + (FIRST ? 0 : kRG * 4 * T::NT));
 }
 
-__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+__device__ __forceinline__ void cp_async8(unsigned sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sdst), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -424,8 +420,24 @@ __device__ __forceinline__ const double* vplane(const Geom& g, const Halo& h,
   return lz < 0 ? h.lo : h.hi;
 }
 
+// In-plane offset of halo cell c of a tile (mirror at the grid edge; cells
+// past the far edge clamp to a valid node, their values are never read).
+template <int DIM>
+__device__ __forceinline__ long long halo_offset(const Geom& g, int x0, int y0, int c) {
+  using T = PipeTile<DIM>;
+  const int hx = c % T::HX, hy = c / T::HX;
+  int gx = x0 + hx - 1;
+  gx = gx < 0 ? 1 : (gx >= g.n0 ? max(g.n0 - 2, 0) : gx);
+  int gy = 0;
+  if (DIM == 3) {
+    gy = y0 + hy - 1;
+    gy = gy < 0 ? 1 : (gy >= g.n1 ? max(g.n1 - 2, 0) : gy);
+  }
+  return gx + (long long)g.n0 * gy;
+}
+
 #ifndef EMRKC_PIPE_MINBLOCKS
-#define EMRKC_PIPE_MINBLOCKS 8
+#define EMRKC_PIPE_MINBLOCKS 5
 #endif
 
 template <int DIM, int FIRST, int ION>
@@ -438,51 +450,54 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   double* gst = vst + kRV * T::VT;                // [kRG][3][NT]
   double* g2s = gst + kRG * 3 * T::NT;            // [kRG][4][NT] (!FIRST)
   const int t = threadIdx.x;
+  // abort word: uniform per block after the first barrier of the z loop
+  __shared__ int skip;
+  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
   {
-    __shared__ int skip;
-    if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
-    load_exp_table(tab, t, T::NT);
-    __syncthreads();
-    if (skip) return;
+    // exp table rides in the first cp.async group with the first planes
+    const unsigned st = (unsigned)__cvta_generic_to_shared(tab);
+    for (int j = t; j < 256; j += T::NT) cp_async8(st + 8u * j, kExp2Tab256 + j);
   }
   const int tx = t % T::TX, ty = t / T::TX;
   const int x0 = blockIdx.x * T::TX;
   const int y0 = DIM == 3 ? blockIdx.y * T::TY : 0;
   const int zb = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
   const int ze = min(g.nzl, zb + a.zc);
-  if (zb >= ze) return;  // uniform per block
   const int cx = x0 + tx, cy = y0 + ty;
   const bool valid = cx < g.n0 && (DIM == 2 || cy < g.n1);
   const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
-  const long long nn = g.nn;
+  const long long nn = g.nn, plane = g.plane;
   const double* G = a.g1;
+  // per-thread copy plan: halo cells t and t + NT of every V stage, and the
+  // thread's own column for the gates (and g_{j-2})
+  const long long voff0 = halo_offset<DIM>(g, x0, y0, t);
+  const bool has1 = t + T::NT < T::VT;
+  const long long voff1 = has1 ? halo_offset<DIM>(g, x0, y0, t + T::NT) : 0;
+  const unsigned sv0 = (unsigned)__cvta_generic_to_shared(vst) + 8u * t;
+  const unsigned sg0 = (unsigned)__cvta_generic_to_shared(gst) + 8u * t;
+  const unsigned sq0 = (unsigned)__cvta_generic_to_shared(g2s) + 8u * t;
+  const double* gcol = G + nn + ip;
+  const double* qcol = FIRST ? nullptr : a.g2 + ip;
 
-  // ---- plane loader: V tile + halo for zz in [zb-1, ze]; gates (and g2)
-  //      for zz in [zb, ze). Cells past the grid edge load a mirror / any
-  //      valid address; their values are never read.
   auto load_plane = [&](int zz) {
-    const int sv = (zz - zb + 1) % kRV;
+    const unsigned sv = sv0 + 8u * T::VT * ((zz - zb + 1) & (kRV - 1));
     const double* vp = vplane(g, h, G, zz);
-    for (int c = t; c < T::VT; c += T::NT) {
-      const int hx = c % T::HX, hy = c / T::HX;
-      int gx = x0 + hx - 1;
-      gx = gx < 0 ? 1 : (gx >= g.n0 ? max(g.n0 - 2, 0) : gx);
-      int gy = 0;
-      if (DIM == 3) {
-        gy = y0 + hy - 1;
-        gy = gy < 0 ? 1 : (gy >= g.n1 ? max(g.n1 - 2, 0) : gy);
-      }
-      cp_async8(vst + sv * T::VT + c, vp + gx + (long long)g.n0 * gy);
-    }
+    cp_async8(sv, vp + voff0);
+    if (has1) cp_async8(sv + 8u * T::NT, vp + voff1);
     if (zz >= zb && zz < ze) {
-      const int sg = (zz - zb) % kRG;
-      const double* gp = G + nn + ip + g.plane * zz;
-      cp_async8(gst + (sg * 3 + 0) * T::NT + t, gp);
-      cp_async8(gst + (sg * 3 + 1) * T::NT + t, gp + nn);
-      cp_async8(gst + (sg * 3 + 2) * T::NT + t, gp + 2 * nn);
+      const unsigned s = (unsigned)((zz - zb) & (kRG - 1));
+      const unsigned sg = sg0 + 8u * 3 * T::NT * s;
+      const double* gp = gcol + plane * zz;
+      cp_async8(sg, gp);
+      cp_async8(sg + 8u * T::NT, gp + nn);
+      cp_async8(sg + 16u * T::NT, gp + 2 * nn);
       if (!FIRST) {
-        const double* qp = a.g2 + ip + g.plane * zz;
-        for (int f = 0; f < 4; ++f) cp_async8(g2s + (sg * 4 + f) * T::NT + t, qp + f * nn);
+        const unsigned sq = sq0 + 8u * 4 * T::NT * s;
+        const double* qp = qcol + plane * zz;
+        cp_async8(sq, qp);
+        cp_async8(sq + 8u * T::NT, qp + nn);
+        cp_async8(sq + 16u * T::NT, qp + 2 * nn);
+        cp_async8(sq + 24u * T::NT, qp + 3 * nn);
       }
     }
     cp_commit();
@@ -495,6 +510,8 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   bool bad = false, guard = false;
   double glo = 2.0, ghi = -1.0;
   const int cell = (DIM == 3 ? (ty + 1) * T::HX : 0) + tx + 1;
+  double* po = a.out + ip + plane * zb;
+  double* pu = ION ? a.u1 + ip + plane * zb : nullptr;
   for (int z = zb; z < ze; ++z) {
     if (z + 2 <= ze) {
       load_plane(z + 2);
@@ -503,43 +520,49 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     }
     cp_wait<1>();
     __syncthreads();
+    if (skip) break;  // uniform: an earlier step aborted
     const int p = z - zb + 1;
-    const double* V0 = vst + (p % kRV) * T::VT;
+    const double* V0 = vst + (p & (kRV - 1)) * T::VT;
     const double vc = V0[cell];
-    const double vm = vst[((p - 1) % kRV) * T::VT + cell];
-    const double vp = vst[((p + 1) % kRV) * T::VT + cell];
+    const double vm = vst[((p - 1) & (kRV - 1)) * T::VT + cell];
+    const double vp = vst[((p + 1) & (kRV - 1)) * T::VT + cell];
     double xs = 0.0, ys = 0.0;
     if (DIM >= 2) xs = V0[cell - 1] + V0[cell + 1];
     if (DIM == 3) ys = V0[cell - T::HX] + V0[cell + T::HX];
-    const int sg = (z - zb) % kRG;
-    const double z0 = gst[(sg * 3 + 0) * T::NT + t];
-    const double z1 = gst[(sg * 3 + 1) * T::NT + t];
-    const double z2 = gst[(sg * 3 + 2) * T::NT + t];
+    const double* G0 = gst + ((z - zb) & (kRG - 1)) * 3 * T::NT + t;
+    const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
     const double stim = (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0;
-    const NodeOut r = node_update_s<DIM, FIRST, ION>(g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2,
-                                                      stim, g2s + sg * 4 * T::NT + t, T::NT);
+    const NodeOut r = node_update_s<DIM, FIRST, ION>(
+        g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, stim,
+        g2s + ((z - zb) & (kRG - 1)) * 4 * T::NT + t, T::NT);
     if (valid) {
-      const long long i = ip + g.plane * z;
-      a.out[nn + i] = r.o1;
-      a.out[2 * nn + i] = r.o2;
-      a.out[3 * nn + i] = r.o3;
+      po[nn] = r.o1;
+      po[2 * nn] = r.o2;
+      po[3 * nn] = r.o3;
       if (ION) {
-        a.u1[i] = r.o0;
-        a.fs[i] = r.fs;
+        *pu = r.o0;  // d_1
       } else {
-        a.out[i] = r.o0;
+        *po = r.o0;
         guard |= fabs(r.o0) > 1e6;
       }
-      bad |= !(finite_hi(r.o0) && finite_hi(r.o1) && finite_hi(r.o2) && finite_hi(r.o3));
+      // one finiteness test per node: a non-finite output poisons the sum
+      bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
       if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
       if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
-      if (a.last) {
-        glo = fmin(glo, fmin(r.o1, fmin(r.o2, r.o3)));
-        ghi = fmax(ghi, fmax(r.o1, fmax(r.o2, r.o3)));
+      if (a.last) {  // gates of an accepted step are finite: plain compares
+        const double mn = r.o1 < r.o2 ? r.o1 : r.o2;
+        const double mx = r.o1 < r.o2 ? r.o2 : r.o1;
+        glo = mn < glo ? mn : glo;
+        ghi = mx > ghi ? mx : ghi;
+        glo = r.o3 < glo ? r.o3 : glo;
+        ghi = r.o3 > ghi ? r.o3 : ghi;
       }
     }
+    po += plane;
+    if (ION) pu += plane;
   }
   cp_wait<0>();
+  if (skip) return;
   if (bad) {
     Col<DIM> c;
     c.c0 = cx;
@@ -554,7 +577,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   }
   if (!ION && a.last && guard)
     atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
-  if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, valid);
+  if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, valid && ze > zb);
 }
 
 // ---------------------------------------------------------------------------
@@ -575,16 +598,17 @@ __global__ void __launch_bounds__(kFThreads)
       const double vp = zval(U, g, c.ip, z + 1, h.lo, h.hi);
       const long long i = c.ip + g.plane * z;
       const double D = lap_fast<DIM>(g, U, i, o, vm, vc, vp);
-      const double uk = fma(a.mueta, D + __ldg(a.fs + i),
-                            fma(a.nu, vc, a.kappa * __ldg(a.um2 + i)));
-      bad_in |= !finite_hi(uk);
-      double vput = uk;
+      const double d1 = __ldg(a.d1 + i);
+      const double base = a.um2 ? fma(a.nu, vc, a.kappa * __ldg(a.um2 + i)) : a.nu * vc;
+      const double dk = fma(a.mueta, fma(d1, a.inv_mue1, D), base);
+      bad_in |= !finite_hi(dk);
+      double vput = dk;
       if (!LAST) {
-        a.uk[i] = uk;
+        a.uk[i] = dk;
       } else {
         const double gv = __ldg(a.g1v + i);
         const double b0 = FIRST ? gv : fma(a.onu, gv, a.okappa * __ldg(a.g2v + i));
-        const double o0 = fma(a.cG, uk - gv, b0);
+        const double o0 = fma(a.cG, dk, b0);
         a.outv[i] = o0;
         bad_out |= !finite_hi(o0);
         guard |= fabs(o0) > 1e6;
@@ -616,17 +640,16 @@ dim3 fgrid(const Geom& g, int zc) {
 
 }  // namespace
 
-// Planes per thread: enough columns x chunks to fill ~2 waves of 148 SMs
-// at 2048 threads, capped so the prologue stays amortised.
+// Planes per block (z-chunk length): 16 amortises the block prologue (abort
+// word, exp table, the cp.async pipeline fill); halved while the grid would
+// give fewer than ~2 waves of 148 SMs x 5 resident blocks.
 int fast_zc(const Geom& g) {
   if (g.dim == 1) return 1;
-  const long long cols = (g.dim == 3) ? (long long)g.n0 * g.n1 : g.n0;
-  const long long want = 148LL * 2048 * 2;
-  long long zc = (cols * g.nzl) / want;
-  if (zc < 1) zc = 1;
-  if (zc > 32) zc = 32;
-  if (zc > g.nzl) zc = g.nzl;
-  return (int)zc;
+  const long long tiles = (g.dim == 3) ? ((g.n0 + 31) / 32) * (long long)((g.n1 + 3) / 4)
+                                       : (g.n0 + 127) / 128;
+  int zc = 16;
+  while (zc > 4 && tiles * ((g.nzl + zc - 1) / zc) < 148LL * 5 * 2) zc /= 2;
+  return zc > g.nzl ? g.nzl : zc;
 }
 
 #define FDISPATCH(g, ...)                                   \
