@@ -119,6 +119,8 @@ typedef struct emrkc_run_result {
   int32_t m;
   double eta;
   double device_ms;     /* CUDA-event time of the stepping loop         */
+  int32_t abort_outer_stage; /* outer stage j of a non-finite abort     */
+  int32_t reserved;
 } emrkc_run_result;
 
 /* RhoEstimate (P/include/mrkc/spectral.hpp:10-16). */
@@ -263,11 +265,32 @@ int emrkc_ipc_export(emrkc_handle* h, void* blob, int64_t len);
 int emrkc_ipc_import(emrkc_handle* h, int32_t side, const void* blob,
                      int64_t len);
 /* Local part of a distributed run: like emrkc_run, but the halo planes go
- * to the imported neighbours; the caller reduces the returned per-rank
- * result (max of abort flags/steps, min/max of gate range). */
+ * to the imported neighbours (peer stores from the producing kernel; the
+ * neighbour's consuming blocks wait on a system-scope arrival counter, so
+ * interior blocks never wait). Ranks do not fold abort words: the caller
+ * reduces the per-rank results (first abort over ranks, min/max of gate
+ * range) and, if a rank aborted, every rank calls emrkc_dist_replay for the
+ * steps before the first abort (+1 for a norm-guard trip) to land on the
+ * reference's final state. Needs the fast kernels. */
 int emrkc_dist_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
                    double epsilon, int32_t variant, double rho_F,
                    double rho_S, emrkc_run_result* res);
+/* Restores the state the last emrkc_dist_run started from and runs nsteps
+ * (collective: all ranks call it with the same arguments). */
+int emrkc_dist_replay(emrkc_handle* h, int64_t step0, int64_t nsteps,
+                      double dt, double epsilon, int32_t variant,
+                      double rho_F, double rho_S, emrkc_run_result* res);
+
+/* Testing aid for the distributed protocol on one process / one GPU:
+ * link two adjacent slab handles directly (no IPC), then run all slabs with
+ * every launch serialised (each device-side wait is satisfied when its
+ * kernel starts, so no kernel ever waits on a concurrent one). replay != 0
+ * restores the checkpoints first (emrkc_dist_replay semantics). */
+int emrkc_dist_link_local(emrkc_handle* lower, emrkc_handle* upper);
+int emrkc_dist_lockstep_run(emrkc_handle* const* hs, int32_t n, int32_t replay,
+                            int64_t step0, int64_t nsteps, double dt,
+                            double epsilon, int32_t variant, double rho_F,
+                            double rho_S, emrkc_run_result* res);
 
 #ifdef __cplusplus
 }  /* extern "C" */

@@ -772,6 +772,7 @@ int oc_run(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
       res->abort_step = step;
       res->abort_stage = rep.abort_stage;
       res->abort_inner = rep.abort_inner;
+      res->abort_outer_stage = rep.abort_outer_stage;
       rc = 0;
       break;
     }

@@ -137,6 +137,8 @@ class RunResult(C.Structure):
         ("m", C.c_int32),
         ("eta", C.c_double),
         ("device_ms", C.c_double),
+        ("abort_outer_stage", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -198,6 +200,9 @@ PROTOTYPES = {
     "emrkc_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
     "emrkc_ipc_import": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]),
     "emrkc_dist_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
+    "emrkc_dist_replay": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
+    "emrkc_dist_link_local": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "emrkc_dist_lockstep_run": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
 }
 
 _lib = None

@@ -238,9 +238,23 @@ struct emrkc_handle {
   double* fs = nullptr;
   double* ye = nullptr;
   double* u[4] = {nullptr, nullptr, nullptr, nullptr};
-  // ghost planes [side: 0 below, 1 above][slot]
+  // ghost planes [side: 0 below, 1 above][slot], carved from one arena that
+  // also holds the arrival counters of the cross-process protocol
   double* ghost[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  unsigned long long* cnt = nullptr;         // [2]: arrivals into ghost[0] / ghost[1]
   emrkc_handle* nbr[2] = {nullptr, nullptr};  // in-process neighbours
+  // cross-process (or in-process lockstep) neighbours: their arena pointers
+  struct {
+    bool linked = false;
+    bool ipc = false;           // opened with cudaIpcOpenMemHandle
+    void* arena = nullptr;
+    double* ghost[2] = {nullptr, nullptr};  // their ghost[1-side][slot]
+    unsigned long long* cnt = nullptr;      // their cnt[1-side]
+  } peer[2];
+  unsigned long long recv[2] = {0, 0};  // arrivals expected so far per side
+  double* ckpt = nullptr;               // dist_run input state, for replay
   long long level = 0;
   // device scalars
   unsigned long long* d_event = nullptr;
@@ -354,7 +368,34 @@ Halo halo_at(const emrkc_handle* h, long long L) {
     x.hi = h->ghost[1][rs];
     x.put_hi = h->nbr[1]->ghost[0][ws];
   }
+  // distributed: neighbours' ghosts + arrival counters (device-side sync)
+  for (int s = 0; s < 2; ++s) {
+    if (!h->peer[s].linked) continue;
+    if (s == 0) {
+      x.lo = h->ghost[0][rs];
+      x.put_lo = h->peer[0].ghost[ws];
+      x.sig_lo = h->peer[0].cnt;
+      x.wait_lo = h->cnt;
+      x.expect_lo = h->recv[0];
+    } else {
+      x.hi = h->ghost[1][rs];
+      x.put_hi = h->peer[1].ghost[ws];
+      x.sig_hi = h->peer[1].cnt;
+      x.wait_hi = h->cnt + 1;
+      x.expect_hi = h->recv[1];
+    }
+    x.timeout_flag = h->d_event;
+  }
   return x;
+}
+
+bool dist_linked(const emrkc_handle* h) { return h->peer[0].linked || h->peer[1].linked; }
+
+// After a level: the neighbours ran the same kernel family on the same x-y
+// geometry, so each sends the same number of arrivals.
+void dist_account(emrkc_handle* h, long long signals) {
+  for (int s = 0; s < 2; ++s)
+    if (h->peer[s].linked) h->recv[s] += static_cast<unsigned long long>(signals);
 }
 
 // One step of the plan, launched level by level (a level = one stencil
@@ -470,6 +511,11 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.event = a.event;
       CK(h, emrkc_k::launch_vin_fast(h->geom, hl, f, h->stream));
     }
+    if (dist_linked(h)) {
+      const bool pipe_family = (k == 1) && h->pipe && h->geom.dim >= 2;
+      dist_account(h, pipe_family ? emrkc_k::halo_signals_pipe(h->geom)
+                                  : emrkc_k::halo_signals_march(h->geom));
+    }
   } else if (pl.m == 1) {
     CK(h, emrkc_k::launch_stage_m1(h->geom, hl, a, 0, h->stream));
   } else if (k == 1) {
@@ -507,7 +553,7 @@ struct Decoded {
 
 Decoded decode_event(unsigned long long ev, const Plan& pl) {
   Decoded d;
-  if (ev == kNoEvent) return d;
+  if (ev == kNoEvent || ev == 0) return d;  // 0: protocol timeout (checked by callers)
   const unsigned long long stride =
       static_cast<unsigned long long>(pl.s) * (pl.m + 1) + 2;
   d.none = false;
@@ -548,11 +594,13 @@ int init_handle(emrkc_handle* h) {
   CK(h, cudaEventCreate(&h->ev1));
   if (h->partitioned) {
     const size_t pl = static_cast<size_t>(h->geom.plane);
+    h->arena_bytes = sizeof(double) * 4 * pl + 256;
+    CK(h, cudaMalloc(&h->arena, h->arena_bytes));
+    CK(h, cudaMemset(h->arena, 0, h->arena_bytes));
+    double* base = static_cast<double*>(h->arena);
     for (int s = 0; s < 2; ++s)
-      for (int k = 0; k < 2; ++k) {
-        CK(h, cudaMalloc(&h->ghost[s][k], sizeof(double) * pl));
-        CK(h, cudaMemset(h->ghost[s][k], 0, sizeof(double) * pl));
-      }
+      for (int k = 0; k < 2; ++k) h->ghost[s][k] = base + (2 * s + k) * pl;
+    h->cnt = reinterpret_cast<unsigned long long*>(base + 4 * pl);
   }
   const char* f = std::getenv("EMRKC_FAST");
   h->fast = f ? std::atoi(f) : 1;
@@ -773,9 +821,10 @@ void emrkc_destroy(emrkc_handle* h) {
   if (h->ye) cudaFree(h->ye);
   for (auto& u : h->u)
     if (u) cudaFree(u);
-  for (auto& s : h->ghost)
-    for (auto& k : s)
-      if (k) cudaFree(k);
+  for (auto& pe : h->peer)
+    if (pe.ipc && pe.arena) cudaIpcCloseMemHandle(pe.arena);
+  if (h->arena) cudaFree(h->arena);
+  if (h->ckpt) cudaFree(h->ckpt);
   if (h->d_event) cudaFree(h->d_event);
   if (h->d_slots) cudaFree(h->d_slots);
   if (h->d_coef) cudaFree(h->d_coef);
@@ -1102,9 +1151,19 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
               int64_t nsteps, double dt, double eps, double rho_F,
               double rho_S, emrkc_run_result* res, bool single_step,
               emrkc_step_report* rep, int64_t flush_bytes = 0,
-              double* launch_ms = nullptr, int64_t launch_ms_len = 0) {
+              double* launch_ms = nullptr, int64_t launch_ms_len = 0,
+              bool lockstep = false) {
   const size_t n = hs.size();
   int rc;
+  const bool dist = dist_linked(hs[0]);
+  if (dist)
+    for (auto* h : hs) {
+      if (!h->fast)
+        return set_err(h, EMRKC_EINVAL, "distributed runs need the fast kernels (EMRKC_FAST=1)");
+      if ((h->z_begin > 0 && !h->peer[0].linked) ||
+          (h->z_end < h->p.n[h->p.dim - 1] && !h->peer[1].linked))
+        return set_err(h, EMRKC_ESTATE, "dist_run: neighbour not imported");
+    }
   for (auto* h : hs) {
     if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
     if ((rc = use_device(h))) return rc;
@@ -1139,8 +1198,36 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
       slots[r] = {hs[r]->ghost[0][L0 & 1], hs[r]->ghost[1][L0 & 1]};
       dst[r] = slots[r].data();
     }
-    if ((rc = exchange_planes(hs, f, dst))) return rc;
-    for (auto* h : hs) CK(h, cudaDeviceSynchronize());
+    if (!dist) {
+      if ((rc = exchange_planes(hs, f, dst))) return rc;
+      for (auto* h : hs) CK(h, cudaDeviceSynchronize());
+    }
+  }
+  if (dist) {
+    // checkpoint for emrkc_dist_replay, then the prime level: every slab
+    // pushes its boundary V planes into the neighbours' current ghost slot
+    cudaEvent_t prev = nullptr;
+    for (auto* h : hs) {
+      CK(h, cudaSetDevice(h->device));
+      if (!h->ckpt) CK(h, cudaMalloc(&h->ckpt, sizeof(double) * h->len));
+      CK(h, cudaMemcpyAsync(h->ckpt, h->buf[h->cur], sizeof(double) * h->len,
+                            cudaMemcpyDeviceToDevice, h->stream));
+      if (lockstep && prev) CK(h, cudaStreamWaitEvent(h->stream, prev, 0));
+      Halo hp{};
+      const int ws = static_cast<int>(h->level & 1);
+      if (h->peer[0].linked) {
+        hp.put_lo = h->peer[0].ghost[ws];
+        hp.sig_lo = h->peer[0].cnt;
+      }
+      if (h->peer[1].linked) {
+        hp.put_hi = h->peer[1].ghost[ws];
+        hp.sig_hi = h->peer[1].cnt;
+      }
+      CK(h, emrkc_k::launch_halo_prime(h->geom, hp, h->buf[h->cur], h->stream));
+      dist_account(h, emrkc_k::halo_signals_prime(h->geom));
+      CK(h, cudaEventRecord(h->ev1, h->stream));
+      prev = h->ev1;
+    }
   }
   std::vector<std::vector<int>> in_idx(n, std::vector<int>(nsteps + 1));
   for (auto* h : hs) {
@@ -1224,12 +1311,20 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
         for (int k = 1; k <= pl.m; ++k) {
           for (size_t q = 0; q < n; ++q) {
             CK(hs[q], cudaSetDevice(hs[q]->device));
+            if (lockstep) {
+              // serialise every launch: each device-side wait is already
+              // satisfied when its kernel starts (test driver on one GPU)
+              const size_t prevq = q == 0 ? n - 1 : q - 1;
+              CK(hs[q], cudaStreamWaitEvent(hs[q]->stream, hs[prevq]->ev1, 0));
+            }
             if ((rc = launch_level(hs[q], &c[q], j, k))) return rc;
+            if (lockstep) CK(hs[q], cudaEventRecord(hs[q]->ev1, hs[q]->stream));
           }
-          if ((rc = sync_neighbours())) return rc;
+          if (!lockstep && (rc = sync_neighbours())) return rc;
         }
       for (size_t q = 0; q < n; ++q) hs[q]->cur = end_step(hs[q], &c[q]);
       // all-slab barrier + abort-word fold
+      if (lockstep) continue;  // distributed semantics: aborts are reconciled by replay
       for (size_t q = 0; q < n; ++q) {
         CK(hs[q], cudaSetDevice(hs[q]->device));
         CK(hs[q], cudaEventRecord(hs[q]->ev1, hs[q]->stream));
@@ -1270,6 +1365,10 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
       all_slots[k + 1] = q == 0 ? slots[k + 1] : std::max(all_slots[k + 1], slots[k + 1]);
     }
   }
+  if (ev == 0)
+    return set_err(hs[0], EMRKC_ECUDA,
+                   "distributed run: a neighbour's halo planes never arrived (10 s); "
+                   "all linked slabs must run concurrently");
   Decoded d = decode_event(ev, pl);
   if (single_step && !d.none && d.guard) d = Decoded{};  // emrkc_step has no guard
   int64_t accepted = nsteps, done = nsteps;
@@ -1298,6 +1397,7 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     res->abort_step = d.none ? -1 : step0 + d.step;
     res->abort_stage = d.guard ? 0 : d.stage;
     res->abort_inner = d.guard ? 0 : d.inner;
+    res->abort_outer_stage = d.guard ? 0 : d.outer_stage;
     // track_gate_range: initial state then each accepted step (simulate.cpp:113,228)
     double lo = 1.0, hi = 0.0;
     auto fold = [&](size_t k) {
@@ -1447,7 +1547,8 @@ int emrkc_run_timed(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
                     double rho_S, int64_t flush_bytes, double* launch_ms,
                     int64_t launch_ms_len, emrkc_run_result* res) {
   if (!h || !res || !launch_ms) return set_global(EMRKC_EINVAL, "null argument");
-  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "emrkc_run_timed: whole-grid handles only");
+  if (h->partitioned && !dist_linked(h))
+    return set_err(h, EMRKC_EINVAL, "emrkc_run_timed: whole-grid or distributed handles only");
   if (variant != EMRKC_VARIANT_STANDARD)
     return set_err(h, EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
   if (nsteps < 0 || flush_bytes < 0) return set_err(h, EMRKC_EINVAL, "emrkc_run_timed: bad sizes");
@@ -1523,34 +1624,136 @@ int emrkc_group_run(emrkc_group* g, int64_t step0, int64_t nsteps, double dt,
 
 // ---- multi-process ----------------------------------------------------------
 
-int64_t emrkc_ipc_blob_size(void) { return 4096; }
+namespace {
+struct IpcBlob {
+  char magic[8];
+  int32_t version;
+  int32_t device;
+  int64_t plane;
+  int64_t z_begin, z_end;
+  int64_t arena_bytes;
+  cudaIpcMemHandle_t mem;
+};
+constexpr char kBlobMagic[8] = {'E', 'M', 'R', 'K', 'C', 'I', 'P', 'C'};
+
+// Points side s of h at a neighbour arena (ghost[1-s][*] and cnt[1-s]).
+void link_peer(emrkc_handle* h, int s, void* arena, bool ipc) {
+  const size_t pl = static_cast<size_t>(h->geom.plane);
+  double* base = static_cast<double*>(arena);
+  const int o = 1 - s;
+  h->peer[s].linked = true;
+  h->peer[s].ipc = ipc;
+  h->peer[s].arena = arena;
+  h->peer[s].ghost[0] = base + (2 * o + 0) * pl;
+  h->peer[s].ghost[1] = base + (2 * o + 1) * pl;
+  h->peer[s].cnt = reinterpret_cast<unsigned long long*>(base + 4 * pl) + o;
+}
+}  // namespace
+
+int64_t emrkc_ipc_blob_size(void) { return static_cast<int64_t>(sizeof(IpcBlob)); }
 
 int emrkc_ipc_export(emrkc_handle* h, void* blob, int64_t len) {
-  (void)blob;
-  (void)len;
-  return set_err(h, EMRKC_EINVAL, "ipc_export: not implemented yet");
+  if (!h || !blob || len < static_cast<int64_t>(sizeof(IpcBlob)))
+    return set_global(EMRKC_EINVAL, "ipc_export: bad arguments");
+  if (!h->partitioned || !h->arena)
+    return set_err(h, EMRKC_EINVAL, "ipc_export: handle is not a partitioned slab");
+  int rc = use_device(h);
+  if (rc) return rc;
+  IpcBlob b{};
+  std::memcpy(b.magic, kBlobMagic, 8);
+  b.version = EMRKC_ABI_VERSION;
+  b.device = h->device;
+  b.plane = h->geom.plane;
+  b.z_begin = h->z_begin;
+  b.z_end = h->z_end;
+  b.arena_bytes = static_cast<int64_t>(h->arena_bytes);
+  CK(h, cudaIpcGetMemHandle(&b.mem, h->arena));
+  std::memcpy(blob, &b, sizeof(b));
+  return EMRKC_OK;
 }
 
-int emrkc_ipc_import(emrkc_handle* h, int32_t side, const void* blob,
-                     int64_t len) {
-  (void)side;
-  (void)blob;
-  (void)len;
-  return set_err(h, EMRKC_EINVAL, "ipc_import: not implemented yet");
+int emrkc_ipc_import(emrkc_handle* h, int32_t side, const void* blob, int64_t len) {
+  if (!h || !blob || len < static_cast<int64_t>(sizeof(IpcBlob)) || (side != 0 && side != 1))
+    return set_global(EMRKC_EINVAL, "ipc_import: bad arguments");
+  IpcBlob b;
+  std::memcpy(&b, blob, sizeof(b));
+  if (std::memcmp(b.magic, kBlobMagic, 8) != 0 || b.version != EMRKC_ABI_VERSION)
+    return set_err(h, EMRKC_EINVAL, "ipc_import: not an emrkc blob");
+  if (b.plane != h->geom.plane)
+    return set_err(h, EMRKC_EINVAL, "ipc_import: plane size mismatch");
+  if ((side == 0 && b.z_end != h->z_begin) || (side == 1 && b.z_begin != h->z_end))
+    return set_err(h, EMRKC_EINVAL, "ipc_import: blob is not the %s neighbour",
+                   side == 0 ? "lower" : "upper");
+  int rc = use_device(h);
+  if (rc) return rc;
+  void* ptr = nullptr;
+  CK(h, cudaIpcOpenMemHandle(&ptr, b.mem, cudaIpcMemLazyEnablePeerAccess));
+  link_peer(h, side, ptr, true);
+  return EMRKC_OK;
 }
 
 int emrkc_dist_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
                    double epsilon, int32_t variant, double rho_F,
                    double rho_S, emrkc_run_result* res) {
-  (void)step0;
-  (void)nsteps;
-  (void)dt;
-  (void)epsilon;
-  (void)variant;
-  (void)rho_F;
-  (void)rho_S;
-  (void)res;
-  return set_err(h, EMRKC_EINVAL, "dist_run: not implemented yet");
+  if (!h || !res) return set_global(EMRKC_EINVAL, "null argument");
+  if (variant != EMRKC_VARIANT_STANDARD)
+    return set_err(h, EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
+  if (!h->partitioned) return set_err(h, EMRKC_EINVAL, "dist_run: handle is not a slab");
+  return run_slabs({h}, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr);
+}
+
+int emrkc_dist_replay(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
+                      double epsilon, int32_t variant, double rho_F, double rho_S,
+                      emrkc_run_result* res) {
+  if (!h || !res) return set_global(EMRKC_EINVAL, "null argument");
+  if (!h->ckpt) return set_err(h, EMRKC_ESTATE, "dist_replay: no dist_run checkpoint");
+  int rc = use_device(h);
+  if (rc) return rc;
+  CK(h, cudaMemcpyAsync(h->buf[h->cur], h->ckpt, sizeof(double) * h->len,
+                        cudaMemcpyDeviceToDevice, h->stream));
+  return emrkc_dist_run(h, step0, nsteps, dt, epsilon, variant, rho_F, rho_S, res);
+}
+
+int emrkc_dist_link_local(emrkc_handle* lower, emrkc_handle* upper) {
+  if (!lower || !upper) return set_global(EMRKC_EINVAL, "null handle");
+  if (lower->z_end != upper->z_begin || lower->geom.plane != upper->geom.plane ||
+      !lower->arena || !upper->arena)
+    return set_global(EMRKC_EINVAL, "dist_link_local: slabs are not adjacent");
+  if (lower->device != upper->device) {
+    cudaSetDevice(lower->device);
+    cudaError_t e = cudaDeviceEnablePeerAccess(upper->device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+      return set_global(EMRKC_ECUDA, "peer access: %s", cudaGetErrorString(e));
+    cudaSetDevice(upper->device);
+    e = cudaDeviceEnablePeerAccess(lower->device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+      return set_global(EMRKC_ECUDA, "peer access: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+  }
+  link_peer(lower, 1, upper->arena, false);
+  link_peer(upper, 0, lower->arena, false);
+  return EMRKC_OK;
+}
+
+int emrkc_dist_lockstep_run(emrkc_handle* const* hs, int32_t n, int32_t replay,
+                            int64_t step0, int64_t nsteps, double dt, double epsilon,
+                            int32_t variant, double rho_F, double rho_S,
+                            emrkc_run_result* res) {
+  if (!hs || n < 1 || !res) return set_global(EMRKC_EINVAL, "bad arguments");
+  if (variant != EMRKC_VARIANT_STANDARD)
+    return set_global(EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
+  std::vector<emrkc_handle*> v(hs, hs + n);
+  for (auto* h : v) {
+    if (!dist_linked(h)) return set_global(EMRKC_ESTATE, "dist_lockstep_run: handles not linked");
+    if (replay) {
+      if (!h->ckpt) return set_err(h, EMRKC_ESTATE, "dist replay: no checkpoint");
+      cudaSetDevice(h->device);
+      CK(h, cudaMemcpy(h->buf[h->cur], h->ckpt, sizeof(double) * h->len,
+                       cudaMemcpyDeviceToDevice));
+    }
+  }
+  return run_slabs(v, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr, 0,
+                   nullptr, 0, /*lockstep=*/true);
 }
 
 }  // extern "C"

@@ -27,11 +27,12 @@ struct FastConsts {
   double l2e256, ln2hi, ln2lo, c24, c6, c12;
   double p1, p01, p001, p07, p0125, r18, r80, e05, em15;
   double gna, gk, gl, vl;
+  double e25;
 };
 __constant__ FastConsts kFC = {
     kL2E256, kLn2_256_hi, kLn2_256_lo, 1.0 / 24.0, 1.0 / 6.0, 1.0 / 12.0,
     0.1, 0.1, 0.01, 0.07, 0.125, 1.0 / 18.0, 0.0125, 1.6487212707001282,
-    0.22313016014842982, 1.2, 0.36, 0.003, -54.387};
+    0.22313016014842982, 1.2, 0.36, 0.003, -54.387, 12.182493960703473};
 // hh_expeuler_fast validity: |V| <= kFastVmax and eta <= kFastEtaMax. There
 // max(alpha + beta) ~ 450/ms (beta_m at V = -150 mV), so |eta Lambda| <= 700
 // and every exp_tab_nc argument stays in range; the batch product stays
@@ -114,11 +115,14 @@ __device__ __forceinline__ void hh_expeuler_fast(double V, double z0, double z1,
   const double um = xm * kFC.p1;
   const double un = xn * kFC.p1;
   const double w = -(V + 65.0);
-  const double e10 = exp_tab_nc(-um, tab);          // exp(-(V+40)/10)
   const double e18 = exp_tab_nc(w * kFC.r18, tab);  // exp(-(V+65)/18)
   const double e80 = exp_tab_nc(w * kFC.r80, tab);  // exp(-(V+65)/80)
   const double e40 = e80 * e80;
   const double e20 = e40 * e40;                     // exp(-(V+65)/20)
+  // exp(-(V+40)/10) = exp(-(V+65)/80)^8 e^{2.5}: ~15 ulp, which reaches
+  // alpha_m = 0.1 x/(1 - e10) amplified by 1/|x/10| <= 1e4 (series below
+  // 1e-4): <= 2e-11 relative, and only within ~1 mV of V = -40.
+  const double e10 = (e20 * e20) * kFC.e25;
   double dm = 1.0 - e10;
   double dn = fma(-e10, kFC.em15, 1.0);             // 1 - exp(-(V+55)/10)
   const double dh = fma(e10, kFC.e05, 1.0);         // 1 + exp(-(V+35)/10)

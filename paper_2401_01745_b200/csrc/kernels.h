@@ -31,6 +31,16 @@ struct Halo {
   const double* hi;   // plane z = zoff+nzl
   double* put_lo;     // where my first plane goes (lower neighbour's hi ghost)
   double* put_hi;     // where my last plane goes (upper neighbour's lo ghost)
+  // Cross-process protocol (null in-process, where stream order suffices):
+  // a block that put a plane bumps the neighbour's arrival counter after a
+  // system-scope fence; a block that reads a ghost plane first waits until
+  // its own counter reaches `expect_*`.
+  unsigned long long* sig_lo;        // lower neighbour's counter for its hi ghost
+  unsigned long long* sig_hi;        // upper neighbour's counter for its lo ghost
+  const unsigned long long* wait_lo; // my counter for my lo ghost
+  const unsigned long long* wait_hi;
+  unsigned long long expect_lo, expect_hi;
+  unsigned long long* timeout_flag;  // the abort word (code 0 = wait timed out)
 };
 
 // One outer stage of emRKC: pointers and coefficients.
@@ -96,6 +106,15 @@ struct FastInnerArgs {
 };
 
 int fast_zc(const Geom& g);
+// Signals per level that a neighbour receives from one launch of each kernel
+// family (blocks that hold the boundary plane of their slab).
+long long halo_signals_pipe(const Geom& g);
+long long halo_signals_march(const Geom& g);
+long long halo_signals_prime(const Geom& g);
+// Copies the first / last V plane of `y` into the neighbours' ghost slots
+// and signals (prime level of a distributed run).
+cudaError_t launch_halo_prime(const Geom& g, const Halo& h, const double* y,
+                              cudaStream_t st);
 cudaError_t launch_node_fast(const Geom& g, const Halo& h, const FastArgs& a,
                              bool ion, cudaStream_t st);
 cudaError_t launch_node_pipe(const Geom& g, const Halo& h, const FastArgs& a,

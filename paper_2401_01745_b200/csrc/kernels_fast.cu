@@ -151,6 +151,47 @@ __device__ __forceinline__ double current_fast(double V, double m, double h, dou
   return fma(gna, V - kVNa, fma(gk, V - kVK, kFC.gl * (V - kFC.vl)));
 }
 
+// ---- cross-process halo protocol (Halo::sig_* / wait_*) -------------------
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Thread 0 spins until the ghost planes this block reads have arrived; the
+// caller's __syncthreads() publishes that to the block. The spin is bounded
+// (~10 s): a neighbour that never arrives (a rank died, or a caller drove
+// linked slabs one at a time) records abort code 0 = protocol timeout
+// instead of hanging the GPU.
+__device__ __forceinline__ void halo_wait(const Halo& h, bool need_lo, bool need_hi) {
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    const long long t0 = clock64();
+    const long long limit = 20000000000LL;  // cycles (~10 s at 2 GHz)
+    bool late = false;
+    if (need_lo && h.wait_lo)
+      while (ld_acquire_sys(h.wait_lo) < h.expect_lo) {
+        __nanosleep(200);
+        if (clock64() - t0 > limit) { late = true; break; }
+      }
+    if (!late && need_hi && h.wait_hi)
+      while (ld_acquire_sys(h.wait_hi) < h.expect_hi) {
+        __nanosleep(200);
+        if (clock64() - t0 > limit) { late = true; break; }
+      }
+    if (late && h.timeout_flag) atomicMin(h.timeout_flag, 0ull);
+  }
+}
+// After all threads of the block wrote their boundary values.
+__device__ __forceinline__ void halo_signal(const Halo& h, bool put_lo, bool put_hi) {
+  if ((put_lo && h.sig_lo) || (put_hi && h.sig_hi)) {
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      __threadfence_system();
+      if (put_lo && h.sig_lo) atomicAdd_system(h.sig_lo, 1ull);
+      if (put_hi && h.sig_hi) atomicAdd_system(h.sig_hi, 1ull);
+    }
+  }
+}
+
 __device__ __forceinline__ bool prologue(const unsigned long long* ev, double* tab) {
   __shared__ int skip;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
@@ -308,7 +349,13 @@ template <int DIM, int FIRST, int ION>
 __global__ void __launch_bounds__(kFThreads, EMRKC_NODE_MINBLOCKS)
     k_node_fast(const Geom g, const Halo h, const FastArgs a) {
   __shared__ double tab[256];
-  if (prologue(a.event, tab)) return;
+  const int bz0 = (DIM == 3 ? blockIdx.z * a.zc : blockIdx.y * FBY * a.zc);
+  const int bz1 = (DIM == 3 ? bz0 + a.zc : bz0 + FBY * a.zc);
+  halo_wait(h, bz0 == 0, bz1 >= g.nzl);
+  if (prologue(a.event, tab)) {  // aborted earlier: still release the neighbours
+    halo_signal(h, bz0 == 0, bz1 >= g.nzl);
+    return;
+  }
   const Col<DIM> c = col_here<DIM>(g, a.zc);
   bool bad = false, guard = false, any = false;
   double glo = 2.0, ghi = -1.0;
@@ -370,6 +417,7 @@ __global__ void __launch_bounds__(kFThreads, EMRKC_NODE_MINBLOCKS)
   if (!ION && a.last && guard)
     atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
   if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, any);
+  halo_signal(h, bz0 == 0, bz1 >= g.nzl);
 }
 
 // ---------------------------------------------------------------------------
@@ -450,6 +498,11 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   double* gst = vst + kRV * T::VT;                // [kRG][3][NT]
   double* g2s = gst + kRG * 3 * T::NT;            // [kRG][4][NT] (!FIRST)
   const int t = threadIdx.x;
+  {
+    const int zb0 = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
+    halo_wait(h, zb0 == 0, zb0 + a.zc >= g.nzl);
+    if (h.wait_lo || h.wait_hi) __syncthreads();
+  }
   // abort word: uniform per block after the first barrier of the z loop
   __shared__ int skip;
   if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
@@ -562,6 +615,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     if (ION) pu += plane;
   }
   cp_wait<0>();
+  halo_signal(h, zb == 0, ze >= g.nzl);  // also when skipping: release the neighbours
   if (skip) return;
   if (bad) {
     Col<DIM> c;
@@ -586,7 +640,13 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
 template <int DIM, int LAST, int FIRST>
 __global__ void __launch_bounds__(kFThreads)
     k_vin_fast(const Geom g, const Halo h, const FastInnerArgs a) {
-  if (prologue(a.event, nullptr)) return;
+  const int bz0 = (DIM == 3 ? blockIdx.z * a.zc : blockIdx.y * FBY * a.zc);
+  const int bz1 = (DIM == 3 ? bz0 + a.zc : bz0 + FBY * a.zc);
+  halo_wait(h, bz0 == 0, bz1 >= g.nzl);
+  if (prologue(a.event, nullptr)) {  // aborted earlier: still release the neighbours
+    halo_signal(h, bz0 == 0, bz1 >= g.nzl);
+    return;
+  }
   const Col<DIM> c = col_here<DIM>(g, a.zc);
   bool bad_in = false, bad_out = false, guard = false;
   if (c.valid) {
@@ -625,6 +685,7 @@ __global__ void __launch_bounds__(kFThreads)
   if (LAST && bad_out) atomicMin(a.event, base + a.m + 1);
   if (LAST && a.last && guard)
     atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+  halo_signal(h, bz0 == 0, bz1 >= g.nzl);
 }
 
 template <int DIM>
@@ -650,6 +711,42 @@ int fast_zc(const Geom& g) {
   int zc = 16;
   while (zc > 4 && tiles * ((g.nzl + zc - 1) / zc) < 148LL * 5 * 2) zc /= 2;
   return zc > g.nzl ? g.nzl : zc;
+}
+
+long long halo_signals_pipe(const Geom& g) {
+  if (g.dim == 3) return (long long)((g.n0 + 31) / 32) * ((g.n1 + 3) / 4);
+  return (g.n0 + 127) / 128;
+}
+long long halo_signals_march(const Geom& g) {
+  if (g.dim == 3) return (long long)((g.n0 + FBX - 1) / FBX) * ((g.n1 + FBY - 1) / FBY);
+  return (g.n0 + FBX - 1) / FBX;
+}
+
+namespace {
+// Prime level: first / last V plane of y into the neighbours' ghost slots.
+// One block per 256 plane points; every block signals the sides it wrote.
+__global__ void k_halo_prime(const Geom g, const Halo h, const double* __restrict__ y) {
+  const long long i = blockIdx.x * 256LL + threadIdx.x;
+  if (i < g.plane) {
+    if (h.put_lo) h.put_lo[i] = y[i];
+    if (h.put_hi) h.put_hi[i] = y[i + g.plane * (g.nzl - 1)];
+  }
+  if ((h.put_lo && h.sig_lo) || (h.put_hi && h.sig_hi)) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      if (h.put_lo && h.sig_lo) atomicAdd_system(h.sig_lo, 1ull);
+      if (h.put_hi && h.sig_hi) atomicAdd_system(h.sig_hi, 1ull);
+    }
+  }
+}
+}  // namespace
+
+long long halo_signals_prime(const Geom& g) { return (g.plane + 255) / 256; }
+
+cudaError_t launch_halo_prime(const Geom& g, const Halo& h, const double* y, cudaStream_t st) {
+  k_halo_prime<<<(unsigned)((g.plane + 255) / 256), 256, 0, st>>>(g, h, y);
+  return cudaGetLastError();
 }
 
 #define FDISPATCH(g, ...)                                   \

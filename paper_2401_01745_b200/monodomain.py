@@ -268,6 +268,39 @@ class MonodomainOperator:
         _check(rc, self._h)
         return rep
 
+    # ---- distributed slabs (paper_2401_01745_b200/dist.py) ----
+    def ipc_export(self) -> bytes:
+        n = int(_lib().emrkc_ipc_blob_size())
+        buf = C.create_string_buffer(n)
+        _check(_lib().emrkc_ipc_export(self._h, buf, n), self._h)
+        return buf.raw
+
+    def ipc_import(self, side: int, blob: bytes):
+        _check(_lib().emrkc_ipc_import(self._h, side, blob, len(blob)), self._h)
+
+    def dist_run(self, step0, nsteps, dt, rho_F, rho_S, epsilon=kDefaultDamping) -> dict:
+        res = RunResult()
+        _check(_lib().emrkc_dist_run(self._h, step0, nsteps, dt, epsilon, capi.EMRKC_VARIANT_STANDARD,
+                                     rho_F, rho_S, C.byref(res)), self._h)
+        return res.as_dict()
+
+    def dist_replay(self, step0, nsteps, dt, rho_F, rho_S, epsilon=kDefaultDamping) -> dict:
+        res = RunResult()
+        _check(_lib().emrkc_dist_replay(self._h, step0, nsteps, dt, epsilon,
+                                        capi.EMRKC_VARIANT_STANDARD, rho_F, rho_S, C.byref(res)),
+               self._h)
+        return res.as_dict()
+
+    def run_timed_dist(self, step0, nsteps, dt, rho_F, rho_S, epsilon=kDefaultDamping,
+                       flush_bytes=256 << 20):
+        rep = plan_step(dt, rho_F, rho_S, epsilon)
+        launch_ms = np.zeros(nsteps * rep.s * rep.m)
+        res = RunResult()
+        _check(_lib().emrkc_run_timed(self._h, step0, nsteps, dt, epsilon, capi.EMRKC_VARIANT_STANDARD,
+                                      rho_F, rho_S, flush_bytes, dptr(launch_ms), launch_ms.size,
+                                      C.byref(res)), self._h)
+        return launch_ms, res.as_dict()
+
     def run(self, step0: int, nsteps: int, dt: float, rho_F: float, rho_S: float,
             epsilon: float = kDefaultDamping) -> RunResult:
         """run_simulation's emRKC loop on the device (P/src/simulate.cpp:176-229)."""
