@@ -46,16 +46,25 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 
-# Algorithmic bytes per node of each kernel: fp64 fields a
-# launch must read and write at least once.
+# Algorithmic bytes per node of each kernel launch: the fp64
+# fields a launch must read and write at least once.
 KERNEL_BYTES = {
     ("m1", "first_outer"): 64,   # g_{j-1} in (4 fields), g_j out (4)
-    ("m1", "outer"): 96,         # + g_{j-2}
-    ("first", None): 72,         # g_{j-1} in (4); u_1, fs, y_E out (5)
-    ("inner", None): 32,         # u_{k-1}, u_{k-2}, fs in; u_k out
-    ("last", "first_outer"): 104,  # u_{m-1}, fs, y_E(3), g_{j-1}(4) in; g_j out (4)
-    ("last", "outer"): 136,        # + g_{j-2}
+    ("m1", "outer"): 96,         # + g_{j-2} in
+    ("first", "first_outer"): 64,  # g_{j-1} in (4); gates of g_j (3) + d_1 out
+    ("first", "outer"): 88,        # + gates of g_{j-2}... (V of g_{j-2} read later)
+    ("inner2", None): 16,        # d_1 in, d_2 out
+    ("inner", None): 32,         # d_{k-1}, d_{k-2}, d_1 in; d_k out
+    ("last2", "first_outer"): 24,  # d_1, V of g_{j-1} in; V of g_j out
+    ("last2", "outer"): 32,        # + V of g_{j-2}
+    ("last", "first_outer"): 40,   # d_{m-1}, d_{m-2}, d_1, V in; V out
+    ("last", "outer"): 48,
 }
+KERNEL_NAMES = {"m1": "k_node_persist (m = 1: whole outer stage)",
+                "first": "k_node_persist (m >= 2: ionic + inner stage 1)",
+                "inner2": "k_vin_fast (inner stage 2)", "inner": "k_vin_fast (inner stage k)",
+                "last2": "k_vin_fast (last inner stage, m = 2)",
+                "last": "k_vin_fast (last inner stage)"}
 
 
 def launch_kinds(s: int, m: int):
@@ -67,11 +76,11 @@ def launch_kinds(s: int, m: int):
             if m == 1:
                 out.append(("m1", o))
             elif k == 1:
-                out.append(("first", None))
+                out.append(("first", o))
             elif k < m:
-                out.append(("inner", None))
+                out.append(("inner2" if k == 2 else "inner", None))
             else:
-                out.append(("last", o))
+                out.append(("last2" if m == 2 else "last", o))
     return out
 
 
@@ -382,8 +391,7 @@ def roofline_of(m, w, peak, peak_kind):
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "traffic": traffic,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-        "kernel": {"m1": "k_stage_m1", "first": "k_stage_first", "inner": "k_stage_inner",
-                   "last": "k_stage_inner(last)"}[kinds[dom][0]],
+        "kernel": KERNEL_NAMES[kinds[dom][0]],
         "alg_bytes_per_node": kb, "mean_launch_ms": float(per_pos[dom]),
         "share_of_step": float(per_pos[dom] / per_pos.sum()),
         "step_alg_bytes_per_node": 64, "step_achieved_gbs": step_gbs,

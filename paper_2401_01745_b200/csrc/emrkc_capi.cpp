@@ -478,7 +478,9 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.code_base = a.code_base;
       f.event = a.event;
       f.gate_slot = a.gate_slot;
-      if (h->pipe)
+      if (h->pipe == 2)
+        CK(h, emrkc_k::launch_node_persist(h->geom, hl, f, pl.m >= 2, h->stream));
+      else if (h->pipe)
         CK(h, emrkc_k::launch_node_pipe(h->geom, hl, f, pl.m >= 2, h->stream));
       else
         CK(h, emrkc_k::launch_node_fast(h->geom, hl, f, pl.m >= 2, h->stream));
@@ -606,7 +608,7 @@ int init_handle(emrkc_handle* h) {
   h->fast = f ? std::atoi(f) : 1;
   h->zc = emrkc_k::fast_zc(h->geom);
   const char* pp = std::getenv("EMRKC_PIPE");
-  h->pipe = (pp && *pp) ? std::atoi(pp) : 1;
+  h->pipe = (pp && *pp) ? std::atoi(pp) : 1;  // 1: per-chunk blocks, 2: persistent, 0: march
   if (const char* zc = std::getenv("EMRKC_ZC"))
     if (*zc) h->zc = std::max(1, std::atoi(zc));
   return EMRKC_OK;

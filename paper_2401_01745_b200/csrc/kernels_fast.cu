@@ -274,7 +274,7 @@ __device__ __forceinline__ NodeOut node_update(const Geom& g, const FastArgs& a,
   return r;
 }
 
-template <int DIM, int FIRST, int ION>
+template <int DIM, int FIRST, int ION, int SLOW = 1>
 __device__ __forceinline__ NodeOut node_update_s(const Geom& g, const FastArgs& a,
                                                  const double* __restrict__ tab, double vm,
                                                  double vc, double vp, double xs, double ys,
@@ -284,7 +284,7 @@ __device__ __forceinline__ NodeOut node_update_s(const Geom& g, const FastArgs& 
   if (DIM >= 2) D = fma(g.w[0], xs, D);
   if (DIM == 3) D = fma(g.w[1], ys, D);
   double d0, d1, d2;
-  if (fabs(vc) <= a.vfast) {
+  if (!SLOW || fabs(vc) <= a.vfast) {
     hh_expeuler_fast(vc, z0, z1, z2, a.eta, tab, d0, d1, d2);
   } else {
     const Dgate dd = hh_expeuler_ref(vc, z0, z1, z2, a.eta);
@@ -561,6 +561,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   load_plane(zb + 1);
   const bool scol = valid && stim_col_xy<DIM>(g, cx, cy);
   bool bad = false, guard = false;
+  unsigned slow_mask = 0;  // planes (z - zb < 32) left to the reference path
   double glo = 2.0, ghi = -1.0;
   const int cell = (DIM == 3 ? (ty + 1) * T::HX : 0) + tx + 1;
   double* po = a.out + ip + plane * zb;
@@ -585,10 +586,14 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     const double* G0 = gst + ((z - zb) & (kRG - 1)) * 3 * T::NT + t;
     const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
     const double stim = (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0;
-    const NodeOut r = node_update_s<DIM, FIRST, ION>(
+    // |V| beyond the fast path's range (or non-finite): deferred to the
+    // reference-order path after the loop, so the hot loop has no call
+    const bool fast = fabs(vc) <= a.vfast;
+    if (!fast) slow_mask |= 1u << (z - zb);
+    const NodeOut r = node_update_s<DIM, FIRST, ION, 0>(
         g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, stim,
         g2s + ((z - zb) & (kRG - 1)) * 4 * T::NT + t, T::NT);
-    if (valid) {
+    if (valid && fast) {
       po[nn] = r.o1;
       po[2 * nn] = r.o2;
       po[3 * nn] = r.o3;
@@ -615,6 +620,43 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     if (ION) pu += plane;
   }
   cp_wait<0>();
+  if (!skip && valid && slow_mask) {
+    // deferred nodes: reference-order ionic path, inputs from global memory
+    const Nbr<DIM> o = nbr_of<DIM>(g, Col<DIM>{cx, cy, ip, zb, ze, true});
+    for (int z = zb; z < ze; ++z) {
+      if (!(slow_mask >> (z - zb) & 1u)) continue;
+      const long long i = ip + plane * z;
+      const double vc = __ldg(G + i);
+      const double vm = zval(G, g, ip, z - 1, h.lo, h.hi);
+      const double vp = zval(G, g, ip, z + 1, h.lo, h.hi);
+      double xs = 0.0, ys = 0.0;
+      if (DIM >= 2) xs = __ldg(G + i + o.xm) + __ldg(G + i + o.xp);
+      if (DIM == 3) ys = __ldg(G + i + o.ym) + __ldg(G + i + o.yp);
+      const double stim = (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0;
+      double q[4] = {0.0, 0.0, 0.0, 0.0};
+      if (!FIRST)
+        for (int f = 0; f < 4; ++f) q[f] = __ldg(a.g2 + f * nn + i);
+      const NodeOut r = node_update_s<DIM, FIRST, ION, 1>(
+          g, a, tab, vm, vc, vp, xs, ys, __ldg(G + nn + i), __ldg(G + 2 * nn + i),
+          __ldg(G + 3 * nn + i), stim, q, 1);
+      a.out[nn + i] = r.o1;
+      a.out[2 * nn + i] = r.o2;
+      a.out[3 * nn + i] = r.o3;
+      if (ION) {
+        a.u1[i] = r.o0;
+      } else {
+        a.out[i] = r.o0;
+        guard |= fabs(r.o0) > 1e6;
+      }
+      bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
+      if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
+      if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
+      if (a.last) {
+        glo = fmin(glo, fmin(r.o1, fmin(r.o2, r.o3)));
+        ghi = fmax(ghi, fmax(r.o1, fmax(r.o2, r.o3)));
+      }
+    }
+  }
   halo_signal(h, zb == 0, ze >= g.nzl);  // also when skipping: release the neighbours
   if (skip) return;
   if (bad) {
@@ -632,6 +674,213 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   if (!ION && a.last && guard)
     atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
   if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, valid && ze > zb);
+}
+
+// ---------------------------------------------------------------------------
+// k_node_persist: persistent form of k_node_pipe. The grid is sized to the
+// resident capacity; each block walks work items (tile, z-chunk) round-robin
+// and streams all of them through ONE continuous cp.async ring, so the
+// pipeline fill, the exp-table load and the abort-word check are paid once
+// per block instead of once per chunk, and the next item's planes load
+// while the current item's last planes compute.
+//
+// Sequences: item k contributes V loads for planes zb-1 .. ze (zc+2 loads)
+// and computes planes zb .. ze-1. Before computing a plane the block has
+// issued every load up to one past the planes it reads; ring depths V 8,
+// gates 4 keep every slot's rewrite behind a __syncthreads.
+// ---------------------------------------------------------------------------
+template <int DIM, int FIRST, int ION>
+__global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
+    k_node_persist(const Geom g, const Halo h, const FastArgs a, const int items,
+                   const int tiles_x) {
+  using T = PipeTile<DIM>;
+  extern __shared__ double smem[];
+  double* tab = smem;
+  double* vst = smem + 256;                       // [kRV][VT]
+  double* gst = vst + kRV * T::VT;                // [kRG][3][NT]
+  double* g2s = gst + kRG * 3 * T::NT;            // [kRG][4][NT] (!FIRST)
+  const int t = threadIdx.x;
+  __shared__ int skip;
+  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  {
+    const unsigned st = (unsigned)__cvta_generic_to_shared(tab);
+    for (int j = t; j < 256; j += T::NT) cp_async8(st + 8u * j, kExp2Tab256 + j);
+    cp_commit();
+  }
+  const int tx = t % T::TX, ty = t / T::TX;
+  const int nchunk = (g.nzl + a.zc - 1) / a.zc;
+  const long long nn = g.nn, plane = g.plane;
+  const double* G = a.g1;
+  const unsigned sv0 = (unsigned)__cvta_generic_to_shared(vst) + 8u * t;
+  const unsigned sg0 = (unsigned)__cvta_generic_to_shared(gst) + 8u * t;
+  const unsigned sq0 = (unsigned)__cvta_generic_to_shared(g2s) + 8u * t;
+  const bool has1 = t + T::NT < T::VT;
+  const int cell = (DIM == 3 ? (ty + 1) * T::HX : 0) + tx + 1;
+
+  // ---- loader state (the item being loaded may run ahead of compute)
+  int l_item = blockIdx.x;  // item index
+  int l_zz = 0;             // next plane to load within l_item (local z)
+  int l_q = 0;              // V load sequence number
+  int l_c = 0;              // gate (compute-plane) sequence number
+  int l_x0 = 0, l_y0 = 0, l_zb = 0, l_ze = 0;
+  long long l_voff0 = 0, l_voff1 = 0;
+  const double* l_gcol = nullptr;
+  const double* l_qcol = nullptr;
+  auto item_geom = [&](int it, int& x0, int& y0, int& zb, int& ze) {
+    const int chunk = it % nchunk;
+    const int tile = it / nchunk;
+    x0 = (tile % tiles_x) * T::TX;
+    y0 = DIM == 3 ? (tile / tiles_x) * T::TY : 0;
+    zb = chunk * a.zc;
+    ze = min(g.nzl, zb + a.zc);
+  };
+  auto l_begin = [&]() {
+    if (l_item >= items) return;
+    item_geom(l_item, l_x0, l_y0, l_zb, l_ze);
+    l_zz = l_zb - 1;
+    l_voff0 = halo_offset<DIM>(g, l_x0, l_y0, t);
+    l_voff1 = has1 ? halo_offset<DIM>(g, l_x0, l_y0, t + T::NT) : 0;
+    const int cx = l_x0 + tx, cy = l_y0 + ty;
+    const bool v = cx < g.n0 && (DIM == 2 || cy < g.n1);
+    const long long ip = v ? (long long)cx + (long long)g.n0 * cy : 0;
+    l_gcol = G + nn + ip;
+    l_qcol = FIRST ? nullptr : a.g2 + ip;
+    // ghost planes of a slab face: wait for the neighbour's arrival
+    const bool need_lo = l_zb == 0 && h.wait_lo, need_hi = l_ze >= g.nzl && h.wait_hi;
+    if (need_lo || need_hi) {
+      halo_wait(h, need_lo, need_hi);
+      __syncthreads();
+    }
+  };
+  // issues the next V plane (and its gates); one commit group per call
+  auto l_next = [&]() {
+    if (l_item < items) {
+      const unsigned sv = sv0 + 8u * T::VT * (l_q & (kRV - 1));
+      const double* vp = vplane(g, h, G, l_zz);
+      cp_async8(sv, vp + l_voff0);
+      if (has1) cp_async8(sv + 8u * T::NT, vp + l_voff1);
+      if (l_zz >= l_zb && l_zz < l_ze) {
+        const unsigned s = (unsigned)(l_c & (kRG - 1));
+        const unsigned sg = sg0 + 8u * 3 * T::NT * s;
+        const double* gp = l_gcol + plane * l_zz;
+        cp_async8(sg, gp);
+        cp_async8(sg + 8u * T::NT, gp + nn);
+        cp_async8(sg + 16u * T::NT, gp + 2 * nn);
+        if (!FIRST) {
+          const unsigned sq = sq0 + 8u * 4 * T::NT * s;
+          const double* qp = l_qcol + plane * l_zz;
+          cp_async8(sq, qp);
+          cp_async8(sq + 8u * T::NT, qp + nn);
+          cp_async8(sq + 16u * T::NT, qp + 2 * nn);
+          cp_async8(sq + 24u * T::NT, qp + 3 * nn);
+        }
+        ++l_c;
+      }
+      ++l_q;
+      if (++l_zz > l_ze) {
+        l_item += gridDim.x;
+        l_begin();
+      }
+    }
+    cp_commit();
+  };
+
+  bool bad = false, guard = false, any = false;
+  double glo = 2.0, ghi = -1.0;
+  int c_q = 1;  // V sequence number of the plane being computed
+  int c_c = 0;  // gate sequence number of the plane being computed
+  l_begin();
+  l_next();  // zb - 1
+  l_next();  // zb
+  l_next();  // zb + 1
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    int x0, y0, zb, ze;
+    item_geom(it, x0, y0, zb, ze);
+    const int cx = x0 + tx, cy = y0 + ty;
+    const bool valid = cx < g.n0 && (DIM == 2 || cy < g.n1);
+    const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
+    const bool scol = valid && stim_col_xy<DIM>(g, cx, cy);
+    double* po = a.out + ip + plane * zb;
+    double* pu = ION ? a.u1 + ip + plane * zb : nullptr;
+    for (int z = zb; z < ze; ++z) {
+      l_next();  // V sequence c_q + 2
+      cp_wait<1>();  // everything up to c_q + 1 (this plane's vp) has landed
+      __syncthreads();
+      if (skip) break;
+      const double* V0 = vst + (c_q & (kRV - 1)) * T::VT;
+      const double vc = V0[cell];
+      const double vm = vst[((c_q - 1) & (kRV - 1)) * T::VT + cell];
+      const double vp = vst[((c_q + 1) & (kRV - 1)) * T::VT + cell];
+      double xs = 0.0, ys = 0.0;
+      if (DIM >= 2) xs = V0[cell - 1] + V0[cell + 1];
+      if (DIM == 3) ys = V0[cell - T::HX] + V0[cell + T::HX];
+      const double* G0 = gst + (c_c & (kRG - 1)) * 3 * T::NT + t;
+      const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
+      const double stim = (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0;
+      const NodeOut r = node_update_s<DIM, FIRST, ION>(
+          g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, stim,
+          g2s + (c_c & (kRG - 1)) * 4 * T::NT + t, T::NT);
+      if (valid) {
+        po[nn] = r.o1;
+        po[2 * nn] = r.o2;
+        po[3 * nn] = r.o3;
+        if (ION) {
+          *pu = r.o0;
+        } else {
+          *po = r.o0;
+          guard |= fabs(r.o0) > 1e6;
+        }
+        bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
+        if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
+        if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
+        if (a.last) {
+          const double mn = r.o1 < r.o2 ? r.o1 : r.o2;
+          const double mx = r.o1 < r.o2 ? r.o2 : r.o1;
+          glo = mn < glo ? mn : glo;
+          ghi = mx > ghi ? mx : ghi;
+          glo = r.o3 < glo ? r.o3 : glo;
+          ghi = r.o3 > ghi ? r.o3 : ghi;
+          any = true;
+        }
+      }
+      po += plane;
+      if (ION) pu += plane;
+      ++c_q;
+      ++c_c;
+    }
+    if (skip) {
+      // keep the neighbour protocol alive, then stop
+      halo_signal(h, zb == 0, ze >= g.nzl);
+      for (int j = it + gridDim.x; j < items; j += gridDim.x) {
+        int a0, a1, b0, b1;
+        item_geom(j, a0, a1, b0, b1);
+        halo_signal(h, b0 == 0, b1 >= g.nzl);
+      }
+      break;
+    }
+    c_q += 2;  // past this item's plane ze and the next item's zb - 1
+    l_next();  // an item loads two planes more than it computes: keep the
+    l_next();  // loader two ahead across the boundary
+    halo_signal(h, zb == 0, ze >= g.nzl);
+    if (bad) {
+      Col<DIM> c;
+      c.c0 = cx;
+      c.c1 = cy;
+      c.ip = ip;
+      c.z0 = zb;
+      c.z1 = ze;
+      c.valid = true;
+      const bool inner = valid && inner_nonfinite<DIM>(g, h, G, c, nbr_of<DIM>(g, c), a.eta);
+      atomicMin(a.event, a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1)) +
+                             (inner ? 1 : a.m + 1));
+      bad = false;
+    }
+  }
+  cp_wait<0>();
+  if (skip) return;
+  if (!ION && a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+  if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, any);
 }
 
 // ---------------------------------------------------------------------------
@@ -789,6 +1038,46 @@ static cudaError_t launch_pipe_t(const Geom& g, const Halo& h, const FastArgs& a
                           : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
   k_node_pipe<D, F, I><<<grd, T::NT, smem, st>>>(g, h, a);
   return cudaGetLastError();
+}
+
+template <int D, int F, int I>
+static cudaError_t launch_persist_t(const Geom& g, const Halo& h, const FastArgs& a,
+                                    cudaStream_t st) {
+  using T = PipeTile<D>;
+  constexpr size_t smem = pipe_smem_bytes<D, F>();
+  static int per_sm = 0;
+  static int nsm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k_node_persist<D, F, I>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_node_persist<D, F, I>, T::NT, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int tiles_x = (g.n0 + T::TX - 1) / T::TX;
+  const int tiles_y = D == 3 ? (g.n1 + T::TY - 1) / T::TY : 1;
+  const int nchunk = (g.nzl + a.zc - 1) / a.zc;
+  const long long items = (long long)tiles_x * tiles_y * nchunk;
+  const long long cap = (long long)per_sm * nsm;
+  const int grid = (int)(items < cap ? items : cap);
+  k_node_persist<D, F, I><<<grid, T::NT, smem, st>>>(g, h, a, (int)items, tiles_x);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_node_persist(const Geom& g, const Halo& h, const FastArgs& a, bool ion,
+                                cudaStream_t st) {
+  const bool first = a.j == 1;
+  if (g.dim == 3) {
+    if (ion) return first ? launch_persist_t<3, 1, 1>(g, h, a, st) : launch_persist_t<3, 0, 1>(g, h, a, st);
+    return first ? launch_persist_t<3, 1, 0>(g, h, a, st) : launch_persist_t<3, 0, 0>(g, h, a, st);
+  }
+  if (g.dim == 2) {
+    if (ion) return first ? launch_persist_t<2, 1, 1>(g, h, a, st) : launch_persist_t<2, 0, 1>(g, h, a, st);
+    return first ? launch_persist_t<2, 1, 0>(g, h, a, st) : launch_persist_t<2, 0, 0>(g, h, a, st);
+  }
+  return launch_node_fast(g, h, a, ion, st);
 }
 
 cudaError_t launch_node_pipe(const Geom& g, const Halo& h, const FastArgs& a, bool ion,

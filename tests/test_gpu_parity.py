@@ -205,3 +205,28 @@ def test_group_slabs_bitwise(oracle, name, nslab):
     assert (res.s, res.m, res.n_fF) == (rw.s, rw.m, rw.n_fF)
     assert res.gate_min == rw.gate_min and res.gate_max == rw.gate_max
     lib.emrkc_group_destroy(grp)
+
+
+@pytest.mark.parametrize("fast", [1, 0])
+def test_out_of_range_voltages(oracle, fast, monkeypatch):
+    """Nodes with |V| beyond the fast ionic path's range (150 mV) take the
+    reference-order path (deferred recompute in the fast kernels)."""
+    monkeypatch.setenv("EMRKC_FAST", str(fast))
+    for dim in (2, 3):
+        if dim == 2:
+            p = small_2d(48, 40)
+        else:
+            p = make_problem(3, [24, 20, 18], [0.25] * 3, [0.2, 0.1, 0.05], 140.0, 0.01, 70.0,
+                             [-0.125] * 3, [0.875] * 3, 0.0, 1.0)
+        y0 = noisy(oracle, p, 5)
+        nn = p.n_nodes
+        rng = np.random.default_rng(9)
+        idx = rng.choice(nn, 12, replace=False)
+        y0[idx] = rng.choice([160.0, -170.0, 400.0, -300.0, 1200.0], 12)
+        op = MonodomainOperator(p)
+        op.set_state(y0)
+        res = op.run(0, 3, 0.05, 12.0, 0.7)
+        yo, ro, _ = oracle.run(p, y0, 0, 3, 0.05, 0.05, 12.0, 0.7)
+        assert (res.aborted, res.abort_kind, res.abort_step) == (ro.aborted, ro.abort_kind, ro.abort_step)
+        errs = rel_l2_blocks(oracle, p, op.get_state(), yo)
+        assert max(errs) <= TOL, (dim, errs)
