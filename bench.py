@@ -60,8 +60,8 @@ KERNEL_BYTES = {
     ("last", "first_outer"): 40,   # d_{m-1}, d_{m-2}, d_1, V in; V out
     ("last", "outer"): 48,
 }
-KERNEL_NAMES = {"m1": "k_node_persist (m = 1: whole outer stage)",
-                "first": "k_node_persist (m >= 2: ionic + inner stage 1)",
+KERNEL_NAMES = {"m1": "k_node_pipe (m = 1: whole outer stage)",
+                "first": "k_node_pipe (m >= 2: ionic + inner stage 1)",
                 "inner2": "k_vin_fast (inner stage 2)", "inner": "k_vin_fast (inner stage k)",
                 "last2": "k_vin_fast (last inner stage, m = 2)",
                 "last": "k_vin_fast (last inner stage)"}

@@ -511,10 +511,13 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.zc = h->zc;
       f.code_base = a.code_base;
       f.event = a.event;
-      CK(h, emrkc_k::launch_vin_fast(h->geom, hl, f, h->stream));
+      if (h->pipe)
+        CK(h, emrkc_k::launch_vin_pipe(h->geom, hl, f, h->stream));
+      else
+        CK(h, emrkc_k::launch_vin_fast(h->geom, hl, f, h->stream));
     }
     if (dist_linked(h)) {
-      const bool pipe_family = (k == 1) && h->pipe && h->geom.dim >= 2;
+      const bool pipe_family = h->pipe && h->geom.dim >= 2;
       dist_account(h, pipe_family ? emrkc_k::halo_signals_pipe(h->geom)
                                   : emrkc_k::halo_signals_march(h->geom));
     }

@@ -123,6 +123,8 @@ cudaError_t launch_node_persist(const Geom& g, const Halo& h, const FastArgs& a,
                                 bool ion, cudaStream_t st);
 cudaError_t launch_vin_fast(const Geom& g, const Halo& h,
                             const FastInnerArgs& a, cudaStream_t st);
+cudaError_t launch_vin_pipe(const Geom& g, const Halo& h,
+                            const FastInnerArgs& a, cudaStream_t st);
 
 // Launch helpers (all asynchronous on `st`). fast: shared-transcendental
 // ionic evaluation (hh_fast) instead of the reference-order one.

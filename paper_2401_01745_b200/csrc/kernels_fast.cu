@@ -884,6 +884,118 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
 }
 
 // ---------------------------------------------------------------------------
+// k_vin_pipe: the V-only inner stage with the same cp.async plane ring as
+// k_node_pipe. Stencil field d_{k-1} with halo; pointwise d_{k-2}, d_1 and,
+// on the last stage, V of g_{j-1} (and g_{j-2}).
+// ---------------------------------------------------------------------------
+template <int DIM>
+constexpr size_t vin_smem_bytes() {
+  using T = PipeTile<DIM>;
+  return sizeof(double) * (kRV * T::VT + kRG * 4 * T::NT);
+}
+
+template <int DIM, int LAST, int FIRST>
+__global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
+    k_vin_pipe(const Geom g, const Halo h, const FastInnerArgs a) {
+  using T = PipeTile<DIM>;
+  extern __shared__ double smem[];
+  double* vst = smem;                  // [kRV][VT]   d_{k-1} with halo
+  double* cst = vst + kRV * T::VT;     // [kRG][4][NT] d1, d_{k-2}, V1, V2
+  const int t = threadIdx.x;
+  {
+    const int zb0 = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
+    halo_wait(h, zb0 == 0, zb0 + a.zc >= g.nzl);
+    if (h.wait_lo || h.wait_hi) __syncthreads();
+  }
+  __shared__ int skip;
+  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  const int tx = t % T::TX, ty = t / T::TX;
+  const int x0 = blockIdx.x * T::TX;
+  const int y0 = DIM == 3 ? blockIdx.y * T::TY : 0;
+  const int zb = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
+  const int ze = min(g.nzl, zb + a.zc);
+  const int cx = x0 + tx, cy = y0 + ty;
+  const bool valid = cx < g.n0 && (DIM == 2 || cy < g.n1);
+  const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
+  const long long plane = g.plane;
+  const double* U = a.um1;
+  const long long voff0 = halo_offset<DIM>(g, x0, y0, t);
+  const bool has1 = t + T::NT < T::VT;
+  const long long voff1 = has1 ? halo_offset<DIM>(g, x0, y0, t + T::NT) : 0;
+  const unsigned sv0 = (unsigned)__cvta_generic_to_shared(vst) + 8u * t;
+  const unsigned sc0 = (unsigned)__cvta_generic_to_shared(cst) + 8u * t;
+  const bool has2 = a.um2 != nullptr;
+  const bool d1_is_u = a.um1 == a.d1;  // k == 2: d_1 is the stencil field itself
+
+  auto load_plane = [&](int zz) {
+    const unsigned sv = sv0 + 8u * T::VT * ((zz - zb + 1) & (kRV - 1));
+    const double* vp = vplane(g, h, U, zz);
+    cp_async8(sv, vp + voff0);
+    if (has1) cp_async8(sv + 8u * T::NT, vp + voff1);
+    if (zz >= zb && zz < ze) {
+      const unsigned sc = sc0 + 8u * 4 * T::NT * ((zz - zb) & (kRG - 1));
+      const long long i = ip + plane * zz;
+      if (!d1_is_u) cp_async8(sc, a.d1 + i);
+      if (has2) cp_async8(sc + 8u * T::NT, a.um2 + i);
+      if (LAST) {
+        cp_async8(sc + 16u * T::NT, a.g1v + i);
+        if (!FIRST) cp_async8(sc + 24u * T::NT, a.g2v + i);
+      }
+    }
+    cp_commit();
+  };
+  load_plane(zb - 1);
+  load_plane(zb);
+  load_plane(zb + 1);
+  bool bad_in = false, bad_out = false, guard = false;
+  const int cell = (DIM == 3 ? (ty + 1) * T::HX : 0) + tx + 1;
+  for (int z = zb; z < ze; ++z) {
+    if (z + 2 <= ze) load_plane(z + 2);
+    else cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    if (skip) break;
+    const int p = z - zb + 1;
+    const double* V0 = vst + (p & (kRV - 1)) * T::VT;
+    const double vc = V0[cell];
+    double D = fma(g.wc, vc, g.w[DIM - 1] * (vst[((p - 1) & (kRV - 1)) * T::VT + cell] +
+                                             vst[((p + 1) & (kRV - 1)) * T::VT + cell]));
+    if (DIM >= 2) D = fma(g.w[0], V0[cell - 1] + V0[cell + 1], D);
+    if (DIM == 3) D = fma(g.w[1], V0[cell - T::HX] + V0[cell + T::HX], D);
+    const double* C0 = cst + ((z - zb) & (kRG - 1)) * 4 * T::NT + t;
+    const double base = has2 ? fma(a.nu, vc, a.kappa * C0[T::NT]) : a.nu * vc;
+    const double d1 = d1_is_u ? vc : C0[0];
+    const double dk = fma(a.mueta, fma(d1, a.inv_mue1, D), base);
+    if (valid) {
+      const long long i = ip + plane * z;
+      bad_in |= !finite_hi(dk);
+      double vput = dk;
+      if (!LAST) {
+        a.uk[i] = dk;
+      } else {
+        const double gv = C0[2 * T::NT];
+        const double b0 = FIRST ? gv : fma(a.onu, gv, a.okappa * C0[3 * T::NT]);
+        const double o0 = fma(a.cG, dk, b0);
+        a.outv[i] = o0;
+        bad_out |= !finite_hi(o0);
+        guard |= fabs(o0) > 1e6;
+        vput = o0;
+      }
+      if (z == 0 && h.put_lo) h.put_lo[ip] = vput;
+      if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = vput;
+    }
+  }
+  cp_wait<0>();
+  halo_signal(h, zb == 0, ze >= g.nzl);
+  if (skip) return;
+  const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
+  if (bad_in) atomicMin(a.event, base + a.k);
+  if (LAST && bad_out) atomicMin(a.event, base + a.m + 1);
+  if (LAST && a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+}
+
+// ---------------------------------------------------------------------------
 // V-only inner stage k >= 2 (LAST: k == m, forms V of g_j).
 // ---------------------------------------------------------------------------
 template <int DIM, int LAST, int FIRST>
@@ -1092,6 +1204,38 @@ cudaError_t launch_node_pipe(const Geom& g, const Halo& h, const FastArgs& a, bo
     return first ? launch_pipe_t<2, 1, 0>(g, h, a, st) : launch_pipe_t<2, 0, 0>(g, h, a, st);
   }
   return launch_node_fast(g, h, a, ion, st);
+}
+
+template <int D, int L, int F>
+static cudaError_t launch_vin_pipe_t(const Geom& g, const Halo& h, const FastInnerArgs& a,
+                                     cudaStream_t st) {
+  using T = PipeTile<D>;
+  constexpr size_t smem = vin_smem_bytes<D>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vin_pipe<D, L, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  const int chunks = (g.nzl + a.zc - 1) / a.zc;
+  const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)
+                          : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
+  k_vin_pipe<D, L, F><<<grd, T::NT, smem, st>>>(g, h, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vin_pipe(const Geom& g, const Halo& h, const FastInnerArgs& a,
+                            cudaStream_t st) {
+  const bool last = a.k == a.m, first = a.j == 1;
+  if (g.dim == 3) {
+    if (!last) return launch_vin_pipe_t<3, 0, 0>(g, h, a, st);
+    return first ? launch_vin_pipe_t<3, 1, 1>(g, h, a, st) : launch_vin_pipe_t<3, 1, 0>(g, h, a, st);
+  }
+  if (g.dim == 2) {
+    if (!last) return launch_vin_pipe_t<2, 0, 0>(g, h, a, st);
+    return first ? launch_vin_pipe_t<2, 1, 1>(g, h, a, st) : launch_vin_pipe_t<2, 1, 0>(g, h, a, st);
+  }
+  return launch_vin_fast(g, h, a, st);
 }
 
 cudaError_t launch_vin_fast(const Geom& g, const Halo& h, const FastInnerArgs& a,
