@@ -71,7 +71,7 @@ __device__ __forceinline__ double exp_tab_nc(double x, const double* __restrict_
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   const double v = tab[n & 255] * p;
-  return __hiloint2double(__double2hiint(v) + ((n >> 8) << 20), __double2loint(v));
+  return __hiloint2double(__double2hiint(v) + (n >> 8) * (1 << 20), __double2loint(v));
 }
 
 __device__ __forceinline__ double rcp_fast(double d) {

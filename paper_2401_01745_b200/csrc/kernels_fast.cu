@@ -442,7 +442,7 @@ constexpr int kRV = 8;  // power of two >= 5
 constexpr int kRG = 4;
 
 template <int DIM, int FIRST>
-constexpr size_t pipe_smem_bytes() {
+constexpr size_t pipe_smem_bytes() {  // dynamic part (k_node_persist adds the table)
   using T = PipeTile<DIM>;
   return sizeof(double) * (256 + kRV * T::VT + kRG * 3 * T::NT + (FIRST ? 0 : kRG * 4 * T::NT));
 }
@@ -493,8 +493,8 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     k_node_pipe(const Geom g, const Halo h, const FastArgs a) {
   using T = PipeTile<DIM>;
   extern __shared__ double smem[];
-  double* tab = smem;
-  double* vst = smem + 256;                       // [kRV][VT]
+  __shared__ double tab[256];                     // static: immediate LDS offsets
+  double* vst = smem;                             // [kRV][VT]
   double* gst = vst + kRV * T::VT;                // [kRG][3][NT]
   double* g2s = gst + kRG * 3 * T::NT;            // [kRG][4][NT] (!FIRST)
   const int t = threadIdx.x;
@@ -503,7 +503,6 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     halo_wait(h, zb0 == 0, zb0 + a.zc >= g.nzl);
     if (h.wait_lo || h.wait_hi) __syncthreads();
   }
-  // abort word: uniform per block after the first barrier of the z loop
   __shared__ int skip;
   if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
   {
@@ -521,32 +520,40 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
   const long long nn = g.nn, plane = g.plane;
   const double* G = a.g1;
-  // per-thread copy plan: halo cells t and t + NT of every V stage, and the
-  // thread's own column for the gates (and g_{j-2})
+  // per-thread copy plan, resolved once: halo cells t and t + NT of every V
+  // stage, the thread's own column for the gates (and g_{j-2})
   const long long voff0 = halo_offset<DIM>(g, x0, y0, t);
   const bool has1 = t + T::NT < T::VT;
   const long long voff1 = has1 ? halo_offset<DIM>(g, x0, y0, t + T::NT) : 0;
+  const double* vsrc0 = G + voff0;  // + plane * zz for an interior plane
+  const double* vsrc1 = G + voff1;
   const unsigned sv0 = (unsigned)__cvta_generic_to_shared(vst) + 8u * t;
   const unsigned sg0 = (unsigned)__cvta_generic_to_shared(gst) + 8u * t;
   const unsigned sq0 = (unsigned)__cvta_generic_to_shared(g2s) + 8u * t;
-  const double* gcol = G + nn + ip;
-  const double* qcol = FIRST ? nullptr : a.g2 + ip;
+  const double* gz0 = G + nn + ip;    // gate columns
+  const double* qz0 = FIRST ? nullptr : a.g2 + ip;
 
   auto load_plane = [&](int zz) {
     const unsigned sv = sv0 + 8u * T::VT * ((zz - zb + 1) & (kRV - 1));
-    const double* vp = vplane(g, h, G, zz);
-    cp_async8(sv, vp + voff0);
-    if (has1) cp_async8(sv + 8u * T::NT, vp + voff1);
+    if (zz >= 0 && zz < g.nzl) {
+      const long long o = plane * zz;
+      cp_async8(sv, vsrc0 + o);
+      if (has1) cp_async8(sv + 8u * T::NT, vsrc1 + o);
+    } else {  // outside the slab: mirror plane or ghost plane (first/last chunk only)
+      const double* vp = vplane(g, h, G, zz);
+      cp_async8(sv, vp + voff0);
+      if (has1) cp_async8(sv + 8u * T::NT, vp + voff1);
+    }
     if (zz >= zb && zz < ze) {
       const unsigned s = (unsigned)((zz - zb) & (kRG - 1));
       const unsigned sg = sg0 + 8u * 3 * T::NT * s;
-      const double* gp = gcol + plane * zz;
+      const double* gp = gz0 + plane * zz;
       cp_async8(sg, gp);
       cp_async8(sg + 8u * T::NT, gp + nn);
       cp_async8(sg + 16u * T::NT, gp + 2 * nn);
       if (!FIRST) {
         const unsigned sq = sq0 + 8u * 4 * T::NT * s;
-        const double* qp = qcol + plane * zz;
+        const double* qp = qz0 + plane * zz;
         cp_async8(sq, qp);
         cp_async8(sq + 8u * T::NT, qp + nn);
         cp_async8(sq + 16u * T::NT, qp + 2 * nn);
@@ -559,14 +566,21 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   load_plane(zb - 1);
   load_plane(zb);
   load_plane(zb + 1);
-  const bool scol = valid && stim_col_xy<DIM>(g, cx, cy);
+  __syncthreads();  // publishes `skip`
+  const bool skipped = skip != 0;
+  // stimulus rows of this column: z in [zs0, zs1] (P/src/monodomain.cpp:151-158)
+  int zs0 = 1, zs1 = 0;
+  if (valid && stim_col_xy<DIM>(g, cx, cy)) {
+    zs0 = g.st_lo[DIM - 1] - g.zoff;
+    zs1 = g.st_hi[DIM - 1] - g.zoff;
+  }
   bool bad = false, guard = false;
   unsigned slow_mask = 0;  // planes (z - zb < 32) left to the reference path
   double glo = 2.0, ghi = -1.0;
   const int cell = (DIM == 3 ? (ty + 1) * T::HX : 0) + tx + 1;
   double* po = a.out + ip + plane * zb;
   double* pu = ION ? a.u1 + ip + plane * zb : nullptr;
-  for (int z = zb; z < ze; ++z) {
+  for (int z = zb; z < ze && !skipped; ++z) {
     if (z + 2 <= ze) {
       load_plane(z + 2);
     } else {
@@ -574,7 +588,6 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     }
     cp_wait<1>();
     __syncthreads();
-    if (skip) break;  // uniform: an earlier step aborted
     const int p = z - zb + 1;
     const double* V0 = vst + (p & (kRV - 1)) * T::VT;
     const double vc = V0[cell];
@@ -585,14 +598,17 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     if (DIM == 3) ys = V0[cell - T::HX] + V0[cell + T::HX];
     const double* G0 = gst + ((z - zb) & (kRG - 1)) * 3 * T::NT + t;
     const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
-    const double stim = (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0;
     // |V| beyond the fast path's range (or non-finite): deferred to the
     // reference-order path after the loop, so the hot loop has no call
     const bool fast = fabs(vc) <= a.vfast;
     if (!fast) slow_mask |= 1u << (z - zb);
-    const NodeOut r = node_update_s<DIM, FIRST, ION, 0>(
-        g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, stim,
+    NodeOut r = node_update_s<DIM, FIRST, ION, 0>(
+        g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, 0.0,
         g2s + ((z - zb) & (kRG - 1)) * 4 * T::NT + t, T::NT);
+    if (z >= zs0 && z <= zs1) {  // stimulus (rare): fs gains +stim
+      if (ION) r.o0 = fma(a.mue1, a.stim, r.o0);
+      else r.o0 = fma(a.cV, a.stim, r.o0);
+    }
     if (valid && fast) {
       po[nn] = r.o1;
       po[2 * nn] = r.o2;
@@ -620,7 +636,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     if (ION) pu += plane;
   }
   cp_wait<0>();
-  if (!skip && valid && slow_mask) {
+  if (!skipped && valid && slow_mask) {
     // deferred nodes: reference-order ionic path, inputs from global memory
     const Nbr<DIM> o = nbr_of<DIM>(g, Col<DIM>{cx, cy, ip, zb, ze, true});
     for (int z = zb; z < ze; ++z) {
@@ -632,7 +648,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
       double xs = 0.0, ys = 0.0;
       if (DIM >= 2) xs = __ldg(G + i + o.xm) + __ldg(G + i + o.xp);
       if (DIM == 3) ys = __ldg(G + i + o.ym) + __ldg(G + i + o.yp);
-      const double stim = (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0;
+      const double stim = (z >= zs0 && z <= zs1) ? a.stim : 0.0;
       double q[4] = {0.0, 0.0, 0.0, 0.0};
       if (!FIRST)
         for (int f = 0; f < 4; ++f) q[f] = __ldg(a.g2 + f * nn + i);
@@ -658,7 +674,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     }
   }
   halo_signal(h, zb == 0, ze >= g.nzl);  // also when skipping: release the neighbours
-  if (skip) return;
+  if (skipped) return;
   if (bad) {
     Col<DIM> c;
     c.c0 = cx;
@@ -676,19 +692,53 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, valid && ze > zb);
 }
 
-// ---------------------------------------------------------------------------
-// k_node_persist: persistent form of k_node_pipe. The grid is sized to the
-// resident capacity; each block walks work items (tile, z-chunk) round-robin
-// and streams all of them through ONE continuous cp.async ring, so the
-// pipeline fill, the exp-table load and the abort-word check are paid once
-// per block instead of once per chunk, and the next item's planes load
-// while the current item's last planes compute.
-//
-// Sequences: item k contributes V loads for planes zb-1 .. ze (zc+2 loads)
-// and computes planes zb .. ze-1. Before computing a plane the block has
-// issued every load up to one past the planes it reads; ring depths V 8,
-// gates 4 keep every slot's rewrite behind a __syncthreads.
-// ---------------------------------------------------------------------------
+// Loader state of one work item (prepared outside the inner loop).
+struct PLoad {
+  long long voff0, voff1;   // halo cells t and t + NT of the tile
+  const double* gcol;       // gate 0 of the thread's column
+  const double* qcol;       // g_{j-2} of the thread's column
+  int zz, zb, ze;           // next plane to load, item planes
+  int live;                 // 0: past the last item
+};
+
+template <int DIM>
+__device__ __forceinline__ void item_geom(int it, int nchunk, int tiles_x, int zc, int nzl,
+                                          int& x0, int& y0, int& zb, int& ze) {
+  using T = PipeTile<DIM>;
+  const int chunk = it % nchunk;
+  const int tile = it / nchunk;
+  x0 = (tile % tiles_x) * T::TX;
+  y0 = DIM == 3 ? (tile / tiles_x) * T::TY : 0;
+  zb = chunk * zc;
+  ze = min(nzl, zb + zc);
+}
+
+template <int DIM, int FIRST>
+__device__ __noinline__ PLoad prep_item(const Geom& g, const Halo& h, const FastArgs& a, int it,
+                                        int items, int nchunk, int tiles_x, int t) {
+  using T = PipeTile<DIM>;
+  PLoad L;
+  L.live = it < items;
+  if (!L.live) {
+    L.voff0 = L.voff1 = 0;
+    L.gcol = L.qcol = nullptr;
+    L.zz = L.zb = L.ze = 0;
+    return L;
+  }
+  int x0, y0;
+  item_geom<DIM>(it, nchunk, tiles_x, a.zc, g.nzl, x0, y0, L.zb, L.ze);
+  L.zz = L.zb - 1;
+  L.voff0 = halo_offset<DIM>(g, x0, y0, t);
+  L.voff1 = (t + T::NT < T::VT) ? halo_offset<DIM>(g, x0, y0, t + T::NT) : 0;
+  const int tx = t % T::TX, ty = t / T::TX;
+  const int cx = x0 + tx, cy = y0 + ty;
+  const bool v = cx < g.n0 && (DIM == 2 || cy < g.n1);
+  const long long ip = v ? (long long)cx + (long long)g.n0 * cy : 0;
+  L.gcol = a.g1 + g.nn + ip;
+  L.qcol = FIRST ? nullptr : a.g2 + ip;
+  return L;
+}
+
 template <int DIM, int FIRST, int ION>
 __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     k_node_persist(const Geom g, const Halo h, const FastArgs a, const int items,
@@ -716,164 +766,195 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   const unsigned sq0 = (unsigned)__cvta_generic_to_shared(g2s) + 8u * t;
   const bool has1 = t + T::NT < T::VT;
   const int cell = (DIM == 3 ? (ty + 1) * T::HX : 0) + tx + 1;
-
-  // ---- loader state (the item being loaded may run ahead of compute)
-  int l_item = blockIdx.x;  // item index
-  int l_zz = 0;             // next plane to load within l_item (local z)
-  int l_q = 0;              // V load sequence number
-  int l_c = 0;              // gate (compute-plane) sequence number
-  int l_x0 = 0, l_y0 = 0, l_zb = 0, l_ze = 0;
-  long long l_voff0 = 0, l_voff1 = 0;
-  const double* l_gcol = nullptr;
-  const double* l_qcol = nullptr;
-  auto item_geom = [&](int it, int& x0, int& y0, int& zb, int& ze) {
-    const int chunk = it % nchunk;
-    const int tile = it / nchunk;
-    x0 = (tile % tiles_x) * T::TX;
-    y0 = DIM == 3 ? (tile / tiles_x) * T::TY : 0;
-    zb = chunk * a.zc;
-    ze = min(g.nzl, zb + a.zc);
+  auto faces = [&](const PLoad& L, bool& lo, bool& hi) {
+    lo = L.live && L.zb == 0 && h.wait_lo;
+    hi = L.live && L.ze >= g.nzl && h.wait_hi;
   };
-  auto l_begin = [&]() {
-    if (l_item >= items) return;
-    item_geom(l_item, l_x0, l_y0, l_zb, l_ze);
-    l_zz = l_zb - 1;
-    l_voff0 = halo_offset<DIM>(g, l_x0, l_y0, t);
-    l_voff1 = has1 ? halo_offset<DIM>(g, l_x0, l_y0, t + T::NT) : 0;
-    const int cx = l_x0 + tx, cy = l_y0 + ty;
-    const bool v = cx < g.n0 && (DIM == 2 || cy < g.n1);
-    const long long ip = v ? (long long)cx + (long long)g.n0 * cy : 0;
-    l_gcol = G + nn + ip;
-    l_qcol = FIRST ? nullptr : a.g2 + ip;
-    // ghost planes of a slab face: wait for the neighbour's arrival
-    const bool need_lo = l_zb == 0 && h.wait_lo, need_hi = l_ze >= g.nzl && h.wait_hi;
-    if (need_lo || need_hi) {
-      halo_wait(h, need_lo, need_hi);
+
+  int q = 0, c = 0;  // V / gate load sequence numbers
+  // issues the next plane of L (one commit group per call); returns false
+  // when L is exhausted (the caller switches L to the next item)
+  auto issue = [&](PLoad& L) {
+    const unsigned sv = sv0 + 8u * T::VT * (q & (kRV - 1));
+    const double* vp = vplane(g, h, G, L.zz);
+    cp_async8(sv, vp + L.voff0);
+    if (has1) cp_async8(sv + 8u * T::NT, vp + L.voff1);
+    if (L.zz >= L.zb && L.zz < L.ze) {
+      const unsigned s = (unsigned)(c & (kRG - 1));
+      const unsigned sg = sg0 + 8u * 3 * T::NT * s;
+      const double* gp = L.gcol + plane * L.zz;
+      cp_async8(sg, gp);
+      cp_async8(sg + 8u * T::NT, gp + nn);
+      cp_async8(sg + 16u * T::NT, gp + 2 * nn);
+      if (!FIRST) {
+        const unsigned sq = sq0 + 8u * 4 * T::NT * s;
+        const double* qp = L.qcol + plane * L.zz;
+        cp_async8(sq, qp);
+        cp_async8(sq + 8u * T::NT, qp + nn);
+        cp_async8(sq + 16u * T::NT, qp + 2 * nn);
+        cp_async8(sq + 24u * T::NT, qp + 3 * nn);
+      }
+      ++c;
+    }
+    ++q;
+    ++L.zz;
+  };
+
+  PLoad ld = prep_item<DIM, FIRST>(g, h, a, blockIdx.x, items, nchunk, tiles_x, t);
+  {
+    bool lo, hi;
+    faces(ld, lo, hi);
+    if (lo || hi) {
+      halo_wait(h, lo, hi);
       __syncthreads();
     }
-  };
-  // issues the next V plane (and its gates); one commit group per call
-  auto l_next = [&]() {
-    if (l_item < items) {
-      const unsigned sv = sv0 + 8u * T::VT * (l_q & (kRV - 1));
-      const double* vp = vplane(g, h, G, l_zz);
-      cp_async8(sv, vp + l_voff0);
-      if (has1) cp_async8(sv + 8u * T::NT, vp + l_voff1);
-      if (l_zz >= l_zb && l_zz < l_ze) {
-        const unsigned s = (unsigned)(l_c & (kRG - 1));
-        const unsigned sg = sg0 + 8u * 3 * T::NT * s;
-        const double* gp = l_gcol + plane * l_zz;
-        cp_async8(sg, gp);
-        cp_async8(sg + 8u * T::NT, gp + nn);
-        cp_async8(sg + 16u * T::NT, gp + 2 * nn);
-        if (!FIRST) {
-          const unsigned sq = sq0 + 8u * 4 * T::NT * s;
-          const double* qp = l_qcol + plane * l_zz;
-          cp_async8(sq, qp);
-          cp_async8(sq + 8u * T::NT, qp + nn);
-          cp_async8(sq + 16u * T::NT, qp + 2 * nn);
-          cp_async8(sq + 24u * T::NT, qp + 3 * nn);
-        }
-        ++l_c;
-      }
-      ++l_q;
-      if (++l_zz > l_ze) {
-        l_item += gridDim.x;
-        l_begin();
-      }
-    }
+  }
+  PLoad nx = prep_item<DIM, FIRST>(g, h, a, blockIdx.x + gridDim.x, items, nchunk, tiles_x, t);
+  for (int r = 0; r < 3; ++r) {
+    if (ld.live) issue(ld);
     cp_commit();
-  };
-
+  }
   bool bad = false, guard = false, any = false;
   double glo = 2.0, ghi = -1.0;
-  int c_q = 1;  // V sequence number of the plane being computed
-  int c_c = 0;  // gate sequence number of the plane being computed
-  l_begin();
-  l_next();  // zb - 1
-  l_next();  // zb
-  l_next();  // zb + 1
+  int cq = 1, cc = 0;  // sequence numbers of the plane being computed
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
     int x0, y0, zb, ze;
-    item_geom(it, x0, y0, zb, ze);
+    item_geom<DIM>(it, nchunk, tiles_x, a.zc, g.nzl, x0, y0, zb, ze);
     const int cx = x0 + tx, cy = y0 + ty;
     const bool valid = cx < g.n0 && (DIM == 2 || cy < g.n1);
     const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
     const bool scol = valid && stim_col_xy<DIM>(g, cx, cy);
     double* po = a.out + ip + plane * zb;
     double* pu = ION ? a.u1 + ip + plane * zb : nullptr;
+    unsigned slow_mask = 0;
     for (int z = zb; z < ze; ++z) {
-      l_next();  // V sequence c_q + 2
-      cp_wait<1>();  // everything up to c_q + 1 (this plane's vp) has landed
+      // keep the loader two planes ahead; it crosses into the next item
+      // (prepared outside this loop) when the current one is exhausted
+      if (ld.zz > ld.ze) {
+        ld = nx;
+        nx.live = 0;
+      }
+      if (ld.live) issue(ld);
+      cp_commit();
+      cp_wait<1>();
       __syncthreads();
       if (skip) break;
-      const double* V0 = vst + (c_q & (kRV - 1)) * T::VT;
+      const double* V0 = vst + (cq & (kRV - 1)) * T::VT;
       const double vc = V0[cell];
-      const double vm = vst[((c_q - 1) & (kRV - 1)) * T::VT + cell];
-      const double vp = vst[((c_q + 1) & (kRV - 1)) * T::VT + cell];
+      const double vm = vst[((cq - 1) & (kRV - 1)) * T::VT + cell];
+      const double vp = vst[((cq + 1) & (kRV - 1)) * T::VT + cell];
       double xs = 0.0, ys = 0.0;
       if (DIM >= 2) xs = V0[cell - 1] + V0[cell + 1];
       if (DIM == 3) ys = V0[cell - T::HX] + V0[cell + T::HX];
-      const double* G0 = gst + (c_c & (kRG - 1)) * 3 * T::NT + t;
+      const double* G0 = gst + (cc & (kRG - 1)) * 3 * T::NT + t;
       const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
       const double stim = (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0;
-      const NodeOut r = node_update_s<DIM, FIRST, ION>(
+      const bool fast = fabs(vc) <= a.vfast;
+      if (!fast) slow_mask |= 1u << (z - zb);
+      const NodeOut rr = node_update_s<DIM, FIRST, ION, 0>(
           g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, stim,
-          g2s + (c_c & (kRG - 1)) * 4 * T::NT + t, T::NT);
-      if (valid) {
-        po[nn] = r.o1;
-        po[2 * nn] = r.o2;
-        po[3 * nn] = r.o3;
+          g2s + (cc & (kRG - 1)) * 4 * T::NT + t, T::NT);
+      if (valid && fast) {
+        po[nn] = rr.o1;
+        po[2 * nn] = rr.o2;
+        po[3 * nn] = rr.o3;
         if (ION) {
-          *pu = r.o0;
+          *pu = rr.o0;
         } else {
-          *po = r.o0;
-          guard |= fabs(r.o0) > 1e6;
+          *po = rr.o0;
+          guard |= fabs(rr.o0) > 1e6;
         }
-        bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
-        if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
-        if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
+        bad |= !finite_hi((rr.o0 + rr.o1) + (rr.o2 + rr.o3));
+        if (z == 0 && h.put_lo) h.put_lo[ip] = rr.o0;
+        if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = rr.o0;
         if (a.last) {
-          const double mn = r.o1 < r.o2 ? r.o1 : r.o2;
-          const double mx = r.o1 < r.o2 ? r.o2 : r.o1;
+          const double mn = rr.o1 < rr.o2 ? rr.o1 : rr.o2;
+          const double mx = rr.o1 < rr.o2 ? rr.o2 : rr.o1;
           glo = mn < glo ? mn : glo;
           ghi = mx > ghi ? mx : ghi;
-          glo = r.o3 < glo ? r.o3 : glo;
-          ghi = r.o3 > ghi ? r.o3 : ghi;
+          glo = rr.o3 < glo ? rr.o3 : glo;
+          ghi = rr.o3 > ghi ? rr.o3 : ghi;
           any = true;
         }
       }
       po += plane;
       if (ION) pu += plane;
-      ++c_q;
-      ++c_c;
+      ++cq;
+      ++cc;
     }
-    if (skip) {
-      // keep the neighbour protocol alive, then stop
-      halo_signal(h, zb == 0, ze >= g.nzl);
-      for (int j = it + gridDim.x; j < items; j += gridDim.x) {
+    if (skip) {  // keep the neighbour protocol alive, then stop
+      for (int j = it; j < items; j += gridDim.x) {
         int a0, a1, b0, b1;
-        item_geom(j, a0, a1, b0, b1);
+        item_geom<DIM>(j, nchunk, tiles_x, a.zc, g.nzl, a0, a1, b0, b1);
         halo_signal(h, b0 == 0, b1 >= g.nzl);
       }
       break;
     }
-    c_q += 2;  // past this item's plane ze and the next item's zb - 1
-    l_next();  // an item loads two planes more than it computes: keep the
-    l_next();  // loader two ahead across the boundary
+    cq += 2;  // past this item's plane ze and the next item's zb - 1
+    // the two extra planes of the next item (its zb - 1 and zb)
+    for (int r = 0; r < 2; ++r) {
+      if (ld.zz > ld.ze) {
+        ld = nx;
+        nx.live = 0;
+      }
+      if (ld.live) issue(ld);
+      cp_commit();
+    }
+    if (valid && slow_mask) {
+      // deferred nodes: reference-order ionic path from global memory
+      const Nbr<DIM> o = nbr_of<DIM>(g, Col<DIM>{cx, cy, ip, zb, ze, true});
+      for (int z = zb; z < ze; ++z) {
+        if (!(slow_mask >> (z - zb) & 1u)) continue;
+        const long long i = ip + plane * z;
+        const double vc = __ldg(G + i);
+        double xs = 0.0, ys = 0.0;
+        if (DIM >= 2) xs = __ldg(G + i + o.xm) + __ldg(G + i + o.xp);
+        if (DIM == 3) ys = __ldg(G + i + o.ym) + __ldg(G + i + o.yp);
+        double qv[4] = {0.0, 0.0, 0.0, 0.0};
+        if (!FIRST)
+          for (int f = 0; f < 4; ++f) qv[f] = __ldg(a.g2 + f * nn + i);
+        const NodeOut rr = node_update_s<DIM, FIRST, ION, 1>(
+            g, a, tab, zval(G, g, ip, z - 1, h.lo, h.hi), vc, zval(G, g, ip, z + 1, h.lo, h.hi),
+            xs, ys, __ldg(G + nn + i), __ldg(G + 2 * nn + i), __ldg(G + 3 * nn + i),
+            (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0, qv, 1);
+        a.out[nn + i] = rr.o1;
+        a.out[2 * nn + i] = rr.o2;
+        a.out[3 * nn + i] = rr.o3;
+        if (ION) {
+          a.u1[i] = rr.o0;
+        } else {
+          a.out[i] = rr.o0;
+          guard |= fabs(rr.o0) > 1e6;
+        }
+        bad |= !finite_hi((rr.o0 + rr.o1) + (rr.o2 + rr.o3));
+        if (z == 0 && h.put_lo) h.put_lo[ip] = rr.o0;
+        if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = rr.o0;
+        if (a.last) {
+          glo = fmin(glo, fmin(rr.o1, fmin(rr.o2, rr.o3)));
+          ghi = fmax(ghi, fmax(rr.o1, fmax(rr.o2, rr.o3)));
+          any = true;
+        }
+      }
+    }
     halo_signal(h, zb == 0, ze >= g.nzl);
     if (bad) {
-      Col<DIM> c;
-      c.c0 = cx;
-      c.c1 = cy;
-      c.ip = ip;
-      c.z0 = zb;
-      c.z1 = ze;
-      c.valid = true;
-      const bool inner = valid && inner_nonfinite<DIM>(g, h, G, c, nbr_of<DIM>(g, c), a.eta);
+      const bool inner = valid && inner_nonfinite<DIM>(g, h, G, Col<DIM>{cx, cy, ip, zb, ze, true},
+                                                       nbr_of<DIM>(g, Col<DIM>{cx, cy, ip, zb, ze, true}),
+                                                       a.eta);
       atomicMin(a.event, a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1)) +
                              (inner ? 1 : a.m + 1));
       bad = false;
+    }
+    // prepare the item after the one the loader is on (outside the hot loop)
+    if (!nx.live) {
+      const int nxt = it + 2 * gridDim.x;
+      nx = prep_item<DIM, FIRST>(g, h, a, nxt, items, nchunk, tiles_x, t);
+      bool lo, hi;
+      faces(nx, lo, hi);
+      if (lo || hi) {
+        halo_wait(h, lo, hi);
+        __syncthreads();
+      }
     }
   }
   cp_wait<0>();
@@ -927,11 +1008,19 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
   const bool has2 = a.um2 != nullptr;
   const bool d1_is_u = a.um1 == a.d1;  // k == 2: d_1 is the stencil field itself
 
+  const double* usrc0 = U + voff0;
+  const double* usrc1 = U + voff1;
   auto load_plane = [&](int zz) {
     const unsigned sv = sv0 + 8u * T::VT * ((zz - zb + 1) & (kRV - 1));
-    const double* vp = vplane(g, h, U, zz);
-    cp_async8(sv, vp + voff0);
-    if (has1) cp_async8(sv + 8u * T::NT, vp + voff1);
+    if (zz >= 0 && zz < g.nzl) {
+      const long long o = plane * zz;
+      cp_async8(sv, usrc0 + o);
+      if (has1) cp_async8(sv + 8u * T::NT, usrc1 + o);
+    } else {
+      const double* vp = vplane(g, h, U, zz);
+      cp_async8(sv, vp + voff0);
+      if (has1) cp_async8(sv + 8u * T::NT, vp + voff1);
+    }
     if (zz >= zb && zz < ze) {
       const unsigned sc = sc0 + 8u * 4 * T::NT * ((zz - zb) & (kRG - 1));
       const long long i = ip + plane * zz;
@@ -947,14 +1036,15 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
   load_plane(zb - 1);
   load_plane(zb);
   load_plane(zb + 1);
+  __syncthreads();  // publishes `skip`
+  const bool skipped = skip != 0;
   bool bad_in = false, bad_out = false, guard = false;
   const int cell = (DIM == 3 ? (ty + 1) * T::HX : 0) + tx + 1;
-  for (int z = zb; z < ze; ++z) {
+  for (int z = zb; z < ze && !skipped; ++z) {
     if (z + 2 <= ze) load_plane(z + 2);
     else cp_commit();
     cp_wait<1>();
     __syncthreads();
-    if (skip) break;
     const int p = z - zb + 1;
     const double* V0 = vst + (p & (kRV - 1)) * T::VT;
     const double vc = V0[cell];
@@ -987,7 +1077,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
   }
   cp_wait<0>();
   halo_signal(h, zb == 0, ze >= g.nzl);
-  if (skip) return;
+  if (skipped) return;
   const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
   if (bad_in) atomicMin(a.event, base + a.k);
   if (LAST && bad_out) atomicMin(a.event, base + a.m + 1);
