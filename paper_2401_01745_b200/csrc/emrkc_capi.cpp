@@ -7,7 +7,9 @@
 // in the same evaluation order so that s, m, eta and every coefficient are
 // bit-identical; all per-node work runs in kernels.cu. There is no CPU
 // fallback: without a device every compute call fails with EMRKC_ECUDA.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -267,6 +269,13 @@ struct emrkc_handle {
   bool plan_uploaded = false;
   int fast = 1;
   int pipe = 1;
+  // TMA descriptors (pipe == 3), encoded on first use per (pointer, kind)
+  struct TmaEntry {
+    const void* ptr;
+    int kind;
+    CUtensorMap map;
+  };
+  std::vector<TmaEntry> tmaps;
   int zc = 1;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::string err;
@@ -434,6 +443,91 @@ void begin_step(emrkc_handle* h, double t, long long step_in_run,
   for (int k = 0; k < 3; ++k) a.u[k] = h->u[k];
 }
 
+// ---- TMA descriptors -------------------------------------------------------
+// Tensor maps over the SoA state (P/include/mrkc/monodomain.hpp:51-60 layout):
+// spatial dims (n0, n1, nzl) [2-D: (n0, nzl)], plus the field axis of stride
+// nn for the gate boxes. Encoded through the driver entry point (no -lcuda).
+enum TmaKind { kTmaHalo = 0, kTmaCenter = 1, kTmaGates = 2, kTmaAll = 3, kTmaGhost = 4 };
+
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// TMA needs 16-byte global strides (n0 even) and a 2-D or 3-D grid.
+bool tma_supported(const emrkc_handle* h) {
+  return h->geom.dim >= 2 && h->geom.n0 % 2 == 0 && tma_encoder() != nullptr;
+}
+
+int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out) {
+  for (const auto& e : h->tmaps)
+    if (e.ptr == ptr && e.kind == kind) {
+      *out = e.map;
+      return EMRKC_OK;
+    }
+  const Geom& g = h->geom;
+  const bool d3 = g.dim == 3;
+  const cuuint32_t tx = d3 ? emrkc_k::kTX3 : emrkc_k::kTX2, ty = d3 ? emrkc_k::kTY3 : 1;
+  const bool halo = kind == kTmaHalo || kind == kTmaGhost;
+  cuuint64_t dims[4];
+  cuuint64_t strides[3];
+  cuuint32_t box[4], es[4] = {1, 1, 1, 1};
+  cuuint32_t rank = 0;
+  dims[rank] = static_cast<cuuint64_t>(g.n0);
+  box[rank++] = halo ? tx + 4 : tx;  // x0-2 .. x0+tx+1: 16-byte aligned start
+  if (d3) {
+    strides[rank - 1] = sizeof(double) * static_cast<cuuint64_t>(g.n0);
+    dims[rank] = static_cast<cuuint64_t>(g.n1);
+    box[rank++] = halo ? ty + 2 : ty;
+  }
+  if (kind != kTmaGhost) {
+    strides[rank - 1] = sizeof(double) * static_cast<cuuint64_t>(g.plane);
+    dims[rank] = static_cast<cuuint64_t>(g.nzl);
+    box[rank++] = 1;
+  }
+  if (kind == kTmaGates || kind == kTmaAll) {
+    strides[rank - 1] = sizeof(double) * static_cast<cuuint64_t>(g.nn);
+    dims[rank] = 4;
+    box[rank++] = kind == kTmaGates ? 3 : 4;
+  }
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
+    return set_err(h, EMRKC_ECUDA, "TMA: buffer %p not 16-byte aligned", ptr);
+  CUtensorMap m;
+  const CUresult r = tma_encoder()(
+      &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(ptr), dims, strides, box, es,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(h, EMRKC_ECUDA, "cuTensorMapEncodeTiled failed (%d, kind %d)", (int)r, kind);
+  h->tmaps.push_back({ptr, kind, m});
+  *out = m;
+  return EMRKC_OK;
+}
+
+int tma_ghosts(emrkc_handle* h, const Halo& hl, CUtensorMap* lo, CUtensorMap* hi) {
+  std::memset(lo, 0, sizeof *lo);
+  std::memset(hi, 0, sizeof *hi);
+  if (hl.lo) {
+    const int rc = tma_map(h, hl.lo, kTmaGhost, lo);
+    if (rc) return rc;
+  }
+  if (hl.hi) {
+    const int rc = tma_map(h, hl.hi, kTmaGhost, hi);
+    if (rc) return rc;
+  }
+  return EMRKC_OK;
+}
+
 // Launches inner stage k (1..m) of outer stage j (1..s).
 int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
   const Plan& pl = h->plan;
@@ -478,7 +572,16 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.code_base = a.code_base;
       f.event = a.event;
       f.gate_slot = a.gate_slot;
-      if (h->pipe == 2)
+      if (h->pipe == 3) {
+        emrkc_k::TmaNode tm;
+        int rc = tma_map(h, f.g1, kTmaHalo, &tm.v);
+        if (!rc) rc = tma_map(h, f.g1, kTmaGates, &tm.gates);
+        if (!rc && f.g2) rc = tma_map(h, f.g2, kTmaAll, &tm.g2);
+        if (!f.g2) std::memset(&tm.g2, 0, sizeof tm.g2);
+        if (!rc) rc = tma_ghosts(h, hl, &tm.glo, &tm.ghi);
+        if (rc) return rc;
+        CK(h, emrkc_k::launch_node_tma(h->geom, hl, f, tm, pl.m >= 2, h->stream));
+      } else if (h->pipe == 2)
         CK(h, emrkc_k::launch_node_persist(h->geom, hl, f, pl.m >= 2, h->stream));
       else if (h->pipe)
         CK(h, emrkc_k::launch_node_pipe(h->geom, hl, f, pl.m >= 2, h->stream));
@@ -511,7 +614,18 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.zc = h->zc;
       f.code_base = a.code_base;
       f.event = a.event;
-      if (h->pipe)
+      if (h->pipe == 3) {
+        emrkc_k::TmaVin tm;
+        std::memset(&tm, 0, sizeof tm);
+        int rc = tma_map(h, f.um1, kTmaHalo, &tm.u);
+        if (!rc) rc = tma_map(h, f.d1, kTmaCenter, &tm.d1);
+        if (!rc && f.um2) rc = tma_map(h, f.um2, kTmaCenter, &tm.um2);
+        if (!rc && k == pl.m) rc = tma_map(h, f.g1v, kTmaCenter, &tm.g1v);
+        if (!rc && k == pl.m && f.g2v) rc = tma_map(h, f.g2v, kTmaCenter, &tm.g2v);
+        if (!rc) rc = tma_ghosts(h, hl, &tm.glo, &tm.ghi);
+        if (rc) return rc;
+        CK(h, emrkc_k::launch_vin_tma(h->geom, hl, f, tm, h->stream));
+      } else if (h->pipe)
         CK(h, emrkc_k::launch_vin_pipe(h->geom, hl, f, h->stream));
       else
         CK(h, emrkc_k::launch_vin_fast(h->geom, hl, f, h->stream));
@@ -611,7 +725,9 @@ int init_handle(emrkc_handle* h) {
   h->fast = f ? std::atoi(f) : 1;
   h->zc = emrkc_k::fast_zc(h->geom);
   const char* pp = std::getenv("EMRKC_PIPE");
-  h->pipe = (pp && *pp) ? std::atoi(pp) : 1;  // 1: per-chunk blocks, 2: persistent, 0: march
+  // 3: TMA-staged blocks, 1: cp.async-staged blocks, 2: persistent, 0: march
+  h->pipe = (pp && *pp) ? std::atoi(pp) : 3;
+  if (h->pipe == 3 && !tma_supported(h)) h->pipe = 1;
   if (const char* zc = std::getenv("EMRKC_ZC"))
     if (*zc) h->zc = std::max(1, std::atoi(zc));
   return EMRKC_OK;

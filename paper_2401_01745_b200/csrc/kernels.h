@@ -4,6 +4,7 @@
 
 #include <cstdint>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace emrkc_k {
@@ -105,6 +106,27 @@ struct FastInnerArgs {
   unsigned long long* event;
 };
 
+// TMA descriptors of one k_node_tma launch (host-encoded, passed as a
+// __grid_constant__ parameter). Boxes: V tile + 1-cell halo, gate fields,
+// g_{j-2} fields, ghost planes.
+struct TmaNode {
+  CUtensorMap v;       // V block of g_{j-1}, box (TX+4, TY+2, 1)
+  CUtensorMap gates;   // all fields of g_{j-1}, box (TX, TY, 1, 3) from field 1
+  CUtensorMap g2;      // all fields of g_{j-2}, box (TX, TY, 1, 4)
+  CUtensorMap glo;     // ghost plane below, box (TX+4, TY+2)
+  CUtensorMap ghi;     // ghost plane above
+};
+struct TmaVin {
+  CUtensorMap u;       // d_{k-1}, box (TX+4, TY+2, 1)
+  CUtensorMap d1;      // center boxes (TX, TY, 1)
+  CUtensorMap um2;
+  CUtensorMap g1v;
+  CUtensorMap g2v;
+  CUtensorMap glo, ghi;
+};
+// Tile shape of the staged kernels (x, y per block; 2-D grids use TX2 x 1).
+constexpr int kTX3 = 32, kTY3 = 4, kTX2 = 128;
+
 int fast_zc(const Geom& g);
 // Signals per level that a neighbour receives from one launch of each kernel
 // family (blocks that hold the boundary plane of their slab).
@@ -121,6 +143,10 @@ cudaError_t launch_node_pipe(const Geom& g, const Halo& h, const FastArgs& a,
                              bool ion, cudaStream_t st);
 cudaError_t launch_node_persist(const Geom& g, const Halo& h, const FastArgs& a,
                                 bool ion, cudaStream_t st);
+cudaError_t launch_node_tma(const Geom& g, const Halo& h, const FastArgs& a,
+                            const TmaNode& tm, bool ion, cudaStream_t st);
+cudaError_t launch_vin_tma(const Geom& g, const Halo& h, const FastInnerArgs& a,
+                           const TmaVin& tm, cudaStream_t st);
 cudaError_t launch_vin_fast(const Geom& g, const Halo& h,
                             const FastInnerArgs& a, cudaStream_t st);
 cudaError_t launch_vin_pipe(const Geom& g, const Halo& h,

@@ -25,7 +25,11 @@
 
 #include "fast_math.cuh"
 #include "hh.cuh"
+#include <cstdlib>
+#include <utility>
+
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace emrkc_k {
 
@@ -498,6 +502,8 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   double* gst = vst + kRV * T::VT;                // [kRG][3][NT]
   double* g2s = gst + kRG * 3 * T::NT;            // [kRG][4][NT] (!FIRST)
   const int t = threadIdx.x;
+  pdl_launch_dependents();
+  pdl_wait();
   {
     const int zb0 = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
     halo_wait(h, zb0 == 0, zb0 + a.zc >= g.nzl);
@@ -983,6 +989,8 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
   double* vst = smem;                  // [kRV][VT]   d_{k-1} with halo
   double* cst = vst + kRV * T::VT;     // [kRG][4][NT] d1, d_{k-2}, V1, V2
   const int t = threadIdx.x;
+  pdl_launch_dependents();
+  pdl_wait();
   {
     const int zb0 = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
     halo_wait(h, zb0 == 0, zb0 + a.zc >= g.nzl);
@@ -1076,6 +1084,412 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
     }
   }
   cp_wait<0>();
+  halo_signal(h, zb == 0, ze >= g.nzl);
+  if (skipped) return;
+  const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
+  if (bad_in) atomicMin(a.event, base + a.k);
+  if (LAST && bad_out) atomicMin(a.event, base + a.m + 1);
+  if (LAST && a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+}
+
+// ---------------------------------------------------------------------------
+// k_node_tma / k_vin_tma: the staged kernels with TMA. Thread 0 issues each
+// plane's bulk tensor copies (V tile + halo, the tile's gates, g_{j-2})
+// two planes ahead; they complete on the plane's mbarrier (transaction
+// bytes), so the compute threads spend no instructions on loading. Halo
+// cells past the grid edge arrive zero-filled: the compute reads the
+// mirrored neighbour there instead (P/src/monodomain.cpp:85-86).
+// ---------------------------------------------------------------------------
+// The box's innermost start coordinate must be 16-byte aligned, so the V
+// box spans x0-2 .. x0+TX+1 (two cells of halo on each side in x).
+// Planes in flight ahead of the computed one. Ring limits: V stages need
+// kTmaLA + 2 <= kRV; gate stages are refilled kTmaLA - 1 planes after their
+// last read (one __syncthreads per plane), so kTmaLA <= kRG.
+#ifndef EMRKC_TMA_LA
+#define EMRKC_TMA_LA 3
+#endif
+constexpr int kTmaLA = EMRKC_TMA_LA;
+static_assert(kTmaLA >= 1 && kTmaLA + 2 <= kRV && kTmaLA <= kRG, "TMA lookahead");
+
+template <int DIM>
+struct TmaTile {
+  using T = PipeTile<DIM>;
+  static constexpr int HX = T::TX + 4;
+  static constexpr int VT = HX * T::HY;           // V cells per stage
+  static constexpr int VS = (VT + 15) & ~15;      // V stage stride (128-byte aligned)
+};
+
+template <int DIM, int FIRST>
+constexpr size_t tma_node_smem_bytes() {
+  using T = PipeTile<DIM>;
+  return sizeof(double) * (kRV * TmaTile<DIM>::VS + kRG * 3 * T::NT +
+                           (FIRST ? 0 : kRG * 4 * T::NT)) + 128;
+}
+
+// Issues the V box of local plane zz (interior, mirror, or ghost).
+template <int DIM>
+__device__ __forceinline__ void tma_vplane(const Geom& g, const CUtensorMap* vmap,
+                                           const CUtensorMap* glo, const CUtensorMap* ghi,
+                                           bool has_lo, bool has_hi, unsigned dst,
+                                           unsigned bar, int x0, int y0, int zz) {
+  int lz = zz;
+  if (zz < 0 || zz >= g.nzl) {
+    int gz = zz + g.zoff;
+    gz = gz < 0 ? 1 : (gz >= g.nzg ? g.nzg - 2 : gz);
+    lz = gz - g.zoff;
+  }
+  if (lz >= 0 && lz < g.nzl) {
+    if (DIM == 3) tma_load_3d(dst, vmap, bar, x0 - 2, y0 - 1, lz);
+    else tma_load_2d(dst, vmap, bar, x0 - 2, lz);
+  } else {
+    const CUtensorMap* gm = lz < 0 ? glo : ghi;
+    if (DIM == 3) tma_load_2d(dst, gm, bar, x0 - 2, y0 - 1);
+    else tma_load_1d(dst, gm, bar, x0 - 2);
+  }
+  (void)has_lo;
+  (void)has_hi;
+}
+
+template <int DIM, int FIRST, int ION>
+__global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
+    k_node_tma(const Geom g, const Halo h, const FastArgs a, const __grid_constant__ TmaNode tm) {
+  using T = PipeTile<DIM>;
+  constexpr int VS = TmaTile<DIM>::VS;
+  extern __shared__ __align__(128) double smem_tma[];
+  // 128-byte aligned stage base (pointer arithmetic keeps the shared space)
+  double* vst = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;  // [kRV][VS]
+  double* gst = vst + kRV * VS;                     // [kRG][3][NT]
+  double* g2s = gst + kRG * 3 * T::NT;              // [kRG][4][NT]
+  __shared__ double tab[256];
+  __shared__ __align__(8) unsigned long long bars[kRV];
+  __shared__ int skip;
+  const int t = threadIdx.x;
+  const int zb = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
+  const int ze = min(g.nzl, zb + a.zc);
+  pdl_launch_dependents();
+  // prologue that reads nothing the previous kernel writes
+  for (int j = t; j < 256; j += T::NT) tab[j] = kExp2Tab256[j];
+  if (t == 0) {
+    for (int s = 0; s < kRV; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    mbar_fence_init();
+    prefetch_tensormap(&tm.v);
+    prefetch_tensormap(&tm.gates);
+    if (!FIRST) prefetch_tensormap(&tm.g2);
+  }
+  pdl_wait();
+  halo_wait(h, zb == 0, ze >= g.nzl);
+  if (t == 0) {
+    // ghost planes arrived through generic peer stores (acquired in
+    // halo_wait); order them before this thread's async-proxy reads
+    fence_proxy_async();
+    skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  }
+  __syncthreads();
+  const bool skipped = skip != 0;
+  const int tx = t % T::TX, ty = t / T::TX;
+  const int x0 = blockIdx.x * T::TX;
+  const int y0 = DIM == 3 ? blockIdx.y * T::TY : 0;
+  const int cx = x0 + tx, cy = y0 + ty;
+  const bool valid = cx < g.n0 && (DIM == 2 || cy < g.n1);
+  const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
+  const long long nn = g.nn, plane = g.plane;
+  const unsigned v0 = smem_u32(vst), gs0 = smem_u32(gst), qs0 = smem_u32(g2s);
+  const unsigned b0 = smem_u32(bars);
+  constexpr unsigned vbytes = 8u * TmaTile<DIM>::VT;
+  const unsigned cbytes = 8u * T::NT * (3 + (FIRST ? 0 : 4));
+  // thread 0: plane zz in [zb, ze) (interior of the slab): V box + gate boxes
+  auto issue_comp = [&](int zz) {
+    const int q = zz - zb + 1;
+    const unsigned bar = b0 + 8u * (q & (kRV - 1));
+    const unsigned vd = v0 + 8u * VS * (q & (kRV - 1));
+    const unsigned sg = (unsigned)((zz - zb) & (kRG - 1));
+    mbar_expect_tx(bar, vbytes + cbytes);
+    if (DIM == 3) {
+      tma_load_3d(vd, &tm.v, bar, x0 - 2, y0 - 1, zz);
+      tma_load_4d(gs0 + 8u * 3 * T::NT * sg, &tm.gates, bar, x0, y0, zz, 1);
+      if (!FIRST) tma_load_4d(qs0 + 8u * 4 * T::NT * sg, &tm.g2, bar, x0, y0, zz, 0);
+    } else {
+      tma_load_2d(vd, &tm.v, bar, x0 - 2, zz);
+      tma_load_3d(gs0 + 8u * 3 * T::NT * sg, &tm.gates, bar, x0, zz, 1);
+      if (!FIRST) tma_load_3d(qs0 + 8u * 4 * T::NT * sg, &tm.g2, bar, x0, zz, 0);
+    }
+  };
+  // thread 0: halo plane zb - 1 or ze (V only; mirror or ghost at the slab edge)
+  auto issue_edge = [&](int zz) {
+    const int q = zz - zb + 1;
+    const unsigned bar = b0 + 8u * (q & (kRV - 1));
+    mbar_expect_tx(bar, vbytes);
+    tma_vplane<DIM>(g, &tm.v, &tm.glo, &tm.ghi, h.lo != nullptr, h.hi != nullptr,
+                    v0 + 8u * VS * (q & (kRV - 1)), bar, x0, y0, zz);
+  };
+  if (!skipped && t == 0) {
+    issue_edge(zb - 1);
+    for (int i = 0; i < kTmaLA; ++i) {
+      if (zb + i < ze) issue_comp(zb + i);
+      else {
+        issue_edge(ze);
+        break;
+      }
+    }
+  }
+  // mirrored in-plane neighbours at the grid edge (halo cells there are 0)
+  constexpr int HXT = TmaTile<DIM>::HX;
+  const int cell = (DIM == 3 ? (ty + 1) * HXT : 0) + tx + 2;
+  const int cxm = cell + (cx > 0 ? -1 : 1), cxp = cell + (cx < g.n0 - 1 ? 1 : -1);
+  const int cym = cell + (cy > 0 ? -HXT : HXT), cyp = cell + (cy < g.n1 - 1 ? HXT : -HXT);
+  int zs0 = 1, zs1 = 0;
+  if (valid && stim_col_xy<DIM>(g, cx, cy)) {
+    zs0 = g.st_lo[DIM - 1] - g.zoff;
+    zs1 = g.st_hi[DIM - 1] - g.zoff;
+  }
+  bool bad = false, guard = false;
+  unsigned slow_mask = 0;
+  double glo = 2.0, ghi = -1.0;
+  double* po = a.out + ip + plane * zb;
+  double* pu = ION ? a.u1 + ip + plane * zb : nullptr;
+  if (!skipped) {
+    mbar_wait(b0, 0);       // plane zb - 1
+    mbar_wait(b0 + 8u, 0);  // plane zb
+  }
+  for (int z = zb; z < ze && !skipped; ++z) {
+    const int p = z - zb + 1;
+    if (t == 0) {
+      if (z + kTmaLA < ze) issue_comp(z + kTmaLA);
+      else if (z + kTmaLA == ze) issue_edge(ze);
+    }
+    mbar_wait(b0 + 8u * ((p + 1) & (kRV - 1)), ((p + 1) >> 3) & 1);
+    const double* V0 = vst + (p & (kRV - 1)) * VS;
+    const double vc = V0[cell];
+    const double vm = vst[((p - 1) & (kRV - 1)) * VS + cell];
+    const double vp = vst[((p + 1) & (kRV - 1)) * VS + cell];
+    double xs = 0.0, ys = 0.0;
+    if (DIM >= 2) xs = V0[cxm] + V0[cxp];
+    if (DIM == 3) ys = V0[cym] + V0[cyp];
+    const double* G0 = gst + ((z - zb) & (kRG - 1)) * 3 * T::NT + t;
+    const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
+    const bool fast = fabs(vc) <= a.vfast;
+    if (!fast) slow_mask |= 1u << (z - zb);
+    NodeOut r = node_update_s<DIM, FIRST, ION, 0>(
+        g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, 0.0,
+        g2s + ((z - zb) & (kRG - 1)) * 4 * T::NT + t, T::NT);
+    if (z >= zs0 && z <= zs1) {
+      if (ION) r.o0 = fma(a.mue1, a.stim, r.o0);
+      else r.o0 = fma(a.cV, a.stim, r.o0);
+    }
+    if (valid && fast) {
+      po[nn] = r.o1;
+      po[2 * nn] = r.o2;
+      po[3 * nn] = r.o3;
+      if (ION) {
+        *pu = r.o0;
+      } else {
+        *po = r.o0;
+        guard |= fabs(r.o0) > 1e6;
+      }
+      bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
+      if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
+      if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
+      if (a.last) {  // select form: fmin / fmax on doubles expand to ~10 instructions
+        const double mn = r.o1 < r.o2 ? r.o1 : r.o2;
+        const double mx = r.o1 < r.o2 ? r.o2 : r.o1;
+        glo = mn < glo ? mn : glo;
+        ghi = mx > ghi ? mx : ghi;
+        glo = r.o3 < glo ? r.o3 : glo;
+        ghi = r.o3 > ghi ? r.o3 : ghi;
+      }
+    }
+    po += plane;
+    if (ION) pu += plane;
+    __syncthreads();  // stage (p - 5) may be refilled next iteration
+  }
+  if (!skipped && valid && slow_mask) {
+    const Nbr<DIM> o = nbr_of<DIM>(g, Col<DIM>{cx, cy, ip, zb, ze, true});
+    const double* G = a.g1;
+    for (int z = zb; z < ze; ++z) {
+      if (!(slow_mask >> (z - zb) & 1u)) continue;
+      const long long i = ip + plane * z;
+      const double vc = __ldg(G + i);
+      const double vm = zval(G, g, ip, z - 1, h.lo, h.hi);
+      const double vp = zval(G, g, ip, z + 1, h.lo, h.hi);
+      double xs = 0.0, ys = 0.0;
+      if (DIM >= 2) xs = __ldg(G + i + o.xm) + __ldg(G + i + o.xp);
+      if (DIM == 3) ys = __ldg(G + i + o.ym) + __ldg(G + i + o.yp);
+      const double stim = (z >= zs0 && z <= zs1) ? a.stim : 0.0;
+      double q[4] = {0.0, 0.0, 0.0, 0.0};
+      if (!FIRST)
+        for (int f = 0; f < 4; ++f) q[f] = __ldg(a.g2 + f * nn + i);
+      const NodeOut r = node_update_s<DIM, FIRST, ION, 1>(
+          g, a, tab, vm, vc, vp, xs, ys, __ldg(G + nn + i), __ldg(G + 2 * nn + i),
+          __ldg(G + 3 * nn + i), stim, q, 1);
+      a.out[nn + i] = r.o1;
+      a.out[2 * nn + i] = r.o2;
+      a.out[3 * nn + i] = r.o3;
+      if (ION) {
+        a.u1[i] = r.o0;
+      } else {
+        a.out[i] = r.o0;
+        guard |= fabs(r.o0) > 1e6;
+      }
+      bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
+      if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
+      if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
+      if (a.last) {
+        glo = fmin(glo, fmin(r.o1, fmin(r.o2, r.o3)));
+        ghi = fmax(ghi, fmax(r.o1, fmax(r.o2, r.o3)));
+      }
+    }
+  }
+  halo_signal(h, zb == 0, ze >= g.nzl);
+  if (skipped) return;
+  if (bad) {
+    Col<DIM> c;
+    c.c0 = cx;
+    c.c1 = cy;
+    c.ip = ip;
+    c.z0 = zb;
+    c.z1 = ze;
+    c.valid = true;
+    const bool inner = inner_nonfinite<DIM>(g, h, a.g1, c, nbr_of<DIM>(g, c), a.eta);
+    atomicMin(a.event, a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1)) +
+                           (inner ? 1 : a.m + 1));
+  }
+  if (!ION && a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+  if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, valid && ze > zb);
+}
+
+template <int DIM>
+constexpr size_t tma_vin_smem_bytes() {
+  using T = PipeTile<DIM>;
+  return sizeof(double) * (kRV * TmaTile<DIM>::VS + kRG * 4 * T::NT) + 128;
+}
+
+template <int DIM, int LAST, int FIRST>
+__global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
+    k_vin_tma(const Geom g, const Halo h, const FastInnerArgs a, const __grid_constant__ TmaVin tm) {
+  using T = PipeTile<DIM>;
+  constexpr int VS = TmaTile<DIM>::VS;
+  extern __shared__ __align__(128) double smem_tma[];
+  // 128-byte aligned stage base (pointer arithmetic keeps the shared space)
+  double* vst = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;  // [kRV][VS]
+  double* cst = vst + kRV * VS;                      // [kRG][4][NT]: d1, d_{k-2}, V1, V2
+  __shared__ __align__(8) unsigned long long bars[kRV];
+  __shared__ int skip;
+  const int t = threadIdx.x;
+  const int zb = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
+  const int ze = min(g.nzl, zb + a.zc);
+  pdl_launch_dependents();
+  if (t == 0) {
+    for (int s = 0; s < kRV; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    mbar_fence_init();
+    prefetch_tensormap(&tm.u);
+  }
+  pdl_wait();
+  halo_wait(h, zb == 0, ze >= g.nzl);
+  if (t == 0) {
+    // ghost planes arrived through generic peer stores (acquired in
+    // halo_wait); order them before this thread's async-proxy reads
+    fence_proxy_async();
+    skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  }
+  __syncthreads();
+  const bool skipped = skip != 0;
+  const int tx = t % T::TX, ty = t / T::TX;
+  const int x0 = blockIdx.x * T::TX;
+  const int y0 = DIM == 3 ? blockIdx.y * T::TY : 0;
+  const int cx = x0 + tx, cy = y0 + ty;
+  const bool valid = cx < g.n0 && (DIM == 2 || cy < g.n1);
+  const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
+  const long long plane = g.plane;
+  const bool has2 = a.um2 != nullptr;
+  const bool d1_is_u = a.um1 == a.d1;
+  const unsigned v0 = smem_u32(vst), c0 = smem_u32(cst), b0 = smem_u32(bars);
+  constexpr unsigned vbytes = 8u * TmaTile<DIM>::VT;
+  const unsigned nb = (d1_is_u ? 0 : 1) + (has2 ? 1 : 0) + (LAST ? (FIRST ? 1 : 2) : 0);
+  const unsigned cbytes = 8u * T::NT * nb;
+  auto center = [&](const CUtensorMap* m, unsigned dst, unsigned bar, int zz) {
+    if (DIM == 3) tma_load_3d(dst, m, bar, x0, y0, zz);
+    else tma_load_2d(dst, m, bar, x0, zz);
+  };
+  auto issue_comp = [&](int zz) {  // thread 0, zz in [zb, ze)
+    const int q = zz - zb + 1;
+    const unsigned bar = b0 + 8u * (q & (kRV - 1));
+    mbar_expect_tx(bar, vbytes + cbytes);
+    const unsigned vd = v0 + 8u * VS * (q & (kRV - 1));
+    if (DIM == 3) tma_load_3d(vd, &tm.u, bar, x0 - 2, y0 - 1, zz);
+    else tma_load_2d(vd, &tm.u, bar, x0 - 2, zz);
+    const unsigned sc = c0 + 8u * 4 * T::NT * ((zz - zb) & (kRG - 1));
+    if (!d1_is_u) center(&tm.d1, sc, bar, zz);
+    if (has2) center(&tm.um2, sc + 8u * T::NT, bar, zz);
+    if (LAST) {
+      center(&tm.g1v, sc + 16u * T::NT, bar, zz);
+      if (!FIRST) center(&tm.g2v, sc + 24u * T::NT, bar, zz);
+    }
+  };
+  auto issue_edge = [&](int zz) {  // thread 0, zz = zb - 1 or ze
+    const int q = zz - zb + 1;
+    const unsigned bar = b0 + 8u * (q & (kRV - 1));
+    mbar_expect_tx(bar, vbytes);
+    tma_vplane<DIM>(g, &tm.u, &tm.glo, &tm.ghi, true, true, v0 + 8u * VS * (q & (kRV - 1)), bar,
+                    x0, y0, zz);
+  };
+  if (!skipped && t == 0) {
+    issue_edge(zb - 1);
+    for (int i = 0; i < kTmaLA; ++i) {
+      if (zb + i < ze) issue_comp(zb + i);
+      else {
+        issue_edge(ze);
+        break;
+      }
+    }
+  }
+  constexpr int HXT = TmaTile<DIM>::HX;
+  const int cell = (DIM == 3 ? (ty + 1) * HXT : 0) + tx + 2;
+  const int cxm = cell + (cx > 0 ? -1 : 1), cxp = cell + (cx < g.n0 - 1 ? 1 : -1);
+  const int cym = cell + (cy > 0 ? -HXT : HXT), cyp = cell + (cy < g.n1 - 1 ? HXT : -HXT);
+  bool bad_in = false, bad_out = false, guard = false;
+  if (!skipped) {
+    mbar_wait(b0, 0);
+    mbar_wait(b0 + 8u, 0);
+  }
+  for (int z = zb; z < ze && !skipped; ++z) {
+    const int p = z - zb + 1;
+    if (t == 0) {
+      if (z + kTmaLA < ze) issue_comp(z + kTmaLA);
+      else if (z + kTmaLA == ze) issue_edge(ze);
+    }
+    mbar_wait(b0 + 8u * ((p + 1) & (kRV - 1)), ((p + 1) >> 3) & 1);
+    const double* V0 = vst + (p & (kRV - 1)) * VS;
+    const double vc = V0[cell];
+    double D = fma(g.wc, vc, g.w[DIM - 1] * (vst[((p - 1) & (kRV - 1)) * VS + cell] +
+                                             vst[((p + 1) & (kRV - 1)) * VS + cell]));
+    if (DIM >= 2) D = fma(g.w[0], V0[cxm] + V0[cxp], D);
+    if (DIM == 3) D = fma(g.w[1], V0[cym] + V0[cyp], D);
+    const double* C0 = cst + ((z - zb) & (kRG - 1)) * 4 * T::NT + t;
+    const double base = has2 ? fma(a.nu, vc, a.kappa * C0[T::NT]) : a.nu * vc;
+    const double d1 = d1_is_u ? vc : C0[0];
+    const double dk = fma(a.mueta, fma(d1, a.inv_mue1, D), base);
+    if (valid) {
+      const long long i = ip + plane * z;
+      bad_in |= !finite_hi(dk);
+      double vput = dk;
+      if (!LAST) {
+        a.uk[i] = dk;
+      } else {
+        const double gv = C0[2 * T::NT];
+        const double bb = FIRST ? gv : fma(a.onu, gv, a.okappa * C0[3 * T::NT]);
+        const double o0 = fma(a.cG, dk, bb);
+        a.outv[i] = o0;
+        bad_out |= !finite_hi(o0);
+        guard |= fabs(o0) > 1e6;
+        vput = o0;
+      }
+      if (z == 0 && h.put_lo) h.put_lo[ip] = vput;
+      if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = vput;
+    }
+    __syncthreads();
+  }
   halo_signal(h, zb == 0, ze >= g.nzl);
   if (skipped) return;
   const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
@@ -1224,6 +1638,32 @@ cudaError_t launch_node_fast(const Geom& g, const Halo& h, const FastArgs& a,
   return cudaGetLastError();
 }
 
+// Launch with programmatic stream serialization (PDL) unless EMRKC_PDL=0.
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("EMRKC_PDL");
+    on = (e && *e) ? (std::atoi(e) != 0) : 1;
+  }
+  return on != 0;
+}
+
+template <typename... P, typename... A>
+static cudaError_t launch_k(void (*kern)(P...), dim3 grd, dim3 blk, size_t smem, cudaStream_t st,
+                            A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grd;
+  cfg.blockDim = blk;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
+
 template <int D, int F, int I>
 static cudaError_t launch_pipe_t(const Geom& g, const Halo& h, const FastArgs& a,
                                  cudaStream_t st) {
@@ -1238,8 +1678,7 @@ static cudaError_t launch_pipe_t(const Geom& g, const Halo& h, const FastArgs& a
   const int chunks = (g.nzl + a.zc - 1) / a.zc;
   const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)
                           : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
-  k_node_pipe<D, F, I><<<grd, T::NT, smem, st>>>(g, h, a);
-  return cudaGetLastError();
+  return launch_k(k_node_pipe<D, F, I>, grd, dim3(T::NT), smem, st, g, h, a);
 }
 
 template <int D, int F, int I>
@@ -1282,6 +1721,62 @@ cudaError_t launch_node_persist(const Geom& g, const Halo& h, const FastArgs& a,
   return launch_node_fast(g, h, a, ion, st);
 }
 
+template <int D, int F, int I>
+static cudaError_t launch_node_tma_t(const Geom& g, const Halo& h, const FastArgs& a,
+                                     const TmaNode& tm, cudaStream_t st) {
+  using T = PipeTile<D>;
+  constexpr size_t smem = tma_node_smem_bytes<D, F>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_node_tma<D, F, I>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  const int chunks = (g.nzl + a.zc - 1) / a.zc;
+  const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)
+                          : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
+  return launch_k(k_node_tma<D, F, I>, grd, dim3(T::NT), smem, st, g, h, a, tm);
+}
+
+cudaError_t launch_node_tma(const Geom& g, const Halo& h, const FastArgs& a, const TmaNode& tm,
+                            bool ion, cudaStream_t st) {
+  const bool first = a.j == 1;
+  if (g.dim == 3) {
+    if (ion) return first ? launch_node_tma_t<3, 1, 1>(g, h, a, tm, st) : launch_node_tma_t<3, 0, 1>(g, h, a, tm, st);
+    return first ? launch_node_tma_t<3, 1, 0>(g, h, a, tm, st) : launch_node_tma_t<3, 0, 0>(g, h, a, tm, st);
+  }
+  if (ion) return first ? launch_node_tma_t<2, 1, 1>(g, h, a, tm, st) : launch_node_tma_t<2, 0, 1>(g, h, a, tm, st);
+  return first ? launch_node_tma_t<2, 1, 0>(g, h, a, tm, st) : launch_node_tma_t<2, 0, 0>(g, h, a, tm, st);
+}
+
+template <int D, int L, int F>
+static cudaError_t launch_vin_tma_t(const Geom& g, const Halo& h, const FastInnerArgs& a,
+                                    const TmaVin& tm, cudaStream_t st) {
+  using T = PipeTile<D>;
+  constexpr size_t smem = tma_vin_smem_bytes<D>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vin_tma<D, L, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  const int chunks = (g.nzl + a.zc - 1) / a.zc;
+  const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)
+                          : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
+  return launch_k(k_vin_tma<D, L, F>, grd, dim3(T::NT), smem, st, g, h, a, tm);
+}
+
+cudaError_t launch_vin_tma(const Geom& g, const Halo& h, const FastInnerArgs& a, const TmaVin& tm,
+                           cudaStream_t st) {
+  const bool last = a.k == a.m, first = a.j == 1;
+  if (g.dim == 3) {
+    if (!last) return launch_vin_tma_t<3, 0, 0>(g, h, a, tm, st);
+    return first ? launch_vin_tma_t<3, 1, 1>(g, h, a, tm, st) : launch_vin_tma_t<3, 1, 0>(g, h, a, tm, st);
+  }
+  if (!last) return launch_vin_tma_t<2, 0, 0>(g, h, a, tm, st);
+  return first ? launch_vin_tma_t<2, 1, 1>(g, h, a, tm, st) : launch_vin_tma_t<2, 1, 0>(g, h, a, tm, st);
+}
+
 cudaError_t launch_node_pipe(const Geom& g, const Halo& h, const FastArgs& a, bool ion,
                              cudaStream_t st) {
   const bool first = a.j == 1;
@@ -1310,8 +1805,7 @@ static cudaError_t launch_vin_pipe_t(const Geom& g, const Halo& h, const FastInn
   const int chunks = (g.nzl + a.zc - 1) / a.zc;
   const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)
                           : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
-  k_vin_pipe<D, L, F><<<grd, T::NT, smem, st>>>(g, h, a);
-  return cudaGetLastError();
+  return launch_k(k_vin_pipe<D, L, F>, grd, dim3(T::NT), smem, st, g, h, a);
 }
 
 cudaError_t launch_vin_pipe(const Geom& g, const Halo& h, const FastInnerArgs& a,
