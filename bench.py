@@ -10,8 +10,10 @@ configs[1] workload of BASELINE.json (HH 3-D 128^3, dt 0.05 ms, T 5 ms =
 100 steps), W = 5, K = 1000 (ten back-to-back repeats of the 100-step run).
 
 `value`  : device time (CUDA events, per kernel launch, on the launching
-           stream) with the state resident in HBM; L2 (126 MB) is flushed by
-           a 256 MiB memset before every timed step, outside the timed pairs.
+           stream) with the state resident in HBM; L2 (126 MB) is flushed
+           before every timed step, outside the timed pairs, by a 256 MiB
+           memset followed by a 256 MiB read pass (so the memset's dirty
+           lines are written back before the step, not during it).
 `e2e`    : the per-call drop-in (emrkc_step_host: pinned host state in,
            one device step, host state out), wall clock around each call.
 `roofline`: the step's dominant kernel, algorithmic bytes / its mean launch
@@ -60,11 +62,25 @@ KERNEL_BYTES = {
     ("last", "first_outer"): 40,   # d_{m-1}, d_{m-2}, d_1, V in; V out
     ("last", "outer"): 48,
 }
-KERNEL_NAMES = {"m1": "k_node_pipe (m = 1: whole outer stage)",
-                "first": "k_node_pipe (m >= 2: ionic + inner stage 1)",
-                "inner2": "k_vin_fast (inner stage 2)", "inner": "k_vin_fast (inner stage k)",
-                "last2": "k_vin_fast (last inner stage, m = 2)",
-                "last": "k_vin_fast (last inner stage)"}
+KERNEL_ROLES = {"m1": ("node", "m = 1: whole outer stage"),
+                "first": ("node", "m >= 2: ionic + inner stage 1"),
+                "inner2": ("vin", "inner stage 2"), "inner": ("vin", "inner stage k"),
+                "last2": ("vin", "last inner stage, m = 2"),
+                "last": ("vin", "last inner stage")}
+
+
+def kernel_name(kind: str, problem) -> str:
+    """Kernel family the library selects (emrkc_capi.cpp init_handle):
+    EMRKC_PIPE 3 (default; TMA, needs n0 even and dim >= 2), 1 (cp.async),
+    2 (persistent node kernel), 0 (z-march)."""
+    pipe = int(os.environ.get("EMRKC_PIPE") or 3)
+    if pipe == 3 and (problem.dim < 2 or int(problem.n[0]) % 2):
+        pipe = 1
+    if problem.dim < 2:
+        pipe = 0
+    role, what = KERNEL_ROLES[kind]
+    fam = {3: "tma", 1: "pipe", 2: "persist" if role == "node" else "pipe", 0: "fast"}[pipe]
+    return f"k_{role}_{fam} ({what})"
 
 
 def launch_kinds(s: int, m: int):
@@ -268,7 +284,8 @@ METRIC = "emRKC node-steps/s (fp64)"
 def config_of(w, n_gpus):
     d = w.describe()
     d["parallelism"] = f"z-slab x{n_gpus}" if n_gpus > 1 else "single GPU"
-    d["l2"] = "flushed (256 MiB memset) before every timed step"
+    d["l2"] = ("flushed before every timed step: 256 MiB memset, then a 256 MiB read pass "
+               "(dirty lines written back outside the timed pairs)")
     return d
 
 
@@ -391,7 +408,7 @@ def roofline_of(m, w, peak, peak_kind):
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "traffic": traffic,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-        "kernel": KERNEL_NAMES[kinds[dom][0]],
+        "kernel": kernel_name(kinds[dom][0], w.problem),
         "alg_bytes_per_node": kb, "mean_launch_ms": float(per_pos[dom]),
         "share_of_step": float(per_pos[dom] / per_pos.sum()),
         "step_alg_bytes_per_node": 64, "step_achieved_gbs": step_gbs,

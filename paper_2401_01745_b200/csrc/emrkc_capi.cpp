@@ -725,7 +725,8 @@ int init_handle(emrkc_handle* h) {
   h->fast = f ? std::atoi(f) : 1;
   h->zc = emrkc_k::fast_zc(h->geom);
   const char* pp = std::getenv("EMRKC_PIPE");
-  // 3: TMA-staged blocks, 1: cp.async-staged blocks, 2: persistent, 0: march
+  // 3: TMA-staged blocks, 1: cp.async-staged blocks, 2: persistent cp.async
+  // node kernel, 0: march
   h->pipe = (pp && *pp) ? std::atoi(pp) : 3;
   if (h->pipe == 3 && !tma_supported(h)) h->pipe = 1;
   if (const char* zc = std::getenv("EMRKC_ZC"))
@@ -1363,15 +1364,28 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     if (launch_ms_len < nsteps * per)
       return set_err(h, EMRKC_EINVAL, "run_timed: launch_ms needs %lld entries",
                      (long long)(nsteps * per));
+    // L2 flush between steps: write a buffer larger than L2, then read a
+    // second one so the dirty lines are written back outside the timed
+    // pairs (L2 left cold and clean)
     void* scratch = nullptr;
-    if (flush_bytes > 0) CK(h, cudaMalloc(&scratch, flush_bytes));
+    void* scratch_rd = nullptr;
+    if (flush_bytes > 0) {
+      CK(h, cudaMalloc(&scratch, flush_bytes));
+      CK(h, cudaMalloc(&scratch_rd, flush_bytes));
+      CK(h, cudaMemset(scratch_rd, 0, flush_bytes));
+    }
     tev.resize(2 * nsteps * per);
     for (auto& e : tev) CK(h, cudaEventCreate(&e));
     int64_t li = 0;
     for (int64_t r = 0; r < nsteps; ++r) {
       const double t = static_cast<double>(step0 + r) * dt;
       in_idx[0][r] = h->cur;
-      if (scratch) CK(h, cudaMemsetAsync(scratch, static_cast<int>(r & 0xff), flush_bytes, h->stream));
+      if (scratch) {
+        CK(h, cudaMemsetAsync(scratch, static_cast<int>(r & 0xff), flush_bytes, h->stream));
+        CK(h, emrkc_k::launch_norm2_partial(static_cast<const double*>(scratch_rd),
+                                            flush_bytes / 8, h->d_red,
+                                            emrkc_k::power_blocks(), h->stream));
+      }
       StepCtx c;
       begin_step(h, t, r, h->d_slots + 2 * r, &c);
       for (int j = 1; j <= pl.s; ++j)
@@ -1392,6 +1406,7 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     }
     for (auto& e : tev) cudaEventDestroy(e);
     if (scratch) cudaFree(scratch);
+    if (scratch_rd) cudaFree(scratch_rd);
     if (res) res->device_ms = tot;  // overwritten below, restored after
   } else if (n == 1) {
     emrkc_handle* h = hs[0];

@@ -25,6 +25,7 @@
 
 #include "fast_math.cuh"
 #include "hh.cuh"
+#include <algorithm>
 #include <cstdlib>
 #include <utility>
 

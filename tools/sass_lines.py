@@ -39,7 +39,7 @@ for addr, txt, _ in ins:
         if tgt < addr:
             loops.append((tgt, addr))
 loops = sorted(set(loops), key=lambda x: x[0] - x[1])
-for i, (a, b) in enumerate(loops[:8]):
+for i, (a, b) in enumerate(loops[:int(sys.argv[5]) if len(sys.argv) > 5 else 8]):
     body_i = [x[1] for x in ins if a <= x[0] <= b]
     print(f"loop {i}: {hex(a)}..{hex(b)} n={len(body_i)} DFMA={sum('DFMA' in t for t in body_i)}"
           f" BAR={sum('BAR.SYNC' in t for t in body_i)} UTMALDG={sum('UTMALDG' in t for t in body_i)}")
