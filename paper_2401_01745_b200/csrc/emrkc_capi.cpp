@@ -730,7 +730,7 @@ int init_handle(emrkc_handle* h) {
   h->pipe = (pp && *pp) ? std::atoi(pp) : 3;
   if (h->pipe == 3 && !tma_supported(h)) h->pipe = 1;
   if (const char* zc = std::getenv("EMRKC_ZC"))
-    if (*zc) h->zc = std::max(1, std::atoi(zc));
+    if (*zc) h->zc = std::min(emrkc_k::kMaxZc, std::max(1, std::atoi(zc)));
   return EMRKC_OK;
 }
 

@@ -127,6 +127,9 @@ struct TmaVin {
 // Tile shape of the staged kernels (x, y per block; 2-D grids use TX2 x 1).
 constexpr int kTX3 = 32, kTY3 = 4, kTX2 = 128;
 
+// z-chunk length of the staged kernels (bounded by the 32-bit deferred-node
+// mask of k_node_pipe / k_node_tma).
+constexpr int kMaxZc = 32;
 int fast_zc(const Geom& g);
 // Signals per level that a neighbour receives from one launch of each kernel
 // family (blocks that hold the boundary plane of their slab).

@@ -1574,6 +1574,20 @@ int fast_zc(const Geom& g) {
   if (g.dim == 1) return 1;
   const long long tiles = (g.dim == 3) ? ((g.n0 + 31) / 32) * (long long)((g.n1 + 3) / 4)
                                        : (g.n0 + 127) / 128;
+  // Longest z-chunk (<= 32: the deferred-node mask width) that still gives
+  // >= 1.7 waves of resident node blocks (5 per SM): long chunks amortise
+  // the halo planes and the pipeline prologue, the wave floor keeps the
+  // tail short (measured on B200).
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  const long long want = (long long)(1.7 * sms * 5);
+  for (int zc = kMaxZc; zc >= 4; --zc)
+    if (tiles * ((g.nzl + zc - 1) / zc) >= want) return zc > g.nzl ? g.nzl : zc;
   int zc = 16;
   while (zc > 4 && tiles * ((g.nzl + zc - 1) / zc) < 148LL * 5 * 2) zc /= 2;
   return zc > g.nzl ? g.nzl : zc;
