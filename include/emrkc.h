@@ -49,7 +49,9 @@ typedef enum emrkc_status {
 
 enum { EMRKC_MODEL_HH = 0 };          /* make_ionic_model("hh"), P/src/ionic.cpp:125-128 */
 enum { EMRKC_RHS_F = 0, EMRKC_RHS_S = 1 }; /* SplitRhs::f_F / f_S */
-enum { EMRKC_VARIANT_STANDARD = 0 };  /* EmrkcVariant::standard, P/include/mrkc/multirate.hpp:37-40 */
+/* EmrkcVariant, P/include/mrkc/multirate.hpp:37-40 (averaged force:
+ * P/src/multirate.cpp:100-105 standard, :106-115 progressive). */
+enum { EMRKC_VARIANT_STANDARD = 0, EMRKC_VARIANT_PROGRESSIVE = 1 };
 enum {
   EMRKC_ABORT_NONE = 0,
   EMRKC_ABORT_NONFINITE = 1,  /* check_stage_finite, P/src/cheb.cpp:73-80 */
@@ -227,6 +229,20 @@ int emrkc_step_host(emrkc_handle* h, double t, const double* y_in,
 int emrkc_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
               double epsilon, int32_t variant, double rho_F, double rho_S,
               emrkc_run_result* res);
+
+/* EXEX-RL, the reference's reference-solution stepper: Rush-Larsen gates
+ * (exponential Euler with dt) and explicit Euler on V with the reaction
+ * evaluated at the new gates — exex_rl_step, P/src/baselines.cpp:192-210,
+ * with rush_larsen_update :89-128. One step of the device state; counters
+ * n_fF = n_fS = n_exp = 1. exex_rl_step never throws NumericalAbort. */
+int emrkc_exex_step(emrkc_handle* h, double t, double dt, emrkc_step_report* report);
+
+/* run_simulation's exex_rl loop (P/src/simulate.cpp:164-165,176-229):
+ * t = step*dt; the ||V||_inf > 1e6 guard (which also trips on a non-finite
+ * V, max_abs_v :67-74) assigns the state and stops; gate range tracking.
+ * res->s = res->m = 1, res->eta = dt. */
+int emrkc_exex_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
+                   emrkc_run_result* res);
 
 /* Benchmark form of emrkc_run: before every step, writes flush_bytes of a
  * scratch buffer (evicts L2; 0 = no flush), then times every kernel launch

@@ -9,8 +9,12 @@
 //                                      binding (P/include/mrkc/monodomain.hpp:119-176,
 //                                      P/src/simulate.cpp:153-157), resident in HBM
 //   emrkc_step(t, y, dt, op, ...)      P/include/mrkc/multirate.hpp:78-81
+//   EmrkcVariant                       P/include/mrkc/multirate.hpp:37-40
 //   DeviceMonodomain::run              the emRKC branch of run_simulation's loop
 //                                      (P/src/simulate.cpp:176-229)
+//   exex_rl_step / DeviceMonodomain::exex_run
+//                                      P/src/baselines.cpp:192-210 and the
+//                                      exex_rl branch of run_simulation
 //
 // Header-only; link libemrkc_b200.so. Errors follow the reference:
 // std::invalid_argument for bad arguments, NumericalAbort for non-finite
@@ -45,6 +49,11 @@ inline void check(int rc, const emrkc_handle* h = nullptr, long step = -1, doubl
   if (rc == EMRKC_ENONFINITE) throw NumericalAbort(msg, step, dt, stage);
   throw std::runtime_error(msg);
 }
+
+enum class EmrkcVariant : int32_t {
+  standard = EMRKC_VARIANT_STANDARD,
+  progressive = EMRKC_VARIANT_PROGRESSIVE
+};
 
 struct StagePlan {
   int s = 1;
@@ -152,20 +161,34 @@ class DeviceMonodomain {
 
   // One step of the device state (y is not assigned on NumericalAbort).
   MultirateStepReport step(double t, double dt, double rho_F, double rho_S,
-                           double epsilon = 0.05) {
+                           double epsilon = 0.05,
+                           EmrkcVariant variant = EmrkcVariant::standard) {
     emrkc_step_report r{};
-    const int rc = emrkc_step(h_, t, dt, epsilon, EMRKC_VARIANT_STANDARD, rho_F, rho_S, &r);
+    const int rc = emrkc_step(h_, t, dt, epsilon, static_cast<int32_t>(variant), rho_F, rho_S, &r);
     check(rc, h_, -1, dt, r.abort_stage);
     return to_report(r);
   }
 
   // run_simulation's emRKC loop (t = step*dt, aborts, norm guard, gate range).
   RunResult run(long step0, long nsteps, double dt, double rho_F, double rho_S,
-                double epsilon = 0.05) {
+                double epsilon = 0.05, EmrkcVariant variant = EmrkcVariant::standard) {
     RunResult res;
-    check(emrkc_run(h_, step0, nsteps, dt, epsilon, EMRKC_VARIANT_STANDARD, rho_F, rho_S,
+    check(emrkc_run(h_, step0, nsteps, dt, epsilon, static_cast<int32_t>(variant), rho_F, rho_S,
                     &res.raw),
           h_);
+    return res;
+  }
+
+  // One EXEX-RL step of the device state (never throws NumericalAbort).
+  void exex_step(double t, double dt) {
+    emrkc_step_report r{};
+    check(emrkc_exex_step(h_, t, dt, &r), h_);
+  }
+
+  // run_simulation's exex_rl loop (norm guard, gate range).
+  RunResult exex_run(long step0, long nsteps, double dt) {
+    RunResult res;
+    check(emrkc_exex_run(h_, step0, nsteps, dt, &res.raw), h_);
     return res;
   }
 
@@ -194,14 +217,23 @@ class DeviceMonodomain {
 // host Vec in, one device step, host Vec out.
 inline Vec emrkc_step(double t, const Vec& y, double dt, DeviceMonodomain& op, double rho_F,
                       double rho_S, double epsilon = 0.05,
-                      MultirateStepReport* report = nullptr) {
+                      MultirateStepReport* report = nullptr,
+                      EmrkcVariant variant = EmrkcVariant::standard) {
   Vec out(y.size());
   emrkc_step_report r{};
   const int rc = emrkc_step_host(op.handle(), t, y.data(), out.data(), (int64_t)y.size(), dt,
-                                 epsilon, EMRKC_VARIANT_STANDARD, rho_F, rho_S, &r);
+                                 epsilon, static_cast<int32_t>(variant), rho_F, rho_S, &r);
   if (report) *report = DeviceMonodomain::to_report(r);
   check(rc, op.handle(), -1, dt, r.abort_stage);
   return out;
+}
+
+// Drop-in of `Vec exex_rl_step(t, y, dt, prob, counters)`
+// (P/src/baselines.cpp:192-210): host Vec in, one device step, host Vec out.
+inline Vec exex_rl_step(double t, const Vec& y, double dt, DeviceMonodomain& op) {
+  op.set_state(y);
+  op.exex_step(t, dt);
+  return op.get_state();
 }
 
 }  // namespace emrkc

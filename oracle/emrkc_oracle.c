@@ -194,6 +194,7 @@ void oc_exponential_euler_step(const double* y, double eta, const double* lam,
 typedef struct fu_ctx {
   const oc_split* rhs;
   const double* fs;
+  const double* expc; /* progressive variant: (y_E - y)/eta, else NULL */
 } fu_ctx;
 
 static void f_u(void* vctx, double r, const double* u, double* out,
@@ -201,17 +202,22 @@ static void f_u(void* vctx, double r, const double* u, double* out,
   fu_ctx* c = (fu_ctx*)vctx;
   c->rhs->f_F(c->rhs->ctx, r, u, out, n);
   if (c->rhs->counters) ++c->rhs->counters->n_fF;
-  for (int64_t i = 0; i < n; ++i) out[i] += c->fs[i];
+  if (c->expc) /* P/src/multirate.cpp:111-112 */
+    for (int64_t i = 0; i < n; ++i) out[i] += c->fs[i] + c->expc[i];
+  else /* :101-103 */
+    for (int64_t i = 0; i < n; ++i) out[i] += c->fs[i];
 }
 
-/* averaged_force_emrkc, standard variant — P/src/multirate.cpp:78-119 */
+/* averaged_force_emrkc — P/src/multirate.cpp:78-119 (standard :100-105,
+ * progressive :106-115) */
 static int averaged_force_k(double t, const double* y, int64_t n, double eta,
-                            const oc_split* rhs, const coeffs* km,
+                            const oc_split* rhs, const coeffs* km, int32_t variant,
                             double* out, int32_t* abort_stage) {
   double* lam = (double*)malloc(sizeof(double) * n);
   double* yinf = (double*)malloc(sizeof(double) * n);
   double* yE = (double*)malloc(sizeof(double) * n);
   double* fs = (double*)malloc(sizeof(double) * n);
+  double* expc = NULL;
   int rc = 0;
   if (!lam || !yinf || !yE || !fs) {
     rc = fail(EMRKC_ENOMEM, "out of memory");
@@ -222,8 +228,20 @@ static int averaged_force_k(double t, const double* y, int64_t n, double eta,
   if (rhs->counters) ++rhs->counters->n_exp;
   rhs->f_S(rhs->ctx, t, yE, fs, n); /* slow term frozen at y_E (:96-97) */
   if (rhs->counters) ++rhs->counters->n_fS;
-  fu_ctx c = {rhs, fs};
-  rc = rkc_iteration_k(t, yE, n, eta, f_u, &c, km, out, abort_stage);
+  if (variant == EMRKC_VARIANT_STANDARD) {
+    fu_ctx c = {rhs, fs, NULL};
+    rc = rkc_iteration_k(t, yE, n, eta, f_u, &c, km, out, abort_stage);
+  } else {
+    /* phi(eta Lambda) f_E(y) = (y_E - y)/eta (:107-109); iterate from y */
+    expc = (double*)malloc(sizeof(double) * n);
+    if (!expc) {
+      rc = fail(EMRKC_ENOMEM, "out of memory");
+      goto done;
+    }
+    for (int64_t i = 0; i < n; ++i) expc[i] = (yE[i] - y[i]) / eta;
+    fu_ctx c = {rhs, fs, expc};
+    rc = rkc_iteration_k(t, y, n, eta, f_u, &c, km, out, abort_stage);
+  }
   if (rc) goto done;
   for (int64_t i = 0; i < n; ++i) out[i] = (out[i] - y[i]) / eta; /* :117 */
 done:
@@ -231,6 +249,7 @@ done:
   free(yinf);
   free(yE);
   free(fs);
+  free(expc);
   return rc;
 }
 
@@ -243,7 +262,7 @@ int oc_averaged_force_emrkc(double t, const double* y, int64_t n, double eta,
   coeffs km;
   int rc = coeffs_make(&km, m, eps);
   if (rc) return rc;
-  rc = averaged_force_k(t, y, n, eta, rhs, &km, out, abort_stage);
+  rc = averaged_force_k(t, y, n, eta, rhs, &km, EMRKC_VARIANT_STANDARD, out, abort_stage);
   coeffs_free(&km);
   return rc;
 }
@@ -256,6 +275,7 @@ typedef struct avg_ctx {
   double eta;
   int rc;
   int32_t inner_stage;
+  int32_t variant;
 } avg_ctx;
 
 static void f_avg(void* vctx, double r, const double* g, double* out,
@@ -266,18 +286,26 @@ static void f_avg(void* vctx, double r, const double* g, double* out,
     return;
   }
   int32_t st = 0;
-  c->rc = averaged_force_k(r, g, n, c->eta, c->rhs, c->km, out, &st);
+  c->rc = averaged_force_k(r, g, n, c->eta, c->rhs, c->km, c->variant, out, &st);
   if (c->rc) {
     c->inner_stage = st;
     for (int64_t i = 0; i < n; ++i) out[i] = NAN;
   }
 }
 
-/* emrkc_step — P/src/multirate.cpp:173-189 with plan_step :129-135 */
 int oc_emrkc_step(double t, const double* y, int64_t n, double dt,
                   const oc_split* rhs, double eps, double* out,
                   emrkc_step_report* rep) {
+  return oc_emrkc_step_v(t, y, n, dt, rhs, eps, EMRKC_VARIANT_STANDARD, out, rep);
+}
+
+/* emrkc_step — P/src/multirate.cpp:173-189 with plan_step :129-135 */
+int oc_emrkc_step_v(double t, const double* y, int64_t n, double dt,
+                    const oc_split* rhs, double eps, int32_t variant,
+                    double* out, emrkc_step_report* rep) {
   memset(rep, 0, sizeof(*rep));
+  if (variant != EMRKC_VARIANT_STANDARD && variant != EMRKC_VARIANT_PROGRESSIVE)
+    return fail(EMRKC_EINVAL, "emrkc_step: unknown variant");
   if (dt <= 0.0) return fail(EMRKC_EINVAL, "emrkc_step: dt must be > 0");
   if (!rhs->exp_part)
     return fail(EMRKC_EINVAL, "emrkc_step: exp_part missing");
@@ -302,7 +330,7 @@ int oc_emrkc_step(double t, const double* y, int64_t n, double dt,
     coeffs_free(&ks);
     return rc;
   }
-  avg_ctx c = {rhs, &km, eta, 0, 0};
+  avg_ctx c = {rhs, &km, eta, 0, 0, variant};
   int32_t outer_stage = 0;
   /* The reference throws out of the inner iteration at the first
    * non-finite inner stage; emulate by running the outer iteration stage by
@@ -742,10 +770,46 @@ static void track_gate_range(const double* y, int64_t nn, int64_t len,
   }
 }
 
-/* run_simulation's emRKC loop — P/src/simulate.cpp:110-113, 176-229 */
 int oc_run(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
            double dt, double eps, double rho_F, double rho_S,
            emrkc_run_result* res, double* wall_s) {
+  return oc_run_method(p, y, step0, nsteps, dt, eps, OC_METHOD_EMRKC, rho_F, rho_S, res,
+                       wall_s);
+}
+
+/* rush_larsen_update + exex_rl_step — P/src/baselines.cpp:89-128,192-210
+ * (HH: no auxiliary variables) */
+int oc_exex_rl_step(const emrkc_problem* p, double t, const double* y, double dt,
+                    double* out) {
+  if (!(dt > 0.0)) return fail(EMRKC_EINVAL, "exex_rl_step: dt must be > 0");
+  const int64_t nn = n_nodes(p);
+  double* dv = (double*)malloc(sizeof(double) * nn);
+  if (!dv) return fail(EMRKC_ENOMEM, "out of memory");
+  memcpy(out, y, sizeof(double) * 4 * nn); /* ynew = y */
+  for (int64_t i = 0; i < nn; ++i) { /* gate_coeffs_field on y; expm1 update */
+    double lam[3], zinf[3];
+    oc_hh_gate_coeffs(y[i], lam, zinf);
+    for (int g = 0; g < 3; ++g) {
+      const int64_t idx = (1 + g) * nn + i;
+      out[idx] = y[idx] + expm1(dt * lam[g]) * (y[idx] - zinf[g]);
+    }
+  }
+  /* v_rhs = v_reaction(t, ynew): V old, gates new; dv = diffusion(V old) */
+  oc_diffusion_apply(p, y, dv);
+  for (int64_t i = 0; i < nn; ++i) {
+    const double z[3] = {out[nn + i], out[2 * nn + i], out[3 * nn + i]};
+    const double v_rhs = oc_stimulus_rate(p, t, i) - oc_hh_ionic_current(y[i], z) / p->C_m;
+    out[i] = y[i] + dt * (dv[i] + v_rhs);
+  }
+  free(dv);
+  return 0;
+}
+
+/* run_simulation's stepping loop — P/src/simulate.cpp:110-113, 176-229:
+ * the emRKC / emRKC-progressive branches (:197-207) and exex_rl (:211-212) */
+int oc_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
+                  double dt, double eps, int32_t method, double rho_F, double rho_S,
+                  emrkc_run_result* res, double* wall_s) {
   int rc = oc_validate(p);
   if (rc) return rc;
   const int64_t nn = n_nodes(p), len = 4 * nn;
@@ -765,7 +829,21 @@ int oc_run(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
   for (int64_t step = step0; step < step0 + nsteps; ++step) {
     const double t = (double)step * dt;
     emrkc_step_report rep;
-    rc = oc_emrkc_step(t, y, len, dt, &rhs, eps, next, &rep);
+    if (method == OC_METHOD_EXEX_RL) {
+      rc = oc_exex_rl_step(p, t, y, dt, next);
+      /* counters: one exp step, one f_S, one f_F (baselines.cpp:105,123,203) */
+      ++ctr.n_exp;
+      ++ctr.n_fS;
+      ++ctr.n_fF;
+      memset(&rep, 0, sizeof rep);
+      rep.s = rep.m = 1;
+      rep.eta = dt;
+    } else {
+      rc = oc_emrkc_step_v(t, y, len, dt, &rhs, eps,
+                           method == OC_METHOD_EMRKC_PROGRESSIVE ? EMRKC_VARIANT_PROGRESSIVE
+                                                                 : EMRKC_VARIANT_STANDARD,
+                           next, &rep);
+    }
     if (rc == EMRKC_ENONFINITE) {
       res->aborted = 1;
       res->abort_kind = EMRKC_ABORT_NONFINITE;

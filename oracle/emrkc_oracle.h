@@ -66,6 +66,10 @@ int oc_averaged_force_emrkc(double t, const double* y, int64_t n, double eta,
 int oc_emrkc_step(double t, const double* y, int64_t n, double dt,
                   const oc_split* rhs, double eps, double* out,
                   emrkc_step_report* rep);
+/* variant: EMRKC_VARIANT_STANDARD / EMRKC_VARIANT_PROGRESSIVE */
+int oc_emrkc_step_v(double t, const double* y, int64_t n, double dt,
+                    const oc_split* rhs, double eps, int32_t variant,
+                    double* out, emrkc_step_report* rep);
 
 /* ---- HH ionic model (P/src/ionic.cpp) ----------------------------------- */
 void oc_hh_rates(double V, double* alpha, double* beta);
@@ -100,6 +104,14 @@ int oc_estimate_rho_cb(oc_rhs_fn f, void* ctx, int64_t n, double t,
 int oc_run(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
            double dt, double eps, double rho_F, double rho_S,
            emrkc_run_result* res, double* wall_s);
+/* Method (P/include/mrkc/config.hpp:17) of oc_run_method */
+enum { OC_METHOD_EMRKC = 0, OC_METHOD_EMRKC_PROGRESSIVE = 1, OC_METHOD_EXEX_RL = 2 };
+int oc_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
+                  double dt, double eps, int32_t method, double rho_F, double rho_S,
+                  emrkc_run_result* res, double* wall_s);
+/* exex_rl_step — P/src/baselines.cpp:192-210 (out: 4n, not aliasing y) */
+int oc_exex_rl_step(const emrkc_problem* p, double t, const double* y, double dt,
+                    double* out);
 int oc_emrkc_step_grid(const emrkc_problem* p, double t, const double* y,
                        double dt, double eps, double rho_F, double rho_S,
                        double* out, emrkc_step_report* rep);

@@ -48,6 +48,7 @@ def _sigs(pre: str):
         "stimulus_rate": (C.c_double, [PP, C.c_double, C.c_int64]),
         "estimate_rho": (C.c_int, [PP, C.c_int32, C.c_double, DP, DP, C.c_double, C.POINTER(RhoResult), DP]),
         "run": (C.c_int, [PP, DP, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(RunResult), DP]),
+        "run_method": (C.c_int, [PP, DP, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult), DP]),
         "rel_l2_error": (C.c_double, [PP, DP, DP]),
         "analytic_rho_F": (C.c_double, [PP]),
         "get_stages": (C.c_int, [C.c_double, C.c_double, C.c_double, I32P, DP, DP]),
@@ -86,6 +87,7 @@ def _sigs(pre: str):
         s["hh_resting_state"] = (C.c_int, [DP, DP])
         s["scalar_averaged_force"] = (C.c_int, [C.c_double] * 6 + [C.c_int32, C.c_double, DP])
         s["scalar_emrkc_step"] = (C.c_int, [C.c_double] * 7 + [DP, I32P, I32P, DP])
+        s["exex_rl_step"] = (C.c_int, [PP, C.c_double, DP, C.c_double, DP])
         s.pop("gate_coeffs")
         s.pop("ionic_current")
         s.pop("resting_state")
@@ -141,6 +143,21 @@ class _Lib:
         res = RunResult()
         wall = C.c_double(0.0)
         rc = self.fn("run")(C.byref(p), dptr(y), step0, nsteps, dt, eps, rho_F, rho_S, C.byref(res), C.byref(wall))
+        if rc:
+            raise ValueError(self.err())
+        return y, res, wall.value
+
+    # Method codes of run_method (P/include/mrkc/config.hpp:17)
+    EMRKC, EMRKC_PROGRESSIVE, EXEX_RL = 0, 1, 2
+
+    def run_method(self, p: Problem, y: np.ndarray, step0: int, nsteps: int, dt: float,
+                   method: int, eps: float = 0.05, rho_F: float = 0.0, rho_S: float = 0.0):
+        """run_simulation's loop for emrkc (0), emrkc_progressive (1), exex_rl (2)."""
+        y = np.ascontiguousarray(y, dtype=np.float64).copy()
+        res = RunResult()
+        wall = C.c_double(0.0)
+        rc = self.fn("run_method")(C.byref(p), dptr(y), step0, nsteps, dt, eps, method, rho_F,
+                                   rho_S, C.byref(res), C.byref(wall))
         if rc:
             raise ValueError(self.err())
         return y, res, wall.value

@@ -23,6 +23,7 @@
 #include <thread>
 #include <vector>
 
+#include "mrkc/baselines.hpp"
 #include "mrkc/cheb.hpp"
 #include "mrkc/ionic.hpp"
 #include "mrkc/monodomain.hpp"
@@ -118,10 +119,11 @@ void track_gate_range(const Vec& y, const StateLayout& lay, double& lo,
   }
 }
 
-// The emRKC branch of run_simulation's loop (P/src/simulate.cpp:176-229).
+// run_simulation's loop (P/src/simulate.cpp:176-229): method 0 emrkc,
+// 1 emrkc_progressive (:197-207), 2 exex_rl (:211-212).
 void run_loop(const MonodomainOperator& op, Vec& y, long step0, long nsteps,
               double dt, double eps, double rho_F, double rho_S,
-              emrkc_run_result* res, double* wall_s) {
+              emrkc_run_result* res, double* wall_s, int method = 0) {
   const StateLayout& lay = op.layout();
   EvalCounters ctr;
   SplitRhs rhs = bind(op, &ctr);
@@ -137,11 +139,18 @@ void run_loop(const MonodomainOperator& op, Vec& y, long step0, long nsteps,
   for (long step = step0; step < step0 + nsteps; ++step) {
     const double t = static_cast<double>(step) * dt;
     try {
-      MultirateStepReport rep;
-      y = emrkc_step(t, y, dt, rhs, eps, EmrkcVariant::standard, &rep);
-      res->s = rep.s;
-      res->m = rep.m;
-      res->eta = rep.eta;
+      if (method == 2) {
+        y = exex_rl_step(t, y, dt, op, &ctr);
+        res->s = res->m = 1;
+        res->eta = dt;
+      } else {
+        MultirateStepReport rep;
+        y = emrkc_step(t, y, dt, rhs, eps,
+                       method == 1 ? EmrkcVariant::progressive : EmrkcVariant::standard, &rep);
+        res->s = rep.s;
+        res->m = rep.m;
+        res->eta = rep.eta;
+      }
     } catch (const NumericalAbort& e) {
       res->aborted = 1;
       res->abort_kind = EMRKC_ABORT_NONFINITE;
@@ -334,6 +343,18 @@ int ref_run(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
     const long len = op->layout().size();
     Vec yv(y, y + len);
     run_loop(*op, yv, step0, nsteps, dt, eps, rho_F, rho_S, res, wall_s);
+    std::memcpy(y, yv.data(), len * sizeof(double));
+  });
+}
+
+int ref_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
+                   double dt, double eps, int32_t method, double rho_F, double rho_S,
+                   emrkc_run_result* res, double* wall_s) {
+  return guarded([&] {
+    const auto op = make_op(p);
+    const long len = op->layout().size();
+    Vec yv(y, y + len);
+    run_loop(*op, yv, step0, nsteps, dt, eps, rho_F, rho_S, res, wall_s, method);
     std::memcpy(y, yv.data(), len * sizeof(double));
   });
 }

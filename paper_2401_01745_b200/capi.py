@@ -27,6 +27,7 @@ EMRKC_MODEL_HH = 0
 EMRKC_RHS_F = 0
 EMRKC_RHS_S = 1
 EMRKC_VARIANT_STANDARD = 0
+EMRKC_VARIANT_PROGRESSIVE = 1
 EMRKC_ABORT_NONE = 0
 EMRKC_ABORT_NONFINITE = 1
 EMRKC_ABORT_NORM_GUARD = 2
@@ -191,6 +192,8 @@ PROTOTYPES = {
     "emrkc_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_step_host": (C.c_int, [C.c_void_p, C.c_double, DP, DP, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
+    "emrkc_exex_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.POINTER(StepReport)]),
+    "emrkc_exex_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.POINTER(RunResult)]),
     "emrkc_run_timed": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.c_int64, DP, C.c_int64, C.POINTER(RunResult)]),
     "emrkc_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_void_p)]),
     "emrkc_group_destroy": (None, [C.c_void_p]),

@@ -140,17 +140,54 @@ double hh_current(double V, const double* z) {
 }
 
 // Per-step plan: plan_step (P/src/multirate.cpp:129-135) + coefficients.
+// Stepping methods of the device path (Method, P/include/mrkc/config.hpp:17).
+enum { kMethodEmrkc = 0, kMethodEmrkcProgressive = 1, kMethodExexRl = 2 };
+
 struct Plan {
   double dt = -1, eps = -1, rho_F = -1, rho_S = -1;
+  int method = -1;
   int s = 0, m = 0;
+  // gate rows of the averaged force: (u_m - z)/eta = gate_c (y_E - z)/eta.
+  // standard: u_m = y_E (the inner iterate starts at y_E and f vanishes on
+  // gate rows); progressive: the inner iteration starts at y with the
+  // constant forcing (y_E - y)/eta on gate rows (P/src/multirate.cpp:106-115),
+  // so u_m - y = c_m (y_E - y) with the inner RKC's c_m (= 1 up to rounding).
+  double gate_c = 1.0;
+  int exex = 0;
   double eta = 0, ell_s = 0, ell_m = 0, beta = 0;
   Coeffs outer, inner;
   std::vector<double> in_mueta;  // mu'_k * eta (rkc_iteration's k.mu[j]*dt)
   std::vector<double> mudt;      // mu_j * dt
 };
 
-int make_plan(double dt, double rho_F, double rho_S, double eps, Plan* p) {
+int make_plan(double dt, double rho_F, double rho_S, double eps, Plan* p,
+              int method = kMethodEmrkc) {
   if (!(dt > 0.0)) return set_global(EMRKC_EINVAL, "emrkc_step: dt must be > 0");
+  p->method = method;
+  p->gate_c = 1.0;
+  p->exex = 0;
+  if (method == kMethodExexRl) {
+    // exex_rl_step (P/src/baselines.cpp:192-210) as the one-stage kernel:
+    // gates y + expm1(dt Lambda)(y - y_inf), V + dt (f_F(V) + v_reaction at
+    // the new gates) = the m = s = 1 node update with eta = dt, mu_1 = 1,
+    // mu'_1 = 1 (so cG = 1 and cV = dt).
+    p->s = p->m = 1;
+    p->eta = dt;
+    p->ell_s = p->ell_m = p->beta = 0.0;
+    int rc;
+    if ((rc = coeffs(1, 0.05, &p->outer))) return rc;
+    if ((rc = coeffs(1, 0.05, &p->inner))) return rc;
+    p->in_mueta.assign(2, 0.0);
+    p->in_mueta[1] = dt;
+    p->mudt.assign(2, 0.0);
+    p->mudt[1] = dt;
+    p->exex = 1;
+    p->dt = dt;
+    p->eps = eps;
+    p->rho_F = rho_F;
+    p->rho_S = rho_S;
+    return EMRKC_OK;
+  }
   int rc = stages(dt, rho_S, eps, &p->s, &p->ell_s, &p->beta);
   if (rc) return rc;
   p->eta = 2.0 * dt / p->ell_s;
@@ -162,6 +199,7 @@ int make_plan(double dt, double rho_F, double rho_S, double eps, Plan* p) {
   for (int k = 1; k <= p->m; ++k) p->in_mueta[k] = p->inner.mu[k] * p->eta;
   p->mudt.assign(p->s + 1, 0.0);
   for (int j = 1; j <= p->s; ++j) p->mudt[j] = p->outer.mu[j] * dt;
+  if (method == kMethodEmrkcProgressive) p->gate_c = p->inner.c[p->m];
   p->dt = dt;
   p->eps = eps;
   p->rho_F = rho_F;
@@ -269,6 +307,7 @@ struct emrkc_handle {
   bool plan_uploaded = false;
   int fast = 1;
   int pipe = 1;
+  int method = 0;  // kMethod* of the next plan (set by the API entry point)
   // TMA descriptors (pipe == 3), encoded on first use per (pointer, kind)
   struct TmaEntry {
     const void* ptr;
@@ -339,9 +378,12 @@ int upload_plan(emrkc_handle* h, double dt, double rho_F, double rho_S,
                 double eps) {
   Plan& pl = h->plan;
   if (pl.dt == dt && pl.rho_F == rho_F && pl.rho_S == rho_S && pl.eps == eps &&
-      h->plan_uploaded)
+      pl.method == h->method && h->plan_uploaded)
     return EMRKC_OK;
-  int rc = make_plan(dt, rho_F, rho_S, eps, &pl);
+  if (h->method != kMethodEmrkc && !h->fast)
+    return set_err(h, EMRKC_EINVAL,
+                   "the progressive variant and EXEX-RL run on the fast kernels (EMRKC_FAST=1)");
+  int rc = make_plan(dt, rho_F, rho_S, eps, &pl, h->method);
   if (rc) return set_err(h, rc, "%s", g_global_err.c_str());
   const size_t need = 3 * (pl.m + 1);
   if (need > h->coef_cap) {
@@ -557,9 +599,10 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.u1 = h->u[3];
       f.eta = pl.eta;
       f.stim = a.stim;
-      f.cG = cG;
+      f.cG = cG * pl.gate_c;  // gate rows (progressive: c_m (y_E - z))
       f.cV = cG * pl.in_mueta[1];
       f.mue1 = pl.in_mueta[1];
+      f.exex = pl.exex;
       f.nu = a.nu;
       f.kappa = a.kappa;
       // fast ionic path only where its range analysis holds (fast_math.cuh)
@@ -1269,6 +1312,14 @@ fail:
 // ---------------------------------------------------------------------------
 // Run loop over a list of slabs in lockstep (one handle: the plain run).
 // ---------------------------------------------------------------------------
+// EmrkcVariant -> method (P/include/mrkc/multirate.hpp:37-40).
+int variant_method(int32_t variant, int* method) {
+  if (variant == EMRKC_VARIANT_STANDARD) *method = kMethodEmrkc;
+  else if (variant == EMRKC_VARIANT_PROGRESSIVE) *method = kMethodEmrkcProgressive;
+  else return EMRKC_EINVAL;
+  return EMRKC_OK;
+}
+
 int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
               int64_t nsteps, double dt, double eps, double rho_F,
               double rho_S, emrkc_run_result* res, bool single_step,
@@ -1605,13 +1656,31 @@ int emrkc_estimate_rho(emrkc_handle* h, int32_t which, double t,
   return power_iteration({h}, which, t, v0, rho0, out, v_out);
 }
 
+namespace {
+int step_impl(emrkc_handle* h, double t, double dt, double epsilon, double rho_F,
+              double rho_S, emrkc_step_report* report);
+}  // namespace
+
 int emrkc_step(emrkc_handle* h, double t, double dt, double epsilon,
                int32_t variant, double rho_F, double rho_S,
                emrkc_step_report* report) {
   if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (variant_method(variant, &h->method))
+    return set_err(h, EMRKC_EINVAL, "emrkc_step: unknown variant %d", variant);
+  return step_impl(h, t, dt, epsilon, rho_F, rho_S, report);
+}
+
+int emrkc_exex_step(emrkc_handle* h, double t, double dt, emrkc_step_report* report) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (!(dt > 0.0)) return set_err(h, EMRKC_EINVAL, "exex_rl_step: dt must be > 0");
+  h->method = kMethodExexRl;
+  return step_impl(h, t, dt, 0.05, 0.0, 0.0, report);
+}
+
+namespace {
+int step_impl(emrkc_handle* h, double t, double dt, double epsilon, double rho_F,
+              double rho_S, emrkc_step_report* report) {
   if (h->partitioned) return set_err(h, EMRKC_EINVAL, "emrkc_step: whole-grid handles only");
-  if (variant != EMRKC_VARIANT_STANDARD)
-    return set_err(h, EMRKC_EINVAL, "emrkc_step: only the standard variant is implemented");
   if (!(dt > 0.0)) return set_err(h, EMRKC_EINVAL, "emrkc_step: dt must be > 0");
   if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
   int rc = use_device(h);
@@ -1655,6 +1724,7 @@ int emrkc_step(emrkc_handle* h, double t, double dt, double epsilon,
   rep->abort_outer_stage = d.outer_stage;
   return set_err(h, EMRKC_ENONFINITE, "rkc_iteration: non-finite value at stage %d", d.stage);
 }
+}  // namespace
 
 int emrkc_step_host(emrkc_handle* h, double t, const double* y_in,
                     double* y_out, int64_t len, double dt, double epsilon,
@@ -1672,10 +1742,20 @@ int emrkc_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
               emrkc_run_result* res) {
   if (!h || !res) return set_global(EMRKC_EINVAL, "null argument");
   if (h->partitioned) return set_err(h, EMRKC_EINVAL, "emrkc_run: whole-grid handles only");
-  if (variant != EMRKC_VARIANT_STANDARD)
-    return set_err(h, EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
+  if (variant_method(variant, &h->method))
+    return set_err(h, EMRKC_EINVAL, "emrkc_run: unknown variant %d", variant);
   if (nsteps < 0) return set_err(h, EMRKC_EINVAL, "emrkc_run: nsteps must be >= 0");
   return run_slabs({h}, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr);
+}
+
+int emrkc_exex_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
+                   emrkc_run_result* res) {
+  if (!h || !res) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "emrkc_exex_run: whole-grid handles only");
+  if (!(dt > 0.0)) return set_err(h, EMRKC_EINVAL, "exex_rl_step: dt must be > 0");
+  if (nsteps < 0) return set_err(h, EMRKC_EINVAL, "emrkc_exex_run: nsteps must be >= 0");
+  h->method = kMethodExexRl;
+  return run_slabs({h}, step0, nsteps, dt, 0.05, 0.0, 0.0, res, false, nullptr);
 }
 
 int emrkc_run_timed(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
@@ -1685,8 +1765,8 @@ int emrkc_run_timed(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
   if (!h || !res || !launch_ms) return set_global(EMRKC_EINVAL, "null argument");
   if (h->partitioned && !dist_linked(h))
     return set_err(h, EMRKC_EINVAL, "emrkc_run_timed: whole-grid or distributed handles only");
-  if (variant != EMRKC_VARIANT_STANDARD)
-    return set_err(h, EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
+  if (variant_method(variant, &h->method))
+    return set_err(h, EMRKC_EINVAL, "emrkc_run: unknown variant %d", variant);
   if (nsteps < 0 || flush_bytes < 0) return set_err(h, EMRKC_EINVAL, "emrkc_run_timed: bad sizes");
   return run_slabs({h}, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr,
                    flush_bytes, launch_ms, launch_ms_len);
@@ -1753,8 +1833,10 @@ int emrkc_group_run(emrkc_group* g, int64_t step0, int64_t nsteps, double dt,
                     double epsilon, int32_t variant, double rho_F,
                     double rho_S, emrkc_run_result* res) {
   if (!g || !res) return set_global(EMRKC_EINVAL, "null argument");
-  if (variant != EMRKC_VARIANT_STANDARD)
-    return set_global(EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
+  int method = 0;
+  if (variant_method(variant, &method))
+    return set_global(EMRKC_EINVAL, "emrkc_run: unknown variant %d", variant);
+  for (auto* h : g->hs) h->method = method;
   return run_slabs(g->hs, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr);
 }
 
@@ -1832,8 +1914,8 @@ int emrkc_dist_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
                    double epsilon, int32_t variant, double rho_F,
                    double rho_S, emrkc_run_result* res) {
   if (!h || !res) return set_global(EMRKC_EINVAL, "null argument");
-  if (variant != EMRKC_VARIANT_STANDARD)
-    return set_err(h, EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
+  if (variant_method(variant, &h->method))
+    return set_err(h, EMRKC_EINVAL, "emrkc_run: unknown variant %d", variant);
   if (!h->partitioned) return set_err(h, EMRKC_EINVAL, "dist_run: handle is not a slab");
   return run_slabs({h}, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr);
 }
@@ -1876,9 +1958,11 @@ int emrkc_dist_lockstep_run(emrkc_handle* const* hs, int32_t n, int32_t replay,
                             int32_t variant, double rho_F, double rho_S,
                             emrkc_run_result* res) {
   if (!hs || n < 1 || !res) return set_global(EMRKC_EINVAL, "bad arguments");
-  if (variant != EMRKC_VARIANT_STANDARD)
-    return set_global(EMRKC_EINVAL, "emrkc_run: only the standard variant is implemented");
+  int method = 0;
+  if (variant_method(variant, &method))
+    return set_global(EMRKC_EINVAL, "emrkc_run: unknown variant %d", variant);
   std::vector<emrkc_handle*> v(hs, hs + n);
+  for (auto* h : v) h->method = method;
   for (auto* h : v) {
     if (!dist_linked(h)) return set_global(EMRKC_ESTATE, "dist_lockstep_run: handles not linked");
     if (replay) {

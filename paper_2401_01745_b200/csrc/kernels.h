@@ -81,6 +81,7 @@ struct FastArgs {
   double nu, kappa;   // outer nu_j, kappa_j (j >= 2)
   double vfast;       // |V| bound of the fast ionic path (0: never)
   int j, m, s, last, zc;
+  int exex;           // EXEX-RL step: non-finite values are not aborts (guard only)
   unsigned long long code_base;
   unsigned long long* event;
   unsigned long long* gate_slot;

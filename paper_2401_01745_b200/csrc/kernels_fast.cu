@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kFThreads, EMRKC_NODE_MINBLOCKS)
         pu += plane;
       } else {
         *po = r.o0;
-        guard |= fabs(r.o0) > 1e6;
+        guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       bad |= !(finite_hi(r.o0) && finite_hi(r.o1) && finite_hi(r.o2) && finite_hi(r.o3));
       if (z == 0 && h.put_lo) h.put_lo[c.ip] = r.o0;
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kFThreads, EMRKC_NODE_MINBLOCKS)
       po += plane;
       if (!FIRST) q2 += plane;
     }
-    if (bad) {
+    if (bad && !a.exex) {  // EXEX-RL never throws NumericalAbort
       const bool inner = inner_nonfinite<DIM>(g, h, G, c, o, a.eta);
       atomicMin(a.event, a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1)) +
                              (inner ? 1 : a.m + 1));
@@ -624,19 +624,19 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         *pu = r.o0;  // d_1
       } else {
         *po = r.o0;
-        guard |= fabs(r.o0) > 1e6;
+        guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       // one finiteness test per node: a non-finite output poisons the sum
       bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
       if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
       if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
-      if (a.last) {  // gates of an accepted step are finite: plain compares
-        const double mn = r.o1 < r.o2 ? r.o1 : r.o2;
-        const double mx = r.o1 < r.o2 ? r.o2 : r.o1;
-        glo = mn < glo ? mn : glo;
-        ghi = mx > ghi ? mx : ghi;
+      if (a.last) {  // std::min / std::max per value (NaN skipped), select form
+        glo = r.o1 < glo ? r.o1 : glo;
+        ghi = ghi < r.o1 ? r.o1 : ghi;
+        glo = r.o2 < glo ? r.o2 : glo;
+        ghi = ghi < r.o2 ? r.o2 : ghi;
         glo = r.o3 < glo ? r.o3 : glo;
-        ghi = r.o3 > ghi ? r.o3 : ghi;
+        ghi = ghi < r.o3 ? r.o3 : ghi;
       }
     }
     po += plane;
@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         a.u1[i] = r.o0;
       } else {
         a.out[i] = r.o0;
-        guard |= fabs(r.o0) > 1e6;
+        guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
       if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   }
   halo_signal(h, zb == 0, ze >= g.nzl);  // also when skipping: release the neighbours
   if (skipped) return;
-  if (bad) {
+  if (bad && !a.exex) {  // EXEX-RL never throws NumericalAbort
     Col<DIM> c;
     c.c0 = cx;
     c.c1 = cy;
@@ -869,18 +869,18 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
           *pu = rr.o0;
         } else {
           *po = rr.o0;
-          guard |= fabs(rr.o0) > 1e6;
+          guard |= !(fabs(rr.o0) <= 1e6);  // also a non-finite V
         }
         bad |= !finite_hi((rr.o0 + rr.o1) + (rr.o2 + rr.o3));
         if (z == 0 && h.put_lo) h.put_lo[ip] = rr.o0;
         if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = rr.o0;
-        if (a.last) {
-          const double mn = rr.o1 < rr.o2 ? rr.o1 : rr.o2;
-          const double mx = rr.o1 < rr.o2 ? rr.o2 : rr.o1;
-          glo = mn < glo ? mn : glo;
-          ghi = mx > ghi ? mx : ghi;
+        if (a.last) {  // std::min / std::max per value (NaN skipped), select form
+          glo = rr.o1 < glo ? rr.o1 : glo;
+          ghi = ghi < rr.o1 ? rr.o1 : ghi;
+          glo = rr.o2 < glo ? rr.o2 : glo;
+          ghi = ghi < rr.o2 ? rr.o2 : ghi;
           glo = rr.o3 < glo ? rr.o3 : glo;
-          ghi = rr.o3 > ghi ? rr.o3 : ghi;
+          ghi = ghi < rr.o3 ? rr.o3 : ghi;
           any = true;
         }
       }
@@ -931,7 +931,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
           a.u1[i] = rr.o0;
         } else {
           a.out[i] = rr.o0;
-          guard |= fabs(rr.o0) > 1e6;
+          guard |= !(fabs(rr.o0) <= 1e6);  // also a non-finite V
         }
         bad |= !finite_hi((rr.o0 + rr.o1) + (rr.o2 + rr.o3));
         if (z == 0 && h.put_lo) h.put_lo[ip] = rr.o0;
@@ -944,7 +944,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
       }
     }
     halo_signal(h, zb == 0, ze >= g.nzl);
-    if (bad) {
+    if (bad && !a.exex) {  // EXEX-RL never throws NumericalAbort
       const bool inner = valid && inner_nonfinite<DIM>(g, h, G, Col<DIM>{cx, cy, ip, zb, ze, true},
                                                        nbr_of<DIM>(g, Col<DIM>{cx, cy, ip, zb, ze, true}),
                                                        a.eta);
@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
         const double o0 = fma(a.cG, dk, b0);
         a.outv[i] = o0;
         bad_out |= !finite_hi(o0);
-        guard |= fabs(o0) > 1e6;
+        guard |= !(fabs(o0) <= 1e6);  // also a non-finite V
         vput = o0;
       }
       if (z == 0 && h.put_lo) h.put_lo[ip] = vput;
@@ -1169,25 +1169,14 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   const int zb = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
   const int ze = min(g.nzl, zb + a.zc);
   pdl_launch_dependents();
-  // prologue that reads nothing the previous kernel writes
-  for (int j = t; j < 256; j += T::NT) tab[j] = kExp2Tab256[j];
-  if (t == 0) {
+  if (t == 0) {  // prologue that reads nothing the previous kernel writes
     for (int s = 0; s < kRV; ++s) mbar_init(smem_u32(&bars[s]), 1);
     mbar_fence_init();
     prefetch_tensormap(&tm.v);
     prefetch_tensormap(&tm.gates);
     if (!FIRST) prefetch_tensormap(&tm.g2);
   }
-  pdl_wait();
-  halo_wait(h, zb == 0, ze >= g.nzl);
-  if (t == 0) {
-    // ghost planes arrived through generic peer stores (acquired in
-    // halo_wait); order them before this thread's async-proxy reads
-    fence_proxy_async();
-    skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
-  }
-  __syncthreads();
-  const bool skipped = skip != 0;
+  __syncthreads();  // barriers initialised before any warp issues onto them
   const int tx = t % T::TX, ty = t / T::TX;
   const int x0 = blockIdx.x * T::TX;
   const int y0 = DIM == 3 ? blockIdx.y * T::TY : 0;
@@ -1199,41 +1188,67 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   const unsigned b0 = smem_u32(bars);
   constexpr unsigned vbytes = 8u * TmaTile<DIM>::VT;
   const unsigned cbytes = 8u * T::NT * (3 + (FIRST ? 0 : 4));
-  // thread 0: plane zz in [zb, ze) (interior of the slab): V box + gate boxes
-  auto issue_comp = [&](int zz) {
+  // The copies of a plane are issued by lane 0 of warps 0 (expect_tx + V
+  // box), 1 (gate box) and 2 (g_{j-2} box): the issue work is spread over
+  // three warps instead of serialising one before the per-plane barrier.
+  const int role = (t & 31) == 0 ? (t >> 5) : -1;
+  auto issue_comp = [&](int zz) {  // plane zz in [zb, ze)
     const int q = zz - zb + 1;
     const unsigned bar = b0 + 8u * (q & (kRV - 1));
-    const unsigned vd = v0 + 8u * VS * (q & (kRV - 1));
     const unsigned sg = (unsigned)((zz - zb) & (kRG - 1));
-    mbar_expect_tx(bar, vbytes + cbytes);
-    if (DIM == 3) {
-      tma_load_3d(vd, &tm.v, bar, x0 - 2, y0 - 1, zz);
-      tma_load_4d(gs0 + 8u * 3 * T::NT * sg, &tm.gates, bar, x0, y0, zz, 1);
-      if (!FIRST) tma_load_4d(qs0 + 8u * 4 * T::NT * sg, &tm.g2, bar, x0, y0, zz, 0);
-    } else {
-      tma_load_2d(vd, &tm.v, bar, x0 - 2, zz);
-      tma_load_3d(gs0 + 8u * 3 * T::NT * sg, &tm.gates, bar, x0, zz, 1);
-      if (!FIRST) tma_load_3d(qs0 + 8u * 4 * T::NT * sg, &tm.g2, bar, x0, zz, 0);
+    if (role == 0) {
+      mbar_expect_tx(bar, vbytes + cbytes);
+      const unsigned vd = v0 + 8u * VS * (q & (kRV - 1));
+      if (DIM == 3) tma_load_3d(vd, &tm.v, bar, x0 - 2, y0 - 1, zz);
+      else tma_load_2d(vd, &tm.v, bar, x0 - 2, zz);
+    } else if (role == 1) {
+      if (DIM == 3) tma_load_4d(gs0 + 8u * 3 * T::NT * sg, &tm.gates, bar, x0, y0, zz, 1);
+      else tma_load_3d(gs0 + 8u * 3 * T::NT * sg, &tm.gates, bar, x0, zz, 1);
+    } else if (!FIRST && role == 2) {
+      if (DIM == 3) tma_load_4d(qs0 + 8u * 4 * T::NT * sg, &tm.g2, bar, x0, y0, zz, 0);
+      else tma_load_3d(qs0 + 8u * 4 * T::NT * sg, &tm.g2, bar, x0, zz, 0);
     }
   };
-  // thread 0: halo plane zb - 1 or ze (V only; mirror or ghost at the slab edge)
-  auto issue_edge = [&](int zz) {
+  // halo plane zb - 1 or ze (V only; mirror or ghost at the slab edge)
+  auto issue_edge = [&](int zz, unsigned extra) {
+    if (role != 0) return;
     const int q = zz - zb + 1;
     const unsigned bar = b0 + 8u * (q & (kRV - 1));
-    mbar_expect_tx(bar, vbytes);
+    mbar_expect_tx(bar, vbytes + extra);
     tma_vplane<DIM>(g, &tm.v, &tm.glo, &tm.ghi, h.lo != nullptr, h.hi != nullptr,
                     v0 + 8u * VS * (q & (kRV - 1)), bar, x0, y0, zz);
   };
-  if (!skipped && t == 0) {
-    issue_edge(zb - 1);
-    for (int i = 0; i < kTmaLA; ++i) {
+  pdl_wait();
+  halo_wait(h, zb == 0, ze >= g.nzl);
+  int nq = 0;  // prologue loads (planes zb - 1 ...)
+  if (role >= 0 && role <= 2) {
+    if (role == 0) {
+      // ghost planes arrived through generic peer stores (acquired in
+      // halo_wait); order them before this thread's async-proxy reads
+      fence_proxy_async();
+      bulk_load(smem_u32(tab), kExp2Tab256, sizeof(double) * 256, b0);  // exp table
+    }
+    issue_edge(zb - 1, sizeof(double) * 256);
+    nq = 1;
+    for (int i = 0; i < kTmaLA; ++i, ++nq) {
       if (zb + i < ze) issue_comp(zb + i);
       else {
-        issue_edge(ze);
+        issue_edge(ze, 0);
+        ++nq;
         break;
       }
     }
   }
+  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  __syncthreads();
+  const bool skipped = skip != 0;
+  if (skipped) {  // aborted earlier: drain the prologue copies, release the neighbours
+    const int np = 1 + min(kTmaLA, ze - zb) + (ze - zb < kTmaLA ? 1 : 0);
+    for (int q = 0; q < np; ++q) mbar_wait(b0 + 8u * q, 0);
+    halo_signal(h, zb == 0, ze >= g.nzl);
+    return;
+  }
+  (void)nq;
   // mirrored in-plane neighbours at the grid edge (halo cells there are 0)
   constexpr int HXT = TmaTile<DIM>::HX;
   const int cell = (DIM == 3 ? (ty + 1) * HXT : 0) + tx + 2;
@@ -1255,9 +1270,9 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   }
   for (int z = zb; z < ze && !skipped; ++z) {
     const int p = z - zb + 1;
-    if (t == 0) {
+    if (role >= 0) {
       if (z + kTmaLA < ze) issue_comp(z + kTmaLA);
-      else if (z + kTmaLA == ze) issue_edge(ze);
+      else if (z + kTmaLA == ze) issue_edge(ze, 0);
     }
     mbar_wait(b0 + 8u * ((p + 1) & (kRV - 1)), ((p + 1) >> 3) & 1);
     const double* V0 = vst + (p & (kRV - 1)) * VS;
@@ -1286,18 +1301,18 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         *pu = r.o0;
       } else {
         *po = r.o0;
-        guard |= fabs(r.o0) > 1e6;
+        guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
       if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
       if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
-      if (a.last) {  // select form: fmin / fmax on doubles expand to ~10 instructions
-        const double mn = r.o1 < r.o2 ? r.o1 : r.o2;
-        const double mx = r.o1 < r.o2 ? r.o2 : r.o1;
-        glo = mn < glo ? mn : glo;
-        ghi = mx > ghi ? mx : ghi;
+      if (a.last) {  // std::min / std::max per value (NaN skipped), select form
+        glo = r.o1 < glo ? r.o1 : glo;
+        ghi = ghi < r.o1 ? r.o1 : ghi;
+        glo = r.o2 < glo ? r.o2 : glo;
+        ghi = ghi < r.o2 ? r.o2 : ghi;
         glo = r.o3 < glo ? r.o3 : glo;
-        ghi = r.o3 > ghi ? r.o3 : ghi;
+        ghi = ghi < r.o3 ? r.o3 : ghi;
       }
     }
     po += plane;
@@ -1330,7 +1345,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         a.u1[i] = r.o0;
       } else {
         a.out[i] = r.o0;
-        guard |= fabs(r.o0) > 1e6;
+        guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
       if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
@@ -1343,7 +1358,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   }
   halo_signal(h, zb == 0, ze >= g.nzl);
   if (skipped) return;
-  if (bad) {
+  if (bad && !a.exex) {  // EXEX-RL never throws NumericalAbort
     Col<DIM> c;
     c.c0 = cx;
     c.c1 = cy;
@@ -1386,16 +1401,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
     mbar_fence_init();
     prefetch_tensormap(&tm.u);
   }
-  pdl_wait();
-  halo_wait(h, zb == 0, ze >= g.nzl);
-  if (t == 0) {
-    // ghost planes arrived through generic peer stores (acquired in
-    // halo_wait); order them before this thread's async-proxy reads
-    fence_proxy_async();
-    skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
-  }
-  __syncthreads();
-  const bool skipped = skip != 0;
+  __syncthreads();  // barriers initialised before any warp issues onto them
   const int tx = t % T::TX, ty = t / T::TX;
   const int x0 = blockIdx.x * T::TX;
   const int y0 = DIM == 3 ? blockIdx.y * T::TY : 0;
@@ -1413,29 +1419,40 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
     if (DIM == 3) tma_load_3d(dst, m, bar, x0, y0, zz);
     else tma_load_2d(dst, m, bar, x0, zz);
   };
-  auto issue_comp = [&](int zz) {  // thread 0, zz in [zb, ze)
+  // lane 0 of warp 0 (expect_tx + halo box), 1 (d_1, d_{k-2}), 2 (V of
+  // g_{j-1}, g_{j-2}) issue a plane's copies
+  const int role = (t & 31) == 0 ? (t >> 5) : -1;
+  auto issue_comp = [&](int zz) {  // zz in [zb, ze)
     const int q = zz - zb + 1;
     const unsigned bar = b0 + 8u * (q & (kRV - 1));
-    mbar_expect_tx(bar, vbytes + cbytes);
-    const unsigned vd = v0 + 8u * VS * (q & (kRV - 1));
-    if (DIM == 3) tma_load_3d(vd, &tm.u, bar, x0 - 2, y0 - 1, zz);
-    else tma_load_2d(vd, &tm.u, bar, x0 - 2, zz);
     const unsigned sc = c0 + 8u * 4 * T::NT * ((zz - zb) & (kRG - 1));
-    if (!d1_is_u) center(&tm.d1, sc, bar, zz);
-    if (has2) center(&tm.um2, sc + 8u * T::NT, bar, zz);
-    if (LAST) {
+    if (role == 0) {
+      mbar_expect_tx(bar, vbytes + cbytes);
+      const unsigned vd = v0 + 8u * VS * (q & (kRV - 1));
+      if (DIM == 3) tma_load_3d(vd, &tm.u, bar, x0 - 2, y0 - 1, zz);
+      else tma_load_2d(vd, &tm.u, bar, x0 - 2, zz);
+    } else if (role == 1) {
+      if (!d1_is_u) center(&tm.d1, sc, bar, zz);
+      if (has2) center(&tm.um2, sc + 8u * T::NT, bar, zz);
+    } else if (LAST && role == 2) {
       center(&tm.g1v, sc + 16u * T::NT, bar, zz);
       if (!FIRST) center(&tm.g2v, sc + 24u * T::NT, bar, zz);
     }
   };
-  auto issue_edge = [&](int zz) {  // thread 0, zz = zb - 1 or ze
+  auto issue_edge = [&](int zz) {  // zz = zb - 1 or ze
+    if (role != 0) return;
     const int q = zz - zb + 1;
     const unsigned bar = b0 + 8u * (q & (kRV - 1));
     mbar_expect_tx(bar, vbytes);
     tma_vplane<DIM>(g, &tm.u, &tm.glo, &tm.ghi, true, true, v0 + 8u * VS * (q & (kRV - 1)), bar,
                     x0, y0, zz);
   };
-  if (!skipped && t == 0) {
+  pdl_wait();
+  halo_wait(h, zb == 0, ze >= g.nzl);
+  if (role >= 0 && role <= 2) {
+    // ghost planes arrived through generic peer stores (acquired in
+    // halo_wait); order them before this thread's async-proxy reads
+    if (role == 0) fence_proxy_async();
     issue_edge(zb - 1);
     for (int i = 0; i < kTmaLA; ++i) {
       if (zb + i < ze) issue_comp(zb + i);
@@ -1444,6 +1461,15 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
         break;
       }
     }
+  }
+  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  __syncthreads();
+  const bool skipped = skip != 0;
+  if (skipped) {  // aborted earlier: drain the prologue copies, release the neighbours
+    const int np = 1 + min(kTmaLA, ze - zb) + (ze - zb < kTmaLA ? 1 : 0);
+    for (int q = 0; q < np; ++q) mbar_wait(b0 + 8u * q, 0);
+    halo_signal(h, zb == 0, ze >= g.nzl);
+    return;
   }
   constexpr int HXT = TmaTile<DIM>::HX;
   const int cell = (DIM == 3 ? (ty + 1) * HXT : 0) + tx + 2;
@@ -1456,7 +1482,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
   }
   for (int z = zb; z < ze && !skipped; ++z) {
     const int p = z - zb + 1;
-    if (t == 0) {
+    if (role >= 0) {
       if (z + kTmaLA < ze) issue_comp(z + kTmaLA);
       else if (z + kTmaLA == ze) issue_edge(ze);
     }
@@ -1483,7 +1509,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
         const double o0 = fma(a.cG, dk, bb);
         a.outv[i] = o0;
         bad_out |= !finite_hi(o0);
-        guard |= fabs(o0) > 1e6;
+        guard |= !(fabs(o0) <= 1e6);  // also a non-finite V
         vput = o0;
       }
       if (z == 0 && h.put_lo) h.put_lo[ip] = vput;
@@ -1537,7 +1563,7 @@ __global__ void __launch_bounds__(kFThreads)
         const double o0 = fma(a.cG, dk, b0);
         a.outv[i] = o0;
         bad_out |= !finite_hi(o0);
-        guard |= fabs(o0) > 1e6;
+        guard |= !(fabs(o0) <= 1e6);  // also a non-finite V
         vput = o0;
       }
       if (z == 0 && h.put_lo) h.put_lo[c.ip] = vput;

@@ -257,11 +257,11 @@ class MonodomainOperator:
         return RhoEstimate(res.rho, res.iterations, bool(res.converged), res.safety, v)
 
     def step(self, t: float, dt: float, rho_F: float, rho_S: float,
-             epsilon: float = kDefaultDamping) -> StepReport:
+             epsilon: float = kDefaultDamping,
+             variant: int = capi.EMRKC_VARIANT_STANDARD) -> StepReport:
         """One emRKC step of the device-resident state (P/src/multirate.cpp:173-189)."""
         rep = StepReport()
-        rc = _lib().emrkc_step(self._h, t, dt, epsilon, capi.EMRKC_VARIANT_STANDARD, rho_F, rho_S,
-                               C.byref(rep))
+        rc = _lib().emrkc_step(self._h, t, dt, epsilon, variant, rho_F, rho_S, C.byref(rep))
         if rc == capi.EMRKC_ENONFINITE:
             raise NumericalAbort(_lib().emrkc_last_error(self._h).decode(), rep.abort_stage,
                                  inner=bool(rep.abort_inner))
@@ -302,11 +302,26 @@ class MonodomainOperator:
         return launch_ms, res.as_dict()
 
     def run(self, step0: int, nsteps: int, dt: float, rho_F: float, rho_S: float,
-            epsilon: float = kDefaultDamping) -> RunResult:
-        """run_simulation's emRKC loop on the device (P/src/simulate.cpp:176-229)."""
+            epsilon: float = kDefaultDamping,
+            variant: int = capi.EMRKC_VARIANT_STANDARD) -> RunResult:
+        """run_simulation's emRKC loop on the device (P/src/simulate.cpp:176-229);
+        variant: EmrkcVariant (Method::emrkc / emrkc_progressive)."""
         res = RunResult()
-        _check(_lib().emrkc_run(self._h, step0, nsteps, dt, epsilon, capi.EMRKC_VARIANT_STANDARD,
+        _check(_lib().emrkc_run(self._h, step0, nsteps, dt, epsilon, variant,
                                 rho_F, rho_S, C.byref(res)), self._h)
+        return res
+
+    def exex_step(self, t: float, dt: float) -> StepReport:
+        """One EXEX-RL step of the device state (exex_rl_step,
+        P/src/baselines.cpp:192-210); never raises NumericalAbort."""
+        rep = StepReport()
+        _check(_lib().emrkc_exex_step(self._h, t, dt, C.byref(rep)), self._h)
+        return rep
+
+    def exex_run(self, step0: int, nsteps: int, dt: float) -> RunResult:
+        """run_simulation's exex_rl loop (P/src/simulate.cpp:164-165,176-229)."""
+        res = RunResult()
+        _check(_lib().emrkc_exex_run(self._h, step0, nsteps, dt, C.byref(res)), self._h)
         return res
 
 
@@ -331,7 +346,8 @@ def estimate_spectral_radius(op: MonodomainOperator, which: int, y: np.ndarray, 
 
 
 def emrkc_step(t: float, y: np.ndarray, dt: float, rhs: SplitRhs,
-               epsilon: float = kDefaultDamping, report: StepReport | None = None) -> np.ndarray:
+               epsilon: float = kDefaultDamping, report: StepReport | None = None,
+               variant: int = capi.EMRKC_VARIANT_STANDARD) -> np.ndarray:
     """Drop-in of ``Vec emrkc_step(t, y, dt, rhs, eps, variant, report)``:
     host vector in, host vector out, one device step in between."""
     y = np.ascontiguousarray(y, dtype=np.float64)
@@ -339,7 +355,7 @@ def emrkc_step(t: float, y: np.ndarray, dt: float, rhs: SplitRhs,
     rep = report if report is not None else StepReport()
     h = rhs.op.handle
     rc = _lib().emrkc_step_host(h, t, dptr(y), dptr(out), y.size, dt, epsilon,
-                                capi.EMRKC_VARIANT_STANDARD, rhs.rho_F, rhs.rho_S, C.byref(rep))
+                                variant, rhs.rho_F, rhs.rho_S, C.byref(rep))
     if rc == capi.EMRKC_ENONFINITE:
         raise NumericalAbort(_lib().emrkc_last_error(h).decode(), rep.abort_stage,
                              inner=bool(rep.abort_inner))
@@ -348,6 +364,14 @@ def emrkc_step(t: float, y: np.ndarray, dt: float, rhs: SplitRhs,
     rhs.counters["n_fS"] += rep.n_fS
     rhs.counters["n_exp_steps"] += rep.n_exp
     return out
+
+
+def exex_rl_step(t: float, y: np.ndarray, dt: float, op: MonodomainOperator) -> np.ndarray:
+    """Drop-in of ``Vec exex_rl_step(t, y, dt, prob, counters)``
+    (P/src/baselines.cpp:192-210): host vector in, one device step, host out."""
+    op.set_state(np.ascontiguousarray(y, dtype=np.float64))
+    op.exex_step(t, dt)
+    return op.get_state()
 
 
 def run_emrkc(problem: Problem, y0: np.ndarray, dt: float, n_steps: int,

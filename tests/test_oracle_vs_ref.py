@@ -57,3 +57,59 @@ def test_single_step_abort_records(oracle, reference):
     assert rca == rcb == 2
     assert ra.abort_stage == rb.abort_stage == 1
     assert (ra.n_fF, ra.n_fS, ra.n_exp) == (rb.n_fF, rb.n_fS, rb.n_exp)
+
+
+def _same_records(ra, rb):
+    for k, _ in ra._fields_:
+        if k != "device_ms":
+            va, vb = getattr(ra, k), getattr(rb, k)
+            assert va == vb or (va != va and vb != vb), k
+
+
+@pytest.mark.parametrize("name,nsteps", [("p2d_128_s3m2", 10), ("p3d_48_s2m2", 4),
+                                         ("hh2d_256x256", 20)])
+def test_progressive_variant_bitwise(oracle, reference, name, nsteps):
+    """emRKC progressive (P/src/multirate.cpp:106-115): restatement vs reference."""
+    w = workloads.get(name)
+    p = w.problem
+    y0 = w.initial_state()
+    eF, _ = reference.estimate_rho(p, 0, 0.0, y0)
+    rS = w.rho_S_forced if w.rho_S_forced is not None else reference.estimate_rho(p, 1, 0.0, y0)[0].rho
+    ya, ra, _ = oracle.run_method(p, y0, 0, nsteps, w.dt, oracle.EMRKC_PROGRESSIVE, w.eps, eF.rho, rS)
+    yb, rb, _ = reference.run_method(p, y0, 0, nsteps, w.dt, reference.EMRKC_PROGRESSIVE, w.eps,
+                                     eF.rho, rS)
+    assert np.array_equal(ya, yb)
+    _same_records(ra, rb)
+    # for HH (no aux) the V rows equal the standard variant's; gates differ
+    # only by rounding (constant forcing on gate rows)
+    ys, _, _ = oracle.run_method(p, y0, 0, nsteps, w.dt, oracle.EMRKC, w.eps, eF.rho, rS)
+    for b in range(4):
+        assert oracle.rel_l2(p, ya[b * p.n_nodes:(b + 1) * p.n_nodes],
+                             ys[b * p.n_nodes:(b + 1) * p.n_nodes]) < 1e-12
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_exex_rl_bitwise(oracle, reference, dim):
+    """EXEX-RL (P/src/baselines.cpp:192-210) inside run_simulation's loop."""
+    w = workloads.get("p2d_128_s3m2" if dim == 2 else "p3d_48_s2m2")
+    p = w.problem
+    y0 = w.initial_state()
+    ya, ra, _ = oracle.run_method(p, y0, 0, 60, 0.002, oracle.EXEX_RL)
+    yb, rb, _ = reference.run_method(p, y0, 0, 60, 0.002, reference.EXEX_RL)
+    assert np.array_equal(ya, yb)
+    _same_records(ra, rb)
+    assert ra.n_fF == ra.n_fS == ra.n_exp == 60 and not ra.aborted
+
+
+def test_exex_rl_nonfinite_gate(oracle, reference):
+    """exex_rl_step never throws: a NaN gate reaches V a step later and the
+    norm guard (max_abs_v -> inf) stops the run with the state assigned."""
+    w = workloads.get("p2d_128_s3m2")
+    p = w.problem
+    y0 = w.initial_state()
+    y0[p.n_nodes + 7] = np.nan
+    ya, ra, _ = oracle.run_method(p, y0, 2, 5, 0.002, oracle.EXEX_RL)
+    yb, rb, _ = reference.run_method(p, y0, 2, 5, 0.002, reference.EXEX_RL)
+    assert np.array_equal(ya, yb, equal_nan=True)
+    _same_records(ra, rb)
+    assert ra.aborted and ra.abort_kind == 2 and ra.abort_step == 2 and ra.steps_done == 1
