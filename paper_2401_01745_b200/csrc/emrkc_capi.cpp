@@ -308,6 +308,7 @@ struct emrkc_handle {
   int fast = 1;
   int pipe = 1;
   int method = 0;  // kMethod* of the next plan (set by the API entry point)
+  int tb = 1;      // temporally blocked inner stages (EMRKC_TB)
   // TMA descriptors (pipe == 3), encoded on first use per (pointer, kind)
   struct TmaEntry {
     const void* ptr;
@@ -556,6 +557,42 @@ int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out) {
   return EMRKC_OK;
 }
 
+// 3-D map over one V-sized field (n0, n1, nzl) with box (bx, by, 1); key
+// distinguishes box shapes in the cache (>= 100).
+int tma_map_box3(emrkc_handle* h, const void* ptr, cuuint32_t bx, cuuint32_t by, int key,
+                 CUtensorMap* out) {
+  for (const auto& e : h->tmaps)
+    if (e.ptr == ptr && e.kind == key) {
+      *out = e.map;
+      return EMRKC_OK;
+    }
+  const Geom& g = h->geom;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.n0), static_cast<cuuint64_t>(g.n1),
+                              static_cast<cuuint64_t>(g.nzl)};
+  const cuuint64_t strides[2] = {sizeof(double) * static_cast<cuuint64_t>(g.n0),
+                                 sizeof(double) * static_cast<cuuint64_t>(g.plane)};
+  const cuuint32_t box[3] = {bx, by, 1}, es[3] = {1, 1, 1};
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
+    return set_err(h, EMRKC_ECUDA, "TMA: buffer %p not 16-byte aligned", ptr);
+  CUtensorMap m;
+  const CUresult r = tma_encoder()(
+      &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(ptr), dims, strides, box, es,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(h, EMRKC_ECUDA, "cuTensorMapEncodeTiled failed (%d, key %d)", (int)r, key);
+  h->tmaps.push_back({ptr, key, m});
+  *out = m;
+  return EMRKC_OK;
+}
+
+// Temporally blocked inner stages (k_vin_tb) apply: 3-D whole-grid handle on
+// the TMA path with 2 <= m - 1 <= kTbMaxK (EMRKC_TB=0 disables).
+bool use_tb(const emrkc_handle* h, const Plan& pl) {
+  return h->tb && h->pipe == 3 && h->geom.dim == 3 && !h->partitioned && pl.m - 1 >= 2 &&
+         pl.m - 1 <= emrkc_k::kTbMaxK;
+}
+
 int tma_ghosts(emrkc_handle* h, const Halo& hl, CUtensorMap* lo, CUtensorMap* hi) {
   std::memset(lo, 0, sizeof *lo);
   std::memset(hi, 0, sizeof *hi);
@@ -630,6 +667,33 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         CK(h, emrkc_k::launch_node_pipe(h->geom, hl, f, pl.m >= 2, h->stream));
       else
         CK(h, emrkc_k::launch_node_fast(h->geom, hl, f, pl.m >= 2, h->stream));
+    } else if (use_tb(h, pl)) {
+      // stages 2..m in one pass at k == 2; levels k > 2 launch nothing
+      if (k == 2) {
+        emrkc_k::TbArgs f{};
+        f.coef = h->d_coef;
+        f.outv = a.out;
+        f.inv_mue1 = 1.0 / pl.in_mueta[1];
+        f.onu = a.nu;
+        f.okappa = a.kappa;
+        f.cG = cG;
+        f.j = j;
+        f.m = pl.m;
+        f.s = pl.s;
+        f.last = a.last;
+        f.zc = h->zc;
+        f.code_base = a.code_base;
+        f.event = a.event;
+        const int K = pl.m - 1;
+        emrkc_k::TmaTb tm;
+        std::memset(&tm, 0, sizeof tm);
+        int rc = tma_map_box3(h, h->u[3], emrkc_k::kTbTX + 2 * emrkc_k::kTbHX,
+                              emrkc_k::kTbTY + 2 * K, 100 + K, &tm.d1);
+        if (!rc) rc = tma_map_box3(h, a.g1, emrkc_k::kTbTX, emrkc_k::kTbTY, 99, &tm.g1v);
+        if (!rc && a.g2) rc = tma_map_box3(h, a.g2, emrkc_k::kTbTX, emrkc_k::kTbTY, 99, &tm.g2v);
+        if (rc) return rc;
+        CK(h, emrkc_k::launch_vin_tb(h->geom, f, tm, h->stream));
+      }
     } else {
       emrkc_k::FastInnerArgs f{};
       // increment form: d_1 stays in u[3] (it also gives a = d_1/(mu'_1 eta)),
@@ -772,6 +836,8 @@ int init_handle(emrkc_handle* h) {
   // node kernel, 0: march
   h->pipe = (pp && *pp) ? std::atoi(pp) : 3;
   if (h->pipe == 3 && !tma_supported(h)) h->pipe = 1;
+  if (const char* tb = std::getenv("EMRKC_TB"))
+    if (*tb) h->tb = std::atoi(tb) != 0;
   if (const char* zc = std::getenv("EMRKC_ZC"))
     if (*zc) h->zc = std::min(emrkc_k::kMaxZc, std::max(1, std::atoi(zc)));
   return EMRKC_OK;

@@ -107,6 +107,28 @@ struct FastInnerArgs {
   unsigned long long* event;
 };
 
+// Temporally blocked inner stages: one pass runs stages k = 2..m (m - 1 = K
+// fused V-only stages, 2 <= K <= kTbMaxK) of outer stage j (3-D, whole-grid
+// handles). Stage k is computed on the tile plus a halo of K + 1 - k cells
+// (recomputed), so only d_1 (halo K), V of g_{j-1} / g_{j-2} and V of g_j
+// touch HBM.
+constexpr int kTbMaxK = 4, kTbTX = 32, kTbTY = 8, kTbHX = 4;
+struct TbArgs {
+  const double* coef;  // device: in_mueta[0..m] | in_nu[0..m] | in_kappa[0..m]
+  double* outv;        // V block of g_j
+  double inv_mue1;     // 1 / (mu'_1 eta)
+  double onu, okappa, cG;  // outer nu_j, kappa_j, mu_j dt / eta
+  int j, m, s, last, zc;
+  unsigned long long code_base;
+  unsigned long long* event;
+};
+struct TmaTb {
+  CUtensorMap d1;      // d_1, box (kTbTX + 2 kTbHX, kTbTY + 2K, 1)
+  CUtensorMap g1v;     // V of g_{j-1}, box (kTbTX, kTbTY, 1)
+  CUtensorMap g2v;     // V of g_{j-2}
+};
+cudaError_t launch_vin_tb(const Geom& g, const TbArgs& a, const TmaTb& tm, cudaStream_t st);
+
 // TMA descriptors of one k_node_tma launch (host-encoded, passed as a
 // __grid_constant__ parameter). Boxes: V tile + 1-cell halo, gate fields,
 // g_{j-2} fields, ghost planes.

@@ -27,6 +27,7 @@
 #include "hh.cuh"
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 
 #include "kernels.h"
@@ -1527,6 +1528,234 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
 }
 
 // ---------------------------------------------------------------------------
+// k_vin_tb<K, FIRST>: inner stages k = 2 .. K+1 (= m) of outer stage j in one
+// pass over HBM (temporal blocking of the V-only inner iteration).
+//
+// A block owns a 32 x 8 tile and a z-chunk [zb, ze) of the final stage. It
+// marches planes t; at step t it receives d_1 of plane t (TMA, box with an
+// x halo of 4 and a y halo of K) and computes stage k at plane t - (k - 1)
+// for k = 2 .. K+1 on the tile grown by K + 1 - k cells, so stage k + 1 finds
+// the neighbours it needs; each stage keeps its last three planes in shared
+// memory. Stage K + 1 forms V of g_j = base + (mu_j dt / eta) d_m directly
+// (centres of V of g_{j-1}, g_{j-2} arrive with the plane group). Only d_1
+// (plus its halo), V of g_{j-1}, g_{j-2} and V of g_j touch HBM: 24-32 B per
+// node for all m - 1 stages instead of 16 + 32 (m - 3) + 40.
+// Neumann mirror: every stencil read maps index -1 -> 1 and n -> n - 2
+// (P/src/monodomain.cpp:85-86), in x, y and z; cells outside the grid are
+// never read. Recurrences exactly as k_vin_tma (increment form).
+// ---------------------------------------------------------------------------
+template <int K>
+struct TbTile {
+  static constexpr int TX = kTbTX, TY = kTbTY, NT = 256;
+  static constexpr int DX = TX + 2 * kTbHX;           // d_1 box width
+  static constexpr int DY = TY + 2 * K;               // d_1 box height
+  static constexpr int DS = ((DX * DY) + 15) & ~15;   // d_1 stage stride
+  static constexpr int RD = 8;                        // d_1 ring (>= K + 1 + look-ahead)
+  static constexpr int CS = TX * TY;                  // centre plane
+  __host__ __device__ static constexpr int h(int k) { return K + 1 - k; } // halo of stage k
+  __host__ __device__ static constexpr int PX(int k) { return TX + 2 * h(k); }
+  __host__ __device__ static constexpr int PY(int k) { return TY + 2 * h(k); }
+  __host__ __device__ static constexpr int PS(int k) { return PX(k) * PY(k); }
+  // offsets (doubles) of the stage rings k = 2..K (3 planes each), then centres
+  __host__ __device__ static constexpr int off_stage(int k) {
+    int o = RD * DS;
+    for (int i = 2; i < k; ++i) o += 3 * PS(i);
+    return o;
+  }
+  __host__ __device__ static constexpr int off_centre() { return (off_stage(K + 1) + 15) & ~15; }
+  __host__ __device__ static constexpr int total() { return off_centre() + 4 * 2 * CS; }
+};
+static_assert(TbTile<kTbMaxK>::DS * 0 == 0 && kTbMaxK + 1 + 3 <= 8, "d_1 ring");
+
+template <int K>
+constexpr size_t tb_smem_bytes() { return sizeof(double) * TbTile<K>::total() + 128; }
+
+// Compile-time loop: f(integral_constant<int, i>) for i in [B, E).
+template <int B, int E, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+__device__ __forceinline__ int mirror_idx(int i, int n) {
+  return i < 0 ? 1 : (i >= n ? n - 2 : i);
+}
+
+template <int K, int FIRST>
+__global__ void __launch_bounds__(TbTile<K>::NT, 2)
+    k_vin_tb(const Geom g, const TbArgs a, const __grid_constant__ TmaTb tm) {
+  using T = TbTile<K>;
+  constexpr int M = K + 1;  // m
+  extern __shared__ __align__(128) double smem_tma[];
+  double* sm = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;
+  __shared__ __align__(8) unsigned long long bars[8];
+  __shared__ double cf[3][kTbMaxK + 2];  // mu'_k eta, nu'_k, kappa'_k (k = 0..m)
+  __shared__ int skip;
+  const int t = threadIdx.x;
+  const int x0 = blockIdx.x * T::TX, y0 = blockIdx.y * T::TY;
+  const int zb = blockIdx.z * a.zc;
+  const int ze = min(g.nzl, zb + a.zc);
+  const int n0 = g.n0, n1 = g.n1, nz = g.nzl;
+  pdl_launch_dependents();
+  if (t == 0) {
+    for (int s = 0; s < 8; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    mbar_fence_init();
+    prefetch_tensormap(&tm.d1);
+    prefetch_tensormap(&tm.g1v);
+    if (!FIRST) prefetch_tensormap(&tm.g2v);
+  }
+  __syncthreads();
+  pdl_wait();
+  if (t < 3 * (M + 1)) cf[t / (M + 1)][t % (M + 1)] = a.coef[t];
+  const int lo1 = max(0, zb - K), hi1 = min(nz, ze + K);  // d_1 planes
+  const int tlast = ze - 1 + K;                           // last step
+  const unsigned b0 = smem_u32(bars);
+  const unsigned dbase = smem_u32(sm), cbase = smem_u32(sm + T::off_centre());
+  auto issue = [&](int s) {  // thread 0: load group of step s
+    const int i = s - lo1;
+    const unsigned bar = b0 + 8u * (i & 7);
+    const int q = s - K;
+    const bool hasd = s < hi1;
+    const bool hasc = q >= zb && q < ze;
+    const unsigned bytes = (hasd ? 8u * T::DX * T::DY : 0u) +
+                           (hasc ? 8u * T::CS * (FIRST ? 1 : 2) : 0u);
+    mbar_expect_tx(bar, bytes);
+    if (hasd) tma_load_3d(dbase + 8u * T::DS * (i & 7), &tm.d1, bar, x0 - kTbHX, y0 - K, s);
+    if (hasc) {
+      const unsigned cd = cbase + 8u * 2 * T::CS * (s & 3);
+      tma_load_3d(cd, &tm.g1v, bar, x0, y0, q);
+      if (!FIRST) tma_load_3d(cd + 8u * T::CS, &tm.g2v, bar, x0, y0, q);
+    }
+  };
+  if (t == 0) {
+    for (int s = lo1; s <= min(tlast, lo1 + kTmaLA - 1); ++s) issue(s);
+    skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  }
+  __syncthreads();
+  const int nlaunched = min(tlast, lo1 + kTmaLA - 1) - lo1 + 1;
+  if (skip) {
+    for (int i = 0; i < nlaunched; ++i) mbar_wait(b0 + 8u * i, 0);
+    return;
+  }
+  const double inv_mue1 = a.inv_mue1;
+  const long long plane = g.plane;
+  unsigned badk = 0u;  // bit k: stage k produced a non-finite interior value
+  bool bad_out = false, guard = false;
+  // Per-thread cells of every stage, fixed for the whole z-march: stage k's
+  // region cells t, t + 256, ... with their source / d_1 offsets, mirrored
+  // neighbour deltas (signed bytes: xm, xp, ym, yp), validity and ownership.
+  constexpr int NT = T::NT;
+  constexpr int NTOT = [] {
+    int n = 0;
+    for (int kk = 2; kk <= M; ++kk) n += (T::PS(kk) + NT - 1) / NT;
+    return n;
+  }();
+  int c_si[NTOT], c_d1[NTOT], c_dl[NTOT], c_out[NTOT], c_s2[NTOT];
+  unsigned c_f[NTOT];  // bit 0 valid, bit 1 own (tile interior)
+  static_for<2, M + 1>([&](auto kc) {
+    constexpr int kk = decltype(kc)::value;
+    constexpr int hk = T::h(kk), PXk = T::PX(kk);
+    constexpr int P = kk == 2 ? T::DX : T::PX(kk - 1);
+    constexpr int base = [] {
+      int b = 0;
+      for (int k2 = 2; k2 < kk; ++k2) b += (T::PS(k2) + NT - 1) / NT;
+      return b;
+    }();
+#pragma unroll
+    for (int i = 0; i < (T::PS(kk) + NT - 1) / NT; ++i) {
+      const int c = t + i * NT;
+      const int cy = c / PXk, cx = c - cy * PXk;
+      const int gx = x0 - hk + cx, gy = y0 - hk + cy;
+      const bool valid = c < T::PS(kk) && gx >= 0 && gx < n0 && gy >= 0 && gy < n1;
+      const bool own = cx >= hk && cx < hk + T::TX && cy >= hk && cy < hk + T::TY;
+      const int dxm = gx > 0 ? -1 : 1, dxp = gx < n0 - 1 ? 1 : -1;
+      const int dym = gy > 0 ? -P : P, dyp = gy < n1 - 1 ? P : -P;
+      c_si[base + i] = kk == 2 ? (cy + K - hk) * T::DX + (cx + kTbHX - hk) : (cy + 1) * P + (cx + 1);
+      c_d1[base + i] = (cy + K - hk) * T::DX + (cx + kTbHX - hk);
+      c_dl[base + i] = (dxm & 0xff) | ((dxp & 0xff) << 8) | ((dym & 0xff) << 16) |
+                       ((dyp & 0xff) << 24);
+      c_out[base + i] = gx + n0 * gy;                                    // final stage
+      c_s2[base + i] = kk >= 4 ? (cy + 2) * T::PX(kk - 2) + (cx + 2) : 0;  // d_{k-2}
+      c_f[base + i] = (valid ? 1u : 0u) | (own ? 2u : 0u);
+    }
+  });
+  for (int s = lo1; s <= tlast; ++s) {
+    if (t == 0 && s + kTmaLA <= tlast) issue(s + kTmaLA);
+    const int i = s - lo1;
+    mbar_wait(b0 + 8u * (i & 7), (i >> 3) & 1);
+    static_for<2, M + 1>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      const int q = s - (k - 1);
+      constexpr int hk = T::h(k);
+      constexpr int base = [] {
+        int b = 0;
+        for (int k2 = 2; k2 < k; ++k2) b += (T::PS(k2) + NT - 1) / NT;
+        return b;
+      }();
+      const bool active = q >= max(0, zb - hk) && q < min(nz, ze + hk);
+      if (active) {
+        const int qm = mirror_idx(q - 1, nz), qp = mirror_idx(q + 1, nz);
+        const double mueta = cf[0][k], nu = cf[1][k], kappa = cf[2][k];
+        const double* Sc;
+        const double* Sm;
+        const double* Sp;
+        if (k == 2) {
+          Sc = sm + ((q - lo1) & 7) * T::DS;
+          Sm = sm + ((qm - lo1) & 7) * T::DS;
+          Sp = sm + ((qp - lo1) & 7) * T::DS;
+        } else {
+          const double* S = sm + T::off_stage(k - 1);
+          Sc = S + (q % 3) * T::PS(k - 1);
+          Sm = S + (qm % 3) * T::PS(k - 1);
+          Sp = S + (qp % 3) * T::PS(k - 1);
+        }
+        const double* D1 = sm + ((q - lo1) & 7) * T::DS;
+        const double* S2 = k >= 4 ? sm + T::off_stage(k - 2) + (q % 3) * T::PS(k - 2) : nullptr;
+        const bool own_plane = q >= zb && q < ze;
+#pragma unroll
+        for (int ii = 0; ii < (T::PS(k) + NT - 1) / NT; ++ii) {
+          const int e = base + ii;
+          if (!(c_f[e] & 1u)) continue;
+          const int si = c_si[e], dl = c_dl[e];
+          const int dxm = (int)(signed char)(dl & 0xff), dxp = (int)(signed char)((dl >> 8) & 0xff);
+          const int dym = (int)(signed char)((dl >> 16) & 0xff), dyp = dl >> 24;
+          const double vc = Sc[si];
+          double D = fma(g.wc, vc, g.w[2] * (Sm[si] + Sp[si]));
+          D = fma(g.w[0], Sc[si + dxm] + Sc[si + dxp], D);
+          D = fma(g.w[1], Sc[si + dym] + Sc[si + dyp], D);
+          const double d1c = D1[c_d1[e]];
+          double bs = nu * vc;
+          if (k == 3) bs = fma(nu, vc, kappa * d1c);
+          if (k >= 4) bs = fma(nu, vc, kappa * S2[c_s2[e]]);
+          const double dk = fma(mueta, fma(d1c, inv_mue1, D), bs);
+          if ((c_f[e] & 2u) && own_plane && !finite_hi(dk)) badk |= 1u << k;
+          if (k < M) {
+            sm[T::off_stage(k) + (q % 3) * T::PS(k) + t + ii * NT] = dk;
+          } else {
+            // final stage: V of g_j (hk == 0: the cell indexes the tile)
+            const int c = t + ii * NT;
+            const double* C0 = sm + T::off_centre() + (s & 3) * 2 * T::CS;
+            const double bb = FIRST ? C0[c] : fma(a.onu, C0[c], a.okappa * C0[T::CS + c]);
+            const double o0 = fma(a.cG, dk, bb);
+            a.outv[(long long)c_out[e] + plane * q] = o0;
+            bad_out |= !finite_hi(o0);
+            guard |= !(fabs(o0) <= 1e6);  // also a non-finite V
+          }
+        }
+      }
+      __syncthreads();
+    });
+  }
+  const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
+  if (badk) atomicMin(a.event, base + (unsigned long long)(__ffs(badk) - 1));
+  if (bad_out) atomicMin(a.event, base + a.m + 1);
+  if (a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+}
+
+// ---------------------------------------------------------------------------
 // V-only inner stage k >= 2 (LAST: k == m, forms V of g_j).
 // ---------------------------------------------------------------------------
 template <int DIM, int LAST, int FIRST>
@@ -1777,6 +2006,30 @@ static cudaError_t launch_node_tma_t(const Geom& g, const Halo& h, const FastArg
   const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)
                           : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
   return launch_k(k_node_tma<D, F, I>, grd, dim3(T::NT), smem, st, g, h, a, tm);
+}
+
+template <int K, int F>
+static cudaError_t launch_vin_tb_t(const Geom& g, const TbArgs& a, const TmaTb& tm,
+                                   cudaStream_t st) {
+  constexpr size_t smem = tb_smem_bytes<K>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vin_tb<K, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int chunks = (g.nzl + a.zc - 1) / a.zc;
+  const dim3 grd((g.n0 + kTbTX - 1) / kTbTX, (g.n1 + kTbTY - 1) / kTbTY, chunks);
+  return launch_k(k_vin_tb<K, F>, grd, dim3(TbTile<K>::NT), smem, st, g, a, tm);
+}
+
+cudaError_t launch_vin_tb(const Geom& g, const TbArgs& a, const TmaTb& tm, cudaStream_t st) {
+  const bool first = a.j == 1;
+  switch (a.m - 1) {
+    case 2: return first ? launch_vin_tb_t<2, 1>(g, a, tm, st) : launch_vin_tb_t<2, 0>(g, a, tm, st);
+    case 3: return first ? launch_vin_tb_t<3, 1>(g, a, tm, st) : launch_vin_tb_t<3, 0>(g, a, tm, st);
+    case 4: return first ? launch_vin_tb_t<4, 1>(g, a, tm, st) : launch_vin_tb_t<4, 0>(g, a, tm, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_node_tma(const Geom& g, const Halo& h, const FastArgs& a, const TmaNode& tm,

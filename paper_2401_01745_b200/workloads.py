@@ -161,5 +161,16 @@ REGISTRY = {
 }
 
 
+def hh3d_cube(N: int, h: float) -> Workload:
+    """Non-BASELINE stiff cube (probe / temporal-blocking measurements): N^3,
+    spacing h mm, sigma as config 2, 8^3 corner stimulus, dt 0.05, T 5 ms."""
+    lo, hi = _box(h, [0, 0, 0], [7, 7, 7])
+    p = make_problem(3, [N] * 3, [h] * 3, [0.2, 0.1, 0.05], 140.0, 0.01, 70.0, lo, hi, 0.0, 1.0)
+    return Workload(f"hh3d_cube_{N}_h{h}", p, 0.05, 5.0, "v_normal_0.1", 90 + N)
+
+
 def get(name: str) -> Workload:
+    if name.startswith("hh3d_cube_"):  # hh3d_cube_<N>_h<h>
+        n, h = name[len("hh3d_cube_"):].split("_h")
+        return hh3d_cube(int(n), float(h))
     return REGISTRY[name]()
