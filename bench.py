@@ -55,6 +55,9 @@ KERNEL_BYTES = {
     ("m1", "outer"): 96,         # + g_{j-2} in
     ("first", "first_outer"): 64,  # g_{j-1} in (4); gates of g_j (3) + d_1 out
     ("first", "outer"): 88,        # + gates of g_{j-2}... (V of g_{j-2} read later)
+    ("tb", "first_outer"): 24,     # k_vin_tb: d_1, V of g_{j-1} in; V of g_j out
+    ("tb", "outer"): 32,           # + V of g_{j-2}
+    ("tb_skip", None): 0,          # stages 3..m ran inside the k = 2 launch
     ("inner2", None): 16,        # d_1 in, d_2 out
     ("inner", None): 32,         # d_{k-1}, d_{k-2}, d_1 in; d_k out
     ("last2", "first_outer"): 24,  # d_1, V of g_{j-1} in; V of g_j out
@@ -66,7 +69,9 @@ KERNEL_ROLES = {"m1": ("node", "m = 1: whole outer stage"),
                 "first": ("node", "m >= 2: ionic + inner stage 1"),
                 "inner2": ("vin", "inner stage 2"), "inner": ("vin", "inner stage k"),
                 "last2": ("vin", "last inner stage, m = 2"),
-                "last": ("vin", "last inner stage")}
+                "last": ("vin", "last inner stage"),
+                "tb": ("vin", "inner stages 2..m, temporally blocked"),
+                "tb_skip": ("vin", "fused into the k = 2 launch")}
 
 
 def kernel_name(kind: str, problem) -> str:
@@ -80,12 +85,23 @@ def kernel_name(kind: str, problem) -> str:
         pipe = 0
     role, what = KERNEL_ROLES[kind]
     fam = {3: "tma", 1: "pipe", 2: "persist" if role == "node" else "pipe", 0: "fast"}[pipe]
+    if kind.startswith("tb"):
+        fam = "tb"
     return f"k_{role}_{fam} ({what})"
 
 
-def launch_kinds(s: int, m: int):
+def tb_active(problem, m: int) -> bool:
+    """k_vin_tb runs stages 2..m (emrkc_capi.cpp use_tb): 3-D whole grid on
+    the TMA path, 2 <= m - 1 <= 4, EMRKC_TB != 0."""
+    pipe = int(os.environ.get("EMRKC_PIPE") or 3)
+    return (problem.dim == 3 and pipe == 3 and int(problem.n[0]) % 2 == 0
+            and int(os.environ.get("EMRKC_TB") or 1) != 0 and 2 <= m - 1 <= 4)
+
+
+def launch_kinds(s: int, m: int, problem=None):
     """(kind, outer) of each launch of one step, in launch order."""
     out = []
+    tb = problem is not None and tb_active(problem, m)
     for j in range(1, s + 1):
         o = "first_outer" if j == 1 else "outer"
         for k in range(1, m + 1):
@@ -93,6 +109,8 @@ def launch_kinds(s: int, m: int):
                 out.append(("m1", o))
             elif k == 1:
                 out.append(("first", o))
+            elif tb:
+                out.append(("tb", o) if k == 2 else ("tb_skip", None))
             elif k < m:
                 out.append(("inner2" if k == 2 else "inner", None))
             else:
@@ -397,7 +415,7 @@ def measure_e2e(op, w, y0, rF, rS, k):
 
 def roofline_of(m, w, peak, peak_kind):
     per_pos = m["launch_ms"].mean(axis=0)
-    kinds = launch_kinds(m["s"], m["m"])
+    kinds = launch_kinds(m["s"], m["m"], w.problem)
     dom = int(np.argmax(per_pos))
     kb = KERNEL_BYTES[kinds[dom]]
     achieved = kb * w.n_nodes / (per_pos[dom] * 1e-3) / 1e9
