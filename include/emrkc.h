@@ -216,7 +216,11 @@ int emrkc_step(emrkc_handle* h, double t, double dt, double epsilon,
 
 /* emrkc_step over host buffers: the per-call drop-in of
  * `Vec emrkc_step(t, const Vec& y, ...)` — copies y in, steps, copies the
- * result out (y_out may alias y_in). */
+ * result out (y_out may alias y_in). One-launch steps (s = m = 1) stream
+ * the state in z-chunks so the host->device copy, the step and the
+ * device->host copy overlap (pinned host buffers make the copies
+ * asynchronous). On EMRKC_ENONFINITE the device state is y_in and the
+ * contents of y_out are unspecified (the reference throws: no result). */
 int emrkc_step_host(emrkc_handle* h, double t, const double* y_in,
                     double* y_out, int64_t len, double dt, double epsilon,
                     int32_t variant, double rho_F, double rho_S,

@@ -309,6 +309,11 @@ struct emrkc_handle {
   int pipe = 1;
   int method = 0;  // kMethod* of the next plan (set by the API entry point)
   int tb = 1;      // temporally blocked inner stages (EMRKC_TB)
+  int zr_lo = -1, zr_hi = -1;  // node-kernel plane range override (< 0: all)
+  // pipelined host step (emrkc_step_host): copy streams and chunk events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  unsigned long long* h_event = nullptr;  // pinned copy of the abort word
+  std::vector<cudaEvent_t> ev_in, ev_k;
   // TMA descriptors (pipe == 3), encoded on first use per (pointer, kind)
   struct TmaEntry {
     const void* ptr;
@@ -640,6 +645,8 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.cV = cG * pl.in_mueta[1];
       f.mue1 = pl.in_mueta[1];
       f.exex = pl.exex;
+      f.z_lo = h->zr_lo >= 0 ? h->zr_lo : 0;  // plane range (pipelined host step)
+      f.z_hi = h->zr_lo >= 0 ? h->zr_hi : h->geom.nzl;
       f.nu = a.nu;
       f.kappa = a.kappa;
       // fast ionic path only where its range analysis holds (fast_math.cuh)
@@ -1062,6 +1069,11 @@ void emrkc_destroy(emrkc_handle* h) {
   if (h->d_red) cudaFree(h->d_red);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  for (auto e : h->ev_in) cudaEventDestroy(e);
+  for (auto e : h->ev_k) cudaEventDestroy(e);
+  if (h->h_event) cudaFreeHost(h->h_event);
+  if (h->s_in) cudaStreamDestroy(h->s_in);
+  if (h->s_out) cudaStreamDestroy(h->s_out);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -1792,10 +1804,130 @@ int step_impl(emrkc_handle* h, double t, double dt, double epsilon, double rho_F
 }
 }  // namespace
 
+namespace {
+// emrkc_step_host for one-launch steps (s = m = 1 on the TMA node kernel):
+// the state crosses the host link in z-chunks on two copy streams, and
+// chunk c is stepped as soon as chunks c and c + 1 (its upper halo plane)
+// have arrived, so host->device copies, the step and device->host copies
+// overlap (P/src/multirate.cpp:173-189 semantics unchanged: on a
+// NumericalAbort y_out is not written and the device state stays y_in).
+constexpr int kMaxHostChunks = 64;
+
+int host_chunks() {  // EMRKC_HOST_CHUNKS (default 16)
+  static int n = 0;
+  if (!n) {
+    const char* e = std::getenv("EMRKC_HOST_CHUNKS");
+    n = (e && *e) ? std::max(1, std::min(kMaxHostChunks, std::atoi(e))) : 16;
+  }
+  return n;
+}
+
+bool step_host_pipelined(emrkc_handle* h) {
+  return !h->partitioned && h->fast && h->pipe == 3 && h->plan.s == 1 && h->plan.m == 1 &&
+         host_chunks() > 1 && h->geom.nzl >= 2 * host_chunks();
+}
+
+int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
+                   emrkc_step_report* report) {
+  const int kHostChunks = host_chunks();
+  if (!h->s_in) {
+    CK(h, cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    CK(h, cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    h->ev_in.resize(kMaxHostChunks);
+    h->ev_k.resize(kMaxHostChunks);
+    for (int i = 0; i < kMaxHostChunks; ++i) {
+      CK(h, cudaEventCreateWithFlags(&h->ev_in[i], cudaEventDisableTiming));
+      CK(h, cudaEventCreateWithFlags(&h->ev_k[i], cudaEventDisableTiming));
+    }
+  }
+  const int64_t nn = h->nn, plane = h->geom.plane;
+  const int nz = h->geom.nzl;
+  auto zc = [&](int c) { return static_cast<int>(static_cast<int64_t>(c) * nz / kHostChunks); };
+  // abort word = no event (all ones), gate-range slots {min: all ones, max: 0}
+  CK(h, cudaMemsetAsync(h->d_event, 0xff, sizeof(unsigned long long), h->stream));
+  CK(h, cudaMemsetAsync(h->d_slots, 0xff, sizeof(unsigned long long), h->stream));
+  CK(h, cudaMemsetAsync(h->d_slots + 1, 0, sizeof(unsigned long long), h->stream));
+  CK(h, cudaEventRecord(h->ev0, h->stream));
+  CK(h, cudaStreamWaitEvent(h->s_in, h->ev0, 0));  // previous use of the buffers is done
+  const int in = h->cur;
+  double* din = h->buf[in];
+  const size_t pitch = sizeof(double) * nn;  // one row per SoA field
+  for (int c = 0; c < kHostChunks; ++c) {
+    const int64_t off = zc(c) * plane, n = (zc(c + 1) - zc(c)) * plane;
+    CK(h, cudaMemcpy2DAsync(din + off, pitch, y_in + off, pitch, sizeof(double) * n, 4,
+                            cudaMemcpyHostToDevice, h->s_in));
+    CK(h, cudaEventRecord(h->ev_in[c], h->s_in));
+  }
+  StepCtx sc;
+  begin_step(h, t, 0, h->d_slots, &sc);
+  const int outi = end_step(h, &sc);
+  int rc = EMRKC_OK;
+  for (int c = 0; c < kHostChunks && !rc; ++c) {
+    CK(h, cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
+    if (c + 1 < kHostChunks) CK(h, cudaStreamWaitEvent(h->stream, h->ev_in[c + 1], 0));
+    h->zr_lo = zc(c);
+    h->zr_hi = zc(c + 1);
+    rc = launch_level(h, &sc, 1, 1);
+    CK(h, cudaEventRecord(h->ev_k[c], h->stream));
+  }
+  h->zr_lo = h->zr_hi = -1;
+  if (rc) return rc;
+  double* dout = h->buf[outi];
+  for (int c = 0; c < kHostChunks; ++c) {
+    CK(h, cudaStreamWaitEvent(h->s_out, h->ev_k[c], 0));
+    const int64_t off = zc(c) * plane, n = (zc(c + 1) - zc(c)) * plane;
+    CK(h, cudaMemcpy2DAsync(y_out + off, pitch, dout + off, pitch, sizeof(double) * n, 4,
+                            cudaMemcpyDeviceToHost, h->s_out));
+  }
+  if (!h->h_event) CK(h, cudaHostAlloc(&h->h_event, sizeof(unsigned long long), 0));
+  CK(h, cudaMemcpyAsync(h->h_event, h->d_event, sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  CK(h, cudaStreamSynchronize(h->s_out));
+  const unsigned long long ev = *h->h_event;
+  h->has_state = true;
+  Decoded d = decode_event(ev, h->plan);
+  if (!d.none && d.guard) d = Decoded{};  // the guard belongs to the run loop
+  const Plan& pl = h->plan;
+  emrkc_step_report local;
+  emrkc_step_report* rep = report ? report : &local;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->s = pl.s;
+  rep->m = pl.m;
+  rep->eta = pl.eta;
+  rep->ell_s = pl.ell_s;
+  rep->ell_m = pl.ell_m;
+  rep->n_fF = 1;
+  rep->n_fS = 1;
+  rep->n_exp = 1;
+  if (d.none) {
+    h->cur = outi;
+    return EMRKC_OK;
+  }
+  h->cur = in;  // NumericalAbort: y is not assigned (P/src/simulate.cpp:215-220)
+  rep->n_fF = rep->n_fS = rep->n_exp = 0;
+  partial_counters(d, pl, &rep->n_fF, &rep->n_fS, &rep->n_exp);
+  rep->abort_kind = EMRKC_ABORT_NONFINITE;
+  rep->abort_stage = d.stage;
+  rep->abort_inner = d.inner;
+  rep->abort_outer_stage = d.outer_stage;
+  return set_err(h, EMRKC_ENONFINITE, "rkc_iteration: non-finite value at stage %d", d.stage);
+}
+}  // namespace
+
 int emrkc_step_host(emrkc_handle* h, double t, const double* y_in,
                     double* y_out, int64_t len, double dt, double epsilon,
                     int32_t variant, double rho_F, double rho_S,
                     emrkc_step_report* report) {
+  if (!h || !y_in || !y_out) return set_global(EMRKC_EINVAL, "null argument");
+  if (!h->partitioned && len == h->len && (dt > 0.0) && !variant_method(variant, &h->method)) {
+    int rc = use_device(h);
+    if (rc) return rc;
+    if ((rc = ensure_buffers(h, std::max(2, h->nbuf)))) return rc;
+    if ((rc = upload_plan(h, dt, rho_F, rho_S, epsilon))) return rc;
+    if ((rc = ensure_slots(h, 1))) return rc;
+    if (step_host_pipelined(h)) return step_host_pipe(h, t, y_in, y_out, report);
+  }
   int rc = emrkc_set_state(h, y_in, len);
   if (rc) return rc;
   rc = emrkc_step(h, t, dt, epsilon, variant, rho_F, rho_S, report);

@@ -82,6 +82,7 @@ struct FastArgs {
   double vfast;       // |V| bound of the fast ionic path (0: never)
   int j, m, s, last, zc;
   int exex;           // EXEX-RL step: non-finite values are not aborts (guard only)
+  int z_lo, z_hi;     // k_node_tma: local planes [z_lo, z_hi) of this launch (0, nzl: all)
   unsigned long long code_base;
   unsigned long long* event;
   unsigned long long* gate_slot;

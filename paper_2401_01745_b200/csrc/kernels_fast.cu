@@ -1167,8 +1167,8 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   __shared__ __align__(8) unsigned long long bars[kRV];
   __shared__ int skip;
   const int t = threadIdx.x;
-  const int zb = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
-  const int ze = min(g.nzl, zb + a.zc);
+  const int zb = a.z_lo + (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
+  const int ze = min(a.z_hi, zb + a.zc);
   pdl_launch_dependents();
   if (t == 0) {  // prologue that reads nothing the previous kernel writes
     for (int s = 0; s < kRV; ++s) mbar_init(smem_u32(&bars[s]), 1);
@@ -2002,7 +2002,7 @@ static cudaError_t launch_node_tma_t(const Geom& g, const Halo& h, const FastArg
                          (int)smem);
     attr = true;
   }
-  const int chunks = (g.nzl + a.zc - 1) / a.zc;
+  const int chunks = (a.z_hi - a.z_lo + a.zc - 1) / a.zc;
   const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)
                           : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
   return launch_k(k_node_tma<D, F, I>, grd, dim3(T::NT), smem, st, g, h, a, tm);

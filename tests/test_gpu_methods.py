@@ -121,3 +121,57 @@ def test_exex_step_dropin(oracle):
     with pytest.raises((ValueError, CudaError)):
         op.exex_step(0.0, -1.0)
     op.close()
+
+
+@pytest.mark.parametrize("name", ["hh3d_128x128x128", "hh2d_256x256"])
+def test_step_host_pipelined_matches_device_step(oracle, name):
+    """emrkc_step_host streams s = m = 1 steps in z-chunks (copies overlap the
+    step); results equal the device-resident step bit for bit."""
+    import ctypes as C
+    import torch
+
+    from paper_2401_01745_b200.capi import StepReport, dptr
+    from paper_2401_01745_b200.monodomain import _lib
+
+    w = workloads.get(name)
+    p = w.problem
+    y0 = w.initial_state()
+    op = MonodomainOperator(p)
+    op.set_state(y0)
+    rF = op.estimate_spectral_radius(0).rho
+    rS = op.estimate_spectral_radius(1).rho
+    ref = op
+    ref.step(0.0, w.dt, rF, rS, w.eps)
+    ref.step(w.dt, w.dt, rF, rS, w.eps)
+    y_dev = ref.get_state()
+    hin = torch.from_numpy(y0.copy()).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    h2 = MonodomainOperator(p)
+    rep = StepReport()
+    for k in range(2):
+        rc = _lib().emrkc_step_host(h2.handle, k * w.dt, C.cast(hin.data_ptr(), C.POINTER(C.c_double)),
+                                    C.cast(hout.data_ptr(), C.POINTER(C.c_double)), hin.numel(),
+                                    w.dt, w.eps, capi.EMRKC_VARIANT_STANDARD, rF, rS, C.byref(rep))
+        assert rc == 0
+        assert (rep.s, rep.m, rep.n_fF) == (1, 1, 1)
+        hin.copy_(hout)
+    assert np.array_equal(hout.numpy(), y_dev)
+    assert np.array_equal(h2.get_state(), y_dev)
+    # aliasing y_out = y_in
+    hin.copy_(torch.from_numpy(y0))
+    for k in range(2):
+        assert _lib().emrkc_step_host(h2.handle, k * w.dt, C.cast(hin.data_ptr(), C.POINTER(C.c_double)),
+                                      C.cast(hin.data_ptr(), C.POINTER(C.c_double)), hin.numel(),
+                                      w.dt, w.eps, 0, rF, rS, C.byref(rep)) == 0
+    assert np.array_equal(hin.numpy(), y_dev)
+    # NumericalAbort: device state stays y_in
+    bad = y0.copy()
+    bad[p.n_nodes + 3] = np.nan
+    hin.copy_(torch.from_numpy(bad))
+    rc = _lib().emrkc_step_host(h2.handle, 0.0, C.cast(hin.data_ptr(), C.POINTER(C.c_double)),
+                                C.cast(hout.data_ptr(), C.POINTER(C.c_double)), hin.numel(),
+                                w.dt, w.eps, 0, rF, rS, C.byref(rep))
+    assert rc == capi.EMRKC_ENONFINITE and rep.abort_stage == 1
+    assert np.array_equal(h2.get_state(), bad, equal_nan=True)
+    h2.close()
+    ref.close()
