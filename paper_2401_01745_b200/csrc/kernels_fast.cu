@@ -1565,7 +1565,9 @@ struct TbTile {
   __host__ __device__ static constexpr int off_centre() { return (off_stage(K + 1) + 15) & ~15; }
   __host__ __device__ static constexpr int total() { return off_centre() + 4 * 2 * CS; }
 };
-static_assert(TbTile<kTbMaxK>::DS * 0 == 0 && kTbMaxK + 1 + 3 <= 8, "d_1 ring");
+// d_1 ring: planes s - K .. s + look-ahead in 8 slots; centre ring: 4 slots
+// hold steps s .. s + look-ahead
+static_assert(kTbMaxK + 1 + kTmaLA <= 8 && kTmaLA + 1 <= 4, "k_vin_tb rings");
 
 template <int K>
 constexpr size_t tb_smem_bytes() { return sizeof(double) * TbTile<K>::total() + 128; }
