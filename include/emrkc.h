@@ -206,6 +206,15 @@ int emrkc_estimate_rho(emrkc_handle* h, int32_t which, double t,
                        const double* v0, double rho0, emrkc_rho_result* out,
                        double* v_out);
 
+/* rel_l2_error (P/src/monodomain.cpp:88-110: trapezoid-weighted L2 with
+ * the quadrature weights :52-63) of SoA block `block` (0 = V, 1..3 the
+ * gates) of the device state against `ref` (n_nodes values, host memory or,
+ * with ref_on_device != 0, device memory). EMRKC_EINVAL if ||ref|| = 0.
+ * Whole-grid handles. Reduction order differs from the reference's serial
+ * sum (~1e-16 relative). */
+int emrkc_rel_l2_error(emrkc_handle* h, int32_t block, const double* ref,
+                       int32_t ref_on_device, double* out);
+
 /* emrkc_step(t, y, dt, rhs, epsilon, variant, report)
  * (P/src/multirate.cpp:173-189) on the device-resident state. On a
  * non-finite stage it returns EMRKC_ENONFINITE, leaves the state

@@ -192,6 +192,7 @@ PROTOTYPES = {
     "emrkc_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_step_host": (C.c_int, [C.c_void_p, C.c_double, DP, DP, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
+    "emrkc_rel_l2_error": (C.c_int, [C.c_void_p, C.c_int32, DP, C.c_int32, DP]),
     "emrkc_exex_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_exex_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.POINTER(RunResult)]),
     "emrkc_run_timed": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.c_int64, DP, C.c_int64, C.POINTER(RunResult)]),

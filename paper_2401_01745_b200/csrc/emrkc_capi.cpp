@@ -303,6 +303,8 @@ struct emrkc_handle {
   double* d_coef = nullptr;  // in_mueta | in_nu | in_kappa (3*(m+1))
   size_t coef_cap = 0;
   double* d_red = nullptr;   // reduction partials + scalar
+  double* d_rel = nullptr;   // rel_l2_error partials
+  double* d_tmp = nullptr;   // one node field (host reference upload)
   Plan plan;
   bool plan_uploaded = false;
   int fast = 1;
@@ -1067,6 +1069,8 @@ void emrkc_destroy(emrkc_handle* h) {
   if (h->d_slots) cudaFree(h->d_slots);
   if (h->d_coef) cudaFree(h->d_coef);
   if (h->d_red) cudaFree(h->d_red);
+  if (h->d_rel) cudaFree(h->d_rel);
+  if (h->d_tmp) cudaFree(h->d_tmp);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   for (auto e : h->ev_in) cudaEventDestroy(e);
@@ -1109,6 +1113,37 @@ int emrkc_get_state(emrkc_handle* h, double* y, int64_t len) {
   CK(h, cudaMemcpyAsync(y, h->buf[h->cur], sizeof(double) * len,
                         cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
+  return EMRKC_OK;
+}
+
+int emrkc_rel_l2_error(emrkc_handle* h, int32_t block, const double* ref, int32_t ref_on_device,
+                       double* out) {
+  if (!h || !ref || !out) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "rel_l2_error: whole-grid handles only");
+  if (block < 0 || block > 3) return set_err(h, EMRKC_EINVAL, "rel_l2_error: block must be 0..3");
+  if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
+  int rc = use_device(h);
+  if (rc) return rc;
+  const int nb = 512;
+  if (!h->d_rel) CK(h, cudaMalloc(&h->d_rel, sizeof(double) * (2 * nb + 2)));
+  const double* b = ref;
+  if (!ref_on_device) {
+    if (!h->d_tmp) CK(h, cudaMalloc(&h->d_tmp, sizeof(double) * h->nn));
+    CK(h, cudaMemcpyAsync(h->d_tmp, ref, sizeof(double) * h->nn, cudaMemcpyHostToDevice,
+                          h->stream));
+    b = h->d_tmp;
+  }
+  CK(h, emrkc_k::launch_rel_l2(h->geom, h->buf[h->cur] + block * h->nn, b, h->d_rel, nb,
+                               h->d_rel + 2 * nb, h->stream));
+  double s[2] = {0.0, 0.0};
+  CK(h, cudaMemcpyAsync(s, h->d_rel + 2 * nb, sizeof(s), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  // l2_norm(u) = sqrt(cell * sum w u^2)  (P/src/monodomain.cpp:92-99)
+  double cell = 1.0;
+  for (int a = 0; a < h->p.dim; ++a) cell *= h->p.dx[a];
+  const double nbn = std::sqrt(cell * s[1]);
+  if (nbn == 0.0) return set_err(h, EMRKC_EINVAL, "rel_l2_error: ||b|| is zero");
+  *out = std::sqrt(cell * s[0]) / nbn;
   return EMRKC_OK;
 }
 

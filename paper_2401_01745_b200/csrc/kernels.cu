@@ -535,6 +535,53 @@ __global__ void __launch_bounds__(kRedThreads)
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
 }
 
+// Trapezoid-weighted sums of (a - b)^2 and b^2 over one node field
+// (rel_l2_error / l2_norm / quadrature_weights, P/src/monodomain.cpp:52-63,
+// 88-110): weight 1/2 per axis where the node sits on that axis' boundary.
+__global__ void __launch_bounds__(kRedThreads)
+    k_rel_l2_partial(const Geom g, const double* __restrict__ a, const double* __restrict__ b,
+                     double* __restrict__ partial) {
+  double sd = 0.0, sb = 0.0;
+  const long long nn = g.nn;
+  for (long long i = blockIdx.x * (long long)kRedThreads + threadIdx.x; i < nn;
+       i += (long long)gridDim.x * kRedThreads) {
+    double w = 1.0;
+    long long r = i;
+    const long long na[3] = {g.n0, g.n1, g.nzl};
+    for (int ax = 0; ax < g.dim; ++ax) {
+      const long long ia = r % na[ax];
+      r /= na[ax];
+      if (ia == 0 || ia == na[ax] - 1) w *= 0.5;
+    }
+    const double d = a[i] - b[i];
+    sd = __dadd_rn(sd, w * d * d);
+    sb = __dadd_rn(sb, w * b[i] * b[i]);
+  }
+  const double td = block_sum(sd);
+  __syncthreads();
+  const double tb = block_sum(sb);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = td;
+    partial[2 * blockIdx.x + 1] = tb;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+    k_sum_partials2(const double* __restrict__ partial, int n, double* __restrict__ out) {
+  double a0 = 0.0, a1 = 0.0;
+  for (int i = threadIdx.x; i < n; i += kRedThreads) {
+    a0 = __dadd_rn(a0, partial[2 * i]);
+    a1 = __dadd_rn(a1, partial[2 * i + 1]);
+  }
+  const double t0 = block_sum(a0);
+  __syncthreads();
+  const double t1 = block_sum(a1);
+  if (threadIdx.x == 0) {
+    out[0] = t0;
+    out[1] = t1;
+  }
+}
+
 __global__ void __launch_bounds__(kRedThreads)
     k_sum_partials(const double* __restrict__ partial, int n,
                    double* __restrict__ out) {
@@ -682,6 +729,13 @@ cudaError_t launch_norm2_partial(const double* x, long long len,
                                  double* partial, int nblocks,
                                  cudaStream_t st) {
   k_norm2_partial<<<nblocks, kRedThreads, 0, st>>>(x, len, partial);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rel_l2(const Geom& g, const double* a, const double* b, double* partial,
+                          int nblocks, double* out2, cudaStream_t st) {
+  k_rel_l2_partial<<<nblocks, kRedThreads, 0, st>>>(g, a, b, partial);
+  k_sum_partials2<<<1, kRedThreads, 0, st>>>(partial, nblocks, out2);
   return cudaGetLastError();
 }
 

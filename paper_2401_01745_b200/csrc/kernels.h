@@ -204,6 +204,10 @@ cudaError_t launch_power(const Geom& g, int which, const double* y,
                          const double* gy_lo, const double* gy_hi,
                          const double* gv_lo, const double* gv_hi,
                          double* partial, int nblocks, cudaStream_t st);
+// Trapezoid-weighted sum((a - b)^2), sum(b^2) of one node field -> out2[0..1]
+// (partial: 2 * nblocks doubles).
+cudaError_t launch_rel_l2(const Geom& g, const double* a, const double* b, double* partial,
+                          int nblocks, double* out2, cudaStream_t st);
 cudaError_t launch_norm2_partial(const double* x, long long len,
                                  double* partial, int nblocks,
                                  cudaStream_t st);

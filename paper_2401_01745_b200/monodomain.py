@@ -311,6 +311,14 @@ class MonodomainOperator:
                                 rho_F, rho_S, C.byref(res)), self._h)
         return res
 
+    def rel_l2_error(self, ref: np.ndarray, block: int = 0) -> float:
+        """rel_l2_error of SoA block ``block`` of the device state against a
+        host field (P/src/monodomain.cpp:88-110), reduced on the device."""
+        ref = np.ascontiguousarray(ref, dtype=np.float64)
+        out = C.c_double(0.0)
+        _check(_lib().emrkc_rel_l2_error(self._h, block, dptr(ref), 0, C.byref(out)), self._h)
+        return out.value
+
     def exex_step(self, t: float, dt: float) -> StepReport:
         """One EXEX-RL step of the device state (exex_rl_step,
         P/src/baselines.cpp:192-210); never raises NumericalAbort."""
