@@ -48,7 +48,10 @@ typedef enum emrkc_status {
 } emrkc_status;
 
 enum { EMRKC_MODEL_HH = 0 };          /* make_ionic_model("hh"), P/src/ionic.cpp:125-128 */
-enum { EMRKC_RHS_F = 0, EMRKC_RHS_S = 1 }; /* SplitRhs::f_F / f_S */
+/* SplitRhs::f_F / f_S; _GATES: f_F_with_gates / f_S_with_gates of the mRKC
+ * stiff-gate split (P/src/monodomain.cpp:287-304, gates from
+ * emrkc_set_stiff_gates) */
+enum { EMRKC_RHS_F = 0, EMRKC_RHS_S = 1, EMRKC_RHS_F_GATES = 2, EMRKC_RHS_S_GATES = 3 };
 /* EmrkcVariant, P/include/mrkc/multirate.hpp:37-40 (averaged force:
  * P/src/multirate.cpp:100-105 standard, :106-115 progressive). */
 enum { EMRKC_VARIANT_STANDARD = 0, EMRKC_VARIANT_PROGRESSIVE = 1 };
@@ -256,6 +259,22 @@ int emrkc_exex_step(emrkc_handle* h, double t, double dt, emrkc_step_report* rep
  * res->s = res->m = 1, res->eta = dt. */
 int emrkc_exex_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
                    emrkc_run_result* res);
+
+/* mRKC with the stiff-gate split (run_simulation, P/src/simulate.cpp:132-150):
+ * gates in `mask` (bit g = gate g; HH: 0 m, 1 h, 2 n) join f_F, the others
+ * join f_S. Default mask 1 (m, the stiffest HH gate). */
+int emrkc_set_stiff_gates(emrkc_handle* h, int32_t mask);
+/* identify_stiff_gates (P/src/ionic.cpp:130-146): gates ordered by their
+ * largest alpha + beta over the V samples (descending). order: n_gates. */
+int emrkc_identify_stiff_gates(int32_t model, const double* V, int64_t n, int32_t* order);
+/* mrkc_step (P/src/multirate.cpp:158-171, averaged force :60-76) on the
+ * device state; rho_F / rho_S of f_F / f_S with gates (EMRKC_RHS_*_GATES).
+ * Counters: n_fF = s m, n_fS = s, n_exp = 0. Whole-grid handles. */
+int emrkc_mrkc_step(emrkc_handle* h, double t, double dt, double epsilon, double rho_F,
+                    double rho_S, emrkc_step_report* report);
+/* run_simulation's mrkc loop (P/src/simulate.cpp:191-195,176-229). */
+int emrkc_mrkc_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt, double epsilon,
+                   double rho_F, double rho_S, emrkc_run_result* res);
 
 /* Benchmark form of emrkc_run: before every step, writes flush_bytes of a
  * scratch buffer (evicts L2; 0 = no flush), then times every kernel launch

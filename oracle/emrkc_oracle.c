@@ -253,6 +253,23 @@ done:
   return rc;
 }
 
+/* averaged_force_mrkc — P/src/multirate.cpp:60-76: slow term frozen at y,
+ * inner RKC from y on f_F + fs */
+static int averaged_force_mrkc_k(double t, const double* y, int64_t n, double eta,
+                                 const oc_split* rhs, const coeffs* km, double* out,
+                                 int32_t* abort_stage) {
+  double* fs = (double*)malloc(sizeof(double) * n);
+  if (!fs) return fail(EMRKC_ENOMEM, "out of memory");
+  rhs->f_S(rhs->ctx, t, y, fs, n);
+  if (rhs->counters) ++rhs->counters->n_fS;
+  fu_ctx c = {rhs, fs, NULL};
+  int rc = rkc_iteration_k(t, y, n, eta, f_u, &c, km, out, abort_stage);
+  if (!rc)
+    for (int64_t i = 0; i < n; ++i) out[i] = (out[i] - y[i]) / eta; /* :74 */
+  free(fs);
+  return rc;
+}
+
 int oc_averaged_force_emrkc(double t, const double* y, int64_t n, double eta,
                             const oc_split* rhs, int32_t m, double eps,
                             double* out, int32_t* abort_stage) {
@@ -286,7 +303,9 @@ static void f_avg(void* vctx, double r, const double* g, double* out,
     return;
   }
   int32_t st = 0;
-  c->rc = averaged_force_k(r, g, n, c->eta, c->rhs, c->km, c->variant, out, &st);
+  c->rc = c->variant == OC_VARIANT_MRKC
+              ? averaged_force_mrkc_k(r, g, n, c->eta, c->rhs, c->km, out, &st)
+              : averaged_force_k(r, g, n, c->eta, c->rhs, c->km, c->variant, out, &st);
   if (c->rc) {
     c->inner_stage = st;
     for (int64_t i = 0; i < n; ++i) out[i] = NAN;
@@ -304,10 +323,12 @@ int oc_emrkc_step_v(double t, const double* y, int64_t n, double dt,
                     const oc_split* rhs, double eps, int32_t variant,
                     double* out, emrkc_step_report* rep) {
   memset(rep, 0, sizeof(*rep));
-  if (variant != EMRKC_VARIANT_STANDARD && variant != EMRKC_VARIANT_PROGRESSIVE)
+  if (variant != EMRKC_VARIANT_STANDARD && variant != EMRKC_VARIANT_PROGRESSIVE &&
+      variant != OC_VARIANT_MRKC)
     return fail(EMRKC_EINVAL, "emrkc_step: unknown variant");
   if (dt <= 0.0) return fail(EMRKC_EINVAL, "emrkc_step: dt must be > 0");
-  if (!rhs->exp_part)
+  /* mrkc_step (P/src/multirate.cpp:158-171) needs no exp_part */
+  if (!rhs->exp_part && variant != OC_VARIANT_MRKC)
     return fail(EMRKC_EINVAL, "emrkc_step: exp_part missing");
   int32_t s, m;
   double ell_s, ell_m, beta;
@@ -720,7 +741,36 @@ done:
 
 typedef struct grid_ctx {
   const emrkc_problem* p;
+  int32_t stiff; /* gate mask of the fast part (mRKC stiff-gate split) */
 } grid_ctx;
+
+/* gate_rows — P/src/monodomain.cpp:223-236: out[g] = Lambda_g (z_g - z_inf_g)
+ * for the gates in mask */
+static void gate_rows(const emrkc_problem* p, const double* y, double* out, int32_t mask) {
+  const int64_t nn = n_nodes(p);
+  if (!(mask & 7)) return;
+  for (int64_t i = 0; i < nn; ++i) {
+    double lam[3], zi[3];
+    oc_hh_gate_coeffs(y[i], lam, zi);
+    for (int g = 0; g < 3; ++g)
+      if (mask >> g & 1) {
+        const int64_t k = (1 + g) * nn + i;
+        out[k] = lam[g] * (y[k] - zi[g]);
+      }
+  }
+}
+
+/* f_F_with_gates / f_S_with_gates — P/src/monodomain.cpp:287-304 */
+void oc_f_F_gates(const emrkc_problem* p, int32_t stiff, double t, const double* y,
+                  double* out) {
+  oc_f_F(p, t, y, out);
+  gate_rows(p, y, out, stiff);
+}
+void oc_f_S_gates(const emrkc_problem* p, int32_t stiff, double t, const double* y,
+                  double* out) {
+  oc_f_S(p, t, y, out);
+  gate_rows(p, y, out, ~stiff & 7);
+}
 
 static void grid_fF(void* c, double t, const double* y, double* out,
                     int64_t n) {
@@ -731,6 +781,14 @@ static void grid_fS(void* c, double t, const double* y, double* out,
                     int64_t n) {
   (void)n;
   oc_f_S(((grid_ctx*)c)->p, t, y, out);
+}
+static void grid_fFg(void* c, double t, const double* y, double* out, int64_t n) {
+  (void)n;
+  oc_f_F_gates(((grid_ctx*)c)->p, ((grid_ctx*)c)->stiff, t, y, out);
+}
+static void grid_fSg(void* c, double t, const double* y, double* out, int64_t n) {
+  (void)n;
+  oc_f_S_gates(((grid_ctx*)c)->p, ((grid_ctx*)c)->stiff, t, y, out);
 }
 static void grid_exp(void* c, const double* y, double* lam, double* yinf,
                      int64_t n) {
@@ -743,9 +801,42 @@ int oc_estimate_rho(const emrkc_problem* p, int32_t which, double t,
                     emrkc_rho_result* out, double* v_out) {
   int rc = oc_validate(p);
   if (rc) return rc;
-  grid_ctx c = {p};
-  return oc_estimate_rho_cb(which == EMRKC_RHS_F ? grid_fF : grid_fS, &c,
-                            oc_state_len(p), t, y, v0, rho0, out, v_out);
+  /* which: EMRKC_RHS_F / _S, or 2 / 3 = f_F / f_S with gate rows, stiff
+   * gate mask in bits 4.. (mRKC split) */
+  grid_ctx c = {p, (which >> 4) & 7};
+  oc_rhs_fn f = grid_fF;
+  switch (which & 15) {
+    case EMRKC_RHS_F: f = grid_fF; break;
+    case EMRKC_RHS_S: f = grid_fS; break;
+    case 2: f = grid_fFg; break;
+    case 3: f = grid_fSg; break;
+    default: return fail(EMRKC_EINVAL, "estimate_rho: unknown rhs");
+  }
+  return oc_estimate_rho_cb(f, &c, oc_state_len(p), t, y, v0, rho0, out, v_out);
+}
+
+/* identify_stiff_gates — P/src/ionic.cpp:130-146: gates ordered by the
+ * largest alpha + beta over the V samples, descending (stable) */
+int oc_identify_stiff_gates(const double* V, int64_t n, int32_t* order) {
+  if (n < 1) return fail(EMRKC_EINVAL, "identify_stiff_gates: empty trajectory");
+  double mr[3] = {0.0, 0.0, 0.0};
+  for (int64_t i = 0; i < n; ++i) {
+    double a[3], b[3];
+    oc_hh_rates(V[i], a, b);
+    for (int g = 0; g < 3; ++g) {
+      const double r = a[g] + b[g];
+      mr[g] = (mr[g] < r) ? r : mr[g]; /* std::max */
+    }
+  }
+  int32_t o[3] = {0, 1, 2};
+  for (int i = 1; i < 3; ++i) /* stable insertion sort, descending */
+    for (int j = i; j > 0 && mr[o[j - 1]] < mr[o[j]]; --j) {
+      const int32_t tmp = o[j];
+      o[j] = o[j - 1];
+      o[j - 1] = tmp;
+    }
+  for (int g = 0; g < 3; ++g) order[g] = o[g];
+  return 0;
 }
 
 /* ======================= run loop (P/src/simulate.cpp) ================== */
@@ -755,7 +846,7 @@ int oc_emrkc_step_grid(const emrkc_problem* p, double t, const double* y,
                        double* out, emrkc_step_report* rep) {
   int rc = oc_validate(p);
   if (rc) return rc;
-  grid_ctx c = {p};
+  grid_ctx c = {p, 0};
   oc_counters ctr = {0, 0, 0};
   oc_split rhs = {grid_fF, grid_fS, grid_exp, &c, rho_F, rho_S, &ctr};
   return oc_emrkc_step(t, y, oc_state_len(p), dt, &rhs, eps, out, rep);
@@ -807,15 +898,29 @@ int oc_exex_rl_step(const emrkc_problem* p, double t, const double* y, double dt
 
 /* run_simulation's stepping loop — P/src/simulate.cpp:110-113, 176-229:
  * the emRKC / emRKC-progressive branches (:197-207) and exex_rl (:211-212) */
+int oc_run_mrkc(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
+                double dt, double eps, int32_t stiff, double rho_F, double rho_S,
+                emrkc_run_result* res, double* wall_s) {
+  return oc_run_method(p, y, step0, nsteps, dt, eps, OC_METHOD_MRKC | ((stiff & 7) << 4), rho_F,
+                       rho_S, res, wall_s);
+}
+
 int oc_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
                   double dt, double eps, int32_t method, double rho_F, double rho_S,
                   emrkc_run_result* res, double* wall_s) {
+  const int32_t stiff = (method >> 4) & 7;
+  method &= 15;
   int rc = oc_validate(p);
   if (rc) return rc;
   const int64_t nn = n_nodes(p), len = 4 * nn;
-  grid_ctx c = {p};
+  grid_ctx c = {p, stiff};
   oc_counters ctr = {0, 0, 0};
   oc_split rhs = {grid_fF, grid_fS, grid_exp, &c, rho_F, rho_S, &ctr};
+  if (method == OC_METHOD_MRKC) { /* simulate.cpp:132-150 */
+    rhs.f_F = grid_fFg;
+    rhs.f_S = grid_fSg;
+    rhs.exp_part = NULL;
+  }
   double* next = (double*)malloc(sizeof(double) * len);
   if (!next) return fail(EMRKC_ENOMEM, "out of memory");
   memset(res, 0, sizeof(*res));
@@ -841,6 +946,7 @@ int oc_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nste
     } else {
       rc = oc_emrkc_step_v(t, y, len, dt, &rhs, eps,
                            method == OC_METHOD_EMRKC_PROGRESSIVE ? EMRKC_VARIANT_PROGRESSIVE
+                           : method == OC_METHOD_MRKC           ? OC_VARIANT_MRKC
                                                                  : EMRKC_VARIANT_STANDARD,
                            next, &rep);
     }

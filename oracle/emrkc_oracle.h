@@ -104,8 +104,22 @@ int oc_estimate_rho_cb(oc_rhs_fn f, void* ctx, int64_t n, double t,
 int oc_run(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
            double dt, double eps, double rho_F, double rho_S,
            emrkc_run_result* res, double* wall_s);
-/* Method (P/include/mrkc/config.hpp:17) of oc_run_method */
-enum { OC_METHOD_EMRKC = 0, OC_METHOD_EMRKC_PROGRESSIVE = 1, OC_METHOD_EXEX_RL = 2 };
+/* Method (P/include/mrkc/config.hpp:17) of oc_run_method; OC_METHOD_MRKC
+ * takes the stiff gate mask in bits 4..6 (oc_run_mrkc) */
+enum { OC_METHOD_EMRKC = 0, OC_METHOD_EMRKC_PROGRESSIVE = 1, OC_METHOD_EXEX_RL = 2,
+       OC_METHOD_MRKC = 3 };
+/* internal variant code of oc_emrkc_step_v for mrkc_step (multirate.cpp:158-171) */
+enum { OC_VARIANT_MRKC = 3 };
+int oc_run_mrkc(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
+                double dt, double eps, int32_t stiff, double rho_F, double rho_S,
+                emrkc_run_result* res, double* wall_s);
+/* f_F_with_gates / f_S_with_gates (P/src/monodomain.cpp:287-304), stiff gate mask */
+void oc_f_F_gates(const emrkc_problem* p, int32_t stiff, double t, const double* y,
+                  double* out);
+void oc_f_S_gates(const emrkc_problem* p, int32_t stiff, double t, const double* y,
+                  double* out);
+/* identify_stiff_gates (P/src/ionic.cpp:130-146) for HH */
+int oc_identify_stiff_gates(const double* V, int64_t n, int32_t* order);
 int oc_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,
                   double dt, double eps, int32_t method, double rho_F, double rho_S,
                   emrkc_run_result* res, double* wall_s);

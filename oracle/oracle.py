@@ -50,6 +50,7 @@ def _sigs(pre: str):
         "run": (C.c_int, [PP, DP, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(RunResult), DP]),
         "run_method": (C.c_int, [PP, DP, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult), DP]),
         "rel_l2_error": (C.c_double, [PP, DP, DP]),
+        "identify_stiff_gates": (C.c_int, [DP, C.c_int64, I32P]),
         "analytic_rho_F": (C.c_double, [PP]),
         "get_stages": (C.c_int, [C.c_double, C.c_double, C.c_double, I32P, DP, DP]),
         "rkc_coeffs": (C.c_int, [C.c_int32, C.c_double, DP, DP, DP, DP, DP, DP, DP]),
@@ -71,6 +72,7 @@ def _sigs(pre: str):
         s["std_uniform_direction"] = (None, [C.c_uint64, C.c_int64, DP])
         s["std_normal"] = (None, [C.c_uint64, C.c_double, C.c_double, C.c_int64, DP])
         s["state_len"] = (C.c_int64, [PP])
+        s["rhs_gates"] = (C.c_int, [PP, C.c_int, C.c_int, C.c_double, DP, DP])
     else:
         s["hh_rates"] = (None, [C.c_double, DP, DP])
         s["f_F"] = (None, [PP, C.c_double, DP, DP])
@@ -88,6 +90,8 @@ def _sigs(pre: str):
         s["scalar_averaged_force"] = (C.c_int, [C.c_double] * 6 + [C.c_int32, C.c_double, DP])
         s["scalar_emrkc_step"] = (C.c_int, [C.c_double] * 7 + [DP, I32P, I32P, DP])
         s["exex_rl_step"] = (C.c_int, [PP, C.c_double, DP, C.c_double, DP])
+        s["f_F_gates"] = (None, [PP, C.c_int32, C.c_double, DP, DP])
+        s["f_S_gates"] = (None, [PP, C.c_int32, C.c_double, DP, DP])
         s.pop("gate_coeffs")
         s.pop("ionic_current")
         s.pop("resting_state")
@@ -147,8 +151,30 @@ class _Lib:
             raise ValueError(self.err())
         return y, res, wall.value
 
-    # Method codes of run_method (P/include/mrkc/config.hpp:17)
-    EMRKC, EMRKC_PROGRESSIVE, EXEX_RL = 0, 1, 2
+    # Method codes of run_method (P/include/mrkc/config.hpp:17); MRKC takes
+    # the stiff gate mask in bits 4..6
+    EMRKC, EMRKC_PROGRESSIVE, EXEX_RL, MRKC = 0, 1, 2, 3
+    # estimate_rho / rhs selectors for the mRKC split: f_F / f_S with gate rows
+    RHS_F_GATES, RHS_S_GATES = 2, 3
+
+    def run_mrkc(self, p: Problem, y: np.ndarray, step0: int, nsteps: int, dt: float,
+                 stiff: int, eps: float = 0.05, rho_F: float = 0.0, rho_S: float = 0.0):
+        """run_simulation's mrkc loop (P/src/simulate.cpp:191-195) with the
+        stiff-gate split (gate mask ``stiff``)."""
+        return self.run_method(p, y, step0, nsteps, dt, self.MRKC | (stiff << 4), eps, rho_F,
+                               rho_S)
+
+    def estimate_rho_gates(self, p: Problem, which: int, stiff: int, t: float, y: np.ndarray):
+        """power iteration on f_F_with_gates (which 2) / f_S_with_gates (3)."""
+        return self.estimate_rho(p, which | (stiff << 4), t, y)
+
+    def identify_stiff_gates(self, V: np.ndarray):
+        V = np.ascontiguousarray(V, dtype=np.float64)
+        out = (C.c_int32 * 3)()
+        rc = self.fn("identify_stiff_gates")(dptr(V), V.size, out)
+        if rc:
+            raise ValueError(self.err())
+        return list(out)
 
     def run_method(self, p: Problem, y: np.ndarray, step0: int, nsteps: int, dt: float,
                    method: int, eps: float = 0.05, rho_F: float = 0.0, rho_S: float = 0.0):
@@ -250,6 +276,13 @@ class Oracle(_Scalar, _Lib):
         self.fn("f_F" if which == 0 else "f_S")(C.byref(p), t, dptr(y), dptr(out))
         return out
 
+    def rhs_gates(self, p: Problem, which: int, stiff: int, t: float, y: np.ndarray):
+        """f_F_with_gates (which 0) / f_S_with_gates (1), P/src/monodomain.cpp:287-304."""
+        out = np.empty_like(y)
+        self.fn("f_F_gates" if which == 0 else "f_S_gates")(C.byref(p), stiff, t, dptr(y),
+                                                            dptr(out))
+        return out
+
     def emrkc_step(self, p, t, y, dt, eps, rho_F, rho_S):
         out = np.empty_like(y)
         rep = StepReport()
@@ -340,6 +373,12 @@ class Reference(_Scalar, _Lib):
     def rhs(self, p: Problem, which: int, t: float, y: np.ndarray) -> np.ndarray:
         out = np.empty_like(y)
         rc = self.fn("rhs")(C.byref(p), which, t, dptr(y), dptr(out))
+        assert rc == 0, self.err()
+        return out
+
+    def rhs_gates(self, p: Problem, which: int, stiff: int, t: float, y: np.ndarray):
+        out = np.empty_like(y)
+        rc = self.fn("rhs_gates")(C.byref(p), which, stiff, t, dptr(y), dptr(out))
         assert rc == 0, self.err()
         return out
 

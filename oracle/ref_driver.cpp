@@ -19,6 +19,7 @@
 #include <limits>
 #include <memory>
 #include <random>
+#include <span>
 #include <string>
 #include <thread>
 #include <vector>
@@ -119,14 +120,32 @@ void track_gate_range(const Vec& y, const StateLayout& lay, double& lo,
   }
 }
 
+std::vector<int> gates_of(int mask) {
+  std::vector<int> g;
+  for (int i = 0; i < 3; ++i)
+    if (mask >> i & 1) g.push_back(i);
+  return g;
+}
+
 // run_simulation's loop (P/src/simulate.cpp:176-229): method 0 emrkc,
-// 1 emrkc_progressive (:197-207), 2 exex_rl (:211-212).
+// 1 emrkc_progressive (:197-207), 2 exex_rl (:211-212), 3 mrkc (:191-195)
+// with the stiff-gate split of :132-150 (gates in `stiff`).
 void run_loop(const MonodomainOperator& op, Vec& y, long step0, long nsteps,
               double dt, double eps, double rho_F, double rho_S,
-              emrkc_run_result* res, double* wall_s, int method = 0) {
+              emrkc_run_result* res, double* wall_s, int method = 0, int stiff_mask = 0) {
   const StateLayout& lay = op.layout();
   EvalCounters ctr;
   SplitRhs rhs = bind(op, &ctr);
+  if (method == 3) {
+    const std::vector<int> stiff = gates_of(stiff_mask);
+    rhs.f_F = [&op, stiff](double t, const Vec& u, Vec& out) {
+      op.f_F_with_gates(stiff, t, u, out);
+    };
+    rhs.f_S = [&op, stiff](double t, const Vec& u, Vec& out) {
+      op.f_S_with_gates(stiff, t, u, out);
+    };
+    rhs.exp_part = nullptr;
+  }
   rhs.rho_F = rho_F;
   rhs.rho_S = rho_S;
   std::memset(res, 0, sizeof(*res));
@@ -143,6 +162,12 @@ void run_loop(const MonodomainOperator& op, Vec& y, long step0, long nsteps,
         y = exex_rl_step(t, y, dt, op, &ctr);
         res->s = res->m = 1;
         res->eta = dt;
+      } else if (method == 3) {
+        MultirateStepReport rep;
+        y = mrkc_step(t, y, dt, rhs, eps, &rep);
+        res->s = rep.s;
+        res->m = rep.m;
+        res->eta = rep.eta;
       } else {
         MultirateStepReport rep;
         y = emrkc_step(t, y, dt, rhs, eps,
@@ -267,10 +292,15 @@ int ref_estimate_rho(const emrkc_problem* p, int which, double t,
     Vec v0v;
     if (v0) v0v.assign(v0, v0 + len);
     RhsFn f;
-    if (which == EMRKC_RHS_F)
+    const std::vector<int> stiff = gates_of((which >> 4) & 7);
+    if ((which & 15) == EMRKC_RHS_F)
       f = [&](double tt, const Vec& u, Vec& o) { op->f_F(tt, u, o); };
-    else
+    else if ((which & 15) == EMRKC_RHS_S)
       f = [&](double tt, const Vec& u, Vec& o) { op->f_S(tt, u, o); };
+    else if ((which & 15) == 2)
+      f = [&](double tt, const Vec& u, Vec& o) { op->f_F_with_gates(stiff, tt, u, o); };
+    else
+      f = [&](double tt, const Vec& u, Vec& o) { op->f_S_with_gates(stiff, tt, u, o); };
     const RhoEstimate est = estimate_spectral_radius(t, yv, f, v0v, rho0);
     out->rho = est.rho;
     out->iterations = est.iterations;
@@ -354,8 +384,31 @@ int ref_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nst
     const auto op = make_op(p);
     const long len = op->layout().size();
     Vec yv(y, y + len);
-    run_loop(*op, yv, step0, nsteps, dt, eps, rho_F, rho_S, res, wall_s, method);
+    run_loop(*op, yv, step0, nsteps, dt, eps, rho_F, rho_S, res, wall_s, method & 15,
+             (method >> 4) & 7);
     std::memcpy(y, yv.data(), len * sizeof(double));
+  });
+}
+
+int ref_identify_stiff_gates(const double* V, int64_t n, int32_t* order) {
+  return guarded([&] {
+    const auto model = make_hh_model();
+    const std::vector<int> o = identify_stiff_gates(*model, std::span<const double>(V, n));
+    for (std::size_t g = 0; g < o.size(); ++g) order[g] = o[g];
+  });
+}
+
+int ref_rhs_gates(const emrkc_problem* p, int which, int stiff, double t, const double* y,
+                  double* out) {
+  return guarded([&] {
+    const auto op = make_op(p);
+    const long len = op->layout().size();
+    const Vec yv(y, y + len);
+    Vec o;
+    const std::vector<int> s = gates_of(stiff);
+    if (which == 0) op->f_F_with_gates(s, t, yv, o);
+    else op->f_S_with_gates(s, t, yv, o);
+    std::memcpy(out, o.data(), len * sizeof(double));
   });
 }
 

@@ -28,6 +28,8 @@ EMRKC_RHS_F = 0
 EMRKC_RHS_S = 1
 EMRKC_VARIANT_STANDARD = 0
 EMRKC_VARIANT_PROGRESSIVE = 1
+EMRKC_RHS_F_GATES = 2
+EMRKC_RHS_S_GATES = 3
 EMRKC_ABORT_NONE = 0
 EMRKC_ABORT_NONFINITE = 1
 EMRKC_ABORT_NORM_GUARD = 2
@@ -193,6 +195,10 @@ PROTOTYPES = {
     "emrkc_step_host": (C.c_int, [C.c_void_p, C.c_double, DP, DP, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
     "emrkc_rel_l2_error": (C.c_int, [C.c_void_p, C.c_int32, DP, C.c_int32, DP]),
+    "emrkc_set_stiff_gates": (C.c_int, [C.c_void_p, C.c_int32]),
+    "emrkc_identify_stiff_gates": (C.c_int, [C.c_int32, DP, C.c_int64, I32P]),
+    "emrkc_mrkc_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(StepReport)]),
+    "emrkc_mrkc_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(RunResult)]),
     "emrkc_exex_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_exex_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.POINTER(RunResult)]),
     "emrkc_run_timed": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.c_int64, DP, C.c_int64, C.POINTER(RunResult)]),

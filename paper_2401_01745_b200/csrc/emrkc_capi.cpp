@@ -120,14 +120,18 @@ double lin_exp_ratio(double x, double k) {
   if (std::abs(u) < 1e-4) return k * (1.0 + u * (0.5 + u / 12.0));
   return x / (1.0 - std::exp(-u));
 }
-void hh_gate_coeffs(double V, double* lam, double* zinf) {
-  double a[3], b[3];
+// HH rates alpha_g, beta_g (P/src/ionic.cpp:98-109)
+void hh_rates(double V, double* a, double* b) {
   a[0] = 0.1 * lin_exp_ratio(V + 40.0, 10.0);
   b[0] = 4.0 * std::exp(-(V + 65.0) / 18.0);
   a[1] = 0.07 * std::exp(-(V + 65.0) / 20.0);
   b[1] = 1.0 / (1.0 + std::exp(-(V + 35.0) / 10.0));
   a[2] = 0.01 * lin_exp_ratio(V + 55.0, 10.0);
   b[2] = 0.125 * std::exp(-(V + 65.0) / 80.0);
+}
+void hh_gate_coeffs(double V, double* lam, double* zinf) {
+  double a[3], b[3];
+  hh_rates(V, a, b);
   for (int g = 0; g < 3; ++g) {
     lam[g] = -(a[g] + b[g]);
     zinf[g] = a[g] / (a[g] + b[g]);
@@ -141,7 +145,10 @@ double hh_current(double V, const double* z) {
 
 // Per-step plan: plan_step (P/src/multirate.cpp:129-135) + coefficients.
 // Stepping methods of the device path (Method, P/include/mrkc/config.hpp:17).
-enum { kMethodEmrkc = 0, kMethodEmrkcProgressive = 1, kMethodExexRl = 2 };
+enum { kMethodEmrkc = 0, kMethodEmrkcProgressive = 1, kMethodExexRl = 2, kMethodMrkc = 3 };
+
+// exp-part evaluations per step (EvalCounters::n_exp_steps): none in mRKC
+inline int exp_per_step(int method, int s) { return method == kMethodMrkc ? 0 : s; }
 
 struct Plan {
   double dt = -1, eps = -1, rho_F = -1, rho_S = -1;
@@ -311,6 +318,9 @@ struct emrkc_handle {
   int pipe = 1;
   int method = 0;  // kMethod* of the next plan (set by the API entry point)
   int tb = 1;      // temporally blocked inner stages (EMRKC_TB)
+  int stiff = 1;   // mRKC stiff-gate split: gates in the fast part (bit 0 = m)
+  double* mr_u[3] = {nullptr, nullptr, nullptr};  // mRKC inner stages (4 blocks each)
+  double* mr_fs = nullptr;                        // mRKC frozen slow term
   int zr_lo = -1, zr_hi = -1;  // node-kernel plane range override (< 0: all)
   // pipelined host step (emrkc_step_host): copy streams and chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -388,7 +398,7 @@ int upload_plan(emrkc_handle* h, double dt, double rho_F, double rho_S,
   if (pl.dt == dt && pl.rho_F == rho_F && pl.rho_S == rho_S && pl.eps == eps &&
       pl.method == h->method && h->plan_uploaded)
     return EMRKC_OK;
-  if (h->method != kMethodEmrkc && !h->fast)
+  if ((h->method == kMethodEmrkcProgressive || h->method == kMethodExexRl) && !h->fast)
     return set_err(h, EMRKC_EINVAL,
                    "the progressive variant and EXEX-RL run on the fast kernels (EMRKC_FAST=1)");
   int rc = make_plan(dt, rho_F, rho_S, eps, &pl, h->method);
@@ -632,6 +642,37 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
   const double r = (j == 1) ? c->t : c->t + pl.outer.c[j - 1] * pl.dt;
   a.stim = stim_rate_at(&h->p, r);
   const Halo hl = halo_at(h, h->level);
+  if (pl.method == kMethodMrkc) {
+    emrkc_k::MrkcArgs f{};
+    f.g1 = a.g1;
+    f.g2 = a.g2;
+    f.out = a.out;
+    f.fs = h->mr_fs;
+    f.um1 = k == 1 ? a.g1 : h->mr_u[(k - 1) % 3];
+    f.um2 = k == 2 ? a.g1 : (k > 2 ? h->mr_u[(k - 2) % 3] : nullptr);
+    f.uk = h->mr_u[k % 3];
+    f.eta = pl.eta;
+    f.mueta = pl.in_mueta[k];
+    f.nu = pl.inner.nu[k];
+    f.kappa = pl.inner.kappa[k];
+    f.mudt = pl.mudt[j];
+    f.onu = a.nu;
+    f.okappa = a.kappa;
+    f.stim = a.stim;
+    f.stiff = h->stiff;
+    f.j = j;
+    f.k = k;
+    f.m = pl.m;
+    f.s = pl.s;
+    f.last = a.last;
+    f.code_base = a.code_base;
+    f.event = a.event;
+    CK(h, emrkc_k::launch_mrkc_stage(h->geom, f, h->stream));
+    if (a.last && k == pl.m)  // gate range of the step's result (simulate.cpp:228)
+      CK(h, emrkc_k::launch_gate_range(h->geom, a.out, a.gate_slot, h->stream));
+    ++h->level;
+    return EMRKC_OK;
+  }
   if (h->fast) {
     const double cG = pl.mudt[j] / pl.eta;
     if (k == 1) {
@@ -815,7 +856,7 @@ Decoded decode_event(unsigned long long ev, const Plan& pl) {
 void partial_counters(const Decoded& d, const Plan& pl, int64_t* fF,
                       int64_t* fS, int64_t* ex) {
   const int j = d.outer_stage;
-  *ex += j;
+  *ex += exp_per_step(pl.method, j);
   *fS += j;
   *fF += static_cast<int64_t>(j - 1) * pl.m + (d.inner ? d.stage : pl.m);
 }
@@ -1070,6 +1111,9 @@ void emrkc_destroy(emrkc_handle* h) {
   if (h->d_coef) cudaFree(h->d_coef);
   if (h->d_red) cudaFree(h->d_red);
   if (h->d_rel) cudaFree(h->d_rel);
+  for (auto& u : h->mr_u)
+    if (u) cudaFree(u);
+  if (h->mr_fs) cudaFree(h->mr_fs);
   if (h->d_tmp) cudaFree(h->d_tmp);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -1162,20 +1206,35 @@ int emrkc_synchronize(emrkc_handle* h) {
   return EMRKC_OK;
 }
 
+namespace {
+// emrkc_eval_rhs / emrkc_estimate_rho selector -> kernel code: F / S, and for
+// the mRKC split f_F / f_S with gate rows (mask in bits 4..6).
+int rhs_code(const emrkc_handle* h, int32_t which, int* code) {
+  switch (which) {
+    case EMRKC_RHS_F: *code = 0; return EMRKC_OK;
+    case EMRKC_RHS_S: *code = 1; return EMRKC_OK;
+    case EMRKC_RHS_F_GATES: *code = 0 | ((h->stiff & 7) << 4); return EMRKC_OK;
+    case EMRKC_RHS_S_GATES: *code = 1 | ((~h->stiff & 7) << 4); return EMRKC_OK;
+    default: return EMRKC_EINVAL;
+  }
+}
+
+}  // namespace
+
 int emrkc_eval_rhs(emrkc_handle* h, int32_t which, double t, const double* y,
                    double* out, int64_t len) {
   if (!h || !y || !out) return set_global(EMRKC_EINVAL, "null argument");
   if (h->partitioned) return set_err(h, EMRKC_EINVAL, "eval_rhs: whole-grid handles only");
   if (len != h->len) return set_err(h, EMRKC_EINVAL, "MonodomainOperator: state size mismatch");
-  if (which != EMRKC_RHS_F && which != EMRKC_RHS_S)
-    return set_err(h, EMRKC_EINVAL, "eval_rhs: which must be F or S");
+  int code = 0;
+  if (rhs_code(h, which, &code)) return set_err(h, EMRKC_EINVAL, "eval_rhs: unknown rhs %d", which);
   int rc = use_device(h);
   if (rc) return rc;
   double *dy = nullptr, *dout = nullptr;
   CK(h, cudaMalloc(&dy, sizeof(double) * len));
   CK(h, cudaMalloc(&dout, sizeof(double) * len));
   CK(h, cudaMemcpyAsync(dy, y, sizeof(double) * len, cudaMemcpyHostToDevice, h->stream));
-  CK(h, emrkc_k::launch_rhs(h->geom, Halo{}, which, dy, stim_rate_at(&h->p, t), dout,
+  CK(h, emrkc_k::launch_rhs(h->geom, Halo{}, code, dy, stim_rate_at(&h->p, t), dout,
                             h->stream));
   CK(h, cudaMemcpyAsync(out, dout, sizeof(double) * len, cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
@@ -1716,7 +1775,7 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     res->gate_max = hi;
     res->n_fF = done * pl.s * pl.m;
     res->n_fS = done * pl.s;
-    res->n_exp = done * pl.s;
+    res->n_exp = done * exp_per_step(pl.method, pl.s);
     if (!d.none && !d.guard) partial_counters(d, pl, &res->n_fF, &res->n_fS, &res->n_exp);
     // plan of the last accepted step (RunResult::steps.back(),
     // P/src/simulate.cpp:205); none when no step was accepted
@@ -1739,7 +1798,7 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     rep->ell_m = pl.ell_m;
     rep->n_fF = static_cast<int64_t>(pl.s) * pl.m;
     rep->n_fS = pl.s;
-    rep->n_exp = pl.s;
+    rep->n_exp = exp_per_step(pl.method, pl.s);
     if (!d.none && !d.guard) {
       rep->n_fF = rep->n_fS = rep->n_exp = 0;
       partial_counters(d, pl, &rep->n_fF, &rep->n_fS, &rep->n_exp);
@@ -1764,9 +1823,10 @@ int emrkc_estimate_rho(emrkc_handle* h, int32_t which, double t,
   if (!h || !out) return set_global(EMRKC_EINVAL, "null argument");
   if (h->partitioned)
     return set_err(h, EMRKC_EINVAL, "estimate_rho: partitioned handles use emrkc_group_estimate_rho");
-  if (which != EMRKC_RHS_F && which != EMRKC_RHS_S)
-    return set_err(h, EMRKC_EINVAL, "estimate_rho: which must be F or S");
-  return power_iteration({h}, which, t, v0, rho0, out, v_out);
+  int code = 0;
+  if (rhs_code(h, which, &code))
+    return set_err(h, EMRKC_EINVAL, "estimate_rho: unknown rhs %d", which);
+  return power_iteration({h}, code, t, v0, rho0, out, v_out);
 }
 
 namespace {
@@ -1823,7 +1883,7 @@ int step_impl(emrkc_handle* h, double t, double dt, double epsilon, double rho_F
   rep->ell_m = pl.ell_m;
   rep->n_fF = static_cast<int64_t>(pl.s) * pl.m;
   rep->n_fS = pl.s;
-  rep->n_exp = pl.s;
+  rep->n_exp = exp_per_step(pl.method, pl.s);
   if (d.none) {
     h->cur = outi;
     return EMRKC_OK;
@@ -1989,6 +2049,62 @@ int emrkc_exex_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
   if (nsteps < 0) return set_err(h, EMRKC_EINVAL, "emrkc_exex_run: nsteps must be >= 0");
   h->method = kMethodExexRl;
   return run_slabs({h}, step0, nsteps, dt, 0.05, 0.0, 0.0, res, false, nullptr);
+}
+
+int emrkc_set_stiff_gates(emrkc_handle* h, int32_t mask) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (mask < 0 || mask > 7) return set_err(h, EMRKC_EINVAL, "stiff gate mask must be 0..7");
+  h->stiff = mask;
+  h->plan_uploaded = false;
+  return EMRKC_OK;
+}
+
+int emrkc_identify_stiff_gates(int32_t model, const double* V, int64_t n, int32_t* order) {
+  if (model != EMRKC_MODEL_HH) return set_global(EMRKC_EINVAL, "unknown ionic model %d", model);
+  if (!V || !order) return set_global(EMRKC_EINVAL, "null argument");
+  if (n < 1) return set_global(EMRKC_EINVAL, "identify_stiff_gates: empty trajectory");
+  double mr[3] = {0.0, 0.0, 0.0};  // max alpha + beta per gate (P/src/ionic.cpp:133-140)
+  for (int64_t i = 0; i < n; ++i) {
+    double a[3], b[3];
+    hh_rates(V[i], a, b);
+    for (int g = 0; g < 3; ++g) mr[g] = std::max(mr[g], a[g] + b[g]);
+  }
+  int o[3] = {0, 1, 2};
+  std::stable_sort(o, o + 3, [&](int x, int y) { return mr[x] > mr[y]; });
+  for (int g = 0; g < 3; ++g) order[g] = o[g];
+  return EMRKC_OK;
+}
+
+namespace {
+int ensure_mrkc(emrkc_handle* h) {
+  for (auto& u : h->mr_u)
+    if (!u) CK(h, cudaMalloc(&u, sizeof(double) * h->len));
+  if (!h->mr_fs) CK(h, cudaMalloc(&h->mr_fs, sizeof(double) * h->len));
+  return EMRKC_OK;
+}
+}  // namespace
+
+int emrkc_mrkc_step(emrkc_handle* h, double t, double dt, double epsilon, double rho_F,
+                    double rho_S, emrkc_step_report* report) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (!(dt > 0.0)) return set_err(h, EMRKC_EINVAL, "mrkc_step: dt must be > 0");
+  int rc = use_device(h);
+  if (rc) return rc;
+  if ((rc = ensure_mrkc(h))) return rc;
+  h->method = kMethodMrkc;
+  return step_impl(h, t, dt, epsilon, rho_F, rho_S, report);
+}
+
+int emrkc_mrkc_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt, double epsilon,
+                   double rho_F, double rho_S, emrkc_run_result* res) {
+  if (!h || !res) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "emrkc_mrkc_run: whole-grid handles only");
+  if (nsteps < 0) return set_err(h, EMRKC_EINVAL, "emrkc_mrkc_run: nsteps must be >= 0");
+  int rc = use_device(h);
+  if (rc) return rc;
+  if ((rc = ensure_mrkc(h))) return rc;
+  h->method = kMethodMrkc;
+  return run_slabs({h}, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr);
 }
 
 int emrkc_run_timed(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,

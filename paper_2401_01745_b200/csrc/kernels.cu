@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kThreads)
   const long long nn = g.nn;
   const double V = y[n.i];
   double r;
-  if (which == 0) {
+  if ((which & 15) == 0) {
     r = lap<DIM>(g, n, V, Ld{y}, [&](long long ip) { return h.lo[ip]; },
                  [&](long long ip) { return h.hi[ip]; });
   } else {
@@ -449,9 +449,88 @@ __global__ void __launch_bounds__(kThreads)
                   y[2 * nn + n.i], y[3 * nn + n.i]);
   }
   out[n.i] = r;
-  out[nn + n.i] = 0.0;
-  out[2 * nn + n.i] = 0.0;
-  out[3 * nn + n.i] = 0.0;
+  // gate rows of the mRKC split (which bits 4..6): Lambda_g (z_g - z_inf_g)
+  // (gate_rows, P/src/monodomain.cpp:223-236)
+  const int gm = (which >> 4) & 7;
+  double l[3] = {0.0, 0.0, 0.0}, zi[3] = {0.0, 0.0, 0.0};
+  if (gm) hh_gate_coeffs_ref(V, l, zi);
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+    out[(q + 1) * nn + n.i] =
+        (gm >> q & 1) ? __dmul_rn(l[q], __dsub_rn(y[(q + 1) * nn + n.i], zi[q])) : 0.0;
+}
+
+// mRKC inner stage k of outer stage j, reference operation order
+// (rkc_iteration, P/src/cheb.cpp:84-105; averaged_force_mrkc,
+// P/src/multirate.cpp:60-76): f_u = f_F_with_gates(u) + fs with the slow
+// term fs = f_S_with_gates(g_{j-1}) frozen at k == 1; at k == m the averaged
+// force (u_m - g_{j-1}) / eta enters the outer recurrence.
+template <int DIM>
+__global__ void __launch_bounds__(kThreads)
+    k_mrkc_stage(const Geom g, const MrkcArgs a) {
+  const Node<DIM> n = node_here<DIM>(g);
+  if (!n.valid) return;
+  if (*(volatile const unsigned long long*)a.event != kNoEvent) return;  // aborted earlier
+  const long long nn = g.nn, i = n.i;
+  const double* U = a.um1;
+  const double V = U[i];
+  const auto none = [](long long) { return 0.0; };  // whole grid: no ghost planes
+  double f[4];
+  f[0] = lap<DIM>(g, n, V, Ld{U}, none, none);
+  double l[3], zi[3];
+  hh_gate_coeffs_ref(V, l, zi);
+#pragma unroll
+  for (int q = 0; q < 3; ++q)
+    f[q + 1] = (a.stiff >> q & 1) ? __dmul_rn(l[q], __dsub_rn(U[(q + 1) * nn + i], zi[q])) : 0.0;
+  double fs[4];
+  if (a.k == 1) {  // U == g_{j-1}
+    fs[0] = slow_v<0>(g, in_stim<DIM>(g, n) ? a.stim : 0.0, V, U[nn + i], U[2 * nn + i],
+                      U[3 * nn + i]);
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+      fs[q + 1] = (a.stiff >> q & 1) ? 0.0
+                                     : __dmul_rn(l[q], __dsub_rn(U[(q + 1) * nn + i], zi[q]));
+    if (a.m > 1)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) a.fs[c * nn + i] = fs[c];
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) fs[c] = a.fs[c * nn + i];
+  }
+  double u[4];
+  bool bad = false;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double fc = __dadd_rn(f[c], fs[c]);
+    const long long jc = c * nn + i;
+    u[c] = a.k == 1 ? __dadd_rn(U[jc], __dmul_rn(a.mueta, fc))
+                    : __dadd_rn(__dadd_rn(__dmul_rn(a.nu, U[jc]), __dmul_rn(a.kappa, a.um2[jc])),
+                                __dmul_rn(a.mueta, fc));
+    bad |= !isfinite(u[c]);
+  }
+  const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
+  if (bad) atomicMin(a.event, base + a.k);
+  if (a.k < a.m) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) a.uk[c * nn + i] = u[c];
+    return;
+  }
+  bool bad_out = false;
+  double o[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const long long jc = c * nn + i;
+    const double y = a.g1[jc];
+    const double force = __ddiv_rn(__dsub_rn(u[c], y), a.eta);  // multirate.cpp:74
+    o[c] = a.j == 1 ? __dadd_rn(y, __dmul_rn(a.mudt, force))
+                    : __dadd_rn(__dadd_rn(__dmul_rn(a.onu, y), __dmul_rn(a.okappa, a.g2[jc])),
+                                __dmul_rn(a.mudt, force));
+    a.out[jc] = o[c];
+    bad_out |= !isfinite(o[c]);
+  }
+  if (bad_out) atomicMin(a.event, base + a.m + 1);
+  if (a.last && !(fabs(o[0]) <= 1e6))
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
 }
 
 template <int DIM>
@@ -504,7 +583,7 @@ __global__ void __launch_bounds__(kRedThreads)
     const Node<DIM> n = node_flat<DIM>(g, i);
     const double zv = z(i);
     double fz;
-    if (which == 0) {
+    if ((which & 15) == 0) {
       fz = lap<DIM>(
           g, n, zv, z,
           [&](long long ip) { return __dadd_rn(gy_lo[ip], __dmul_rn(q, gv_lo[ip])); },
@@ -515,10 +594,20 @@ __global__ void __launch_bounds__(kRedThreads)
     }
     const double d = __dsub_rn(fz, fy[i]);
     vout[i] = d;
-    vout[nn + i] = 0.0;
-    vout[2 * nn + i] = 0.0;
-    vout[3 * nn + i] = 0.0;
     acc = __dadd_rn(acc, __dmul_rn(d, d));
+    const int gm = (which >> 4) & 7;  // gate rows of the mRKC split
+    double l[3] = {0.0, 0.0, 0.0}, zi[3] = {0.0, 0.0, 0.0};
+    if (gm) hh_gate_coeffs_ref(zv, l, zi);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      double dq = 0.0;
+      if (gm >> q & 1) {
+        const long long k = (q + 1) * nn + i;
+        dq = __dsub_rn(__dmul_rn(l[q], __dsub_rn(z(k), zi[q])), fy[k]);
+        acc = __dadd_rn(acc, __dmul_rn(dq, dq));
+      }
+      vout[(q + 1) * nn + i] = dq;
+    }
   }
   const double t = block_sum(acc);
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
@@ -701,6 +790,12 @@ cudaError_t launch_rhs(const Geom& g, const Halo& h, int which,
                        cudaStream_t st) {
   const dim3 blk(BX, BY);
   DISPATCH_DIM(g, { k_rhs<D><<<grid_of<D>(g), blk, 0, st>>>(g, h, which, y, stim, out); });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mrkc_stage(const Geom& g, const MrkcArgs& a, cudaStream_t st) {
+  const dim3 blk(BX, BY);
+  DISPATCH_DIM(g, { k_mrkc_stage<D><<<grid_of<D>(g), blk, 0, st>>>(g, a); });
   return cudaGetLastError();
 }
 

@@ -66,6 +66,26 @@ struct StageArgs {
   int last;                      // j == s: guard + gate range
 };
 
+// mRKC (P/src/multirate.cpp:60-76,158-171) with the stiff-gate split of
+// run_simulation (P/src/simulate.cpp:132-150): inner stage k of outer j.
+struct MrkcArgs {
+  const double* g1;   // g_{j-1} = u_0 (state layout)
+  const double* g2;   // g_{j-2} (j >= 2)
+  double* out;        // g_j (written at k == m)
+  double* fs;         // frozen slow term f_S_with_gates(g_{j-1}) (4 blocks)
+  const double* um1;  // u_{k-1} (4 blocks; g_{j-1} for k == 1)
+  const double* um2;  // u_{k-2} (k >= 2; g_{j-1} for k == 2)
+  double* uk;         // u_k (k < m)
+  double eta, mueta, nu, kappa;  // inner: eta, mu'_k eta, nu'_k, kappa'_k
+  double mudt, onu, okappa;      // outer: mu_j dt, nu_j, kappa_j
+  double stim;                   // stimulus rate at the outer stage time
+  int stiff;                     // gate mask of the fast part
+  int j, k, m, s, last;
+  unsigned long long code_base;
+  unsigned long long* event;
+};
+cudaError_t launch_mrkc_stage(const Geom& g, const MrkcArgs& a, cudaStream_t st);
+
 // Arguments of the fast kernels (kernels_fast.cu): one outer stage j.
 struct FastArgs {
   const double* g1;   // g_{j-1}

@@ -319,6 +319,28 @@ class MonodomainOperator:
         _check(_lib().emrkc_rel_l2_error(self._h, block, dptr(ref), 0, C.byref(out)), self._h)
         return out.value
 
+    # ---- mRKC with the stiff-gate split (P/src/multirate.cpp:158-171) ----
+    def set_stiff_gates(self, mask: int):
+        """Gates (bit g) in the fast part f_F (P/src/simulate.cpp:132-150)."""
+        _check(_lib().emrkc_set_stiff_gates(self._h, mask), self._h)
+
+    def mrkc_step(self, t: float, dt: float, rho_F: float, rho_S: float,
+                  epsilon: float = kDefaultDamping) -> StepReport:
+        rep = StepReport()
+        rc = _lib().emrkc_mrkc_step(self._h, t, dt, epsilon, rho_F, rho_S, C.byref(rep))
+        if rc == capi.EMRKC_ENONFINITE:
+            raise NumericalAbort(_lib().emrkc_last_error(self._h).decode(), rep.abort_stage,
+                                 inner=bool(rep.abort_inner))
+        _check(rc, self._h)
+        return rep
+
+    def mrkc_run(self, step0: int, nsteps: int, dt: float, rho_F: float, rho_S: float,
+                 epsilon: float = kDefaultDamping) -> RunResult:
+        res = RunResult()
+        _check(_lib().emrkc_mrkc_run(self._h, step0, nsteps, dt, epsilon, rho_F, rho_S,
+                                     C.byref(res)), self._h)
+        return res
+
     def exex_step(self, t: float, dt: float) -> StepReport:
         """One EXEX-RL step of the device state (exex_rl_step,
         P/src/baselines.cpp:192-210); never raises NumericalAbort."""
@@ -372,6 +394,15 @@ def emrkc_step(t: float, y: np.ndarray, dt: float, rhs: SplitRhs,
     rhs.counters["n_fS"] += rep.n_fS
     rhs.counters["n_exp_steps"] += rep.n_exp
     return out
+
+
+def identify_stiff_gates(V: np.ndarray, model: int = capi.EMRKC_MODEL_HH) -> list:
+    """identify_stiff_gates (P/src/ionic.cpp:130-146): gates by their largest
+    alpha + beta over the V samples, stiffest first."""
+    V = np.ascontiguousarray(V, dtype=np.float64)
+    out = (C.c_int32 * 3)()
+    _check(_lib().emrkc_identify_stiff_gates(model, dptr(V), V.size, out))
+    return list(out)
 
 
 def exex_rl_step(t: float, y: np.ndarray, dt: float, op: MonodomainOperator) -> np.ndarray:

@@ -113,3 +113,41 @@ def test_exex_rl_nonfinite_gate(oracle, reference):
     assert np.array_equal(ya, yb, equal_nan=True)
     _same_records(ra, rb)
     assert ra.aborted and ra.abort_kind == 2 and ra.abort_step == 2 and ra.steps_done == 1
+
+
+def test_mrkc_pieces_bitwise(oracle, reference):
+    """Stiff-gate split (P/src/monodomain.cpp:223-236,287-304) and
+    identify_stiff_gates (P/src/ionic.cpp:130-146)."""
+    w = workloads.parity_3d()
+    p = w.problem
+    rng = np.random.default_rng(9)
+    nn = p.n_nodes
+    y = np.concatenate([rng.uniform(-90, 50, nn), rng.uniform(0, 1, 3 * nn)])
+    for stiff in (1, 2, 5, 7):
+        for which in (0, 1):
+            assert np.array_equal(oracle.rhs_gates(p, which, stiff, 0.3, y),
+                                  reference.rhs_gates(p, which, stiff, 0.3, y))
+    V = np.linspace(-90, 40, 200)
+    assert oracle.identify_stiff_gates(V) == reference.identify_stiff_gates(V)
+    assert oracle.identify_stiff_gates(V)[0] == 0  # m is the stiffest HH gate
+    for which in (oracle.RHS_F_GATES, oracle.RHS_S_GATES):
+        a, va = oracle.estimate_rho_gates(p, which, 1, 0.0, w.initial_state())
+        b, vb = reference.estimate_rho(p, which | (1 << 4), 0.0, w.initial_state())
+        assert (a.rho, a.iterations) == (b.rho, b.iterations) and np.array_equal(va, vb)
+
+
+@pytest.mark.parametrize("name,nsteps", [("p2d_128_s3m2", 10), ("p3d_48_s2m2", 4),
+                                         ("hh2d_256x256", 20)])
+def test_mrkc_bitwise(oracle, reference, name, nsteps):
+    """mrkc_step (P/src/multirate.cpp:158-171) with the m gate in the fast part."""
+    w = workloads.get(name)
+    p = w.problem
+    y0 = w.initial_state()
+    rF = reference.estimate_rho(p, 2 | (1 << 4), 0.0, y0)[0].rho
+    rS = w.rho_S_forced if w.rho_S_forced is not None else \
+        reference.estimate_rho(p, 3 | (1 << 4), 0.0, y0)[0].rho
+    ya, ra, _ = oracle.run_mrkc(p, y0, 0, nsteps, w.dt, 1, w.eps, rF, rS)
+    yb, rb, _ = reference.run_mrkc(p, y0, 0, nsteps, w.dt, 1, w.eps, rF, rS)
+    assert np.array_equal(ya, yb)
+    _same_records(ra, rb)
+    assert ra.n_exp == 0 and ra.n_fF == nsteps * ra.s * ra.m and ra.n_fS == nsteps * ra.s
