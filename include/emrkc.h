@@ -276,6 +276,22 @@ int emrkc_mrkc_step(emrkc_handle* h, double t, double dt, double epsilon, double
 int emrkc_mrkc_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt, double epsilon,
                    double rho_F, double rho_S, emrkc_run_result* res);
 
+/* IMEX-RL (imex_rl_step, P/src/baselines.cpp:132-190): Rush-Larsen gates,
+ * then (I - dt D) V = V + dt v_rhs by CG (cg_solve :20-82) in sqrt(w)-scaled
+ * coordinates with the Jacobi preconditioner (jacobi != 0), relative
+ * tolerance rel_tol (CgConfig default 1e-8) and max_iters (0: 10 sqrt(n)+1),
+ * all on the device; *cg_iters (nullable) receives the CG iterations.
+ * Counters: n_fF = iterations + 2, n_fS = n_exp = 1. A CG that does not
+ * converge is the reference's NumericalAbort (EMRKC_ENONFINITE, stage -1). */
+int emrkc_imex_step(emrkc_handle* h, double t, double dt, double rel_tol, int64_t max_iters,
+                    int32_t jacobi, emrkc_step_report* report, int64_t* cg_iters);
+/* run_simulation's imex_rl loop (P/src/simulate.cpp:164-165,176-229) with
+ * CgConfig (rel_tol, max_iters, jacobi); *cg_iters_total (nullable) is
+ * EvalCounters::cg_iters_total. */
+int emrkc_imex_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt, double rel_tol,
+                   int64_t max_iters, int32_t jacobi, emrkc_run_result* res,
+                   int64_t* cg_iters_total);
+
 /* Benchmark form of emrkc_run: before every step, writes flush_bytes of a
  * scratch buffer (evicts L2; 0 = no flush), then times every kernel launch
  * of the step with its own CUDA-event pair on the handle's stream.

@@ -896,6 +896,190 @@ int oc_exex_rl_step(const emrkc_problem* p, double t, const double* y, double dt
   return 0;
 }
 
+/* cg_solve — P/src/baselines.cpp:20-82 on the IMEX operator
+ * op(u) = u - dt sqrt(w) D(u / sqrt(w)) (:150-158) */
+static double dotv(const double* a, const double* b, int64_t n) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+
+typedef struct imex_op {
+  const emrkc_problem* p;
+  const double* sw;
+  const double* isw;
+  double dt;
+  double* unscaled;
+  double* scratch;
+} imex_op;
+
+static void imex_apply(const imex_op* o, const double* u, double* out, int64_t nn) {
+  for (int64_t i = 0; i < nn; ++i) o->unscaled[i] = o->isw[i] * u[i];
+  oc_diffusion_apply(o->p, o->unscaled, o->scratch);
+  for (int64_t i = 0; i < nn; ++i) out[i] = u[i] - o->dt * o->sw[i] * o->scratch[i];
+}
+
+/* quadrature_weights — P/src/monodomain.cpp:52-63 */
+static void quad_weights(const emrkc_problem* p, double* w) {
+  const int64_t nn = n_nodes(p);
+  for (int64_t i = 0; i < nn; ++i) w[i] = 1.0;
+  for (int a = 0; a < p->dim; ++a) {
+    const int64_t stride = axis_stride(p, a), na = p->n[a];
+    for (int64_t i = 0; i < nn; ++i) {
+      const int64_t ia = (i / stride) % na;
+      if (ia == 0 || ia == na - 1) w[i] *= 0.5;
+    }
+  }
+}
+
+/* imex_rl_step — P/src/baselines.cpp:132-190 (HH). Returns EMRKC_ENONFINITE
+ * when CG does not converge; *iters = CG iterations, *applies = op applies. */
+int oc_imex_rl_step(const emrkc_problem* p, double t, const double* y, double dt,
+                    double rel_tol, int64_t max_iters, int32_t jacobi, double* out,
+                    int64_t* iters, int64_t* applies) {
+  if (!(dt > 0.0)) return fail(EMRKC_EINVAL, "imex_rl_step: dt must be > 0");
+  const int64_t nn = n_nodes(p);
+  double* buf = (double*)malloc(sizeof(double) * 13 * nn);
+  if (!buf) return fail(EMRKC_ENOMEM, "out of memory");
+  double *w = buf, *sw = buf + nn, *isw = buf + 2 * nn, *un = buf + 3 * nn, *sc = buf + 4 * nn;
+  double *b = buf + 5 * nn, *x = buf + 6 * nn, *r = buf + 7 * nn, *z = buf + 8 * nn;
+  double *pp = buf + 9 * nn, *q = buf + 10 * nn, *vr = buf + 11 * nn, *e = buf + 12 * nn;
+  /* rush_larsen_update (:89-128): gates at y's V, reaction at the new gates */
+  memcpy(out, y, sizeof(double) * 4 * nn);
+  for (int64_t i = 0; i < nn; ++i) {
+    double lam[3], zinf[3];
+    oc_hh_gate_coeffs(y[i], lam, zinf);
+    for (int g = 0; g < 3; ++g) {
+      const int64_t idx = (1 + g) * nn + i;
+      out[idx] = y[idx] + expm1(dt * lam[g]) * (y[idx] - zinf[g]);
+    }
+  }
+  for (int64_t i = 0; i < nn; ++i) {
+    const double zz[3] = {out[nn + i], out[2 * nn + i], out[3 * nn + i]};
+    vr[i] = oc_stimulus_rate(p, t, i) - oc_hh_ionic_current(y[i], zz) / p->C_m;
+  }
+  quad_weights(p, w);
+  for (int64_t i = 0; i < nn; ++i) {
+    sw[i] = sqrt(w[i]);
+    isw[i] = 1.0 / sw[i];
+  }
+  imex_op o = {p, sw, isw, dt, un, sc};
+  for (int64_t i = 0; i < nn; ++i) {
+    b[i] = sw[i] * (y[i] + dt * vr[i]);
+    x[i] = sw[i] * y[i];
+  }
+  for (int64_t i = 0; i < nn; ++i) e[i] = 0.0;
+  e[0] = 1.0;
+  oc_diffusion_apply(p, e, sc);
+  const double diag = 1.0 - dt * sc[0];
+  /* cg_solve */
+  int64_t it = 0, ap = 0;
+  int converged = 1;
+  const double nb = sqrt(dotv(b, b, nn));
+  if (nb == 0.0) {
+    for (int64_t i = 0; i < nn; ++i) x[i] = 0.0;
+  } else {
+    const int64_t max_it =
+        max_iters > 0 ? max_iters : (int64_t)(10.0 * sqrt((double)nn)) + 1;
+    imex_apply(&o, x, q, nn);
+    ++ap;
+    for (int64_t i = 0; i < nn; ++i) r[i] = b[i] - q[i];
+    for (int64_t i = 0; i < nn; ++i) z[i] = jacobi ? r[i] / diag : r[i];
+    memcpy(pp, z, sizeof(double) * nn);
+    double rz = dotv(r, z, nn);
+    double rnorm = sqrt(dotv(r, r, nn));
+    const double tol = rel_tol * nb;
+    while (rnorm > tol) {
+      if (it >= max_it) {
+        converged = 0;
+        break;
+      }
+      imex_apply(&o, pp, q, nn);
+      ++ap;
+      const double alpha = rz / dotv(pp, q, nn);
+      for (int64_t i = 0; i < nn; ++i) {
+        x[i] += alpha * pp[i];
+        r[i] -= alpha * q[i];
+      }
+      for (int64_t i = 0; i < nn; ++i) z[i] = jacobi ? r[i] / diag : r[i];
+      const double rz_new = dotv(r, z, nn);
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      for (int64_t i = 0; i < nn; ++i) pp[i] = z[i] + beta * pp[i];
+      rnorm = sqrt(dotv(r, r, nn));
+      ++it;
+    }
+  }
+  *iters = it;
+  *applies = ap;
+  int rc = 0;
+  if (!converged)
+    rc = fail(EMRKC_ENONFINITE, "imex_rl_step: CG did not converge");
+  else
+    for (int64_t i = 0; i < nn; ++i) out[i] = isw[i] * x[i];
+  free(buf);
+  return rc;
+}
+
+/* run_simulation's imex_rl loop (P/src/simulate.cpp:176-229) */
+int oc_run_imex(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps, double dt,
+                double rel_tol, int64_t max_iters, int32_t jacobi, emrkc_run_result* res,
+                int64_t* cg_iters_total) {
+  int rc = oc_validate(p);
+  if (rc) return rc;
+  const int64_t nn = n_nodes(p), len = 4 * nn;
+  double* next = (double*)malloc(sizeof(double) * len);
+  if (!next) return fail(EMRKC_ENOMEM, "out of memory");
+  memset(res, 0, sizeof(*res));
+  res->n_steps = nsteps;
+  res->abort_step = -1;
+  res->gate_min = 1.0;
+  res->gate_max = 0.0;
+  res->s = res->m = 1;
+  res->eta = dt;
+  track_gate_range(y, nn, len, &res->gate_min, &res->gate_max);
+  int64_t tot = 0;
+  for (int64_t step = step0; step < step0 + nsteps; ++step) {
+    const double t = (double)step * dt;
+    int64_t it = 0, ap = 0;
+    rc = oc_imex_rl_step(p, t, y, dt, rel_tol, max_iters, jacobi, next, &it, &ap);
+    ++res->n_exp; /* rush_larsen_update (:105-106,123-124) */
+    ++res->n_fS;
+    res->n_fF += ap + 1; /* probe + solve applies (:181) */
+    tot += it;
+    if (rc == EMRKC_ENONFINITE) {
+      res->aborted = 1;
+      res->abort_kind = EMRKC_ABORT_NONFINITE;
+      res->abort_step = step;
+      res->abort_stage = -1;
+      rc = 0;
+      break;
+    }
+    if (rc) break;
+    memcpy(y, next, sizeof(double) * len);
+    ++res->steps_done;
+    double mv = 0.0;
+    for (int64_t i = 0; i < nn; ++i) {
+      if (!isfinite(y[i])) {
+        mv = INFINITY;
+        break;
+      }
+      const double ay = fabs(y[i]);
+      mv = (mv < ay) ? ay : mv;
+    }
+    if (mv > 1e6) {
+      res->aborted = 1;
+      res->abort_kind = EMRKC_ABORT_NORM_GUARD;
+      res->abort_step = step;
+      break;
+    }
+    track_gate_range(y, nn, len, &res->gate_min, &res->gate_max);
+  }
+  if (cg_iters_total) *cg_iters_total = tot;
+  free(next);
+  return rc;
+}
+
 /* run_simulation's stepping loop — P/src/simulate.cpp:110-113, 176-229:
  * the emRKC / emRKC-progressive branches (:197-207) and exex_rl (:211-212) */
 int oc_run_mrkc(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,

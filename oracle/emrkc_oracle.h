@@ -118,6 +118,14 @@ void oc_f_F_gates(const emrkc_problem* p, int32_t stiff, double t, const double*
                   double* out);
 void oc_f_S_gates(const emrkc_problem* p, int32_t stiff, double t, const double* y,
                   double* out);
+/* imex_rl_step (P/src/baselines.cpp:132-190) and its run loop, CgConfig
+ * (rel_tol, max_iters (0: 10 sqrt(n) + 1), jacobi) */
+int oc_imex_rl_step(const emrkc_problem* p, double t, const double* y, double dt,
+                    double rel_tol, int64_t max_iters, int32_t jacobi, double* out,
+                    int64_t* iters, int64_t* applies);
+int oc_run_imex(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps, double dt,
+                double rel_tol, int64_t max_iters, int32_t jacobi, emrkc_run_result* res,
+                int64_t* cg_iters_total);
 /* identify_stiff_gates (P/src/ionic.cpp:130-146) for HH */
 int oc_identify_stiff_gates(const double* V, int64_t n, int32_t* order);
 int oc_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps,

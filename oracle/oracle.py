@@ -51,6 +51,7 @@ def _sigs(pre: str):
         "run_method": (C.c_int, [PP, DP, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult), DP]),
         "rel_l2_error": (C.c_double, [PP, DP, DP]),
         "identify_stiff_gates": (C.c_int, [DP, C.c_int64, I32P]),
+        "run_imex": (C.c_int, [PP, DP, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64, C.c_int32, C.POINTER(RunResult), C.POINTER(C.c_int64)]),
         "analytic_rho_F": (C.c_double, [PP]),
         "get_stages": (C.c_int, [C.c_double, C.c_double, C.c_double, I32P, DP, DP]),
         "rkc_coeffs": (C.c_int, [C.c_int32, C.c_double, DP, DP, DP, DP, DP, DP, DP]),
@@ -167,6 +168,18 @@ class _Lib:
     def estimate_rho_gates(self, p: Problem, which: int, stiff: int, t: float, y: np.ndarray):
         """power iteration on f_F_with_gates (which 2) / f_S_with_gates (3)."""
         return self.estimate_rho(p, which | (stiff << 4), t, y)
+
+    def run_imex(self, p: Problem, y: np.ndarray, step0: int, nsteps: int, dt: float,
+                 rel_tol: float = 1e-8, max_iters: int = 0, jacobi: bool = True):
+        """run_simulation's imex_rl loop; returns (state, RunResult, cg_iters_total)."""
+        y = np.ascontiguousarray(y, dtype=np.float64).copy()
+        res = RunResult()
+        it = C.c_int64(0)
+        rc = self.fn("run_imex")(C.byref(p), dptr(y), step0, nsteps, dt, rel_tol, max_iters,
+                                 int(jacobi), C.byref(res), C.byref(it))
+        if rc:
+            raise ValueError(self.err())
+        return y, res, it.value
 
     def identify_stiff_gates(self, V: np.ndarray):
         V = np.ascontiguousarray(V, dtype=np.float64)

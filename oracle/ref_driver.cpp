@@ -390,6 +390,56 @@ int ref_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nst
   });
 }
 
+// run_simulation's imex_rl loop (P/src/simulate.cpp:176-229, :208-210)
+int ref_run_imex(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps, double dt,
+                 double rel_tol, int64_t max_iters, int32_t jacobi, emrkc_run_result* res,
+                 int64_t* cg_iters_total) {
+  return guarded([&] {
+    const auto op = make_op(p);
+    const StateLayout& lay = op->layout();
+    const long len = lay.size();
+    Vec yv(y, y + len);
+    EvalCounters ctr;
+    CgConfig cfg;
+    cfg.rel_tol = rel_tol;
+    cfg.max_iters = max_iters;
+    cfg.preconditioner = jacobi ? CgConfig::Precond::jacobi : CgConfig::Precond::none;
+    std::memset(res, 0, sizeof(*res));
+    res->n_steps = nsteps;
+    res->abort_step = -1;
+    res->gate_min = 1.0;
+    res->gate_max = 0.0;
+    res->s = res->m = 1;
+    res->eta = dt;
+    track_gate_range(yv, lay, res->gate_min, res->gate_max);
+    for (long step = step0; step < step0 + nsteps; ++step) {
+      const double t = static_cast<double>(step) * dt;
+      try {
+        yv = imex_rl_step(t, yv, dt, *op, cfg, &ctr);
+      } catch (const NumericalAbort& e) {
+        res->aborted = 1;
+        res->abort_kind = EMRKC_ABORT_NONFINITE;
+        res->abort_step = step;
+        res->abort_stage = -1;
+        break;
+      }
+      ++res->steps_done;
+      if (max_abs_v(yv, lay.n_nodes) > 1e6) {
+        res->aborted = 1;
+        res->abort_kind = EMRKC_ABORT_NORM_GUARD;
+        res->abort_step = step;
+        break;
+      }
+      track_gate_range(yv, lay, res->gate_min, res->gate_max);
+    }
+    res->n_fF = ctr.n_fF;
+    res->n_fS = ctr.n_fS;
+    res->n_exp = ctr.n_exp_steps;
+    if (cg_iters_total) *cg_iters_total = ctr.cg_iters_total;
+    std::memcpy(y, yv.data(), len * sizeof(double));
+  });
+}
+
 int ref_identify_stiff_gates(const double* V, int64_t n, int32_t* order) {
   return guarded([&] {
     const auto model = make_hh_model();

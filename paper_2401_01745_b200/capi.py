@@ -199,6 +199,8 @@ PROTOTYPES = {
     "emrkc_identify_stiff_gates": (C.c_int, [C.c_int32, DP, C.c_int64, I32P]),
     "emrkc_mrkc_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_mrkc_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(RunResult)]),
+    "emrkc_imex_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int32, C.POINTER(StepReport), C.POINTER(C.c_int64)]),
+    "emrkc_imex_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int64, C.c_int32, C.POINTER(RunResult), C.POINTER(C.c_int64)]),
     "emrkc_exex_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_exex_run": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.POINTER(RunResult)]),
     "emrkc_run_timed": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.c_int64, DP, C.c_int64, C.POINTER(RunResult)]),

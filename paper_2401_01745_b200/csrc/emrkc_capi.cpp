@@ -321,6 +321,11 @@ struct emrkc_handle {
   int stiff = 1;   // mRKC stiff-gate split: gates in the fast part (bit 0 = m)
   double* mr_u[3] = {nullptr, nullptr, nullptr};  // mRKC inner stages (4 blocks each)
   double* mr_fs = nullptr;                        // mRKC frozen slow term
+  double* cg_v = nullptr;   // IMEX-RL CG vectors b, x, r, z, p, q (6 n_nodes)
+  double* cg_part = nullptr;  // CG partial sums (3 * power_blocks())
+  emrkc_k::CgScalars* cg_s = nullptr;   // device scalars
+  emrkc_k::CgScalars* cg_h = nullptr;   // pinned host copy
+  int* guard_d = nullptr;
   int zr_lo = -1, zr_hi = -1;  // node-kernel plane range override (< 0: all)
   // pipelined host step (emrkc_step_host): copy streams and chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -1114,6 +1119,11 @@ void emrkc_destroy(emrkc_handle* h) {
   for (auto& u : h->mr_u)
     if (u) cudaFree(u);
   if (h->mr_fs) cudaFree(h->mr_fs);
+  if (h->cg_v) cudaFree(h->cg_v);
+  if (h->cg_part) cudaFree(h->cg_part);
+  if (h->cg_s) cudaFree(h->cg_s);
+  if (h->cg_h) cudaFreeHost(h->cg_h);
+  if (h->guard_d) cudaFree(h->guard_d);
   if (h->d_tmp) cudaFree(h->d_tmp);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -2105,6 +2115,157 @@ int emrkc_mrkc_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt, do
   if ((rc = ensure_mrkc(h))) return rc;
   h->method = kMethodMrkc;
   return run_slabs({h}, step0, nsteps, dt, epsilon, rho_F, rho_S, res, false, nullptr);
+}
+
+namespace {
+// One imex_rl_step (P/src/baselines.cpp:132-190) of buf[cur] into the other
+// buffer. Returns 0 with *ok = 0 when CG did not converge (NumericalAbort).
+int imex_step_dev(emrkc_handle* h, double t, double dt, double rel_tol, int64_t max_iters,
+                  int jacobi, int* ok, int64_t* iters, int* guard) {
+  const int64_t nn = h->nn;
+  const int nb = emrkc_k::power_blocks();
+  if (!h->cg_v) CK(h, cudaMalloc(&h->cg_v, sizeof(double) * 6 * nn));
+  if (!h->cg_part) CK(h, cudaMalloc(&h->cg_part, sizeof(double) * 3 * nb));
+  if (!h->cg_s) CK(h, cudaMalloc(&h->cg_s, sizeof(emrkc_k::CgScalars)));
+  if (!h->cg_h) CK(h, cudaHostAlloc(&h->cg_h, sizeof(emrkc_k::CgScalars), 0));
+  if (!h->guard_d) CK(h, cudaMalloc(&h->guard_d, sizeof(int)));
+  double* b = h->cg_v;
+  double* x = b + nn;
+  double* r = x + nn;
+  double* z = r + nn;
+  double* pp = z + nn;
+  double* q = pp + nn;
+  double* part = h->cg_part;        // 2 nb
+  double* part_b = h->cg_part + 2 * nb;  // nb
+  const int in = h->cur, out = 1 - (h->cur & 1);
+  double* y = h->buf[in];
+  double* yo = h->buf[out];
+  // diag(I - dt D): constant for the reflection stencil (:171-177)
+  const double diag = jacobi ? 1.0 - dt * emrkc_k::diffusion_diag(h->geom) : 0.0;
+  const long long max_it = max_iters > 0
+                               ? max_iters
+                               : static_cast<long long>(10.0 * std::sqrt(static_cast<double>(nn))) + 1;
+  CK(h, emrkc_k::launch_imex_prep(h->geom, y, dt, stim_rate_at(&h->p, t), yo, b, x, part_b, nb,
+                                  h->stream));
+  CK(h, emrkc_k::launch_cg_init(h->geom, dt, diag, b, x, r, z, pp, part, nb, h->cg_s, rel_tol,
+                                max_it, part_b, h->stream));
+  constexpr int kBatch = 8;  // iterations between host checks of the loop test
+  for (long long done_it = 0;; done_it += kBatch) {
+    for (int i = 0; i < kBatch; ++i)
+      CK(h, emrkc_k::launch_cg_iter(h->geom, dt, diag, x, r, z, pp, q, part, nb, h->cg_s,
+                                    h->stream));
+    CK(h, cudaMemcpyAsync(h->cg_h, h->cg_s, sizeof(emrkc_k::CgScalars),
+                          cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (h->cg_h->done || done_it > max_it + kBatch) break;
+  }
+  CK(h, emrkc_k::launch_cg_finish(h->geom, x, yo, h->cg_s, h->stream));
+  CK(h, cudaMemsetAsync(h->guard_d, 0, sizeof(int), h->stream));
+  CK(h, emrkc_k::launch_v_guard(nn, yo, h->guard_d, h->stream));
+  int g = 0;
+  CK(h, cudaMemcpyAsync(&g, h->guard_d, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  *ok = h->cg_h->converged && h->cg_h->done;
+  *iters = h->cg_h->it;
+  *guard = g;
+  return EMRKC_OK;
+}
+}  // namespace
+
+int emrkc_imex_step(emrkc_handle* h, double t, double dt, double rel_tol, int64_t max_iters,
+                    int32_t jacobi, emrkc_step_report* report, int64_t* cg_iters) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "imex_rl_step: whole-grid handles only");
+  if (!(dt > 0.0)) return set_err(h, EMRKC_EINVAL, "imex_rl_step: dt must be > 0");
+  if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
+  int rc = use_device(h);
+  if (rc) return rc;
+  if ((rc = ensure_buffers(h, std::max(2, h->nbuf)))) return rc;
+  int ok = 0, guard = 0;
+  int64_t it = 0;
+  if ((rc = imex_step_dev(h, t, dt, rel_tol, max_iters, jacobi, &ok, &it, &guard))) return rc;
+  emrkc_step_report local;
+  emrkc_step_report* rep = report ? report : &local;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->s = rep->m = 1;
+  rep->eta = dt;
+  rep->n_fF = it + 2;  // CG applies (iterations + 1) + the diagonal probe
+  rep->n_fS = 1;
+  rep->n_exp = 1;
+  if (cg_iters) *cg_iters = it;
+  if (!ok) {
+    rep->abort_kind = EMRKC_ABORT_NONFINITE;
+    rep->abort_stage = -1;
+    return set_err(h, EMRKC_ENONFINITE, "imex_rl_step: CG did not converge");
+  }
+  h->cur = 1 - (h->cur & 1);
+  return EMRKC_OK;
+}
+
+int emrkc_imex_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt, double rel_tol,
+                   int64_t max_iters, int32_t jacobi, emrkc_run_result* res,
+                   int64_t* cg_iters_total) {
+  if (!h || !res) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "imex_rl_step: whole-grid handles only");
+  if (!(dt > 0.0)) return set_err(h, EMRKC_EINVAL, "imex_rl_step: dt must be > 0");
+  if (nsteps < 0) return set_err(h, EMRKC_EINVAL, "emrkc_imex_run: nsteps must be >= 0");
+  if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
+  int rc = use_device(h);
+  if (rc) return rc;
+  if ((rc = ensure_buffers(h, std::max(2, h->nbuf)))) return rc;
+  if ((rc = ensure_slots(h, 1))) return rc;
+  std::memset(res, 0, sizeof(*res));
+  res->n_steps = nsteps;
+  res->abort_step = -1;
+  res->s = res->m = 1;
+  res->eta = dt;
+  // gate range of the initial state and of every accepted step (simulate.cpp:113,228)
+  const unsigned long long init[2] = {kNoEvent, 0ull};
+  CK(h, cudaMemcpyAsync(h->d_slots, init, sizeof(init), cudaMemcpyHostToDevice, h->stream));
+  CK(h, emrkc_k::launch_gate_range(h->geom, h->buf[h->cur], h->d_slots, h->stream));
+  int64_t iters_total = 0;
+  CK(h, cudaEventRecord(h->ev0, h->stream));
+  for (int64_t s = 0; s < nsteps; ++s) {
+    const int64_t step = step0 + s;
+    const double t = static_cast<double>(step) * dt;  // simulate.cpp:177
+    int ok = 0, guard = 0;
+    int64_t it = 0;
+    if ((rc = imex_step_dev(h, t, dt, rel_tol, max_iters, jacobi, &ok, &it, &guard))) return rc;
+    res->n_fF += it + 2;
+    res->n_fS += 1;
+    res->n_exp += 1;
+    iters_total += it;
+    if (!ok) {  // NumericalAbort: y is not assigned
+      res->aborted = 1;
+      res->abort_kind = EMRKC_ABORT_NONFINITE;
+      res->abort_step = step;
+      res->abort_stage = -1;
+      break;
+    }
+    h->cur = 1 - (h->cur & 1);
+    ++res->steps_done;
+    if (guard) {
+      res->aborted = 1;
+      res->abort_kind = EMRKC_ABORT_NORM_GUARD;
+      res->abort_step = step;
+      break;
+    }
+    CK(h, emrkc_k::launch_gate_range(h->geom, h->buf[h->cur], h->d_slots, h->stream));
+  }
+  CK(h, cudaEventRecord(h->ev1, h->stream));
+  unsigned long long sl[2];
+  CK(h, cudaMemcpyAsync(sl, h->d_slots, sizeof(sl), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  // track_gate_range from gate_min = 1, gate_max = 0 (simulate.cpp:111-113)
+  res->gate_min = 1.0;
+  res->gate_max = 0.0;
+  if (sl[0] != kNoEvent) res->gate_min = std::min(1.0, emrkc_k::double_of(sl[0]));
+  if (sl[1] != 0ull) res->gate_max = std::max(0.0, emrkc_k::double_of(sl[1]));
+  float ms = 0.0f;
+  CK(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  res->device_ms = ms;
+  if (cg_iters_total) *cg_iters_total = iters_total;
+  return EMRKC_OK;
 }
 
 int emrkc_run_timed(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,

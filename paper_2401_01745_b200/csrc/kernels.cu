@@ -671,6 +671,215 @@ __global__ void __launch_bounds__(kRedThreads)
   }
 }
 
+// ---- IMEX-RL (P/src/baselines.cpp:89-190) ---------------------------------
+// sqrt of the trapezoid node weight (quadrature_weights,
+// P/src/monodomain.cpp:52-63): 1/2 per axis on which the node is a boundary.
+template <int DIM>
+__device__ __forceinline__ double sqrt_w(const Geom& g, long long i) {
+  double w = 1.0;
+  long long r = i;
+  const long long na[3] = {g.n0, g.n1, g.nzl};
+#pragma unroll
+  for (int ax = 0; ax < DIM; ++ax) {
+    const long long ia = r % na[ax];
+    r /= na[ax];
+    if (ia == 0 || ia == na[ax] - 1) w *= 0.5;
+  }
+  return sqrt(w);
+}
+
+// Rush-Larsen part (rush_larsen_update, baselines.cpp:89-128) and the CG
+// right-hand side / warm start (:164-168): gates of `out`, b, x; partials
+// of ||b||^2.
+template <int DIM>
+__global__ void __launch_bounds__(kRedThreads)
+    k_imex_prep(const Geom g, const double* __restrict__ y, double dt, double stim,
+                double* __restrict__ out, double* __restrict__ b, double* __restrict__ x,
+                double* __restrict__ partial) {
+  const long long nn = g.nn;
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)kRedThreads + threadIdx.x; i < nn;
+       i += (long long)gridDim.x * kRedThreads) {
+    const Node<DIM> n = node_flat<DIM>(g, i);
+    const double V = y[i];
+    double l[3], zi[3], zn[3];
+    hh_gate_coeffs_ref(V, l, zi);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double z = y[(q + 1) * nn + i];
+      zn[q] = __dadd_rn(z, __dmul_rn(expm1(__dmul_rn(dt, l[q])), __dsub_rn(z, zi[q])));
+      out[(q + 1) * nn + i] = zn[q];
+    }
+    const double vr = slow_v<0>(g, in_stim<DIM>(g, n) ? stim : 0.0, V, zn[0], zn[1], zn[2]);
+    const double sw = sqrt_w<DIM>(g, i);
+    const double bi = __dmul_rn(sw, __dadd_rn(V, __dmul_rn(dt, vr)));
+    b[i] = bi;
+    x[i] = __dmul_rn(sw, V);
+    acc = __dadd_rn(acc, __dmul_rn(bi, bi));
+  }
+  const double t = block_sum(acc);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// op(u) = u - dt sqrt(w) D(u / sqrt(w)) at node i (the CG operator, :154-158)
+template <int DIM>
+__device__ __forceinline__ double cg_op(const Geom& g, const Node<DIM>& n,
+                                        const double* __restrict__ u, double dt) {
+  const auto f = [&](long long j) { return __ddiv_rn(u[j], sqrt_w<DIM>(g, j)); };
+  const auto none = [](long long) { return 0.0; };
+  const double d = lap<DIM>(g, n, f(n.i), f, none, none);
+  return __dsub_rn(u[n.i], __dmul_rn(__dmul_rn(dt, sqrt_w<DIM>(g, n.i)), d));
+}
+
+// r = b - op(x), z = r / diag (Jacobi, diag <= 0: none), p = z; partials
+// of r.z and r.r (cg_solve, :41-49)
+template <int DIM>
+__global__ void __launch_bounds__(kRedThreads)
+    k_cg_init(const Geom g, double dt, double diag, const double* __restrict__ b,
+              const double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+              double* __restrict__ p, double* __restrict__ partial) {
+  const long long nn = g.nn;
+  double arz = 0.0, arr = 0.0;
+  for (long long i = blockIdx.x * (long long)kRedThreads + threadIdx.x; i < nn;
+       i += (long long)gridDim.x * kRedThreads) {
+    const Node<DIM> n = node_flat<DIM>(g, i);
+    const double ri = __dsub_rn(b[i], cg_op<DIM>(g, n, x, dt));
+    const double zz = diag > 0.0 ? __ddiv_rn(ri, diag) : ri;
+    r[i] = ri;
+    z[i] = zz;
+    p[i] = zz;
+    arz = __dadd_rn(arz, __dmul_rn(ri, zz));
+    arr = __dadd_rn(arr, __dmul_rn(ri, ri));
+  }
+  const double t0 = block_sum(arz);
+  __syncthreads();
+  const double t1 = block_sum(arr);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = t0;
+    partial[2 * blockIdx.x + 1] = t1;
+  }
+}
+
+// One-block scalar steps of cg_solve. phase 0: ||b|| and the initial r.z,
+// r.r (loop entry); phase 1: alpha = rz / p.q; phase 2: beta, rnorm, the
+// loop test (while rnorm > tol, iterations < max_iters).
+__global__ void __launch_bounds__(kRedThreads)
+    k_cg_scalar(const double* __restrict__ partial, int n, int phase, CgScalars* cs,
+                const double* __restrict__ partial_b, double rel_tol, long long max_it) {
+  double a0 = 0.0, a1 = 0.0, ab = 0.0;
+  for (int i = threadIdx.x; i < n; i += kRedThreads) {
+    if (phase == 1) {
+      a0 = __dadd_rn(a0, partial[i]);
+    } else {
+      a0 = __dadd_rn(a0, partial[2 * i]);
+      a1 = __dadd_rn(a1, partial[2 * i + 1]);
+    }
+    if (phase == 0) ab = __dadd_rn(ab, partial_b[i]);
+  }
+  const double t0 = block_sum(a0);
+  __syncthreads();
+  const double t1 = block_sum(a1);
+  __syncthreads();
+  const double tb = block_sum(ab);
+  if (threadIdx.x != 0) return;
+  if (phase == 0) {
+    cs->nb2 = tb;
+    cs->tol = rel_tol * sqrt(tb);
+    cs->rz = t0;
+    cs->rr = t1;
+    cs->it = 0;
+    cs->max_it = max_it;
+    cs->converged = 1;
+    cs->done = !(sqrt(t1) > cs->tol);
+    return;
+  }
+  if (cs->done) return;
+  if (phase == 1) {
+    cs->pq = t0;
+    cs->alpha = __ddiv_rn(cs->rz, t0);
+    return;
+  }
+  cs->beta = __ddiv_rn(t0, cs->rz);
+  cs->rz = t0;
+  cs->rr = t1;
+  cs->it += 1;
+  if (!(sqrt(t1) > cs->tol)) {
+    cs->done = 1;
+  } else if (cs->it >= cs->max_it) {
+    cs->done = 1;
+    cs->converged = 0;
+  }
+}
+
+// q = op(p); partials of p.q
+template <int DIM>
+__global__ void __launch_bounds__(kRedThreads)
+    k_cg_apply(const Geom g, double dt, const double* __restrict__ p, double* __restrict__ q,
+               double* __restrict__ partial, const CgScalars* cs) {
+  if (cs->done) return;
+  const long long nn = g.nn;
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)kRedThreads + threadIdx.x; i < nn;
+       i += (long long)gridDim.x * kRedThreads) {
+    const Node<DIM> n = node_flat<DIM>(g, i);
+    const double qi = cg_op<DIM>(g, n, p, dt);
+    q[i] = qi;
+    acc = __dadd_rn(acc, __dmul_rn(p[i], qi));
+  }
+  const double t = block_sum(acc);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// x += alpha p, r -= alpha q, z = r / diag; partials of r.z, r.r
+__global__ void __launch_bounds__(kRedThreads)
+    k_cg_update(long long nn, double diag, double* __restrict__ x, double* __restrict__ r,
+                double* __restrict__ z, const double* __restrict__ p,
+                const double* __restrict__ q, double* __restrict__ partial,
+                const CgScalars* cs) {
+  if (cs->done) return;
+  const double alpha = cs->alpha;
+  double arz = 0.0, arr = 0.0;
+  for (long long i = blockIdx.x * (long long)kRedThreads + threadIdx.x; i < nn;
+       i += (long long)gridDim.x * kRedThreads) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+    const double ri = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+    r[i] = ri;
+    const double zz = diag > 0.0 ? __ddiv_rn(ri, diag) : ri;
+    z[i] = zz;
+    arz = __dadd_rn(arz, __dmul_rn(ri, zz));
+    arr = __dadd_rn(arr, __dmul_rn(ri, ri));
+  }
+  const double t0 = block_sum(arz);
+  __syncthreads();
+  const double t1 = block_sum(arr);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = t0;
+    partial[2 * blockIdx.x + 1] = t1;
+  }
+}
+
+// p = z + beta p (after the loop test: skipped once done)
+__global__ void __launch_bounds__(kRedThreads)
+    k_cg_dir(long long nn, const double* __restrict__ z, double* __restrict__ p,
+             const CgScalars* cs) {
+  if (cs->done) return;
+  const double beta = cs->beta;
+  for (long long i = blockIdx.x * (long long)kRedThreads + threadIdx.x; i < nn;
+       i += (long long)gridDim.x * kRedThreads)
+    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+}
+
+// V_new = x / sqrt(w) (:185); x = 0 when ||b|| = 0 (:25-29)
+template <int DIM>
+__global__ void __launch_bounds__(kRedThreads)
+    k_cg_finish(const Geom g, const double* __restrict__ x, double* __restrict__ out,
+                const CgScalars* cs) {
+  const bool zero = cs->nb2 == 0.0;
+  for (long long i = blockIdx.x * (long long)kRedThreads + threadIdx.x; i < g.nn;
+       i += (long long)gridDim.x * kRedThreads)
+    out[i] = zero ? 0.0 : __dmul_rn(__ddiv_rn(1.0, sqrt_w<DIM>(g, i)), x[i]);
+}
+
 __global__ void __launch_bounds__(kRedThreads)
     k_sum_partials(const double* __restrict__ partial, int n,
                    double* __restrict__ out) {
@@ -797,6 +1006,67 @@ cudaError_t launch_mrkc_stage(const Geom& g, const MrkcArgs& a, cudaStream_t st)
   const dim3 blk(BX, BY);
   DISPATCH_DIM(g, { k_mrkc_stage<D><<<grid_of<D>(g), blk, 0, st>>>(g, a); });
   return cudaGetLastError();
+}
+
+cudaError_t launch_imex_prep(const Geom& g, const double* y, double dt, double stim,
+                             double* out, double* b, double* x, double* partial, int nblocks,
+                             cudaStream_t st) {
+  DISPATCH_DIM(g, {
+    k_imex_prep<D><<<nblocks, kRedThreads, 0, st>>>(g, y, dt, stim, out, b, x, partial);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_init(const Geom& g, double dt, double diag, const double* b,
+                           const double* x, double* r, double* z, double* p, double* partial,
+                           int nblocks, CgScalars* cs, double rel_tol, long long max_it,
+                           const double* partial_b, cudaStream_t st) {
+  DISPATCH_DIM(g, {
+    k_cg_init<D><<<nblocks, kRedThreads, 0, st>>>(g, dt, diag, b, x, r, z, p, partial);
+  });
+  k_cg_scalar<<<1, kRedThreads, 0, st>>>(partial, nblocks, 0, cs, partial_b, rel_tol, max_it);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_iter(const Geom& g, double dt, double diag, double* x, double* r,
+                           double* z, double* p, double* q, double* partial, int nblocks,
+                           CgScalars* cs, cudaStream_t st) {
+  DISPATCH_DIM(g, {
+    k_cg_apply<D><<<nblocks, kRedThreads, 0, st>>>(g, dt, p, q, partial, cs);
+  });
+  k_cg_scalar<<<1, kRedThreads, 0, st>>>(partial, nblocks, 1, cs, nullptr, 0.0, 0);
+  k_cg_update<<<nblocks, kRedThreads, 0, st>>>(g.nn, diag, x, r, z, p, q, partial, cs);
+  k_cg_scalar<<<1, kRedThreads, 0, st>>>(partial, nblocks, 2, cs, nullptr, 0.0, 0);
+  k_cg_dir<<<nblocks, kRedThreads, 0, st>>>(g.nn, z, p, cs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_finish(const Geom& g, const double* x, double* out, const CgScalars* cs,
+                             cudaStream_t st) {
+  DISPATCH_DIM(g, { k_cg_finish<D><<<power_blocks(), kRedThreads, 0, st>>>(g, x, out, cs); });
+  return cudaGetLastError();
+}
+
+// norm guard of run_simulation (max_abs_v > 1e6, non-finite -> inf;
+// P/src/simulate.cpp:67-74,222-227): flag = 1 if any |V| > 1e6 or NaN
+__global__ void k_v_guard(long long nn, const double* __restrict__ y, int* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nn;
+       i += (long long)gridDim.x * blockDim.x)
+    if (!(fabs(y[i]) <= 1e6)) atomicOr(flag, 1);
+}
+
+cudaError_t launch_v_guard(long long nn, const double* y, int* flag, cudaStream_t st) {
+  k_v_guard<<<power_blocks(), 256, 0, st>>>(nn, y, flag);
+  return cudaGetLastError();
+}
+
+double diffusion_diag(const Geom& g) {
+  // diffusion_apply(e_0)[0]: node 0 is a corner; the mirror doubles the
+  // neighbour weight of every axis, the centre term is -2 w_a per axis
+  // (P/src/monodomain.cpp:73-90) -> sum over axes of w_a (0 - 2 + 0)
+  double d = 0.0;
+  for (int a = 0; a < g.dim; ++a) d += g.w[a] * (0.0 - 2.0 * 1.0 + 0.0);
+  return d;
 }
 
 cudaError_t launch_exp_part(const Geom& g, const double* y, double* lam,

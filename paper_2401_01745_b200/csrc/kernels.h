@@ -86,6 +86,35 @@ struct MrkcArgs {
 };
 cudaError_t launch_mrkc_stage(const Geom& g, const MrkcArgs& a, cudaStream_t st);
 
+// IMEX-RL (P/src/baselines.cpp:132-190): Rush-Larsen gates, then
+// (I - dt D) V_new = V + dt v_rhs by Jacobi-preconditioned CG in
+// sqrt(w)-scaled coordinates (w: trapezoid node weights). Device scalars:
+struct CgScalars {
+  double nb2;      // ||b||^2
+  double rz, pq, rr;
+  double alpha, beta;
+  double tol;      // rel_tol ||b||
+  long long it, max_it;
+  int done, converged;
+};
+// vectors (n_nodes each): b, x, r, z, p, q
+cudaError_t launch_imex_prep(const Geom& g, const double* y, double dt, double stim,
+                             double* out, double* b, double* x, double* partial, int nblocks,
+                             cudaStream_t st);
+cudaError_t launch_cg_init(const Geom& g, double dt, double diag, const double* b,
+                           const double* x, double* r, double* z, double* p, double* partial,
+                           int nblocks, CgScalars* cs, double rel_tol, long long max_it,
+                           const double* partial_b, cudaStream_t st);
+cudaError_t launch_cg_iter(const Geom& g, double dt, double diag, double* x, double* r,
+                           double* z, double* p, double* q, double* partial, int nblocks,
+                           CgScalars* cs, cudaStream_t st);
+cudaError_t launch_cg_finish(const Geom& g, const double* x, double* out, const CgScalars* cs,
+                             cudaStream_t st);
+cudaError_t launch_v_guard(long long nn, const double* y, int* flag, cudaStream_t st);
+// diffusion_apply of the unit vector at node 0, component 0 (the constant
+// diagonal of the reflection stencil, baselines.cpp:171-177)
+double diffusion_diag(const Geom& g);
+
 // Arguments of the fast kernels (kernels_fast.cu): one outer stage j.
 struct FastArgs {
   const double* g1;   // g_{j-1}

@@ -341,6 +341,28 @@ class MonodomainOperator:
                                      C.byref(res)), self._h)
         return res
 
+    # ---- IMEX-RL (P/src/baselines.cpp:132-190) ----
+    def imex_step(self, t: float, dt: float, rel_tol: float = 1e-8, max_iters: int = 0,
+                  jacobi: bool = True):
+        """One IMEX-RL step; returns (report, CG iterations)."""
+        rep = StepReport()
+        it = C.c_int64(0)
+        rc = _lib().emrkc_imex_step(self._h, t, dt, rel_tol, max_iters, int(jacobi),
+                                    C.byref(rep), C.byref(it))
+        if rc == capi.EMRKC_ENONFINITE:
+            raise NumericalAbort(_lib().emrkc_last_error(self._h).decode(), -1)
+        _check(rc, self._h)
+        return rep, it.value
+
+    def imex_run(self, step0: int, nsteps: int, dt: float, rel_tol: float = 1e-8,
+                 max_iters: int = 0, jacobi: bool = True):
+        """run_simulation's imex_rl loop; returns (RunResult, cg_iters_total)."""
+        res = RunResult()
+        it = C.c_int64(0)
+        _check(_lib().emrkc_imex_run(self._h, step0, nsteps, dt, rel_tol, max_iters, int(jacobi),
+                                     C.byref(res), C.byref(it)), self._h)
+        return res, it.value
+
     def exex_step(self, t: float, dt: float) -> StepReport:
         """One EXEX-RL step of the device state (exex_rl_step,
         P/src/baselines.cpp:192-210); never raises NumericalAbort."""

@@ -151,3 +151,30 @@ def test_mrkc_bitwise(oracle, reference, name, nsteps):
     assert np.array_equal(ya, yb)
     _same_records(ra, rb)
     assert ra.n_exp == 0 and ra.n_fF == nsteps * ra.s * ra.m and ra.n_fS == nsteps * ra.s
+
+
+@pytest.mark.parametrize("name,dt,nsteps,jacobi", [("p2d_128_s3m2", 0.02, 8, True),
+                                                   ("p3d_48_s2m2", 0.05, 3, True),
+                                                   ("hh2d_256x256", 0.05, 10, False)])
+def test_imex_rl_bitwise(oracle, reference, name, dt, nsteps, jacobi):
+    """imex_rl_step with cg_solve (P/src/baselines.cpp:20-82,132-190)."""
+    w = workloads.get(name)
+    p = w.problem
+    y0 = w.initial_state()
+    ya, ra, ia = oracle.run_imex(p, y0, 0, nsteps, dt, 1e-8, 0, jacobi)
+    yb, rb, ib = reference.run_imex(p, y0, 0, nsteps, dt, 1e-8, 0, jacobi)
+    assert np.array_equal(ya, yb)
+    _same_records(ra, rb)
+    assert ia == ib > 0 and ra.n_fF == ia + 2 * nsteps
+
+
+def test_imex_rl_cg_failure(oracle, reference):
+    """max_iters too small: NumericalAbort, state not assigned."""
+    w = workloads.get("p2d_128_s3m2")
+    p = w.problem
+    y0 = w.initial_state()
+    ya, ra, _ = oracle.run_imex(p, y0, 4, 3, 0.05, 1e-12, 2, True)
+    yb, rb, _ = reference.run_imex(p, y0, 4, 3, 0.05, 1e-12, 2, True)
+    _same_records(ra, rb)
+    assert ra.aborted and ra.abort_step == 4 and ra.steps_done == 0
+    assert np.array_equal(ya, y0) and np.array_equal(yb, y0)
