@@ -179,6 +179,48 @@ class DeviceMonodomain {
     return res;
   }
 
+  // mRKC with the stiff-gate split (gates in `mask` join f_F).
+  void set_stiff_gates(int mask) { check(emrkc_set_stiff_gates(h_, mask), h_); }
+  MultirateStepReport mrkc_step(double t, double dt, double rho_F, double rho_S,
+                                double epsilon = 0.05) {
+    emrkc_step_report r{};
+    const int rc = emrkc_mrkc_step(h_, t, dt, epsilon, rho_F, rho_S, &r);
+    check(rc, h_, -1, dt, r.abort_stage);
+    return to_report(r);
+  }
+  RunResult mrkc_run(long step0, long nsteps, double dt, double rho_F, double rho_S,
+                     double epsilon = 0.05) {
+    RunResult res;
+    check(emrkc_mrkc_run(h_, step0, nsteps, dt, epsilon, rho_F, rho_S, &res.raw), h_);
+    return res;
+  }
+
+  // IMEX-RL with CgConfig (rel_tol, max_iters 0 = 10 sqrt(n) + 1, jacobi).
+  long imex_step(double t, double dt, double rel_tol = 1e-8, long max_iters = 0,
+                 bool jacobi = true) {
+    emrkc_step_report r{};
+    int64_t it = 0;
+    check(emrkc_imex_step(h_, t, dt, rel_tol, max_iters, jacobi ? 1 : 0, &r, &it), h_, -1, dt);
+    return static_cast<long>(it);
+  }
+  RunResult imex_run(long step0, long nsteps, double dt, double rel_tol = 1e-8,
+                     long max_iters = 0, bool jacobi = true, long* cg_iters_total = nullptr) {
+    RunResult res;
+    int64_t it = 0;
+    check(emrkc_imex_run(h_, step0, nsteps, dt, rel_tol, max_iters, jacobi ? 1 : 0, &res.raw,
+                         &it),
+          h_);
+    if (cg_iters_total) *cg_iters_total = static_cast<long>(it);
+    return res;
+  }
+
+  // rel_l2_error of SoA block `block` of the device state against host `ref`.
+  double rel_l2_error(const Vec& ref, int block = 0) const {
+    double e = 0.0;
+    check(emrkc_rel_l2_error(h_, block, ref.data(), 0, &e), h_);
+    return e;
+  }
+
   // One EXEX-RL step of the device state (never throws NumericalAbort).
   void exex_step(double t, double dt) {
     emrkc_step_report r{};
