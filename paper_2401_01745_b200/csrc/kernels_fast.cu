@@ -1112,6 +1112,12 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
 #define EMRKC_TMA_LA 3
 #endif
 constexpr int kTmaLA = EMRKC_TMA_LA;
+#ifndef EMRKC_ISSUE1
+#define EMRKC_ISSUE1 1
+#endif
+#ifndef EMRKC_HALOPUT
+#define EMRKC_HALOPUT 1
+#endif
 static_assert(kTmaLA >= 1 && kTmaLA + 2 <= kRV && kTmaLA <= kRG, "TMA lookahead");
 
 template <int DIM>
@@ -1202,10 +1208,12 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
       const unsigned vd = v0 + 8u * VS * (q & (kRV - 1));
       if (DIM == 3) tma_load_3d(vd, &tm.v, bar, x0 - 2, y0 - 1, zz);
       else tma_load_2d(vd, &tm.v, bar, x0 - 2, zz);
-    } else if (role == 1) {
+    }
+    if (role == (EMRKC_ISSUE1 ? 0 : 1)) {
       if (DIM == 3) tma_load_4d(gs0 + 8u * 3 * T::NT * sg, &tm.gates, bar, x0, y0, zz, 1);
       else tma_load_3d(gs0 + 8u * 3 * T::NT * sg, &tm.gates, bar, x0, zz, 1);
-    } else if (!FIRST && role == 2) {
+    }
+    if (!FIRST && role == (EMRKC_ISSUE1 ? 0 : 2)) {
       if (DIM == 3) tma_load_4d(qs0 + 8u * 4 * T::NT * sg, &tm.g2, bar, x0, y0, zz, 0);
       else tma_load_3d(qs0 + 8u * 4 * T::NT * sg, &tm.g2, bar, x0, zz, 0);
     }
@@ -1222,7 +1230,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   pdl_wait();
   halo_wait(h, zb == 0, ze >= g.nzl);
   int nq = 0;  // prologue loads (planes zb - 1 ...)
-  if (role >= 0 && role <= 2) {
+  if (EMRKC_ISSUE1 ? role == 0 : (role >= 0 && role <= 2)) {
     if (role == 0) {
       // ghost planes arrived through generic peer stores (acquired in
       // halo_wait); order them before this thread's async-proxy reads
@@ -1269,9 +1277,15 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     mbar_wait(b0, 0);       // plane zb - 1
     mbar_wait(b0 + 8u, 0);  // plane zb
   }
+#if EMRKC_HALOPUT
+  // halo puts hoisted: the plane (if any) whose V this thread stores into a
+  // neighbour's ghost slot (-1: none)
+  const int zpl = (h.put_lo != nullptr) ? 0 : -1;
+  const int zph = (h.put_hi != nullptr) ? g.nzl - 1 : -1;
+#endif
   for (int z = zb; z < ze && !skipped; ++z) {
     const int p = z - zb + 1;
-    if (role >= 0) {
+    if (EMRKC_ISSUE1 ? role == 0 : role >= 0) {
       if (z + kTmaLA < ze) issue_comp(z + kTmaLA);
       else if (z + kTmaLA == ze) issue_edge(ze, 0);
     }
@@ -1305,8 +1319,13 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
+#if EMRKC_HALOPUT
+      if (z == zpl) h.put_lo[ip] = r.o0;
+      if (z == zph) h.put_hi[ip] = r.o0;
+#else
       if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
       if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
+#endif
       if (a.last) {  // std::min / std::max per value (NaN skipped), select form
         glo = r.o1 < glo ? r.o1 : glo;
         ghi = ghi < r.o1 ? r.o1 : ghi;
@@ -1432,10 +1451,12 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
       const unsigned vd = v0 + 8u * VS * (q & (kRV - 1));
       if (DIM == 3) tma_load_3d(vd, &tm.u, bar, x0 - 2, y0 - 1, zz);
       else tma_load_2d(vd, &tm.u, bar, x0 - 2, zz);
-    } else if (role == 1) {
+    }
+    if (role == (EMRKC_ISSUE1 ? 0 : 1)) {
       if (!d1_is_u) center(&tm.d1, sc, bar, zz);
       if (has2) center(&tm.um2, sc + 8u * T::NT, bar, zz);
-    } else if (LAST && role == 2) {
+    }
+    if (LAST && role == (EMRKC_ISSUE1 ? 0 : 2)) {
       center(&tm.g1v, sc + 16u * T::NT, bar, zz);
       if (!FIRST) center(&tm.g2v, sc + 24u * T::NT, bar, zz);
     }
@@ -1450,7 +1471,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
   };
   pdl_wait();
   halo_wait(h, zb == 0, ze >= g.nzl);
-  if (role >= 0 && role <= 2) {
+  if (EMRKC_ISSUE1 ? role == 0 : (role >= 0 && role <= 2)) {
     // ghost planes arrived through generic peer stores (acquired in
     // halo_wait); order them before this thread's async-proxy reads
     if (role == 0) fence_proxy_async();
@@ -1483,7 +1504,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
   }
   for (int z = zb; z < ze && !skipped; ++z) {
     const int p = z - zb + 1;
-    if (role >= 0) {
+    if (EMRKC_ISSUE1 ? role == 0 : role >= 0) {
       if (z + kTmaLA < ze) issue_comp(z + kTmaLA);
       else if (z + kTmaLA == ze) issue_edge(ze);
     }

@@ -25,6 +25,8 @@ def t(f, reps=10):
 
 
 def both():
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s1):
         d1.copy_(h1, non_blocking=True)
     with torch.cuda.stream(s2):
