@@ -2273,7 +2273,7 @@ int emrkc_run_timed(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
                     double rho_S, int64_t flush_bytes, double* launch_ms,
                     int64_t launch_ms_len, emrkc_run_result* res) {
   if (!h || !res || !launch_ms) return set_global(EMRKC_EINVAL, "null argument");
-  if (h->partitioned && !dist_linked(h))
+  if (h->partitioned && !dist_linked(h) && !(h->z_begin == 0 && h->z_end == h->p.n[h->p.dim - 1]))
     return set_err(h, EMRKC_EINVAL, "emrkc_run_timed: whole-grid or distributed handles only");
   if (variant_method(variant, &h->method))
     return set_err(h, EMRKC_EINVAL, "emrkc_run: unknown variant %d", variant);

@@ -169,6 +169,22 @@ def hh3d_cube(N: int, h: float) -> Workload:
     return Workload(f"hh3d_cube_{N}_h{h}", p, 0.05, 5.0, "v_normal_0.1", 90 + N)
 
 
+def z_scaled(w: Workload, n: int) -> Workload:
+    """Weak-scaling form of ``w`` for n z-slabs: the grid repeated n times
+    along the slab axis (same spacing, conductivities, stimulus box, dt, T),
+    so each of n equal slabs holds exactly ``w``'s node count."""
+    if n == 1:
+        return w
+    p = w.problem
+    q = make_problem(p.dim, [int(p.n[a]) * (n if a == p.dim - 1 else 1) for a in range(p.dim)],
+                     [p.dx[a] for a in range(p.dim)], [p.sigma[a] for a in range(p.dim)],
+                     p.chi, p.C_m, p.stim_chi_amplitude, [p.stim_lo[a] for a in range(p.dim)],
+                     [p.stim_hi[a] for a in range(p.dim)], p.stim_t0, p.stim_t1)
+    return Workload(f"{w.name}_zx{n}", q, w.dt, w.t_end, w.noise, w.seed, w.eps, w.rho_S_forced,
+                    note=(w.note + "; " if w.note else "") +
+                    f"weak scaling: {w.name} repeated {n}x along z (one copy per GPU)")
+
+
 def get(name: str) -> Workload:
     if name.startswith("hh3d_cube_"):  # hh3d_cube_<N>_h<h>
         n, h = name[len("hh3d_cube_"):].split("_h")
