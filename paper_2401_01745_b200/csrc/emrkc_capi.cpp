@@ -302,6 +302,9 @@ struct emrkc_handle {
   } peer[2];
   unsigned long long recv[2] = {0, 0};  // arrivals expected so far per side
   double* ckpt = nullptr;               // dist_run input state, for replay
+  double* res_v = nullptr;              // resident runs: V ping-pong [2][nn]
+  double* res_stim = nullptr;           // resident runs: stimulus rate per step
+  int64_t res_stim_n = 0;
   long long level = 0;
   // device scalars
   unsigned long long* d_event = nullptr;
@@ -1111,6 +1114,8 @@ void emrkc_destroy(emrkc_handle* h) {
     if (pe.ipc && pe.arena) cudaIpcCloseMemHandle(pe.arena);
   if (h->arena) cudaFree(h->arena);
   if (h->ckpt) cudaFree(h->ckpt);
+  if (h->res_v) cudaFree(h->res_v);
+  if (h->res_stim) cudaFree(h->res_stim);
   if (h->d_event) cudaFree(h->d_event);
   if (h->d_slots) cudaFree(h->d_slots);
   if (h->d_coef) cudaFree(h->d_coef);
@@ -1502,6 +1507,67 @@ int variant_method(int32_t variant, int* method) {
   return EMRKC_OK;
 }
 
+// Whole-run resident kernel (k_resident): small whole-grid runs with
+// s = m = 1 on the fast kernels (EMRKC_RESIDENT=0 disables).
+bool resident_ok(const emrkc_handle* h, int64_t nsteps) {
+  static const bool on = [] {
+    const char* e = std::getenv("EMRKC_RESIDENT");
+    return !(e && *e == '0');
+  }();
+  const Plan& pl = h->plan;
+  return on && h->fast && !h->partitioned && nsteps >= 2 && pl.s == 1 && pl.m == 1 &&
+         pl.method != kMethodMrkc && (h->geom.dim == 2 || h->geom.dim == 3) &&
+         h->geom.nn <= emrkc_k::resident_capacity(h->geom.dim);
+}
+
+// One cooperative launch for steps step0 .. step0 + nsteps - 1; the run's
+// final state lands in buffer *out_idx. The abort word and the per-step
+// gate-range slots are the per-step kernels' (decode_event, fold).
+int run_resident(emrkc_handle* h, int64_t step0, int64_t nsteps, int* out_idx) {
+  const Plan& pl = h->plan;
+  int rc = ensure_buffers(h, std::max(2, h->nbuf));
+  if (rc) return rc;
+  const int in = h->cur, out = (in + 1) % h->nbuf;
+  if (!h->res_v) CK(h, cudaMalloc(&h->res_v, sizeof(double) * 2 * h->nn));
+  if (h->res_stim_n < nsteps) {
+    if (h->res_stim) cudaFree(h->res_stim);
+    h->res_stim = nullptr;
+    CK(h, cudaMalloc(&h->res_stim, sizeof(double) * nsteps));
+    h->res_stim_n = nsteps;
+  }
+  std::vector<double> stim(nsteps);
+  for (int64_t r = 0; r < nsteps; ++r)  // stage time t = step dt (simulate.cpp:177)
+    stim[r] = stim_rate_at(&h->p, static_cast<double>(step0 + r) * pl.dt);
+  CK(h, cudaMemcpyAsync(h->res_stim, stim.data(), sizeof(double) * nsteps,
+                        cudaMemcpyHostToDevice, h->stream));
+  emrkc_k::ResidentArgs ra{};
+  emrkc_k::FastArgs& f = ra.f;  // launch_level's j = k = 1 arguments
+  const double cG = pl.mudt[1] / pl.eta;
+  f.eta = pl.eta;
+  f.cG = cG * pl.gate_c;
+  f.cV = cG * pl.in_mueta[1];
+  f.mue1 = pl.in_mueta[1];
+  f.exex = pl.exex;
+  f.vfast = pl.eta <= 1.5 ? 150.0 : -1.0;
+  f.j = 1;
+  f.m = pl.m;
+  f.s = pl.s;
+  f.last = 1;
+  f.z_lo = 0;
+  f.z_hi = h->geom.nzl;
+  f.event = h->d_event;
+  ra.y_in = h->buf[in];
+  ra.y_out = h->buf[out];
+  ra.vbuf = h->res_v;
+  ra.stim = h->res_stim;
+  ra.nsteps = nsteps;
+  ra.stride = static_cast<unsigned long long>(pl.s) * (pl.m + 1) + 2;  // begin_step's
+  ra.slots = h->d_slots;
+  CK(h, emrkc_k::launch_resident(h->geom, ra, h->stream));
+  *out_idx = out;
+  return EMRKC_OK;
+}
+
 int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
               int64_t nsteps, double dt, double eps, double rho_F,
               double rho_S, emrkc_run_result* res, bool single_step,
@@ -1641,6 +1707,12 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     if (scratch) cudaFree(scratch);
     if (scratch_rd) cudaFree(scratch_rd);
     if (res) res->device_ms = tot;  // overwritten below, restored after
+  } else if (n == 1 && !single_step && resident_ok(hs[0], nsteps)) {
+    emrkc_handle* h = hs[0];
+    int out = 0;
+    if ((rc = run_resident(h, step0, nsteps, &out))) return rc;
+    for (int64_t r = 0; r < nsteps; ++r) in_idx[0][r] = out;  // rollback is in-kernel
+    h->cur = out;
   } else if (n == 1) {
     emrkc_handle* h = hs[0];
     for (int64_t r = 0; r < nsteps; ++r) {

@@ -137,6 +137,25 @@ struct FastArgs {
   unsigned long long* gate_slot;
 };
 
+// Whole-run resident kernel for small grids (s = m = 1; emRKC standard /
+// progressive, EXEX-RL): one cooperative launch runs all steps of an
+// emrkc_run. Every thread keeps its nodes' gates in registers, V ping-pongs
+// through two L2-resident fields, and a grid barrier separates the steps;
+// the node arithmetic is k_node_tma's, operation for operation.
+struct ResidentArgs {
+  FastArgs f;                    // stage coefficients (g1/g2/out/stim unused)
+  const double* y_in;            // state at the run start (4 blocks)
+  double* y_out;                 // state the run ends on (4 blocks)
+  double* vbuf;                  // [2][nn] V ping-pong
+  const double* stim;            // stimulus rate per step [nsteps]
+  long long nsteps;
+  unsigned long long stride;     // abort-ordinal stride per step
+  unsigned long long* slots;     // per-step gate range [2 * nsteps]
+};
+// Largest grid the resident kernel takes on this device (0: none).
+long long resident_capacity(int dim);
+cudaError_t launch_resident(const Geom& g, const ResidentArgs& a, cudaStream_t st);
+
 // Inner stages in increment form: d_k = u_k - V (V = y_E's V block), so
 // d_k = nu' d_{k-1} + kappa' d_{k-2} + mu'_k eta (a + f_F(d_{k-1})) with
 // a = (f_F + f_S)(y_E) = d_1 / (mu'_1 eta) and d_0 = 0 (f_F is linear and

@@ -30,6 +30,8 @@
 #include <type_traits>
 #include <utility>
 
+#include <cooperative_groups.h>
+
 #include "kernels.h"
 #include "tma.cuh"
 
@@ -1394,6 +1396,238 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
   if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, valid && ze > zb);
 }
+
+// ---------------------------------------------------------------------------
+// k_resident: a whole emrkc_run on a small grid in one cooperative launch
+// (s = m = 1). Config 1 (256^2) and the small sweep grids are launch- and
+// latency-bound one step per launch (~11 us for 65k nodes); here every
+// thread owns R nodes for the whole run (gates in registers, old and new for
+// the abort rollback), V ping-pongs through vbuf (L2-resident, read with
+// ld.global.cg so no stale L1 line survives a step), and one grid barrier
+// per step publishes V and the step's abort ordinal. The run-loop semantics
+// are the per-step kernels' (P/src/simulate.cpp:176-229): a non-finite step
+// leaves the pre-step state, a norm-guard step keeps its result, later steps
+// do not run; per-step gate ranges go to the same slots.
+// ---------------------------------------------------------------------------
+constexpr int kResNT = 256;
+template <int DIM, int R>
+__global__ void __launch_bounds__(kResNT) k_resident(const Geom g, const ResidentArgs ra) {
+  namespace cgr = cooperative_groups;
+  const FastArgs& a = ra.f;
+  __shared__ double tab[256];
+  __shared__ unsigned long long ev_sh;
+  __shared__ unsigned long long rlo[kResNT / 32], rhi[kResNT / 32];
+  const int t = threadIdx.x;
+  load_exp_table(tab, t, kResNT);
+  const long long nn = g.nn;
+  const long long b0 = nn * blockIdx.x / gridDim.x, b1 = nn * (blockIdx.x + 1) / gridDim.x;
+  // node k of this thread: b0 + t + k * NT; flags: bit0 x>0, bit1 x<n0-1,
+  // bit2 y>0, bit3 y<n1-1, bit4 z>0, bit5 z<n2-1, bit6 in the stimulus box
+  long long idx[R];
+  unsigned fl[R];
+  double z0[R], z1[R], z2[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    idx[k] = b0 + t + (long long)k * kResNT;
+    fl[k] = 0;
+    z0[k] = z1[k] = z2[k] = 0.0;
+    if (idx[k] < b1) {
+      const long long i = idx[k];
+      const int x = (int)(i % g.n0);
+      const int y = DIM == 3 ? (int)((i / g.n0) % g.n1) : (int)(i / g.n0);
+      const int zz = DIM == 3 ? (int)(i / g.plane) : 0;
+      fl[k] = (x > 0 ? 1u : 0u) | (x < g.n0 - 1 ? 2u : 0u) | (y > 0 ? 4u : 0u) |
+              (y < (DIM == 3 ? g.n1 : g.nzg) - 1 ? 8u : 0u);
+      if (DIM == 3) fl[k] |= (zz > 0 ? 16u : 0u) | (zz < g.nzg - 1 ? 32u : 0u);
+      const bool box = DIM == 3 ? (stim_col_xy<3>(g, x, y) && zz >= g.st_lo[2] && zz <= g.st_hi[2])
+                                : (stim_col_xy<2>(g, x, y) && y >= g.st_lo[1] && y <= g.st_hi[1]);
+      if (box) fl[k] |= 64u;
+      z0[k] = ra.y_in[nn + i];
+      z1[k] = ra.y_in[2 * nn + i];
+      z2[k] = ra.y_in[3 * nn + i];
+      ra.vbuf[i] = ra.y_in[i];
+    }
+  }
+  cgr::grid_group grid = cgr::this_grid();
+  grid.sync();
+  const long long sx = 1, sy = g.n0, sz = DIM == 3 ? g.plane : 0;
+  // the slab axis (z in 3-D, y in 2-D) is the stencil's "vm/vp" direction
+  const long long sv = DIM == 3 ? sz : sy;
+  long long r = 0;
+  int fin = 0;      // buffer holding the final V
+  bool keep_new = false;
+  double n0v[R], n1v[R], n2v[R];
+  for (; r < ra.nsteps; ++r) {
+    const double* V = ra.vbuf + (r & 1) * nn;
+    double* Vn = ra.vbuf + ((r + 1) & 1) * nn;
+    const double stim = ra.stim[r];
+    const unsigned long long cb = (unsigned long long)r * ra.stride;
+    bool inner_bad = false, outer_bad = false, guard = false;
+    double glo = 2.0, ghi = -1.0;
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      n0v[k] = z0[k];
+      n1v[k] = z1[k];
+      n2v[k] = z2[k];
+      if (idx[k] >= b1) continue;
+      const long long i = idx[k];
+      const unsigned f = fl[k];
+      const double vc = __ldcg(V + i);
+      // slab-axis neighbours (mirror at the boundary, P/src/monodomain.cpp:85-86)
+      const unsigned bm = DIM == 3 ? 16u : 4u, bp = DIM == 3 ? 32u : 8u;
+      const double vm = __ldcg(V + i + ((f & bm) ? -sv : sv));
+      const double vp = __ldcg(V + i + ((f & bp) ? sv : -sv));
+      const double xs = __ldcg(V + i + ((f & 1u) ? -sx : sx)) + __ldcg(V + i + ((f & 2u) ? sx : -sx));
+      double ys = 0.0;
+      if (DIM == 3) ys = __ldcg(V + i + ((f & 4u) ? -sy : sy)) + __ldcg(V + i + ((f & 8u) ? sy : -sy));
+      const bool box = (f & 64u) != 0;
+      const bool fast = fabs(vc) <= a.vfast;
+      NodeOut o;
+      if (fast) {
+        o = node_update_s<DIM, 1, 0, 0>(g, a, tab, vm, vc, vp, xs, ys, z0[k], z1[k], z2[k], 0.0,
+                                         nullptr, 1);
+        if (box) o.o0 = fma(a.cV, stim, o.o0);
+      } else {  // k_node_tma's deferred-node arithmetic
+        double q[4] = {0.0, 0.0, 0.0, 0.0};
+        o = node_update_s<DIM, 1, 0, 1>(g, a, tab, vm, vc, vp, xs, ys, z0[k], z1[k], z2[k],
+                                         box ? stim : 0.0, q, 1);
+      }
+      Vn[i] = o.o0;
+      n0v[k] = o.o1;
+      n1v[k] = o.o2;
+      n2v[k] = o.o3;
+      guard |= !(fabs(o.o0) <= 1e6);
+      if (!finite_hi((o.o0 + o.o1) + (o.o2 + o.o3)) && !a.exex) {
+        // inner stage 1 is checked before the outer stage (P/src/cheb.cpp:73-80)
+        double D = fma(g.wc, vc, g.w[DIM - 1] * (vp + vm));
+        if (DIM >= 2) D = fma(g.w[0], xs, D);
+        if (DIM == 3) D = fma(g.w[1], ys, D);
+        const Dgate d = hh_expeuler_ref(vc, z0[k], z1[k], z2[k], a.eta);
+        const double y0 = z0[k] + d.d0, y1 = z1[k] + d.d1, y2 = z2[k] + d.d2;
+        const double fs = -current_fast(vc, y0, y1, y2) * g.inv_Cm;
+        if (!(finite_hi(D + fs) && finite_hi(y0) && finite_hi(y1) && finite_hi(y2)))
+          inner_bad = true;
+        else
+          outer_bad = true;
+      }
+      any = true;
+      glo = o.o1 < glo ? o.o1 : glo;
+      ghi = ghi < o.o1 ? o.o1 : ghi;
+      glo = o.o2 < glo ? o.o2 : glo;
+      ghi = ghi < o.o2 ? o.o2 : ghi;
+      glo = o.o3 < glo ? o.o3 : glo;
+      ghi = ghi < o.o3 ? o.o3 : ghi;
+    }
+    if (inner_bad) atomicMin(a.event, cb + 1ull);
+    else if (outer_bad) atomicMin(a.event, cb + 2ull);
+    if (guard) atomicMin(a.event, cb + 3ull);
+    {  // block gate range of this step -> its slot
+      unsigned long long lo = any ? ord_of(glo) : ~0ull, hi = any ? ord_of(ghi) : 0ull;
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      if ((t & 31) == 0) {
+        rlo[t >> 5] = lo;
+        rhi[t >> 5] = hi;
+      }
+      __syncthreads();
+      if (t == 0) {
+        for (int w = 1; w < kResNT / 32; ++w) {
+          lo = min(lo, rlo[w]);
+          hi = max(hi, rhi[w]);
+        }
+        if (lo != ~0ull) atomicMin(ra.slots + 2 * r, lo);
+        if (hi != 0ull) atomicMax(ra.slots + 2 * r + 1, hi);
+      }
+    }
+    grid.sync();  // V of step r and the step's abort ordinal are published
+    if (t == 0) ev_sh = *(volatile const unsigned long long*)a.event;
+    __syncthreads();
+    const unsigned long long ev = ev_sh;
+    if (ev != kNoEvent) {  // this step raised an event (earlier ones did not)
+      if (ev - cb == 3ull) {  // norm guard: the step's result is the state
+        fin = (int)((r + 1) & 1);
+        keep_new = true;
+      } else {                // NumericalAbort: the pre-step state
+        fin = (int)(r & 1);
+      }
+      break;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      z0[k] = n0v[k];
+      z1[k] = n1v[k];
+      z2[k] = n2v[k];
+    }
+    __syncthreads();  // ev_sh is rewritten next step
+  }
+  if (r == ra.nsteps) fin = (int)(r & 1);
+  const double* Vf = ra.vbuf + fin * nn;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    if (idx[k] >= b1) continue;
+    const long long i = idx[k];
+    ra.y_out[i] = __ldcg(Vf + i);
+    ra.y_out[nn + i] = keep_new ? n0v[k] : z0[k];
+    ra.y_out[2 * nn + i] = keep_new ? n1v[k] : z1[k];
+    ra.y_out[3 * nn + i] = keep_new ? n2v[k] : z2[k];
+  }
+}
+
+template <int DIM, int R>
+static int resident_blocks() {
+  static int nb = -1;
+  if (nb < 0) {
+    int per = 0, dev = 0, nsm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_resident<DIM, R>, kResNT, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    nb = per * nsm;
+  }
+  return nb;
+}
+
+template <int DIM, int R>
+static cudaError_t launch_resident_t(const Geom& g, const ResidentArgs& a, cudaStream_t st) {
+  const int nb = resident_blocks<DIM, R>();
+  // fewest blocks that keep R nodes per thread, at most one wave
+  long long want = (g.nn + (long long)kResNT * R - 1) / ((long long)kResNT * R);
+  if (want > nb) return cudaErrorInvalidValue;
+  // spread over every SM when the grid allows (shorter per-step chains)
+  if (want < nb) want = std::min<long long>(nb, (g.nn + kResNT - 1) / kResNT);
+  Geom gg = g;
+  ResidentArgs aa = a;
+  void* args[] = {&gg, &aa};
+  return cudaLaunchCooperativeKernel((const void*)k_resident<DIM, R>, dim3((unsigned)want),
+                                     dim3(kResNT), args, 0, st);
+}
+
+}  // namespace
+
+long long resident_capacity(int dim) {
+  if (dim == 3) return (long long)resident_blocks<3, 4>() * kResNT * 4;
+  if (dim == 2) return (long long)resident_blocks<2, 4>() * kResNT * 4;
+  return 0;
+}
+
+cudaError_t launch_resident(const Geom& g, const ResidentArgs& a, cudaStream_t st) {
+  // R nodes per thread: the smallest that fits one co-resident wave
+  if (g.dim == 3) {
+    if (g.nn <= (long long)resident_blocks<3, 1>() * kResNT) return launch_resident_t<3, 1>(g, a, st);
+    if (g.nn <= (long long)resident_blocks<3, 2>() * kResNT * 2) return launch_resident_t<3, 2>(g, a, st);
+    return launch_resident_t<3, 4>(g, a, st);
+  }
+  if (g.dim == 2) {
+    if (g.nn <= (long long)resident_blocks<2, 1>() * kResNT) return launch_resident_t<2, 1>(g, a, st);
+    if (g.nn <= (long long)resident_blocks<2, 2>() * kResNT * 2) return launch_resident_t<2, 2>(g, a, st);
+    return launch_resident_t<2, 4>(g, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+namespace {
 
 template <int DIM>
 constexpr size_t tma_vin_smem_bytes() {
