@@ -33,7 +33,7 @@ for name in args.names:
                  "node_steps_per_s": w.n_nodes * args.steps / (tot * 1e-3),
                  "ms_per_step": tot / args.steps, "step_frac_hbm": rf["step_frac"],
                  "dominant_kernel": rf["kernel"], "dominant_frac": rf["frac"],
-                 "run_node_steps_per_s": m["run"]["value"], "run_ms_per_step": m["run"]["ms_per_step"],
+                 "run": m["run"],
                  "note": w.note})
     m["op"].close()
     print(json.dumps(rows[-1]), file=sys.stderr, flush=True)
