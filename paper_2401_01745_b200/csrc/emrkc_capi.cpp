@@ -1563,7 +1563,12 @@ int run_resident(emrkc_handle* h, int64_t step0, int64_t nsteps, int* out_idx) {
   ra.nsteps = nsteps;
   ra.stride = static_cast<unsigned long long>(pl.s) * (pl.m + 1) + 2;  // begin_step's
   ra.slots = h->d_slots;
-  CK(h, emrkc_k::launch_resident(h->geom, ra, h->stream));
+  const cudaError_t e = emrkc_k::launch_resident(h->geom, ra, h->stream);
+  if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorInvalidValue) {
+    cudaGetLastError();  // not co-resident here (e.g. a shared GPU): per-step launches
+    return -1;
+  }
+  CK(h, e);
   *out_idx = out;
   return EMRKC_OK;
 }
@@ -1656,6 +1661,7 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     CK(h, cudaEventRecord(h->ev0, h->stream));
   }
   std::vector<cudaEvent_t> tev;
+  int resident_out = 0;
   if (n == 1 && launch_ms) {
     // benchmark form: flush L2 before each step, one event pair per launch
     emrkc_handle* h = hs[0];
@@ -1707,12 +1713,12 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     if (scratch) cudaFree(scratch);
     if (scratch_rd) cudaFree(scratch_rd);
     if (res) res->device_ms = tot;  // overwritten below, restored after
-  } else if (n == 1 && !single_step && resident_ok(hs[0], nsteps)) {
+  } else if (n == 1 && !single_step && resident_ok(hs[0], nsteps) &&
+             (rc = run_resident(hs[0], step0, nsteps, &resident_out)) >= 0) {
+    if (rc) return rc;
     emrkc_handle* h = hs[0];
-    int out = 0;
-    if ((rc = run_resident(h, step0, nsteps, &out))) return rc;
-    for (int64_t r = 0; r < nsteps; ++r) in_idx[0][r] = out;  // rollback is in-kernel
-    h->cur = out;
+    for (int64_t r = 0; r < nsteps; ++r) in_idx[0][r] = resident_out;  // rollback is in-kernel
+    h->cur = resident_out;
   } else if (n == 1) {
     emrkc_handle* h = hs[0];
     for (int64_t r = 0; r < nsteps; ++r) {
