@@ -356,6 +356,15 @@ int emrkc_dist_lockstep_run(emrkc_handle* const* hs, int32_t n, int32_t replay,
                             double epsilon, int32_t variant, double rho_F,
                             double rho_S, emrkc_run_result* res);
 
+/* Testing aid for the cross-process (IPC) path with fewer GPUs than ranks:
+ * when a hook is set, emrkc_dist_run / emrkc_dist_replay synchronise the
+ * handle's stream after every stencil level and call hook(ctx) (e.g. a
+ * host barrier across the ranks) before the next level, so every
+ * device-side halo wait is already satisfied when its kernel starts and
+ * ranks sharing one GPU never spin on each other. NULL clears it. */
+typedef void (*emrkc_level_hook)(void* ctx);
+int emrkc_set_level_hook(emrkc_handle* h, emrkc_level_hook hook, void* ctx);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -170,6 +170,9 @@ def dptr(a: np.ndarray | None):
 
 
 # Every function the header declares: name -> (restype, argtypes).
+# emrkc_level_hook: void (*)(void* ctx)
+LEVEL_HOOK = C.CFUNCTYPE(None, C.c_void_p)
+
 PROTOTYPES = {
     "emrkc_version": (C.c_char_p, []),
     "emrkc_global_error": (C.c_char_p, []),
@@ -215,6 +218,7 @@ PROTOTYPES = {
     "emrkc_dist_replay": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
     "emrkc_dist_link_local": (C.c_int, [C.c_void_p, C.c_void_p]),
     "emrkc_dist_lockstep_run": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
+    "emrkc_set_level_hook": (C.c_int, [C.c_void_p, LEVEL_HOOK, C.c_void_p]),
 }
 
 _lib = None

@@ -302,6 +302,8 @@ struct emrkc_handle {
   } peer[2];
   unsigned long long recv[2] = {0, 0};  // arrivals expected so far per side
   double* ckpt = nullptr;               // dist_run input state, for replay
+  emrkc_level_hook level_hook = nullptr;  // testing aid (emrkc_set_level_hook)
+  void* level_ctx = nullptr;
   double* res_v = nullptr;              // resident runs: V ping-pong [2][nn]
   double* res_stim = nullptr;           // resident runs: stimulus rate per step
   int64_t res_stim_n = 0;
@@ -823,6 +825,10 @@ int enqueue_step(emrkc_handle* h, double t, long long step_in_run,
     for (int k = 1; k <= h->plan.m; ++k) {
       const int rc = launch_level(h, &c, j, k);
       if (rc) return rc;
+      if (h->level_hook) {  // lockstep across processes (testing aid)
+        CK(h, cudaStreamSynchronize(h->stream));
+        h->level_hook(h->level_ctx);
+      }
     }
   *out_idx = end_step(h, &c);
   return EMRKC_OK;
@@ -1651,6 +1657,10 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
       }
       CK(h, emrkc_k::launch_halo_prime(h->geom, hp, h->buf[h->cur], h->stream));
       dist_account(h, emrkc_k::halo_signals_prime(h->geom));
+      if (h->level_hook) {
+        CK(h, cudaStreamSynchronize(h->stream));
+        h->level_hook(h->level_ctx);
+      }
       CK(h, cudaEventRecord(h->ev1, h->stream));
       prev = h->ev1;
     }
@@ -2518,6 +2528,13 @@ int emrkc_dist_replay(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
   CK(h, cudaMemcpyAsync(h->buf[h->cur], h->ckpt, sizeof(double) * h->len,
                         cudaMemcpyDeviceToDevice, h->stream));
   return emrkc_dist_run(h, step0, nsteps, dt, epsilon, variant, rho_F, rho_S, res);
+}
+
+int emrkc_set_level_hook(emrkc_handle* h, emrkc_level_hook hook, void* ctx) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  h->level_hook = hook;
+  h->level_ctx = ctx;
+  return EMRKC_OK;
 }
 
 int emrkc_dist_link_local(emrkc_handle* lower, emrkc_handle* upper) {
