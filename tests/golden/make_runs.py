@@ -22,7 +22,8 @@ from paper_2401_01745_b200 import workloads  # noqa: E402
 # (workload, steps): config 5 at N = 100 runs into the reference's own
 # NumericalAbort at step 47 (HH at h = 0.1 mm, m = 2); N = 50 and config 2
 # run clean over their full T.
-RUNS = [("hh3d_sweep_100", 60), ("hh3d_sweep_50", 100), ("hh3d_128x128x128", 100)]
+RUNS = [("hh3d_sweep_100", 60), ("hh3d_sweep_50", 100), ("hh3d_128x128x128", 100),
+        ("hh3d_sweep_200", 60)]
 # The reference's own conditioning: the same run from y0 (1 + 1e-15 u),
 # u ~ U(-1, 1) seeded, diverges from the unperturbed run by "sensitivity"
 # (trapezoid rel-L2 per block, the reference's rel_l2_error).
