@@ -469,7 +469,7 @@ def b200_arm(args, w):
     line = {
         "metric": METRIC, "value": value, "unit": "node-steps/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded HH resting state + N(0, 0.1 mV) V noise)",
         "config": config_of(w, 1),
         "plan": {"s": m["s"], "m": m["m"], "rho_F": m["rF"], "rho_S": m["rS"],
