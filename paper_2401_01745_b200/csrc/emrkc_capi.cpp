@@ -1521,7 +1521,8 @@ bool resident_ok(const emrkc_handle* h, int64_t nsteps) {
     return !(e && *e == '0');
   }();
   const Plan& pl = h->plan;
-  return on && h->fast && !h->partitioned && nsteps >= 2 && pl.s == 1 && pl.m == 1 &&
+  return on && h->fast && !h->partitioned && nsteps >= 2 && nsteps <= 10000000 &&
+         pl.s == 1 && pl.m == 1 &&
          pl.method != kMethodMrkc && (h->geom.dim == 2 || h->geom.dim == 3) &&
          h->geom.nn <= emrkc_k::resident_capacity(h->geom.dim);
 }
@@ -1534,7 +1535,9 @@ int run_resident(emrkc_handle* h, int64_t step0, int64_t nsteps, int* out_idx) {
   int rc = ensure_buffers(h, std::max(2, h->nbuf));
   if (rc) return rc;
   const int in = h->cur, out = (in + 1) % h->nbuf;
-  if (!h->res_v) CK(h, cudaMalloc(&h->res_v, sizeof(double) * 2 * h->nn));
+  if (!h->res_v) CK(h, cudaMalloc(&h->res_v, sizeof(double) * (2 * h->nn + 2)));
+  unsigned* bar = reinterpret_cast<unsigned*>(h->res_v + 2 * h->nn);
+  CK(h, cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), h->stream));
   if (h->res_stim_n < nsteps) {
     if (h->res_stim) cudaFree(h->res_stim);
     h->res_stim = nullptr;
@@ -1569,6 +1572,7 @@ int run_resident(emrkc_handle* h, int64_t step0, int64_t nsteps, int* out_idx) {
   ra.nsteps = nsteps;
   ra.stride = static_cast<unsigned long long>(pl.s) * (pl.m + 1) + 2;  // begin_step's
   ra.slots = h->d_slots;
+  ra.bar = bar;
   const cudaError_t e = emrkc_k::launch_resident(h->geom, ra, h->stream);
   if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorInvalidValue) {
     cudaGetLastError();  // not co-resident here (e.g. a shared GPU): per-step launches

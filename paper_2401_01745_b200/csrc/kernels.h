@@ -150,7 +150,8 @@ struct ResidentArgs {
   const double* stim;            // stimulus rate per step [nsteps]
   long long nsteps;
   unsigned long long stride;     // abort-ordinal stride per step
-  unsigned long long* slots;     // per-step gate range [2 * nsteps]
+  unsigned long long* slots;     // gate range of the accepted steps -> slots[0..1]
+  unsigned* bar;                 // [2] grid-barrier arrival counters (zeroed by the host)
 };
 // Largest grid the resident kernel takes on this device (0: none).
 long long resident_capacity(int dim);

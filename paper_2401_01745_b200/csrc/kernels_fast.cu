@@ -165,6 +165,11 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 // Thread 0 spins until the ghost planes this block reads have arrived; the
 // caller's __syncthreads() publishes that to the block. The spin is bounded
 // (~10 s): a neighbour that never arrives (a rank died, or a caller drove
@@ -1404,15 +1409,16 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
 // thread owns R nodes for the whole run (gates in registers, old and new for
 // the abort rollback), V ping-pongs through vbuf (L2-resident, read with
 // ld.global.cg so no stale L1 line survives a step), and one grid barrier
-// per step publishes V and the step's abort ordinal. The run-loop semantics
-// are the per-step kernels' (P/src/simulate.cpp:176-229): a non-finite step
-// leaves the pre-step state, a norm-guard step keeps its result, later steps
-// do not run; per-step gate ranges go to the same slots.
+// per step (a monotonic arrival counter; cooperative launch guarantees
+// co-residency) publishes V and the step's abort ordinal. The run-loop
+// semantics are the per-step kernels' (P/src/simulate.cpp:176-229): a
+// non-finite step leaves the pre-step state, a norm-guard step keeps its
+// result, later steps do not run; the gate range over the accepted steps
+// goes to slot 0, which the host folds like the per-step slots.
 // ---------------------------------------------------------------------------
 constexpr int kResNT = 256;
 template <int DIM, int R>
 __global__ void __launch_bounds__(kResNT) k_resident(const Geom g, const ResidentArgs ra) {
-  namespace cgr = cooperative_groups;
   const FastArgs& a = ra.f;
   __shared__ double tab[256];
   __shared__ unsigned long long ev_sh;
@@ -1448,13 +1454,22 @@ __global__ void __launch_bounds__(kResNT) k_resident(const Geom g, const Residen
       ra.vbuf[i] = ra.y_in[i];
     }
   }
-  cgr::grid_group grid = cgr::this_grid();
-  grid.sync();
+  // vbuf[0] complete before any block reads a neighbour (arrival 0)
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();
+    atomicAdd(ra.bar + 1, 1u);
+    while (ld_acquire_gpu_u32(ra.bar + 1) < gridDim.x) {
+    }
+  }
+  __syncthreads();
   const long long sx = 1, sy = g.n0, sz = DIM == 3 ? g.plane : 0;
   // the slab axis (z in 3-D, y in 2-D) is the stencil's "vm/vp" direction
   const long long sv = DIM == 3 ? sz : sy;
   long long r = 0;
   int fin = 0;      // buffer holding the final V
+  double rglo = 2.0, rghi = -1.0;  // gate range over the accepted steps
+  bool rany = false;
   bool keep_new = false;
   double n0v[R], n1v[R], n2v[R];
   for (; r < ra.nsteps; ++r) {
@@ -1522,28 +1537,18 @@ __global__ void __launch_bounds__(kResNT) k_resident(const Geom g, const Residen
     if (inner_bad) atomicMin(a.event, cb + 1ull);
     else if (outer_bad) atomicMin(a.event, cb + 2ull);
     if (guard) atomicMin(a.event, cb + 3ull);
-    {  // block gate range of this step -> its slot
-      unsigned long long lo = any ? ord_of(glo) : ~0ull, hi = any ? ord_of(ghi) : 0ull;
-      for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    // grid barrier: a monotonic arrival counter (zeroed by the host); the
+    // abort word is read by the arriving thread once everyone is in, so
+    // the step's V and its abort ordinal are published together
+    __syncthreads();  // the block's V stores and abort atomics are done
+    if (t == 0) {
+      __threadfence();
+      atomicAdd(ra.bar, 1u);
+      const unsigned target = (unsigned)(r + 1) * gridDim.x;
+      while (ld_acquire_gpu_u32(ra.bar) < target) {
       }
-      if ((t & 31) == 0) {
-        rlo[t >> 5] = lo;
-        rhi[t >> 5] = hi;
-      }
-      __syncthreads();
-      if (t == 0) {
-        for (int w = 1; w < kResNT / 32; ++w) {
-          lo = min(lo, rlo[w]);
-          hi = max(hi, rhi[w]);
-        }
-        if (lo != ~0ull) atomicMin(ra.slots + 2 * r, lo);
-        if (hi != 0ull) atomicMax(ra.slots + 2 * r + 1, hi);
-      }
+      ev_sh = *(volatile const unsigned long long*)a.event;
     }
-    grid.sync();  // V of step r and the step's abort ordinal are published
-    if (t == 0) ev_sh = *(volatile const unsigned long long*)a.event;
     __syncthreads();
     const unsigned long long ev = ev_sh;
     if (ev != kNoEvent) {  // this step raised an event (earlier ones did not)
@@ -1561,7 +1566,32 @@ __global__ void __launch_bounds__(kResNT) k_resident(const Geom g, const Residen
       z1[k] = n1v[k];
       z2[k] = n2v[k];
     }
-    __syncthreads();  // ev_sh is rewritten next step
+    if (any) {  // an accepted step: into the run's gate range (simulate.cpp:228)
+      rglo = glo < rglo ? glo : rglo;
+      rghi = rghi < ghi ? ghi : rghi;
+      rany = true;
+    }
+  }
+  {  // the run's gate range over its accepted steps -> slot 0 (the host folds
+     // slots 0 .. accepted - 1; the others stay empty)
+    unsigned long long lo = rany ? ord_of(rglo) : ~0ull, hi = rany ? ord_of(rghi) : 0ull;
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((t & 31) == 0) {
+      rlo[t >> 5] = lo;
+      rhi[t >> 5] = hi;
+    }
+    __syncthreads();
+    if (t == 0) {
+      for (int w = 1; w < kResNT / 32; ++w) {
+        lo = min(lo, rlo[w]);
+        hi = max(hi, rhi[w]);
+      }
+      if (lo != ~0ull) atomicMin(ra.slots, lo);
+      if (hi != 0ull) atomicMax(ra.slots + 1, hi);
+    }
   }
   if (r == ra.nsteps) fin = (int)(r & 1);
   const double* Vf = ra.vbuf + fin * nn;
