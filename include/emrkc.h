@@ -356,6 +356,19 @@ int emrkc_dist_lockstep_run(emrkc_handle* const* hs, int32_t n, int32_t replay,
                             double epsilon, int32_t variant, double rho_F,
                             double rho_S, emrkc_run_result* res);
 
+/* Wide halo of the temporally blocked inner stages on slabs (north_star
+ * (4); no reference counterpart — the reference never partitions). With
+ * K = m - 1 inner stages fused into one pass (k_vin_tb, 2 <= K <= 4), a
+ * slab needs K planes of d_1 from each neighbour: the inner-stage-1 kernel
+ * stores its first / last K planes of d_1 straight into the neighbours' d_1
+ * ghosts (peer stores, double-buffered by outer stage), and the fused pass
+ * marches K planes into them. Only possible when every slab of the
+ * partition is at least K planes deep, so the caller states the smallest
+ * slab depth; every slab of a run must be given the same value
+ * (emrkc_group_create and emrkc_dist_lockstep_run set it themselves). 0
+ * (the default) keeps the per-stage inner kernels (one V plane per level). */
+int emrkc_set_slab_min_depth(emrkc_handle* h, int64_t min_planes);
+
 /* Testing aid for the cross-process (IPC) path with fewer GPUs than ranks:
  * when a hook is set, emrkc_dist_run / emrkc_dist_replay synchronise the
  * handle's stream after every stencil level and call hook(ctx) (e.g. a

@@ -218,6 +218,7 @@ PROTOTYPES = {
     "emrkc_dist_replay": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
     "emrkc_dist_link_local": (C.c_int, [C.c_void_p, C.c_void_p]),
     "emrkc_dist_lockstep_run": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
+    "emrkc_set_slab_min_depth": (C.c_int, [C.c_void_p, C.c_int64]),
     "emrkc_set_level_hook": (C.c_int, [C.c_void_p, LEVEL_HOOK, C.c_void_p]),
 }
 

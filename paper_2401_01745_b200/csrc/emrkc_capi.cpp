@@ -288,6 +288,11 @@ struct emrkc_handle {
   // ghost planes [side: 0 below, 1 above][slot], carved from one arena that
   // also holds the arrival counters of the cross-process protocol
   double* ghost[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  // 3-D slabs: d_1 ghosts of the wide halo [side][outer-stage parity],
+  // kTbMaxK planes each (k_vin_tb on slabs)
+  double* dghost[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int64_t min_depth = 0;  // smallest slab depth of the partition (0: unknown)
+  long long kstage = 0;   // wide-halo outer stages run (d_1 ghost parity)
   void* arena = nullptr;
   size_t arena_bytes = 0;
   unsigned long long* cnt = nullptr;         // [2]: arrivals into ghost[0] / ghost[1]
@@ -298,6 +303,7 @@ struct emrkc_handle {
     bool ipc = false;           // opened with cudaIpcOpenMemHandle
     void* arena = nullptr;
     double* ghost[2] = {nullptr, nullptr};  // their ghost[1-side][slot]
+    double* dghost[2] = {nullptr, nullptr}; // their dghost[1-side][parity]
     unsigned long long* cnt = nullptr;      // their cnt[1-side]
   } peer[2];
   unsigned long long recv[2] = {0, 0};  // arrivals expected so far per side
@@ -376,6 +382,15 @@ int set_err(emrkc_handle* h, int code, const char* fmt, ...) {
 int use_device(emrkc_handle* h) {
   CK(h, cudaSetDevice(h->device));
   return EMRKC_OK;
+}
+
+// Ghost arena of a partitioned handle (both ends of a link compute the same
+// layout): V ghost planes [side][slot] (4 planes), then for 3-D the d_1 ghosts
+// of the wide halo [side][parity][kTbMaxK planes], then the two arrival
+// counters.
+size_t arena_planes(int dim) { return 4 + (dim == 3 ? 4 * emrkc_k::kTbMaxK : 0); }
+double* dghost_at(double* base, size_t pl, int side, int par) {
+  return base + (4 + static_cast<size_t>(2 * side + par) * emrkc_k::kTbMaxK) * pl;
 }
 
 int ensure_buffers(emrkc_handle* h, int nb) {
@@ -587,7 +602,7 @@ int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out) {
 // 3-D map over one V-sized field (n0, n1, nzl) with box (bx, by, 1); key
 // distinguishes box shapes in the cache (>= 100).
 int tma_map_box3(emrkc_handle* h, const void* ptr, cuuint32_t bx, cuuint32_t by, int key,
-                 CUtensorMap* out) {
+                 CUtensorMap* out, int64_t nz = -1) {
   for (const auto& e : h->tmaps)
     if (e.ptr == ptr && e.kind == key) {
       *out = e.map;
@@ -595,7 +610,7 @@ int tma_map_box3(emrkc_handle* h, const void* ptr, cuuint32_t bx, cuuint32_t by,
     }
   const Geom& g = h->geom;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.n0), static_cast<cuuint64_t>(g.n1),
-                              static_cast<cuuint64_t>(g.nzl)};
+                              static_cast<cuuint64_t>(nz >= 0 ? nz : g.nzl)};
   const cuuint64_t strides[2] = {sizeof(double) * static_cast<cuuint64_t>(g.n0),
                                  sizeof(double) * static_cast<cuuint64_t>(g.plane)};
   const cuuint32_t box[3] = {bx, by, 1}, es[3] = {1, 1, 1};
@@ -613,11 +628,23 @@ int tma_map_box3(emrkc_handle* h, const void* ptr, cuuint32_t bx, cuuint32_t by,
   return EMRKC_OK;
 }
 
-// Temporally blocked inner stages (k_vin_tb) apply: 3-D whole-grid handle on
-// the TMA path with 2 <= m - 1 <= kTbMaxK (EMRKC_TB=0 disables).
+// Temporally blocked inner stages (k_vin_tb) apply: 3-D handle on the TMA
+// path with 2 <= K = m - 1 <= kTbMaxK (EMRKC_TB=0 disables). Slabs exchange
+// K planes of d_1 (the wide halo), so every slab of the partition must be at
+// least K planes deep (min_depth: emrkc_set_slab_min_depth, or the group).
 bool use_tb(const emrkc_handle* h, const Plan& pl) {
-  return h->tb && h->pipe == 3 && h->geom.dim == 3 && !h->partitioned && pl.m - 1 >= 2 &&
-         pl.m - 1 <= emrkc_k::kTbMaxK;
+  const int K = pl.m - 1;
+  if (!(h->tb && h->pipe == 3 && h->geom.dim == 3 && K >= 2 && K <= emrkc_k::kTbMaxK))
+    return false;
+  return !h->partitioned || h->min_depth >= K;
+}
+
+// The neighbours' d_1 ghosts this handle's inner-stage-1 kernel stores into
+// (side 0: the lower neighbour's upper ghost), parity par.
+double* nbr_dghost(const emrkc_handle* h, int side, int par) {
+  if (h->nbr[side]) return h->nbr[side]->dghost[1 - side][par];
+  if (h->peer[side].linked) return h->peer[side].dghost[par];
+  return nullptr;
 }
 
 int tma_ghosts(emrkc_handle* h, const Halo& hl, CUtensorMap* lo, CUtensorMap* hi) {
@@ -685,6 +712,10 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
   }
   if (h->fast) {
     const double cG = pl.mudt[j] / pl.eta;
+    // arrivals this level sends each neighbour (cross-process protocol)
+    long long signals = h->pipe && h->geom.dim >= 2 ? emrkc_k::halo_signals_pipe(h->geom)
+                                                     : emrkc_k::halo_signals_march(h->geom);
+    if (use_tb(h, pl) && k > 2) return EMRKC_OK;  // fused into level k == 2: no level
     if (k == 1) {
       emrkc_k::FastArgs f{};
       f.g1 = a.g1;
@@ -720,7 +751,17 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         if (!f.g2) std::memset(&tm.g2, 0, sizeof tm.g2);
         if (!rc) rc = tma_ghosts(h, hl, &tm.glo, &tm.ghi);
         if (rc) return rc;
-        CK(h, emrkc_k::launch_node_tma(h->geom, hl, f, tm, pl.m >= 2, h->stream));
+        Halo hn = hl;
+        if (h->partitioned && use_tb(h, pl)) {
+          // wide halo: K planes of d_1 into the neighbours' d_1 ghosts
+          const int par = static_cast<int>(h->kstage & 1);
+          hn.put_lo = hn.put_hi = nullptr;
+          hn.kput = pl.m - 1;
+          hn.kput_lo = hl.put_lo ? nbr_dghost(h, 0, par) : nullptr;
+          hn.kput_hi = hl.put_hi ? nbr_dghost(h, 1, par) : nullptr;
+          signals = emrkc_k::halo_signals_pipe(h->geom) * hn.kput;
+        }
+        CK(h, emrkc_k::launch_node_tma(h->geom, hn, f, tm, pl.m >= 2, h->stream));
       } else if (h->pipe == 2)
         CK(h, emrkc_k::launch_node_persist(h->geom, hl, f, pl.m >= 2, h->stream));
       else if (h->pipe)
@@ -747,12 +788,26 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         const int K = pl.m - 1;
         emrkc_k::TmaTb tm;
         std::memset(&tm, 0, sizeof tm);
-        int rc = tma_map_box3(h, h->u[3], emrkc_k::kTbTX + 2 * emrkc_k::kTbHX,
-                              emrkc_k::kTbTY + 2 * K, 100 + K, &tm.d1);
+        const cuuint32_t bx = emrkc_k::kTbTX + 2 * emrkc_k::kTbHX, by = emrkc_k::kTbTY + 2 * K;
+        int rc = tma_map_box3(h, h->u[3], bx, by, 100 + K, &tm.d1);
         if (!rc) rc = tma_map_box3(h, a.g1, emrkc_k::kTbTX, emrkc_k::kTbTY, 99, &tm.g1v);
         if (!rc && a.g2) rc = tma_map_box3(h, a.g2, emrkc_k::kTbTX, emrkc_k::kTbTY, 99, &tm.g2v);
+        // slabs: this handle's d_1 ghosts (K planes per face with a neighbour)
+        Halo ht = hl;
+        ht.lo = ht.hi = nullptr;
+        const int par = static_cast<int>(h->kstage & 1);
+        if (hl.lo) {
+          ht.lo = h->dghost[0][par];
+          if (!rc) rc = tma_map_box3(h, ht.lo, bx, by, 200 + K, &tm.d1lo, K);
+        }
+        if (hl.hi) {
+          ht.hi = h->dghost[1][par];
+          if (!rc) rc = tma_map_box3(h, ht.hi, bx, by, 200 + K, &tm.d1hi, K);
+        }
         if (rc) return rc;
-        CK(h, emrkc_k::launch_vin_tb(h->geom, f, tm, h->stream));
+        CK(h, emrkc_k::launch_vin_tb(h->geom, ht, f, tm, h->stream));
+        ++h->kstage;
+        signals = emrkc_k::halo_signals_tb(h->geom);
       }
     } else {
       emrkc_k::FastInnerArgs f{};
@@ -797,11 +852,7 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       else
         CK(h, emrkc_k::launch_vin_fast(h->geom, hl, f, h->stream));
     }
-    if (dist_linked(h)) {
-      const bool pipe_family = h->pipe && h->geom.dim >= 2;
-      dist_account(h, pipe_family ? emrkc_k::halo_signals_pipe(h->geom)
-                                  : emrkc_k::halo_signals_march(h->geom));
-    }
+    if (dist_linked(h)) dist_account(h, signals);
   } else if (pl.m == 1) {
     CK(h, emrkc_k::launch_stage_m1(h->geom, hl, a, 0, h->stream));
   } else if (k == 1) {
@@ -884,13 +935,17 @@ int init_handle(emrkc_handle* h) {
   CK(h, cudaEventCreate(&h->ev1));
   if (h->partitioned) {
     const size_t pl = static_cast<size_t>(h->geom.plane);
-    h->arena_bytes = sizeof(double) * 4 * pl + 256;
+    const size_t np = arena_planes(h->geom.dim);
+    h->arena_bytes = sizeof(double) * np * pl + 256;
     CK(h, cudaMalloc(&h->arena, h->arena_bytes));
     CK(h, cudaMemset(h->arena, 0, h->arena_bytes));
     double* base = static_cast<double*>(h->arena);
     for (int s = 0; s < 2; ++s)
-      for (int k = 0; k < 2; ++k) h->ghost[s][k] = base + (2 * s + k) * pl;
-    h->cnt = reinterpret_cast<unsigned long long*>(base + 4 * pl);
+      for (int k = 0; k < 2; ++k) {
+        h->ghost[s][k] = base + (2 * s + k) * pl;
+        if (h->geom.dim == 3) h->dghost[s][k] = dghost_at(base, pl, s, k);
+      }
+    h->cnt = reinterpret_cast<unsigned long long*>(base + np * pl);
   }
   const char* f = std::getenv("EMRKC_FAST");
   h->fast = f ? std::atoi(f) : 1;
@@ -2394,10 +2449,14 @@ int emrkc_group_create(emrkc_handle* const* hs, int32_t n, emrkc_group** out) {
   }
   if (z != p0.n[p0.dim - 1])
     return set_global(EMRKC_EINVAL, "group: slabs do not cover the grid");
+  int64_t min_depth = z;
+  for (int r = 0; r < n; ++r) min_depth = std::min(min_depth, hs[r]->z_end - hs[r]->z_begin);
   for (int r = 0; r < n; ++r) {
     hs[r]->nbr[0] = r > 0 ? hs[r - 1] : nullptr;
     hs[r]->nbr[1] = r + 1 < n ? hs[r + 1] : nullptr;
     hs[r]->level = 0;
+    hs[r]->kstage = 0;
+    hs[r]->min_depth = min_depth;
     // peer access for stores into neighbours on other devices
     for (int o = 0; o < n; ++o) {
       if (hs[o]->device == hs[r]->device) continue;
@@ -2466,7 +2525,10 @@ void link_peer(emrkc_handle* h, int s, void* arena, bool ipc) {
   h->peer[s].arena = arena;
   h->peer[s].ghost[0] = base + (2 * o + 0) * pl;
   h->peer[s].ghost[1] = base + (2 * o + 1) * pl;
-  h->peer[s].cnt = reinterpret_cast<unsigned long long*>(base + 4 * pl) + o;
+  for (int par = 0; par < 2; ++par)
+    h->peer[s].dghost[par] = h->geom.dim == 3 ? dghost_at(base, pl, o, par) : nullptr;
+  h->peer[s].cnt =
+      reinterpret_cast<unsigned long long*>(base + arena_planes(h->geom.dim) * pl) + o;
 }
 }  // namespace
 
@@ -2534,6 +2596,16 @@ int emrkc_dist_replay(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt,
   return emrkc_dist_run(h, step0, nsteps, dt, epsilon, variant, rho_F, rho_S, res);
 }
 
+int emrkc_set_slab_min_depth(emrkc_handle* h, int64_t min_planes) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (!h->partitioned) return set_err(h, EMRKC_EINVAL, "set_slab_min_depth: not a slab");
+  if (min_planes < 0 || min_planes > h->z_end - h->z_begin)
+    return set_err(h, EMRKC_EINVAL, "set_slab_min_depth: %lld exceeds this slab's depth",
+                   (long long)min_planes);
+  h->min_depth = min_planes;
+  return EMRKC_OK;
+}
+
 int emrkc_set_level_hook(emrkc_handle* h, emrkc_level_hook hook, void* ctx) {
   if (!h) return set_global(EMRKC_EINVAL, "null handle");
   h->level_hook = hook;
@@ -2571,7 +2643,12 @@ int emrkc_dist_lockstep_run(emrkc_handle* const* hs, int32_t n, int32_t replay,
   if (variant_method(variant, &method))
     return set_global(EMRKC_EINVAL, "emrkc_run: unknown variant %d", variant);
   std::vector<emrkc_handle*> v(hs, hs + n);
-  for (auto* h : v) h->method = method;
+  int64_t min_depth = v[0]->z_end - v[0]->z_begin;
+  for (auto* h : v) min_depth = std::min(min_depth, h->z_end - h->z_begin);
+  for (auto* h : v) {
+    h->method = method;
+    h->min_depth = min_depth;
+  }
   for (auto* h : v) {
     if (!dist_linked(h)) return set_global(EMRKC_ESTATE, "dist_lockstep_run: handles not linked");
     if (replay) {

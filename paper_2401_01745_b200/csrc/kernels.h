@@ -42,6 +42,17 @@ struct Halo {
   const unsigned long long* wait_hi;
   unsigned long long expect_lo, expect_hi;
   unsigned long long* timeout_flag;  // the abort word (code 0 = wait timed out)
+  // Wide d_1 halo of the temporally blocked inner stages on slabs (north_star
+  // (4): K-plane halos when K stages are blocked). kput > 0: the inner-stage-1
+  // node kernel stores its first / last kput planes of d_1 into the
+  // neighbours' d_1 ghosts instead of one plane into put_lo / put_hi:
+  // plane z < kput to kput_lo + z * plane (the lower neighbour's upper ghost),
+  // plane z >= nzl - kput to kput_hi + (z - nzl + kput) * plane. A block
+  // signals one arrival per plane it stored, so a side expects
+  // kput * halo_signals_pipe arrivals whatever the sender's z-chunking.
+  double* kput_lo;
+  double* kput_hi;
+  int kput;
 };
 
 // One outer stage of emRKC: pointers and coefficients.
@@ -196,8 +207,16 @@ struct TmaTb {
   CUtensorMap d1;      // d_1, box (kTbTX + 2 kTbHX, kTbTY + 2K, 1)
   CUtensorMap g1v;     // V of g_{j-1}, box (kTbTX, kTbTY, 1)
   CUtensorMap g2v;     // V of g_{j-2}
+  CUtensorMap d1lo;    // slabs: K ghost planes of d_1 below (global z0 - K ..), box as d1
+  CUtensorMap d1hi;    // K ghost planes above (global z1 ..)
 };
-cudaError_t launch_vin_tb(const Geom& g, const TbArgs& a, const TmaTb& tm, cudaStream_t st);
+// Slabs (h.lo / h.hi non-null: the d_1 ghosts of that face, K planes each):
+// the march extends K planes into the ghosts instead of mirroring, and the
+// final stage stores its boundary V planes into put_lo / put_hi (one arrival
+// per block and side, halo_signals_tb).
+cudaError_t launch_vin_tb(const Geom& g, const Halo& h, const TbArgs& a, const TmaTb& tm,
+                          cudaStream_t st);
+long long halo_signals_tb(const Geom& g);
 
 // TMA descriptors of one k_node_tma launch (host-encoded, passed as a
 // __grid_constant__ parameter). Boxes: V tile + 1-cell halo, gate fields,

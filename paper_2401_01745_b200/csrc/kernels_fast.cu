@@ -205,6 +205,41 @@ __device__ __forceinline__ void halo_signal(const Halo& h, bool put_lo, bool put
   }
 }
 
+// Weighted form (wide d_1 halo): wlo / whi arrivals, one per plane stored.
+__device__ __forceinline__ void halo_signal_w(const Halo& h, int wlo, int whi) {
+  if ((wlo > 0 && h.sig_lo) || (whi > 0 && h.sig_hi)) {
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      __threadfence_system();
+      if (wlo > 0 && h.sig_lo) atomicAdd_system(h.sig_lo, (unsigned long long)wlo);
+      if (whi > 0 && h.sig_hi) atomicAdd_system(h.sig_hi, (unsigned long long)whi);
+    }
+  }
+}
+
+// Boundary planes a z-chunk [zb, ze) of a node kernel stores into the
+// neighbours: planes z < zl go to plo + z * plane, planes z >= zh to
+// phi + (z - zh) * plane. One plane (put_lo / put_hi) or, with h.kput, the
+// K planes of the wide d_1 halo.
+struct PutPlan {
+  double* plo;
+  double* phi;
+  int zl, zh;
+};
+__device__ __forceinline__ PutPlan put_plan(const Halo& h, int nzl) {
+  PutPlan pp;
+  const int w = h.kput > 0 ? h.kput : 1;
+  pp.plo = h.kput > 0 ? h.kput_lo : h.put_lo;
+  pp.phi = h.kput > 0 ? h.kput_hi : h.put_hi;
+  pp.zl = pp.plo ? w : 0;
+  pp.zh = pp.phi ? nzl - w : 0x7fffffff;
+  return pp;
+}
+// Arrivals of the chunk [zb, ze) per side (planes it stores).
+__device__ __forceinline__ void put_signal(const Halo& h, const PutPlan& pp, int zb, int ze) {
+  halo_signal_w(h, max(0, min(ze, pp.zl) - zb), max(0, ze - max(zb, pp.zh)));
+}
+
 __device__ __forceinline__ bool prologue(const unsigned long long* ev, double* tab) {
   __shared__ int skip;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
@@ -1122,9 +1157,6 @@ constexpr int kTmaLA = EMRKC_TMA_LA;
 #ifndef EMRKC_ISSUE1
 #define EMRKC_ISSUE1 1
 #endif
-#ifndef EMRKC_HALOPUT
-#define EMRKC_HALOPUT 1
-#endif
 static_assert(kTmaLA >= 1 && kTmaLA + 2 <= kRV && kTmaLA <= kRG, "TMA lookahead");
 
 template <int DIM>
@@ -1135,10 +1167,26 @@ struct TmaTile {
   static constexpr int VS = (VT + 15) & ~15;      // V stage stride (128-byte aligned)
 };
 
+// k_node_tma gate ring and barrier period: with FIRST (no g_{j-2} fields)
+// the gate ring is deep enough for one __syncthreads per EMRKC_SYNCP planes
+// (a slot is rewritten kRGn(FIRST) - kTmaLA planes after its last read).
+#ifndef EMRKC_EVWARP1
+#define EMRKC_EVWARP1 1
+#endif
+#ifndef EMRKC_SYNCP
+#define EMRKC_SYNCP 1
+#endif
+template <int FIRST>
+__host__ __device__ constexpr int kRGn() { return FIRST && EMRKC_SYNCP > 1 ? 8 : kRG; }
+template <int FIRST>
+__host__ __device__ constexpr int kSyncP() { return FIRST ? EMRKC_SYNCP : 1; }
+static_assert(EMRKC_SYNCP == 1 || (EMRKC_SYNCP == 2 && kTmaLA + 4 <= kRV),
+              "k_node_tma barrier period");
+
 template <int DIM, int FIRST>
 constexpr size_t tma_node_smem_bytes() {
   using T = PipeTile<DIM>;
-  return sizeof(double) * (kRV * TmaTile<DIM>::VS + kRG * 3 * T::NT +
+  return sizeof(double) * (kRV * TmaTile<DIM>::VS + kRGn<FIRST>() * 3 * T::NT +
                            (FIRST ? 0 : kRG * 4 * T::NT)) + 128;
 }
 
@@ -1175,7 +1223,8 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   // 128-byte aligned stage base (pointer arithmetic keeps the shared space)
   double* vst = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;  // [kRV][VS]
   double* gst = vst + kRV * VS;                     // [kRG][3][NT]
-  double* g2s = gst + kRG * 3 * T::NT;              // [kRG][4][NT]
+  constexpr int RG = kRGn<FIRST>();
+  double* g2s = gst + RG * 3 * T::NT;               // [kRG][4][NT]
   __shared__ double tab[256];
   __shared__ __align__(8) unsigned long long bars[kRV];
   __shared__ int skip;
@@ -1209,7 +1258,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   auto issue_comp = [&](int zz) {  // plane zz in [zb, ze)
     const int q = zz - zb + 1;
     const unsigned bar = b0 + 8u * (q & (kRV - 1));
-    const unsigned sg = (unsigned)((zz - zb) & (kRG - 1));
+    const unsigned sg = (unsigned)((zz - zb) & (RG - 1));
     if (role == 0) {
       mbar_expect_tx(bar, vbytes + cbytes);
       const unsigned vd = v0 + 8u * VS * (q & (kRV - 1));
@@ -1255,13 +1304,13 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
       }
     }
   }
-  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  if (t == (EMRKC_EVWARP1 ? 32 : 0)) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
   __syncthreads();
   const bool skipped = skip != 0;
   if (skipped) {  // aborted earlier: drain the prologue copies, release the neighbours
     const int np = 1 + min(kTmaLA, ze - zb) + (ze - zb < kTmaLA ? 1 : 0);
     for (int q = 0; q < np; ++q) mbar_wait(b0 + 8u * q, 0);
-    halo_signal(h, zb == 0, ze >= g.nzl);
+    put_signal(h, put_plan(h, g.nzl), zb, ze);
     return;
   }
   (void)nq;
@@ -1284,12 +1333,9 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     mbar_wait(b0, 0);       // plane zb - 1
     mbar_wait(b0 + 8u, 0);  // plane zb
   }
-#if EMRKC_HALOPUT
-  // halo puts hoisted: the plane (if any) whose V this thread stores into a
-  // neighbour's ghost slot (-1: none)
-  const int zpl = (h.put_lo != nullptr) ? 0 : -1;
-  const int zph = (h.put_hi != nullptr) ? g.nzl - 1 : -1;
-#endif
+  // halo puts hoisted: planes z < pp.zl / z >= pp.zh of this column go to
+  // the neighbours' ghosts (one plane, or K planes of d_1 for the wide halo)
+  const PutPlan pp = put_plan(h, g.nzl);
   for (int z = zb; z < ze && !skipped; ++z) {
     const int p = z - zb + 1;
     if (EMRKC_ISSUE1 ? role == 0 : role >= 0) {
@@ -1304,13 +1350,13 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     double xs = 0.0, ys = 0.0;
     if (DIM >= 2) xs = V0[cxm] + V0[cxp];
     if (DIM == 3) ys = V0[cym] + V0[cyp];
-    const double* G0 = gst + ((z - zb) & (kRG - 1)) * 3 * T::NT + t;
+    const double* G0 = gst + ((z - zb) & (RG - 1)) * 3 * T::NT + t;
     const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
     const bool fast = fabs(vc) <= a.vfast;
     if (!fast) slow_mask |= 1u << (z - zb);
     NodeOut r = node_update_s<DIM, FIRST, ION, 0>(
         g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, 0.0,
-        g2s + ((z - zb) & (kRG - 1)) * 4 * T::NT + t, T::NT);
+        g2s + ((z - zb) & (RG - 1)) * 4 * T::NT + t, T::NT);
     if (z >= zs0 && z <= zs1) {
       if (ION) r.o0 = fma(a.mue1, a.stim, r.o0);
       else r.o0 = fma(a.cV, a.stim, r.o0);
@@ -1326,13 +1372,8 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
-#if EMRKC_HALOPUT
-      if (z == zpl) h.put_lo[ip] = r.o0;
-      if (z == zph) h.put_hi[ip] = r.o0;
-#else
-      if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
-      if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
-#endif
+      if (z < pp.zl) pp.plo[ip + plane * z] = r.o0;
+      if (z >= pp.zh) pp.phi[ip + plane * (z - pp.zh)] = r.o0;
       if (a.last) {  // std::min / std::max per value (NaN skipped), select form
         glo = r.o1 < glo ? r.o1 : glo;
         ghi = ghi < r.o1 ? r.o1 : ghi;
@@ -1344,7 +1385,9 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     }
     po += plane;
     if (ION) pu += plane;
-    __syncthreads();  // stage (p - 5) may be refilled next iteration
+    // stage (p - 5) may be refilled next iteration; with a period of 2 the
+    // deeper gate ring keeps every refill behind a barrier
+    if (kSyncP<FIRST>() == 1 || ((z - zb) & 1)) __syncthreads();
   }
   if (!skipped && valid && slow_mask) {
     const Nbr<DIM> o = nbr_of<DIM>(g, Col<DIM>{cx, cy, ip, zb, ze, true});
@@ -1375,15 +1418,15 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
-      if (z == 0 && h.put_lo) h.put_lo[ip] = r.o0;
-      if (z == g.nzl - 1 && h.put_hi) h.put_hi[ip] = r.o0;
+      if (z < pp.zl) pp.plo[ip + plane * z] = r.o0;
+      if (z >= pp.zh) pp.phi[ip + plane * (z - pp.zh)] = r.o0;
       if (a.last) {
         glo = fmin(glo, fmin(r.o1, fmin(r.o2, r.o3)));
         ghi = fmax(ghi, fmax(r.o1, fmax(r.o2, r.o3)));
       }
     }
   }
-  halo_signal(h, zb == 0, ze >= g.nzl);
+  put_signal(h, pp, zb, ze);
   if (skipped) return;
   if (bad && !a.exex) {  // EXEX-RL never throws NumericalAbort
     Col<DIM> c;
@@ -1748,7 +1791,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
       }
     }
   }
-  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  if (t == (EMRKC_EVWARP1 ? 32 : 0)) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
   __syncthreads();
   const bool skipped = skip != 0;
   if (skipped) {  // aborted earlier: drain the prologue copies, release the neighbours
@@ -1866,13 +1909,10 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
-__device__ __forceinline__ int mirror_idx(int i, int n) {
-  return i < 0 ? 1 : (i >= n ? n - 2 : i);
-}
 
 template <int K, int FIRST>
 __global__ void __launch_bounds__(TbTile<K>::NT, 2)
-    k_vin_tb(const Geom g, const TbArgs a, const __grid_constant__ TmaTb tm) {
+    k_vin_tb(const Geom g, const Halo h, const TbArgs a, const __grid_constant__ TmaTb tm) {
   using T = TbTile<K>;
   constexpr int M = K + 1;  // m
   extern __shared__ __align__(128) double smem_tma[];
@@ -1896,7 +1936,10 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
   __syncthreads();
   pdl_wait();
   if (t < 3 * (M + 1)) cf[t / (M + 1)][t % (M + 1)] = a.coef[t];
-  const int lo1 = max(0, zb - K), hi1 = min(nz, ze + K);  // d_1 planes
+  // slab faces with a neighbour (h.lo / h.hi: its K d_1 ghost planes) march
+  // into the ghosts; global boundaries mirror (P/src/monodomain.cpp:85-86)
+  const bool gl = h.lo != nullptr, gh = h.hi != nullptr;
+  const int lo1 = max(gl ? -K : 0, zb - K), hi1 = min(gh ? nz + K : nz, ze + K);  // d_1 planes
   const int tlast = ze - 1 + K;                           // last step
   const unsigned b0 = smem_u32(bars);
   const unsigned dbase = smem_u32(sm), cbase = smem_u32(sm + T::off_centre());
@@ -1909,7 +1952,12 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
     const unsigned bytes = (hasd ? 8u * T::DX * T::DY : 0u) +
                            (hasc ? 8u * T::CS * (FIRST ? 1 : 2) : 0u);
     mbar_expect_tx(bar, bytes);
-    if (hasd) tma_load_3d(dbase + 8u * T::DS * (i & 7), &tm.d1, bar, x0 - kTbHX, y0 - K, s);
+    if (hasd) {
+      const unsigned dd = dbase + 8u * T::DS * (i & 7);
+      if (s < 0) tma_load_3d(dd, &tm.d1lo, bar, x0 - kTbHX, y0 - K, s + K);
+      else if (s >= nz) tma_load_3d(dd, &tm.d1hi, bar, x0 - kTbHX, y0 - K, s - nz);
+      else tma_load_3d(dd, &tm.d1, bar, x0 - kTbHX, y0 - K, s);
+    }
     if (hasc) {
       const unsigned cd = cbase + 8u * 2 * T::CS * (s & 3);
       tma_load_3d(cd, &tm.g1v, bar, x0, y0, q);
@@ -1917,6 +1965,10 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
     }
   };
   if (t == 0) {
+    if (lo1 < 0 || hi1 > nz) {
+      halo_wait(h, lo1 < 0, hi1 > nz);
+      fence_proxy_async();  // peer-stored ghosts before the async-proxy reads
+    }
     for (int s = lo1; s <= min(tlast, lo1 + kTmaLA - 1); ++s) issue(s);
     skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
   }
@@ -1924,8 +1976,11 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
   const int nlaunched = min(tlast, lo1 + kTmaLA - 1) - lo1 + 1;
   if (skip) {
     for (int i = 0; i < nlaunched; ++i) mbar_wait(b0 + 8u * i, 0);
+    halo_signal(h, zb == 0, ze >= nz);  // release the neighbours
     return;
   }
+  // ring slot of a stage plane (q >= -K - 1 on slabs)
+  auto r3 = [](int q) { return (q + 6) % 3; };
   const double inv_mue1 = a.inv_mue1;
   const long long plane = g.plane;
   unsigned badk = 0u;  // bit k: stage k produced a non-finite interior value
@@ -1981,9 +2036,11 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
         for (int k2 = 2; k2 < k; ++k2) b += (T::PS(k2) + NT - 1) / NT;
         return b;
       }();
-      const bool active = q >= max(0, zb - hk) && q < min(nz, ze + hk);
+      const bool active = q >= (gl ? zb - hk : max(0, zb - hk)) &&
+                          q < (gh ? ze + hk : min(nz, ze + hk));
       if (active) {
-        const int qm = mirror_idx(q - 1, nz), qp = mirror_idx(q + 1, nz);
+        const int qm = (q < 1 && !gl) ? 1 : q - 1;
+        const int qp = (q + 1 >= nz && !gh) ? nz - 2 : q + 1;
         const double mueta = cf[0][k], nu = cf[1][k], kappa = cf[2][k];
         const double* Sc;
         const double* Sm;
@@ -1994,12 +2051,12 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
           Sp = sm + ((qp - lo1) & 7) * T::DS;
         } else {
           const double* S = sm + T::off_stage(k - 1);
-          Sc = S + (q % 3) * T::PS(k - 1);
-          Sm = S + (qm % 3) * T::PS(k - 1);
-          Sp = S + (qp % 3) * T::PS(k - 1);
+          Sc = S + r3(q) * T::PS(k - 1);
+          Sm = S + r3(qm) * T::PS(k - 1);
+          Sp = S + r3(qp) * T::PS(k - 1);
         }
         const double* D1 = sm + ((q - lo1) & 7) * T::DS;
-        const double* S2 = k >= 4 ? sm + T::off_stage(k - 2) + (q % 3) * T::PS(k - 2) : nullptr;
+        const double* S2 = k >= 4 ? sm + T::off_stage(k - 2) + r3(q) * T::PS(k - 2) : nullptr;
         const bool own_plane = q >= zb && q < ze;
 #pragma unroll
         for (int ii = 0; ii < (T::PS(k) + NT - 1) / NT; ++ii) {
@@ -2019,7 +2076,7 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
           const double dk = fma(mueta, fma(d1c, inv_mue1, D), bs);
           if ((c_f[e] & 2u) && own_plane && !finite_hi(dk)) badk |= 1u << k;
           if (k < M) {
-            sm[T::off_stage(k) + (q % 3) * T::PS(k) + t + ii * NT] = dk;
+            sm[T::off_stage(k) + r3(q) * T::PS(k) + t + ii * NT] = dk;
           } else {
             // final stage: V of g_j (hk == 0: the cell indexes the tile)
             const int c = t + ii * NT;
@@ -2027,6 +2084,8 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
             const double bb = FIRST ? C0[c] : fma(a.onu, C0[c], a.okappa * C0[T::CS + c]);
             const double o0 = fma(a.cG, dk, bb);
             a.outv[(long long)c_out[e] + plane * q] = o0;
+            if (q == 0 && h.put_lo) h.put_lo[c_out[e]] = o0;
+            if (q == nz - 1 && h.put_hi) h.put_hi[c_out[e]] = o0;
             bad_out |= !finite_hi(o0);
             guard |= !(fabs(o0) <= 1e6);  // also a non-finite V
           }
@@ -2035,6 +2094,7 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
       __syncthreads();
     });
   }
+  halo_signal(h, zb == 0, ze >= nz);
   const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
   if (badk) atomicMin(a.event, base + (unsigned long long)(__ffs(badk) - 1));
   if (bad_out) atomicMin(a.event, base + a.m + 1);
@@ -2296,7 +2356,7 @@ static cudaError_t launch_node_tma_t(const Geom& g, const Halo& h, const FastArg
 }
 
 template <int K, int F>
-static cudaError_t launch_vin_tb_t(const Geom& g, const TbArgs& a, const TmaTb& tm,
+static cudaError_t launch_vin_tb_t(const Geom& g, const Halo& h, const TbArgs& a, const TmaTb& tm,
                                    cudaStream_t st) {
   constexpr size_t smem = tb_smem_bytes<K>();
   static bool attr = false;
@@ -2306,17 +2366,22 @@ static cudaError_t launch_vin_tb_t(const Geom& g, const TbArgs& a, const TmaTb& 
   }
   const int chunks = (g.nzl + a.zc - 1) / a.zc;
   const dim3 grd((g.n0 + kTbTX - 1) / kTbTX, (g.n1 + kTbTY - 1) / kTbTY, chunks);
-  return launch_k(k_vin_tb<K, F>, grd, dim3(TbTile<K>::NT), smem, st, g, a, tm);
+  return launch_k(k_vin_tb<K, F>, grd, dim3(TbTile<K>::NT), smem, st, g, h, a, tm);
 }
 
-cudaError_t launch_vin_tb(const Geom& g, const TbArgs& a, const TmaTb& tm, cudaStream_t st) {
+cudaError_t launch_vin_tb(const Geom& g, const Halo& h, const TbArgs& a, const TmaTb& tm,
+                          cudaStream_t st) {
   const bool first = a.j == 1;
   switch (a.m - 1) {
-    case 2: return first ? launch_vin_tb_t<2, 1>(g, a, tm, st) : launch_vin_tb_t<2, 0>(g, a, tm, st);
-    case 3: return first ? launch_vin_tb_t<3, 1>(g, a, tm, st) : launch_vin_tb_t<3, 0>(g, a, tm, st);
-    case 4: return first ? launch_vin_tb_t<4, 1>(g, a, tm, st) : launch_vin_tb_t<4, 0>(g, a, tm, st);
+    case 2: return first ? launch_vin_tb_t<2, 1>(g, h, a, tm, st) : launch_vin_tb_t<2, 0>(g, h, a, tm, st);
+    case 3: return first ? launch_vin_tb_t<3, 1>(g, h, a, tm, st) : launch_vin_tb_t<3, 0>(g, h, a, tm, st);
+    case 4: return first ? launch_vin_tb_t<4, 1>(g, h, a, tm, st) : launch_vin_tb_t<4, 0>(g, h, a, tm, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+long long halo_signals_tb(const Geom& g) {
+  return (long long)((g.n0 + kTbTX - 1) / kTbTX) * ((g.n1 + kTbTY - 1) / kTbTY);
 }
 
 cudaError_t launch_node_tma(const Geom& g, const Halo& h, const FastArgs& a, const TmaNode& tm,

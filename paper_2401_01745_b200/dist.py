@@ -37,6 +37,11 @@ def partition(problem: Problem, world: int, rank: int) -> Partition:
     return part
 
 
+def min_slab_depth(problem: Problem, world: int) -> int:
+    """Smallest slab (planes) of the world-rank partition."""
+    return min(int(p.z_end - p.z_begin) for p in (partition(problem, world, r) for r in range(world)))
+
+
 def slab_of(problem: Problem, part: Partition, y_global: np.ndarray) -> np.ndarray:
     """Local slab of a global reference-layout state."""
     nn = problem.n_nodes
@@ -116,6 +121,9 @@ class DistSlab:
             self.op.ipc_import(0, blobs[self.ctx.rank - 1])
         if self.ctx.rank + 1 < self.ctx.world:
             self.op.ipc_import(1, blobs[self.ctx.rank + 1])
+        # every rank derives the same partition, hence the same smallest slab
+        # depth: the wide d_1 halo is switched on (or off) consistently
+        self.op.set_slab_min_depth(min_slab_depth(self.problem, self.ctx.world))
 
     def set_global_state(self, y_global: np.ndarray):
         self.op.set_state(slab_of(self.problem, self.part, y_global))

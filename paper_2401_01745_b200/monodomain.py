@@ -278,6 +278,11 @@ class MonodomainOperator:
     def ipc_import(self, side: int, blob: bytes):
         _check(_lib().emrkc_ipc_import(self._h, side, blob, len(blob)), self._h)
 
+    def set_slab_min_depth(self, planes: int):
+        """Smallest slab depth of the partition: enables the K-plane d_1 halo
+        of the temporally blocked inner stages (emrkc_set_slab_min_depth)."""
+        _check(_lib().emrkc_set_slab_min_depth(self._h, int(planes)), self._h)
+
     def dist_run(self, step0, nsteps, dt, rho_F, rho_S, epsilon=kDefaultDamping) -> dict:
         res = RunResult()
         _check(_lib().emrkc_dist_run(self._h, step0, nsteps, dt, epsilon, capi.EMRKC_VARIANT_STANDARD,

@@ -24,11 +24,17 @@ def main(out):
     ctx = pdist.DistContext(rank, world,
                             lambda b: _gather(b, world), lambda d: _gather(d, world))
     results = {}
-    cases = [("p3d_48_s2m2", 12), ("hh2d_256x256", 10), ("hh3d_sweep_25", 15)]
-    for name, n in cases:
+    # key@tb: rho_F forced up to m = 5 with s = 1, so the inner stages 2..5
+    # run temporally blocked with the wide (K = 4 plane) d_1 halo
+    cases = [("p3d_48_s2m2", 12), ("hh2d_256x256", 10), ("hh3d_sweep_25", 15),
+             ("p3d_48_s2m2@tb", 6)]
+    for key, n in cases:
+        name = key.split("@")[0]
         w = workloads.get(name)
         rF = 16.0 if w.problem.dim == 3 else 9.1
         rS = w.rho_S_forced if w.rho_S_forced is not None else 0.7114
+        if key.endswith("@tb"):
+            rF, rS = 700.0, 0.7114
         slab = pdist.DistSlab(w.problem, ctx, 0)
         slab.link()
         barrier = HOOK(lambda _c: dist.barrier())
@@ -50,10 +56,10 @@ def main(out):
                 m = b - a
                 for k in range(4):
                     full[k * nn + a:k * nn + b] = ys[r][k * m:(k + 1) * m]
-            results[name + "/y"] = full
-            results[name + "/rec"] = np.array([rec["s"], rec["m"], rec["aborted"], rec["n_fF"]])
-            results[name + "/rho"] = np.array([rF, rS])
-            results[name + "/n"] = np.array([n])
+            results[key + "/y"] = full
+            results[key + "/rec"] = np.array([rec["s"], rec["m"], rec["aborted"], rec["n_fF"]])
+            results[key + "/rho"] = np.array([rF, rS])
+            results[key + "/n"] = np.array([n])
     if rank == 0:
         np.savez(out, **results)
     dist.barrier()

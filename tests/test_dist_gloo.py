@@ -36,6 +36,9 @@ class FakeOp:
     def ipc_import(self, side, blob):
         self.imported[side] = blob
 
+    def set_slab_min_depth(self, planes):
+        self.min_depth = planes
+
     def dist_run(self, step0, nsteps, *a):
         self.calls.append(("run", step0, nsteps))
         if self.abort is None:
@@ -69,6 +72,9 @@ def _worker(rank, world, port, scenario, q):
     op = FakeOp(rank, abort)
     slab = dist.DistSlab(hh3d_128().problem, ctx, op=op)
     slab.link()
+    # the smallest slab of the partition, the same on every rank
+    assert op.min_depth == min(dist.partition(slab.problem, world, r).z_end -
+                               dist.partition(slab.problem, world, r).z_begin for r in range(world))
     glob = slab.run(0, 10, 0.05, 15.0, 0.7)
     q.put((rank, {k: v for k, v in glob.items()}, op.imported, op.calls,
            (slab.part.z_begin, slab.part.z_end)))

@@ -51,12 +51,26 @@ def gather(p, ops):
     return y
 
 
+# *_tb: rho_F forced so that 2 <= K = m - 1 <= 4 inner stages run temporally
+# blocked (k_vin_tb) on every slab, with the K-plane d_1 halo between slabs
+TB_CASES = {"3d_tb_m3": (3, 1), "3d_tb_m5": (5, 1), "3d_tb_s2m4": (4, 2)}
+
+
 @pytest.mark.parametrize("nslab", [2, 3, 4])
-@pytest.mark.parametrize("case", ["3d_m2", "2d_m1", "3d_m1"])
+@pytest.mark.parametrize("case", ["3d_m2", "2d_m1", "3d_m1", *TB_CASES])
 def test_dist_protocol_bitwise(case, nslab):
     if case == "3d_m2":
         w = workloads.parity_3d()
         p, y0, dt, rF, rS, n = w.problem, w.initial_state(), w.dt, 400.0, 50.0, 6
+    elif case == "3d_tb_m3":
+        w = workloads.hh3d_sweep(25)
+        p, y0, dt, rF, rS, n = w.problem, w.initial_state(), w.dt, 250.0, 0.7, 10
+    elif case == "3d_tb_m5":
+        w = workloads.parity_3d()
+        p, y0, dt, rF, rS, n = w.problem, w.initial_state(), w.dt, 700.0, 0.7, 6
+    elif case == "3d_tb_s2m4":
+        w = workloads.parity_3d()
+        p, y0, dt, rF, rS, n = w.problem, w.initial_state(), w.dt, 1500.0, 50.0, 6
     elif case == "2d_m1":
         p = make_problem(2, [96, 64], [0.25, 0.25], [0.1, 0.1], 140.0, 0.01, 70.0,
                          [-0.125, -0.125], [3.875, 3.875], 0.0, 1.0)
@@ -75,6 +89,8 @@ def test_dist_protocol_bitwise(case, nslab):
     res = lockstep(ops, 0, 0, n, dt, rF, rS)
     assert np.array_equal(gather(p, ops), yw)
     assert (res.s, res.m, res.n_fF, res.aborted) == (rw.s, rw.m, rw.n_fF, 0)
+    if case in TB_CASES:
+        assert (res.m, res.s) == TB_CASES[case]
     # a second run continues the counters / level bookkeeping consistently
     res2 = lockstep(ops, 0, n, 3, dt, rF, rS)
     whole.run(n, 3, dt, rF, rS)

@@ -34,3 +34,16 @@ def test_slab_initial_state_matches_global(name, world):
         part = dist.partition(w.problem, world, r)
         np.testing.assert_array_equal(dist.slab_initial_state(w, part),
                                       dist.slab_of(w.problem, part, y))
+
+
+@pytest.mark.parametrize("nz,world,expect", [(200, 8, 25), (48, 5, 9), (25, 4, 6), (128, 1, 128)])
+def test_min_slab_depth(nz, world, expect):
+    """Every rank derives the same smallest slab depth (the switch of the
+    K-plane d_1 halo must agree across ranks)."""
+    w = workloads.get("hh3d_sweep_25")
+    p = workloads.z_scaled(w, 1).problem
+    p.n[2] = nz
+    depths = [int(dist.partition(p, world, r).z_end - dist.partition(p, world, r).z_begin)
+              for r in range(world)]
+    assert sum(depths) == nz
+    assert dist.min_slab_depth(p, world) == min(depths) == expect

@@ -27,10 +27,11 @@ def ranks(request, tmp_path_factory):
     return np.load(out)
 
 
-@pytest.mark.parametrize("name", ["p3d_48_s2m2", "hh2d_256x256", "hh3d_sweep_25"])
+@pytest.mark.parametrize("name", ["p3d_48_s2m2", "hh2d_256x256", "hh3d_sweep_25",
+                                  "p3d_48_s2m2@tb"])
 def test_ipc_slabs_bitwise(ranks, name):
     two_ranks = ranks
-    w = workloads.get(name)
+    w = workloads.get(name.split("@")[0])
     rF, rS = two_ranks[name + "/rho"]
     n = int(two_ranks[name + "/n"][0])
     op = MonodomainOperator(w.problem)
@@ -40,5 +41,7 @@ def test_ipc_slabs_bitwise(ranks, name):
     op.close()
     s, m, aborted, nff = two_ranks[name + "/rec"]
     assert (res.s, res.m, res.aborted, res.n_fF) == (s, m, aborted, nff)
+    if name.endswith("@tb"):
+        assert (s, m) == (1, 5)  # K = 4 blocked stages: the widest halo
     got = two_ranks[name + "/y"]
     assert np.array_equal(got, y), np.abs(got - y).max()

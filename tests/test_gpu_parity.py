@@ -156,7 +156,7 @@ def test_norm_guard(oracle):
 
 
 @pytest.mark.parametrize("nslab", [2, 3, 5])
-@pytest.mark.parametrize("name", ["p3d_48_s2m2", "hh2d_small"])
+@pytest.mark.parametrize("name", ["p3d_48_s2m2", "hh2d_small", "p3d_48_tb"])
 def test_group_slabs_bitwise(oracle, name, nslab):
     """z-slab decomposition on one device: bitwise equal to the whole grid
     (the stencil has no order-dependent reductions)."""
@@ -169,6 +169,11 @@ def test_group_slabs_bitwise(oracle, name, nslab):
         p = small_2d(64, 50)
         y0 = noisy(oracle, p)
         dt, rF, rS, n = 0.05, 10.0, 0.7, 30
+    elif name == "p3d_48_tb":  # m = 5: K = 4 temporally blocked stages, 4-plane d_1 halo
+        w = workloads.get("p3d_48_s2m2")
+        p = w.problem
+        y0 = w.initial_state()
+        dt, rF, rS, n = w.dt, 700.0, 0.7, 6
     else:
         w = workloads.get(name)
         p = w.problem
@@ -203,6 +208,8 @@ def test_group_slabs_bitwise(oracle, name, nslab):
             yg[s0:s0 + nn_l] = loc[b * nn_l:(b + 1) * nn_l]
     assert np.array_equal(yg, yw), np.abs(yg - yw).max()
     assert (res.s, res.m, res.n_fF) == (rw.s, rw.m, rw.n_fF)
+    if name == "p3d_48_tb":
+        assert (res.s, res.m) == (1, 5)
     assert res.gate_min == rw.gate_min and res.gate_max == rw.gate_max
     lib.emrkc_group_destroy(grp)
 
