@@ -1325,6 +1325,9 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     zs1 = g.st_hi[DIM - 1] - g.zoff;
   }
   bool bad = false, guard = false;
+  // finite test folded over the hot loop: min over nodes of the sum's
+  // (~hi & exponent mask); 0 means some node produced Inf/NaN
+  unsigned finacc = 0x7ff00000u;
   unsigned slow_mask = 0;
   double glo = 2.0, ghi = -1.0;
   double* po = a.out + ip + plane * zb;
@@ -1371,7 +1374,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         *po = r.o0;
         guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
-      bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
+      finacc = min(finacc, ~(unsigned)__double2hiint((r.o0 + r.o1) + (r.o2 + r.o3)) & 0x7ff00000u);
       if (z < pp.zl) pp.plo[ip + plane * z] = r.o0;
       if (z >= pp.zh) pp.phi[ip + plane * (z - pp.zh)] = r.o0;
       if (a.last) {  // std::min / std::max per value (NaN skipped), select form
@@ -1389,6 +1392,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     // deeper gate ring keeps every refill behind a barrier
     if (kSyncP<FIRST>() == 1 || ((z - zb) & 1)) __syncthreads();
   }
+  bad = finacc == 0u;
   if (!skipped && valid && slow_mask) {
     const Nbr<DIM> o = nbr_of<DIM>(g, Col<DIM>{cx, cy, ip, zb, ze, true});
     const double* G = a.g1;
