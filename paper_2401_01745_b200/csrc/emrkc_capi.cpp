@@ -393,6 +393,14 @@ double* dghost_at(double* base, size_t pl, int side, int par) {
   return base + (4 + static_cast<size_t>(2 * side + par) * emrkc_k::kTbMaxK) * pl;
 }
 
+// The fast ionic path's V window for this eta (fast_math.cuh) as centre and
+// radius: |V - vmid| <= vrad (empty window: vrad < 0, never fast).
+void fast_window(double eta, double* vmid, double* vrad) {
+  const double lo = emrkc_k::fast_vlo(eta), hi = emrkc_k::fast_vhi(eta);
+  *vmid = 0.5 * (lo + hi);
+  *vrad = 0.5 * (hi - lo);
+}
+
 int ensure_buffers(emrkc_handle* h, int nb) {
   for (int i = h->nbuf; i < nb; ++i)
     CK(h, cudaMalloc(&h->buf[i], sizeof(double) * h->len));
@@ -734,7 +742,7 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.nu = a.nu;
       f.kappa = a.kappa;
       // fast ionic path only where its range analysis holds (fast_math.cuh)
-      f.vfast = pl.eta <= 1.5 ? 150.0 : -1.0;
+      fast_window(pl.eta, &f.vmid, &f.vfast);
       f.j = j;
       f.m = pl.m;
       f.s = pl.s;
@@ -1612,7 +1620,7 @@ int run_resident(emrkc_handle* h, int64_t step0, int64_t nsteps, int* out_idx) {
   f.cV = cG * pl.in_mueta[1];
   f.mue1 = pl.in_mueta[1];
   f.exex = pl.exex;
-  f.vfast = pl.eta <= 1.5 ? 150.0 : -1.0;
+  fast_window(pl.eta, &f.vmid, &f.vfast);
   f.j = 1;
   f.m = pl.m;
   f.s = pl.s;

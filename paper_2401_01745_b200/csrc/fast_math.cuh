@@ -33,13 +33,18 @@ __constant__ FastConsts kFC = {
     kL2E256, kLn2_256_hi, kLn2_256_lo, 1.0 / 24.0, 1.0 / 6.0, 1.0 / 12.0,
     0.1, 0.1, 0.01, 0.07, 0.125, 1.0 / 18.0, 0.0125, 1.6487212707001282,
     0.22313016014842982, 1.2, 0.36, 0.003, -54.387, 12.182493960703473};
-// hh_expeuler_fast validity: |V| <= kFastVmax and eta <= kFastEtaMax. There
-// max(alpha + beta) ~ 450/ms (beta_m at V = -150 mV), so |eta Lambda| <= 700
-// and every exp_tab_nc argument stays in range; the batch product stays
-// < 1e140. Other nodes take the reference-order path (hh_expeuler_ref),
-// which also catches non-finite V.
-constexpr double kFastVmax = 150.0;
-constexpr double kFastEtaMax = 1.5;
+// hh_expeuler_fast validity window (host: fast_window, per eta): every
+// exp_tab_nc argument stays within +-700 and the batch product finite. The
+// rates that grow without bound are beta_m = 4 e^{-(V+65)/18} below rest and
+// alpha_m ~ 0.1 (V + 40), alpha_n ~ 0.01 (V + 55) above it, so
+//   V >= max(-400, -65 - 18 ln(150 / eta))   (eta beta_m <= 600)
+//   V <= min(10000, 6000 / eta - 80)         (eta (alpha_m + beta_m) <= 600)
+// (at V = -400 the batch product is ~1e110, far from overflow; at 10000 the
+// shared exponentials' arguments are ~ -560). Nodes outside the window (and
+// non-finite V) take the reference-order path (hh_expeuler_ref). Before this
+// window the bound was a fixed |V| <= 150 for eta <= 1.5: a strong stimulus
+// pushed whole planes past +150 mV into the per-thread reference path.
+// (kernels.h: fast_vlo / fast_vhi)
 
 __device__ __forceinline__ double exp_tab(double x, const double* __restrict__ tab) {
   const int hi = __double2hiint(x);
@@ -97,7 +102,7 @@ __device__ __forceinline__ void load_exp_table(double* sh, int tid, int nthreads
 }
 
 // ---------------------------------------------------------------------------
-// Valid for |V| <= kFastVmax, eta <= kFastEtaMax (see above).
+// Valid inside the fast_vlo(eta) .. fast_vhi(eta) window (see above).
 //
 // Exponential Euler of the three HH gates at one node, with the rates
 // evaluated through shared exponentials (hh.cuh, hh_gate_coeffs_fast) and
@@ -159,8 +164,8 @@ __device__ __forceinline__ void hh_expeuler_fast(double V, double z0, double z1,
   const double idh = iB * pm, ipm = iB * dh;
   const double ipn = iC * ph, iph = iC * pn;
   const double me = -eta;
-  // eta*Lambda_g = -eta (alpha+beta) = -eta p/d >= -700 for |V| <= kFastVmax
-  // and eta <= kFastEtaMax (host-checked), so exp_tab_nc needs no clamp.
+  // eta*Lambda_g = -eta (alpha+beta) = -eta p/d >= -600 inside the window
+  // (host-checked per node), so exp_tab_nc needs no clamp.
   const double em = exp_tab_nc(me * (pm * idm), tab) - 1.0;
   const double eh = exp_tab_nc(me * (ph * idh), tab) - 1.0;
   const double en = exp_tab_nc(me * (pn * idn), tab) - 1.0;

@@ -132,7 +132,7 @@ __device__ __forceinline__ void hh_gate_coeffs_fast(double V, double* lam,
 }
 
 // Reference-order exponential Euler of the gates (the fast kernels' path
-// for |V| > kFastVmax or non-finite V): d = expm1(eta*Lambda)(z - z_inf).
+// for V outside fast_math.cuh's window, or non-finite V): d = expm1(eta*Lambda)(z - z_inf).
 struct Dgate {
   double d0, d1, d2;
 };

@@ -2,6 +2,8 @@
 // Internal to libemrkc_b200.so (not part of the C ABI).
 #pragma once
 
+#include <cmath>
+
 #include <cstdint>
 
 #include <cuda.h>
@@ -139,7 +141,7 @@ struct FastArgs {
   double cV;          // cG * mu'_1 eta  (m == 1: V of g_j = base + cV (f_F + f_S))
   double mue1;        // mu'_1 eta       (m >= 2: u_1 = V + mue1 (f_F + f_S))
   double nu, kappa;   // outer nu_j, kappa_j (j >= 2)
-  double vfast;       // |V| bound of the fast ionic path (0: never)
+  double vmid, vfast; // fast ionic path iff |V - vmid| <= vfast (fast_window)
   int j, m, s, last, zc;
   int exex;           // EXEX-RL step: non-finite values are not aborts (guard only)
   int z_lo, z_hi;     // k_node_tma: local planes [z_lo, z_hi) of this launch (0, nzl: all)
@@ -242,6 +244,12 @@ constexpr int kTX3 = 32, kTY3 = 4, kTX2 = 128;
 // z-chunk length of the staged kernels (bounded by the 32-bit deferred-node
 // mask of k_node_pipe / k_node_tma).
 constexpr int kMaxZc = 32;
+
+// Window of V where the fast ionic path (fast_math.cuh, hh_expeuler_fast)
+// is valid for this eta: eta * (alpha + beta) <= 600 for every gate and every
+// exponential argument within +-700 (derivation in fast_math.cuh).
+inline double fast_vlo(double eta) { return std::fmax(-400.0, -65.0 - 18.0 * std::log(150.0 / eta)); }
+inline double fast_vhi(double eta) { return std::fmin(10000.0, 6000.0 / eta - 80.0); }
 int fast_zc(const Geom& g);
 // Signals per level that a neighbour receives from one launch of each kernel
 // family (blocks that hold the boundary plane of their slab).

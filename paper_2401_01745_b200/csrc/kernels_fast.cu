@@ -296,7 +296,7 @@ __device__ __forceinline__ NodeOut node_update(const Geom& g, const FastArgs& a,
   if (DIM >= 2) D = fma(g.w[0], xs, D);
   if (DIM == 3) D = fma(g.w[1], ys, D);
   double d0, d1, d2;
-  if (fabs(vc) <= a.vfast) {
+  if (fabs(vc - a.vmid) <= a.vfast) {
     hh_expeuler_fast(vc, z0, z1, z2, a.eta, tab, d0, d1, d2);
   } else {
     const Dgate dd = hh_expeuler_ref(vc, z0, z1, z2, a.eta);
@@ -332,7 +332,7 @@ __device__ __forceinline__ NodeOut node_update_s(const Geom& g, const FastArgs& 
   if (DIM >= 2) D = fma(g.w[0], xs, D);
   if (DIM == 3) D = fma(g.w[1], ys, D);
   double d0, d1, d2;
-  if (!SLOW || fabs(vc) <= a.vfast) {
+  if (!SLOW || fabs(vc - a.vmid) <= a.vfast) {
     hh_expeuler_fast(vc, z0, z1, z2, a.eta, tab, d0, d1, d2);
   } else {
     const Dgate dd = hh_expeuler_ref(vc, z0, z1, z2, a.eta);
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
     // |V| beyond the fast path's range (or non-finite): deferred to the
     // reference-order path after the loop, so the hot loop has no call
-    const bool fast = fabs(vc) <= a.vfast;
+    const bool fast = fabs(vc - a.vmid) <= a.vfast;
     if (!fast) slow_mask |= 1u << (z - zb);
     NodeOut r = node_update_s<DIM, FIRST, ION, 0>(
         g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, 0.0,
@@ -899,7 +899,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
       const double* G0 = gst + (cc & (kRG - 1)) * 3 * T::NT + t;
       const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
       const double stim = (scol && stim_z<DIM>(g, z)) ? a.stim : 0.0;
-      const bool fast = fabs(vc) <= a.vfast;
+      const bool fast = fabs(vc - a.vmid) <= a.vfast;
       if (!fast) slow_mask |= 1u << (z - zb);
       const NodeOut rr = node_update_s<DIM, FIRST, ION, 0>(
           g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, stim,
@@ -1355,7 +1355,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     if (DIM == 3) ys = V0[cym] + V0[cyp];
     const double* G0 = gst + ((z - zb) & (RG - 1)) * 3 * T::NT + t;
     const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
-    const bool fast = fabs(vc) <= a.vfast;
+    const bool fast = fabs(vc - a.vmid) <= a.vfast;
     if (!fast) slow_mask |= 1u << (z - zb);
     NodeOut r = node_update_s<DIM, FIRST, ION, 0>(
         g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, 0.0,
@@ -1544,7 +1544,7 @@ __global__ void __launch_bounds__(kResNT) k_resident(const Geom g, const Residen
       double ys = 0.0;
       if (DIM == 3) ys = __ldcg(V + i + ((f & 4u) ? -sy : sy)) + __ldcg(V + i + ((f & 8u) ? sy : -sy));
       const bool box = (f & 64u) != 0;
-      const bool fast = fabs(vc) <= a.vfast;
+      const bool fast = fabs(vc - a.vmid) <= a.vfast;
       NodeOut o;
       if (fast) {
         o = node_update_s<DIM, 1, 0, 0>(g, a, tab, vm, vc, vp, xs, ys, z0[k], z1[k], z2[k], 0.0,
