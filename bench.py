@@ -345,10 +345,16 @@ def measure_device(w, device, warmup, steps, with_e2e=True, clocks=None, ramp_s=
         op.run(0, max(1, min(50, w.n_steps)), w.dt, rF, rS, w.eps)
         op.set_state(y0)
         ramp += 1
+    # a simulation that hits NumericalAbort / the norm guard at step kr is
+    # timed over its first kr steps only (later steps would only run the
+    # kernels' skip path and inflate the rate)
+    op.set_state(y0)
+    rr = op.run(0, w.n_steps, w.dt, rF, rS, w.eps)
+    kr = max(1, int(rr.abort_step)) if rr.aborted else w.n_steps
     chunks = []
     left = steps
     while left > 0:
-        chunks.append(min(left, w.n_steps))
+        chunks.append(min(left, kr))
         left -= chunks[-1]
     launch_ms = np.zeros(steps * per)
     results = []
@@ -368,9 +374,6 @@ def measure_device(w, device, warmup, steps, with_e2e=True, clocks=None, ramp_s=
     # loop; small grids take the one-launch resident kernel), device events
     # around the run, no L2 flush between its steps
     # (a run that aborts is timed over the steps before the abort only)
-    op.set_state(y0)
-    rr = op.run(0, w.n_steps, w.dt, rF, rS, w.eps)
-    kr = int(rr.abort_step) if rr.aborted else w.n_steps
     run = None
     if kr >= 2:
         run_ms = []
@@ -385,7 +388,8 @@ def measure_device(w, device, warmup, steps, with_e2e=True, clocks=None, ramp_s=
                        ", best of 3, device time of the run, no L2 flush between steps"}
     out = {"op": op, "y0": y0, "rF": rF, "rS": rS, "s": rep.s, "m": rep.m, "run": run,
            "launch_ms": launch_ms.reshape(steps, per), "res": results[-1], "steps": steps,
-           "repeats": len(chunks), "aborted": any(r.aborted for r in results)}
+           "repeats": len(chunks), "aborted": any(r.aborted for r in results),
+           "abort_at": kr if kr < w.n_steps else None}
     if with_e2e:
         out["e2e"] = measure_e2e(op, w, y0, rF, rS, min(steps, 20))
         out["e2e_run"] = measure_e2e_run(op, w, y0, rF, rS)
@@ -516,7 +520,9 @@ def b200_arm(args, w):
                  "eta": res.eta, "aborted": bool(m["aborted"]),
                  "timed_repeats": m["repeats"],
                  "timed_note": f"{args.steps} timed steps = {m['repeats']} repeat(s) of the "
-                               f"workload's simulation from the seeded state (<= {w.n_steps} steps each)"},
+                               f"workload's simulation from the seeded state (<= {w.n_steps} steps each)" +
+                               (f"; the simulation hits the reference's NumericalAbort/guard at step "
+                                f"{m['abort_at']}, so each repeat stops there" if m.get("abort_at") else "")},
         "roofline": roofline_of(m, w, peak, peak_kind),
         "e2e": m["e2e"],
         "e2e_run": m["e2e_run"],

@@ -562,15 +562,18 @@ bool tma_supported(const emrkc_handle* h) {
   return h->geom.dim >= 2 && h->geom.n0 % 2 == 0 && tma_encoder() != nullptr;
 }
 
-int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out) {
+// rmul: tile rows x rmul (the multi-row inner-stage kernel, vin_rows)
+int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out, int rmul = 1) {
+  const int key = kind + 1000 * (rmul - 1);
   for (const auto& e : h->tmaps)
-    if (e.ptr == ptr && e.kind == kind) {
+    if (e.ptr == ptr && e.kind == key) {
       *out = e.map;
       return EMRKC_OK;
     }
   const Geom& g = h->geom;
   const bool d3 = g.dim == 3;
-  const cuuint32_t tx = d3 ? emrkc_k::kTX3 : emrkc_k::kTX2, ty = d3 ? emrkc_k::kTY3 : 1;
+  const cuuint32_t tx = d3 ? emrkc_k::kTX3 : emrkc_k::kTX2,
+                   ty = d3 ? emrkc_k::kTY3 * static_cast<cuuint32_t>(rmul) : 1;
   const bool halo = kind == kTmaHalo || kind == kTmaGhost;
   cuuint64_t dims[4];
   cuuint64_t strides[3];
@@ -602,7 +605,7 @@ int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out) {
       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_err(h, EMRKC_ECUDA, "cuTensorMapEncodeTiled failed (%d, kind %d)", (int)r, kind);
-  h->tmaps.push_back({ptr, kind, m});
+  h->tmaps.push_back({ptr, key, m});
   *out = m;
   return EMRKC_OK;
 }
@@ -655,15 +658,15 @@ double* nbr_dghost(const emrkc_handle* h, int side, int par) {
   return nullptr;
 }
 
-int tma_ghosts(emrkc_handle* h, const Halo& hl, CUtensorMap* lo, CUtensorMap* hi) {
+int tma_ghosts(emrkc_handle* h, const Halo& hl, CUtensorMap* lo, CUtensorMap* hi, int rmul = 1) {
   std::memset(lo, 0, sizeof *lo);
   std::memset(hi, 0, sizeof *hi);
   if (hl.lo) {
-    const int rc = tma_map(h, hl.lo, kTmaGhost, lo);
+    const int rc = tma_map(h, hl.lo, kTmaGhost, lo, rmul);
     if (rc) return rc;
   }
   if (hl.hi) {
-    const int rc = tma_map(h, hl.hi, kTmaGhost, hi);
+    const int rc = tma_map(h, hl.hi, kTmaGhost, hi, rmul);
     if (rc) return rc;
   }
   return EMRKC_OK;
@@ -847,14 +850,16 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       if (h->pipe == 3) {
         emrkc_k::TmaVin tm;
         std::memset(&tm, 0, sizeof tm);
-        int rc = tma_map(h, f.um1, kTmaHalo, &tm.u);
-        if (!rc) rc = tma_map(h, f.d1, kTmaCenter, &tm.d1);
-        if (!rc && f.um2) rc = tma_map(h, f.um2, kTmaCenter, &tm.um2);
-        if (!rc && k == pl.m) rc = tma_map(h, f.g1v, kTmaCenter, &tm.g1v);
-        if (!rc && k == pl.m && f.g2v) rc = tma_map(h, f.g2v, kTmaCenter, &tm.g2v);
-        if (!rc) rc = tma_ghosts(h, hl, &tm.glo, &tm.ghi);
+        const int rm = emrkc_k::vin_rows(h->geom);
+        int rc = tma_map(h, f.um1, kTmaHalo, &tm.u, rm);
+        if (!rc) rc = tma_map(h, f.d1, kTmaCenter, &tm.d1, rm);
+        if (!rc && f.um2) rc = tma_map(h, f.um2, kTmaCenter, &tm.um2, rm);
+        if (!rc && k == pl.m) rc = tma_map(h, f.g1v, kTmaCenter, &tm.g1v, rm);
+        if (!rc && k == pl.m && f.g2v) rc = tma_map(h, f.g2v, kTmaCenter, &tm.g2v, rm);
+        if (!rc) rc = tma_ghosts(h, hl, &tm.glo, &tm.ghi, rm);
         if (rc) return rc;
         CK(h, emrkc_k::launch_vin_tma(h->geom, hl, f, tm, h->stream));
+        signals = emrkc_k::halo_signals_vin(h->geom);
       } else if (h->pipe)
         CK(h, emrkc_k::launch_vin_pipe(h->geom, hl, f, h->stream));
       else

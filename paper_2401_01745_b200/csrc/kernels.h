@@ -268,6 +268,10 @@ cudaError_t launch_node_persist(const Geom& g, const Halo& h, const FastArgs& a,
                                 bool ion, cudaStream_t st);
 cudaError_t launch_node_tma(const Geom& g, const Halo& h, const FastArgs& a,
                             const TmaNode& tm, bool ion, cudaStream_t st);
+// Rows per thread of the 3-D inner-stage kernel (its TMA boxes are
+// (TX+4) x (4 rows + 2) and TX x 4 rows, rows = vin_rows); 1 in 2-D.
+int vin_rows(const Geom& g);
+long long halo_signals_vin(const Geom& g);  // arrivals per side of a launch_vin_tma level
 cudaError_t launch_vin_tma(const Geom& g, const Halo& h, const FastInnerArgs& a,
                            const TmaVin& tm, cudaStream_t st);
 cudaError_t launch_vin_fast(const Geom& g, const Halo& h,

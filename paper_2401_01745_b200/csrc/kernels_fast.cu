@@ -1860,6 +1860,178 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
 }
 
 // ---------------------------------------------------------------------------
+// k_vin_tma_r<LAST, FIRST, R>: k_vin_tma (3-D) with R rows per thread. The
+// inner stages k >= 2 move 16-40 B per node and do ~12 FP64 operations, so
+// one node per thread per plane left them issue-bound (75-85% issue, ncu):
+// the per-plane work — mbarrier wait, ring-slot arithmetic, the plane
+// barrier, thread 0's copy issue — cost more than the node. A 32 x 4R tile
+// with 128 threads spreads that work over R nodes. The centre ring holds only
+// the fields this launch reads (nb of d_1, d_{k-2}, V of g_{j-1}, g_{j-2}).
+// Same arithmetic, in the same order, as k_vin_tma (bitwise equal).
+// ---------------------------------------------------------------------------
+#ifndef EMRKC_VIN_R
+#define EMRKC_VIN_R 2
+#endif
+template <int R>
+struct VinTileR {
+  static constexpr int TX = 32, TY = 4 * R, NT = 128;
+  static constexpr int CS = TX * TY;                 // centre cells
+  static constexpr int HX = TX + 4, HY = TY + 2;
+  static constexpr int VT = HX * HY;
+  static constexpr int VS = (VT + 15) & ~15;
+};
+template <int R>
+size_t tma_vin_r_smem_bytes(int nb) {
+  return sizeof(double) * ((size_t)kRV * VinTileR<R>::VS + (size_t)kRG * nb * VinTileR<R>::CS) + 128;
+}
+
+template <int LAST, int FIRST, int R>
+__global__ void __launch_bounds__(128)
+    k_vin_tma_r(const Geom g, const Halo h, const FastInnerArgs a, const __grid_constant__ TmaVin tm) {
+  using T = VinTileR<R>;
+  constexpr int VS = T::VS;
+  extern __shared__ __align__(128) double smem_tma[];
+  double* vst = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;  // [kRV][VS]
+  double* cst = vst + kRV * VS;                      // [kRG][nb][CS]
+  __shared__ __align__(8) unsigned long long bars[kRV];
+  __shared__ int skip;
+  const int t = threadIdx.x;
+  const int zb = blockIdx.z * a.zc;
+  const int ze = min(g.nzl, zb + a.zc);
+  pdl_launch_dependents();
+  if (t == 0) {
+    for (int s = 0; s < kRV; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    mbar_fence_init();
+    prefetch_tensormap(&tm.u);
+  }
+  __syncthreads();  // barriers initialised before any warp issues onto them
+  const int tx = t % T::TX, ty = t / T::TX;  // rows ty, ty + 4, ...
+  const int x0 = blockIdx.x * T::TX, y0 = blockIdx.y * T::TY;
+  const long long plane = g.plane;
+  const bool has2 = a.um2 != nullptr;
+  const bool d1_is_u = a.um1 == a.d1;
+  // centre fields present, packed: d_1, d_{k-2}, V of g_{j-1}, V of g_{j-2}
+  const int f_um2 = d1_is_u ? 0 : 1;
+  const int f_g1 = f_um2 + (has2 ? 1 : 0);
+  const int nb = f_g1 + (LAST ? (FIRST ? 1 : 2) : 0);
+  const unsigned v0 = smem_u32(vst), c0 = smem_u32(cst), b0 = smem_u32(bars);
+  constexpr unsigned vbytes = 8u * T::VT;
+  const unsigned cbytes = 8u * T::CS * nb;
+  auto issue_comp = [&](int zz) {  // zz in [zb, ze); thread 0
+    const int q = zz - zb + 1;
+    const unsigned bar = b0 + 8u * (q & (kRV - 1));
+    const unsigned sc = c0 + 8u * T::CS * nb * ((zz - zb) & (kRG - 1));
+    mbar_expect_tx(bar, vbytes + cbytes);
+    tma_load_3d(v0 + 8u * VS * (q & (kRV - 1)), &tm.u, bar, x0 - 2, y0 - 1, zz);
+    if (!d1_is_u) tma_load_3d(sc, &tm.d1, bar, x0, y0, zz);
+    if (has2) tma_load_3d(sc + 8u * T::CS * f_um2, &tm.um2, bar, x0, y0, zz);
+    if (LAST) {
+      tma_load_3d(sc + 8u * T::CS * f_g1, &tm.g1v, bar, x0, y0, zz);
+      if (!FIRST) tma_load_3d(sc + 8u * T::CS * (f_g1 + 1), &tm.g2v, bar, x0, y0, zz);
+    }
+  };
+  auto issue_edge = [&](int zz) {  // zz = zb - 1 or ze; thread 0
+    const int q = zz - zb + 1;
+    const unsigned bar = b0 + 8u * (q & (kRV - 1));
+    mbar_expect_tx(bar, vbytes);
+    tma_vplane<3>(g, &tm.u, &tm.glo, &tm.ghi, true, true, v0 + 8u * VS * (q & (kRV - 1)), bar,
+                  x0, y0, zz);
+  };
+  pdl_wait();
+  halo_wait(h, zb == 0, ze >= g.nzl);
+  if (t == 0) {
+    // ghost planes arrived through generic peer stores (acquired in
+    // halo_wait); order them before this thread's async-proxy reads
+    fence_proxy_async();
+    issue_edge(zb - 1);
+    for (int i = 0; i < kTmaLA; ++i) {
+      if (zb + i < ze) issue_comp(zb + i);
+      else {
+        issue_edge(ze);
+        break;
+      }
+    }
+  }
+  if (t == (EMRKC_EVWARP1 ? 32 : 0)) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  __syncthreads();
+  if (skip) {  // aborted earlier: drain the prologue copies, release the neighbours
+    const int np = 1 + min(kTmaLA, ze - zb) + (ze - zb < kTmaLA ? 1 : 0);
+    for (int q = 0; q < np; ++q) mbar_wait(b0 + 8u * q, 0);
+    halo_signal(h, zb == 0, ze >= g.nzl);
+    return;
+  }
+  // per-row cells: V-box cell, mirrored neighbours, global column, validity
+  constexpr int HXT = T::HX;
+  const int cx = x0 + tx;
+  const int dxm = cx > 0 ? -1 : 1, dxp = cx < g.n0 - 1 ? 1 : -1;
+  int cell[R], dym[R], dyp[R];
+  long long ipr[R];
+  unsigned vmask = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int ry = ty + 4 * r, cy = y0 + ry;
+    cell[r] = (ry + 1) * HXT + tx + 2;
+    dym[r] = cy > 0 ? -HXT : HXT;
+    dyp[r] = cy < g.n1 - 1 ? HXT : -HXT;
+    const bool valid = cx < g.n0 && cy < g.n1;
+    if (valid) vmask |= 1u << r;
+    ipr[r] = valid ? (long long)cx + (long long)g.n0 * cy : 0;
+  }
+  bool bad_in = false, bad_out = false, guard = false;
+  mbar_wait(b0, 0);
+  mbar_wait(b0 + 8u, 0);
+  for (int z = zb; z < ze; ++z) {
+    const int p = z - zb + 1;
+    if (t == 0) {
+      if (z + kTmaLA < ze) issue_comp(z + kTmaLA);
+      else if (z + kTmaLA == ze) issue_edge(ze);
+    }
+    mbar_wait(b0 + 8u * ((p + 1) & (kRV - 1)), ((p + 1) >> 3) & 1);
+    const double* V0 = vst + (p & (kRV - 1)) * VS;
+    const double* Vm = vst + ((p - 1) & (kRV - 1)) * VS;
+    const double* Vp = vst + ((p + 1) & (kRV - 1)) * VS;
+    const double* C0 = cst + ((z - zb) & (kRG - 1)) * T::CS * nb + t;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int c = cell[r];
+      const double vc = V0[c];
+      double D = fma(g.wc, vc, g.w[2] * (Vm[c] + Vp[c]));
+      D = fma(g.w[0], V0[c + dxm] + V0[c + dxp], D);
+      D = fma(g.w[1], V0[c + dym[r]] + V0[c + dyp[r]], D);
+      const double* Cr = C0 + r * T::NT;  // row r of the tile: cells t + 128 r
+      const double base = has2 ? fma(a.nu, vc, a.kappa * Cr[T::CS * f_um2]) : a.nu * vc;
+      const double d1 = d1_is_u ? vc : Cr[0];
+      const double dk = fma(a.mueta, fma(d1, a.inv_mue1, D), base);
+      if (vmask >> r & 1u) {
+        const long long i = ipr[r] + plane * z;
+        bad_in |= !finite_hi(dk);
+        double vput = dk;
+        if (!LAST) {
+          a.uk[i] = dk;
+        } else {
+          const double gv = Cr[T::CS * f_g1];
+          const double bb = FIRST ? gv : fma(a.onu, gv, a.okappa * Cr[T::CS * (f_g1 + 1)]);
+          const double o0 = fma(a.cG, dk, bb);
+          a.outv[i] = o0;
+          bad_out |= !finite_hi(o0);
+          guard |= !(fabs(o0) <= 1e6);  // also a non-finite V
+          vput = o0;
+        }
+        if (z == 0 && h.put_lo) h.put_lo[ipr[r]] = vput;
+        if (z == g.nzl - 1 && h.put_hi) h.put_hi[ipr[r]] = vput;
+      }
+    }
+    __syncthreads();
+  }
+  halo_signal(h, zb == 0, ze >= g.nzl);
+  const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
+  if (bad_in) atomicMin(a.event, base + a.k);
+  if (LAST && bad_out) atomicMin(a.event, base + a.m + 1);
+  if (LAST && a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+}
+
+// ---------------------------------------------------------------------------
 // k_vin_tb<K, FIRST>: inner stages k = 2 .. K+1 (= m) of outer stage j in one
 // pass over HBM (temporal blocking of the V-only inner iteration).
 //
@@ -2416,9 +2588,39 @@ static cudaError_t launch_vin_tma_t(const Geom& g, const Halo& h, const FastInne
   return launch_k(k_vin_tma<D, L, F>, grd, dim3(T::NT), smem, st, g, h, a, tm);
 }
 
+template <int L, int F, int R>
+static cudaError_t launch_vin_tma_r_t(const Geom& g, const Halo& h, const FastInnerArgs& a,
+                                      const TmaVin& tm, cudaStream_t st) {
+  using T = VinTileR<R>;
+  const int nb = (a.um1 == a.d1 ? 0 : 1) + (a.um2 ? 1 : 0) + (L ? (F ? 1 : 2) : 0);
+  const size_t smem = tma_vin_r_smem_bytes<R>(nb);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_vin_tma_r<L, F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tma_vin_r_smem_bytes<R>(4));
+    attr = true;
+  }
+  const int chunks = (g.nzl + a.zc - 1) / a.zc;
+  const dim3 grd((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks);
+  return launch_k(k_vin_tma_r<L, F, R>, grd, dim3(T::NT), smem, st, g, h, a, tm);
+}
+
+int vin_rows(const Geom& g) { return g.dim == 3 ? EMRKC_VIN_R : 1; }
+long long halo_signals_vin(const Geom& g) {
+  if (g.dim != 3) return halo_signals_pipe(g);
+  const int ty = 4 * EMRKC_VIN_R;
+  return (long long)((g.n0 + 31) / 32) * ((g.n1 + ty - 1) / ty);
+}
+
 cudaError_t launch_vin_tma(const Geom& g, const Halo& h, const FastInnerArgs& a, const TmaVin& tm,
                            cudaStream_t st) {
   const bool last = a.k == a.m, first = a.j == 1;
+  if (g.dim == 3 && EMRKC_VIN_R > 1) {
+    constexpr int R = EMRKC_VIN_R > 1 ? EMRKC_VIN_R : 2;
+    if (!last) return launch_vin_tma_r_t<0, 0, R>(g, h, a, tm, st);
+    return first ? launch_vin_tma_r_t<1, 1, R>(g, h, a, tm, st)
+                 : launch_vin_tma_r_t<1, 0, R>(g, h, a, tm, st);
+  }
   if (g.dim == 3) {
     if (!last) return launch_vin_tma_t<3, 0, 0>(g, h, a, tm, st);
     return first ? launch_vin_tma_t<3, 1, 1>(g, h, a, tm, st) : launch_vin_tma_t<3, 1, 0>(g, h, a, tm, st);
