@@ -157,7 +157,7 @@ def test_norm_guard(oracle):
 
 @pytest.mark.parametrize("nslab", [2, 3, 5])
 @pytest.mark.parametrize("name", ["p3d_48_s2m2", "hh2d_small", "p3d_48_tb"])
-def test_group_slabs_bitwise(oracle, name, nslab):
+def test_group_slabs_bitwise(oracle, name, nslab, monkeypatch):
     """z-slab decomposition on one device: bitwise equal to the whole grid
     (the stencil has no order-dependent reductions)."""
     import ctypes as C
@@ -170,6 +170,7 @@ def test_group_slabs_bitwise(oracle, name, nslab):
         y0 = noisy(oracle, p)
         dt, rF, rS, n = 0.05, 10.0, 0.7, 30
     elif name == "p3d_48_tb":  # m = 5: K = 4 temporally blocked stages, 4-plane d_1 halo
+        monkeypatch.setenv("EMRKC_TB", "1")  # off by default
         w = workloads.get("p3d_48_s2m2")
         p = w.problem
         y0 = w.initial_state()
