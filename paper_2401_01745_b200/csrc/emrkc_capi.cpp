@@ -2079,11 +2079,11 @@ namespace {
 // NumericalAbort y_out is not written and the device state stays y_in).
 constexpr int kMaxHostChunks = 64;
 
-int host_chunks() {  // EMRKC_HOST_CHUNKS (default 16)
+int host_chunks() {  // EMRKC_HOST_CHUNKS (default 8)
   static int n = 0;
   if (!n) {
     const char* e = std::getenv("EMRKC_HOST_CHUNKS");
-    n = (e && *e) ? std::max(1, std::min(kMaxHostChunks, std::atoi(e))) : 16;
+    n = (e && *e) ? std::max(1, std::min(kMaxHostChunks, std::atoi(e))) : 8;
   }
   return n;
 }
@@ -2109,6 +2109,10 @@ int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
   const int64_t nn = h->nn, plane = h->geom.plane;
   const int nz = h->geom.nzl;
   auto zc = [&](int c) { return static_cast<int>(static_cast<int64_t>(c) * nz / kHostChunks); };
+  // Kernel / copy-out ranges lag the copy-in chunks by one plane: plane p
+  // needs p + 1, so the kernel of chunk c covers [zc(c) - 1, zc(c+1) - 1) and
+  // starts as soon as chunk c is in (not c + 1); its output goes out at once.
+  auto kr = [&](int c) { return c == 0 ? 0 : (c == kHostChunks ? nz : zc(c) - 1); };
   // abort word = no event (all ones), gate-range slots {min: all ones, max: 0}
   CK(h, cudaMemsetAsync(h->d_event, 0xff, sizeof(unsigned long long), h->stream));
   CK(h, cudaMemsetAsync(h->d_slots, 0xff, sizeof(unsigned long long), h->stream));
@@ -2130,9 +2134,8 @@ int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
   int rc = EMRKC_OK;
   for (int c = 0; c < kHostChunks && !rc; ++c) {
     CK(h, cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
-    if (c + 1 < kHostChunks) CK(h, cudaStreamWaitEvent(h->stream, h->ev_in[c + 1], 0));
-    h->zr_lo = zc(c);
-    h->zr_hi = zc(c + 1);
+    h->zr_lo = kr(c);
+    h->zr_hi = kr(c + 1);
     rc = launch_level(h, &sc, 1, 1);
     CK(h, cudaEventRecord(h->ev_k[c], h->stream));
   }
@@ -2141,7 +2144,7 @@ int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
   double* dout = h->buf[outi];
   for (int c = 0; c < kHostChunks; ++c) {
     CK(h, cudaStreamWaitEvent(h->s_out, h->ev_k[c], 0));
-    const int64_t off = zc(c) * plane, n = (zc(c + 1) - zc(c)) * plane;
+    const int64_t off = kr(c) * plane, n = (kr(c + 1) - kr(c)) * plane;
     CK(h, cudaMemcpy2DAsync(y_out + off, pitch, dout + off, pitch, sizeof(double) * n, 4,
                             cudaMemcpyDeviceToHost, h->s_out));
   }
