@@ -6,8 +6,12 @@
 
 A step is one emRKC time step (P/src/multirate.cpp:173-189) of the whole
 workload grid; node-steps/s = nodes x steps / seconds. Defaults: N = 1, the
-configs[1] workload of BASELINE.json (HH 3-D 128^3, dt 0.05 ms, T 5 ms =
-100 steps), W = 5, K = 1000 (ten back-to-back repeats of the 100-step run).
+largest single-GPU configuration of BASELINE.json: config 4's grid
+(512x512x256 = 67M nodes, h 0.1 mm, sigma (0.3, 0.1, 0.1), dt 0.05 ms; HH
+stands in for the absent TTP model, s = 1, m = 2; the simulation hits the
+reference's own NumericalAbort at step 65, so timed repeats stop there),
+W = 5, K = 100. BASELINE configs[1] (128^3) and configs[0] (2-D 256^2) are
+`also` lines.
 
 `value`  : device time (CUDA events, per kernel launch, on the launching
            stream) with the state resident in HBM; L2 (126 MB) is flushed
@@ -19,11 +23,14 @@ configs[1] workload of BASELINE.json (HH 3-D 128^3, dt 0.05 ms, T 5 ms =
 `roofline`: the step's dominant kernel, algorithmic bytes / its mean launch
            time against MEASURED_PEAKS.json hbm_gbs.
 `cpu_baseline`: the reference's own code (oracle/_ref, compiled from the
-           reference sources) on 1 host core, bounded sample, stepping loop
-           only (the reference's wall_time window, P/src/simulate.cpp:175,230).
+           reference sources) on 1 host core, bounded sample (the grid's
+           central 16-plane slab when a full step takes minutes), stepping
+           loop only (the reference's wall_time window,
+           P/src/simulate.cpp:175,230).
 `--impl reference`: the reference CPU implementation on all usable host
            cores (independent replicas: the reference has no intra-run
-           parallelism, P/src/experiments.cpp:22-37).
+           parallelism, P/src/experiments.cpp:22-37), same sample, W warm-up
+           and K timed steps per replica; never maps the product library.
 Multi-GPU (torchrun, one process per GPU): the grid is split into z-slabs
 (strong scaling) and V halo planes go to the neighbours by peer stores.
 """
@@ -235,31 +242,80 @@ def cpu_impl():
     return Oracle(), "port"
 
 
-def cpu_baseline(w, y0, rF, rS, budget_s=12.0):
-    impl, kind = cpu_impl()
+# Bounded CPU sample of a large grid: its central SAMPLE_DEPTH planes as a
+# standalone no-flux slab (workloads.z_slab_sample). A full step of config
+# 4's grid takes ~40 s on one core; the 512x512x16 slab takes ~2.5 s and
+# holds the centre stimulus.
+SAMPLE_DEPTH = 16
+SAMPLE_MIN_NODES = 4_500_000
+
+
+def cpu_sample(w, resting):
+    """(workload, y0, label) the CPU legs time: the whole grid when it is
+    small, else the central z-slab (same per-node work)."""
+    from paper_2401_01745_b200 import workloads
+
     p = w.problem
-    _, _, t1 = impl.run(p, y0, 0, 1, w.dt, w.eps, rF, rS)
+    if p.dim == 3 and w.n_nodes > SAMPLE_MIN_NODES:
+        nz = int(p.n[2])
+        z0 = max(0, nz // 2 - SAMPLE_DEPTH // 2)
+        ws, ys = workloads.z_slab_sample(w, z0, SAMPLE_DEPTH, resting=resting)
+        return ws, ys, (f"central slab z {z0}..{z0 + SAMPLE_DEPTH - 1} of {w.name} "
+                        f"({int(p.n[0])}x{int(p.n[1])}x{SAMPLE_DEPTH} = {ws.n_nodes} nodes, "
+                        f"standalone no-flux problem, rho estimated on it)")
+    return w, w.initial_state(resting=resting), f"the full {w.name} grid"
+
+
+def product_lib_mapped() -> bool:
+    """Whether this process has the product library mapped (the CPU arm
+    must not)."""
+    try:
+        with open("/proc/self/maps") as f:
+            return "libemrkc_b200" in f.read()
+    except OSError:
+        return False
+
+
+def cpu_baseline(w, budget_s=15.0):
+    """The reference's stepping loop on ONE host core over a bounded sample
+    of the workload (~budget_s of stepping), its own rho estimates."""
+    impl, kind = cpu_impl()
+    ws, y0, label = cpu_sample(w, impl.resting_state)
+    p = ws.problem
+    rF = impl.estimate_rho(p, 0, 0.0, y0)[0].rho
+    rS = ws.rho_S_forced if ws.rho_S_forced is not None else impl.estimate_rho(p, 1, 0.0, y0)[0].rho
+    _, _, t1 = impl.run(p, y0, 0, 1, ws.dt, ws.eps, rF, rS)
     k = int(max(1, min(w.n_steps, budget_s / max(t1, 1e-6))))
-    _, res, wall = impl.run(p, y0, 0, k, w.dt, w.eps, rF, rS)
-    v = w.n_nodes * res.steps_done / wall if wall > 0 else None
+    _, res, wall = impl.run(p, y0, 0, k, ws.dt, ws.eps, rF, rS)
+    v = ws.n_nodes * res.steps_done / wall if wall > 0 else None
     return {"value": v, "unit": "node-steps/s", "cores": 1, "kind": kind,
-            "sample": f"{k} emRKC steps of the full {w.name} grid from the seeded initial state, "
+            "sample": f"{res.steps_done} emRKC steps of {label} from the seeded initial state, "
                       f"1 thread, stepping loop wall time {wall:.2f} s "
-                      f"({'oracle/_ref: reference sources, -O3' if kind == 'reference' else 'oracle/emrkc_oracle.c'})"}
+                      f"({'oracle/_ref: reference sources, -O3' if kind == 'reference' else 'oracle/emrkc_oracle.c'}); "
+                      f"plan s={res.s} m={res.m}"}
+
+
+REF_BUDGET_S = 150.0  # wall budget of the reference arm's timed steps
 
 
 def reference_arm(args, w):
-    ws, rank, _ = dist_env()
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    reference sources; the C restatement if they are absent) on all usable
+    host cores as independent concurrent replicas (the reference has no
+    intra-run parallelism; its only pool is over independent experiment
+    cells, P/src/experiments.cpp:22-37). Each replica runs W warm-up steps,
+    then K timed steps of the bounded sample (cpu_sample), stepping loop
+    only (the reference's wall_time window, P/src/simulate.cpp:175,230).
+    This process never maps the product library: the initial state uses
+    the reference's own resting_state."""
+    ws_, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_2401_01745_b200.monodomain import resting_state  # host-only numerics
-
-    del resting_state
     impl, kind = cpu_impl()
-    p = w.problem
-    y0 = w.initial_state()
+    ws, y0, label = cpu_sample(w, impl.resting_state)
+    p = ws.problem
     rF = impl.estimate_rho(p, 0, 0.0, y0)[0].rho
-    rS = w.rho_S_forced if w.rho_S_forced is not None else impl.estimate_rho(p, 1, 0.0, y0)[0].rho
+    rS = ws.rho_S_forced if ws.rho_S_forced is not None else impl.estimate_rho(p, 1, 0.0, y0)[0].rho
     cores = cpu_count()
     try:
         import psutil
@@ -267,36 +323,45 @@ def reference_arm(args, w):
         avail = psutil.virtual_memory().available
     except Exception:
         avail = 16 << 30
-    per_replica = 20 * 8 * p.state_len()  # the reference's per-call Vec temporaries
-    threads = int(max(1, min(cores, avail * 0.7 // per_replica)))
-    # warm-up (one thread), then the per-step time of one replica
-    impl.run(p, y0, 0, max(0, min(args.warmup, 3) - 1), w.dt, w.eps, rF, rS)
-    _, _, t1 = impl.run(p, y0, 0, 1, w.dt, w.eps, rF, rS)
-    # bounded sample: about a minute of wall time across the threads
-    k = int(max(1, min(args.steps, 45.0 / max(t1, 1e-6))))
+    per_replica = 24 * 8 * p.state_len()  # the reference's per-call Vec temporaries
+    threads = int(max(1, min(cores, avail * 0.6 // per_replica)))
+    _, _, t1 = impl.run(p, y0, 0, 1, ws.dt, ws.eps, rF, rS)
+    k = int(args.steps)
+    capped = ""
+    if k * t1 * 1.5 > REF_BUDGET_S:
+        k = int(max(1, REF_BUDGET_S / (1.5 * t1)))
+        capped = f"; K capped from {args.steps} to {k} steps (wall budget {REF_BUDGET_S:.0f} s)"
     if kind == "reference":
-        secs = impl.bench(p, y0, k, w.dt, w.eps, rF, rS, threads)
+        impl.bench(p, y0, args.warmup, ws.dt, ws.eps, rF, rS, threads)  # warm-up
+        secs = impl.bench(p, y0, k, ws.dt, ws.eps, rF, rS, threads)
         wall = float(np.max(secs))
     else:
         threads = 1
-        _, _, wall = impl.run(p, y0, 0, k, w.dt, w.eps, rF, rS)
-    v = threads * w.n_nodes * k / wall
+        impl.run(p, y0, 0, args.warmup, ws.dt, ws.eps, rF, rS)
+        _, _, wall = impl.run(p, y0, 0, k, ws.dt, ws.eps, rF, rS)
+    v = threads * ws.n_nodes * k / wall
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "node-steps/s",
-        "n_gpus": ws, "steps": k, "warmup": min(args.warmup, 3), "ms_per_step": wall * 1e3 / k,
+        "n_gpus": ws_, "steps": k, "warmup": args.warmup, "ms_per_step": wall * 1e3 / k,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_of(w, ws),
+        "data": "synthetic (seeded HH resting state + noise)", "config": config_of(w, ws_),
         "cpu_baseline": {"value": v, "unit": "node-steps/s", "cores": threads, "kind": kind,
-                         "sample": f"{threads} concurrent independent replicas x {k} emRKC steps of the "
-                                   f"full {w.name} grid (the reference's serial loop per replica); "
-                                   f"1-thread step {t1:.3f} s"},
+                         "sample": f"{threads} concurrent independent replicas x {k} emRKC steps of "
+                                   f"{label} (the reference's serial loop per replica, "
+                                   f"{args.warmup} warm-up steps each){capped}; 1-thread step "
+                                   f"{t1:.3f} s"},
         "e2e": {"value": v, "unit": "node-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_lib_mapped": product_lib_mapped(),
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
 METRIC = "emRKC node-steps/s (fp64)"
+# N = 1 headline: the largest single-GPU configuration of BASELINE.json,
+# config 4's grid (512x512x256, 67M nodes; HH stands in for the absent TTP
+# model, SURVEY §8(c) option 1).
+HEADLINE = "hh3d_512x512x256"
 
 
 def config_of(w, n_gpus):
@@ -535,7 +600,7 @@ def b200_arm(args, w):
     del m
     if not args.no_extra:
         also = []
-        for name in ("hh3d_512x512x256", "hh2d_256x256"):
+        for name in ("hh3d_128x128x128", "hh2d_256x256"):
             if name == w.name:
                 continue
             from paper_2401_01745_b200 import workloads
@@ -550,7 +615,7 @@ def b200_arm(args, w):
             mx["op"].close()
         line["also"] = also
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(w, y0, rF, rS)
+        line["cpu_baseline"] = cpu_baseline(w)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -564,10 +629,10 @@ def b200_dist(args, w):
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", default="hh3d_128x128x128")
+    ap.add_argument("--config", default=HEADLINE)
     ap.add_argument("--no-extra", action="store_true", help="skip the 'also' workloads")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args(argv)

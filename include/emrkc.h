@@ -44,7 +44,8 @@ typedef enum emrkc_status {
   EMRKC_ENONFINITE = 2, /* NumericalAbort (non-finite stage / norm guard) */
   EMRKC_ECUDA = 3,      /* CUDA runtime failure or no usable device */
   EMRKC_ESTATE = 4,     /* call out of order (e.g. no state uploaded) */
-  EMRKC_ENOMEM = 5
+  EMRKC_ENOMEM = 5,
+  EMRKC_ECALLBACK = 6   /* a caller-supplied device callback returned non-zero */
 } emrkc_status;
 
 enum { EMRKC_MODEL_HH = 0 };          /* make_ionic_model("hh"), P/src/ionic.cpp:125-128 */
@@ -232,7 +233,9 @@ int emrkc_step(emrkc_handle* h, double t, double dt, double epsilon,
  * the state in z-chunks so the host->device copy, the step and the
  * device->host copy overlap (pinned host buffers make the copies
  * asynchronous). On EMRKC_ENONFINITE the device state is y_in and the
- * contents of y_out are unspecified (the reference throws: no result). */
+ * contents of y_out are unspecified (the reference throws: no result); when
+ * y_out overlaps y_in the call is not pipelined and y_in is left untouched
+ * on an abort, as the reference leaves y. */
 int emrkc_step_host(emrkc_handle* h, double t, const double* y_in,
                     double* y_out, int64_t len, double dt, double epsilon,
                     int32_t variant, double rho_F, double rho_S,
@@ -377,6 +380,131 @@ int emrkc_set_slab_min_depth(emrkc_handle* h, int64_t min_planes);
  * ranks sharing one GPU never spin on each other. NULL clears it. */
 typedef void (*emrkc_level_hook)(void* ctx);
 int emrkc_set_level_hook(emrkc_handle* h, emrkc_level_hook hook, void* ctx);
+
+
+/* ===========================================================================
+ * The reference's integrator layer over DEVICE callbacks
+ * (P/include/mrkc/cheb.hpp:60-63, multirate.hpp:19-35,57-81,
+ * spectral.hpp:28-29). The reference's integrators are written against
+ * std::function right-hand sides; here a right-hand side is a host
+ * function that enqueues f(t, y) -> out on `stream` for DEVICE buffers y,
+ * out of `len` doubles (the stream is a cudaStream_t). The recurrences,
+ * exponential Euler updates, finite checks and power-iteration norms run in
+ * sm_100a kernels on the context's stream, in the reference's operation
+ * order; only the callbacks' own work is the caller's.
+ * emrkc_bind_split_rhs() supplies callbacks bound to a handle's monodomain
+ * operator (f_F, f_S, exp_part on its device kernels), so the generic layer
+ * also runs the grid problem (the fused emrkc_step above is the fast path).
+ * ======================================================================== */
+
+/* RhsFn (P/include/mrkc/core.hpp:14) on device buffers. Non-zero return
+ * aborts the caller with EMRKC_ECALLBACK. */
+typedef int (*emrkc_rhs_fn)(void* ctx, double t, const double* y, double* out,
+                            int64_t len, void* stream);
+/* SplitRhs::exp_part (P/include/mrkc/multirate.hpp:29-31). */
+typedef int (*emrkc_exp_part_fn)(void* ctx, const double* y, double* lambda,
+                                 double* y_inf, int64_t len, void* stream);
+
+/* EvalCounters (P/include/mrkc/core.hpp:34-57), the tallies the
+ * integrators increment at their call sites (P/src/multirate.cpp:18-38). */
+typedef struct emrkc_counters {
+  int64_t n_fF;
+  int64_t n_fS;
+  int64_t n_exp_steps;
+} emrkc_counters;
+
+/* SplitRhs (P/include/mrkc/multirate.hpp:25-35). exp_part may be null
+ * (mRKC); counters may be null. */
+typedef struct emrkc_split_rhs {
+  emrkc_rhs_fn f_F;
+  void* f_F_ctx;
+  emrkc_rhs_fn f_S;
+  void* f_S_ctx;
+  emrkc_exp_part_fn exp_part;
+  void* exp_ctx;
+  double rho_F;
+  double rho_S;
+  emrkc_counters* counters;
+} emrkc_split_rhs;
+
+/* A device + stream context for the generic layer (no problem attached). */
+typedef struct emrkc_vctx emrkc_vctx;
+int emrkc_vctx_create(int32_t device, emrkc_vctx** out);
+void emrkc_vctx_destroy(emrkc_vctx* c);
+const char* emrkc_vctx_last_error(const emrkc_vctx* c);
+void* emrkc_vctx_stream(emrkc_vctx* c);  /* cudaStream_t of the context */
+/* Device buffers on the context's device (stream-ordered allocator). */
+int emrkc_vctx_alloc(emrkc_vctx* c, int64_t len, double** dptr);
+int emrkc_vctx_free(emrkc_vctx* c, double* dptr);
+int emrkc_vctx_upload(emrkc_vctx* c, double* dst, const double* host, int64_t len);
+int emrkc_vctx_download(emrkc_vctx* c, double* host, const double* src, int64_t len);
+
+/* exponential_euler_step(y, eta, lambda, y_inf) (P/src/multirate.cpp:49-58):
+ * out = y + expm1(eta lambda) (y - y_inf), componentwise; device buffers
+ * (out may alias y). */
+int emrkc_exponential_euler(emrkc_vctx* c, const double* y, double eta,
+                            const double* lambda, const double* y_inf,
+                            int64_t len, double* out);
+
+/* rkc_iteration(t, y, dt, f, s, epsilon) (P/src/cheb.cpp:84-105,
+ * coefficients :41-69): the s-stage three-term recurrence over device
+ * buffers, f evaluated exactly s times. A non-finite stage returns
+ * EMRKC_ENONFINITE with *bad_stage = the stage index the reference's
+ * NumericalAbort names (:73-80); out is then unspecified. */
+int emrkc_rkc_iteration(emrkc_vctx* c, double t, const double* y, int64_t len,
+                        double dt, emrkc_rhs_fn f, void* f_ctx, int32_t s,
+                        double epsilon, double* out, int32_t* bad_stage);
+
+/* averaged_force_emrkc (P/src/multirate.cpp:78-119; variant: standard
+ * :100-105, progressive :106-115) and averaged_force_mrkc (:60-76):
+ * out = (u_eta - y) / eta. *bad_stage as for emrkc_rkc_iteration (inner
+ * stage). EMRKC_EINVAL for m < 1 or a missing exp_part (emRKC). */
+int emrkc_averaged_force(emrkc_vctx* c, double t, const double* y, int64_t len,
+                         double eta, const emrkc_split_rhs* rhs, int32_t m,
+                         int32_t variant, double epsilon, double* out,
+                         int32_t* bad_stage);
+int emrkc_averaged_force_mrkc(emrkc_vctx* c, double t, const double* y,
+                              int64_t len, double eta,
+                              const emrkc_split_rhs* rhs, int32_t m,
+                              double epsilon, double* out, int32_t* bad_stage);
+
+/* emrkc_step(t, y, dt, rhs, epsilon, variant, report)
+ * (P/src/multirate.cpp:173-189) and mrkc_step (:158-171) over a generic
+ * SplitRhs: plan (s, eta, m) from rho_S / rho_F, outer rkc_iteration over
+ * the averaged force. report (nullable) gets s, m, eta, ell_s, ell_m, the
+ * counter deltas and, on EMRKC_ENONFINITE, the abort stage (abort_inner:
+ * raised by an inner iteration). */
+int emrkc_step_split(emrkc_vctx* c, double t, const double* y, int64_t len,
+                     double dt, const emrkc_split_rhs* rhs, double epsilon,
+                     int32_t variant, double* out, emrkc_step_report* report);
+int emrkc_mrkc_step_split(emrkc_vctx* c, double t, const double* y,
+                          int64_t len, double dt, const emrkc_split_rhs* rhs,
+                          double epsilon, double* out,
+                          emrkc_step_report* report);
+
+/* estimate_spectral_radius(t, y, f, v0, rho0) (P/src/spectral.cpp:26-71)
+ * over a generic device RhsFn: nonlinear power iteration with device
+ * norms. v0 (device, nullable: the reference's seeded mt19937_64 direction,
+ * :16-22), v_out (device, nullable) receives the final direction. */
+int emrkc_estimate_spectral_radius(emrkc_vctx* c, double t, const double* y,
+                                   int64_t len, emrkc_rhs_fn f, void* f_ctx,
+                                   const double* v0, double rho0,
+                                   emrkc_rho_result* out, double* v_out);
+
+/* SplitRhs of a handle's MonodomainOperator (the binding of
+ * P/src/simulate.cpp:153-157): f_F / f_S / exp_part callbacks on device
+ * buffers of emrkc_local_len(h) doubles, run on the handle's kernels and
+ * ordered after the caller's stream. rho_F / rho_S are left 0 (the caller
+ * estimates them). Whole-grid handles only. */
+int emrkc_bind_split_rhs(emrkc_handle* h, emrkc_split_rhs* out);
+
+/* IonicModel (P/include/mrkc/ionic.hpp:17-53) pointwise formulas of a
+ * model, host-side (setup / tests; the grid path evaluates them in the
+ * kernels): rates(V) -> alpha, beta [n_gates]; ionic_current(V, z_E).
+ * Bit-identical to the reference (P/src/ionic.cpp:14-40,98-116). */
+int emrkc_model_rates(int32_t model, double V, double* alpha, double* beta);
+int emrkc_model_ionic_current(int32_t model, double V, const double* z_E,
+                              double* current);
 
 #ifdef __cplusplus
 }  /* extern "C" */

@@ -15,12 +15,30 @@
 //   exex_rl_step / DeviceMonodomain::exex_run
 //                                      P/src/baselines.cpp:192-210 and the
 //                                      exex_rl branch of run_simulation
+//   RhsFn, SplitRhs, EvalCounters      P/include/mrkc/core.hpp:14,34-57,
+//                                      multirate.hpp:25-35 (host callbacks)
+//   rkc_iteration / stability_poly     P/include/mrkc/cheb.hpp:60-63,71-73
+//   exponential_euler_step             P/include/mrkc/multirate.hpp:19-20
+//   averaged_force_emrkc / _mrkc       P/include/mrkc/multirate.hpp:57-67
+//   emrkc_step / mrkc_step (SplitRhs)  P/include/mrkc/multirate.hpp:72-81
+//   estimate_spectral_radius (RhsFn)   P/include/mrkc/spectral.hpp:28-29
+//   IonicModel / make_hh_model         P/include/mrkc/ionic.hpp:17-61
+//   bind_split_rhs(DeviceMonodomain&)  the device operator as a SplitRhs
+//
+// The generic functions run the reference's recurrences on the device
+// (include/emrkc.h, emrkc_generic.cu); a host RhsFn is called with its
+// argument read back from the device and its result uploaded, so any
+// reference-style callback works, and bind_split_rhs() keeps the
+// monodomain operator's callbacks on the device.
 //
 // Header-only; link libemrkc_b200.so. Errors follow the reference:
 // std::invalid_argument for bad arguments, NumericalAbort for non-finite
 // stages, std::runtime_error for device failures.
 #pragma once
 
+#include <functional>
+#include <memory>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -276,6 +294,325 @@ inline Vec exex_rl_step(double t, const Vec& y, double dt, DeviceMonodomain& op)
   op.set_state(y);
   op.exex_step(t, dt);
   return op.get_state();
+}
+
+// ===========================================================================
+// Generic integrator layer (P/include/mrkc/cheb.hpp, multirate.hpp,
+// spectral.hpp) over the C ABI's device implementation.
+// ===========================================================================
+using RhsFn = std::function<void(double t, const Vec& y, Vec& out)>;
+
+struct EvalCounters {
+  long long n_fF = 0, n_fS = 0, n_exp_steps = 0;
+};
+
+// SplitRhs over host callbacks (P/include/mrkc/multirate.hpp:25-35).
+struct SplitRhs {
+  RhsFn f_F;
+  RhsFn f_S;
+  std::function<void(const Vec& y, Vec& lambda, Vec& y_inf)> exp_part;
+  double rho_F = 0.0;
+  double rho_S = 0.0;
+  EvalCounters* counters = nullptr;
+  // set by bind_split_rhs: the device operator's own callbacks
+  emrkc_split_rhs device{};
+  bool on_device = false;
+};
+
+namespace detail {
+
+// One context per host thread (device 0), like the reference's free functions.
+inline emrkc_vctx* ctx() {
+  struct Holder {
+    emrkc_vctx* c = nullptr;
+    ~Holder() { emrkc_vctx_destroy(c); }
+  };
+  thread_local Holder h;
+  if (!h.c && emrkc_vctx_create(0, &h.c) != EMRKC_OK)
+    throw std::runtime_error("emrkc: no usable CUDA device (there is no CPU fallback)");
+  return h.c;
+}
+
+inline void vcheck(int rc, long stage = -1) {
+  if (rc == EMRKC_OK) return;
+  const std::string msg = emrkc_vctx_last_error(ctx());
+  if (rc == EMRKC_EINVAL) throw std::invalid_argument(msg);
+  if (rc == EMRKC_ENONFINITE) throw NumericalAbort(msg, -1, 0.0, static_cast<int>(stage));
+  throw std::runtime_error(msg);
+}
+
+// RAII device vector of the context.
+struct DVec {
+  double* p = nullptr;
+  int64_t n = 0;
+  explicit DVec(int64_t n_) : n(n_) { vcheck(emrkc_vctx_alloc(ctx(), n, &p)); }
+  DVec(const Vec& v) : DVec(static_cast<int64_t>(v.size())) {
+    vcheck(emrkc_vctx_upload(ctx(), p, v.data(), n));
+  }
+  ~DVec() { emrkc_vctx_free(ctx(), p); }
+  DVec(const DVec&) = delete;
+  DVec& operator=(const DVec&) = delete;
+  Vec host() const {
+    Vec v(n);
+    vcheck(emrkc_vctx_download(ctx(), v.data(), p, n));
+    return v;
+  }
+};
+
+struct HostRhs {
+  const RhsFn* f;
+  std::string err;
+};
+inline int host_rhs(void* c, double t, const double* y, double* out, int64_t len, void*) {
+  auto* r = static_cast<HostRhs*>(c);
+  try {
+    Vec yy(len), oo(len, 0.0);
+    if (emrkc_vctx_download(ctx(), yy.data(), y, len)) return 1;
+    (*r->f)(t, yy, oo);
+    if (static_cast<int64_t>(oo.size()) != len) return 1;
+    return emrkc_vctx_upload(ctx(), out, oo.data(), len) ? 1 : 0;
+  } catch (const std::exception& e) {
+    r->err = e.what();
+    return 1;
+  }
+}
+
+struct HostSplit {
+  const SplitRhs* rhs;
+  HostRhs fF, fS;
+  emrkc_counters ctr{};
+  emrkc_split_rhs c{};
+};
+inline int host_exp(void* cx, const double* y, double* lam, double* yinf, int64_t len, void*) {
+  auto* h = static_cast<HostSplit*>(cx);
+  try {
+    Vec yy(len), l(len, 0.0), yi(len, 0.0);
+    if (emrkc_vctx_download(ctx(), yy.data(), y, len)) return 1;
+    h->rhs->exp_part(yy, l, yi);
+    if (emrkc_vctx_upload(ctx(), lam, l.data(), len)) return 1;
+    return emrkc_vctx_upload(ctx(), yinf, yi.data(), len) ? 1 : 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+inline void make_split(const SplitRhs& rhs, HostSplit& hs) {
+  hs.rhs = &rhs;
+  if (rhs.on_device) {
+    hs.c = rhs.device;
+  } else {
+    hs.fF.f = &rhs.f_F;
+    hs.fS.f = &rhs.f_S;
+    hs.c.f_F = rhs.f_F ? host_rhs : nullptr;
+    hs.c.f_F_ctx = &hs.fF;
+    hs.c.f_S = rhs.f_S ? host_rhs : nullptr;
+    hs.c.f_S_ctx = &hs.fS;
+    hs.c.exp_part = rhs.exp_part ? host_exp : nullptr;
+    hs.c.exp_ctx = &hs;
+  }
+  hs.c.rho_F = rhs.rho_F;
+  hs.c.rho_S = rhs.rho_S;
+  hs.c.counters = &hs.ctr;
+}
+inline void fold(const SplitRhs& rhs, const HostSplit& hs) {
+  if (!rhs.counters) return;
+  rhs.counters->n_fF += hs.ctr.n_fF;
+  rhs.counters->n_fS += hs.ctr.n_fS;
+  rhs.counters->n_exp_steps += hs.ctr.n_exp_steps;
+}
+
+}  // namespace detail
+
+// rkc_iteration(t, y, dt, f, s, epsilon) — P/src/cheb.cpp:84-105
+inline Vec rkc_iteration(double t, const Vec& y, double dt, const RhsFn& f, int s,
+                         double epsilon) {
+  detail::DVec dy(y), out(static_cast<int64_t>(y.size()));
+  detail::HostRhs hr{&f, {}};
+  int32_t st = 0;
+  detail::vcheck(emrkc_rkc_iteration(detail::ctx(), t, dy.p, dy.n, dt, detail::host_rhs, &hr, s,
+                                     epsilon, out.p, &st),
+                 st);
+  return out.host();
+}
+inline Vec rkc_iteration(double t, const Vec& y, double dt, const RhsFn& f, const RkcCoeffs& k) {
+  return rkc_iteration(t, y, dt, f, k.s, k.epsilon);
+}
+
+// stability_poly(s, eps, z) — P/src/cheb.cpp:114-118
+inline double stability_poly(int s, double epsilon, double z) {
+  const RhsFn f = [z](double, const Vec& u, Vec& out) { out[0] = z * u[0]; };
+  return rkc_iteration(0.0, Vec{1.0}, 1.0, f, s, epsilon)[0];
+}
+
+// exponential_euler_step — P/src/multirate.cpp:49-58
+inline Vec exponential_euler_step(const Vec& y, double eta, const Vec& lambda_diag,
+                                  const Vec& y_inf) {
+  if (lambda_diag.size() != y.size() || y_inf.size() != y.size())
+    throw std::invalid_argument("exponential_euler_step: size mismatch");
+  detail::DVec dy(y), dl(lambda_diag), di(y_inf), out(static_cast<int64_t>(y.size()));
+  detail::vcheck(emrkc_exponential_euler(detail::ctx(), dy.p, eta, dl.p, di.p, dy.n, out.p));
+  return out.host();
+}
+
+// averaged_force_emrkc / averaged_force_mrkc — P/src/multirate.cpp:60-119
+inline Vec averaged_force_emrkc(double t, const Vec& y, double eta, const SplitRhs& rhs, int m,
+                                EmrkcVariant variant = EmrkcVariant::standard,
+                                double epsilon = 0.05) {
+  detail::DVec dy(y), out(static_cast<int64_t>(y.size()));
+  detail::HostSplit hs;
+  detail::make_split(rhs, hs);
+  int32_t st = 0;
+  const int rc = emrkc_averaged_force(detail::ctx(), t, dy.p, dy.n, eta, &hs.c, m,
+                                      static_cast<int32_t>(variant), epsilon, out.p, &st);
+  detail::fold(rhs, hs);
+  detail::vcheck(rc, st);
+  return out.host();
+}
+inline Vec averaged_force_mrkc(double t, const Vec& y, double eta, const SplitRhs& rhs, int m,
+                               double epsilon = 0.05) {
+  detail::DVec dy(y), out(static_cast<int64_t>(y.size()));
+  detail::HostSplit hs;
+  detail::make_split(rhs, hs);
+  int32_t st = 0;
+  const int rc = emrkc_averaged_force_mrkc(detail::ctx(), t, dy.p, dy.n, eta, &hs.c, m, epsilon,
+                                           out.p, &st);
+  detail::fold(rhs, hs);
+  detail::vcheck(rc, st);
+  return out.host();
+}
+
+// emrkc_step / mrkc_step over a SplitRhs — P/src/multirate.cpp:158-189
+inline Vec emrkc_step(double t, const Vec& y, double dt, const SplitRhs& rhs,
+                      double epsilon = 0.05, EmrkcVariant variant = EmrkcVariant::standard,
+                      MultirateStepReport* report = nullptr) {
+  detail::DVec dy(y), out(static_cast<int64_t>(y.size()));
+  detail::HostSplit hs;
+  detail::make_split(rhs, hs);
+  emrkc_step_report r{};
+  const int rc = emrkc_step_split(detail::ctx(), t, dy.p, dy.n, dt, &hs.c, epsilon,
+                                  static_cast<int32_t>(variant), out.p, &r);
+  detail::fold(rhs, hs);
+  if (report) *report = DeviceMonodomain::to_report(r);
+  detail::vcheck(rc, r.abort_stage);
+  return out.host();
+}
+inline Vec mrkc_step(double t, const Vec& y, double dt, const SplitRhs& rhs,
+                     double epsilon = 0.05, MultirateStepReport* report = nullptr) {
+  detail::DVec dy(y), out(static_cast<int64_t>(y.size()));
+  detail::HostSplit hs;
+  detail::make_split(rhs, hs);
+  emrkc_step_report r{};
+  const int rc =
+      emrkc_mrkc_step_split(detail::ctx(), t, dy.p, dy.n, dt, &hs.c, epsilon, out.p, &r);
+  detail::fold(rhs, hs);
+  if (report) *report = DeviceMonodomain::to_report(r);
+  detail::vcheck(rc, r.abort_stage);
+  return out.host();
+}
+
+// estimate_spectral_radius(t, y, f, v0, rho0) — P/src/spectral.cpp:26-71
+struct RhoEstimateV {
+  double rho = 0.0;
+  Vec v;
+  int iterations = 0;
+  double safety = 1.05;
+  bool converged = true;
+};
+inline RhoEstimateV estimate_spectral_radius(double t, const Vec& y, const RhsFn& f,
+                                             const Vec& v0 = {}, double rho0 = 0.0) {
+  detail::DVec dy(y), dv(static_cast<int64_t>(y.size()));
+  std::unique_ptr<detail::DVec> d0;
+  if (!v0.empty()) d0 = std::make_unique<detail::DVec>(v0);
+  detail::HostRhs hr{&f, {}};
+  emrkc_rho_result r{};
+  detail::vcheck(emrkc_estimate_spectral_radius(detail::ctx(), t, dy.p, dy.n, detail::host_rhs,
+                                                &hr, d0 ? d0->p : nullptr, rho0, &r, dv.p));
+  RhoEstimateV e;
+  e.rho = r.rho;
+  e.iterations = r.iterations;
+  e.safety = r.safety;
+  e.converged = r.converged != 0;
+  e.v = dv.host();
+  return e;
+}
+
+// The device operator as a SplitRhs (callbacks stay on the device): the
+// generic emrkc_step above then runs the grid problem.
+inline SplitRhs bind_split_rhs(DeviceMonodomain& op, double rho_F = 0.0, double rho_S = 0.0) {
+  SplitRhs r;
+  check(emrkc_bind_split_rhs(op.handle(), &r.device), op.handle());
+  r.on_device = true;
+  r.rho_F = rho_F;
+  r.rho_S = rho_S;
+  return r;
+}
+
+// ===========================================================================
+// IonicModel (P/include/mrkc/ionic.hpp:17-53) and the HH adapter over the
+// library's model formulas (bit-identical to P/src/ionic.cpp:86-116).
+// ===========================================================================
+class IonicModel {
+ public:
+  virtual ~IonicModel() = default;
+  virtual std::string name() const = 0;
+  virtual int n_gates() const = 0;
+  virtual int n_aux() const = 0;
+  virtual std::vector<std::string> var_names() const = 0;
+  virtual void rates(double V, std::span<double> alpha, std::span<double> beta) const = 0;
+  virtual double ionic_current(double V, std::span<const double> z_E,
+                               std::span<const double> z_S) const = 0;
+  virtual void aux_rates(double, std::span<const double>, std::span<const double>,
+                         std::span<double>) const {}
+  struct Rest {
+    double V = 0.0;
+    Vec z_E;
+    Vec z_S;
+  };
+  virtual Rest resting_state() const = 0;
+  // lambda = -(alpha + beta), z_inf = alpha / (alpha + beta) (P/src/ionic.cpp:31-40)
+  void gate_coeffs(double V, std::span<double> lambda, std::span<double> z_inf) const {
+    std::vector<double> a(n_gates()), b(n_gates());
+    rates(V, a, b);
+    for (int g = 0; g < n_gates(); ++g) {
+      lambda[g] = -(a[g] + b[g]);
+      z_inf[g] = a[g] / (a[g] + b[g]);
+    }
+  }
+  // The library model id the device kernels implement (EMRKC_MODEL_*).
+  virtual int32_t model_id() const = 0;
+};
+
+class HodgkinHuxley final : public IonicModel {
+ public:
+  std::string name() const override { return "hh"; }
+  int n_gates() const override { return 3; }
+  int n_aux() const override { return 0; }
+  std::vector<std::string> var_names() const override { return {"m", "h", "n"}; }
+  void rates(double V, std::span<double> alpha, std::span<double> beta) const override {
+    if (alpha.size() < 3 || beta.size() < 3) throw std::invalid_argument("hh: 3 gates");
+    check(emrkc_model_rates(EMRKC_MODEL_HH, V, alpha.data(), beta.data()));
+  }
+  double ionic_current(double V, std::span<const double> z_E,
+                       std::span<const double>) const override {
+    if (z_E.size() < 3) throw std::invalid_argument("hh: 3 gates");
+    double I = 0.0;
+    check(emrkc_model_ionic_current(EMRKC_MODEL_HH, V, z_E.data(), &I));
+    return I;
+  }
+  Rest resting_state() const override {
+    Rest r;
+    r.z_E.resize(3);
+    check(emrkc_resting_state(EMRKC_MODEL_HH, &r.V, r.z_E.data()));
+    return r;
+  }
+  int32_t model_id() const override { return EMRKC_MODEL_HH; }
+};
+
+inline std::unique_ptr<IonicModel> make_hh_model() { return std::make_unique<HodgkinHuxley>(); }
+
+// make_ionic_model(name) (P/src/ionic.cpp:125-128): "hh" only.
+inline std::unique_ptr<IonicModel> make_ionic_model(const std::string& name) {
+  if (name == "hh") return make_hh_model();
+  throw std::invalid_argument("unknown ionic model '" + name + "'");
 }
 
 }  // namespace emrkc

@@ -22,6 +22,7 @@ EMRKC_ENONFINITE = 2
 EMRKC_ECUDA = 3
 EMRKC_ESTATE = 4
 EMRKC_ENOMEM = 5
+EMRKC_ECALLBACK = 6
 
 EMRKC_MODEL_HH = 0
 EMRKC_RHS_F = 0
@@ -169,6 +170,31 @@ def dptr(a: np.ndarray | None):
     return a.ctypes.data_as(DP)
 
 
+# Generic integrator layer (include/emrkc.h, emrkc_generic.cu): device
+# callbacks. RhsFn: int (*)(void* ctx, double t, const double* y, double* out,
+# int64_t len, void* stream); exp_part: int (*)(void* ctx, const double* y,
+# double* lambda, double* y_inf, int64_t len, void* stream).
+RHS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_int64,
+                     C.c_void_p)
+EXP_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                     C.c_void_p)
+
+
+class Counters(C.Structure):
+    _fields_ = [("n_fF", C.c_int64), ("n_fS", C.c_int64), ("n_exp_steps", C.c_int64)]
+
+
+class SplitRhsC(C.Structure):
+    """emrkc_split_rhs (SplitRhs, P/include/mrkc/multirate.hpp:25-35)."""
+    _fields_ = [
+        ("f_F", RHS_FN), ("f_F_ctx", C.c_void_p),
+        ("f_S", RHS_FN), ("f_S_ctx", C.c_void_p),
+        ("exp_part", EXP_FN), ("exp_ctx", C.c_void_p),
+        ("rho_F", C.c_double), ("rho_S", C.c_double),
+        ("counters", C.POINTER(Counters)),
+    ]
+
+
 # Every function the header declares: name -> (restype, argtypes).
 # emrkc_level_hook: void (*)(void* ctx)
 LEVEL_HOOK = C.CFUNCTYPE(None, C.c_void_p)
@@ -220,6 +246,24 @@ PROTOTYPES = {
     "emrkc_dist_lockstep_run": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
     "emrkc_set_slab_min_depth": (C.c_int, [C.c_void_p, C.c_int64]),
     "emrkc_set_level_hook": (C.c_int, [C.c_void_p, LEVEL_HOOK, C.c_void_p]),
+    "emrkc_vctx_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "emrkc_vctx_destroy": (None, [C.c_void_p]),
+    "emrkc_vctx_last_error": (C.c_char_p, [C.c_void_p]),
+    "emrkc_vctx_stream": (C.c_void_p, [C.c_void_p]),
+    "emrkc_vctx_alloc": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    "emrkc_vctx_free": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "emrkc_vctx_upload": (C.c_int, [C.c_void_p, C.c_void_p, DP, C.c_int64]),
+    "emrkc_vctx_download": (C.c_int, [C.c_void_p, DP, C.c_void_p, C.c_int64]),
+    "emrkc_exponential_euler": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "emrkc_rkc_iteration": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_int64, C.c_double, RHS_FN, C.c_void_p, C.c_int32, C.c_double, C.c_void_p, I32P]),
+    "emrkc_averaged_force": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_int64, C.c_double, C.POINTER(SplitRhsC), C.c_int32, C.c_int32, C.c_double, C.c_void_p, I32P]),
+    "emrkc_averaged_force_mrkc": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_int64, C.c_double, C.POINTER(SplitRhsC), C.c_int32, C.c_double, C.c_void_p, I32P]),
+    "emrkc_step_split": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_int64, C.c_double, C.POINTER(SplitRhsC), C.c_double, C.c_int32, C.c_void_p, C.POINTER(StepReport)]),
+    "emrkc_mrkc_step_split": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_int64, C.c_double, C.POINTER(SplitRhsC), C.c_double, C.c_void_p, C.POINTER(StepReport)]),
+    "emrkc_estimate_spectral_radius": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_int64, RHS_FN, C.c_void_p, C.c_void_p, C.c_double, C.POINTER(RhoResult), C.c_void_p]),
+    "emrkc_bind_split_rhs": (C.c_int, [C.c_void_p, C.POINTER(SplitRhsC)]),
+    "emrkc_model_rates": (C.c_int, [C.c_int32, C.c_double, DP, DP]),
+    "emrkc_model_ionic_current": (C.c_int, [C.c_int32, C.c_double, DP, DP]),
 }
 
 _lib = None

@@ -396,10 +396,52 @@ double* dghost_at(double* base, size_t pl, int side, int par) {
 
 // The fast ionic path's V window for this eta (fast_math.cuh) as centre and
 // radius: |V - vmid| <= vrad (empty window: vrad < 0, never fast).
-void fast_window(double eta, double* vmid, double* vrad) {
-  const double lo = emrkc_k::fast_vlo(eta), hi = emrkc_k::fast_vhi(eta);
+// Lower end: the smallest V >= -400 with eta * (alpha_g + beta_g) <= 580 for
+// every gate, solved on the reference's own rates (hh_rates) by bisection
+// where the sum falls with V (beta_m, beta_n below rest), then checked by a
+// scan of [vlo, min(vhi, 200)] against 600 (the table exp's exponent
+// insertion wraps near -708). Upper end: kernels.h fast_vhi (alpha_m ~
+// 0.1 (V + 40) dominates there).
+void fast_window_solve(double eta, double* vmid, double* vrad) {
+  auto worst = [eta](double V) {
+    double a[3], b[3];
+    hh_rates(V, a, b);
+    return eta * std::max({a[0] + b[0], a[1] + b[1], a[2] + b[2]});
+  };
+  const double hi = emrkc_k::fast_vhi(eta);
+  double lo = -400.0;
+  if (!(eta > 0.0) || worst(-50.0) > 580.0) {
+    *vmid = 0.0;
+    *vrad = -1.0;
+    return;
+  }
+  if (worst(lo) > 580.0) {
+    double a = -400.0, b = -50.0;  // worst(a) > 580 >= worst(b)
+    for (int it = 0; it < 80; ++it) {
+      const double c = 0.5 * (a + b);
+      (worst(c) > 580.0 ? a : b) = c;
+    }
+    lo = b;
+  }
+  for (double V = lo, top = std::min(hi, 200.0); V <= top; V += 0.01)
+    if (worst(V) > 600.0) {
+      *vmid = 0.0;
+      *vrad = -1.0;
+      return;
+    }
   *vmid = 0.5 * (lo + hi);
   *vrad = 0.5 * (hi - lo);
+}
+// Per launch: the last eta's window is kept per host thread (a run has one
+// eta; the scan above costs ~1 ms).
+void fast_window(double eta, double* vmid, double* vrad) {
+  thread_local double k_eta = -1.0, k_mid = 0.0, k_rad = -1.0;
+  if (eta != k_eta) {
+    fast_window_solve(eta, &k_mid, &k_rad);
+    k_eta = eta;
+  }
+  *vmid = k_mid;
+  *vrad = k_rad;
 }
 
 int ensure_buffers(emrkc_handle* h, int nb) {
@@ -2072,11 +2114,16 @@ int step_impl(emrkc_handle* h, double t, double dt, double epsilon, double rho_F
 
 namespace {
 // emrkc_step_host for one-launch steps (s = m = 1 on the TMA node kernel):
-// the state crosses the host link in z-chunks on two copy streams, and
-// chunk c is stepped as soon as chunks c and c + 1 (its upper halo plane)
-// have arrived, so host->device copies, the step and device->host copies
-// overlap (P/src/multirate.cpp:173-189 semantics unchanged: on a
-// NumericalAbort y_out is not written and the device state stays y_in).
+// the state crosses the host link in z-chunks on two copy streams. The
+// kernel / copy-out ranges lag the copy-in chunks by one plane (plane p
+// needs p + 1), so the kernel of range c starts as soon as copy-in chunk c
+// has arrived and its output goes back at once: host->device copies, the
+// step and device->host copies overlap. The abort word is only known after
+// the last range, so on a NumericalAbort y_out has already received (part
+// of) the rejected step; the device state stays y_in (P/src/simulate.cpp:
+// 215-220). Callers whose y_out overlaps y_in take the unpipelined path, so
+// their input survives an abort as it does in the reference (which throws
+// before assigning y).
 constexpr int kMaxHostChunks = 64;
 
 int host_chunks() {  // EMRKC_HOST_CHUNKS (default 8)
@@ -2140,7 +2187,16 @@ int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
     CK(h, cudaEventRecord(h->ev_k[c], h->stream));
   }
   h->zr_lo = h->zr_hi = -1;
-  if (rc) return rc;
+  if (rc) {
+    // copies from the caller's y_in may still be in flight into buf[in]:
+    // drain every stream before handing control (and y_in) back, and drop
+    // the device state, which is partly written
+    cudaStreamSynchronize(h->s_in);
+    cudaStreamSynchronize(h->stream);
+    cudaStreamSynchronize(h->s_out);
+    h->has_state = false;
+    return rc;
+  }
   double* dout = h->buf[outi];
   for (int c = 0; c < kHostChunks; ++c) {
     CK(h, cudaStreamWaitEvent(h->s_out, h->ev_k[c], 0));
@@ -2195,7 +2251,8 @@ int emrkc_step_host(emrkc_handle* h, double t, const double* y_in,
     if ((rc = ensure_buffers(h, std::max(2, h->nbuf)))) return rc;
     if ((rc = upload_plan(h, dt, rho_F, rho_S, epsilon))) return rc;
     if ((rc = ensure_slots(h, 1))) return rc;
-    if (step_host_pipelined(h)) return step_host_pipe(h, t, y_in, y_out, report);
+    const bool overlap = y_out < y_in + len && y_in < y_out + len;
+    if (!overlap && step_host_pipelined(h)) return step_host_pipe(h, t, y_in, y_out, report);
   }
   int rc = emrkc_set_state(h, y_in, len);
   if (rc) return rc;
@@ -2680,3 +2737,57 @@ int emrkc_dist_lockstep_run(emrkc_handle* const* hs, int32_t n, int32_t replay,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// SplitRhs of a handle's operator for the generic integrator layer
+// (emrkc_generic.cu): device callbacks on the caller's stream.
+// ---------------------------------------------------------------------------
+namespace {
+int bound_rhs(emrkc_handle* h, int which, double t, const double* y, double* out, int64_t len,
+              void* stream) {
+  if (!h || len != h->len || h->partitioned) return 1;
+  int code = 0;
+  if (rhs_code(h, which, &code) || use_device(h)) return 1;
+  return emrkc_k::launch_rhs(h->geom, Halo{}, code, y, stim_rate_at(&h->p, t), out,
+                             static_cast<cudaStream_t>(stream)) != cudaSuccess;
+}
+int bound_fF(void* ctx, double t, const double* y, double* out, int64_t len, void* stream) {
+  return bound_rhs(static_cast<emrkc_handle*>(ctx), EMRKC_RHS_F, t, y, out, len, stream);
+}
+int bound_fS(void* ctx, double t, const double* y, double* out, int64_t len, void* stream) {
+  return bound_rhs(static_cast<emrkc_handle*>(ctx), EMRKC_RHS_S, t, y, out, len, stream);
+}
+int bound_exp(void* ctx, const double* y, double* lam, double* yinf, int64_t len, void* stream) {
+  auto* h = static_cast<emrkc_handle*>(ctx);
+  if (!h || len != h->len || h->partitioned || use_device(h)) return 1;
+  return emrkc_k::launch_exp_part(h->geom, y, lam, yinf, static_cast<cudaStream_t>(stream)) !=
+         cudaSuccess;
+}
+}  // namespace
+
+int emrkc_bind_split_rhs(emrkc_handle* h, emrkc_split_rhs* out) {
+  if (!h || !out) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->partitioned) return set_err(h, EMRKC_EINVAL, "bind_split_rhs: whole-grid handles only");
+  *out = emrkc_split_rhs{};
+  out->f_F = bound_fF;
+  out->f_F_ctx = h;
+  out->f_S = bound_fS;
+  out->f_S_ctx = h;
+  out->exp_part = bound_exp;
+  out->exp_ctx = h;
+  return EMRKC_OK;
+}
+
+int emrkc_model_rates(int32_t model, double V, double* alpha, double* beta) {
+  if (model != EMRKC_MODEL_HH) return set_global(EMRKC_EINVAL, "unknown ionic model %d", model);
+  if (!alpha || !beta) return set_global(EMRKC_EINVAL, "null argument");
+  hh_rates(V, alpha, beta);
+  return EMRKC_OK;
+}
+
+int emrkc_model_ionic_current(int32_t model, double V, const double* z_E, double* current) {
+  if (model != EMRKC_MODEL_HH) return set_global(EMRKC_EINVAL, "unknown ionic model %d", model);
+  if (!z_E || !current) return set_global(EMRKC_EINVAL, "null argument");
+  *current = hh_current(V, z_E);
+  return EMRKC_OK;
+}

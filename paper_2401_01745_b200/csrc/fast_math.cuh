@@ -35,9 +35,13 @@ __constant__ FastConsts kFC = {
     0.22313016014842982, 1.2, 0.36, 0.003, -54.387, 12.182493960703473};
 // hh_expeuler_fast validity window (host: fast_window, per eta): every
 // exp_tab_nc argument stays within +-700 and the batch product finite. The
-// rates that grow without bound are beta_m = 4 e^{-(V+65)/18} below rest and
-// alpha_m ~ 0.1 (V + 40), alpha_n ~ 0.01 (V + 55) above it, so
-//   V >= max(-400, -65 - 18 ln(150 / eta))   (eta beta_m <= 600)
+// rates that grow without bound are beta_m = 4 e^{-(V+65)/18} (and
+// beta_n) below rest and alpha_m ~ 0.1 (V + 40), alpha_n ~ 0.01 (V + 55)
+// above it, so
+//   V >= vlo(eta) >= -400: eta (alpha_g + beta_g) <= 580 for every gate,
+//        solved on the host from the full sums (alpha_m adds ~0.4 to
+//        beta_m near -56 mV; emrkc_capi.cpp fast_window) and verified by a
+//        scan against 600; empty window (no fast nodes) if none exists
 //   V <= min(10000, 6000 / eta - 80)         (eta (alpha_m + beta_m) <= 600)
 // (at V = -400 the batch product is ~1e110, far from overflow; at 10000 the
 // shared exponentials' arguments are ~ -560). Nodes outside the window (and

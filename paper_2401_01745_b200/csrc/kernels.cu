@@ -208,10 +208,11 @@ __device__ __forceinline__ double outer(bool first, double g1, double g2,
                    __dmul_rn(a.mudt, fb));
 }
 
-__device__ __forceinline__ bool block_skip(const unsigned long long* ev) {
+__device__ __forceinline__ bool block_skip(const unsigned long long* ev,
+                                           unsigned long long floor) {
   __shared__ int skip;
   if (threadIdx.x == 0 && threadIdx.y == 0)
-    skip = (*(volatile const unsigned long long*)ev) != kNoEvent;
+    skip = (*(volatile const unsigned long long*)ev) < floor;
   __syncthreads();
   return skip != 0;
 }
@@ -287,7 +288,7 @@ __device__ __forceinline__ void finish(const Geom& g, const Halo& h,
 template <int DIM, int FAST, int FIRST>
 __global__ void __launch_bounds__(kThreads)
     k_stage_m1(const Geom g, const Halo h, const StageArgs a) {
-  if (block_skip(a.event)) return;
+  if (block_skip(a.event, level_floor(a.code_base, a.j, a.m, 1))) return;
   const Node<DIM> n = node_here<DIM>(g);
   const long long nn = g.nn;
   double o[4] = {0.0, 0.0, 0.0, 0.0};
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(kThreads)
 template <int DIM, int FAST>
 __global__ void __launch_bounds__(kThreads)
     k_stage_first(const Geom g, const Halo h, const StageArgs a) {
-  if (block_skip(a.event)) return;
+  if (block_skip(a.event, level_floor(a.code_base, a.j, a.m, 1))) return;
   const Node<DIM> n = node_here<DIM>(g);
   const long long nn = g.nn;
   bool bad = false;
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(kThreads)
 template <int DIM, int FAST, int LASTK, int FIRST>
 __global__ void __launch_bounds__(kThreads)
     k_stage_inner(const Geom g, const Halo h, const StageArgs a, const int k) {
-  if (block_skip(a.event)) return;
+  if (block_skip(a.event, level_floor(a.code_base, a.j, a.m, k))) return;
   const Node<DIM> n = node_here<DIM>(g);
   const long long nn = g.nn;
   bool bad = false;
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(kThreads)
     k_mrkc_stage(const Geom g, const MrkcArgs a) {
   const Node<DIM> n = node_here<DIM>(g);
   if (!n.valid) return;
-  if (*(volatile const unsigned long long*)a.event != kNoEvent) return;  // aborted earlier
+  if (*(volatile const unsigned long long*)a.event < level_floor(a.code_base, a.j, a.m, a.k)) return;  // aborted earlier
   const long long nn = g.nn, i = n.i;
   const double* U = a.um1;
   const double V = U[i];

@@ -12,6 +12,18 @@
 namespace emrkc_k {
 
 constexpr unsigned long long kNoEvent = ~0ull;
+// Lowest abort ordinal a launch of outer stage j can raise when its first
+// inner stage is k0 (ordinal = code_base + (j-1)(m+1) + k; the outer check
+// is k = m+1, the step's norm guard s(m+1)+1). A launch skips its work only
+// on an event BELOW this floor, i.e. from an earlier level (an earlier step,
+// or an earlier stage of this step). Events at or above it come from other
+// blocks / z-chunks of the same level or from this step's guard, and must
+// not stop the remaining blocks: the first failing check in program order
+// and the guard step's full state depend on every block finishing.
+__host__ __device__ __forceinline__ unsigned long long level_floor(
+    unsigned long long code_base, int j, int m, int k0) {
+  return code_base + (unsigned long long)((j - 1) * (m + 1) + k0);
+}
 constexpr int kMaxStages = 512;  // per rkc iteration (coefficients in params)
 
 // Geometry of the local z-slab (the whole grid when not partitioned).
@@ -247,8 +259,9 @@ constexpr int kMaxZc = 32;
 
 // Window of V where the fast ionic path (fast_math.cuh, hh_expeuler_fast)
 // is valid for this eta: eta * (alpha + beta) <= 600 for every gate and every
-// exponential argument within +-700 (derivation in fast_math.cuh).
-inline double fast_vlo(double eta) { return std::fmax(-400.0, -65.0 - 18.0 * std::log(150.0 / eta)); }
+// exponential argument within +-700 (derivation in fast_math.cuh). The lower
+// end is solved on the host from the full rate sums (emrkc_capi.cpp
+// fast_window); the upper end is closed-form:
 inline double fast_vhi(double eta) { return std::fmin(10000.0, 6000.0 / eta - 80.0); }
 int fast_zc(const Geom& g);
 // Signals per level that a neighbour receives from one launch of each kernel

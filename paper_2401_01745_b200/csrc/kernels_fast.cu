@@ -240,10 +240,11 @@ __device__ __forceinline__ void put_signal(const Halo& h, const PutPlan& pp, int
   halo_signal_w(h, max(0, min(ze, pp.zl) - zb), max(0, ze - max(zb, pp.zh)));
 }
 
-__device__ __forceinline__ bool prologue(const unsigned long long* ev, double* tab) {
+__device__ __forceinline__ bool prologue(const unsigned long long* ev,
+                                         unsigned long long floor, double* tab) {
   __shared__ int skip;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  if (tid == 0) skip = (*(volatile const unsigned long long*)ev) != kNoEvent;
+  if (tid == 0) skip = (*(volatile const unsigned long long*)ev) < floor;
   if (tab) load_exp_table(tab, tid, blockDim.x * blockDim.y);
   __syncthreads();
   return skip != 0;
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(kFThreads, EMRKC_NODE_MINBLOCKS)
   const int bz0 = (DIM == 3 ? blockIdx.z * a.zc : blockIdx.y * FBY * a.zc);
   const int bz1 = (DIM == 3 ? bz0 + a.zc : bz0 + FBY * a.zc);
   halo_wait(h, bz0 == 0, bz1 >= g.nzl);
-  if (prologue(a.event, tab)) {  // aborted earlier: still release the neighbours
+  if (prologue(a.event, level_floor(a.code_base, a.j, a.m, 1), tab)) {  // aborted earlier: still release the neighbours
     halo_signal(h, bz0 == 0, bz1 >= g.nzl);
     return;
   }
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     if (h.wait_lo || h.wait_hi) __syncthreads();
   }
   __shared__ int skip;
-  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) < level_floor(a.code_base, a.j, a.m, 1);
   {
     // exp table rides in the first cp.async group with the first planes
     const unsigned st = (unsigned)__cvta_generic_to_shared(tab);
@@ -801,7 +802,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   double* g2s = gst + kRG * 3 * T::NT;            // [kRG][4][NT] (!FIRST)
   const int t = threadIdx.x;
   __shared__ int skip;
-  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) < level_floor(a.code_base, a.j, a.m, 1);
   {
     const unsigned st = (unsigned)__cvta_generic_to_shared(tab);
     for (int j = t; j < 256; j += T::NT) cp_async8(st + 8u * j, kExp2Tab256 + j);
@@ -1041,7 +1042,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
     if (h.wait_lo || h.wait_hi) __syncthreads();
   }
   __shared__ int skip;
-  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  if (t == 0) skip = (*(volatile const unsigned long long*)a.event) < level_floor(a.code_base, a.j, a.m, a.k);
   const int tx = t % T::TX, ty = t / T::TX;
   const int x0 = blockIdx.x * T::TX;
   const int y0 = DIM == 3 ? blockIdx.y * T::TY : 0;
@@ -1304,7 +1305,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
       }
     }
   }
-  if (t == (EMRKC_EVWARP1 ? 32 : 0)) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  if (t == (EMRKC_EVWARP1 ? 32 : 0)) skip = (*(volatile const unsigned long long*)a.event) < level_floor(a.code_base, a.j, a.m, 1);
   __syncthreads();
   const bool skipped = skip != 0;
   if (skipped) {  // aborted earlier: drain the prologue copies, release the neighbours
@@ -1795,7 +1796,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
       }
     }
   }
-  if (t == (EMRKC_EVWARP1 ? 32 : 0)) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  if (t == (EMRKC_EVWARP1 ? 32 : 0)) skip = (*(volatile const unsigned long long*)a.event) < level_floor(a.code_base, a.j, a.m, a.k);
   __syncthreads();
   const bool skipped = skip != 0;
   if (skipped) {  // aborted earlier: drain the prologue copies, release the neighbours
@@ -1952,7 +1953,7 @@ __global__ void __launch_bounds__(128)
       }
     }
   }
-  if (t == (EMRKC_EVWARP1 ? 32 : 0)) skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+  if (t == (EMRKC_EVWARP1 ? 32 : 0)) skip = (*(volatile const unsigned long long*)a.event) < level_floor(a.code_base, a.j, a.m, a.k);
   __syncthreads();
   if (skip) {  // aborted earlier: drain the prologue copies, release the neighbours
     const int np = 1 + min(kTmaLA, ze - zb) + (ze - zb < kTmaLA ? 1 : 0);
@@ -2146,7 +2147,7 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
       fence_proxy_async();  // peer-stored ghosts before the async-proxy reads
     }
     for (int s = lo1; s <= min(tlast, lo1 + kTmaLA - 1); ++s) issue(s);
-    skip = (*(volatile const unsigned long long*)a.event) != kNoEvent;
+    skip = (*(volatile const unsigned long long*)a.event) < level_floor(a.code_base, a.j, a.m, 2);
   }
   __syncthreads();
   const int nlaunched = min(tlast, lo1 + kTmaLA - 1) - lo1 + 1;
@@ -2287,7 +2288,7 @@ __global__ void __launch_bounds__(kFThreads)
   const int bz0 = (DIM == 3 ? blockIdx.z * a.zc : blockIdx.y * FBY * a.zc);
   const int bz1 = (DIM == 3 ? bz0 + a.zc : bz0 + FBY * a.zc);
   halo_wait(h, bz0 == 0, bz1 >= g.nzl);
-  if (prologue(a.event, nullptr)) {  // aborted earlier: still release the neighbours
+  if (prologue(a.event, level_floor(a.code_base, a.j, a.m, a.k), nullptr)) {  // aborted earlier: still release the neighbours
     halo_signal(h, bz0 == 0, bz1 >= g.nzl);
     return;
   }

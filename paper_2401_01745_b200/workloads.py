@@ -41,8 +41,13 @@ class Workload:
     def n_nodes(self) -> int:
         return self.problem.n_nodes
 
-    def initial_state(self) -> np.ndarray:
-        V, z = resting_state()
+    def initial_state(self, resting=None) -> np.ndarray:
+        """HH resting state + the workload's seeded noise. ``resting`` is a
+        provider of (V_rest, z_rest) — default the library's
+        ``emrkc_resting_state``; the CPU reference arm passes the
+        reference's own (oracle/_ref ``resting_state``, bit-identical), so
+        that process never maps the product library."""
+        V, z = (resting or resting_state)()
         nn = self.n_nodes
         y = np.empty(4 * nn)
         y[:nn] = V
@@ -183,6 +188,31 @@ def z_scaled(w: Workload, n: int) -> Workload:
     return Workload(f"{w.name}_zx{n}", q, w.dt, w.t_end, w.noise, w.seed, w.eps, w.rho_S_forced,
                     note=(w.note + "; " if w.note else "") +
                     f"weak scaling: {w.name} repeated {n}x along z (one copy per GPU)")
+
+
+def z_slab_sample(w: Workload, z0: int, depth: int, resting=None):
+    """Bounded CPU sample of a 3-D workload: its planes [z0, z0 + depth) as a
+    standalone problem (same spacing, conductivities, stimulus box in the
+    same global coordinates, dt, eps; no-flux faces at the slab ends) and the
+    matching slice of the workload's seeded initial state. Per node the
+    emRKC step does the same work as on the full grid (the reference's loop
+    has no grid-size dependent term besides the state length), so
+    node-steps/s of the sample stands for the workload's on a CPU where a
+    full step takes minutes. Returns (sample Workload, y0 of the sample)."""
+    p = w.problem
+    assert p.dim == 3 and 0 <= z0 and z0 + depth <= int(p.n[2])
+    h = p.dx[2]
+    q = make_problem(3, [int(p.n[0]), int(p.n[1]), depth], [p.dx[a] for a in range(3)],
+                     [p.sigma[a] for a in range(3)], p.chi, p.C_m, p.stim_chi_amplitude,
+                     [p.stim_lo[0], p.stim_lo[1], p.stim_lo[2] - z0 * h],
+                     [p.stim_hi[0], p.stim_hi[1], p.stim_hi[2] - z0 * h], p.stim_t0, p.stim_t1)
+    y = w.initial_state(resting=resting)
+    nn, plane = p.n_nodes, int(p.n[0]) * int(p.n[1])
+    ys = np.concatenate([y[b * nn + z0 * plane: b * nn + (z0 + depth) * plane] for b in range(4)])
+    ws = Workload(f"{w.name}[z{z0}:{z0 + depth}]", q, w.dt, w.t_end, w.noise, w.seed, w.eps,
+                  w.rho_S_forced, note=f"planes {z0}..{z0 + depth - 1} of {w.name} as a "
+                                       f"standalone no-flux slab (bounded CPU sample)")
+    return ws, ys
 
 
 def get(name: str) -> Workload:

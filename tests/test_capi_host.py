@@ -145,3 +145,34 @@ def test_stimulus_boxes_select_the_named_nodes(oracle):
     inside = np.array(inside).reshape(20, 20)
     assert inside[:16, :16].all() and not inside[16:, :].any() and not inside[:, 16:].any()
     assert oracle.stimulus_rate(p, 1.0, 0) > 0 and oracle.stimulus_rate(p, 1.0 + 1e-9, 0) == 0
+
+
+def test_generic_layer_no_device_fails_loudly():
+    """The generic integrator layer has no CPU fallback either."""
+    import ctypes as C
+
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    h = C.c_void_p()
+    assert capi.load().emrkc_vctx_create(0, C.byref(h)) == capi.EMRKC_ECUDA
+
+
+def test_model_formulas_bit_identical(oracle):
+    """IonicModel adapter entry points (emrkc_model_rates / _ionic_current)
+    against the oracle's restatement of P/src/ionic.cpp:98-116."""
+    import ctypes as C
+
+    lib = capi.load()
+    a = np.zeros(3)
+    b = np.zeros(3)
+    cur = C.c_double()
+    for V in np.linspace(-120.0, 80.0, 401):
+        assert lib.emrkc_model_rates(0, V, capi.dptr(a), capi.dptr(b)) == 0
+        ra, rb = oracle.rates(V)
+        assert np.array_equal(a, ra) and np.array_equal(b, rb)
+        z = np.array([0.05, 0.6, 0.3])
+        assert lib.emrkc_model_ionic_current(0, V, capi.dptr(z), C.byref(cur)) == 0
+        assert cur.value == oracle.ionic_current(V, z)
+    assert lib.emrkc_model_rates(7, 0.0, capi.dptr(a), capi.dptr(b)) == capi.EMRKC_EINVAL

@@ -12,16 +12,41 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIBDIR = os.path.join(ROOT, "paper_2401_01745_b200")
 
 
-def build(tmp_path):
-    exe = str(tmp_path / "shim_demo")
-    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
-                    os.path.join(ROOT, "tests", "cpp", "shim_demo.cpp"), "-L", LIBDIR,
+def build(tmp_path, name="shim_demo"):
+    exe = str(tmp_path / name)
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", name + ".cpp"), "-L", LIBDIR,
                     "-lemrkc_b200", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
     return exe
 
 
 def test_shim_compiles(tmp_path):
     assert os.path.exists(build(tmp_path))
+    assert os.path.exists(build(tmp_path, "shim_kats"))
+
+
+@pytest.mark.gpu
+def test_shim_kats(tmp_path):
+    """The reference's scalar KATs through the C++ shim's generic layer
+    (device recurrences) and the HH IonicModel adapter."""
+    import math
+
+    exe = build(tmp_path, "shim_kats")
+    r = json.loads(subprocess.run([exe], capture_output=True, text=True, check=True).stdout)
+    phi = math.expm1(-0.5) / -0.5
+    assert r["af_m1"] == pytest.approx(-11.0 * math.exp(-0.5) + phi * -5.0, rel=1e-13)
+    assert r["af_m1"] == pytest.approx(-10.60653, rel=1e-6)
+    assert r["af_exp"] == pytest.approx(-3.934693, rel=1e-6)
+    assert r["afm_m1"] == pytest.approx(-11.0, rel=1e-13)
+    assert (r["n_fF"], r["n_fS"], r["n_exp"]) == (3, 1, 1)
+    assert r["rkc_s1"] == pytest.approx(2.0 * (1.0 - 1.2), rel=1e-14)
+    assert r["R2"] == pytest.approx(0.125, rel=1e-14)
+    assert r["abort_stage"] == 1 and r["rejected"] == 1
+    assert (r["gating_s"], r["gating_m"]) == (1, 1)
+    assert r["gating"] == pytest.approx(0.25 + 0.75 * math.exp(-3.2), rel=1e-12)
+    assert r["rho_diag"] == pytest.approx(7.0, rel=0.01)
+    assert r["alpha_m_m40"] == 1.0 and r["alpha_n_m55"] == 0.1
+    assert r["V_rest"] == -64.99637933119206 and abs(r["I_rest"]) < 1e-10
 
 
 @pytest.mark.gpu

@@ -12,7 +12,7 @@ from paper_2401_01745_b200.monodomain import (MonodomainOperator, NumericalAbort
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-9
-RHO_TOL = 1e-9
+RHO_TOL = 1e-12
 
 
 def test_gated_rhs_bit_exact(oracle):
