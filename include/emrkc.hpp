@@ -428,9 +428,9 @@ inline Vec rkc_iteration(double t, const Vec& y, double dt, const RhsFn& f, int 
   detail::DVec dy(y), out(static_cast<int64_t>(y.size()));
   detail::HostRhs hr{&f, {}};
   int32_t st = 0;
-  detail::vcheck(emrkc_rkc_iteration(detail::ctx(), t, dy.p, dy.n, dt, detail::host_rhs, &hr, s,
-                                     epsilon, out.p, &st),
-                 st);
+  const int rc = emrkc_rkc_iteration(detail::ctx(), t, dy.p, dy.n, dt, detail::host_rhs, &hr, s,
+                                     epsilon, out.p, &st);
+  detail::vcheck(rc, st);
   return out.host();
 }
 inline Vec rkc_iteration(double t, const Vec& y, double dt, const RhsFn& f, const RkcCoeffs& k) {

@@ -888,6 +888,8 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.s = pl.s;
       f.last = a.last;
       f.zc = h->zc;
+      f.z_lo = h->zr_lo >= 0 ? h->zr_lo : 0;  // plane range (pipelined host step)
+      f.z_hi = h->zr_lo >= 0 ? h->zr_hi : h->geom.nzl;
       f.code_base = a.code_base;
       f.event = a.event;
       if (h->pipe == 3) {
@@ -1469,6 +1471,14 @@ int exchange_planes(const std::vector<emrkc_handle*>& hs,
   return EMRKC_OK;
 }
 
+bool rho_serial() {
+  static const bool on = [] {
+    const char* e = std::getenv("EMRKC_RHO_SERIAL");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
 // estimate_spectral_radius (P/src/spectral.cpp:26-71) over a list of slabs
 // (one whole-grid handle is the common case). Norms are sums of per-slab
 // deterministic device reductions.
@@ -1496,14 +1506,36 @@ int power_iteration(const std::vector<emrkc_handle*>& hs, int which, double t,
   auto cleanup = [&]() {
     for (size_t r = 0; r < n; ++r) power_free(hs[r], &w[r]);
   };
+  // ||x||^2 in the reference's serial order (P/src/spectral.cpp:10-14) over
+  // the global vector: SoA block by block, slabs in z order within a block,
+  // the running sum chained from piece to piece. Bit-identical to the
+  // reference, so q, z, f(z) - f(y) and rho are too (EMRKC_RHO_SERIAL=0:
+  // the deterministic parallel reduction instead, ~1e-12 relative).
   auto sum_norm2 = [&](auto field_of) -> double {
     double tot = 0.0;
-    for (size_t r = 0; r < n; ++r) {
-      double part = 0.0;
-      rc = norm2sq(hs[r], field_of(r), hs[r]->len, &part);
-      if (rc) return 0.0;
-      tot += part;
+    if (!rho_serial()) {
+      for (size_t r = 0; r < n; ++r) {
+        double part = 0.0;
+        rc = norm2sq(hs[r], field_of(r), hs[r]->len, &part);
+        if (rc) return 0.0;
+        tot += part;
+      }
+      return tot;
     }
+    for (int b = 0; b < 4; ++b)
+      for (size_t r = 0; r < n; ++r) {
+        emrkc_handle* h = hs[r];
+        cudaSetDevice(h->device);
+        cudaError_t e = emrkc_k::launch_sumsq_serial(field_of(r) + b * h->nn, h->nn, tot,
+                                                     h->d_red, h->stream);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(&tot, h->d_red, sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) {
+          rc = set_err(h, EMRKC_ECUDA, "power iteration: %s", cudaGetErrorString(e));
+          return 0.0;
+        }
+      }
     return tot;
   };
   std::vector<const double*> ys(n), vs(n);
@@ -1581,6 +1613,11 @@ int power_iteration(const std::vector<emrkc_handle*>& hs, int which, double t,
         goto fail;
       }
       tot += part;
+    }
+    if (rho_serial()) {
+      const int an = 1 - a;
+      tot = sum_norm2([&](size_t r) { return w[r].v[an]; });
+      if (rc) goto fail;
     }
     a = 1 - a;
     const double nv = std::sqrt(tot);
@@ -2113,12 +2150,13 @@ int step_impl(emrkc_handle* h, double t, double dt, double epsilon, double rho_F
 }  // namespace
 
 namespace {
-// emrkc_step_host for one-launch steps (s = m = 1 on the TMA node kernel):
-// the state crosses the host link in z-chunks on two copy streams. The
-// kernel / copy-out ranges lag the copy-in chunks by one plane (plane p
-// needs p + 1), so the kernel of range c starts as soon as copy-in chunk c
-// has arrived and its output goes back at once: host->device copies, the
-// step and device->host copies overlap. The abort word is only known after
+// emrkc_step_host for one-outer-stage steps (s = 1, any m, on the TMA
+// kernels): the state crosses the host link in z-chunks on two copy
+// streams. Stencil level k's range lags the copy-in chunks by k planes
+// (plane p of level k needs level k - 1 at p + 1), so the levels of range
+// c start as soon as copy-in chunk c has arrived and the last level's
+// output goes back at once: host->device copies, the step and
+// device->host copies overlap. The abort word is only known after
 // the last range, so on a NumericalAbort y_out has already received (part
 // of) the rejected step; the device state stays y_in (P/src/simulate.cpp:
 // 215-220). Callers whose y_out overlaps y_in take the unpipelined path, so
@@ -2136,8 +2174,10 @@ int host_chunks() {  // EMRKC_HOST_CHUNKS (default 8)
 }
 
 bool step_host_pipelined(emrkc_handle* h) {
-  return !h->partitioned && h->fast && h->pipe == 3 && h->plan.s == 1 && h->plan.m == 1 &&
-         host_chunks() > 1 && h->geom.nzl >= 2 * host_chunks();
+  const Plan& pl = h->plan;
+  return !h->partitioned && h->fast && h->pipe == 3 && pl.s == 1 && pl.method != kMethodMrkc &&
+         !use_tb(h, pl) && host_chunks() > 1 &&
+         h->geom.nzl >= (pl.m + 1) * host_chunks();
 }
 
 int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
@@ -2156,10 +2196,15 @@ int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
   const int64_t nn = h->nn, plane = h->geom.plane;
   const int nz = h->geom.nzl;
   auto zc = [&](int c) { return static_cast<int>(static_cast<int64_t>(c) * nz / kHostChunks); };
-  // Kernel / copy-out ranges lag the copy-in chunks by one plane: plane p
-  // needs p + 1, so the kernel of chunk c covers [zc(c) - 1, zc(c+1) - 1) and
-  // starts as soon as chunk c is in (not c + 1); its output goes out at once.
-  auto kr = [&](int c) { return c == 0 ? 0 : (c == kHostChunks ? nz : zc(c) - 1); };
+  // Kernel / copy-out ranges lag the copy-in chunks: plane p of stencil
+  // level k needs level k - 1 (or the input) at p + 1, so level k of chunk c
+  // covers [zc(c) - k, zc(c+1) - k) and starts as soon as chunk c is in and
+  // level k - 1 of chunk c is done (same stream); the output of the last
+  // level goes out at once.
+  const int m = h->plan.m;
+  auto kr = [&](int c, int k) {
+    return c == 0 ? 0 : (c == kHostChunks ? nz : zc(c) - k);
+  };
   // abort word = no event (all ones), gate-range slots {min: all ones, max: 0}
   CK(h, cudaMemsetAsync(h->d_event, 0xff, sizeof(unsigned long long), h->stream));
   CK(h, cudaMemsetAsync(h->d_slots, 0xff, sizeof(unsigned long long), h->stream));
@@ -2181,9 +2226,11 @@ int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
   int rc = EMRKC_OK;
   for (int c = 0; c < kHostChunks && !rc; ++c) {
     CK(h, cudaStreamWaitEvent(h->stream, h->ev_in[c], 0));
-    h->zr_lo = kr(c);
-    h->zr_hi = kr(c + 1);
-    rc = launch_level(h, &sc, 1, 1);
+    for (int k = 1; k <= m && !rc; ++k) {
+      h->zr_lo = kr(c, k);
+      h->zr_hi = kr(c + 1, k);
+      rc = launch_level(h, &sc, 1, k);
+    }
     CK(h, cudaEventRecord(h->ev_k[c], h->stream));
   }
   h->zr_lo = h->zr_hi = -1;
@@ -2200,7 +2247,7 @@ int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
   double* dout = h->buf[outi];
   for (int c = 0; c < kHostChunks; ++c) {
     CK(h, cudaStreamWaitEvent(h->s_out, h->ev_k[c], 0));
-    const int64_t off = kr(c) * plane, n = (kr(c + 1) - kr(c)) * plane;
+    const int64_t off = kr(c, m) * plane, n = (kr(c + 1, m) - kr(c, m)) * plane;
     CK(h, cudaMemcpy2DAsync(y_out + off, pitch, dout + off, pitch, sizeof(double) * n, 4,
                             cudaMemcpyDeviceToHost, h->s_out));
   }
@@ -2222,9 +2269,9 @@ int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
   rep->eta = pl.eta;
   rep->ell_s = pl.ell_s;
   rep->ell_m = pl.ell_m;
-  rep->n_fF = 1;
-  rep->n_fS = 1;
-  rep->n_exp = 1;
+  rep->n_fF = static_cast<int64_t>(pl.s) * pl.m;
+  rep->n_fS = pl.s;
+  rep->n_exp = exp_per_step(pl.method, pl.s);
   if (d.none) {
     h->cur = outi;
     return EMRKC_OK;

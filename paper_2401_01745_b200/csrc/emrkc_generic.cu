@@ -12,9 +12,9 @@
 //   f_u      f_F(u) + fs   |  f_F(u) + (fs + expc)      :101-102, :111-112
 //   force    (u - y) / eta                              :117
 //   power    z = y + q v,  v = f(z) - f(y)              P/src/spectral.cpp:57-59
-// Norms are deterministic fixed-grid reductions (same order every call; not
-// the reference's serial order, ~1e-16 relative). Finite checks are device
-// flags read once per stage, so NumericalAbort names the same stage and the
+// Norms are summed in the reference's serial order (bit-identical). Finite
+// checks are device flags read once per stage, so NumericalAbort names the
+// same stage and the
 // callback counts match the reference's exactly. This is not the hot path:
 // the fused emrkc_step kernels (kernels_fast.cu) are; this layer makes the
 // reference's generic API (and its scalar known-answer tests) run on the
@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "../../include/emrkc.h"
+#include "kernels.h"
 
 struct emrkc_vctx {
   int device = 0;
@@ -133,29 +134,6 @@ __global__ void k_sub(double* __restrict__ v, const double* __restrict__ a,
     v[i] = __dsub_rn(a[i], b[i]);
 }
 
-// sum of squares: fixed grid of kRedBlocks, each a fixed-order partial
-__global__ void k_sumsq_part(const double* __restrict__ x, int64_t n, double* part) {
-  __shared__ double sh[kThreads];
-  double s = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    s = __dadd_rn(s, __dmul_rn(x[i], x[i]));
-  sh[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = kThreads / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + o]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
-}
-__global__ void k_sum_parts(double* part, int nb) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s = __dadd_rn(s, part[b]);
-    part[kRedBlocks] = s;
-  }
-}
-
 // Device scratch, released on scope exit (stream-ordered).
 struct Scratch {
   emrkc_vctx* c;
@@ -188,10 +166,10 @@ int stage_nonfinite(emrkc_vctx* c, const double* x, int64_t n, bool* bad) {
   return EMRKC_OK;
 }
 
+// ||x|| in the reference's serial order (P/src/spectral.cpp:10-14),
+// bit-identical to it (kernels.cu k_sumsq_serial).
 int norm2(emrkc_vctx* c, const double* x, int64_t n, double* out) {
-  k_sumsq_part<<<kRedBlocks, kThreads, 0, c->stream>>>(x, n, c->d_part);
-  k_sum_parts<<<1, 32, 0, c->stream>>>(c->d_part, kRedBlocks);
-  GK(c, cudaGetLastError());
+  GK(c, emrkc_k::launch_sumsq_serial(x, n, 0.0, c->d_part + kRedBlocks, c->stream));
   GK(c, cudaMemcpyAsync(c->h_sum, c->d_part + kRedBlocks, sizeof(double),
                         cudaMemcpyDeviceToHost, c->stream));
   GK(c, cudaStreamSynchronize(c->stream));

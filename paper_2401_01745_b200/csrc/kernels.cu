@@ -1091,6 +1091,61 @@ cudaError_t launch_power(const Geom& g, int which, const double* y,
   return cudaGetLastError();
 }
 
+// Sum of squares in the reference's SERIAL order (P/src/spectral.cpp:10-14:
+// s += x * x, i = 0 .. n-1, no FMA), continuing from acc: one block, the
+// squares staged through a double-buffered shared chunk by warps 1..7 while
+// thread 0 runs the dependent add chain. Bit-identical to the reference's
+// norm2 (so the power iteration's q = delta / ||v|| and every z = y + q v
+// are too); a run of segments chained through acc covers a vector held in
+// several pieces (SoA blocks of z-slabs, in global order).
+constexpr int kSerT = 256, kSerC = 2048;
+__global__ void __launch_bounds__(kSerT) k_sumsq_serial(const double* __restrict__ x, long long n,
+                                                        double acc, double* out) {
+  __shared__ double buf[2][kSerC];
+  const int t = threadIdx.x;
+  const long long nch = (n + kSerC - 1) / kSerC;
+  for (int k = t; k < kSerC; k += kSerT) buf[0][k] = k < n ? __dmul_rn(x[k], x[k]) : 0.0;
+  __syncthreads();
+  double s = acc;
+  for (long long c = 0; c < nch; ++c) {
+    const int cur = (int)(c & 1);
+    if (t >= 32) {
+      if (c + 1 < nch) {
+        const long long base = (c + 1) * kSerC;
+        for (int k = t - 32; k < kSerC; k += kSerT - 32) {
+          const long long i = base + k;
+          buf[cur ^ 1][k] = i < n ? __dmul_rn(x[i], x[i]) : 0.0;
+        }
+      }
+    } else if (t == 0) {
+      const int len = (int)min((long long)kSerC, n - c * kSerC);
+      const double* b = buf[cur];
+      int k = 0;
+      for (; k + 8 <= len; k += 8) {
+        const double b0 = b[k], b1 = b[k + 1], b2 = b[k + 2], b3 = b[k + 3];
+        const double b4 = b[k + 4], b5 = b[k + 5], b6 = b[k + 6], b7 = b[k + 7];
+        s = __dadd_rn(s, b0);
+        s = __dadd_rn(s, b1);
+        s = __dadd_rn(s, b2);
+        s = __dadd_rn(s, b3);
+        s = __dadd_rn(s, b4);
+        s = __dadd_rn(s, b5);
+        s = __dadd_rn(s, b6);
+        s = __dadd_rn(s, b7);
+      }
+      for (; k < len; ++k) s = __dadd_rn(s, b[k]);
+    }
+    __syncthreads();
+  }
+  if (t == 0) *out = s;
+}
+
+cudaError_t launch_sumsq_serial(const double* x, long long len, double acc, double* out,
+                                cudaStream_t st) {
+  k_sumsq_serial<<<1, kSerT, 0, st>>>(x, len, acc, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_norm2_partial(const double* x, long long len,
                                  double* partial, int nblocks,
                                  cudaStream_t st) {

@@ -198,6 +198,7 @@ struct FastInnerArgs {
   double mueta, nu, kappa;  // inner mu'_k eta, nu'_k, kappa'_k
   double onu, okappa, cG;   // outer nu_j, kappa_j, mu_j dt / eta
   int j, k, m, s, last, zc;
+  int z_lo, z_hi;     // k_vin_tma*: local planes [z_lo, z_hi) of this launch
   unsigned long long code_base;
   unsigned long long* event;
 };
@@ -326,6 +327,10 @@ cudaError_t launch_norm2_partial(const double* x, long long len,
                                  cudaStream_t st);
 cudaError_t launch_sum_partials(const double* partial, int nblocks,
                                 double* out, cudaStream_t st);
+// Serial-order sum of squares (the reference's norm2 order), continuing
+// from acc, result to *out (device).
+cudaError_t launch_sumsq_serial(const double* x, long long len, double acc, double* out,
+                                cudaStream_t st);
 
 // Gate range of a state (ordered-u64 min/max into slot[0..1]) and
 // max |V| (ordered) into *vmax (nullable).

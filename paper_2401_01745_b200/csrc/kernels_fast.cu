@@ -1725,8 +1725,8 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, 7)
   __shared__ __align__(8) unsigned long long bars[kRV];
   __shared__ int skip;
   const int t = threadIdx.x;
-  const int zb = (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
-  const int ze = min(g.nzl, zb + a.zc);
+  const int zb = a.z_lo + (DIM == 3 ? blockIdx.z : blockIdx.y) * a.zc;
+  const int ze = min(a.z_hi, zb + a.zc);
   pdl_launch_dependents();
   if (t == 0) {
     for (int s = 0; s < kRV; ++s) mbar_init(smem_u32(&bars[s]), 1);
@@ -1897,8 +1897,8 @@ __global__ void __launch_bounds__(128)
   __shared__ __align__(8) unsigned long long bars[kRV];
   __shared__ int skip;
   const int t = threadIdx.x;
-  const int zb = blockIdx.z * a.zc;
-  const int ze = min(g.nzl, zb + a.zc);
+  const int zb = a.z_lo + blockIdx.z * a.zc;
+  const int ze = min(a.z_hi, zb + a.zc);
   pdl_launch_dependents();
   if (t == 0) {
     for (int s = 0; s < kRV; ++s) mbar_init(smem_u32(&bars[s]), 1);
@@ -2583,7 +2583,7 @@ static cudaError_t launch_vin_tma_t(const Geom& g, const Halo& h, const FastInne
                          (int)smem);
     attr = true;
   }
-  const int chunks = (g.nzl + a.zc - 1) / a.zc;
+  const int chunks = (a.z_hi - a.z_lo + a.zc - 1) / a.zc;
   const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)
                           : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
   return launch_k(k_vin_tma<D, L, F>, grd, dim3(T::NT), smem, st, g, h, a, tm);
@@ -2601,7 +2601,7 @@ static cudaError_t launch_vin_tma_r_t(const Geom& g, const Halo& h, const FastIn
                          (int)tma_vin_r_smem_bytes<R>(4));
     attr = true;
   }
-  const int chunks = (g.nzl + a.zc - 1) / a.zc;
+  const int chunks = (a.z_hi - a.z_lo + a.zc - 1) / a.zc;
   const dim3 grd((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks);
   return launch_k(k_vin_tma_r<L, F, R>, grd, dim3(T::NT), smem, st, g, h, a, tm);
 }

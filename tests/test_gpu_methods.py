@@ -123,9 +123,11 @@ def test_exex_step_dropin(oracle):
     op.close()
 
 
-@pytest.mark.parametrize("name", ["hh3d_128x128x128", "hh2d_256x256"])
+@pytest.mark.parametrize("name", ["hh3d_128x128x128", "hh2d_256x256", "hh3d_sweep_100",
+                                  "hh3d_sweep_200"])
 def test_step_host_pipelined_matches_device_step(oracle, name):
-    """emrkc_step_host streams s = m = 1 steps in z-chunks (copies overlap the
+    """emrkc_step_host streams s = 1 steps in z-chunks, stencil level k
+    lagging the copy-in by k planes (m = 1, 2 and 4 here; copies overlap the
     step); results equal the device-resident step bit for bit."""
     import ctypes as C
     import torch
@@ -153,7 +155,7 @@ def test_step_host_pipelined_matches_device_step(oracle, name):
                                     C.cast(hout.data_ptr(), C.POINTER(C.c_double)), hin.numel(),
                                     w.dt, w.eps, capi.EMRKC_VARIANT_STANDARD, rF, rS, C.byref(rep))
         assert rc == 0
-        assert (rep.s, rep.m, rep.n_fF) == (1, 1, 1)
+        assert rep.s == 1 and rep.n_fF == rep.m and (rep.n_fS, rep.n_exp) == (1, 1)
         hin.copy_(hout)
     assert np.array_equal(hout.numpy(), y_dev)
     assert np.array_equal(h2.get_state(), y_dev)

@@ -63,6 +63,9 @@ def test_rho_parity(oracle, dim):
         assert got.iterations == ref.iterations
         assert got.converged == bool(ref.converged)
         assert abs(got.rho - ref.rho) <= RHO_TOL * ref.rho, (which, got.rho, ref.rho)
+        # norms summed in the reference's serial order: q, z = y + q v and
+        # f(z) - f(y) are bit-identical, and so is rho
+        assert got.rho == ref.rho, (which, got.rho, ref.rho)
 
 
 def run_both(oracle, w, nsteps=None, fast=None, monkeypatch=None):
