@@ -71,6 +71,8 @@ KERNEL_BYTES = {
     ("last2", "outer"): 32,        # + V of g_{j-2}
     ("last", "first_outer"): 40,   # d_{m-1}, d_{m-2}, d_1, V in; V out
     ("last", "outer"): 48,
+    ("fused", "first_outer"): 64,  # k_fused2: g_0 in (4 fields), g_1 out (4); d_1 stays on chip
+    ("fused_skip", None): 0,       # level 2 ran inside the fused launch
 }
 KERNEL_ROLES = {"m1": ("node", "m = 1: whole outer stage"),
                 "first": ("node", "m >= 2: ionic + inner stage 1"),
@@ -78,7 +80,10 @@ KERNEL_ROLES = {"m1": ("node", "m = 1: whole outer stage"),
                 "last2": ("vin", "last inner stage, m = 2"),
                 "last": ("vin", "last inner stage"),
                 "tb": ("vin", "inner stages 2..m, temporally blocked"),
-                "tb_skip": ("vin", "fused into the k = 2 launch")}
+                "tb_skip": ("vin", "fused into the k = 2 launch"),
+                "fused": ("fused2", "s = 1, m = 2: node update + inner stage 2 + outer update "
+                                    "in one persistent pass"),
+                "fused_skip": ("fused2", "level 2 ran inside the fused launch")}
 
 
 def kernel_name(kind: str, problem) -> str:
@@ -91,6 +96,8 @@ def kernel_name(kind: str, problem) -> str:
     if problem.dim < 2:
         pipe = 0
     role, what = KERNEL_ROLES[kind]
+    if role == "fused2":
+        return f"k_fused2 ({what})"
     fam = {3: "tma", 1: "pipe", 2: "persist" if role == "node" else "pipe", 0: "fast"}[pipe]
     if kind.startswith("tb"):
         fam = "tb"
@@ -105,8 +112,12 @@ def tb_active(problem, m: int) -> bool:
             and int(os.environ.get("EMRKC_TB") or 0) != 0 and 2 <= m - 1 <= 4)
 
 
-def launch_kinds(s: int, m: int, problem=None):
-    """(kind, outer) of each launch of one step, in launch order."""
+def launch_kinds(s: int, m: int, problem=None, fused: bool = False):
+    """(kind, outer) of each launch of one step, in launch order (fused: the
+    library runs the s = 1, m = 2 step as one k_fused2 pass,
+    emrkc_fused_active)."""
+    if fused:
+        return [("fused", "first_outer"), ("fused_skip", None)]
     out = []
     tb = problem is not None and tb_active(problem, m)
     for j in range(1, s + 1):
@@ -452,6 +463,7 @@ def measure_device(w, device, warmup, steps, with_e2e=True, clocks=None, ramp_s=
                        (f" up to its NumericalAbort/guard at step {kr}" if kr < w.n_steps else "") +
                        ", best of 3, device time of the run, no L2 flush between steps"}
     out = {"op": op, "y0": y0, "rF": rF, "rS": rS, "s": rep.s, "m": rep.m, "run": run,
+           "fused": bool(lib.emrkc_fused_active(op.handle)),
            "launch_ms": launch_ms.reshape(steps, per), "res": results[-1], "steps": steps,
            "repeats": len(chunks), "aborted": any(r.aborted for r in results),
            "abort_at": kr if kr < w.n_steps else None}
@@ -543,7 +555,7 @@ def measure_e2e_run(op, w, y0, rF, rS, reps=3):
 
 def roofline_of(m, w, peak, peak_kind):
     per_pos = m["launch_ms"].mean(axis=0)
-    kinds = launch_kinds(m["s"], m["m"], w.problem)
+    kinds = launch_kinds(m["s"], m["m"], w.problem, m.get("fused", False))
     dom = int(np.argmax(per_pos))
     kb = KERNEL_BYTES[kinds[dom]]
     achieved = kb * w.n_nodes / (per_pos[dom] * 1e-3) / 1e9
@@ -592,7 +604,7 @@ def b200_arm(args, w):
         "e2e": m["e2e"],
         "e2e_run": m["e2e_run"],
         "run": m["run"],
-        "gpu_launches": int(args.steps * m["s"] * m["m"]),
+        "gpu_launches": int(args.steps * (1 if m["fused"] else m["s"] * m["m"])),
         "clocks": clocks,
     }
     y0, rF, rS = m["y0"], m["rF"], m["rS"]

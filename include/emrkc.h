@@ -189,6 +189,11 @@ int64_t emrkc_local_len(const emrkc_handle* h);
 /* Upload / download the (local) state in reference Vec layout. */
 int emrkc_set_state(emrkc_handle* h, const double* y, int64_t len);
 int emrkc_get_state(emrkc_handle* h, double* y, int64_t len);
+/* Kernel plan of the handle's current step plan (after a step / run):
+ * 1 when one step runs as the single fused pass (k_fused2: s = 1, m = 2,
+ * 3-D whole grid), 0 when it runs as one launch per stencil level. A
+ * diagnostic for benches and tests; no reference counterpart. */
+int32_t emrkc_fused_active(emrkc_handle* h);
 /* Device pointer of the current state (valid until the next step/run). */
 int emrkc_state_device_ptr(emrkc_handle* h, double** dptr);
 int emrkc_synchronize(emrkc_handle* h);

@@ -339,6 +339,14 @@ struct emrkc_handle {
   emrkc_k::CgScalars* cg_h = nullptr;   // pinned host copy
   int* guard_d = nullptr;
   int zr_lo = -1, zr_hi = -1;  // node-kernel plane range override (< 0: all)
+  // fused s = 1, m = 2 step (k_fused2): tile plan, exchange ring, flags
+  int fused = 0;                    // EMRKC_FUSED=1: the fused s = 1, m = 2 pass (slower
+                                    // on B200 than the two-kernel step)
+  int fu_ntx = 0, fu_nty = 0, fu_nzc = 0;  // 0: not planned / not possible
+  bool fu_planned = false;
+  double* fu_xch = nullptr;
+  unsigned long long* fu_flags = nullptr;
+  unsigned long long fu_epoch = 0;
   // pipelined host step (emrkc_step_host): copy streams and chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   unsigned long long* h_event = nullptr;  // pinned copy of the abort word
@@ -655,6 +663,39 @@ int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out, int rm
 
 // 3-D map over one V-sized field (n0, n1, nzl) with box (bx, by, 1); key
 // distinguishes box shapes in the cache (>= 100).
+// k_fused2 boxes: kind 0 = V with halo (kFuTX + 4, kFuTY + 2, 1), kind 1 =
+// the three gate fields (kFuTX, kFuTY, 1, 3) from field 1.
+int tma_map_fused(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out) {
+  const int key = 3000 + kind;
+  for (const auto& e : h->tmaps)
+    if (e.ptr == ptr && e.kind == key) {
+      *out = e.map;
+      return EMRKC_OK;
+    }
+  const Geom& g = h->geom;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.n0), static_cast<cuuint64_t>(g.n1),
+                              static_cast<cuuint64_t>(g.nzl), 4};
+  const cuuint64_t strides[3] = {sizeof(double) * static_cast<cuuint64_t>(g.n0),
+                                 sizeof(double) * static_cast<cuuint64_t>(g.plane),
+                                 sizeof(double) * static_cast<cuuint64_t>(g.nn)};
+  const cuuint32_t box[4] = {
+      static_cast<cuuint32_t>(kind == 0 ? emrkc_k::kFuTX + 4 : emrkc_k::kFuTX),
+      static_cast<cuuint32_t>(kind == 0 ? emrkc_k::kFuTY + 2 : emrkc_k::kFuTY), 1, 3};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
+    return set_err(h, EMRKC_ECUDA, "TMA: buffer %p not 16-byte aligned", ptr);
+  CUtensorMap m;
+  const CUresult r = tma_encoder()(
+      &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, kind == 0 ? 3 : 4, const_cast<void*>(ptr), dims,
+      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(h, EMRKC_ECUDA, "cuTensorMapEncodeTiled failed (%d, fused %d)", (int)r, kind);
+  h->tmaps.push_back({ptr, key, m});
+  *out = m;
+  return EMRKC_OK;
+}
+
 int tma_map_box3(emrkc_handle* h, const void* ptr, cuuint32_t bx, cuuint32_t by, int key,
                  CUtensorMap* out, int64_t nz = -1) {
   for (const auto& e : h->tmaps)
@@ -691,6 +732,54 @@ bool use_tb(const emrkc_handle* h, const Plan& pl) {
   if (!(h->tb && h->pipe == 3 && h->geom.dim == 3 && K >= 2 && K <= emrkc_k::kTbMaxK))
     return false;
   return !h->partitioned || h->min_depth >= K;
+}
+
+// Fused s = 1, m = 2 step (k_fused2): whole-grid 3-D handles on the TMA
+// path whose plane splits into >= 90% of the co-resident block slots
+// (ntx = n0 / 64 column tiles of width 64, nty tile rows of <= 14 rows,
+// nzc z-chunks of >= 8 planes).
+bool fused_plan(emrkc_handle* h) {
+  if (h->fu_planned) return h->fu_ntx > 0;
+  h->fu_planned = true;
+  const Geom& g = h->geom;
+  if (g.dim != 3 || g.n0 % emrkc_k::kFuTX || g.n1 < 2 * emrkc_k::kFuTY || g.nzl < 8) return false;
+  const int per_sm = emrkc_k::fused_blocks_per_sm();
+  int sms = 0;
+  if (per_sm < 1 || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device) !=
+                        cudaSuccess)
+    return false;
+  const int slots = per_sm * sms;
+  const int ntx = g.n0 / emrkc_k::kFuTX;
+  const int ny_min = (g.n1 + emrkc_k::kFuTY - 1) / emrkc_k::kFuTY;
+  int best = 0, bty = 0, bz = 0;
+  for (int nzc = 1; nzc <= 16 && g.nzl / nzc >= 8; ++nzc)
+    for (int nty = ny_min; nty <= g.n1 / 2; ++nty) {
+      const long long tiles = (long long)ntx * nty * nzc;
+      if (tiles > slots) break;
+      if (tiles > best) {
+        best = static_cast<int>(tiles);
+        bty = nty;
+        bz = nzc;
+      }
+    }
+  if (best < 0.9 * slots) return false;
+  const size_t xn = static_cast<size_t>(best) * 4 * 4 * emrkc_k::kFuTX;
+  if (cudaMalloc(&h->fu_xch, sizeof(double) * xn) != cudaSuccess ||
+      cudaMalloc(&h->fu_flags, sizeof(unsigned long long) * best) != cudaSuccess ||
+      cudaMemset(h->fu_flags, 0, sizeof(unsigned long long) * best) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  h->fu_ntx = ntx;
+  h->fu_nty = bty;
+  h->fu_nzc = bz;
+  return true;
+}
+
+bool use_fused(emrkc_handle* h, const Plan& pl) {
+  return h->fused && h->fast && h->pipe == 3 && !h->partitioned && h->zr_lo < 0 &&
+         h->geom.dim == 3 && pl.s == 1 && pl.m == 2 && !pl.exex && pl.method != kMethodMrkc &&
+         fused_plan(h);
 }
 
 // The neighbours' d_1 ghosts this handle's inner-stage-1 kernel stores into
@@ -770,6 +859,7 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
     long long signals = h->pipe && h->geom.dim >= 2 ? emrkc_k::halo_signals_pipe(h->geom)
                                                      : emrkc_k::halo_signals_march(h->geom);
     if (use_tb(h, pl) && k > 2) return EMRKC_OK;  // fused into level k == 2: no level
+    if (k == 2 && use_fused(h, pl)) return EMRKC_OK;  // ran inside the k == 1 launch
     if (k == 1) {
       emrkc_k::FastArgs f{};
       f.g1 = a.g1;
@@ -797,6 +887,29 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.code_base = a.code_base;
       f.event = a.event;
       f.gate_slot = a.gate_slot;
+      if (use_fused(h, pl)) {
+        // the whole step (levels 1 and 2) in one persistent pass
+        emrkc_k::FusedArgs fa{};
+        fa.f = f;
+        fa.inv_mue1 = 1.0 / pl.in_mueta[1];
+        fa.mueta2 = pl.in_mueta[2];
+        fa.nu2 = pl.inner.nu[2];
+        fa.cG2 = cG;
+        fa.xch = h->fu_xch;
+        fa.flags = h->fu_flags;
+        h->fu_epoch += 1ull << 32;
+        fa.epoch = h->fu_epoch;
+        fa.ntx = h->fu_ntx;
+        fa.nty = h->fu_nty;
+        fa.nzc = h->fu_nzc;
+        emrkc_k::TmaFused tm;
+        int rc = tma_map_fused(h, f.g1, 0, &tm.v);
+        if (!rc) rc = tma_map_fused(h, f.g1, 1, &tm.gates);
+        if (rc) return rc;
+        CK(h, emrkc_k::launch_fused2(h->geom, fa, tm, h->stream));
+        ++h->level;
+        return EMRKC_OK;
+      }
       if (h->pipe == 3) {
         emrkc_k::TmaNode tm;
         int rc = tma_map(h, f.g1, kTmaHalo, &tm.v);
@@ -1015,6 +1128,8 @@ int init_handle(emrkc_handle* h) {
   if (h->pipe == 3 && !tma_supported(h)) h->pipe = 1;
   if (const char* tb = std::getenv("EMRKC_TB"))
     if (*tb) h->tb = std::atoi(tb) != 0;
+  if (const char* fu = std::getenv("EMRKC_FUSED"))
+    if (*fu) h->fused = std::atoi(fu) != 0;
   if (const char* zc = std::getenv("EMRKC_ZC"))
     if (*zc) h->zc = std::min(emrkc_k::kMaxZc, std::max(1, std::atoi(zc)));
   return EMRKC_OK;
@@ -1240,6 +1355,8 @@ void emrkc_destroy(emrkc_handle* h) {
   if (h->d_coef) cudaFree(h->d_coef);
   if (h->d_red) cudaFree(h->d_red);
   if (h->d_rel) cudaFree(h->d_rel);
+  if (h->fu_xch) cudaFree(h->fu_xch);
+  if (h->fu_flags) cudaFree(h->fu_flags);
   for (auto& u : h->mr_u)
     if (u) cudaFree(u);
   if (h->mr_fs) cudaFree(h->mr_fs);
@@ -2837,4 +2954,9 @@ int emrkc_model_ionic_current(int32_t model, double V, const double* z_E, double
   if (!z_E || !current) return set_global(EMRKC_EINVAL, "null argument");
   *current = hh_current(V, z_E);
   return EMRKC_OK;
+}
+
+int32_t emrkc_fused_active(emrkc_handle* h) {
+  if (!h || !h->plan_uploaded) return 0;
+  return use_fused(h, h->plan) ? 1 : 0;
 }

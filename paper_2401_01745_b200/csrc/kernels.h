@@ -203,6 +203,28 @@ struct FastInnerArgs {
   unsigned long long* event;
 };
 
+// Fused s = 1, m = 2 step (k_fused2, kernels_fast.cu): node update + inner
+// stage 2 + outer update in one pass; persistent co-resident grid of
+// ntx x nty column tiles (kFuTX wide, <= kFuTY rows) x nzc z-chunks, d_1
+// tile edges exchanged through an L2-resident ring with per-block flags.
+constexpr int kFuTX = 64, kFuTY = 14, kFuNT = 256;
+struct FusedArgs {
+  FastArgs f;                 // node phase (j = 1, ION): g1, out, eta, stim, cG, mue1, window, events
+  double inv_mue1;            // 1 / (mu'_1 eta)
+  double mueta2, nu2;         // inner stage 2: mu'_2 eta, nu'_2
+  double cG2;                 // outer: mu_1 dt / eta
+  double* xch;                // exchange ring [blocks][4 planes][4 sides][kFuTX]
+  unsigned long long* flags;  // [blocks]: epoch + (last published plane + 1)
+  unsigned long long epoch;   // strictly increasing per launch (flags never reset)
+  int ntx, nty, nzc;
+};
+struct TmaFused {
+  CUtensorMap v;      // V of g_0, box (kFuTX + 4, kFuTY + 2, 1)
+  CUtensorMap gates;  // all fields of g_0, box (kFuTX, kFuTY, 1, 3) from field 1
+};
+int fused_blocks_per_sm();
+cudaError_t launch_fused2(const Geom& g, const FusedArgs& a, const TmaFused& tm, cudaStream_t st);
+
 // Temporally blocked inner stages: one pass runs stages k = 2..m (m - 1 = K
 // fused V-only stages, 2 <= K <= kTbMaxK) of outer stage j (3-D, whole-grid
 // handles). Stage k is computed on the tile plus a halo of K + 1 - k cells

@@ -2344,6 +2344,357 @@ dim3 fgrid(const Geom& g, int zc) {
   return dim3((g.nzl + kFThreads - 1) / kFThreads, 1, 1);
 }
 
+// ---------------------------------------------------------------------------
+// k_fused2: a whole emRKC step with s = 1, m = 2 in ONE pass over HBM (3-D,
+// whole grid): the node update (exponential Euler of the gates, f_S(y_E),
+// 7-point stencil, inner stage 1 -> d_1, gate rows of g_1) of plane z and
+// inner stage 2 + the outer update of plane z - 1 (V of g_1), so d_1 never
+// touches HBM: 64 B per node instead of 64 (node kernel) + 24 (inner
+// kernel). Inner stage 2 needs f_F(d_1) on the x/y neighbours of a tile,
+// which other blocks compute: the grid is persistent and co-resident (a
+// cooperative launch, one 64 x ~14 column tile and a z-range per block, two
+// blocks per SM), each block stores the edge rows / columns of its d_1
+// plane into an L2-resident exchange ring and publishes the plane on a
+// monotone flag (fence + relaxed store); iteration z runs inner stage 2 of
+// plane z - 2 first (the neighbours published its edges one whole
+// iteration earlier: lanes 0..3 poll one flag each, then fence, then the
+// edges are read with ld.cg) and then the node update of plane z. The stencil has no order-dependent
+// reductions: the arithmetic is k_node_tma<3,1,1>'s and k_vin_tma_r<1,1>'s
+// operation for operation (bitwise equal to the two-kernel step).
+// Per block: V boxes (68 x 16) two planes ahead, gate boxes (64 x 14 x 3)
+// one plane ahead (TMA), a 3-plane ring of d_1 tiles with a one-cell halo
+// filled from the neighbours' edges (or mirrored at the grid boundary,
+// P/src/monodomain.cpp:85-86), z-chunks recompute d_1 one plane beyond
+// each end. Nodes outside the fast ionic window take the reference-order
+// path in a per-plane second pass (rare).
+// ---------------------------------------------------------------------------
+constexpr int kFuRV = 4, kFuRG = 2, kFuRD = 3, kFuRX = 4;
+constexpr int kFuVX = kFuTX + 4, kFuVY = kFuTY + 2;
+constexpr int kFuVS = ((kFuVX * kFuVY) + 15) & ~15;
+constexpr int kFuGF = kFuTX * kFuTY;  // one gate field of a tile
+constexpr int kFuGS = 3 * kFuGF;
+constexpr int kFuDX = kFuTX + 2;
+constexpr int kFuDS = ((kFuDX * (kFuTY + 2)) + 15) & ~15;
+static_assert(kFuTX == 64 && kFuNT == 256 && kFuTY * kFuTX <= 4 * kFuNT, "fused tile");
+
+constexpr size_t fused_smem_bytes() {
+  return sizeof(double) * (kFuRV * kFuVS + kFuRG * kFuGS + kFuRD * kFuDS) + 128;
+}
+
+__device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kFuNT, 2)
+    k_fused2(const Geom g, const FusedArgs A, const __grid_constant__ TmaFused tm) {
+  const FastArgs& a = A.f;
+  extern __shared__ __align__(128) double smem_fu[];
+  double* vst = smem_fu + ((128u - (smem_u32(smem_fu) & 127u)) & 127u) / 8;  // [RV][VS]
+  double* gst = vst + kFuRV * kFuVS;                                          // [RG][GS]
+  double* dst = gst + kFuRG * kFuGS;                                          // [RD][DS]
+  __shared__ double tab[256];
+  __shared__ __align__(8) unsigned long long vbar[kFuRV], gbar[kFuRG];
+  __shared__ int skip, timed_out;
+  __shared__ unsigned long long rlo[kFuNT / 32], rhi[kFuNT / 32];
+  const int t = threadIdx.x;
+  const int ntile = A.ntx * A.nty;
+  const int zi = blockIdx.x / ntile, tile = blockIdx.x % ntile;
+  const int txi = tile % A.ntx, tyi = tile / A.ntx;
+  const int x0 = txi * kFuTX;
+  const int y0 = (int)((long long)tyi * g.n1 / A.nty);
+  const int TYH = (int)((long long)(tyi + 1) * g.n1 / A.nty) - y0;
+  const int nz = g.nzl;
+  const int zb = (int)((long long)zi * nz / A.nzc), ze = (int)((long long)(zi + 1) * nz / A.nzc);
+  const int zA = max(zb - 1, 0), zE = min(ze + 1, nz);  // d_1 planes [zA, zE)
+  const long long nn = g.nn, plane = g.plane;
+  if (t == 0) {
+    for (int q = 0; q < kFuRV; ++q) mbar_init(smem_u32(&vbar[q]), 1);
+    for (int q = 0; q < kFuRG; ++q) mbar_init(smem_u32(&gbar[q]), 1);
+    mbar_fence_init();
+    prefetch_tensormap(&tm.v);
+    prefetch_tensormap(&tm.gates);
+    skip = (*(volatile const unsigned long long*)a.event) < level_floor(a.code_base, a.j, a.m, 1);
+    timed_out = 0;
+  }
+  load_exp_table(tab, t, kFuNT);
+  __syncthreads();
+  // every block takes the same decision: events of this launch are >= the floor
+  if (skip) return;
+  const unsigned v0s = smem_u32(vst), g0s = smem_u32(gst);
+  auto issue_v = [&](int zz) {  // V box of plane zz in [zA - 1, zE]
+    const int q = zz - zA + 1;
+    const unsigned bar = smem_u32(&vbar[q & (kFuRV - 1)]);
+    mbar_expect_tx(bar, 8u * kFuVX * kFuVY);
+    tma_vplane<3>(g, &tm.v, nullptr, nullptr, false, false,
+                  v0s + 8u * kFuVS * (q & (kFuRV - 1)), bar, x0, y0, zz);
+  };
+  auto issue_g = [&](int zz) {  // gate box of plane zz in [zA, zE)
+    const int q = zz - zA;
+    const unsigned bar = smem_u32(&gbar[q & (kFuRG - 1)]);
+    mbar_expect_tx(bar, 8u * kFuGS);
+    tma_load_4d(g0s + 8u * kFuGS * (q & (kFuRG - 1)), &tm.gates, bar, x0, y0, zz, 1);
+  };
+  if (t == 0) {
+    issue_v(zA - 1);
+    issue_v(zA);
+    if (zA + 1 <= zE) issue_v(zA + 1);
+    issue_g(zA);
+  }
+  const int lx = t & (kFuTX - 1), ly0 = t / kFuTX;
+  const int cx = x0 + lx;
+  const int dxm = cx > 0 ? -1 : 1, dxp = cx < g.n0 - 1 ? 1 : -1;
+  const bool stx = cx >= g.st_lo[0] && cx <= g.st_hi[0];
+  double* const outv = a.out;  // V block of g_1 (stage 2); gate rows at + nn
+  unsigned finacc = 0x7ff00000u;
+  bool bad_slow = false, bad_in = false, bad_out = false, guard = false, any_out = false;
+  double glo = 2.0, ghi = -1.0;
+  mbar_wait(smem_u32(&vbar[0]), 0);  // V(zA - 1)
+  mbar_wait(smem_u32(&vbar[1]), 0);  // V(zA)
+  const int base_cta = zi * ntile;
+  // neighbour of side s (W, E, S, N) in this z-chunk, -1 at the grid edge
+  const int nbr = t < 4 ? (t == 0 ? (txi > 0 ? tile - 1 : -1)
+                                  : t == 1 ? (txi < A.ntx - 1 ? tile + 1 : -1)
+                                  : t == 2 ? (tyi > 0 ? tile - A.ntx : -1)
+                                           : (tyi < A.nty - 1 ? tile + A.ntx : -1))
+                        : -1;
+  // Iteration z: phase B of plane z - 2 (its d_1 edges were published by the
+  // neighbours one whole iteration ago), then phase A of plane z.
+  for (int z = zA; z <= ze + 1; ++z) {
+    const int zz = z - 2;
+    const bool doB = zz >= zb && zz < ze;
+    // ---- phase B: inner stage 2 + outer update of plane zz
+    if (doB) {
+      if (nbr >= 0) {  // lanes 0..3 of warp 0: one neighbour flag each
+        const unsigned long long want = A.epoch + (unsigned long long)(zz + 1);
+        const unsigned long long t0 = globaltimer_ns();
+        while (ld_relaxed_gpu_u64(A.flags + base_cta + nbr) < want) {
+          if (globaltimer_ns() - t0 > 4000000000ull) {  // a neighbour never came: bail
+            timed_out = 1;
+            atomicMin(a.event, 0ull);
+            break;
+          }
+        }
+        fence_acq_rel_gpu();
+      }
+      __syncthreads();
+      if (timed_out) return;
+      double* Dz = dst + (zz % kFuRD) * kFuDS;
+      const int slot = zz & (kFuRX - 1);
+      auto xedge = [&](int nbtile, int side, int i) {
+        return __ldcg(A.xch + ((size_t)(base_cta + nbtile) * kFuRX + slot) * 4 * kFuTX +
+                      side * kFuTX + i);
+      };
+      if (t < kFuTY) {  // west halo column <- the west tile's east edge (or mirror x = 1)
+        if (t < TYH)
+          Dz[(t + 1) * kFuDX] = txi > 0 ? xedge(tile - 1, 1, t) : Dz[(t + 1) * kFuDX + 2];
+      } else if (t >= 64 && t < 64 + kFuTY) {  // east <- east tile's west edge (or x = n0 - 2)
+        const int i = t - 64;
+        if (i < TYH)
+          Dz[(i + 1) * kFuDX + kFuTX + 1] =
+              txi < A.ntx - 1 ? xedge(tile + 1, 0, i) : Dz[(i + 1) * kFuDX + kFuTX - 1];
+      } else if (t >= 128 && t < 192) {  // south <- south tile's north edge (or y = 1)
+        const int i = t - 128;
+        Dz[i + 1] = tyi > 0 ? xedge(tile - A.ntx, 3, i) : Dz[2 * kFuDX + i + 1];
+      } else if (t >= 192) {  // north <- north tile's south edge (or y = n1 - 2)
+        const int i = t - 192;
+        Dz[(TYH + 1) * kFuDX + i + 1] =
+            tyi < A.nty - 1 ? xedge(tile + A.ntx, 2, i) : Dz[(TYH - 1) * kFuDX + i + 1];
+      }
+      __syncthreads();
+      const double* Dm = dst + ((zz == 0 ? 1 : zz - 1) % kFuRD) * kFuDS;
+      const double* Dp = dst + ((zz == nz - 1 ? nz - 2 : zz + 1) % kFuRD) * kFuDS;
+      const double* Vg = vst + ((zz - zA + 1) & (kFuRV - 1)) * kFuVS;  // V of g_0 at zz
+      for (int r = 0; r < 4; ++r) {
+        const int ly = ly0 + 4 * r;
+        if (ly >= TYH) break;
+        const int c = (ly + 1) * kFuDX + lx + 1;
+        const double d1 = Dz[c];
+        double D = fma(g.wc, d1, g.w[2] * (Dm[c] + Dp[c]));
+        D = fma(g.w[0], Dz[c - 1] + Dz[c + 1], D);
+        D = fma(g.w[1], Dz[c - kFuDX] + Dz[c + kFuDX], D);
+        const double dk = fma(A.mueta2, fma(d1, A.inv_mue1, D), A.nu2 * d1);
+        const double o0 = fma(A.cG2, dk, Vg[(ly + 1) * kFuVX + lx + 2]);
+        outv[(cx + (long long)g.n0 * (y0 + ly)) + plane * zz] = o0;
+        bad_in |= !finite_hi(dk);
+        bad_out |= !finite_hi(o0);
+        guard |= !(fabs(o0) <= 1e6);  // also a non-finite V
+      }
+    }
+    // V(zz) and d_1(zz - 1) are free: the ring slots take V(z + 2) and d_1(z)
+    if (doB) __syncthreads();
+    const bool doA = z < zE;
+    const int qv = z - zA + 1;
+    if (t == 0) {
+      if (z + 2 <= zE) issue_v(z + 2);
+      if (z + 1 < zE) issue_g(z + 1);
+    }
+    // ---- phase A: node update of plane z -> d_1 (smem + edges), gates of g_1
+    unsigned slow = 0;
+    if (doA) {
+      mbar_wait(smem_u32(&vbar[(qv + 1) & (kFuRV - 1)]), ((qv + 1) >> 2) & 1);
+      mbar_wait(smem_u32(&gbar[(z - zA) & (kFuRG - 1)]), ((z - zA) >> 1) & 1);
+      const double* V0 = vst + (qv & (kFuRV - 1)) * kFuVS;
+      const double* Vm = vst + ((qv - 1) & (kFuRV - 1)) * kFuVS;
+      const double* Vp = vst + ((qv + 1) & (kFuRV - 1)) * kFuVS;
+      const double* G0 = gst + ((z - zA) & (kFuRG - 1)) * kFuGS;
+      double* D0 = dst + (z % kFuRD) * kFuDS;
+      double* X = A.xch + ((size_t)blockIdx.x * kFuRX + (z & (kFuRX - 1))) * 4 * kFuTX;
+      const bool outp = z >= zb && z < ze;
+      const bool stz = stim_z<3>(g, z) && stx;
+      for (int r = 0; r < 4; ++r) {
+        const int ly = ly0 + 4 * r;
+        if (ly >= TYH) break;
+        const int cy = y0 + ly;
+        const int c = (ly + 1) * kFuVX + lx + 2;
+        const double vc = V0[c];
+        if (!(fabs(vc - a.vmid) <= a.vfast)) {
+          slow |= 1u << r;
+          continue;
+        }
+        const double xs = V0[c + dxm] + V0[c + dxp];
+        const double ys = V0[c + (cy > 0 ? -kFuVX : kFuVX)] + V0[c + (cy < g.n1 - 1 ? kFuVX : -kFuVX)];
+        const int gi = ly * kFuTX + lx;
+        NodeOut o = node_update_s<3, 1, 1, 0>(g, a, tab, Vm[c], vc, Vp[c], xs, ys, G0[gi],
+                                             G0[kFuGF + gi], G0[2 * kFuGF + gi], 0.0, nullptr, 0);
+        if (stz && cy >= g.st_lo[1] && cy <= g.st_hi[1]) o.o0 = fma(a.mue1, a.stim, o.o0);
+        D0[(ly + 1) * kFuDX + lx + 1] = o.o0;
+        if (lx == 0) X[ly] = o.o0;
+        if (lx == kFuTX - 1) X[kFuTX + ly] = o.o0;
+        if (ly == 0) X[2 * kFuTX + lx] = o.o0;
+        if (ly == TYH - 1) X[3 * kFuTX + lx] = o.o0;
+        if (outp) {
+          double* po = a.out + (cx + (long long)g.n0 * cy) + plane * z;
+          po[nn] = o.o1;
+          po[2 * nn] = o.o2;
+          po[3 * nn] = o.o3;
+          finacc = min(finacc,
+                       ~(unsigned)__double2hiint((o.o0 + o.o1) + (o.o2 + o.o3)) & 0x7ff00000u);
+          any_out = true;
+          if (a.last) {
+            glo = o.o1 < glo ? o.o1 : glo;
+            ghi = ghi < o.o1 ? o.o1 : ghi;
+            glo = o.o2 < glo ? o.o2 : glo;
+            ghi = ghi < o.o2 ? o.o2 : ghi;
+            glo = o.o3 < glo ? o.o3 : glo;
+            ghi = ghi < o.o3 ? o.o3 : ghi;
+          }
+        }
+      }
+    }
+    // nodes outside the fast window: reference-order ionic path, this plane
+    if (__syncthreads_or(slow != 0)) {
+      if (slow) {
+        const double* V0 = vst + (qv & (kFuRV - 1)) * kFuVS;
+        const double* Vm = vst + ((qv - 1) & (kFuRV - 1)) * kFuVS;
+        const double* Vp = vst + ((qv + 1) & (kFuRV - 1)) * kFuVS;
+        const double* G0 = gst + ((z - zA) & (kFuRG - 1)) * kFuGS;
+        double* D0 = dst + (z % kFuRD) * kFuDS;
+        double* X = A.xch + ((size_t)blockIdx.x * kFuRX + (z & (kFuRX - 1))) * 4 * kFuTX;
+        const bool outp = z >= zb && z < ze;
+        const bool stz = stim_z<3>(g, z) && stx;
+        for (int r = 0; r < 4; ++r) {
+          if (!(slow >> r & 1u)) continue;
+          const int ly = ly0 + 4 * r;
+          const int cy = y0 + ly;
+          const int c = (ly + 1) * kFuVX + lx + 2;
+          const double xs = V0[c + dxm] + V0[c + dxp];
+          const double ys =
+              V0[c + (cy > 0 ? -kFuVX : kFuVX)] + V0[c + (cy < g.n1 - 1 ? kFuVX : -kFuVX)];
+          const int gi = ly * kFuTX + lx;
+          const double stim = (stz && cy >= g.st_lo[1] && cy <= g.st_hi[1]) ? a.stim : 0.0;
+          double q[4] = {0.0, 0.0, 0.0, 0.0};
+          const NodeOut o = node_update_s<3, 1, 1, 1>(g, a, tab, Vm[c], V0[c], Vp[c], xs, ys,
+                                                      G0[gi], G0[kFuGF + gi], G0[2 * kFuGF + gi],
+                                                      stim, q, 1);
+          D0[(ly + 1) * kFuDX + lx + 1] = o.o0;
+          if (lx == 0) X[ly] = o.o0;
+          if (lx == kFuTX - 1) X[kFuTX + ly] = o.o0;
+          if (ly == 0) X[2 * kFuTX + lx] = o.o0;
+          if (ly == TYH - 1) X[3 * kFuTX + lx] = o.o0;
+          if (outp) {
+            double* po = a.out + (cx + (long long)g.n0 * cy) + plane * z;
+            po[nn] = o.o1;
+            po[2 * nn] = o.o2;
+            po[3 * nn] = o.o3;
+            bad_slow |= !finite_hi((o.o0 + o.o1) + (o.o2 + o.o3));
+            any_out = true;
+            if (a.last) {
+              glo = fmin(glo, fmin(o.o1, fmin(o.o2, o.o3)));
+              ghi = fmax(ghi, fmax(o.o1, fmax(o.o2, o.o3)));
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // publish d_1 plane z (its edges) to the neighbours
+    if (t == 0 && doA) {
+      __threadfence();
+      st_relaxed_gpu_u64(A.flags + blockIdx.x, A.epoch + (unsigned long long)(z + 1));
+    }
+  }
+  // ---- events (first failing check in program order wins), gate range
+  const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
+  if ((finacc == 0u || bad_slow) && !a.exex) {
+    bool inner = false;
+    for (int r = 0; r < 4; ++r) {
+      const int ly = ly0 + 4 * r;
+      if (ly >= TYH) break;
+      Col<3> c;
+      c.c0 = cx;
+      c.c1 = y0 + ly;
+      c.ip = cx + (long long)g.n0 * (y0 + ly);
+      c.z0 = zb;
+      c.z1 = ze;
+      c.valid = true;
+      inner |= inner_nonfinite<3>(g, Halo{}, a.g1, c, nbr_of<3>(g, c), a.eta);
+    }
+    atomicMin(a.event, base + (inner ? 1ull : (unsigned long long)(a.m + 1)));
+  }
+  if (bad_in) atomicMin(a.event, base + 2ull);
+  if (bad_out) atomicMin(a.event, base + (unsigned long long)(a.m + 1));
+  if (a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+  if (a.last) {
+    unsigned long long lo = any_out ? ord_of(glo) : ~0ull, hi = any_out ? ord_of(ghi) : 0ull;
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((t & 31) == 0) {
+      rlo[t >> 5] = lo;
+      rhi[t >> 5] = hi;
+    }
+    __syncthreads();
+    if (t == 0) {
+      for (int w = 1; w < kFuNT / 32; ++w) {
+        lo = min(lo, rlo[w]);
+        hi = max(hi, rhi[w]);
+      }
+      if (lo != ~0ull) atomicMin(a.gate_slot, lo);
+      if (hi != 0ull) atomicMax(a.gate_slot + 1, hi);
+    }
+  }
+}
+
 }  // namespace
 
 // Planes per block (z-chunk length): 16 amortises the block prologue (abort
@@ -2687,6 +3038,37 @@ cudaError_t launch_vin_fast(const Geom& g, const Halo& h, const FastInnerArgs& a
     else k_vin_fast<D, 1, 0><<<grd, blk, 0, st>>>(g, h, a);
   });
   return cudaGetLastError();
+}
+
+
+// Fused s = 1, m = 2 step: resident blocks per SM of k_fused2 (0 if it
+// cannot run) and the cooperative launch.
+int fused_blocks_per_sm() {
+  static int nb = -1;
+  if (nb < 0) {
+    cudaFuncSetAttribute(k_fused2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)fused_smem_bytes());
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fused2, kFuNT,
+                                                      fused_smem_bytes()) != cudaSuccess)
+      nb = 0;
+    cudaGetLastError();
+  }
+  return nb;
+}
+
+cudaError_t launch_fused2(const Geom& g, const FusedArgs& a, const TmaFused& tm, cudaStream_t st) {
+  if (fused_blocks_per_sm() < 1) return cudaErrorNotSupported;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(a.ntx * a.nty * a.nzc));
+  cfg.blockDim = dim3(kFuNT);
+  cfg.dynamicSmemBytes = fused_smem_bytes();
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // co-residency or an error, never a hang
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_fused2, g, a, tm);
 }
 
 }  // namespace emrkc_k
