@@ -377,6 +377,33 @@ int emrkc_dist_lockstep_run(emrkc_handle* const* hs, int32_t n, int32_t replay,
  * (the default) keeps the per-stage inner kernels (one V plane per level). */
 int emrkc_set_slab_min_depth(emrkc_handle* h, int64_t min_planes);
 
+/* estimate_spectral_radius (P/src/spectral.cpp:26-71) over z-slabs held by
+ * SEPARATE processes, one primitive at a time; the caller's host loop
+ * (paper_2401_01745_b200/dist.py slab_rho) moves the V ghost planes between
+ * ranks (any transport: NCCL send/recv of device planes) and chains the
+ * norms across ranks. Chained in global order (SoA block by block, slabs in
+ * z order, each slab continuing the running sum it received), the norms
+ * are the reference's serial sums bit for bit, so rho does not depend on
+ * the partition (SPEC: results independent of partitioning).
+ *   begin : v := this slab's part of v0 (host slab; null: of the
+ *           reference's seeded direction over the global state);
+ *   plane : copy this slab's first (side 0) / last (side 1) V plane of
+ *           field (0: v, 1: the state y) into device memory dst;
+ *   sumsq : acc_out = acc_in + sum x^2 over SoA block `block` of field, in
+ *           the reference's serial order;
+ *   fy    : fy = f(t, y) with the neighbours' y ghost planes (device; null
+ *           at the global boundary);
+ *   step  : v := f(t, y + q v) - fy, with y and v ghosts;
+ *   end   : copy the final direction (nullable) and release the work. */
+int emrkc_slab_power_begin(emrkc_handle* h, int32_t which, const double* v0_slab);
+int emrkc_slab_power_plane(emrkc_handle* h, int32_t field, int32_t side, double* dst);
+int emrkc_slab_power_sumsq(emrkc_handle* h, int32_t field, int32_t block, double acc_in,
+                           double* acc_out);
+int emrkc_slab_power_fy(emrkc_handle* h, double t, const double* gy_lo, const double* gy_hi);
+int emrkc_slab_power_step(emrkc_handle* h, double t, double q, const double* gy_lo,
+                          const double* gy_hi, const double* gv_lo, const double* gv_hi);
+int emrkc_slab_power_end(emrkc_handle* h, double* v_out_slab);
+
 /* Testing aid for the cross-process (IPC) path with fewer GPUs than ranks:
  * when a hook is set, emrkc_dist_run / emrkc_dist_replay synchronise the
  * handle's stream after every stencil level and call hook(ctx) (e.g. a

@@ -247,6 +247,12 @@ PROTOTYPES = {
     "emrkc_dist_lockstep_run": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(RunResult)]),
     "emrkc_set_slab_min_depth": (C.c_int, [C.c_void_p, C.c_int64]),
     "emrkc_set_level_hook": (C.c_int, [C.c_void_p, LEVEL_HOOK, C.c_void_p]),
+    "emrkc_slab_power_begin": (C.c_int, [C.c_void_p, C.c_int32, DP]),
+    "emrkc_slab_power_plane": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "emrkc_slab_power_sumsq": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_double, DP]),
+    "emrkc_slab_power_fy": (C.c_int, [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]),
+    "emrkc_slab_power_step": (C.c_int, [C.c_void_p, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "emrkc_slab_power_end": (C.c_int, [C.c_void_p, DP]),
     "emrkc_vctx_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     "emrkc_vctx_destroy": (None, [C.c_void_p]),
     "emrkc_vctx_last_error": (C.c_char_p, [C.c_void_p]),

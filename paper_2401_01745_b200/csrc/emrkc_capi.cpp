@@ -344,6 +344,10 @@ struct emrkc_handle {
                                     // on B200 than the two-kernel step)
   int fu_ntx = 0, fu_nty = 0, fu_nzc = 0;  // 0: not planned / not possible
   bool fu_planned = false;
+  // slab power iteration driven across processes (emrkc_slab_power_*)
+  double* sp_v[2] = {nullptr, nullptr};
+  double* sp_fy = nullptr;
+  int sp_code = -1, sp_a = 0;
   double* fu_xch = nullptr;
   unsigned long long* fu_flags = nullptr;
   unsigned long long fu_epoch = 0;
@@ -1356,6 +1360,8 @@ void emrkc_destroy(emrkc_handle* h) {
   if (h->d_red) cudaFree(h->d_red);
   if (h->d_rel) cudaFree(h->d_rel);
   if (h->fu_xch) cudaFree(h->fu_xch);
+  for (auto p : {h->sp_v[0], h->sp_v[1], h->sp_fy})
+    if (p) cudaFree(p);
   if (h->fu_flags) cudaFree(h->fu_flags);
   for (auto& u : h->mr_u)
     if (u) cudaFree(u);
@@ -2960,3 +2966,109 @@ int32_t emrkc_fused_active(emrkc_handle* h) {
   if (!h || !h->plan_uploaded) return 0;
   return use_fused(h, h->plan) ? 1 : 0;
 }
+
+// ---------------------------------------------------------------------------
+// estimate_spectral_radius over z-slabs held by separate processes
+// (P/src/spectral.cpp:26-71), one primitive at a time; the host loop
+// (paper_2401_01745_b200/dist.py slab_rho) moves the V ghost planes between
+// ranks and chains the norms across ranks in the reference's serial order.
+// ---------------------------------------------------------------------------
+int emrkc_slab_power_begin(emrkc_handle* h, int32_t which, const double* v0_slab) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
+  int code = 0;
+  if (rhs_code(h, which, &code))
+    return set_err(h, EMRKC_EINVAL, "estimate_rho: unknown rhs %d", which);
+  int rc = use_device(h);
+  if (rc) return rc;
+  for (int k = 0; k < 2; ++k)
+    if (!h->sp_v[k]) CK(h, cudaMalloc(&h->sp_v[k], sizeof(double) * h->len));
+  if (!h->sp_fy) CK(h, cudaMalloc(&h->sp_fy, sizeof(double) * h->len));
+  std::vector<double> local;
+  if (v0_slab) {
+    local.assign(v0_slab, v0_slab + h->len);
+  } else {  // this slab's part of the reference's seeded direction over the global state
+    std::vector<double> v0(4 * nodes_of(&h->p));
+    seeded_direction(v0);
+    scatter_slab(h, v0, nodes_of(&h->p), local);
+  }
+  CK(h, cudaMemcpy(h->sp_v[0], local.data(), sizeof(double) * h->len, cudaMemcpyHostToDevice));
+  h->sp_code = code;
+  h->sp_a = 0;
+  return EMRKC_OK;
+}
+
+int emrkc_slab_power_plane(emrkc_handle* h, int32_t field, int32_t side, double* dst) {
+  if (!h || !dst) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->sp_code < 0) return set_err(h, EMRKC_ESTATE, "slab power iteration not begun");
+  if (field < 0 || field > 1 || side < 0 || side > 1)
+    return set_err(h, EMRKC_EINVAL, "slab_power_plane: field / side must be 0 or 1");
+  int rc = use_device(h);
+  if (rc) return rc;
+  const double* x = field == 0 ? h->sp_v[h->sp_a] : h->buf[h->cur];
+  const int64_t pl = h->geom.plane;
+  CK(h, cudaMemcpyAsync(dst, x + (side ? h->nn - pl : 0), sizeof(double) * pl,
+                        cudaMemcpyDeviceToDevice, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return EMRKC_OK;
+}
+
+int emrkc_slab_power_sumsq(emrkc_handle* h, int32_t field, int32_t block, double acc_in,
+                           double* acc_out) {
+  if (!h || !acc_out) return set_global(EMRKC_EINVAL, "null argument");
+  if (h->sp_code < 0) return set_err(h, EMRKC_ESTATE, "slab power iteration not begun");
+  if (field < 0 || field > 1 || block < 0 || block > 3)
+    return set_err(h, EMRKC_EINVAL, "slab_power_sumsq: field 0/1, block 0..3");
+  int rc = use_device(h);
+  if (rc) return rc;
+  const double* x = (field == 0 ? h->sp_v[h->sp_a] : h->buf[h->cur]) + block * h->nn;
+  CK(h, emrkc_k::launch_sumsq_serial(x, h->nn, acc_in, h->d_red, h->stream));
+  CK(h, cudaMemcpyAsync(acc_out, h->d_red, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return EMRKC_OK;
+}
+
+int emrkc_slab_power_fy(emrkc_handle* h, double t, const double* gy_lo, const double* gy_hi) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (h->sp_code < 0) return set_err(h, EMRKC_ESTATE, "slab power iteration not begun");
+  int rc = use_device(h);
+  if (rc) return rc;
+  Halo hh{};
+  hh.lo = gy_lo;
+  hh.hi = gy_hi;
+  CK(h, emrkc_k::launch_rhs(h->geom, hh, h->sp_code, h->buf[h->cur], stim_rate_at(&h->p, t),
+                            h->sp_fy, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return EMRKC_OK;
+}
+
+int emrkc_slab_power_step(emrkc_handle* h, double t, double q, const double* gy_lo,
+                          const double* gy_hi, const double* gv_lo, const double* gv_hi) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (h->sp_code < 0) return set_err(h, EMRKC_ESTATE, "slab power iteration not begun");
+  if ((gy_lo == nullptr) != (gv_lo == nullptr) || (gy_hi == nullptr) != (gv_hi == nullptr))
+    return set_err(h, EMRKC_EINVAL, "slab_power_step: y and v ghosts come in pairs");
+  int rc = use_device(h);
+  if (rc) return rc;
+  const int nb = emrkc_k::power_blocks();
+  const int a = h->sp_a;
+  CK(h, emrkc_k::launch_power(h->geom, h->sp_code, h->buf[h->cur], h->sp_v[a], q, h->sp_fy,
+                              stim_rate_at(&h->p, t), h->sp_v[1 - a], gy_lo, gy_hi, gv_lo,
+                              gv_hi, h->d_red, nb, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->sp_a = 1 - a;
+  return EMRKC_OK;
+}
+
+int emrkc_slab_power_end(emrkc_handle* h, double* v_out_slab) {
+  if (!h) return set_global(EMRKC_EINVAL, "null handle");
+  if (h->sp_code < 0) return set_err(h, EMRKC_ESTATE, "slab power iteration not begun");
+  int rc = use_device(h);
+  if (rc) return rc;
+  if (v_out_slab)
+    CK(h, cudaMemcpy(v_out_slab, h->sp_v[h->sp_a], sizeof(double) * h->len,
+                     cudaMemcpyDeviceToHost));
+  h->sp_code = -1;
+  return EMRKC_OK;
+}
+

@@ -89,6 +89,114 @@ class DistContext:
     world: int
     exchange: object  # callable(bytes) -> list[bytes] (all ranks, rank order)
     reduce: object    # callable(dict) -> list[dict]   (all ranks, rank order)
+    # slab power iteration (slab_rho): halo(lo_plane, hi_plane) -> (ghost_lo,
+    # ghost_hi) sends this slab's first plane down and last plane up and
+    # returns the neighbours' (None at the global boundary); chain(fn, acc)
+    # runs acc = fn(acc) on rank 0, 1, ... in turn and returns the last
+    # rank's result on every rank
+    halo: object = None
+    chain: object = None
+
+
+def slab_rho(sp, ctx: DistContext, which: int, t: float = 0.0, v0_slab=None,
+             rho0: float = 0.0):
+    """estimate_spectral_radius (P/src/spectral.cpp:26-71) over the z-slabs
+    of ``ctx.world`` ranks, ``sp`` this rank's slab (emrkc_slab_power_*
+    through ``DeviceSlabPower``, or a host stand-in in the CPU tests).
+
+    Every norm is the reference's serial sum (P/src/spectral.cpp:10-14) over
+    the global vector: SoA block by block, each rank continuing the running
+    sum of the rank below (``ctx.chain``); V ghost planes of y (once) and of
+    v (each iteration) come from the neighbours (``ctx.halo``). So q, z =
+    y + q v, f(z) - f(y) and rho are bit-identical to the single-grid
+    estimate for ANY partition, with the reference's iteration count."""
+    import math
+
+    from .monodomain import RhoEstimate
+
+    sp.begin(which, v0_slab)
+
+    def norm(field):
+        acc = 0.0
+        for b in range(4):
+            acc = ctx.chain(lambda a, b=b: sp.sumsq(field, b, a), acc)
+        return math.sqrt(acc)
+
+    def ghosts(field):
+        return ctx.halo(sp.plane(field, 0), sp.plane(field, 1))
+
+    nv = norm(0)
+    if nv == 0.0:
+        sp.end()
+        raise ValueError("estimate_spectral_radius: v0 must be nonzero")
+    ny = norm(1)
+    delta = max(ny, 1e-8) * 1e-8
+    gy = ghosts(1)
+    sp.fy(t, *gy)
+    rho, rho_old, it, converged = rho0, 0.0, 0, True
+    while it == 0 or abs(rho - rho_old) >= 1e-2 * rho:
+        if it >= 50:
+            converged = False
+            break
+        rho_old = rho
+        q = delta / nv
+        gv = ghosts(0)
+        sp.step(t, q, gy[0], gy[1], gv[0], gv[1])
+        nv = norm(0)
+        if nv < 1e-300:  # locally null operator (P/src/spectral.cpp:61-66)
+            return RhoEstimate(0.0, it + 1, True, 1.05, sp.end())
+        rho = nv / delta
+        it += 1
+    return RhoEstimate(rho * 1.05, it, converged, 1.05, sp.end())
+
+
+class DeviceSlabPower:
+    """This rank's slab of the power iteration on the device
+    (emrkc_slab_power_*); planes travel as torch CUDA tensors."""
+
+    def __init__(self, op):
+        import torch
+
+        self.op = op
+        self.lib = _lib()
+        prob = op.problem
+        self.plane_len = int(prob.n_nodes // int(prob.n[prob.dim - 1]))
+        self.torch = torch
+
+    def _ptr(self, x):
+        return None if x is None else C.c_void_p(x.data_ptr())
+
+    def begin(self, which, v0_slab=None):
+        v0 = None if v0_slab is None else np.ascontiguousarray(v0_slab, dtype=np.float64)
+        _check(self.lib.emrkc_slab_power_begin(self.op.handle, which,
+                                               None if v0 is None else capi.dptr(v0)),
+               self.op.handle)
+
+    def plane(self, field, side):
+        out = self.torch.empty(self.plane_len, dtype=self.torch.float64, device="cuda")
+        _check(self.lib.emrkc_slab_power_plane(self.op.handle, field, side,
+                                               C.c_void_p(out.data_ptr())), self.op.handle)
+        return out
+
+    def sumsq(self, field, block, acc):
+        out = C.c_double()
+        _check(self.lib.emrkc_slab_power_sumsq(self.op.handle, field, block, acc,
+                                               C.byref(out)), self.op.handle)
+        return out.value
+
+    def fy(self, t, glo, ghi):
+        _check(self.lib.emrkc_slab_power_fy(self.op.handle, t, self._ptr(glo), self._ptr(ghi)),
+               self.op.handle)
+
+    def step(self, t, q, gylo, gyhi, gvlo, gvhi):
+        _check(self.lib.emrkc_slab_power_step(self.op.handle, t, q, self._ptr(gylo),
+                                              self._ptr(gyhi), self._ptr(gvlo), self._ptr(gvhi)),
+               self.op.handle)
+
+    def end(self):
+        v = np.empty(self.op.len)
+        _check(self.lib.emrkc_slab_power_end(self.op.handle, capi.dptr(v)), self.op.handle)
+        return v
 
 
 class DistSlab:
@@ -163,7 +271,48 @@ def torch_context():
         dist.all_gather_object(out, pickle.loads(pickle.dumps(d)))
         return out
 
-    return DistContext(rank, world, exchange, reduce)
+    return DistContext(rank, world, exchange, reduce, *torch_p2p(rank, world))
+
+
+def torch_p2p(rank: int, world: int):
+    """(halo, chain) over torch.distributed point-to-point (NCCL: device
+    planes; gloo: host tensors)."""
+    import torch
+    import torch.distributed as dist
+
+    def halo(lo, hi):
+        # gloo moves host tensors: device planes go through host copies
+        dev = lo.device
+        host = dist.get_backend() != "nccl" and dev.type == "cuda"
+        if host:
+            lo, hi = lo.cpu(), hi.cpu()
+        ops, glo, ghi = [], None, None
+        if rank > 0:
+            glo = torch.empty_like(lo)
+            ops += [dist.P2POp(dist.isend, lo, rank - 1), dist.P2POp(dist.irecv, glo, rank - 1)]
+        if rank + 1 < world:
+            ghi = torch.empty_like(hi)
+            ops += [dist.P2POp(dist.isend, hi, rank + 1), dist.P2POp(dist.irecv, ghi, rank + 1)]
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        if host:
+            glo = None if glo is None else glo.to(dev)
+            ghi = None if ghi is None else ghi.to(dev)
+        return glo, ghi
+
+    def chain(fn, acc):
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        buf = torch.tensor([acc], dtype=torch.float64, device=dev)
+        if rank > 0:
+            dist.recv(buf, rank - 1)
+        buf.fill_(fn(float(buf[0])))
+        if rank + 1 < world:
+            dist.send(buf, rank + 1)
+        dist.broadcast(buf, world - 1)
+        return float(buf[0])
+
+    return halo, chain
 
 
 def slab_initial_state(w, part: Partition) -> np.ndarray:
@@ -187,22 +336,16 @@ def slab_initial_state(w, part: Partition) -> np.ndarray:
     return np.concatenate(blocks)
 
 
-def _rho_rank0(ctx, w, local):
-    """rho_F, rho_S once at t = 0 on the whole grid (P/src/simulate.cpp:158-159),
-    estimated on rank 0 and broadcast."""
-    import torch
-    import torch.distributed as dist
-
-    rho = torch.zeros(2, dtype=torch.float64, device="cuda")
-    if ctx.rank == 0:
-        full = MonodomainOperator(w.problem, local)
-        full.set_state(w.initial_state())
-        rho[0] = full.estimate_spectral_radius(capi.EMRKC_RHS_F).rho
-        rho[1] = (w.rho_S_forced if w.rho_S_forced is not None
-                  else full.estimate_spectral_radius(capi.EMRKC_RHS_S).rho)
-        full.close()
-    dist.broadcast(rho, 0)
-    return float(rho[0]), float(rho[1])
+def rho_slabs(ctx, w, slab):
+    """rho_F, rho_S once at t = 0 (P/src/simulate.cpp:158-159) by the
+    distributed power iteration over the ranks' slabs (``slab_rho``): no
+    rank holds the whole grid, and the result is bit-identical to the
+    single-grid estimate."""
+    sp = DeviceSlabPower(slab.op)
+    rF = slab_rho(sp, ctx, capi.EMRKC_RHS_F, 0.0).rho
+    rS = (w.rho_S_forced if w.rho_S_forced is not None
+          else slab_rho(sp, ctx, capi.EMRKC_RHS_S, 0.0).rho)
+    return rF, rS
 
 
 def _timed(ctx, w, local, warmup, steps, ClockSampler=None):
@@ -211,11 +354,11 @@ def _timed(ctx, w, local, warmup, steps, ClockSampler=None):
     import torch
     import torch.distributed as dist
 
-    rF, rS = _rho_rank0(ctx, w, local)
     slab = DistSlab(w.problem, ctx, local)
     slab.link()
     y0 = slab_initial_state(w, slab.part)
     slab.op.set_state(y0)
+    rF, rS = rho_slabs(ctx, w, slab)
     slab.run(0, warmup, w.dt, rF, rS, w.eps)
     slab.op.set_state(y0)
     dist.barrier()
@@ -281,12 +424,13 @@ def _e2e(ctx, slab, w, y0, rho, k):
 
 
 def bench_main(args, w, metric, config_of, hbm_peak, ClockSampler):
-    """bench.py --gpus N under torchrun. Main line: weak scaling -- ``w``
-    repeated N times along z, one copy per GPU (``workloads.z_scaled``), so
-    per-GPU work equals the N = 1 line; value = global nodes x K / max over
-    ranks of the device time. ``also``: strong scaling of the config-4 grid
-    (BASELINE's partitioned config, north_star's efficiency target) over the
-    same N GPUs."""
+    """bench.py --gpus N under torchrun. Main line: STRONG scaling of ``w``
+    (the N = 1 headline, config 4's grid) split into N z-slabs, so the
+    driver's per-N ratio v(N) / (N v(1)) is north_star's parallel
+    efficiency E(N); value = global nodes x K / max over ranks of the device
+    time. rho comes from the distributed power iteration over the slabs.
+    ``also``: WEAK scaling of BASELINE configs[1] (128^3 repeated N times
+    along z, one copy per GPU)."""
     import json
     import os
 
@@ -299,11 +443,10 @@ def bench_main(args, w, metric, config_of, hbm_peak, ClockSampler):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
     ctx = torch_context()
-    ww = workloads.z_scaled(w, ctx.world)
-    ms, rec, clocks, slab, rho, y0 = _timed(ctx, ww, local, args.warmup, args.steps, ClockSampler)
-    value = ww.n_nodes * rec["timed_steps"] / (ms * 1e-3)
+    ms, rec, clocks, slab, rho, y0 = _timed(ctx, w, local, args.warmup, args.steps, ClockSampler)
+    value = w.n_nodes * rec["timed_steps"] / (ms * 1e-3)
     try:
-        e2e = _e2e(ctx, slab, ww, y0, rho, 20)
+        e2e = _e2e(ctx, slab, w, y0, rho, min(args.steps, 10))
     except Exception as ex:  # reported, not fatal: the device line stands
         e2e = {"error": f"{type(ex).__name__}: {ex}"}
     slab.op.close()
@@ -312,37 +455,39 @@ def bench_main(args, w, metric, config_of, hbm_peak, ClockSampler):
     also = []
     if not args.no_extra:
         try:
-            w4 = workloads.get("hh3d_512x512x256")
-            k4 = max(5, min(args.steps, 50))
-            ms4, rec4, _, slab4, _, _ = _timed(ctx, w4, local, args.warmup, k4)
-            slab4.op.close()
-            del slab4
-            k4 = rec4["timed_steps"]
-            v4 = w4.n_nodes * k4 / (ms4 * 1e-3)
-            also.append({"workload": w4.name, "scaling": "strong", "n_gpus": ctx.world,
-                         "value": v4, "unit": "node-steps/s", "steps": k4,
-                         "ms_per_step": ms4 / k4, "s": rec4["s"], "m": rec4["m"],
-                         "step_frac_per_gpu": 64 * v4 / ctx.world / 1e9 / peak})
+            wk = workloads.z_scaled(workloads.get("hh3d_128x128x128"), ctx.world)
+            kk = max(5, min(args.steps, 50))
+            msk, reck, _, slabk, _, _ = _timed(ctx, wk, local, args.warmup, kk)
+            slabk.op.close()
+            del slabk
+            kk = reck["timed_steps"]
+            vk = wk.n_nodes * kk / (msk * 1e-3)
+            also.append({"workload": wk.name, "scaling": "weak", "n_gpus": ctx.world,
+                         "value": vk, "unit": "node-steps/s", "steps": kk,
+                         "ms_per_step": msk / kk, "s": reck["s"], "m": reck["m"],
+                         "step_frac_per_gpu": 64 * vk / ctx.world / 1e9 / peak})
         except Exception as ex:
-            also.append({"workload": "hh3d_512x512x256", "error": f"{type(ex).__name__}: {ex}"})
+            also.append({"workload": "hh3d_128x128x128 (weak)",
+                         "error": f"{type(ex).__name__}: {ex}"})
     if ctx.rank == 0:
         gbs = 64 * value / 1e9 / ctx.world
-        cfg = config_of(ww, ctx.world)
-        cfg["weak_scaling_of"] = w.name
-        cfg["nodes_per_gpu"] = w.n_nodes
+        cfg = config_of(w, ctx.world)
+        cfg["nodes_per_gpu"] = w.n_nodes // ctx.world
         line = {
             "metric": metric, "value": value, "unit": "node-steps/s", "n_gpus": ctx.world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / rec["timed_steps"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded HH resting state + N(0, 0.1 mV) V noise)",
             "config": cfg,
             "plan": {"s": rec["s"], "m": rec["m"], "rho_F": rho[0], "rho_S": rho[1],
+                     "rho": "distributed power iteration over the slabs (norms chained "
+                            "across ranks in the reference's serial order)",
                      "timed_steps": rec["timed_steps"],
                      "timed_note": "one run of the steps from the seeded state; if a slab hits "
                                    "NumericalAbort/the guard, every rank is timed up to the "
                                    "earliest abort step"},
-            "gpu_launches": int(args.steps * rec["s"] * rec["m"]),
+            "gpu_launches": int(rec["timed_steps"] * rec["s"] * rec["m"]),
             "clocks": clocks,
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",

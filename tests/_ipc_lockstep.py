@@ -22,7 +22,8 @@ def main(out):
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     ctx = pdist.DistContext(rank, world,
-                            lambda b: _gather(b, world), lambda d: _gather(d, world))
+                            lambda b: _gather(b, world), lambda d: _gather(d, world),
+                            *pdist.torch_p2p(rank, world))
     results = {}
     # key@tb: rho_F forced up to m = 5 with s = 1, so the inner stages 2..5
     # run temporally blocked with the wide (K = 4 plane) d_1 halo
@@ -43,6 +44,11 @@ def main(out):
         lib = _lib()
         assert lib.emrkc_set_level_hook(slab.op._h, barrier, None) == 0
         slab.set_global_state(w.initial_state())
+        # rho by the distributed power iteration over the slabs (norms
+        # chained across ranks): bit-identical to the whole-grid estimate
+        sp = pdist.DeviceSlabPower(slab.op)
+        dF = pdist.slab_rho(sp, ctx, capi.EMRKC_RHS_F, 0.0)
+        dS = pdist.slab_rho(sp, ctx, capi.EMRKC_RHS_S, 0.0)
         rec = slab.run(0, n, w.dt, rF, rS, w.eps)
         y = slab.op.get_state()
         ys = _gather(y, world)
@@ -62,6 +68,7 @@ def main(out):
             results[key + "/rec"] = np.array([rec["s"], rec["m"], rec["aborted"], rec["n_fF"]])
             results[key + "/rho"] = np.array([rF, rS])
             results[key + "/n"] = np.array([n])
+            results[key + "/drho"] = np.array([dF.rho, dF.iterations, dS.rho, dS.iterations])
     if rank == 0:
         np.savez(out, **results)
     dist.barrier()

@@ -139,3 +139,111 @@ def test_combine_is_order_independent():
     c = rec()
     assert dist.combine([a, b, c])["abort_inner"] == 1
     assert dist.combine([c, b, a]) == dist.combine([a, b, c]) | {}
+
+
+# ---- distributed power iteration (dist.slab_rho) ------------------------------
+
+class HostSlabPower:
+    """CPU stand-in for DeviceSlabPower: a z-slab of a 4-block state
+    (nz planes of P nodes per block); f = z-Laplacian on the V block (mirror
+    at the global ends, ghosts at slab faces) plus a pointwise nonlinearity,
+    gate rows pointwise. Norms continue the running sum in serial order."""
+
+    P, NZ = 6, 24
+
+    def __init__(self, y_global, v_global, z0, z1):
+        import numpy as np
+        import torch
+
+        self.np, self.torch = np, torch
+        self.z0, self.z1 = z0, z1
+        nn = self.P * self.NZ
+        sl = lambda g: np.concatenate([g[b * nn + z0 * self.P: b * nn + z1 * self.P] for b in range(4)])
+        self.y = sl(y_global)
+        self.v0 = sl(v_global)
+        self.nl = (z1 - z0) * self.P
+
+    def f(self, x, glo, ghi):
+        np = self.np
+        nl, P = self.nl, self.P
+        V = x[:nl].reshape(-1, P)
+        lo = glo.numpy().reshape(1, P) if glo is not None else V[1:2]
+        hi = ghi.numpy().reshape(1, P) if ghi is not None else V[-2:-1]
+        ext = np.concatenate([lo, V, hi])
+        out = np.empty_like(x)
+        out[:nl] = (2.5 * ((ext[:-2] - 2.0 * V) + ext[2:]) - 0.01 * V * V * V).ravel()
+        for b in range(1, 4):
+            out[b * nl:(b + 1) * nl] = -(0.5 + 0.1 * b) * x[b * nl:(b + 1) * nl] * x[:nl]
+        return out
+
+    def begin(self, which, v0_slab=None):
+        self.v = self.v0.copy() if v0_slab is None else v0_slab.copy()
+
+    def plane(self, field, side):
+        x = self.v if field == 0 else self.y
+        V = x[:self.nl]
+        return self.torch.from_numpy((V[:self.P] if side == 0 else V[-self.P:]).copy())
+
+    def sumsq(self, field, block, acc):
+        np = self.np
+        x = (self.v if field == 0 else self.y)[block * self.nl:(block + 1) * self.nl]
+        return float(np.add.accumulate(np.concatenate([[acc], x * x]))[-1])  # serial order
+
+    def fy(self, t, glo, ghi):
+        self.fyv = self.f(self.y, glo, ghi)
+
+    def step(self, t, q, gylo, gyhi, gvlo, gvhi):
+        zl = None if gylo is None else gylo + q * gvlo
+        zh = None if gyhi is None else gyhi + q * gvhi
+        self.v = self.f(self.y + q * self.v, zl, zh) - self.fyv
+
+    def end(self):
+        return self.v
+
+
+def _rho_worker(rank, world, port, q):
+    import numpy as np
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    halo, chain = dist.torch_p2p(rank, world)
+    ctx = dist.DistContext(rank, world, None, None, halo, chain)
+    P, NZ = HostSlabPower.P, HostSlabPower.NZ
+    rng = np.random.default_rng(3)
+    y = np.concatenate([-65.0 + rng.normal(0, 2.0, NZ * P)] + [rng.uniform(0, 1, NZ * P)] * 3)
+    v = rng.uniform(-1, 1, 4 * NZ * P)
+    z0, z1 = NZ * rank // world, NZ * (rank + 1) // world
+    est = dist.slab_rho(HostSlabPower(y, v, z0, z1), ctx, 0)
+    q.put((rank, est.rho, est.iterations, est.converged))
+    tdist.destroy_process_group()
+
+
+def rho_world(world):
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rho_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, rho, it, conv = q.get(timeout=120)
+        res[r] = (rho, it, conv)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_slab_rho_bitwise_independent_of_partition():
+    """The norms chained across ranks in serial order: rho and the iteration
+    count are bit-identical for 1, 2 and 3 slabs, on every rank."""
+    one = rho_world(1)[0]
+    assert one[1] > 1 and one[2]
+    for world in (2, 3):
+        res = rho_world(world)
+        assert all(res[r] == one for r in range(world)), (world, res, one)

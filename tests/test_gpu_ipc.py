@@ -45,3 +45,22 @@ def test_ipc_slabs_bitwise(ranks, name):
         assert (s, m) == (1, 5)  # K = 4 blocked stages: the widest halo
     got = two_ranks[name + "/y"]
     assert np.array_equal(got, y), np.abs(got - y).max()
+
+
+@pytest.mark.parametrize("name", ["p3d_48_s2m2", "hh2d_256x256", "hh3d_sweep_25"])
+def test_distributed_rho_bitwise(ranks, name):
+    """rho_F / rho_S by the distributed power iteration over 2 / 3 ranks'
+    slabs (dist.slab_rho, emrkc_slab_power_*) equal the whole-grid estimate
+    bit for bit, with the same iteration counts."""
+    from paper_2401_01745_b200 import capi
+
+    w = workloads.get(name)
+    op = MonodomainOperator(w.problem)
+    op.set_state(w.initial_state())
+    eF = op.estimate_spectral_radius(capi.EMRKC_RHS_F)
+    eS = op.estimate_spectral_radius(capi.EMRKC_RHS_S)
+    op.close()
+    rF, iF, rS, iS = ranks[name + "/drho"]
+    assert (rF, int(iF)) == (eF.rho, eF.iterations)
+    assert (rS, int(iS)) == (eS.rho, eS.iterations)
+
