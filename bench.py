@@ -73,6 +73,8 @@ KERNEL_BYTES = {
     ("last", "outer"): 48,
     ("fused", "first_outer"): 64,  # k_fused2: g_0 in (4 fields), g_1 out (4); d_1 stays on chip
     ("fused_skip", None): 0,       # level 2 ran inside the fused launch
+    ("zpipe", "first_outer"): 64,  # the whole z-pipelined step (node + inner chunks, 2 streams)
+    ("zpipe_skip", None): 0,       # timed inside the step's event pair
 }
 KERNEL_ROLES = {"m1": ("node", "m = 1: whole outer stage"),
                 "first": ("node", "m >= 2: ionic + inner stage 1"),
@@ -83,7 +85,10 @@ KERNEL_ROLES = {"m1": ("node", "m = 1: whole outer stage"),
                 "tb_skip": ("vin", "fused into the k = 2 launch"),
                 "fused": ("fused2", "s = 1, m = 2: node update + inner stage 2 + outer update "
                                     "in one persistent pass"),
-                "fused_skip": ("fused2", "level 2 ran inside the fused launch")}
+                "fused_skip": ("fused2", "level 2 ran inside the fused launch"),
+                "zpipe": ("zpipe", "s = 1: node-kernel z-chunks overlapped with the inner-stage "
+                                   "chunks on a second stream (one event pair per step)"),
+                "zpipe_skip": ("zpipe", "timed with the step")}
 
 
 def kernel_name(kind: str, problem) -> str:
@@ -98,6 +103,8 @@ def kernel_name(kind: str, problem) -> str:
     role, what = KERNEL_ROLES[kind]
     if role == "fused2":
         return f"k_fused2 ({what})"
+    if role == "zpipe":
+        return f"k_node_tma + k_vin_tma_r z-pipelined step ({what})"
     fam = {3: "tma", 1: "pipe", 2: "persist" if role == "node" else "pipe", 0: "fast"}[pipe]
     if kind.startswith("tb"):
         fam = "tb"
@@ -112,12 +119,14 @@ def tb_active(problem, m: int) -> bool:
             and int(os.environ.get("EMRKC_TB") or 0) != 0 and 2 <= m - 1 <= 4)
 
 
-def launch_kinds(s: int, m: int, problem=None, fused: bool = False):
-    """(kind, outer) of each launch of one step, in launch order (fused: the
-    library runs the s = 1, m = 2 step as one k_fused2 pass,
-    emrkc_fused_active)."""
-    if fused:
+def launch_kinds(s: int, m: int, problem=None, fused: int = 0):
+    """(kind, outer) of each launch of one step, in launch order
+    (emrkc_fused_active: 1 = the s = 1, m = 2 step as one k_fused2 pass,
+    2 = the z-pipelined step, timed as one unit)."""
+    if fused == 1:
         return [("fused", "first_outer"), ("fused_skip", None)]
+    if fused == 2:
+        return [("zpipe", "first_outer")] + [("zpipe_skip", None)] * (s * m - 1)
     out = []
     tb = problem is not None and tb_active(problem, m)
     for j in range(1, s + 1):
@@ -463,7 +472,7 @@ def measure_device(w, device, warmup, steps, with_e2e=True, clocks=None, ramp_s=
                        (f" up to its NumericalAbort/guard at step {kr}" if kr < w.n_steps else "") +
                        ", best of 3, device time of the run, no L2 flush between steps"}
     out = {"op": op, "y0": y0, "rF": rF, "rS": rS, "s": rep.s, "m": rep.m, "run": run,
-           "fused": bool(lib.emrkc_fused_active(op.handle)),
+           "fused": int(lib.emrkc_fused_active(op.handle)),
            "launch_ms": launch_ms.reshape(steps, per), "res": results[-1], "steps": steps,
            "repeats": len(chunks), "aborted": any(r.aborted for r in results),
            "abort_at": kr if kr < w.n_steps else None}
@@ -553,9 +562,19 @@ def measure_e2e_run(op, w, y0, rF, rS, reps=3):
                    "run_simulation's loop) + emrkc_get_state"}
 
 
+def gpu_launches_per_step(m) -> int:
+    """Kernel launches of one step: 1 (fused), K node chunks + K (m - 1)
+    inner chunks (z-pipelined, EMRKC_ZPIPE=K), else s m."""
+    if m["fused"] == 1:
+        return 1
+    if m["fused"] == 2:
+        return int(os.environ.get("EMRKC_ZPIPE") or 0) * m["m"]
+    return m["s"] * m["m"]
+
+
 def roofline_of(m, w, peak, peak_kind):
     per_pos = m["launch_ms"].mean(axis=0)
-    kinds = launch_kinds(m["s"], m["m"], w.problem, m.get("fused", False))
+    kinds = launch_kinds(m["s"], m["m"], w.problem, m.get("fused", 0))
     dom = int(np.argmax(per_pos))
     kb = KERNEL_BYTES[kinds[dom]]
     achieved = kb * w.n_nodes / (per_pos[dom] * 1e-3) / 1e9
@@ -604,7 +623,7 @@ def b200_arm(args, w):
         "e2e": m["e2e"],
         "e2e_run": m["e2e_run"],
         "run": m["run"],
-        "gpu_launches": int(args.steps * (1 if m["fused"] else m["s"] * m["m"])),
+        "gpu_launches": int(args.steps * gpu_launches_per_step(m)),
         "clocks": clocks,
     }
     y0, rF, rS = m["y0"], m["rF"], m["rS"]

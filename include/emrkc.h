@@ -191,8 +191,11 @@ int emrkc_set_state(emrkc_handle* h, const double* y, int64_t len);
 int emrkc_get_state(emrkc_handle* h, double* y, int64_t len);
 /* Kernel plan of the handle's current step plan (after a step / run):
  * 1 when one step runs as the single fused pass (k_fused2: s = 1, m = 2,
- * 3-D whole grid), 0 when it runs as one launch per stencil level. A
- * diagnostic for benches and tests; no reference counterpart. */
+ * 3-D whole grid, EMRKC_FUSED=1), 2 when it runs z-pipelined (node-kernel
+ * chunks on the handle's stream, inner-stage chunks overlapping them on a
+ * second stream, EMRKC_ZPIPE=K chunks), 0 when it runs as one launch per
+ * stencil level. A diagnostic for benches and tests; no reference
+ * counterpart. */
 int32_t emrkc_fused_active(emrkc_handle* h);
 /* Device pointer of the current state (valid until the next step/run). */
 int emrkc_state_device_ptr(emrkc_handle* h, double** dptr);

@@ -339,6 +339,12 @@ struct emrkc_handle {
   emrkc_k::CgScalars* cg_h = nullptr;   // pinned host copy
   int* guard_d = nullptr;
   int zr_lo = -1, zr_hi = -1;  // node-kernel plane range override (< 0: all)
+  // z-pipelined step (EMRKC_ZPIPE): inner-stage chunks on a second stream,
+  // each chunk behind the node-kernel chunk it needs
+  cudaStream_t s_aux = nullptr;      // stream of the inner-stage chunks
+  cudaStream_t ls = nullptr;         // launch_level's stream (null: stream)
+  std::vector<cudaEvent_t> zp_ev;    // node chunk c done
+  cudaEvent_t zp_join = nullptr;     // inner chunks of the step done
   // fused s = 1, m = 2 step (k_fused2): tile plan, exchange ring, flags
   int fused = 0;                    // EMRKC_FUSED=1: the fused s = 1, m = 2 pass (slower
                                     // on B200 than the two-kernel step)
@@ -391,6 +397,8 @@ int set_err(emrkc_handle* h, int code, const char* fmt, ...) {
       return set_err((h), EMRKC_ECUDA, "%s: %s (%s:%d)", #call,              \
                      cudaGetErrorString(e_), __FILE__, __LINE__);            \
   } while (0)
+
+cudaStream_t lstream(const emrkc_handle* h) { return h->ls ? h->ls : h->stream; }
 
 int use_device(emrkc_handle* h) {
   CK(h, cudaSetDevice(h->device));
@@ -851,9 +859,9 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
     f.last = a.last;
     f.code_base = a.code_base;
     f.event = a.event;
-    CK(h, emrkc_k::launch_mrkc_stage(h->geom, f, h->stream));
+    CK(h, emrkc_k::launch_mrkc_stage(h->geom, f, lstream(h)));
     if (a.last && k == pl.m)  // gate range of the step's result (simulate.cpp:228)
-      CK(h, emrkc_k::launch_gate_range(h->geom, a.out, a.gate_slot, h->stream));
+      CK(h, emrkc_k::launch_gate_range(h->geom, a.out, a.gate_slot, lstream(h)));
     ++h->level;
     return EMRKC_OK;
   }
@@ -910,7 +918,7 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         int rc = tma_map_fused(h, f.g1, 0, &tm.v);
         if (!rc) rc = tma_map_fused(h, f.g1, 1, &tm.gates);
         if (rc) return rc;
-        CK(h, emrkc_k::launch_fused2(h->geom, fa, tm, h->stream));
+        CK(h, emrkc_k::launch_fused2(h->geom, fa, tm, lstream(h)));
         ++h->level;
         return EMRKC_OK;
       }
@@ -932,13 +940,13 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
           hn.kput_hi = hl.put_hi ? nbr_dghost(h, 1, par) : nullptr;
           signals = emrkc_k::halo_signals_pipe(h->geom) * hn.kput;
         }
-        CK(h, emrkc_k::launch_node_tma(h->geom, hn, f, tm, pl.m >= 2, h->stream));
+        CK(h, emrkc_k::launch_node_tma(h->geom, hn, f, tm, pl.m >= 2, lstream(h)));
       } else if (h->pipe == 2)
-        CK(h, emrkc_k::launch_node_persist(h->geom, hl, f, pl.m >= 2, h->stream));
+        CK(h, emrkc_k::launch_node_persist(h->geom, hl, f, pl.m >= 2, lstream(h)));
       else if (h->pipe)
-        CK(h, emrkc_k::launch_node_pipe(h->geom, hl, f, pl.m >= 2, h->stream));
+        CK(h, emrkc_k::launch_node_pipe(h->geom, hl, f, pl.m >= 2, lstream(h)));
       else
-        CK(h, emrkc_k::launch_node_fast(h->geom, hl, f, pl.m >= 2, h->stream));
+        CK(h, emrkc_k::launch_node_fast(h->geom, hl, f, pl.m >= 2, lstream(h)));
     } else if (use_tb(h, pl)) {
       // stages 2..m in one pass at k == 2; levels k > 2 launch nothing
       if (k == 2) {
@@ -976,7 +984,7 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
           if (!rc) rc = tma_map_box3(h, ht.hi, bx, by, 200 + K, &tm.d1hi, K);
         }
         if (rc) return rc;
-        CK(h, emrkc_k::launch_vin_tb(h->geom, ht, f, tm, h->stream));
+        CK(h, emrkc_k::launch_vin_tb(h->geom, ht, f, tm, lstream(h)));
         ++h->kstage;
         signals = emrkc_k::halo_signals_tb(h->geom);
       }
@@ -1020,20 +1028,20 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         if (!rc && k == pl.m && f.g2v) rc = tma_map(h, f.g2v, kTmaCenter, &tm.g2v, rm);
         if (!rc) rc = tma_ghosts(h, hl, &tm.glo, &tm.ghi, rm);
         if (rc) return rc;
-        CK(h, emrkc_k::launch_vin_tma(h->geom, hl, f, tm, h->stream));
+        CK(h, emrkc_k::launch_vin_tma(h->geom, hl, f, tm, lstream(h)));
         signals = emrkc_k::halo_signals_vin(h->geom);
       } else if (h->pipe)
-        CK(h, emrkc_k::launch_vin_pipe(h->geom, hl, f, h->stream));
+        CK(h, emrkc_k::launch_vin_pipe(h->geom, hl, f, lstream(h)));
       else
-        CK(h, emrkc_k::launch_vin_fast(h->geom, hl, f, h->stream));
+        CK(h, emrkc_k::launch_vin_fast(h->geom, hl, f, lstream(h)));
     }
     if (dist_linked(h)) dist_account(h, signals);
   } else if (pl.m == 1) {
-    CK(h, emrkc_k::launch_stage_m1(h->geom, hl, a, 0, h->stream));
+    CK(h, emrkc_k::launch_stage_m1(h->geom, hl, a, 0, lstream(h)));
   } else if (k == 1) {
-    CK(h, emrkc_k::launch_stage_first(h->geom, hl, a, 0, h->stream));
+    CK(h, emrkc_k::launch_stage_first(h->geom, hl, a, 0, lstream(h)));
   } else {
-    CK(h, emrkc_k::launch_stage_inner(h->geom, hl, a, k, 0, h->stream));
+    CK(h, emrkc_k::launch_stage_inner(h->geom, hl, a, k, 0, lstream(h)));
   }
   ++h->level;
   return EMRKC_OK;
@@ -1043,8 +1051,79 @@ int end_step(emrkc_handle* h, const StepCtx* c) {
   return c->w[(h->plan.s - 1) % c->nw];
 }
 
+// z-pipelined step (s = 1, m >= 2, whole grid, TMA kernels): the node kernel
+// (level 1) runs in EMRKC_ZPIPE z-chunks on the handle's stream, and level
+// k >= 2 of chunk c runs on a second stream as soon as level k - 1 of chunk
+// c is done, its plane range lagging by k planes (plane p of level k needs
+// level k - 1 at p + 1; the ranges of emrkc_step_host). The node kernel is
+// FP64-issue bound and the inner stages HBM bound, so the two overlap on the
+// SMs; the results are the unpipelined step's bit for bit.
+int zpipe_chunks() {
+  static int n = -1;
+  if (n < 0) {
+    const char* e = std::getenv("EMRKC_ZPIPE");
+    n = (e && *e) ? std::max(0, std::min(64, std::atoi(e))) : 0;
+  }
+  return n;
+}
+
+bool use_zpipe(emrkc_handle* h, const Plan& pl) {
+  const int K = zpipe_chunks();
+  return K > 1 && !h->partitioned && h->fast && h->pipe == 3 && pl.s == 1 && pl.m >= 2 &&
+         pl.method != kMethodMrkc && !pl.exex && !use_tb(h, pl) && !use_fused(h, pl) &&
+         h->zr_lo < 0 && !h->level_hook && h->geom.nzl >= (pl.m + 1) * K;
+}
+
+int enqueue_step_zpipe(emrkc_handle* h, double t, long long step_in_run,
+                       unsigned long long* gate_slot, int* out_idx) {
+  const int K = zpipe_chunks();
+  if (!h->s_aux) {
+    CK(h, cudaStreamCreateWithFlags(&h->s_aux, cudaStreamNonBlocking));
+    h->zp_ev.resize(64);
+    for (auto& e : h->zp_ev) CK(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(h, cudaEventCreateWithFlags(&h->zp_join, cudaEventDisableTiming));
+  }
+  const Plan& pl = h->plan;
+  const int nz = h->geom.nzl, m = pl.m;
+  auto zc = [&](int c) { return static_cast<int>(static_cast<int64_t>(c) * nz / K); };
+  auto kr = [&](int c, int k) { return c == 0 ? 0 : (c == K ? nz : zc(c) - k); };
+  StepCtx c;
+  begin_step(h, t, step_in_run, gate_slot, &c);
+  // the second stream starts behind everything enqueued so far
+  CK(h, cudaEventRecord(h->zp_join, h->stream));
+  CK(h, cudaStreamWaitEvent(h->s_aux, h->zp_join, 0));
+  int rc = EMRKC_OK;
+  for (int q = 0; q <= K && !rc; ++q) {
+    if (q < K) {  // node kernel, chunk q
+      h->ls = h->stream;
+      h->zr_lo = kr(q, 1);
+      h->zr_hi = kr(q + 1, 1);
+      rc = launch_level(h, &c, 1, 1);
+      if (!rc) CK(h, cudaEventRecord(h->zp_ev[q], h->stream));
+    }
+    if (q >= 1 && !rc) {  // inner stages, chunk q - 1
+      CK(h, cudaStreamWaitEvent(h->s_aux, h->zp_ev[q - 1], 0));
+      h->ls = h->s_aux;
+      for (int k = 2; k <= m && !rc; ++k) {
+        h->zr_lo = kr(q - 1, k);
+        h->zr_hi = kr(q, k);
+        rc = launch_level(h, &c, 1, k);
+      }
+    }
+  }
+  h->ls = nullptr;
+  h->zr_lo = h->zr_hi = -1;
+  // the handle's stream continues behind the whole step
+  CK(h, cudaEventRecord(h->zp_join, h->s_aux));
+  CK(h, cudaStreamWaitEvent(h->stream, h->zp_join, 0));
+  if (rc) return rc;
+  *out_idx = end_step(h, &c);
+  return EMRKC_OK;
+}
+
 int enqueue_step(emrkc_handle* h, double t, long long step_in_run,
                  unsigned long long* gate_slot, int* out_idx) {
+  if (use_zpipe(h, h->plan)) return enqueue_step_zpipe(h, t, step_in_run, gate_slot, out_idx);
   StepCtx c;
   begin_step(h, t, step_in_run, gate_slot, &c);
   for (int j = 1; j <= h->plan.s; ++j)
@@ -1360,6 +1439,10 @@ void emrkc_destroy(emrkc_handle* h) {
   if (h->d_red) cudaFree(h->d_red);
   if (h->d_rel) cudaFree(h->d_rel);
   if (h->fu_xch) cudaFree(h->fu_xch);
+  for (auto e : h->zp_ev)
+    if (e) cudaEventDestroy(e);
+  if (h->zp_join) cudaEventDestroy(h->zp_join);
+  if (h->s_aux) cudaStreamDestroy(h->s_aux);
   for (auto p : {h->sp_v[0], h->sp_v[1], h->sp_fy})
     if (p) cudaFree(p);
   if (h->fu_flags) cudaFree(h->fu_flags);
@@ -1975,6 +2058,21 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
         CK(h, emrkc_k::launch_norm2_partial(static_cast<const double*>(scratch_rd),
                                             flush_bytes / 8, h->d_red,
                                             emrkc_k::power_blocks(), h->stream));
+      }
+      if (use_zpipe(h, pl)) {
+        // two streams overlap: one event pair around the whole step (first
+        // entry), the other entries of the step 0
+        CK(h, cudaEventRecord(tev[2 * li], h->stream));
+        int outi = 0;
+        if ((rc = enqueue_step_zpipe(h, t, r, h->d_slots + 2 * r, &outi))) return rc;
+        CK(h, cudaEventRecord(tev[2 * li + 1], h->stream));
+        for (int64_t q = 1; q < per; ++q) {
+          CK(h, cudaEventRecord(tev[2 * (li + q)], h->stream));
+          CK(h, cudaEventRecord(tev[2 * (li + q) + 1], h->stream));
+        }
+        li += per;
+        h->cur = outi;
+        continue;
       }
       StepCtx c;
       begin_step(h, t, r, h->d_slots + 2 * r, &c);
@@ -2964,7 +3062,8 @@ int emrkc_model_ionic_current(int32_t model, double V, const double* z_E, double
 
 int32_t emrkc_fused_active(emrkc_handle* h) {
   if (!h || !h->plan_uploaded) return 0;
-  return use_fused(h, h->plan) ? 1 : 0;
+  if (use_fused(h, h->plan)) return 1;
+  return use_zpipe(h, h->plan) ? 2 : 0;
 }
 
 // ---------------------------------------------------------------------------
