@@ -341,6 +341,7 @@ struct emrkc_handle {
   int zr_lo = -1, zr_hi = -1;  // node-kernel plane range override (< 0: all)
   // z-pipelined step (EMRKC_ZPIPE): inner-stage chunks on a second stream,
   // each chunk behind the node-kernel chunk it needs
+  int zpipe = 0;                     // EMRKC_ZPIPE chunks (0: off; measured slower)
   cudaStream_t s_aux = nullptr;      // stream of the inner-stage chunks
   cudaStream_t ls = nullptr;         // launch_level's stream (null: stream)
   std::vector<cudaEvent_t> zp_ev;    // node chunk c done
@@ -1058,17 +1059,8 @@ int end_step(emrkc_handle* h, const StepCtx* c) {
 // level k - 1 at p + 1; the ranges of emrkc_step_host). The node kernel is
 // FP64-issue bound and the inner stages HBM bound, so the two overlap on the
 // SMs; the results are the unpipelined step's bit for bit.
-int zpipe_chunks() {
-  static int n = -1;
-  if (n < 0) {
-    const char* e = std::getenv("EMRKC_ZPIPE");
-    n = (e && *e) ? std::max(0, std::min(64, std::atoi(e))) : 0;
-  }
-  return n;
-}
-
 bool use_zpipe(emrkc_handle* h, const Plan& pl) {
-  const int K = zpipe_chunks();
+  const int K = h->zpipe;
   return K > 1 && !h->partitioned && h->fast && h->pipe == 3 && pl.s == 1 && pl.m >= 2 &&
          pl.method != kMethodMrkc && !pl.exex && !use_tb(h, pl) && !use_fused(h, pl) &&
          h->zr_lo < 0 && !h->level_hook && h->geom.nzl >= (pl.m + 1) * K;
@@ -1076,7 +1068,7 @@ bool use_zpipe(emrkc_handle* h, const Plan& pl) {
 
 int enqueue_step_zpipe(emrkc_handle* h, double t, long long step_in_run,
                        unsigned long long* gate_slot, int* out_idx) {
-  const int K = zpipe_chunks();
+  const int K = h->zpipe;
   if (!h->s_aux) {
     CK(h, cudaStreamCreateWithFlags(&h->s_aux, cudaStreamNonBlocking));
     h->zp_ev.resize(64);
@@ -1213,6 +1205,8 @@ int init_handle(emrkc_handle* h) {
     if (*tb) h->tb = std::atoi(tb) != 0;
   if (const char* fu = std::getenv("EMRKC_FUSED"))
     if (*fu) h->fused = std::atoi(fu) != 0;
+  if (const char* zp = std::getenv("EMRKC_ZPIPE"))
+    if (*zp) h->zpipe = std::max(0, std::min(64, std::atoi(zp)));
   if (const char* zc = std::getenv("EMRKC_ZC"))
     if (*zc) h->zc = std::min(emrkc_k::kMaxZc, std::max(1, std::atoi(zc)));
   return EMRKC_OK;
