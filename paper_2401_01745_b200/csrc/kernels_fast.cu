@@ -35,6 +35,10 @@
 #include "kernels.h"
 #include "tma.cuh"
 
+#ifndef EMRKC_EXPERIMENTAL
+#define EMRKC_EXPERIMENTAL 0
+#endif
+
 namespace emrkc_k {
 
 using namespace emrkc_dev;
@@ -743,6 +747,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, valid && ze > zb);
 }
 
+#if EMRKC_EXPERIMENTAL  // k_node_persist: measured slower than k_node_tma
 // Loader state of one work item (prepared outside the inner loop).
 struct PLoad {
   long long voff0, voff1;   // halo cells t and t + NT of the tile
@@ -1014,6 +1019,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
   if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, any);
 }
+#endif  // EMRKC_EXPERIMENTAL
 
 // ---------------------------------------------------------------------------
 // k_vin_pipe: the V-only inner stage with the same cp.async plane ring as
@@ -2392,11 +2398,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned 
 __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -2826,6 +2827,7 @@ static cudaError_t launch_pipe_t(const Geom& g, const Halo& h, const FastArgs& a
   return launch_k(k_node_pipe<D, F, I>, grd, dim3(T::NT), smem, st, g, h, a);
 }
 
+#if EMRKC_EXPERIMENTAL
 template <int D, int F, int I>
 static cudaError_t launch_persist_t(const Geom& g, const Halo& h, const FastArgs& a,
                                     cudaStream_t st) {
@@ -2865,6 +2867,14 @@ cudaError_t launch_node_persist(const Geom& g, const Halo& h, const FastArgs& a,
   }
   return launch_node_fast(g, h, a, ion, st);
 }
+#else
+// The persistent node kernel is compiled only with -DEMRKC_EXPERIMENTAL=1;
+// EMRKC_PIPE=2 selects the TMA / cp.async kernels otherwise (emrkc_capi.cpp).
+cudaError_t launch_node_persist(const Geom& g, const Halo& h, const FastArgs& a, bool ion,
+                                cudaStream_t st) {
+  return launch_node_pipe(g, h, a, ion, st);
+}
+#endif
 
 template <int D, int F, int I>
 static cudaError_t launch_node_tma_t(const Geom& g, const Halo& h, const FastArgs& a,

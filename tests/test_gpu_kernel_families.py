@@ -1,6 +1,7 @@
 """Every selectable fast-kernel family against the oracle: EMRKC_PIPE = 3
 (TMA-staged, default), 1 (cp.async-staged), 2 (persistent cp.async node
-kernel), 0 (plain loads, z-march), on 3-D and 2-D grids with s = 1 / m = 1
+kernel when built with -DEMRKC_EXPERIMENTAL=1, measured slower; the
+cp.async kernels otherwise), 0 (plain loads, z-march), on 3-D and 2-D grids with s = 1 / m = 1
 and forced s = 2 / m = 2 (outer stages j >= 2 and V-only inner stages).
 Runs use emrkc_step per step (the resident whole-run kernel would bypass
 the families on small grids)."""
