@@ -1,9 +1,12 @@
 """BASELINE's large grids run on the GPU against the reference's own records
 (tests/golden/big_<workload>.npz, made by tests/golden/make_big_runs.py from
 oracle/_ref = the unmodified reference sources): config 4's grid
-(512x512x256, HH standing in for TTP: s = 1, m = 2) run to its T or to the
-reference's own abort, config 3's grid (256x256x128, HH standing in for CRN)
-over its full 400 steps.
+(512x512x256, HH standing in for TTP: s = 1, m = 2) run into the
+reference's own abort at step 65; config 3's grid (256x256x128, HH standing
+in for CRN) over 20 steps (reference self-divergence 1e-16: the 1e-9 bar),
+60 steps (self-divergence ~2e-9: 4x that) and its full 400 steps (the
+reference diverges from itself by 0.05-0.5 there: record and rho only);
+config 5 at N = 50 over its full T (three sensitivity seeds).
 
 Exact: s, m, rho iteration counts, abort step / kind / stage, counters.
 Within the bar: rho (RHO_TOL), gate range, and per block the per-plane sums
@@ -68,8 +71,14 @@ def test_big_run_against_reference(path):
     sens = [max(s["rel_l2"][b] for s in meta["sensitivity"]) if meta["sensitivity"] else 0.0
             for b in range(4)]
     bars = [max(TOL, 4.0 * sv) for sv in sens]
-    assert abs(res["gate_min"] - rec["gate_min"]) <= max(bars[1:])
-    assert abs(res["gate_max"] - rec["gate_max"]) <= max(bars[1:])
+    # A run whose reference diverges from ITSELF by more than 1e-3 under a
+    # 1e-15 input perturbation (config 3's grid over its full T: 0.05-0.5)
+    # has no reproducible field to compare: the record (s, m, counters, no
+    # abort) and rho are asserted above, the field differences are printed.
+    chaotic = max(sens) > 1e-3
+    if not chaotic:
+        assert abs(res["gate_min"] - rec["gate_min"]) <= max(bars[1:])
+        assert abs(res["gate_max"] - rec["gate_max"]) <= max(bars[1:])
     nn = p.n_nodes
     n_planes = int(p.n[p.dim - 1])
     idx = g["sample_index"]
@@ -82,8 +91,10 @@ def test_big_run_against_reference(path):
             "norm2": abs(float(np.linalg.norm(blk)) - float(g[f"norm2_{b}"])) / float(g[f"norm2_{b}"]),
             "sample": _rel(blk[idx], g["sample"][b]),
         }
-        print(meta["workload"], "block", b, errs, "bar", bars[b])
-        assert max(errs.values()) <= bars[b], (b, errs, bars[b])
+        print(meta["workload"], meta["steps"], "block", b, errs, "bar", bars[b],
+              "(ill-conditioned: not asserted)" if chaotic else "")
+        if not chaotic:
+            assert max(errs.values()) <= bars[b], (b, errs, bars[b])
 
 
 @pytest.mark.slow
