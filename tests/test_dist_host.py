@@ -47,3 +47,36 @@ def test_min_slab_depth(nz, world, expect):
               for r in range(world)]
     assert sum(depths) == nz
     assert dist.min_slab_depth(p, world) == min(depths) == expect
+
+
+def test_z_slab_sample_is_the_central_planes(oracle):
+    """bench.py's bounded CPU sample (workloads.z_slab_sample): the planes
+    [z0, z0 + depth) of the workload's seeded initial state, the same
+    spacing and conductivities, the stimulus box in the same global
+    coordinates (the same nodes are stimulated), and the initial state from
+    the reference's own resting state is the product's bit for bit."""
+    w = workloads.get("hh3d_sweep_50")
+    z0, d = 3, 9  # the 8^3 corner stimulus covers sample planes 0..4
+    ws, ys = workloads.z_slab_sample(w, z0, d)
+    p, q = w.problem, ws.problem
+    assert [int(q.n[a]) for a in range(3)] == [50, 50, d]
+    y = w.initial_state()
+    nn, plane = p.n_nodes, 50 * 50
+    for b in range(4):
+        np.testing.assert_array_equal(ys[b * q.n_nodes:(b + 1) * q.n_nodes],
+                                      y[b * nn + z0 * plane: b * nn + (z0 + d) * plane])
+    for a in range(3):
+        assert q.dx[a] == p.dx[a] and q.sigma[a] == p.sigma[a]
+    # stimulated nodes: global z in the box <=> sample z + z0 in the box
+    hits = 0
+    for z in range(d):
+        for node in (0, 7, 55):
+            i_s = node + plane * z
+            i_g = node + plane * (z + z0)
+            st = oracle.stimulus_rate(q, 0.5, i_s) > 0
+            assert st == (oracle.stimulus_rate(p, 0.5, i_g) > 0)
+            hits += st
+    assert hits == 5 * 2  # nodes 0 and 7 (x, y <= 7) on planes z + z0 = 3..7
+    from oracle.oracle import Oracle
+
+    np.testing.assert_array_equal(w.initial_state(resting=Oracle().resting_state), y)
