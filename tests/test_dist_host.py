@@ -76,7 +76,7 @@ def test_z_slab_sample_is_the_central_planes(oracle):
             st = oracle.stimulus_rate(q, 0.5, i_s) > 0
             assert st == (oracle.stimulus_rate(p, 0.5, i_g) > 0)
             hits += st
-    assert hits == 5 * 2  # nodes 0 and 7 (x, y <= 7) on planes z + z0 = 3..7
+    assert hits == 3 * 5  # nodes 0, 7, 55 (x, y <= 7) on planes z + z0 = 3..7
     from oracle.oracle import Oracle
 
     np.testing.assert_array_equal(w.initial_state(resting=Oracle().resting_state), y)
