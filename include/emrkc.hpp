@@ -36,6 +36,7 @@
 // stages, std::runtime_error for device failures.
 #pragma once
 
+#include <exception>
 #include <functional>
 #include <memory>
 #include <span>
@@ -361,7 +362,7 @@ struct DVec {
 
 struct HostRhs {
   const RhsFn* f;
-  std::string err;
+  std::exception_ptr err;  // what the callback threw (rethrown by the caller)
 };
 inline int host_rhs(void* c, double t, const double* y, double* out, int64_t len, void*) {
   auto* r = static_cast<HostRhs*>(c);
@@ -371,8 +372,8 @@ inline int host_rhs(void* c, double t, const double* y, double* out, int64_t len
     (*r->f)(t, yy, oo);
     if (static_cast<int64_t>(oo.size()) != len) return 1;
     return emrkc_vctx_upload(ctx(), out, oo.data(), len) ? 1 : 0;
-  } catch (const std::exception& e) {
-    r->err = e.what();
+  } catch (...) {
+    r->err = std::current_exception();
     return 1;
   }
 }
@@ -380,6 +381,7 @@ inline int host_rhs(void* c, double t, const double* y, double* out, int64_t len
 struct HostSplit {
   const SplitRhs* rhs;
   HostRhs fF, fS;
+  std::exception_ptr err;  // thrown by exp_part
   emrkc_counters ctr{};
   emrkc_split_rhs c{};
 };
@@ -391,7 +393,8 @@ inline int host_exp(void* cx, const double* y, double* lam, double* yinf, int64_
     h->rhs->exp_part(yy, l, yi);
     if (emrkc_vctx_upload(ctx(), lam, l.data(), len)) return 1;
     return emrkc_vctx_upload(ctx(), yinf, yi.data(), len) ? 1 : 0;
-  } catch (const std::exception&) {
+  } catch (...) {
+    h->err = std::current_exception();
     return 1;
   }
 }
@@ -414,6 +417,9 @@ inline void make_split(const SplitRhs& rhs, HostSplit& hs) {
   hs.c.counters = &hs.ctr;
 }
 inline void fold(const SplitRhs& rhs, const HostSplit& hs) {
+  // a callback's own exception wins over the ECALLBACK status it caused
+  for (const std::exception_ptr& e : {hs.fF.err, hs.fS.err, hs.err})
+    if (e) std::rethrow_exception(e);
   if (!rhs.counters) return;
   rhs.counters->n_fF += hs.ctr.n_fF;
   rhs.counters->n_fS += hs.ctr.n_fS;
@@ -430,6 +436,7 @@ inline Vec rkc_iteration(double t, const Vec& y, double dt, const RhsFn& f, int 
   int32_t st = 0;
   const int rc = emrkc_rkc_iteration(detail::ctx(), t, dy.p, dy.n, dt, detail::host_rhs, &hr, s,
                                      epsilon, out.p, &st);
+  if (hr.err) std::rethrow_exception(hr.err);  // the callback's own exception
   detail::vcheck(rc, st);
   return out.host();
 }
@@ -524,8 +531,10 @@ inline RhoEstimateV estimate_spectral_radius(double t, const Vec& y, const RhsFn
   if (!v0.empty()) d0 = std::make_unique<detail::DVec>(v0);
   detail::HostRhs hr{&f, {}};
   emrkc_rho_result r{};
-  detail::vcheck(emrkc_estimate_spectral_radius(detail::ctx(), t, dy.p, dy.n, detail::host_rhs,
-                                                &hr, d0 ? d0->p : nullptr, rho0, &r, dv.p));
+  const int rc = emrkc_estimate_spectral_radius(detail::ctx(), t, dy.p, dy.n, detail::host_rhs,
+                                                &hr, d0 ? d0->p : nullptr, rho0, &r, dv.p);
+  if (hr.err) std::rethrow_exception(hr.err);
+  detail::vcheck(rc);
   RhoEstimateV e;
   e.rho = r.rho;
   e.iterations = r.iterations;

@@ -70,6 +70,10 @@ class DeviceContext:
         if rc == capi.EMRKC_ENONFINITE:
             raise NumericalAbort(msg, stage, inner=inner)
         if rc == capi.EMRKC_ECALLBACK:
+            if _CB_ERROR:
+                ex = _CB_ERROR[0]
+                _CB_ERROR.clear()
+                raise RuntimeError(msg) from ex
             raise RuntimeError(msg)
         raise CudaError(msg)
 
@@ -111,6 +115,11 @@ def context() -> DeviceContext:
     return _CTX
 
 
+# The first exception a Python callback raised inside the C library (it
+# returns non-zero there, EMRKC_ECALLBACK); re-raised by DeviceContext.check.
+_CB_ERROR: list = []
+
+
 def _wrap_rhs(ctx: DeviceContext, f: Callable, counter: Optional[list] = None):
     """Python f(t, y) -> out as a device RhsFn (read back, call, upload)."""
 
@@ -119,12 +128,13 @@ def _wrap_rhs(ctx: DeviceContext, f: Callable, counter: Optional[list] = None):
             yy = ctx.download(y, n)
             oo = np.ascontiguousarray(f(t, yy), dtype=np.float64)
             if oo.shape != (n,):
-                return 1
+                raise ValueError(f"RhsFn returned shape {oo.shape}, expected ({n},)")
             ctx.write(out, oo)
             if counter is not None:
                 counter[0] += 1
             return 0
-        except Exception:
+        except Exception as ex:  # noqa: BLE001 - handed back to the caller
+            _CB_ERROR.append(ex)
             return 1
 
     return capi.RHS_FN(cb)
@@ -139,7 +149,8 @@ def _wrap_exp(ctx: DeviceContext, e: Callable):
             ctx.write(lam, np.broadcast_to(np.asarray(l, dtype=np.float64), (n,)))
             ctx.write(yinf, np.broadcast_to(np.asarray(yi, dtype=np.float64), (n,)))
             return 0
-        except Exception:
+        except Exception as ex:  # noqa: BLE001 - handed back to the caller
+            _CB_ERROR.append(ex)
             return 1
 
     return capi.EXP_FN(cb)

@@ -301,3 +301,22 @@ def test_generic_grid_step_matches_fused_and_oracle(oracle, rho_F, rho_S):
         assert oracle.rel_l2(p, y_gen[sl], y_ref[sl]) <= 1e-13
         assert oracle.rel_l2(p, y_fused[sl], y_gen[sl]) <= 1e-12
     assert fF.iterations == rF.iterations and fF.rho == rF.rho
+
+
+def test_callback_exception_propagates():
+    """A right-hand side that raises aborts the device iteration and its own
+    exception reaches the caller (as the cause of EMRKC_ECALLBACK)."""
+    def bad(t, y):
+        raise KeyError("boom")
+
+    with pytest.raises(RuntimeError) as ei:
+        I.rkc_iteration(0.0, [1.0], 0.1, bad, 3, 0.05)
+    assert isinstance(ei.value.__cause__, KeyError)
+    rhs = scalar_split(-1.0, -1.0, -1.0)
+    rhs.f_S = bad
+    with pytest.raises(RuntimeError) as ei:
+        I.emrkc_step(0.0, [1.0], 0.1, rhs)
+    assert isinstance(ei.value.__cause__, KeyError)
+    # the context is usable afterwards
+    out = I.rkc_iteration(0.0, [2.0], 0.3, lambda t, y: -4.0 * y, 1, 0.05)
+    assert out[0] == pytest.approx(2.0 * (1.0 - 1.2), rel=1e-14)
