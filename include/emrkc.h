@@ -49,6 +49,18 @@ typedef enum emrkc_status {
 } emrkc_status;
 
 enum { EMRKC_MODEL_HH = 0 };          /* make_ionic_model("hh"), P/src/ionic.cpp:125-128 */
+/* SYNTHETIC width stand-in (SURVEY §8(c) option 2; no physiology claim): HH
+ * plus n_aux passive auxiliary ("concentration-like") variables, so a state
+ * has the CRN / TTP width N = 4 + n_aux (21 / 19) without their unavailable
+ * equations. V and the gates follow HH exactly (the current ignores the aux
+ * variables); aux a relaxes linearly towards a V-dependent target through
+ * IonicModel::aux_rates (P/include/mrkc/ionic.hpp:33-36, f_S aux rows
+ * P/src/monodomain.cpp:191-221):
+ *   g_S,a = k_a * ((s1_a * V + s0_a) - z_a),
+ *   k_a = 0.002 * (1 + a % 5), s1_a = 0.01 * (a % 3), s0_a = 0.5 + 0.1 * (a % 4),
+ * evaluated in that order without FMA; rest: z_a = s1_a * V_rest + s0_a. */
+enum { EMRKC_MODEL_HH_AUX = 1 };
+#define EMRKC_MAX_AUX 20
 /* SplitRhs::f_F / f_S; _GATES: f_F_with_gates / f_S_with_gates of the mRKC
  * stiff-gate split (P/src/monodomain.cpp:287-304, gates from
  * emrkc_set_stiff_gates) */
@@ -69,7 +81,7 @@ enum {
  * P/src/monodomain.cpp:9-32; extent = (n-1)*dx here). */
 typedef struct emrkc_problem {
   int32_t dim;                 /* 1, 2 or 3 */
-  int32_t model;               /* EMRKC_MODEL_HH */
+  int32_t model;               /* EMRKC_MODEL_HH / EMRKC_MODEL_HH_AUX */
   int64_t n[3];                /* nodes per axis (1 on unused axes) */
   double dx[3];                /* [mm] */
   double sigma[3];             /* Conductivity::sigma [mS/mm] */
@@ -79,6 +91,8 @@ typedef struct emrkc_problem {
   double stim_lo[3];           /* box_lo [mm] */
   double stim_hi[3];           /* box_hi [mm] */
   double stim_t0, stim_t1;     /* window [ms], inclusive */
+  int32_t n_aux;               /* EMRKC_MODEL_HH_AUX: auxiliary variables (0 for HH) */
+  int32_t reserved;
 } emrkc_problem;
 
 /* z-slab ownership along the slowest axis (axis dim-1). [z_begin, z_end).
@@ -167,6 +181,9 @@ int emrkc_model_info(int32_t model, int32_t* n_gates, int32_t* n_aux);
 
 /* IonicModel::resting_state — P/src/ionic.cpp:42-77. gates: n_gates. */
 int emrkc_resting_state(int32_t model, double* V, double* gates);
+/* MonodomainOperator::initial_state (P/src/monodomain.cpp:306-319): the
+ * uniform resting state in Vec layout [V | gates | aux] (len = state len). */
+int emrkc_initial_state(const emrkc_problem* p, double* y, int64_t len);
 
 /* StateLayout::size() of the (local) state — P/include/mrkc/monodomain.hpp:56. */
 int64_t emrkc_state_len(const emrkc_problem* p, const emrkc_partition* part);

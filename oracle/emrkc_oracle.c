@@ -497,13 +497,25 @@ static int64_t n_nodes(const emrkc_problem* p) {
   return nn;
 }
 
-int64_t oc_state_len(const emrkc_problem* p) { return n_nodes(p) * 4; }
+/* auxiliary variables of the SYNTHETIC width stand-in EMRKC_MODEL_HH_AUX
+ * (include/emrkc.h; the reference runs it through oracle/ref_driver.cpp's
+ * HHAux IonicModel) */
+static int n_aux_of(const emrkc_problem* p) {
+  return p->model == EMRKC_MODEL_HH_AUX ? p->n_aux : 0;
+}
+static double aux_k(int a) { return 0.002 * (double)(1 + a % 5); }
+static double aux_s1(int a) { return 0.01 * (double)(a % 3); }
+static double aux_s0(int a) { return 0.5 + 0.1 * (double)(a % 4); }
+
+int64_t oc_state_len(const emrkc_problem* p) { return n_nodes(p) * (4 + n_aux_of(p)); }
 
 int oc_validate(const emrkc_problem* p) {
   if (p->dim < 1 || p->dim > 3)
     return fail(EMRKC_EINVAL, "grid: dim must be 1, 2, or 3");
-  if (p->model != EMRKC_MODEL_HH)
+  if (p->model != EMRKC_MODEL_HH && p->model != EMRKC_MODEL_HH_AUX)
     return fail(EMRKC_EINVAL, "unknown ionic model");
+  if (p->model == EMRKC_MODEL_HH_AUX && (p->n_aux < 1 || p->n_aux > EMRKC_MAX_AUX))
+    return fail(EMRKC_EINVAL, "hh_aux: n_aux out of range");
   for (int a = 0; a < p->dim; ++a)
     if (p->n[a] < 2 || !(p->dx[a] > 0.0))
       return fail(EMRKC_EINVAL, "grid: extent and dx must be positive");
@@ -549,26 +561,32 @@ double oc_stimulus_rate(const emrkc_problem* p, double t, int64_t node) {
 /* f_F — P/src/monodomain.cpp:207-212 */
 void oc_f_F(const emrkc_problem* p, double t, const double* y, double* out) {
   (void)t;
-  const int64_t nn = n_nodes(p);
-  for (int64_t k = nn; k < 4 * nn; ++k) out[k] = 0.0;
+  const int64_t nn = n_nodes(p), len = oc_state_len(p);
+  for (int64_t k = nn; k < len; ++k) out[k] = 0.0;
   oc_diffusion_apply(p, y, out);
 }
 
-/* f_S — P/src/monodomain.cpp:214-221 -> v_reaction :160-173 */
+/* f_S — P/src/monodomain.cpp:214-221 -> v_reaction :160-173, aux rows
+ * aux_rates_field :191-205 */
 void oc_f_S(const emrkc_problem* p, double t, const double* y, double* out) {
-  const int64_t nn = n_nodes(p);
-  for (int64_t k = nn; k < 4 * nn; ++k) out[k] = 0.0;
+  const int64_t nn = n_nodes(p), len = oc_state_len(p);
+  const int na = n_aux_of(p);
+  for (int64_t k = nn; k < len; ++k) out[k] = 0.0;
   for (int64_t i = 0; i < nn; ++i) {
     const double z[3] = {y[nn + i], y[2 * nn + i], y[3 * nn + i]};
     out[i] = oc_stimulus_rate(p, t, i) - oc_hh_ionic_current(y[i], z) / p->C_m;
+    for (int a = 0; a < na; ++a) {
+      const int64_t k = (4 + a) * nn + i;
+      out[k] = aux_k(a) * ((aux_s1(a) * y[i] + aux_s0(a)) - y[k]);
+    }
   }
 }
 
 /* exp_part — P/src/monodomain.cpp:246-256 -> gate_coeffs_field :175-189 */
 void oc_exp_part(const emrkc_problem* p, const double* y, double* lam,
                  double* yinf) {
-  const int64_t nn = n_nodes(p);
-  for (int64_t k = 0; k < 4 * nn; ++k) lam[k] = yinf[k] = 0.0;
+  const int64_t nn = n_nodes(p), len = oc_state_len(p);
+  for (int64_t k = 0; k < len; ++k) lam[k] = yinf[k] = 0.0;
   for (int64_t i = 0; i < nn; ++i) {
     double l[3], zi[3];
     oc_hh_gate_coeffs(y[i], l, zi);
@@ -588,6 +606,10 @@ int oc_initial_state(const emrkc_problem* p, double* y) {
   for (int64_t i = 0; i < nn; ++i) y[i] = V;
   for (int g = 0; g < 3; ++g)
     for (int64_t i = 0; i < nn; ++i) y[(1 + g) * nn + i] = z[g];
+  for (int a = 0; a < n_aux_of(p); ++a) { /* HHAux::resting_state */
+    const double za = aux_s1(a) * V + aux_s0(a);
+    for (int64_t i = 0; i < nn; ++i) y[(4 + a) * nn + i] = za;
+  }
   return 0;
 }
 
@@ -1027,6 +1049,7 @@ int oc_run_imex(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps
                 int64_t* cg_iters_total) {
   int rc = oc_validate(p);
   if (rc) return rc;
+  if (n_aux_of(p)) return fail(EMRKC_EINVAL, "hh_aux: emRKC (standard / progressive) only");
   const int64_t nn = n_nodes(p), len = 4 * nn;
   double* next = (double*)malloc(sizeof(double) * len);
   if (!next) return fail(EMRKC_ENOMEM, "out of memory");
@@ -1037,7 +1060,7 @@ int oc_run_imex(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps
   res->gate_max = 0.0;
   res->s = res->m = 1;
   res->eta = dt;
-  track_gate_range(y, nn, len, &res->gate_min, &res->gate_max);
+  track_gate_range(y, nn, 4 * nn, &res->gate_min, &res->gate_max);
   int64_t tot = 0;
   for (int64_t step = step0; step < step0 + nsteps; ++step) {
     const double t = (double)step * dt;
@@ -1073,7 +1096,7 @@ int oc_run_imex(const emrkc_problem* p, double* y, int64_t step0, int64_t nsteps
       res->abort_step = step;
       break;
     }
-    track_gate_range(y, nn, len, &res->gate_min, &res->gate_max);
+    track_gate_range(y, nn, 4 * nn, &res->gate_min, &res->gate_max);
   }
   if (cg_iters_total) *cg_iters_total = tot;
   free(next);
@@ -1096,7 +1119,9 @@ int oc_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nste
   method &= 15;
   int rc = oc_validate(p);
   if (rc) return rc;
-  const int64_t nn = n_nodes(p), len = 4 * nn;
+  const int64_t nn = n_nodes(p), len = oc_state_len(p);
+  if (n_aux_of(p) && method != OC_METHOD_EMRKC && method != OC_METHOD_EMRKC_PROGRESSIVE)
+    return fail(EMRKC_EINVAL, "hh_aux: emRKC (standard / progressive) only");
   grid_ctx c = {p, stiff};
   oc_counters ctr = {0, 0, 0};
   oc_split rhs = {grid_fF, grid_fS, grid_exp, &c, rho_F, rho_S, &ctr};
@@ -1112,7 +1137,7 @@ int oc_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nste
   res->abort_step = -1;
   res->gate_min = 1.0;
   res->gate_max = 0.0;
-  track_gate_range(y, nn, len, &res->gate_min, &res->gate_max);
+  track_gate_range(y, nn, 4 * nn, &res->gate_min, &res->gate_max);
   struct timespec w0, w1;
   clock_gettime(CLOCK_MONOTONIC, &w0);
   for (int64_t step = step0; step < step0 + nsteps; ++step) {
@@ -1166,7 +1191,7 @@ int oc_run_method(const emrkc_problem* p, double* y, int64_t step0, int64_t nste
       res->abort_step = step;
       break;
     }
-    track_gate_range(y, nn, len, &res->gate_min, &res->gate_max);
+    track_gate_range(y, nn, 4 * nn, &res->gate_min, &res->gate_max);
   }
   clock_gettime(CLOCK_MONOTONIC, &w1);
   if (wall_s)

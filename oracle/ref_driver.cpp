@@ -39,8 +39,54 @@ namespace {
 
 thread_local std::string g_err;
 
+// EMRKC_MODEL_HH_AUX (include/emrkc.h): the SYNTHETIC width stand-in, HH plus
+// n_aux passive auxiliary variables, written here as an IonicModel of the
+// reference's own interface (P/include/mrkc/ionic.hpp:17-53) so that the
+// reference's generic machinery — StateLayout with n_aux, f_S aux rows
+// (aux_rates_field, P/src/monodomain.cpp:191-221), exponential Euler passing
+// aux through — runs it. Test infrastructure; no physiology.
+class HHAux final : public IonicModel {
+ public:
+  explicit HHAux(int n_aux) : hh_(make_hh_model()), na_(n_aux) {}
+  std::string name() const override { return "hh_aux"; }
+  int n_gates() const override { return 3; }
+  int n_aux() const override { return na_; }
+  std::vector<std::string> var_names() const override {
+    std::vector<std::string> v = {"m", "h", "n"};
+    for (int a = 0; a < na_; ++a) v.push_back("aux" + std::to_string(a));
+    return v;
+  }
+  void rates(double V, std::span<double> alpha, std::span<double> beta) const override {
+    hh_->rates(V, alpha, beta);
+  }
+  double ionic_current(double V, std::span<const double> z_E,
+                       std::span<const double>) const override {
+    return hh_->ionic_current(V, z_E, {});
+  }
+  static double k(int a) { return 0.002 * static_cast<double>(1 + a % 5); }
+  static double s1(int a) { return 0.01 * static_cast<double>(a % 3); }
+  static double s0(int a) { return 0.5 + 0.1 * static_cast<double>(a % 4); }
+  void aux_rates(double V, std::span<const double>, std::span<const double> z_S,
+                 std::span<double> out) const override {
+    for (int a = 0; a < na_; ++a) out[a] = k(a) * ((s1(a) * V + s0(a)) - z_S[a]);
+  }
+  Rest resting_state() const override {
+    Rest r = hh_->resting_state();
+    r.z_S.resize(na_);
+    for (int a = 0; a < na_; ++a) r.z_S[a] = s1(a) * r.V + s0(a);
+    return r;
+  }
+
+ private:
+  std::unique_ptr<IonicModel> hh_;
+  int na_;
+};
+
 std::unique_ptr<MonodomainOperator> make_op(const emrkc_problem* p) {
-  if (p->model != EMRKC_MODEL_HH) throw ConfigError("unknown ionic model");
+  if (p->model != EMRKC_MODEL_HH && p->model != EMRKC_MODEL_HH_AUX)
+    throw ConfigError("unknown ionic model");
+  if (p->model == EMRKC_MODEL_HH_AUX && (p->n_aux < 1 || p->n_aux > EMRKC_MAX_AUX))
+    throw ConfigError("hh_aux: n_aux out of range");
   std::vector<double> extent(p->dim), dx(p->dim);
   for (int a = 0; a < p->dim; ++a) {
     dx[a] = p->dx[a];
@@ -61,7 +107,11 @@ std::unique_ptr<MonodomainOperator> make_op(const emrkc_problem* p) {
   }
   st.t_start = p->stim_t0;
   st.t_end = p->stim_t1;
-  std::shared_ptr<const IonicModel> model = make_hh_model();
+  std::shared_ptr<const IonicModel> model;
+  if (p->model == EMRKC_MODEL_HH_AUX)
+    model = std::make_shared<HHAux>(p->n_aux);
+  else
+    model = make_hh_model();
   return std::make_unique<MonodomainOperator>(g, c, model, st);
 }
 
@@ -210,7 +260,7 @@ const char* ref_last_error(void) { return g_err.c_str(); }
 int64_t ref_state_len(const emrkc_problem* p) {
   int64_t nn = 1;
   for (int a = 0; a < p->dim; ++a) nn *= p->n[a];
-  return nn * 4;  // HH: V + 3 gates
+  return nn * (4 + (p->model == EMRKC_MODEL_HH_AUX ? p->n_aux : 0));  // V + 3 gates + aux
 }
 
 int ref_resting_state(double* V, double* gates) {

@@ -25,6 +25,8 @@ EMRKC_ENOMEM = 5
 EMRKC_ECALLBACK = 6
 
 EMRKC_MODEL_HH = 0
+EMRKC_MODEL_HH_AUX = 1  # SYNTHETIC width stand-in: HH + n_aux passive aux variables
+EMRKC_MAX_AUX = 20
 EMRKC_RHS_F = 0
 EMRKC_RHS_S = 1
 EMRKC_VARIANT_STANDARD = 0
@@ -50,7 +52,14 @@ class Problem(C.Structure):
         ("stim_hi", C.c_double * 3),
         ("stim_t0", C.c_double),
         ("stim_t1", C.c_double),
+        ("n_aux", C.c_int32),
+        ("reserved", C.c_int32),
     ]
+
+    @property
+    def n_fields(self) -> int:
+        """SoA blocks of the state: V, 3 HH gates, n_aux auxiliary."""
+        return 4 + int(self.n_aux)
 
     @property
     def n_nodes(self) -> int:
@@ -65,11 +74,13 @@ class Problem(C.Structure):
         return tuple(int(self.n[a]) for a in reversed(range(self.dim)))
 
     def state_len(self) -> int:
-        return 4 * self.n_nodes
+        return self.n_fields * self.n_nodes
 
     def describe(self) -> dict:
         return {
             "dim": self.dim,
+            "model": self.model,
+            "n_aux": int(self.n_aux),
             "n": [int(self.n[a]) for a in range(3)],
             "dx": list(self.dx),
             "sigma": list(self.sigma),
@@ -88,6 +99,7 @@ class Problem(C.Structure):
         p = cls()
         p.dim = d["dim"]
         p.model = d.get("model", EMRKC_MODEL_HH)
+        p.n_aux = d.get("n_aux", 0)
         for a in range(3):
             p.n[a] = d["n"][a]
             p.dx[a] = d["dx"][a]
@@ -207,6 +219,7 @@ PROTOTYPES = {
     "emrkc_plan_step": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(StepReport)]),
     "emrkc_model_info": (C.c_int, [C.c_int32, I32P, I32P]),
     "emrkc_resting_state": (C.c_int, [C.c_int32, DP, DP]),
+    "emrkc_initial_state": (C.c_int, [C.POINTER(Problem), DP, C.c_int64]),
     "emrkc_state_len": (C.c_int64, [C.POINTER(Problem), C.POINTER(Partition)]),
     "emrkc_partition_slab": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(Partition)]),
     "emrkc_create": (C.c_int, [C.POINTER(Problem), C.c_int32, C.POINTER(Partition), C.POINTER(C.c_void_p)]),

@@ -220,12 +220,22 @@ int64_t nodes_of(const emrkc_problem* p) {
   return nn;
 }
 
+// SoA fields of a state: V, 3 HH gates, the aux variables of
+// EMRKC_MODEL_HH_AUX (include/emrkc.h)
+int fields_of(const emrkc_problem* p) {
+  return 4 + (p->model == EMRKC_MODEL_HH_AUX ? p->n_aux : 0);
+}
+double aux_s1(int a) { return 0.01 * static_cast<double>(a % 3); }
+double aux_s0(int a) { return 0.5 + 0.1 * static_cast<double>(a % 4); }
+
 int validate(const emrkc_problem* p) {
   if (!p) return set_global(EMRKC_EINVAL, "null problem");
   if (p->dim < 1 || p->dim > 3)
     return set_global(EMRKC_EINVAL, "grid: dim must be 1, 2, or 3");
-  if (p->model != EMRKC_MODEL_HH)
+  if (p->model != EMRKC_MODEL_HH && p->model != EMRKC_MODEL_HH_AUX)
     return set_global(EMRKC_EINVAL, "unknown ionic model %d", p->model);
+  if (p->model == EMRKC_MODEL_HH_AUX && (p->n_aux < 1 || p->n_aux > EMRKC_MAX_AUX))
+    return set_global(EMRKC_EINVAL, "hh_aux: n_aux must be in [1, %d]", EMRKC_MAX_AUX);
   for (int a = 0; a < p->dim; ++a) {
     if (p->n[a] < 2 || !(p->dx[a] > 0.0))
       return set_global(EMRKC_EINVAL, "grid: extent and dx must be positive");
@@ -498,6 +508,12 @@ int upload_plan(emrkc_handle* h, double dt, double rho_F, double rho_S,
   if ((h->method == kMethodEmrkcProgressive || h->method == kMethodExexRl) && !h->fast)
     return set_err(h, EMRKC_EINVAL,
                    "the progressive variant and EXEX-RL run on the fast kernels (EMRKC_FAST=1)");
+  if (h->geom.naux > 0 &&
+      (h->method == kMethodExexRl || h->method == kMethodMrkc || !h->fast || h->pipe != 3 ||
+       h->geom.dim < 2))
+    return set_err(h, EMRKC_EINVAL,
+                   "hh_aux (the synthetic width stand-in) runs emRKC (standard / progressive) "
+                   "on the TMA kernels of 2-D / 3-D grids only");
   int rc = make_plan(dt, rho_F, rho_S, eps, &pl, h->method);
   if (rc) return set_err(h, rc, "%s", g_global_err.c_str());
   const size_t need = 3 * (pl.m + 1);
@@ -655,10 +671,10 @@ int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out, int rm
     dims[rank] = static_cast<cuuint64_t>(g.nzl);
     box[rank++] = 1;
   }
-  if (kind == kTmaGates || kind == kTmaAll) {
+  if (kind == kTmaGates || kind == kTmaAll) {  // gates (+ aux) from field 1 / all fields
     strides[rank - 1] = sizeof(double) * static_cast<cuuint64_t>(g.nn);
-    dims[rank] = 4;
-    box[rank++] = kind == kTmaGates ? 3 : 4;
+    dims[rank] = static_cast<cuuint64_t>(g.nf);
+    box[rank++] = static_cast<cuuint32_t>(kind == kTmaGates ? g.nf - 1 : g.nf);
   }
   if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
     return set_err(h, EMRKC_ECUDA, "TMA: buffer %p not 16-byte aligned", ptr);
@@ -791,6 +807,7 @@ bool fused_plan(emrkc_handle* h) {
 
 bool use_fused(emrkc_handle* h, const Plan& pl) {
   return h->fused && h->fast && h->pipe == 3 && !h->partitioned && h->zr_lo < 0 &&
+         h->geom.naux == 0 &&
          h->geom.dim == 3 && pl.s == 1 && pl.m == 2 && !pl.exex && pl.method != kMethodMrkc &&
          fused_plan(h);
 }
@@ -890,6 +907,8 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.z_hi = h->zr_lo >= 0 ? h->zr_hi : h->geom.nzl;
       f.nu = a.nu;
       f.kappa = a.kappa;
+      // aux rows (EMRKC_MODEL_HH_AUX): the inner iterate is z + c_m eta g_S
+      f.cA = pl.mudt[j] * pl.inner.c[pl.m];
       // fast ionic path only where its range analysis holds (fast_math.cuh)
       fast_window(pl.eta, &f.vmid, &f.vfast);
       f.j = j;
@@ -1329,7 +1348,22 @@ int64_t emrkc_state_len(const emrkc_problem* p, const emrkc_partition* part) {
     const int za = p->dim - 1;
     nn = nn / p->n[za] * (part->z_end - part->z_begin);
   }
-  return 4 * nn;
+  return fields_of(p) * nn;
+}
+
+int emrkc_initial_state(const emrkc_problem* p, double* y, int64_t len) {
+  int rc = validate(p);
+  if (rc) return rc;
+  if (!y || len != fields_of(p) * nodes_of(p))
+    return set_global(EMRKC_EINVAL, "initial_state: need the global state length");
+  double V = 0.0, z[3];
+  if ((rc = emrkc_resting_state(EMRKC_MODEL_HH, &V, z))) return rc;
+  const int64_t nn = nodes_of(p);
+  std::fill(y, y + nn, V);
+  for (int g = 0; g < 3; ++g) std::fill(y + (1 + g) * nn, y + (2 + g) * nn, z[g]);
+  for (int a = 0; a < fields_of(p) - 4; ++a)  // HHAux::resting_state (include/emrkc.h)
+    std::fill(y + (4 + a) * nn, y + (5 + a) * nn, aux_s1(a) * V + aux_s0(a));
+  return EMRKC_OK;
 }
 
 int emrkc_partition_slab(int64_t n_z, int32_t nranks, int32_t rank,
@@ -1400,8 +1434,10 @@ int emrkc_create(const emrkc_problem* p, int32_t device,
       g.st_hi[a] = 0;
     }
   }
+  g.naux = fields_of(p) - 4;
+  g.nf = fields_of(p);
   h->nn = g.nn;
-  h->len = 4 * g.nn;
+  h->len = static_cast<int64_t>(g.nf) * g.nn;
   if ((rc = init_handle(h))) {
     g_global_err = h->err;
     emrkc_destroy(h);
@@ -1618,7 +1654,7 @@ void scatter_slab(const emrkc_handle* h, const std::vector<double>& global,
                   int64_t global_nn, std::vector<double>& local) {
   local.resize(h->len);
   const int64_t off = h->z_begin * h->geom.plane;
-  for (int b = 0; b < 4; ++b)
+  for (int b = 0; b < h->geom.nf; ++b)
     std::memcpy(local.data() + b * h->nn, global.data() + b * global_nn + off,
                 sizeof(double) * h->nn);
 }
@@ -1689,7 +1725,7 @@ int power_iteration(const std::vector<emrkc_handle*>& hs, int which, double t,
   emrkc_handle* h0 = hs[0];
   const emrkc_problem& p = h0->p;
   const int64_t gnn = nodes_of(&p);
-  const int64_t glen = 4 * gnn;
+  const int64_t glen = static_cast<int64_t>(h0->geom.nf) * gnn;
   for (auto* h : hs)
     if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
   std::vector<double> v0(glen);
@@ -1722,7 +1758,7 @@ int power_iteration(const std::vector<emrkc_handle*>& hs, int which, double t,
       }
       return tot;
     }
-    for (int b = 0; b < 4; ++b)
+    for (int b = 0; b < h0->geom.nf; ++b)
       for (size_t r = 0; r < n; ++r) {
         emrkc_handle* h = hs[r];
         cudaSetDevice(h->device);
@@ -1840,7 +1876,7 @@ vout:
       cudaSetDevice(h->device);
       cudaMemcpy(local.data(), w[r].v[a], sizeof(double) * h->len, cudaMemcpyDeviceToHost);
       const int64_t off = h->z_begin * h->geom.plane;
-      for (int b = 0; b < 4; ++b)
+      for (int b = 0; b < h->geom.nf; ++b)
         std::memcpy(v_out_global + b * gnn + off, local.data() + b * h->nn,
                     sizeof(double) * h->nn);
     }
@@ -1870,6 +1906,7 @@ bool resident_ok(const emrkc_handle* h, int64_t nsteps) {
   }();
   const Plan& pl = h->plan;
   return on && h->fast && !h->partitioned && nsteps >= 2 && nsteps <= 10000000 &&
+         h->geom.naux == 0 &&
          pl.s == 1 && pl.m == 1 &&
          pl.method != kMethodMrkc && (h->geom.dim == 2 || h->geom.dim == 3) &&
          h->geom.nn <= emrkc_k::resident_capacity(h->geom.dim);
@@ -2431,7 +2468,7 @@ int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
   const size_t pitch = sizeof(double) * nn;  // one row per SoA field
   for (int c = 0; c < kHostChunks; ++c) {
     const int64_t off = zc(c) * plane, n = (zc(c + 1) - zc(c)) * plane;
-    CK(h, cudaMemcpy2DAsync(din + off, pitch, y_in + off, pitch, sizeof(double) * n, 4,
+    CK(h, cudaMemcpy2DAsync(din + off, pitch, y_in + off, pitch, sizeof(double) * n, h->geom.nf,
                             cudaMemcpyHostToDevice, h->s_in));
     CK(h, cudaEventRecord(h->ev_in[c], h->s_in));
   }
@@ -2463,7 +2500,7 @@ int step_host_pipe(emrkc_handle* h, double t, const double* y_in, double* y_out,
   for (int c = 0; c < kHostChunks; ++c) {
     CK(h, cudaStreamWaitEvent(h->s_out, h->ev_k[c], 0));
     const int64_t off = kr(c, m) * plane, n = (kr(c + 1, m) - kr(c, m)) * plane;
-    CK(h, cudaMemcpy2DAsync(y_out + off, pitch, dout + off, pitch, sizeof(double) * n, 4,
+    CK(h, cudaMemcpy2DAsync(y_out + off, pitch, dout + off, pitch, sizeof(double) * n, h->geom.nf,
                             cudaMemcpyDeviceToHost, h->s_out));
   }
   if (!h->h_event) CK(h, cudaHostAlloc(&h->h_event, sizeof(unsigned long long), 0));
@@ -2659,6 +2696,7 @@ int emrkc_imex_step(emrkc_handle* h, double t, double dt, double rel_tol, int64_
                     int32_t jacobi, emrkc_step_report* report, int64_t* cg_iters) {
   if (!h) return set_global(EMRKC_EINVAL, "null handle");
   if (h->partitioned) return set_err(h, EMRKC_EINVAL, "imex_rl_step: whole-grid handles only");
+  if (h->geom.naux > 0) return set_err(h, EMRKC_EINVAL, "imex_rl_step: HH only");
   if (!(dt > 0.0)) return set_err(h, EMRKC_EINVAL, "imex_rl_step: dt must be > 0");
   if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
   int rc = use_device(h);
@@ -2690,6 +2728,7 @@ int emrkc_imex_run(emrkc_handle* h, int64_t step0, int64_t nsteps, double dt, do
                    int64_t* cg_iters_total) {
   if (!h || !res) return set_global(EMRKC_EINVAL, "null argument");
   if (h->partitioned) return set_err(h, EMRKC_EINVAL, "imex_rl_step: whole-grid handles only");
+  if (h->geom.naux > 0) return set_err(h, EMRKC_EINVAL, "imex_rl_step: HH only");
   if (!(dt > 0.0)) return set_err(h, EMRKC_EINVAL, "imex_rl_step: dt must be > 0");
   if (nsteps < 0) return set_err(h, EMRKC_EINVAL, "emrkc_imex_run: nsteps must be >= 0");
   if (!h->has_state) return set_err(h, EMRKC_ESTATE, "no state uploaded");
@@ -3081,7 +3120,7 @@ int emrkc_slab_power_begin(emrkc_handle* h, int32_t which, const double* v0_slab
   if (v0_slab) {
     local.assign(v0_slab, v0_slab + h->len);
   } else {  // this slab's part of the reference's seeded direction over the global state
-    std::vector<double> v0(4 * nodes_of(&h->p));
+    std::vector<double> v0(static_cast<size_t>(h->geom.nf) * nodes_of(&h->p));
     seeded_direction(v0);
     scatter_slab(h, v0, nodes_of(&h->p), local);
   }
@@ -3110,8 +3149,8 @@ int emrkc_slab_power_sumsq(emrkc_handle* h, int32_t field, int32_t block, double
                            double* acc_out) {
   if (!h || !acc_out) return set_global(EMRKC_EINVAL, "null argument");
   if (h->sp_code < 0) return set_err(h, EMRKC_ESTATE, "slab power iteration not begun");
-  if (field < 0 || field > 1 || block < 0 || block > 3)
-    return set_err(h, EMRKC_EINVAL, "slab_power_sumsq: field 0/1, block 0..3");
+  if (field < 0 || field > 1 || block < 0 || block >= h->geom.nf)
+    return set_err(h, EMRKC_EINVAL, "slab_power_sumsq: field 0/1, block 0..fields-1");
   int rc = use_device(h);
   if (rc) return rc;
   const double* x = (field == 0 ? h->sp_v[h->sp_a] : h->buf[h->cur]) + block * h->nn;

@@ -21,6 +21,7 @@
 #include <climits>
 #include <cstdio>
 
+#include "aux.cuh"
 #include "hh.cuh"
 #include "kernels.h"
 
@@ -459,6 +460,12 @@ __global__ void __launch_bounds__(kThreads)
   for (int q = 0; q < 3; ++q)
     out[(q + 1) * nn + n.i] =
         (gm >> q & 1) ? __dmul_rn(l[q], __dsub_rn(y[(q + 1) * nn + n.i], zi[q])) : 0.0;
+  // aux rows (EMRKC_MODEL_HH_AUX): f_F 0, f_S aux_rates_field
+  // (P/src/monodomain.cpp:191-205, 214-221)
+  for (int a = 0; a < g.naux; ++a) {
+    const long long k = (4 + a) * nn + n.i;
+    out[k] = (which & 15) == 0 ? 0.0 : aux_rate_ref(a, V, y[k]);
+  }
 }
 
 // mRKC inner stage k of outer stage j, reference operation order
@@ -550,6 +557,10 @@ __global__ void __launch_bounds__(kThreads)
     lam[(q + 1) * nn + n.i] = l[q];
     yinf[(q + 1) * nn + n.i] = zi[q];
   }
+  for (int a = 0; a < g.naux; ++a) {  // exp_part is zero on the aux rows
+    lam[(4 + a) * nn + n.i] = 0.0;
+    yinf[(4 + a) * nn + n.i] = 0.0;
+  }
 }
 
 constexpr int kRedThreads = 256;
@@ -608,6 +619,16 @@ __global__ void __launch_bounds__(kRedThreads)
         acc = __dadd_rn(acc, __dmul_rn(dq, dq));
       }
       vout[(q + 1) * nn + i] = dq;
+    }
+    // aux rows: f_S(z) - f_S(y) (f_F is zero there)
+    for (int a = 0; a < g.naux; ++a) {
+      const long long k = (4 + a) * nn + i;
+      double da = 0.0;
+      if ((which & 15) != 0) {
+        da = __dsub_rn(aux_rate_ref(a, zv, z(k)), fy[k]);
+        acc = __dadd_rn(acc, __dmul_rn(da, da));
+      }
+      vout[k] = da;
     }
   }
   const double t = block_sum(acc);

@@ -38,6 +38,8 @@ struct Geom {
   double wc;              // -2 sum_a w_a (fast kernels)
   double inv_Cm, Cm;
   int st_lo[3], st_hi[3]; // stimulus node box per axis (global, inclusive)
+  int naux;               // auxiliary fields (EMRKC_MODEL_HH_AUX; 0 for HH)
+  int nf;                 // SoA fields of the state: 4 + naux
 };
 
 // Ghost planes of the V field consumed by one stencil level.
@@ -153,6 +155,7 @@ struct FastArgs {
   double cV;          // cG * mu'_1 eta  (m == 1: V of g_j = base + cV (f_F + f_S))
   double mue1;        // mu'_1 eta       (m >= 2: u_1 = V + mue1 (f_F + f_S))
   double nu, kappa;   // outer nu_j, kappa_j (j >= 2)
+  double cA;          // aux rows: mu_j dt c_m (g_j = base + cA g_S; inner c_m)
   double vmid, vfast; // fast ionic path iff |V - vmid| <= vfast (fast_window)
   int j, m, s, last, zc;
   int exex;           // EXEX-RL step: non-finite values are not aborts (guard only)

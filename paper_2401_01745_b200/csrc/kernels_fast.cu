@@ -23,6 +23,7 @@
 //               forms V of g_j.
 #include <cstdio>
 
+#include "aux.cuh"
 #include "fast_math.cuh"
 #include "hh.cuh"
 #include <algorithm>
@@ -383,6 +384,10 @@ __device__ __noinline__ bool inner_nonfinite(const Geom& g, const Halo& h, const
     const double y0 = z0 + d.d0, y1 = z1 + d.d1, y2 = z2 + d.d2;
     const double fs = -current_fast(V, y0, y1, y2) * g.inv_Cm;
     inner |= !(finite_hi(D + fs) && finite_hi(y0) && finite_hi(y1) && finite_hi(y2));
+    for (int q = 0; q < g.naux; ++q) {  // aux rows of u_1: z + mu'_1 eta g_S(V, z)
+      const double za = __ldg(G + (4 + q) * g.nn + j);
+      inner |= !(finite_hi(za) && finite_hi(aux_rate_fast(q, V, za)));
+    }
   }
   return inner;
 }
@@ -1191,10 +1196,10 @@ static_assert(EMRKC_SYNCP == 1 || (EMRKC_SYNCP == 2 && kTmaLA + 4 <= kRV),
               "k_node_tma barrier period");
 
 template <int DIM, int FIRST>
-constexpr size_t tma_node_smem_bytes() {
+constexpr size_t tma_node_smem_bytes(int naux = 0) {
   using T = PipeTile<DIM>;
-  return sizeof(double) * (kRV * TmaTile<DIM>::VS + kRGn<FIRST>() * 3 * T::NT +
-                           (FIRST ? 0 : kRG * 4 * T::NT)) + 128;
+  return sizeof(double) * (kRV * TmaTile<DIM>::VS + kRGn<FIRST>() * (3 + naux) * T::NT +
+                           (FIRST ? 0 : kRG * (4 + naux) * T::NT)) + 128;
 }
 
 // Issues the V box of local plane zz (interior, mirror, or ghost).
@@ -1229,9 +1234,12 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   extern __shared__ __align__(128) double smem_tma[];
   // 128-byte aligned stage base (pointer arithmetic keeps the shared space)
   double* vst = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;  // [kRV][VS]
-  double* gst = vst + kRV * VS;                     // [kRG][3][NT]
+  // gate stage: the three gates and the aux fields of the synthetic width
+  // stand-in (g.naux, include/emrkc.h), fields 1 .. nf - 1 of g_{j-1}
+  const int GF = 3 + g.naux, QF = 4 + g.naux;
+  double* gst = vst + kRV * VS;                     // [kRG][GF][NT]
   constexpr int RG = kRGn<FIRST>();
-  double* g2s = gst + RG * 3 * T::NT;               // [kRG][4][NT]
+  double* g2s = gst + RG * GF * T::NT;              // [kRG][QF][NT]
   __shared__ double tab[256];
   __shared__ __align__(8) unsigned long long bars[kRV];
   __shared__ int skip;
@@ -1257,7 +1265,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   const unsigned v0 = smem_u32(vst), gs0 = smem_u32(gst), qs0 = smem_u32(g2s);
   const unsigned b0 = smem_u32(bars);
   constexpr unsigned vbytes = 8u * TmaTile<DIM>::VT;
-  const unsigned cbytes = 8u * T::NT * (3 + (FIRST ? 0 : 4));
+  const unsigned cbytes = 8u * T::NT * (GF + (FIRST ? 0 : QF));
   // The copies of a plane are issued by lane 0 of warps 0 (expect_tx + V
   // box), 1 (gate box) and 2 (g_{j-2} box): the issue work is spread over
   // three warps instead of serialising one before the per-plane barrier.
@@ -1273,12 +1281,12 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
       else tma_load_2d(vd, &tm.v, bar, x0 - 2, zz);
     }
     if (role == (EMRKC_ISSUE1 ? 0 : 1)) {
-      if (DIM == 3) tma_load_4d(gs0 + 8u * 3 * T::NT * sg, &tm.gates, bar, x0, y0, zz, 1);
-      else tma_load_3d(gs0 + 8u * 3 * T::NT * sg, &tm.gates, bar, x0, zz, 1);
+      if (DIM == 3) tma_load_4d(gs0 + 8u * GF * T::NT * sg, &tm.gates, bar, x0, y0, zz, 1);
+      else tma_load_3d(gs0 + 8u * GF * T::NT * sg, &tm.gates, bar, x0, zz, 1);
     }
     if (!FIRST && role == (EMRKC_ISSUE1 ? 0 : 2)) {
-      if (DIM == 3) tma_load_4d(qs0 + 8u * 4 * T::NT * sg, &tm.g2, bar, x0, y0, zz, 0);
-      else tma_load_3d(qs0 + 8u * 4 * T::NT * sg, &tm.g2, bar, x0, zz, 0);
+      if (DIM == 3) tma_load_4d(qs0 + 8u * QF * T::NT * sg, &tm.g2, bar, x0, y0, zz, 0);
+      else tma_load_3d(qs0 + 8u * QF * T::NT * sg, &tm.g2, bar, x0, zz, 0);
     }
   };
   // halo plane zb - 1 or ze (V only; mirror or ghost at the slab edge)
@@ -1360,13 +1368,14 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     double xs = 0.0, ys = 0.0;
     if (DIM >= 2) xs = V0[cxm] + V0[cxp];
     if (DIM == 3) ys = V0[cym] + V0[cyp];
-    const double* G0 = gst + ((z - zb) & (RG - 1)) * 3 * T::NT + t;
+    const double* G0 = gst + ((z - zb) & (RG - 1)) * GF * T::NT + t;
+    const double* Q0 = g2s + ((z - zb) & (RG - 1)) * QF * T::NT + t;
     const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
     const bool fast = fabs(vc - a.vmid) <= a.vfast;
     if (!fast) slow_mask |= 1u << (z - zb);
     NodeOut r = node_update_s<DIM, FIRST, ION, 0>(
         g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, 0.0,
-        g2s + ((z - zb) & (RG - 1)) * 4 * T::NT + t, T::NT);
+        Q0, T::NT);
     if (z >= zs0 && z <= zs1) {
       if (ION) r.o0 = fma(a.mue1, a.stim, r.o0);
       else r.o0 = fma(a.cV, a.stim, r.o0);
@@ -1382,6 +1391,15 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       finacc = min(finacc, ~(unsigned)__double2hiint((r.o0 + r.o1) + (r.o2 + r.o3)) & 0x7ff00000u);
+      // aux rows: y_E = z (no exponential part), f_S = g_S(V, z), the inner
+      // iterate z + c_m eta g_S, g_j = base + (mu_j dt c_m) g_S
+      for (int q = 0; q < g.naux; ++q) {
+        const double za = G0[(3 + q) * T::NT];
+        const double base = FIRST ? za : fma(a.nu, za, a.kappa * Q0[(4 + q) * T::NT]);
+        const double oa = fma(a.cA, aux_rate_fast(q, vc, za), base);
+        po[(4 + q) * nn] = oa;
+        finacc = min(finacc, ~(unsigned)__double2hiint(oa) & 0x7ff00000u);
+      }
       if (z < pp.zl) pp.plo[ip + plane * z] = r.o0;
       if (z >= pp.zh) pp.phi[ip + plane * (z - pp.zh)] = r.o0;
       if (a.last) {  // std::min / std::max per value (NaN skipped), select form
@@ -1429,6 +1447,13 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
+      for (int q = 0; q < g.naux; ++q) {
+        const double za = __ldg(G + (4 + q) * nn + i);
+        const double base = FIRST ? za : fma(a.nu, za, a.kappa * __ldg(a.g2 + (4 + q) * nn + i));
+        const double oa = fma(a.cA, aux_rate_fast(q, vc, za), base);
+        a.out[(4 + q) * nn + i] = oa;
+        bad |= !finite_hi(oa);
+      }
       if (z < pp.zl) pp.plo[ip + plane * z] = r.o0;
       if (z >= pp.zh) pp.phi[ip + plane * (z - pp.zh)] = r.o0;
       if (a.last) {
@@ -2880,12 +2905,12 @@ template <int D, int F, int I>
 static cudaError_t launch_node_tma_t(const Geom& g, const Halo& h, const FastArgs& a,
                                      const TmaNode& tm, cudaStream_t st) {
   using T = PipeTile<D>;
-  constexpr size_t smem = tma_node_smem_bytes<D, F>();
-  static bool attr = false;
-  if (!attr) {
+  const size_t smem = tma_node_smem_bytes<D, F>(g.naux);
+  static size_t attr = 0;
+  if (smem > attr) {
     cudaFuncSetAttribute(k_node_tma<D, F, I>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    attr = true;
+    attr = smem;
   }
   const int chunks = (a.z_hi - a.z_lo + a.zc - 1) / a.zc;
   const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)

@@ -47,7 +47,8 @@ def slab_of(problem: Problem, part: Partition, y_global: np.ndarray) -> np.ndarr
     nn = problem.n_nodes
     plane = nn // int(problem.n[problem.dim - 1])
     z0, z1 = int(part.z_begin), int(part.z_end)
-    return np.concatenate([y_global[b * nn + z0 * plane: b * nn + z1 * plane] for b in range(4)])
+    return np.concatenate([y_global[b * nn + z0 * plane: b * nn + z1 * plane]
+                           for b in range(problem.n_fields)])
 
 
 def first_event_key(rec: dict):
@@ -118,7 +119,7 @@ def slab_rho(sp, ctx: DistContext, which: int, t: float = 0.0, v0_slab=None,
 
     def norm(field):
         acc = 0.0
-        for b in range(4):
+        for b in range(sp.n_fields):
             acc = ctx.chain(lambda a, b=b: sp.sumsq(field, b, a), acc)
         return math.sqrt(acc)
 
@@ -160,6 +161,7 @@ class DeviceSlabPower:
         self.op = op
         self.lib = _lib()
         prob = op.problem
+        self.n_fields = prob.n_fields
         self.plane_len = int(prob.n_nodes // int(prob.n[prob.dim - 1]))
         self.torch = torch
 
@@ -324,14 +326,18 @@ def slab_initial_state(w, part: Partition) -> np.ndarray:
     nn = w.n_nodes
     plane = nn // int(p.n[p.dim - 1])
     a, b = int(part.z_begin) * plane, int(part.z_end) * plane
+    from .workloads import aux_rest
+
     V, z = resting_state()
     rng = np.random.default_rng(w.seed)
-    blocks = [np.full(b - a, V)] + [np.full(b - a, z[g]) for g in range(3)]
+    nf = p.n_fields
+    blocks = [np.full(b - a, V)] + [np.full(b - a, z[g]) for g in range(3)] + \
+        [np.full(b - a, aux_rest(q, V)) for q in range(nf - 4)]
     if w.noise == "v_normal_0.1":
         blocks[0] += rng.normal(0.0, 0.1, nn)[a:b]
     elif w.noise == "mult_uniform_0.01":
-        f = rng.uniform(0.99, 1.01, 4 * nn)
-        for k in range(4):
+        f = rng.uniform(0.99, 1.01, nf * nn)
+        for k in range(nf):
             blocks[k] *= f[k * nn + a:k * nn + b]
     return np.concatenate(blocks)
 

@@ -117,11 +117,14 @@ def resting_state(model: int = capi.EMRKC_MODEL_HH):
 
 def make_problem(dim: int, n, dx, sigma, chi=140.0, C_m=0.01, stim_amplitude=0.0,
                  stim_lo=(0.0, 0.0, 0.0), stim_hi=(0.0, 0.0, 0.0), stim_t0=0.0,
-                 stim_t1=0.0) -> Problem:
-    """Problem struct (grid by node counts; units mm, ms, mS/mm, uA/mm^3)."""
+                 stim_t1=0.0, n_aux: int = 0) -> Problem:
+    """Problem struct (grid by node counts; units mm, ms, mS/mm, uA/mm^3).
+    n_aux > 0 selects EMRKC_MODEL_HH_AUX, the SYNTHETIC width stand-in (HH
+    plus n_aux passive auxiliary variables; include/emrkc.h)."""
     p = Problem()
     p.dim = dim
-    p.model = capi.EMRKC_MODEL_HH
+    p.model = capi.EMRKC_MODEL_HH_AUX if n_aux else capi.EMRKC_MODEL_HH
+    p.n_aux = n_aux
     n = list(n) + [1] * (3 - len(n))
     dx = list(dx) + [0.0] * (3 - len(dx))
     sigma = list(sigma) + [0.0] * (3 - len(sigma))
@@ -156,6 +159,9 @@ class StateLayout:
     def gate_offset(self, g: int) -> int:
         return self.n_nodes * (1 + g)
 
+    def aux_offset(self, a: int) -> int:
+        return self.n_nodes * (1 + self.n_gates + a)
+
 
 @dataclass
 class RhoEstimate:
@@ -185,7 +191,7 @@ class MonodomainOperator:
                                    C.byref(h)))
         self._h = h
         self.len = int(_lib().emrkc_local_len(h))
-        self.layout_ = StateLayout(self.len // 4)
+        self.layout_ = StateLayout(self.len // problem.n_fields, 3, int(problem.n_aux))
 
     def close(self):
         if self._h:
@@ -206,14 +212,17 @@ class MonodomainOperator:
         return self.layout_
 
     def initial_state(self) -> np.ndarray:
-        """Uniform resting state (P/src/monodomain.cpp:306-319)."""
-        V, z = resting_state()
-        nn = self.layout_.n_nodes
-        y = np.empty(4 * nn)
-        y[:nn] = V
-        for g in range(3):
-            y[(1 + g) * nn:(2 + g) * nn] = z[g]
-        return y
+        """Uniform resting state (P/src/monodomain.cpp:306-319) of this
+        handle's slab (the whole grid without a partition)."""
+        p = self.problem
+        y = np.empty(p.state_len())
+        _check(_lib().emrkc_initial_state(C.byref(p), dptr(y), y.size))
+        if self.partition is None:
+            return y
+        nn, nf = p.n_nodes, p.n_fields
+        plane = nn // int(p.n[p.dim - 1])
+        a, b = int(self.partition.z_begin) * plane, int(self.partition.z_end) * plane
+        return np.concatenate([y[k * nn + a:k * nn + b] for k in range(nf)])
 
     def set_state(self, y: np.ndarray):
         y = np.ascontiguousarray(y, dtype=np.float64)

@@ -42,17 +42,21 @@ class Workload:
         return self.problem.n_nodes
 
     def initial_state(self, resting=None) -> np.ndarray:
-        """HH resting state + the workload's seeded noise. ``resting`` is a
+        """HH resting state (plus the auxiliary rest values of the synthetic
+        width stand-in) + the workload's seeded noise. ``resting`` is a
         provider of (V_rest, z_rest) — default the library's
         ``emrkc_resting_state``; the CPU reference arm passes the
         reference's own (oracle/_ref ``resting_state``, bit-identical), so
         that process never maps the product library."""
         V, z = (resting or resting_state)()
         nn = self.n_nodes
-        y = np.empty(4 * nn)
+        na = int(self.problem.n_aux)
+        y = np.empty((4 + na) * nn)
         y[:nn] = V
         for g in range(3):
             y[(1 + g) * nn:(2 + g) * nn] = z[g]
+        for a in range(na):  # HHAux::resting_state (include/emrkc.h)
+            y[(4 + a) * nn:(5 + a) * nn] = aux_rest(a, V)
         rng = np.random.default_rng(self.seed)
         if self.noise == "v_normal_0.1":
             y[:nn] += rng.normal(0.0, 0.1, nn)
@@ -72,11 +76,19 @@ class Workload:
             "dt_ms": self.dt,
             "t_end_ms": self.t_end,
             "steps": self.n_steps,
-            "ionic_model": "hh",
+            "ionic_model": ("hh_aux (SYNTHETIC width stand-in: HH + %d passive aux)" % p.n_aux
+                            if p.n_aux else "hh"),
+            "state_fields": p.n_fields,
             "noise": self.noise,
             "seed": self.seed,
             "note": self.note,
         }
+
+
+def aux_rest(a: int, V: float) -> float:
+    """Rest value of auxiliary variable a of EMRKC_MODEL_HH_AUX
+    (include/emrkc.h): s1_a V_rest + s0_a, the C expression's order."""
+    return (0.01 * float(a % 3)) * V + (0.5 + 0.1 * float(a % 4))
 
 
 def _box(h, lo_idx, hi_idx):
@@ -152,6 +164,22 @@ def parity_3d() -> Workload:
     return Workload("p3d_48_s2m2", p, 0.05, 2.0, "v_normal_0.1", 8, rho_S_forced=50.0)
 
 
+def synthetic_width(w: Workload, n_fields: int) -> Workload:
+    """``w``'s grid, stimulus, dt, T and noise with the SYNTHETIC width
+    stand-in EMRKC_MODEL_HH_AUX of n_fields SoA fields (SURVEY §8(c)
+    option 2: CRN's 21 / TTP's 19 state variables for configs 3 / 4, whose
+    equations are not available; no physiology claim)."""
+    p = w.problem
+    q = make_problem(p.dim, [int(p.n[a]) for a in range(p.dim)], [p.dx[a] for a in range(p.dim)],
+                     [p.sigma[a] for a in range(p.dim)], p.chi, p.C_m, p.stim_chi_amplitude,
+                     [p.stim_lo[a] for a in range(p.dim)], [p.stim_hi[a] for a in range(p.dim)],
+                     p.stim_t0, p.stim_t1, n_aux=n_fields - 4)
+    return Workload(f"{w.name}_w{n_fields}", q, w.dt, w.t_end, w.noise, w.seed, w.eps,
+                    w.rho_S_forced,
+                    note=f"SYNTHETIC width stand-in: HH + {n_fields - 4} passive auxiliary "
+                         f"variables (N = {n_fields}), no physiology claim; {w.note}")
+
+
 REGISTRY = {
     "hh2d_256x256": hh2d_256,
     "hh3d_128x128x128": hh3d_128,
@@ -163,6 +191,9 @@ REGISTRY = {
     "hh3d_sweep_200": lambda: hh3d_sweep(200),
     "p2d_128_s3m2": parity_2d,
     "p3d_48_s2m2": parity_3d,
+    # configs 3 / 4 at their models' state width (CRN 21, TTP 19), synthetic
+    "hh3d_256x256x128_w21": lambda: synthetic_width(hh3d_256x256x128(), 21),
+    "hh3d_512x512x256_w19": lambda: synthetic_width(hh3d_512x512x256(), 19),
 }
 
 
@@ -184,7 +215,8 @@ def z_scaled(w: Workload, n: int) -> Workload:
     q = make_problem(p.dim, [int(p.n[a]) * (n if a == p.dim - 1 else 1) for a in range(p.dim)],
                      [p.dx[a] for a in range(p.dim)], [p.sigma[a] for a in range(p.dim)],
                      p.chi, p.C_m, p.stim_chi_amplitude, [p.stim_lo[a] for a in range(p.dim)],
-                     [p.stim_hi[a] for a in range(p.dim)], p.stim_t0, p.stim_t1)
+                     [p.stim_hi[a] for a in range(p.dim)], p.stim_t0, p.stim_t1,
+                     n_aux=int(p.n_aux))
     return Workload(f"{w.name}_zx{n}", q, w.dt, w.t_end, w.noise, w.seed, w.eps, w.rho_S_forced,
                     note=(w.note + "; " if w.note else "") +
                     f"weak scaling: {w.name} repeated {n}x along z (one copy per GPU)")
@@ -205,10 +237,12 @@ def z_slab_sample(w: Workload, z0: int, depth: int, resting=None):
     q = make_problem(3, [int(p.n[0]), int(p.n[1]), depth], [p.dx[a] for a in range(3)],
                      [p.sigma[a] for a in range(3)], p.chi, p.C_m, p.stim_chi_amplitude,
                      [p.stim_lo[0], p.stim_lo[1], p.stim_lo[2] - z0 * h],
-                     [p.stim_hi[0], p.stim_hi[1], p.stim_hi[2] - z0 * h], p.stim_t0, p.stim_t1)
+                     [p.stim_hi[0], p.stim_hi[1], p.stim_hi[2] - z0 * h], p.stim_t0, p.stim_t1,
+                     n_aux=int(p.n_aux))
     y = w.initial_state(resting=resting)
     nn, plane = p.n_nodes, int(p.n[0]) * int(p.n[1])
-    ys = np.concatenate([y[b * nn + z0 * plane: b * nn + (z0 + depth) * plane] for b in range(4)])
+    ys = np.concatenate([y[b * nn + z0 * plane: b * nn + (z0 + depth) * plane]
+                         for b in range(p.n_fields)])
     ws = Workload(f"{w.name}[z{z0}:{z0 + depth}]", q, w.dt, w.t_end, w.noise, w.seed, w.eps,
                   w.rho_S_forced, note=f"planes {z0}..{z0 + depth - 1} of {w.name} as a "
                                        f"standalone no-flux slab (bounded CPU sample)")

@@ -43,7 +43,7 @@ NSAMP = 65536
 
 def block_stats(y, nn, n_planes):
     out = {}
-    for b in range(4):
+    for b in range(len(y) // nn):
         blk = y[b * nn:(b + 1) * nn]
         pl = blk.reshape(n_planes, -1)
         out[f"norm2_{b}"] = np.float64(np.linalg.norm(blk))
@@ -82,7 +82,7 @@ def main():
         y1 = y0 * (1.0 + 1e-15 * np.random.default_rng(seed).uniform(-1.0, 1.0, y0.size))
         yp, resp, _ = ref.run(p, y1, 0, n, w.dt, w.eps, rF.rho, rS.rho)
         sv = [float(ref_rel_l2(ref, p, yp[b * nn:(b + 1) * nn], y[b * nn:(b + 1) * nn]))
-              for b in range(4)]
+              for b in range(p.n_fields)]
         same = bool(resp.abort_step == res.abort_step and resp.aborted == res.aborted)
         sens.append({"seed": seed, "rel_l2": sv, "same_abort": same})
         print(w.name, "sensitivity seed", seed, sv, "same abort", same, flush=True)
@@ -96,7 +96,7 @@ def main():
     out = a.out or os.path.join(HERE, f"big_{w.name}.npz")
     np.savez_compressed(out, meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8),
                         sample_index=idx.astype(np.int64),
-                        sample=np.stack([y[b * nn:(b + 1) * nn][idx] for b in range(4)]),
+                        sample=np.stack([y[b * nn:(b + 1) * nn][idx] for b in range(p.n_fields)]),
                         **st)
     print("wrote", out, flush=True)
 

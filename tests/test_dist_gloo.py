@@ -150,6 +150,7 @@ class HostSlabPower:
     gate rows pointwise. Norms continue the running sum in serial order."""
 
     P, NZ = 6, 24
+    n_fields = 4
 
     def __init__(self, y_global, v_global, z0, z1):
         import numpy as np

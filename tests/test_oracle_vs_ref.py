@@ -178,3 +178,39 @@ def test_imex_rl_cg_failure(oracle, reference):
     _same_records(ra, rb)
     assert ra.aborted and ra.abort_step == 4 and ra.steps_done == 0
     assert np.array_equal(ya, y0) and np.array_equal(yb, y0)
+
+
+@pytest.mark.parametrize("n_aux,rS,nsteps", [(15, 0.7, 6), (17, 60.0, 4)])
+def test_synthetic_width_bitwise(oracle, reference, n_aux, rS, nsteps):
+    """EMRKC_MODEL_HH_AUX (the SYNTHETIC width stand-in, include/emrkc.h): the
+    C restatement against the reference's own generic machinery (StateLayout
+    with n_aux, f_S aux rows, exponential Euler passing aux through) running
+    the harness's HHAux IonicModel: bit-identical operator pieces, rho and
+    runs (s = 1 and forced s = 2, m = 2)."""
+    from paper_2401_01745_b200.monodomain import make_problem
+
+    h = 0.1
+    p = make_problem(3, [12, 10, 9], [h] * 3, [0.3, 0.1, 0.1], 140.0, 0.01, 70.0,
+                     [-0.05] * 3, [0.35] * 3, 0.0, 1.0, n_aux=n_aux)
+    assert p.state_len() == (4 + n_aux) * p.n_nodes
+    y0 = oracle.initial_state(p)
+    assert np.array_equal(y0, reference.initial_state(p))
+    rng = np.random.default_rng(9)
+    y = y0 * rng.uniform(0.99, 1.01, y0.size)
+    for which in (0, 1):
+        assert np.array_equal(oracle.rhs(p, which, 0.5, y), reference.rhs(p, which, 0.5, y))
+    la, ia = oracle.exp_part(p, y)
+    lb, ib = reference.exp_part(p, y)
+    assert np.array_equal(la, lb) and np.array_equal(ia, ib)
+    eF, _ = oracle.estimate_rho(p, 0, 0.0, y)
+    fF, _ = reference.estimate_rho(p, 0, 0.0, y)
+    eS, _ = oracle.estimate_rho(p, 1, 0.0, y)
+    fS, _ = reference.estimate_rho(p, 1, 0.0, y)
+    assert (eF.rho, eF.iterations, eS.rho, eS.iterations) == \
+        (fF.rho, fF.iterations, fS.rho, fS.iterations)
+    ya, ra, _ = oracle.run(p, y, 0, nsteps, 0.05, 0.05, 250.0, rS)
+    yb, rb, _ = reference.run(p, y, 0, nsteps, 0.05, 0.05, 250.0, rS)
+    assert np.array_equal(ya, yb) and (ra.s, ra.m) == (rb.s, rb.m)
+    for k, _ in ra._fields_:
+        if k != "device_ms":
+            assert getattr(ra, k) == getattr(rb, k), k
