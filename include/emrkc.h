@@ -176,7 +176,8 @@ int emrkc_rkc_coeffs(int32_t s, double epsilon, double* omega0,
 int emrkc_plan_step(double dt, double rho_F, double rho_S, double epsilon,
                     emrkc_step_report* plan);
 
-/* IonicModel::n_gates/n_aux — P/include/mrkc/ionic.hpp:22-23. */
+/* IonicModel::n_gates/n_aux — P/include/mrkc/ionic.hpp:22-23 (HH_AUX: the
+ * aux count is per problem; the maximum, EMRKC_MAX_AUX, is reported). */
 int emrkc_model_info(int32_t model, int32_t* n_gates, int32_t* n_aux);
 
 /* IonicModel::resting_state — P/src/ionic.cpp:42-77. gates: n_gates. */

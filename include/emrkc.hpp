@@ -36,6 +36,7 @@
 // stages, std::runtime_error for device failures.
 #pragma once
 
+#include <algorithm>
 #include <exception>
 #include <functional>
 #include <memory>
@@ -131,29 +132,34 @@ struct RunResult {
 class DeviceMonodomain {
  public:
   explicit DeviceMonodomain(const emrkc_problem& p, int device = 0,
-                            const emrkc_partition* part = nullptr) {
+                            const emrkc_partition* part = nullptr)
+      : p_(p), part_(part ? *part : emrkc_partition{0, p.n[p.dim - 1]}) {
     check(emrkc_create(&p, device, part, &h_));
   }
   ~DeviceMonodomain() { emrkc_destroy(h_); }
   DeviceMonodomain(const DeviceMonodomain&) = delete;
   DeviceMonodomain& operator=(const DeviceMonodomain&) = delete;
-  DeviceMonodomain(DeviceMonodomain&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  DeviceMonodomain(DeviceMonodomain&& o) noexcept : p_(o.p_), part_(o.part_), h_(o.h_) {
+    o.h_ = nullptr;
+  }
 
   emrkc_handle* handle() const { return h_; }
   int64_t size() const { return emrkc_local_len(h_); }
 
-  // Uniform resting state (P/src/monodomain.cpp:306-319).
+  // Uniform resting state (P/src/monodomain.cpp:306-319) of this handle's
+  // slab: [V | gates | aux] (aux for EMRKC_MODEL_HH_AUX).
   Vec initial_state() const {
-    double V = 0.0, z[3];
-    check(emrkc_resting_state(EMRKC_MODEL_HH, &V, z));
-    const int64_t nn = size() / 4;
-    Vec y(size());
-    for (int64_t i = 0; i < nn; ++i) {
-      y[i] = V;
-      for (int g = 0; g < 3; ++g) y[(1 + g) * nn + i] = z[g];
-    }
+    const int64_t glen = emrkc_state_len(&p_, nullptr);
+    Vec g(glen);
+    check(emrkc_initial_state(&p_, g.data(), glen));
+    const int64_t nz = p_.n[p_.dim - 1], gnn = glen / fields(), plane = gnn / nz;
+    const int64_t a = part_.z_begin * plane, n = (part_.z_end - part_.z_begin) * plane;
+    Vec y(static_cast<size_t>(fields() * n));
+    for (int64_t f = 0; f < fields(); ++f)
+      std::copy(g.begin() + f * gnn + a, g.begin() + f * gnn + a + n, y.begin() + f * n);
     return y;
   }
+  int64_t fields() const { return 4 + (p_.model == EMRKC_MODEL_HH_AUX ? p_.n_aux : 0); }
 
   void set_state(const Vec& y) { check(emrkc_set_state(h_, y.data(), (int64_t)y.size()), h_); }
   Vec get_state() const {
@@ -271,6 +277,8 @@ class DeviceMonodomain {
     out.resize(y.size());
     check(emrkc_eval_rhs(h_, which, t, y.data(), out.data(), (int64_t)y.size()), h_);
   }
+  emrkc_problem p_{};
+  emrkc_partition part_{};
   emrkc_handle* h_ = nullptr;
 };
 

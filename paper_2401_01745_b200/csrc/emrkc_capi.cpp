@@ -1302,10 +1302,11 @@ int emrkc_plan_step(double dt, double rho_F, double rho_S, double epsilon,
 }
 
 int emrkc_model_info(int32_t model, int32_t* n_gates, int32_t* n_aux) {
-  if (model != EMRKC_MODEL_HH)
+  if (model != EMRKC_MODEL_HH && model != EMRKC_MODEL_HH_AUX)
     return set_global(EMRKC_EINVAL, "unknown ionic model %d", model);
   if (n_gates) *n_gates = 3;
-  if (n_aux) *n_aux = 0;
+  // HH_AUX: the problem's n_aux (1 .. EMRKC_MAX_AUX); reported as the maximum
+  if (n_aux) *n_aux = model == EMRKC_MODEL_HH ? 0 : EMRKC_MAX_AUX;
   return EMRKC_OK;
 }
 
