@@ -320,3 +320,103 @@ def test_callback_exception_propagates():
     # the context is usable afterwards
     out = I.rkc_iteration(0.0, [2.0], 0.3, lambda t, y: -4.0 * y, 1, 0.05)
     assert out[0] == pytest.approx(2.0 * (1.0 - 1.2), rel=1e-14)
+
+
+# ---- the reference's nonlinear-system checks (P/tests/test_multirate.cpp:236-389)
+
+def _test_system(lE=-3.0):
+    """y0' = -5 y0 (fast), y1' = -y1 y0 (slow), y2' = lE (y2 - 0.5) (exp)."""
+    def fF(t, y):
+        out = np.zeros_like(y)
+        out[0] = -5.0 * y[0]
+        return out
+
+    def fS(t, y):
+        out = np.zeros_like(y)
+        out[1] = -y[1] * y[0]
+        return out
+
+    def ex(y):
+        lam = np.zeros_like(y)
+        yinf = np.zeros_like(y)
+        lam[2], yinf[2] = lE, 0.5
+        return lam, yinf
+
+    def exact(t, y0):
+        return np.array([y0[0] * math.exp(-5.0 * t),
+                         y0[1] * math.exp((math.exp(-5.0 * t) - 1.0) / 5.0 * y0[0]),
+                         0.5 + (y0[2] - 0.5) * math.exp(lE * t)])
+
+    return (lambda: I.GenericSplitRhs(fF, fS, ex, 5.0, 1.5)), exact
+
+
+def _slope(xs, ys):
+    x, y = np.log(xs), np.log(ys)
+    n = len(x)
+    return (n * (x * y).sum() - x.sum() * y.sum()) / (n * (x * x).sum() - x.sum() ** 2)
+
+
+def test_emrkc_lambda_zero_equals_mrkc_nonlinear():
+    """:287-314, 30 random nonlinear systems, 1e-13."""
+    rng = np.random.default_rng(23)
+    for _ in range(30):
+        n = 2 + int(rng.integers(0, 9))
+
+        def fF(t, y):
+            out = -30.0 * y
+            out[1:] += 2.0 * y[:-1]
+            return out
+
+        rhs = I.GenericSplitRhs(fF, lambda t, y: -0.5 * y * y + 0.1 * np.sin(y),
+                                lambda y: (np.zeros_like(y), np.full_like(y, 0.3)), 35.0, 2.0)
+        y = rng.random(n)
+        dt = 0.05 + 0.2 * rng.random()
+        a, _ = I.mrkc_step(0.0, y, dt, rhs)
+        b, _ = I.emrkc_step(0.0, y, dt, rhs)
+        assert np.abs(a - b).max() < 1e-13
+
+
+@pytest.mark.parametrize("variant", [capi.EMRKC_VARIANT_STANDARD, capi.EMRKC_VARIANT_PROGRESSIVE])
+def test_local_error_order_two(variant):
+    """:316-342: one-step error slope 2 +- 0.15 over dt = 2^-4 .. 2^-10."""
+    mk, exact = _test_system()
+    y0 = np.array([1.0, 1.0, 0.9])
+    hs, errs = [], []
+    for k in range(4, 11):
+        dt = 2.0 ** -k
+        out, _ = I.emrkc_step(0.0, y0, dt, mk(), 0.05, variant)
+        hs.append(dt)
+        errs.append(np.abs(out - exact(dt, y0)).max())
+    assert abs(_slope(hs, errs) - 2.0) <= 0.15
+
+
+def test_global_first_order():
+    """:344-389: global error slope 1 +- 0.1 for emRKC and for mRKC with the
+    exponential part folded into f_S, dt = 2^-3 .. 2^-8 to T = 1."""
+    mk, exact = _test_system()
+    y0 = np.array([1.0, 1.0, 0.9])
+
+    def em(t, y, dt):
+        return I.emrkc_step(t, y, dt, mk())[0]
+
+    def mr(t, y, dt):
+        r = mk()
+        base = r.f_S
+
+        def fS(t2, y2):
+            out = base(t2, y2)
+            out[2] += -3.0 * (y2[2] - 0.5)
+            return out
+
+        return I.mrkc_step(t, y, dt, I.GenericSplitRhs(r.f_F, fS, None, 5.0, 4.0))[0]
+
+    for stepper in (em, mr):
+        hs, errs = [], []
+        for k in range(3, 9):
+            dt = 2.0 ** -k
+            y = y0.copy()
+            for i in range(round(1.0 / dt)):
+                y = stepper(i * dt, y, dt)
+            hs.append(dt)
+            errs.append(np.abs(y - exact(1.0, y0)).max())
+        assert abs(_slope(hs, errs) - 1.0) <= 0.1
