@@ -1220,6 +1220,7 @@ int init_handle(emrkc_handle* h) {
   // node kernel, 0: march
   h->pipe = (pp && *pp) ? std::atoi(pp) : 3;
   if (h->pipe == 3 && !tma_supported(h)) h->pipe = 1;
+  if (h->pipe != 3) h->zc = std::min(h->zc, emrkc_k::kMaxZcPipe);
   if (const char* tb = std::getenv("EMRKC_TB"))
     if (*tb) h->tb = std::atoi(tb) != 0;
   if (const char* fu = std::getenv("EMRKC_FUSED"))
@@ -1227,7 +1228,9 @@ int init_handle(emrkc_handle* h) {
   if (const char* zp = std::getenv("EMRKC_ZPIPE"))
     if (*zp) h->zpipe = std::max(0, std::min(64, std::atoi(zp)));
   if (const char* zc = std::getenv("EMRKC_ZC"))
-    if (*zc) h->zc = std::min(emrkc_k::kMaxZc, std::max(1, std::atoi(zc)));
+    if (*zc)
+      h->zc = std::min(h->pipe == 3 ? emrkc_k::kMaxZc : emrkc_k::kMaxZcPipe,
+                       std::max(1, std::atoi(zc)));
   return EMRKC_OK;
 }
 

@@ -279,9 +279,10 @@ struct TmaVin {
 // Tile shape of the staged kernels (x, y per block; 2-D grids use TX2 x 1).
 constexpr int kTX3 = 32, kTY3 = 4, kTX2 = 128;
 
-// z-chunk length of the staged kernels (bounded by the 32-bit deferred-node
-// mask of k_node_pipe / k_node_tma).
-constexpr int kMaxZc = 32;
+// z-chunk length of the staged kernels: k_node_tma's deferred-node mask is
+// 64 bits wide; k_node_pipe / k_node_persist keep a 32-bit one (kMaxZcPipe).
+constexpr int kMaxZc = 64;
+constexpr int kMaxZcPipe = 32;
 
 // Window of V where the fast ionic path (fast_math.cuh, hh_expeuler_fast)
 // is valid for this eta: eta * (alpha + beta) <= 600 for every gate and every

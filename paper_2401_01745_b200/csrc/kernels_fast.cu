@@ -1343,7 +1343,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   // finite test folded over the hot loop: min over nodes of the sum's
   // (~hi & exponent mask); 0 means some node produced Inf/NaN
   unsigned finacc = 0x7ff00000u;
-  unsigned slow_mask = 0;
+  unsigned long long slow_mask = 0;  // planes z - zb (< kMaxZc = 64) left to the reference path
   double glo = 2.0, ghi = -1.0;
   double* po = a.out + ip + plane * zb;
   double* pu = ION ? a.u1 + ip + plane * zb : nullptr;
@@ -1372,7 +1372,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     const double* Q0 = g2s + ((z - zb) & (RG - 1)) * QF * T::NT + t;
     const double z0 = G0[0], z1 = G0[T::NT], z2 = G0[2 * T::NT];
     const bool fast = fabs(vc - a.vmid) <= a.vfast;
-    if (!fast) slow_mask |= 1u << (z - zb);
+    if (!fast) slow_mask |= 1ull << (z - zb);
     NodeOut r = node_update_s<DIM, FIRST, ION, 0>(
         g, a, tab, vm, vc, vp, xs, ys, z0, z1, z2, 0.0,
         Q0, T::NT);
@@ -1422,7 +1422,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     const Nbr<DIM> o = nbr_of<DIM>(g, Col<DIM>{cx, cy, ip, zb, ze, true});
     const double* G = a.g1;
     for (int z = zb; z < ze; ++z) {
-      if (!(slow_mask >> (z - zb) & 1u)) continue;
+      if (!(slow_mask >> (z - zb) & 1ull)) continue;
       const long long i = ip + plane * z;
       const double vc = __ldg(G + i);
       const double vm = zval(G, g, ip, z - 1, h.lo, h.hi);
@@ -2730,7 +2730,7 @@ int fast_zc(const Geom& g) {
   if (g.dim == 1) return 1;
   const long long tiles = (g.dim == 3) ? ((g.n0 + 31) / 32) * (long long)((g.n1 + 3) / 4)
                                        : (g.n0 + 127) / 128;
-  // Longest z-chunk (<= 32: the deferred-node mask width) that still gives
+  // Longest z-chunk (<= 48, below the 64-bit deferred-node mask) that still gives
   // >= 1.7 waves of resident node blocks (5 per SM): long chunks amortise
   // the halo planes and the pipeline prologue, the wave floor keeps the
   // tail short (measured on B200).
@@ -2742,7 +2742,9 @@ int fast_zc(const Geom& g) {
       sms = 148;
   }
   const long long want = (long long)(1.7 * sms * 5);
-  for (int zc = kMaxZc; zc >= 4; --zc)
+  // longest chunk: 48 (config-4 step, B200, r02: zc 32 / 48 / 64 -> 1.205 /
+  // 1.186 / 1.200 ms)
+  for (int zc = 48; zc >= 4; --zc)
     if (tiles * ((g.nzl + zc - 1) / zc) >= want) return zc > g.nzl ? g.nzl : zc;
   int zc = 16;
   while (zc > 4 && tiles * ((g.nzl + zc - 1) / zc) < 148LL * 5 * 2) zc /= 2;
