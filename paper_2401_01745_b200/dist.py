@@ -354,9 +354,10 @@ def rho_slabs(ctx, w, slab):
     return rF, rS
 
 
-def _timed(ctx, w, local, warmup, steps, ClockSampler=None):
+def _timed(ctx, w, local, warmup, steps, ClockSampler=None, rho=None):
     """Device time of ``steps`` distributed steps of ``w`` (L2 flushed before
-    every step), max over ranks; returns (ms, record, clocks, slab, rho)."""
+    every step), max over ranks; returns (ms, record, clocks, slab, rho).
+    ``rho``: given (rho_F, rho_S) instead of the distributed estimate."""
     import torch
     import torch.distributed as dist
 
@@ -364,7 +365,7 @@ def _timed(ctx, w, local, warmup, steps, ClockSampler=None):
     slab.link()
     y0 = slab_initial_state(w, slab.part)
     slab.op.set_state(y0)
-    rF, rS = rho_slabs(ctx, w, slab)
+    rF, rS = rho if rho is not None else rho_slabs(ctx, w, slab)
     slab.run(0, warmup, w.dt, rF, rS, w.eps)
     slab.op.set_state(y0)
     dist.barrier()
@@ -475,6 +476,29 @@ def bench_main(args, w, metric, config_of, hbm_peak, ClockSampler):
         except Exception as ex:
             also.append({"workload": "hh3d_128x128x128 (weak)",
                          "error": f"{type(ex).__name__}: {ex}"})
+        # strong scaling of config 4's grid at the TTP state width (19
+        # fields, the SYNTHETIC width stand-in; rho of the HH state of the
+        # same grid, the plan is the same): per-N values next to the N = 1
+        # line's also entry give E(N) at 304 B/node
+        if w.name == "hh3d_512x512x256":
+            try:
+                w19 = workloads.get("hh3d_512x512x256_w19")
+                k19 = max(5, min(args.steps, 40))
+                ms19, rec19, _, slab19, _, _ = _timed(ctx, w19, local, args.warmup, k19,
+                                                      rho=rho)
+                slab19.op.close()
+                del slab19
+                k19 = rec19["timed_steps"]
+                v19 = w19.n_nodes * k19 / (ms19 * 1e-3)
+                also.append({"workload": w19.name, "scaling": "strong", "n_gpus": ctx.world,
+                             "value": v19, "unit": "node-steps/s", "steps": k19,
+                             "ms_per_step": ms19 / k19, "s": rec19["s"], "m": rec19["m"],
+                             "state_fields": 19,
+                             "step_frac_per_gpu": 304 * v19 / ctx.world / 1e9 / peak,
+                             "note": w19.note})
+            except Exception as ex:
+                also.append({"workload": "hh3d_512x512x256_w19 (strong)",
+                             "error": f"{type(ex).__name__}: {ex}"})
     if ctx.rank == 0:
         gbs = 64 * value / 1e9 / ctx.world
         cfg = config_of(w, ctx.world)
