@@ -1226,7 +1226,9 @@ __device__ __forceinline__ void tma_vplane(const Geom& g, const CUtensorMap* vma
   (void)has_hi;
 }
 
-template <int DIM, int FIRST, int ION>
+// AUX = 0 compiles the aux rows out (HH proper: constant ring strides, no
+// per-plane aux loop); AUX = 1 is the synthetic width stand-in (g.naux > 0).
+template <int DIM, int FIRST, int ION, int AUX>
 __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
     k_node_tma(const Geom g, const Halo h, const FastArgs a, const __grid_constant__ TmaNode tm) {
   using T = PipeTile<DIM>;
@@ -1236,7 +1238,8 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
   double* vst = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;  // [kRV][VS]
   // gate stage: the three gates and the aux fields of the synthetic width
   // stand-in (g.naux, include/emrkc.h), fields 1 .. nf - 1 of g_{j-1}
-  const int GF = 3 + g.naux, QF = 4 + g.naux;
+  const int NA = AUX ? g.naux : 0;
+  const int GF = 3 + NA, QF = 4 + NA;
   double* gst = vst + kRV * VS;                     // [kRG][GF][NT]
   constexpr int RG = kRGn<FIRST>();
   double* g2s = gst + RG * GF * T::NT;              // [kRG][QF][NT]
@@ -1393,7 +1396,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
       finacc = min(finacc, ~(unsigned)__double2hiint((r.o0 + r.o1) + (r.o2 + r.o3)) & 0x7ff00000u);
       // aux rows: y_E = z (no exponential part), f_S = g_S(V, z), the inner
       // iterate z + c_m eta g_S, g_j = base + (mu_j dt c_m) g_S
-      for (int q = 0; q < g.naux; ++q) {
+      for (int q = 0; q < NA; ++q) {
         const double za = G0[(3 + q) * T::NT];
         const double base = FIRST ? za : fma(a.nu, za, a.kappa * Q0[(4 + q) * T::NT]);
         const double oa = fma(a.cA, aux_rate_fast(q, vc, za), base);
@@ -1447,7 +1450,7 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
         guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
       }
       bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
-      for (int q = 0; q < g.naux; ++q) {
+      for (int q = 0; q < NA; ++q) {
         const double za = __ldg(G + (4 + q) * nn + i);
         const double base = FIRST ? za : fma(a.nu, za, a.kappa * __ldg(a.g2 + (4 + q) * nn + i));
         const double oa = fma(a.cA, aux_rate_fast(q, vc, za), base);
@@ -2903,21 +2906,28 @@ cudaError_t launch_node_persist(const Geom& g, const Halo& h, const FastArgs& a,
 }
 #endif
 
-template <int D, int F, int I>
-static cudaError_t launch_node_tma_t(const Geom& g, const Halo& h, const FastArgs& a,
+template <int D, int F, int I, int AUX>
+static cudaError_t launch_node_tma_a(const Geom& g, const Halo& h, const FastArgs& a,
                                      const TmaNode& tm, cudaStream_t st) {
   using T = PipeTile<D>;
   const size_t smem = tma_node_smem_bytes<D, F>(g.naux);
   static size_t attr = 0;
   if (smem > attr) {
-    cudaFuncSetAttribute(k_node_tma<D, F, I>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_node_tma<D, F, I, AUX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = smem;
   }
   const int chunks = (a.z_hi - a.z_lo + a.zc - 1) / a.zc;
   const dim3 grd = D == 3 ? dim3((g.n0 + T::TX - 1) / T::TX, (g.n1 + T::TY - 1) / T::TY, chunks)
                           : dim3((g.n0 + T::TX - 1) / T::TX, chunks, 1);
-  return launch_k(k_node_tma<D, F, I>, grd, dim3(T::NT), smem, st, g, h, a, tm);
+  return launch_k(k_node_tma<D, F, I, AUX>, grd, dim3(T::NT), smem, st, g, h, a, tm);
+}
+
+template <int D, int F, int I>
+static cudaError_t launch_node_tma_t(const Geom& g, const Halo& h, const FastArgs& a,
+                                     const TmaNode& tm, cudaStream_t st) {
+  return g.naux > 0 ? launch_node_tma_a<D, F, I, 1>(g, h, a, tm, st)
+                    : launch_node_tma_a<D, F, I, 0>(g, h, a, tm, st);
 }
 
 template <int K, int F>
