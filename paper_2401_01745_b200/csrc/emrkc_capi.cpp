@@ -971,7 +971,13 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       // stages 2..m in one pass at k == 2; levels k > 2 launch nothing
       if (k == 2) {
         emrkc_k::TbArgs f{};
-        f.coef = h->d_coef;
+        for (int kk = 0; kk <= pl.m; ++kk) {
+          f.mueta[kk] = pl.in_mueta[kk];
+          f.nu[kk] = pl.inner.nu[kk];
+          f.kappa[kk] = pl.inner.kappa[kk];
+        }
+        f.g1v = a.g1;
+        f.g2v = a.g2;
         f.outv = a.out;
         f.inv_mue1 = 1.0 / pl.in_mueta[1];
         f.onu = a.nu;
@@ -981,16 +987,14 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         f.m = pl.m;
         f.s = pl.s;
         f.last = a.last;
-        f.zc = h->zc;
+        const int K = pl.m - 1;
+        f.zc = emrkc_k::tb_zc(h->geom, K);
         f.code_base = a.code_base;
         f.event = a.event;
-        const int K = pl.m - 1;
         emrkc_k::TmaTb tm;
         std::memset(&tm, 0, sizeof tm);
         const cuuint32_t bx = emrkc_k::kTbTX + 2 * emrkc_k::kTbHX, by = emrkc_k::kTbTY + 2 * K;
         int rc = tma_map_box3(h, h->u[3], bx, by, 100 + K, &tm.d1);
-        if (!rc) rc = tma_map_box3(h, a.g1, emrkc_k::kTbTX, emrkc_k::kTbTY, 99, &tm.g1v);
-        if (!rc && a.g2) rc = tma_map_box3(h, a.g2, emrkc_k::kTbTX, emrkc_k::kTbTY, 99, &tm.g2v);
         // slabs: this handle's d_1 ghosts (K planes per face with a neighbour)
         Halo ht = hl;
         ht.lo = ht.hi = nullptr;

@@ -233,9 +233,11 @@ cudaError_t launch_fused2(const Geom& g, const FusedArgs& a, const TmaFused& tm,
 // handles). Stage k is computed on the tile plus a halo of K + 1 - k cells
 // (recomputed), so only d_1 (halo K), V of g_{j-1} / g_{j-2} and V of g_j
 // touch HBM.
-constexpr int kTbMaxK = 4, kTbTX = 32, kTbTY = 8, kTbHX = 4;
+constexpr int kTbMaxK = 4, kTbTX = 32, kTbTY = 16, kTbHX = 4;
 struct TbArgs {
-  const double* coef;  // device: in_mueta[0..m] | in_nu[0..m] | in_kappa[0..m]
+  double mueta[kTbMaxK + 2], nu[kTbMaxK + 2], kappa[kTbMaxK + 2];  // mu'_k eta, nu'_k, kappa'_k (k = 0..m)
+  const double* g1v;   // V block of g_{j-1}
+  const double* g2v;   // V block of g_{j-2} (j >= 2)
   double* outv;        // V block of g_j
   double inv_mue1;     // 1 / (mu'_1 eta)
   double onu, okappa, cG;  // outer nu_j, kappa_j, mu_j dt / eta
@@ -245,8 +247,6 @@ struct TbArgs {
 };
 struct TmaTb {
   CUtensorMap d1;      // d_1, box (kTbTX + 2 kTbHX, kTbTY + 2K, 1)
-  CUtensorMap g1v;     // V of g_{j-1}, box (kTbTX, kTbTY, 1)
-  CUtensorMap g2v;     // V of g_{j-2}
   CUtensorMap d1lo;    // slabs: K ghost planes of d_1 below (global z0 - K ..), box as d1
   CUtensorMap d1hi;    // K ghost planes above (global z1 ..)
 };
@@ -257,6 +257,7 @@ struct TmaTb {
 cudaError_t launch_vin_tb(const Geom& g, const Halo& h, const TbArgs& a, const TmaTb& tm,
                           cudaStream_t st);
 long long halo_signals_tb(const Geom& g);
+int tb_zc(const Geom& g, int K);  // wave-aware z-chunk of a k_vin_tb launch
 
 // TMA descriptors of one k_node_tma launch (host-encoded, passed as a
 // __grid_constant__ parameter). Boxes: V tile + 1-cell halo, gate fields,

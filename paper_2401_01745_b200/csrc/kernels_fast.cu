@@ -2070,46 +2070,64 @@ __global__ void __launch_bounds__(128)
 // k_vin_tb<K, FIRST>: inner stages k = 2 .. K+1 (= m) of outer stage j in one
 // pass over HBM (temporal blocking of the V-only inner iteration).
 //
-// A block owns a 32 x 8 tile and a z-chunk [zb, ze) of the final stage. It
-// marches planes t; at step t it receives d_1 of plane t (TMA, box with an
-// x halo of 4 and a y halo of K) and computes stage k at plane t - (k - 1)
-// for k = 2 .. K+1 on the tile grown by K + 1 - k cells, so stage k + 1 finds
-// the neighbours it needs; each stage keeps its last three planes in shared
-// memory. Stage K + 1 forms V of g_j = base + (mu_j dt / eta) d_m directly
-// (centres of V of g_{j-1}, g_{j-2} arrive with the plane group). Only d_1
+// A block owns a 32 x 16 tile and a z-chunk [zb, ze) of the final stage and
+// marches planes s. Its threads own the columns of the stage-2 region (the
+// tile grown by K - 1 cells, x range widened to even cells), an x-adjacent
+// PAIR of columns per thread, for the whole march. At step s
+//   * d_1 of plane s arrives by TMA (box with an x halo of 4 and a y halo of
+//     K, a 4-plane ring, two planes of look-ahead);
+//   * stage k computes plane s - (k - 1); columns less than k - 2 cells
+//     inside the region compute values nobody reads (no per-cell tests);
+//   * the z neighbours and the centre of a column are the thread's own
+//     values of the previous stage: each column keeps the last K + 1 planes
+//     of d_1 and the last three planes of stages 2..K in registers, so a
+//     stage reads only in-plane neighbours from shared memory — per pair two
+//     128-bit loads (y - 1, y + 1) and two 64-bit loads (x - 1 of the left
+//     cell, x + 1 of the right cell; the inner x neighbours are the pair's
+//     own registers);
+//   * stage k < m publishes its pair with one 128-bit store into a
+//     double-buffered shared plane; stage k + 1 reads the plane published
+//     one step earlier, so ONE __syncthreads per step orders every stage.
+// The march is unrolled by the ring size: ring slot and buffer parity are
+// compile-time constants and every shared access is [thread register +
+// immediate]. Steps at the chunk ends (a stage outside its plane range, a z
+// mirror, no d_1 plane left) take the EDGE instance with the tests.
+// Stage K + 1 forms V of g_j = base + (mu_j dt / eta) d_m directly (V of
+// g_{j-1}, g_{j-2} by 128-bit loads at the start of the step). Only d_1
 // (plus its halo), V of g_{j-1}, g_{j-2} and V of g_j touch HBM: 24-32 B per
 // node for all m - 1 stages instead of 16 + 32 (m - 3) + 40.
-// Neumann mirror: every stencil read maps index -1 -> 1 and n -> n - 2
-// (P/src/monodomain.cpp:85-86), in x, y and z; cells outside the grid are
-// never read. Recurrences exactly as k_vin_tma (increment form).
+// Neumann mirror (P/src/monodomain.cpp:85-86): in x and y the per-thread
+// neighbour addresses point at the mirrored cell; in z the column window is
+// patched when a stage reaches plane 0 or nz - 1. Cells outside the grid
+// hold values nobody reads. Recurrences exactly as k_vin_tma (increment
+// form, same operation order: bitwise equal, tests/test_gpu_tb.py).
 // ---------------------------------------------------------------------------
+constexpr int kTbRD = 4, kTbLA = 2;  // d_1 ring planes, look-ahead (RD >= LA + 2)
 template <int K>
 struct TbTile {
-  static constexpr int TX = kTbTX, TY = kTbTY, NT = 256;
-  static constexpr int DX = TX + 2 * kTbHX;           // d_1 box width
-  static constexpr int DY = TY + 2 * K;               // d_1 box height
-  static constexpr int DS = ((DX * DY) + 15) & ~15;   // d_1 stage stride
-  static constexpr int RD = 8;                        // d_1 ring (>= K + 1 + look-ahead)
-  static constexpr int CS = TX * TY;                  // centre plane
-  __host__ __device__ static constexpr int h(int k) { return K + 1 - k; } // halo of stage k
-  __host__ __device__ static constexpr int PX(int k) { return TX + 2 * h(k); }
-  __host__ __device__ static constexpr int PY(int k) { return TY + 2 * h(k); }
-  __host__ __device__ static constexpr int PS(int k) { return PX(k) * PY(k); }
-  // offsets (doubles) of the stage rings k = 2..K (3 planes each), then centres
-  __host__ __device__ static constexpr int off_stage(int k) {
-    int o = RD * DS;
-    for (int i = 2; i < k; ++i) o += 3 * PS(i);
-    return o;
+  static constexpr int TX = kTbTX, TY = kTbTY;
+  static constexpr int BX = TX + 2 * kTbHX, BY = TY + 2 * K;  // d_1 box
+  static constexpr int PS = BX * BY;
+  static constexpr int PSS = (PS + 15) & ~15;                 // plane stride (128 B)
+  static constexpr int HK = (K - 1 + 1) & ~1;                 // x halo of the region (even)
+  static constexpr int PR = (TX + 2 * HK) / 2;                // column pairs per row
+  static constexpr int RY = TY + 2 * (K - 1);                 // region rows
+  static constexpr int NC = PR * RY;                          // threads owning pairs
+  static constexpr int NT = (NC + 31) & ~31;
+  // shared planes: d_1 ring, then two planes per published stage 2..K
+  __host__ __device__ static constexpr int ring_off(int slot) { return 8 * slot * PSS; }
+  __host__ __device__ static constexpr int stage_off(int k, int par) {
+    return 8 * (kTbRD + 2 * (k - 2) + par) * PSS;
   }
-  __host__ __device__ static constexpr int off_centre() { return (off_stage(K + 1) + 15) & ~15; }
-  __host__ __device__ static constexpr int total() { return off_centre() + 4 * 2 * CS; }
+  __host__ __device__ static constexpr int total() { return (kTbRD + 2 * (K - 1)) * PSS; }
 };
-// d_1 ring: planes s - K .. s + look-ahead in 8 slots; centre ring: 4 slots
-// hold steps s .. s + look-ahead
-static_assert(kTbMaxK + 1 + kTmaLA <= 8 && kTmaLA + 1 <= 4, "k_vin_tb rings");
+static_assert(kTbRD == 4 && kTbRD >= kTbLA + 2, "k_vin_tb d_1 ring (march unrolled by 4)");
+static_assert(kTbTY % 2 == 0 && kTbHX >= kTbMaxK && kTbHX % 2 == 0, "k_vin_tb tile");
 
 template <int K>
 constexpr size_t tb_smem_bytes() { return sizeof(double) * TbTile<K>::total() + 128; }
+template <int K>
+constexpr int tb_min_blocks() { return K == 2 ? 3 : (K == 3 ? 2 : 1); }
 
 // Compile-time loop: f(integral_constant<int, i>) for i in [B, E).
 template <int B, int E, typename F>
@@ -2120,16 +2138,172 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
+// Shared-memory accesses at [register + immediate] (OFF >= 0) or, in the EDGE
+// instance, [register + run-time offset] (the compiler cannot reorder them
+// across the step barrier: volatile + memory clobber).
+template <int OFF>
+__device__ __forceinline__ void lds2(unsigned a, int off, double& x, double& y) {
+  if constexpr (OFF >= 0)
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(x), "=d"(y) : "r"(a), "n"(OFF) : "memory");
+  else
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a + off) : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ double lds1(unsigned a, int off) {
+  double x;
+  if constexpr (OFF >= 0)
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(x) : "r"(a), "n"(OFF) : "memory");
+  else
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a + off) : "memory");
+  return x;
+}
+template <int OFF>
+__device__ __forceinline__ void sts2(unsigned a, int off, double x, double y) {
+  if constexpr (OFF >= 0)
+    asm volatile("st.shared.v2.f64 [%0+%1], {%2, %3};" ::"r"(a), "n"(OFF), "d"(x), "d"(y) : "memory");
+  else
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a + off), "d"(x), "d"(y) : "memory");
+}
+// all-ones accumulator of non-finite high words: max over (hi & sel) | 0x800fffff
+__device__ __forceinline__ unsigned nf_acc(unsigned acc, double v, unsigned sel) {
+  return max(acc, ((unsigned)__double2hiint(v) & sel) | 0x800fffffu);
+}
+
+// Per-thread constants and march state of k_vin_tb.
+struct TbCtx {
+  unsigned aC, aXm, aXp, aYm, aYp;  // shared byte addresses in plane 0
+  unsigned b0, sel;
+  bool own, gl, gh;
+  int zb, ze, nz, lo1, hi1;
+  long long plane;
+  double inv_mue1;
+};
+template <int K>
+struct TbState {
+  // column windows: D[c][i] = d_1 at plane s - K + i; W[c][k - 2][i] = stage k
+  // at plane (s - k + 1) - 2 + i, k = 2..K
+  double D[2][K + 1], W[2][K > 1 ? K - 1 : 1][3];
+  unsigned acc[K + 2];  // per stage: all ones once an owned value was non-finite
+  unsigned acc_o;
+  bool guard;
+  long long go;         // final-stage output offset of the step
+};
+
+// One march step at ring phase (s - lo1) & 3 (PH, compile time, when
+// !EDGE). EDGE = false is the steady state: every stage on a plane of the
+// chunk, no z mirror, d_1 of plane s exists.
+template <int K, int FIRST, bool EDGE, int PH>
+__device__ __forceinline__ void tb_step(const Geom& g, const Halo& h, const TbArgs& a,
+                                        const TbCtx& c, TbState<K>& st, const int s) {
+  using T = TbTile<K>;
+  constexpr int M = K + 1;
+  const int i = s - c.lo1;
+  const int ph = EDGE ? (i & 3) : PH;
+  // V of g_{j-1} / g_{j-2} for the final stage's plane, early
+  const int qo = s - K;
+  const bool outp = !EDGE || (qo >= c.zb && qo < c.ze);
+  double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
+  if (c.own && outp) {
+    v1 = __ldg(reinterpret_cast<const double2*>(a.g1v + st.go));
+    if (!FIRST) v2 = __ldg(reinterpret_cast<const double2*>(a.g2v + st.go));
+  }
+  const bool has_d = !EDGE || s < c.hi1;
+  if (has_d) mbar_wait(c.b0 + 8u * ph, (i >> 2) & 1);
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+    for (int q = 0; q < K; ++q) st.D[cc][q] = st.D[cc][q + 1];
+  if (has_d) lds2<EDGE ? -1 : T::ring_off(PH)>(c.aC, T::ring_off(1) * ph, st.D[0][K], st.D[1][K]);
+  static_for<2, M + 1>([&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    constexpr int hk = K + 1 - k;
+    const int q = s - (k - 1);
+    const bool active = !EDGE || (q >= (c.gl ? c.zb - hk : max(0, c.zb - hk)) &&
+                                  q < (c.gh ? c.ze + hk : min(c.nz, c.ze + hk)));
+    const bool mlo = EDGE && q < 1 && !c.gl, mhi = EDGE && q + 1 >= c.nz && !c.gh;
+    const bool own_plane = !EDGE || (q >= c.zb && q < c.ze);
+    const double mueta = a.mueta[k], nu = a.nu[k], kappa = a.kappa[k];
+    // in-plane neighbours: d_1 of plane s - 1 (k = 2) or the plane stage
+    // k - 1 published one step ago
+    constexpr int SRC = EDGE ? -1
+                             : (k == 2 ? T::ring_off((PH + 3) & 3)
+                                       : T::stage_off(k >= 3 ? k - 1 : 2, (PH & 1) ^ 1));
+    const int src = k == 2 ? T::ring_off(1) * ((ph + 3) & 3)
+                           : T::stage_off(k >= 3 ? k - 1 : 2, 0) + T::ring_off(1) * ((ph & 1) ^ 1);
+    double dk[2] = {0.0, 0.0};
+    if (active) {
+      double z0[2], z1[2], z2[2];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        if constexpr (k == 2) {
+          z0[cc] = st.D[cc][K - 2];
+          z1[cc] = st.D[cc][K - 1];
+          z2[cc] = st.D[cc][K];
+        } else {
+          z0[cc] = st.W[cc][k - 3][0];
+          z1[cc] = st.W[cc][k - 3][1];
+          z2[cc] = st.W[cc][k - 3][2];
+        }
+        if (mlo) z0[cc] = z2[cc];
+        if (mhi) z2[cc] = z0[cc];
+      }
+      double ym[2], yp[2];
+      lds2<SRC>(c.aYm, src, ym[0], ym[1]);
+      lds2<SRC>(c.aYp, src, yp[0], yp[1]);
+      const double xm0 = lds1<SRC>(c.aXm, src), xp1 = lds1<SRC>(c.aXp, src);
+      const double xs[2] = {xm0 + z1[1], z1[0] + xp1};
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const double vc = z1[cc];
+        double L = fma(g.wc, vc, g.w[2] * (z0[cc] + z2[cc]));
+        L = fma(g.w[0], xs[cc], L);
+        L = fma(g.w[1], ym[cc] + yp[cc], L);
+        const double d1c = st.D[cc][K - (k - 1)];
+        double bs = nu * vc;
+        if constexpr (k == 3) bs = fma(nu, vc, kappa * d1c);
+        if constexpr (k >= 4) bs = fma(nu, vc, kappa * st.W[cc][k >= 4 ? k - 4 : 0][0]);
+        dk[cc] = fma(mueta, fma(d1c, c.inv_mue1, L), bs);
+        if (own_plane) st.acc[k] = nf_acc(st.acc[k], dk[cc], c.sel);
+      }
+      if constexpr (k < M) {
+        sts2<EDGE ? -1 : T::stage_off(k < M ? k : 2, PH & 1)>(
+            c.aC, T::stage_off(k < M ? k : 2, 0) + T::ring_off(1) * (ph & 1), dk[0], dk[1]);
+      } else if (c.own && own_plane) {
+        // final stage: V of g_j
+        double2 o;
+        o.x = fma(a.cG, dk[0], FIRST ? v1.x : fma(a.onu, v1.x, a.okappa * v2.x));
+        o.y = fma(a.cG, dk[1], FIRST ? v1.y : fma(a.onu, v1.y, a.okappa * v2.y));
+        *reinterpret_cast<double2*>(a.outv + st.go) = o;
+        if (EDGE) {
+          if (q == 0 && h.put_lo) *reinterpret_cast<double2*>(h.put_lo + (st.go - c.plane * q)) = o;
+          if (q == c.nz - 1 && h.put_hi)
+            *reinterpret_cast<double2*>(h.put_hi + (st.go - c.plane * q)) = o;
+        }
+        st.acc_o = nf_acc(nf_acc(st.acc_o, o.x, 0xffffffffu), o.y, 0xffffffffu);
+        st.guard |= !(fabs(o.x) <= 1e6) || !(fabs(o.y) <= 1e6);  // also a non-finite V
+      }
+    }
+    if constexpr (k < M) {  // the stage's own windows move every step
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        st.W[cc][k < M ? k - 2 : 0][0] = st.W[cc][k < M ? k - 2 : 0][1];
+        st.W[cc][k < M ? k - 2 : 0][1] = st.W[cc][k < M ? k - 2 : 0][2];
+        st.W[cc][k < M ? k - 2 : 0][2] = dk[cc];
+      }
+    }
+  });
+  st.go += c.plane;
+}
 
 template <int K, int FIRST>
-__global__ void __launch_bounds__(TbTile<K>::NT, 2)
+__global__ void __launch_bounds__(TbTile<K>::NT, tb_min_blocks<K>())
     k_vin_tb(const Geom g, const Halo h, const TbArgs a, const __grid_constant__ TmaTb tm) {
   using T = TbTile<K>;
   constexpr int M = K + 1;  // m
+  constexpr int PSS = T::PSS, BX = T::BX;
   extern __shared__ __align__(128) double smem_tma[];
   double* sm = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;
-  __shared__ __align__(8) unsigned long long bars[8];
-  __shared__ double cf[3][kTbMaxK + 2];  // mu'_k eta, nu'_k, kappa'_k (k = 0..m)
+  __shared__ __align__(8) unsigned long long bars[kTbRD];
   __shared__ int skip;
   const int t = threadIdx.x;
   const int x0 = blockIdx.x * T::TX, y0 = blockIdx.y * T::TY;
@@ -2138,178 +2312,121 @@ __global__ void __launch_bounds__(TbTile<K>::NT, 2)
   const int n0 = g.n0, n1 = g.n1, nz = g.nzl;
   pdl_launch_dependents();
   if (t == 0) {
-    for (int s = 0; s < 8; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    for (int s = 0; s < kTbRD; ++s) mbar_init(smem_u32(&bars[s]), 1);
     mbar_fence_init();
     prefetch_tensormap(&tm.d1);
-    prefetch_tensormap(&tm.g1v);
-    if (!FIRST) prefetch_tensormap(&tm.g2v);
   }
   __syncthreads();
   pdl_wait();
-  if (t < 3 * (M + 1)) cf[t / (M + 1)][t % (M + 1)] = a.coef[t];
   // slab faces with a neighbour (h.lo / h.hi: its K d_1 ghost planes) march
   // into the ghosts; global boundaries mirror (P/src/monodomain.cpp:85-86)
   const bool gl = h.lo != nullptr, gh = h.hi != nullptr;
   const int lo1 = max(gl ? -K : 0, zb - K), hi1 = min(gh ? nz + K : nz, ze + K);  // d_1 planes
   const int tlast = ze - 1 + K;                           // last step
-  const unsigned b0 = smem_u32(bars);
-  const unsigned dbase = smem_u32(sm), cbase = smem_u32(sm + T::off_centre());
-  auto issue = [&](int s) {  // thread 0: load group of step s
+  const unsigned b0 = smem_u32(bars), dbase = smem_u32(sm);
+  auto issue = [&](int s) {  // thread 0: d_1 of plane s in [lo1, hi1)
     const int i = s - lo1;
-    const unsigned bar = b0 + 8u * (i & 7);
-    const int q = s - K;
-    const bool hasd = s < hi1;
-    const bool hasc = q >= zb && q < ze;
-    const unsigned bytes = (hasd ? 8u * T::DX * T::DY : 0u) +
-                           (hasc ? 8u * T::CS * (FIRST ? 1 : 2) : 0u);
-    mbar_expect_tx(bar, bytes);
-    if (hasd) {
-      const unsigned dd = dbase + 8u * T::DS * (i & 7);
-      if (s < 0) tma_load_3d(dd, &tm.d1lo, bar, x0 - kTbHX, y0 - K, s + K);
-      else if (s >= nz) tma_load_3d(dd, &tm.d1hi, bar, x0 - kTbHX, y0 - K, s - nz);
-      else tma_load_3d(dd, &tm.d1, bar, x0 - kTbHX, y0 - K, s);
-    }
-    if (hasc) {
-      const unsigned cd = cbase + 8u * 2 * T::CS * (s & 3);
-      tma_load_3d(cd, &tm.g1v, bar, x0, y0, q);
-      if (!FIRST) tma_load_3d(cd + 8u * T::CS, &tm.g2v, bar, x0, y0, q);
-    }
+    const unsigned bar = b0 + 8u * (i & (kTbRD - 1));
+    mbar_expect_tx(bar, 8u * T::PS);
+    const unsigned dd = dbase + 8u * PSS * (i & (kTbRD - 1));
+    if (s < 0) tma_load_3d(dd, &tm.d1lo, bar, x0 - kTbHX, y0 - K, s + K);
+    else if (s >= nz) tma_load_3d(dd, &tm.d1hi, bar, x0 - kTbHX, y0 - K, s - nz);
+    else tma_load_3d(dd, &tm.d1, bar, x0 - kTbHX, y0 - K, s);
   };
+  const int npro = min(kTbLA, hi1 - lo1);
   if (t == 0) {
     if (lo1 < 0 || hi1 > nz) {
       halo_wait(h, lo1 < 0, hi1 > nz);
       fence_proxy_async();  // peer-stored ghosts before the async-proxy reads
     }
-    for (int s = lo1; s <= min(tlast, lo1 + kTmaLA - 1); ++s) issue(s);
+    for (int i = 0; i < npro; ++i) issue(lo1 + i);
     skip = (*(volatile const unsigned long long*)a.event) < level_floor(a.code_base, a.j, a.m, 2);
   }
   __syncthreads();
-  const int nlaunched = min(tlast, lo1 + kTmaLA - 1) - lo1 + 1;
   if (skip) {
-    for (int i = 0; i < nlaunched; ++i) mbar_wait(b0 + 8u * i, 0);
+    for (int i = 0; i < npro; ++i) mbar_wait(b0 + 8u * i, 0);
     halo_signal(h, zb == 0, ze >= nz);  // release the neighbours
     return;
   }
-  // ring slot of a stage plane (q >= -K - 1 on slabs)
-  auto r3 = [](int q) { return (q + 6) % 3; };
-  const double inv_mue1 = a.inv_mue1;
-  const long long plane = g.plane;
-  unsigned badk = 0u;  // bit k: stage k produced a non-finite interior value
-  bool bad_out = false, guard = false;
-  // Per-thread cells of every stage, fixed for the whole z-march: stage k's
-  // region cells t, t + 256, ... with their source / d_1 offsets, mirrored
-  // neighbour deltas (signed bytes: xm, xp, ym, yp), validity and ownership.
-  constexpr int NT = T::NT;
-  constexpr int NTOT = [] {
-    int n = 0;
-    for (int kk = 2; kk <= M; ++kk) n += (T::PS(kk) + NT - 1) / NT;
-    return n;
-  }();
-  int c_si[NTOT], c_d1[NTOT], c_dl[NTOT], c_out[NTOT], c_s2[NTOT];
-  unsigned c_f[NTOT];  // bit 0 valid, bit 1 own (tile interior)
-  static_for<2, M + 1>([&](auto kc) {
-    constexpr int kk = decltype(kc)::value;
-    constexpr int hk = T::h(kk), PXk = T::PX(kk);
-    constexpr int P = kk == 2 ? T::DX : T::PX(kk - 1);
-    constexpr int base = [] {
-      int b = 0;
-      for (int k2 = 2; k2 < kk; ++k2) b += (T::PS(k2) + NT - 1) / NT;
-      return b;
-    }();
+  // The thread's pair of columns (cells 0 and 1, x-adjacent, even x first):
+  // shared byte addresses of the pair and of its mirrored in-plane
+  // neighbours inside plane 0 (a plane's offset is an immediate), ownership
+  // (the pair lies in the tile and the grid) and the output offset. Threads
+  // past the last pair repeat an earlier pair (identical values, no outputs).
+  const int tt = t < T::NC ? t : t - T::NC;
+  const int px = tt % T::PR, cy = tt / T::PR;
+  const int gx = x0 - T::HK + 2 * px, gy = y0 - (K - 1) + cy;
+  const int ci = (cy + 1) * BX + (kTbHX - T::HK) + 2 * px;  // cell 0 in the box
+  TbCtx c;
+  c.own = t < T::NC && gx >= x0 && gx < min(x0 + T::TX, n0) && gy >= y0 &&
+          gy < min(y0 + T::TY, n1);
+  c.sel = c.own ? 0xffffffffu : 0u;
+  c.aC = dbase + 8u * ci;
+  // x - 1 of cell 0 (mirror at x = 0; box column 0 has no left cell: any value)
+  c.aXm = c.aC + ((gx > 0 && kTbHX - T::HK + 2 * px > 0) ? -8 : 8);
+  c.aXp = c.aC + 8u + (gx + 1 < n0 - 1 ? 8 : -8);  // x + 1 of cell 1
+  c.aYm = c.aC + (gy > 0 ? -8 * BX : 8 * BX);
+  c.aYp = c.aC + (gy < n1 - 1 ? 8 * BX : -8 * BX);
+  c.b0 = b0;
+  c.gl = gl;
+  c.gh = gh;
+  c.zb = zb;
+  c.ze = ze;
+  c.nz = nz;
+  c.lo1 = lo1;
+  c.hi1 = hi1;
+  c.plane = g.plane;
+  c.inv_mue1 = a.inv_mue1;
+  TbState<K> st;
+  st.go = (long long)gx + (long long)n0 * gy + g.plane * (lo1 - K);
 #pragma unroll
-    for (int i = 0; i < (T::PS(kk) + NT - 1) / NT; ++i) {
-      const int c = t + i * NT;
-      const int cy = c / PXk, cx = c - cy * PXk;
-      const int gx = x0 - hk + cx, gy = y0 - hk + cy;
-      const bool valid = c < T::PS(kk) && gx >= 0 && gx < n0 && gy >= 0 && gy < n1;
-      const bool own = cx >= hk && cx < hk + T::TX && cy >= hk && cy < hk + T::TY;
-      const int dxm = gx > 0 ? -1 : 1, dxp = gx < n0 - 1 ? 1 : -1;
-      const int dym = gy > 0 ? -P : P, dyp = gy < n1 - 1 ? P : -P;
-      c_si[base + i] = kk == 2 ? (cy + K - hk) * T::DX + (cx + kTbHX - hk) : (cy + 1) * P + (cx + 1);
-      c_d1[base + i] = (cy + K - hk) * T::DX + (cx + kTbHX - hk);
-      c_dl[base + i] = (dxm & 0xff) | ((dxp & 0xff) << 8) | ((dym & 0xff) << 16) |
-                       ((dyp & 0xff) << 24);
-      c_out[base + i] = gx + n0 * gy;                                    // final stage
-      c_s2[base + i] = kk >= 4 ? (cy + 2) * T::PX(kk - 2) + (cx + 2) : 0;  // d_{k-2}
-      c_f[base + i] = (valid ? 1u : 0u) | (own ? 2u : 0u);
-    }
-  });
-  for (int s = lo1; s <= tlast; ++s) {
-    if (t == 0 && s + kTmaLA <= tlast) issue(s + kTmaLA);
-    const int i = s - lo1;
-    mbar_wait(b0 + 8u * (i & 7), (i >> 3) & 1);
-    static_for<2, M + 1>([&](auto kc) {
-      constexpr int k = decltype(kc)::value;
-      const int q = s - (k - 1);
-      constexpr int hk = T::h(k);
-      constexpr int base = [] {
-        int b = 0;
-        for (int k2 = 2; k2 < k; ++k2) b += (T::PS(k2) + NT - 1) / NT;
-        return b;
-      }();
-      const bool active = q >= (gl ? zb - hk : max(0, zb - hk)) &&
-                          q < (gh ? ze + hk : min(nz, ze + hk));
-      if (active) {
-        const int qm = (q < 1 && !gl) ? 1 : q - 1;
-        const int qp = (q + 1 >= nz && !gh) ? nz - 2 : q + 1;
-        const double mueta = cf[0][k], nu = cf[1][k], kappa = cf[2][k];
-        const double* Sc;
-        const double* Sm;
-        const double* Sp;
-        if (k == 2) {
-          Sc = sm + ((q - lo1) & 7) * T::DS;
-          Sm = sm + ((qm - lo1) & 7) * T::DS;
-          Sp = sm + ((qp - lo1) & 7) * T::DS;
-        } else {
-          const double* S = sm + T::off_stage(k - 1);
-          Sc = S + r3(q) * T::PS(k - 1);
-          Sm = S + r3(qm) * T::PS(k - 1);
-          Sp = S + r3(qp) * T::PS(k - 1);
-        }
-        const double* D1 = sm + ((q - lo1) & 7) * T::DS;
-        const double* S2 = k >= 4 ? sm + T::off_stage(k - 2) + r3(q) * T::PS(k - 2) : nullptr;
-        const bool own_plane = q >= zb && q < ze;
+  for (int k = 0; k <= M; ++k) st.acc[k] = 0u;
+  st.acc_o = 0u;
+  st.guard = false;
 #pragma unroll
-        for (int ii = 0; ii < (T::PS(k) + NT - 1) / NT; ++ii) {
-          const int e = base + ii;
-          if (!(c_f[e] & 1u)) continue;
-          const int si = c_si[e], dl = c_dl[e];
-          const int dxm = (int)(signed char)(dl & 0xff), dxp = (int)(signed char)((dl >> 8) & 0xff);
-          const int dym = (int)(signed char)((dl >> 16) & 0xff), dyp = dl >> 24;
-          const double vc = Sc[si];
-          double D = fma(g.wc, vc, g.w[2] * (Sm[si] + Sp[si]));
-          D = fma(g.w[0], Sc[si + dxm] + Sc[si + dxp], D);
-          D = fma(g.w[1], Sc[si + dym] + Sc[si + dyp], D);
-          const double d1c = D1[c_d1[e]];
-          double bs = nu * vc;
-          if (k == 3) bs = fma(nu, vc, kappa * d1c);
-          if (k >= 4) bs = fma(nu, vc, kappa * S2[c_s2[e]]);
-          const double dk = fma(mueta, fma(d1c, inv_mue1, D), bs);
-          if ((c_f[e] & 2u) && own_plane && !finite_hi(dk)) badk |= 1u << k;
-          if (k < M) {
-            sm[T::off_stage(k) + r3(q) * T::PS(k) + t + ii * NT] = dk;
-          } else {
-            // final stage: V of g_j (hk == 0: the cell indexes the tile)
-            const int c = t + ii * NT;
-            const double* C0 = sm + T::off_centre() + (s & 3) * 2 * T::CS;
-            const double bb = FIRST ? C0[c] : fma(a.onu, C0[c], a.okappa * C0[T::CS + c]);
-            const double o0 = fma(a.cG, dk, bb);
-            a.outv[(long long)c_out[e] + plane * q] = o0;
-            if (q == 0 && h.put_lo) h.put_lo[c_out[e]] = o0;
-            if (q == nz - 1 && h.put_hi) h.put_hi[c_out[e]] = o0;
-            bad_out |= !finite_hi(o0);
-            guard |= !(fabs(o0) <= 1e6);  // also a non-finite V
-          }
-        }
-      }
-      __syncthreads();
-    });
+  for (int cc = 0; cc < 2; ++cc) {
+#pragma unroll
+    for (int q = 0; q <= K; ++q) st.D[cc][q] = 0.0;
+#pragma unroll
+    for (int k = 0; k < K - 1; ++k) st.W[cc][k][0] = st.W[cc][k][1] = st.W[cc][k][2] = 0.0;
+  }
+  // steady steps: every stage's plane s - k + 1 lies in [max(zb, 1), min(ze, nz - 1))
+  const int st0 = max(zb, 1) + K, st1 = min(ze, nz - 1);
+  int s = lo1;
+  // edge steps up to the first steady step at ring phase 0
+  for (; s <= tlast && (s < st0 || ((s - lo1) & 3) != 0); ++s) {
+    if (t == 0 && s + kTbLA < hi1) issue(s + kTbLA);
+    tb_step<K, FIRST, true, 0>(g, h, a, c, st, s);
+    __syncthreads();
+  }
+  for (; s + 3 <= st1; s += 4) {
+    if (t == 0 && s + kTbLA < hi1) issue(s + kTbLA);
+    tb_step<K, FIRST, false, 0>(g, h, a, c, st, s);
+    __syncthreads();
+    if (t == 0 && s + 1 + kTbLA < hi1) issue(s + 1 + kTbLA);
+    tb_step<K, FIRST, false, 1>(g, h, a, c, st, s + 1);
+    __syncthreads();
+    if (t == 0 && s + 2 + kTbLA < hi1) issue(s + 2 + kTbLA);
+    tb_step<K, FIRST, false, 2>(g, h, a, c, st, s + 2);
+    __syncthreads();
+    if (t == 0 && s + 3 + kTbLA < hi1) issue(s + 3 + kTbLA);
+    tb_step<K, FIRST, false, 3>(g, h, a, c, st, s + 3);
+    __syncthreads();
+  }
+  for (; s <= tlast; ++s) {
+    if (t == 0 && s + kTbLA < hi1) issue(s + kTbLA);
+    tb_step<K, FIRST, true, 0>(g, h, a, c, st, s);
+    __syncthreads();
   }
   halo_signal(h, zb == 0, ze >= nz);
   const unsigned long long base = a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1));
+  unsigned badk = 0u;
+#pragma unroll
+  for (int k = 2; k <= M; ++k)
+    if (st.acc[k] == 0xffffffffu) badk |= 1u << k;
   if (badk) atomicMin(a.event, base + (unsigned long long)(__ffs(badk) - 1));
-  if (bad_out) atomicMin(a.event, base + a.m + 1);
-  if (a.last && guard)
+  if (st.acc_o == 0xffffffffu) atomicMin(a.event, base + a.m + 1);
+  if (a.last && st.guard)
     atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
 }
 
@@ -2910,7 +3027,14 @@ template <int D, int F, int I, int AUX>
 static cudaError_t launch_node_tma_a(const Geom& g, const Halo& h, const FastArgs& a,
                                      const TmaNode& tm, cudaStream_t st) {
   using T = PipeTile<D>;
-  const size_t smem = tma_node_smem_bytes<D, F>(g.naux);
+  // EMRKC_NODE_PAD: extra dynamic shared memory per block (caps the resident
+  // node blocks per SM so that inner-stage blocks of the z-pipelined step
+  // fit beside them; experiments only)
+  static const size_t pad = [] {
+    const char* e = std::getenv("EMRKC_NODE_PAD");
+    return e && *e ? (size_t)std::max(0, std::atoi(e)) : (size_t)0;
+  }();
+  const size_t smem = tma_node_smem_bytes<D, F>(g.naux) + pad;
   static size_t attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(k_node_tma<D, F, I, AUX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2953,6 +3077,48 @@ cudaError_t launch_vin_tb(const Geom& g, const Halo& h, const TbArgs& a, const T
     case 4: return first ? launch_vin_tb_t<4, 1>(g, h, a, tm, st) : launch_vin_tb_t<4, 0>(g, h, a, tm, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// z-chunk of a k_vin_tb launch: a block marches zc + 2K planes (plus a
+// prologue worth ~6) for zc planes of output, and the grid runs in waves of
+// (resident blocks per SM) x SMs; pick the chunk count whose waves x march
+// length is smallest (chunks of >= 8 planes).
+template <int K>
+static int tb_slots() {
+  static int slots = -1;
+  if (slots < 0) {
+    int nb = 0, sms = 0, dev = 0;
+    cudaFuncSetAttribute(k_vin_tb<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tb_smem_bytes<K>());
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_vin_tb<K, 1>, TbTile<K>::NT,
+                                                      tb_smem_bytes<K>()) != cudaSuccess ||
+        cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      nb = 0;
+    cudaGetLastError();
+    slots = nb > 0 && sms > 0 ? nb * sms : 148 * tb_min_blocks<K>();
+  }
+  return slots;
+}
+
+int tb_zc(const Geom& g, int K) {
+  const int slots = K == 2 ? tb_slots<2>() : (K == 3 ? tb_slots<3>() : tb_slots<4>());
+  const long long tiles = halo_signals_tb(g);
+  const int nz = g.nzl;
+  int best_zc = nz;
+  long long best = -1;
+  for (int chunks = 1; chunks <= nz; ++chunks) {
+    const int zc = (nz + chunks - 1) / chunks;
+    if (zc < 8 && chunks > 1) break;
+    const int real = (nz + zc - 1) / zc;
+    const long long waves = (tiles * real + slots - 1) / slots;
+    const long long cost = waves * (zc + 2 * K + 6);
+    if (best < 0 || cost < best) {
+      best = cost;
+      best_zc = zc;
+    }
+  }
+  return best_zc;
 }
 
 long long halo_signals_tb(const Geom& g) {
