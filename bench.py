@@ -113,10 +113,10 @@ def kernel_name(kind: str, problem) -> str:
 
 def tb_active(problem, m: int) -> bool:
     """k_vin_tb runs stages 2..m (emrkc_capi.cpp use_tb): 3-D whole grid on
-    the TMA path, 2 <= m - 1 <= 4, EMRKC_TB=1 (off by default)."""
+    the TMA path, 2 <= m - 1 <= 4 (default; EMRKC_TB=0 disables)."""
     pipe = int(os.environ.get("EMRKC_PIPE") or 3)
     return (problem.dim == 3 and pipe == 3 and int(problem.n[0]) % 2 == 0
-            and int(os.environ.get("EMRKC_TB") or 0) != 0 and 2 <= m - 1 <= 4)
+            and int(os.environ.get("EMRKC_TB") or 1) != 0 and 2 <= m - 1 <= 4)
 
 
 def launch_kinds(s: int, m: int, problem=None, fused: int = 0):

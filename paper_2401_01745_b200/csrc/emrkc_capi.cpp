@@ -338,8 +338,8 @@ struct emrkc_handle {
   int fast = 1;
   int pipe = 1;
   int method = 0;  // kMethod* of the next plan (set by the API entry point)
-  int tb = 0;      // temporally blocked inner stages (EMRKC_TB=1; off: the
-                   // per-stage two-row kernels are faster on B200)
+  int tb = 1;      // temporally blocked inner stages 2..m in one pass (k_vin_tb,
+                   // 3 <= m <= 5; EMRKC_TB=0: one kernel per stage)
   int stiff = 1;   // mRKC stiff-gate split: gates in the fast part (bit 0 = m)
   double* mr_u[3] = {nullptr, nullptr, nullptr};  // mRKC inner stages (4 blocks each)
   double* mr_fs = nullptr;                        // mRKC frozen slow term
@@ -753,7 +753,7 @@ int tma_map_box3(emrkc_handle* h, const void* ptr, cuuint32_t bx, cuuint32_t by,
 }
 
 // Temporally blocked inner stages (k_vin_tb) apply: 3-D handle on the TMA
-// path with 2 <= K = m - 1 <= kTbMaxK, when enabled (EMRKC_TB=1). Slabs exchange
+// path with 2 <= K = m - 1 <= kTbMaxK (default; EMRKC_TB=0 disables). Slabs exchange
 // K planes of d_1 (the wide halo), so every slab of the partition must be at
 // least K planes deep (min_depth: emrkc_set_slab_min_depth, or the group).
 bool use_tb(const emrkc_handle* h, const Plan& pl) {
@@ -993,7 +993,7 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         f.event = a.event;
         emrkc_k::TmaTb tm;
         std::memset(&tm, 0, sizeof tm);
-        const cuuint32_t bx = emrkc_k::kTbTX + 2 * emrkc_k::kTbHX, by = emrkc_k::kTbTY + 2 * K;
+        const cuuint32_t bx = emrkc_k::kTbTX + 2 * emrkc_k::tb_hx(K), by = emrkc_k::kTbTY + 2 * K;
         int rc = tma_map_box3(h, h->u[3], bx, by, 100 + K, &tm.d1);
         // slabs: this handle's d_1 ghosts (K planes per face with a neighbour)
         Halo ht = hl;

@@ -233,7 +233,8 @@ cudaError_t launch_fused2(const Geom& g, const FusedArgs& a, const TmaFused& tm,
 // handles). Stage k is computed on the tile plus a halo of K + 1 - k cells
 // (recomputed), so only d_1 (halo K), V of g_{j-1} / g_{j-2} and V of g_j
 // touch HBM.
-constexpr int kTbMaxK = 4, kTbTX = 32, kTbTY = 16, kTbHX = 4;
+constexpr int kTbMaxK = 4, kTbTX = 32, kTbTY = 16;
+constexpr int tb_hx(int K) { return (K + 1) & ~1; }  // x halo of the d_1 box: K rounded up to even
 struct TbArgs {
   double mueta[kTbMaxK + 2], nu[kTbMaxK + 2], kappa[kTbMaxK + 2];  // mu'_k eta, nu'_k, kappa'_k (k = 0..m)
   const double* g1v;   // V block of g_{j-1}
@@ -246,7 +247,7 @@ struct TbArgs {
   unsigned long long* event;
 };
 struct TmaTb {
-  CUtensorMap d1;      // d_1, box (kTbTX + 2 kTbHX, kTbTY + 2K, 1)
+  CUtensorMap d1;      // d_1, box (kTbTX + 2 tb_hx(K), kTbTY + 2K, 1)
   CUtensorMap d1lo;    // slabs: K ghost planes of d_1 below (global z0 - K ..), box as d1
   CUtensorMap d1hi;    // K ghost planes above (global z1 ..)
 };

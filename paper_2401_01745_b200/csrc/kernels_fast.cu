@@ -2102,15 +2102,22 @@ __global__ void __launch_bounds__(128)
 // hold values nobody reads. Recurrences exactly as k_vin_tma (increment
 // form, same operation order: bitwise equal, tests/test_gpu_tb.py).
 // ---------------------------------------------------------------------------
+#ifndef EMRKC_TB_PIPE
+#define EMRKC_TB_PIPE 0  // neighbour loads of stage k + 1 before stage k computes
+#endif
 constexpr int kTbRD = 4, kTbLA = 2;  // d_1 ring planes, look-ahead (RD >= LA + 2)
 template <int K>
 struct TbTile {
   static constexpr int TX = kTbTX, TY = kTbTY;
-  static constexpr int BX = TX + 2 * kTbHX, BY = TY + 2 * K;  // d_1 box
+  static constexpr int HB = tb_hx(K);                         // x halo of the d_1 box (even)
+  static constexpr int BX = TX + 2 * HB, BY = TY + 2 * K;     // d_1 box
   static constexpr int PS = BX * BY;
   static constexpr int PSS = (PS + 15) & ~15;                 // plane stride (128 B)
-  static constexpr int HK = (K - 1 + 1) & ~1;                 // x halo of the region (even)
-  static constexpr int PR = (TX + 2 * HK) / 2;                // column pairs per row
+  // The region the threads own spans the whole box width (columns further
+  // than K - 1 from the tile compute values nobody reads), so a thread's
+  // shared address is linear in its index: 128-bit accesses of a warp never
+  // conflict.
+  static constexpr int PR = BX / 2;                           // column pairs per row
   static constexpr int RY = TY + 2 * (K - 1);                 // region rows
   static constexpr int NC = PR * RY;                          // threads owning pairs
   static constexpr int NT = (NC + 31) & ~31;
@@ -2122,7 +2129,7 @@ struct TbTile {
   __host__ __device__ static constexpr int total() { return (kTbRD + 2 * (K - 1)) * PSS; }
 };
 static_assert(kTbRD == 4 && kTbRD >= kTbLA + 2, "k_vin_tb d_1 ring (march unrolled by 4)");
-static_assert(kTbTY % 2 == 0 && kTbHX >= kTbMaxK && kTbHX % 2 == 0, "k_vin_tb tile");
+static_assert(kTbTY % 2 == 0 && tb_hx(kTbMaxK) >= kTbMaxK, "k_vin_tb tile");
 
 template <int K>
 constexpr size_t tb_smem_bytes() { return sizeof(double) * TbTile<K>::total() + 128; }
@@ -2214,6 +2221,27 @@ __device__ __forceinline__ void tb_step(const Geom& g, const Halo& h, const TbAr
 #pragma unroll
     for (int q = 0; q < K; ++q) st.D[cc][q] = st.D[cc][q + 1];
   if (has_d) lds2<EDGE ? -1 : T::ring_off(PH)>(c.aC, T::ring_off(1) * ph, st.D[0][K], st.D[1][K]);
+  // In-plane neighbours of stage k: d_1 of plane s - 1 (k = 2) or the plane
+  // stage k - 1 published one step ago. The loads of stage k + 1 are issued
+  // before stage k computes (every plane read here was published before the
+  // step's barrier), so their latency hides behind the arithmetic.
+  double nb[2][6];  // ym0, ym1, yp0, yp1, xm0, xp1 (double-buffered by stage parity)
+  auto load_nb = [&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    if constexpr (k <= M) {
+      constexpr int SRC = EDGE ? -1
+                               : (k == 2 ? T::ring_off((PH + 3) & 3)
+                                         : T::stage_off(k >= 3 ? k - 1 : 2, (PH & 1) ^ 1));
+      const int src = k == 2 ? T::ring_off(1) * ((ph + 3) & 3)
+                             : T::stage_off(k >= 3 ? k - 1 : 2, 0) + T::ring_off(1) * ((ph & 1) ^ 1);
+      double* n = nb[k & 1];
+      lds2<SRC>(c.aYm, src, n[0], n[1]);
+      lds2<SRC>(c.aYp, src, n[2], n[3]);
+      n[4] = lds1<SRC>(c.aXm, src);
+      n[5] = lds1<SRC>(c.aXp, src);
+    }
+  };
+  if (EMRKC_TB_PIPE) load_nb(std::integral_constant<int, 2>{});
   static_for<2, M + 1>([&](auto kc) {
     constexpr int k = decltype(kc)::value;
     constexpr int hk = K + 1 - k;
@@ -2223,13 +2251,9 @@ __device__ __forceinline__ void tb_step(const Geom& g, const Halo& h, const TbAr
     const bool mlo = EDGE && q < 1 && !c.gl, mhi = EDGE && q + 1 >= c.nz && !c.gh;
     const bool own_plane = !EDGE || (q >= c.zb && q < c.ze);
     const double mueta = a.mueta[k], nu = a.nu[k], kappa = a.kappa[k];
-    // in-plane neighbours: d_1 of plane s - 1 (k = 2) or the plane stage
-    // k - 1 published one step ago
-    constexpr int SRC = EDGE ? -1
-                             : (k == 2 ? T::ring_off((PH + 3) & 3)
-                                       : T::stage_off(k >= 3 ? k - 1 : 2, (PH & 1) ^ 1));
-    const int src = k == 2 ? T::ring_off(1) * ((ph + 3) & 3)
-                           : T::stage_off(k >= 3 ? k - 1 : 2, 0) + T::ring_off(1) * ((ph & 1) ^ 1);
+    if (EMRKC_TB_PIPE) load_nb(std::integral_constant<int, k + 1>{});
+    else load_nb(kc);
+    const double* n = nb[k & 1];
     double dk[2] = {0.0, 0.0};
     if (active) {
       double z0[2], z1[2], z2[2];
@@ -2247,17 +2271,13 @@ __device__ __forceinline__ void tb_step(const Geom& g, const Halo& h, const TbAr
         if (mlo) z0[cc] = z2[cc];
         if (mhi) z2[cc] = z0[cc];
       }
-      double ym[2], yp[2];
-      lds2<SRC>(c.aYm, src, ym[0], ym[1]);
-      lds2<SRC>(c.aYp, src, yp[0], yp[1]);
-      const double xm0 = lds1<SRC>(c.aXm, src), xp1 = lds1<SRC>(c.aXp, src);
-      const double xs[2] = {xm0 + z1[1], z1[0] + xp1};
+      const double xs[2] = {n[4] + z1[1], z1[0] + n[5]};
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
         const double vc = z1[cc];
         double L = fma(g.wc, vc, g.w[2] * (z0[cc] + z2[cc]));
         L = fma(g.w[0], xs[cc], L);
-        L = fma(g.w[1], ym[cc] + yp[cc], L);
+        L = fma(g.w[1], n[cc] + n[2 + cc], L);
         const double d1c = st.D[cc][K - (k - 1)];
         double bs = nu * vc;
         if constexpr (k == 3) bs = fma(nu, vc, kappa * d1c);
@@ -2329,9 +2349,9 @@ __global__ void __launch_bounds__(TbTile<K>::NT, tb_min_blocks<K>())
     const unsigned bar = b0 + 8u * (i & (kTbRD - 1));
     mbar_expect_tx(bar, 8u * T::PS);
     const unsigned dd = dbase + 8u * PSS * (i & (kTbRD - 1));
-    if (s < 0) tma_load_3d(dd, &tm.d1lo, bar, x0 - kTbHX, y0 - K, s + K);
-    else if (s >= nz) tma_load_3d(dd, &tm.d1hi, bar, x0 - kTbHX, y0 - K, s - nz);
-    else tma_load_3d(dd, &tm.d1, bar, x0 - kTbHX, y0 - K, s);
+    if (s < 0) tma_load_3d(dd, &tm.d1lo, bar, x0 - T::HB, y0 - K, s + K);
+    else if (s >= nz) tma_load_3d(dd, &tm.d1hi, bar, x0 - T::HB, y0 - K, s - nz);
+    else tma_load_3d(dd, &tm.d1, bar, x0 - T::HB, y0 - K, s);
   };
   const int npro = min(kTbLA, hi1 - lo1);
   if (t == 0) {
@@ -2355,16 +2375,17 @@ __global__ void __launch_bounds__(TbTile<K>::NT, tb_min_blocks<K>())
   // past the last pair repeat an earlier pair (identical values, no outputs).
   const int tt = t < T::NC ? t : t - T::NC;
   const int px = tt % T::PR, cy = tt / T::PR;
-  const int gx = x0 - T::HK + 2 * px, gy = y0 - (K - 1) + cy;
-  const int ci = (cy + 1) * BX + (kTbHX - T::HK) + 2 * px;  // cell 0 in the box
+  const int gx = x0 - T::HB + 2 * px, gy = y0 - (K - 1) + cy;
+  const int ci = BX + 2 * tt;  // cell 0 in the box: row cy + 1, column 2 px
   TbCtx c;
   c.own = t < T::NC && gx >= x0 && gx < min(x0 + T::TX, n0) && gy >= y0 &&
           gy < min(y0 + T::TY, n1);
   c.sel = c.own ? 0xffffffffu : 0u;
   c.aC = dbase + 8u * ci;
   // x - 1 of cell 0 (mirror at x = 0; box column 0 has no left cell: any value)
-  c.aXm = c.aC + ((gx > 0 && kTbHX - T::HK + 2 * px > 0) ? -8 : 8);
-  c.aXp = c.aC + 8u + (gx + 1 < n0 - 1 ? 8 : -8);  // x + 1 of cell 1
+  c.aXm = c.aC + ((gx > 0 && px > 0) ? -8 : 8);
+  // x + 1 of cell 1 (mirror at x = n0 - 1; none right of the last box column)
+  c.aXp = c.aC + 8u + ((gx + 1 < n0 - 1 && px < T::PR - 1) ? 8 : -8);
   c.aYm = c.aC + (gy > 0 ? -8 * BX : 8 * BX);
   c.aYp = c.aC + (gy < n1 - 1 ? 8 * BX : -8 * BX);
   c.b0 = b0;

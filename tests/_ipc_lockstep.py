@@ -36,7 +36,7 @@ def main(out):
         rS = w.rho_S_forced if w.rho_S_forced is not None else 0.7114
         if key.endswith("@tb"):
             rF, rS = 700.0, 0.7114
-        # handles read EMRKC_TB when created (off by default)
+        # handles read EMRKC_TB when created (on by default)
         os.environ["EMRKC_TB"] = "1" if key.endswith("@tb") else "0"
         slab = pdist.DistSlab(w.problem, ctx, 0)
         slab.link()

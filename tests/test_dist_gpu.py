@@ -60,7 +60,7 @@ TB_CASES = {"3d_tb_m3": (3, 1), "3d_tb_m5": (5, 1), "3d_tb_s2m4": (4, 2)}
 @pytest.mark.parametrize("case", ["3d_m2", "2d_m1", "3d_m1", *TB_CASES])
 def test_dist_protocol_bitwise(case, nslab, monkeypatch):
     if case in TB_CASES:
-        monkeypatch.setenv("EMRKC_TB", "1")  # off by default
+        monkeypatch.setenv("EMRKC_TB", "1")  # the default
     if case == "3d_m2":
         w = workloads.parity_3d()
         p, y0, dt, rF, rS, n = w.problem, w.initial_state(), w.dt, 400.0, 50.0, 6

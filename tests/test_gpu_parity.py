@@ -172,7 +172,7 @@ def test_group_slabs_bitwise(oracle, name, nslab, monkeypatch):
         y0 = noisy(oracle, p)
         dt, rF, rS, n = 0.05, 10.0, 0.7, 30
     elif name == "p3d_48_tb":  # m = 5: K = 4 temporally blocked stages, 4-plane d_1 halo
-        monkeypatch.setenv("EMRKC_TB", "1")  # off by default
+        monkeypatch.setenv("EMRKC_TB", "1")  # the default
         w = workloads.get("p3d_48_s2m2")
         p = w.problem
         y0 = w.initial_state()

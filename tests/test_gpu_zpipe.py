@@ -27,6 +27,7 @@ def state(oracle, p, seed=0):
 
 def run(p, y0, n, K, monkeypatch, rF, rS=0.7, step_after=True):
     monkeypatch.setenv("EMRKC_ZPIPE", str(K))
+    monkeypatch.setenv("EMRKC_TB", "0")  # the z-pipelined step chains per-stage inner kernels
     op = MonodomainOperator(p)
     op.set_state(y0)
     res = op.run(0, n, 0.05, rF, rS).as_dict()
