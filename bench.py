@@ -656,8 +656,10 @@ def b200_arm(args, w):
         # (the aux rows' eigenvalues, |k_a| <= 0.01/ms, do not reach rho_S or
         # rho_F; the plan s, m is the same).
         hh_rho = {"hh3d_512x512x256_w19": (rF, rS) if w.name == "hh3d_512x512x256" else None}
-        for name in ("hh3d_128x128x128", "hh2d_256x256", "hh3d_512x512x256_w19",
-                     "hh3d_256x256x128_w21"):
+        # config 3's grid with HH, and config 5's finest grid (N = 200, m = 4:
+        # inner stages 2..4 in one temporally blocked pass, k_vin_tb)
+        for name in ("hh3d_128x128x128", "hh2d_256x256", "hh3d_256x256x128", "hh3d_sweep_200",
+                     "hh3d_512x512x256_w19", "hh3d_256x256x128_w21"):
             if name == w.name:
                 continue
             wx = workloads.get(name)
