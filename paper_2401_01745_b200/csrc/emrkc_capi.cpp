@@ -340,6 +340,7 @@ struct emrkc_handle {
   int method = 0;  // kMethod* of the next plan (set by the API entry point)
   int tb = 1;      // temporally blocked inner stages 2..m in one pass (k_vin_tb,
                    // 3 <= m <= 5; EMRKC_TB=0: one kernel per stage)
+  int pair = 1;    // pair-per-thread node kernel on 3-D whole grids (EMRKC_PAIR=0: k_node_tma)
   int stiff = 1;   // mRKC stiff-gate split: gates in the fast part (bit 0 = m)
   double* mr_u[3] = {nullptr, nullptr, nullptr};  // mRKC inner stages (4 blocks each)
   double* mr_fs = nullptr;                        // mRKC frozen slow term
@@ -642,9 +643,11 @@ bool tma_supported(const emrkc_handle* h) {
   return h->geom.dim >= 2 && h->geom.n0 % 2 == 0 && tma_encoder() != nullptr;
 }
 
-// rmul: tile rows x rmul (the multi-row inner-stage kernel, vin_rows)
-int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out, int rmul = 1) {
-  const int key = kind + 1000 * (rmul - 1);
+// rmul: tile rows x rmul (the multi-row inner-stage kernel, vin_rows);
+// xmul: tile width x xmul (3-D; the pair-per-thread node kernel)
+int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out, int rmul = 1,
+            int xmul = 1) {
+  const int key = kind + 1000 * (rmul - 1) + 100000 * (xmul - 1);
   for (const auto& e : h->tmaps)
     if (e.ptr == ptr && e.kind == key) {
       *out = e.map;
@@ -652,7 +655,7 @@ int tma_map(emrkc_handle* h, const void* ptr, int kind, CUtensorMap* out, int rm
     }
   const Geom& g = h->geom;
   const bool d3 = g.dim == 3;
-  const cuuint32_t tx = d3 ? emrkc_k::kTX3 : emrkc_k::kTX2,
+  const cuuint32_t tx = d3 ? emrkc_k::kTX3 * static_cast<cuuint32_t>(xmul) : emrkc_k::kTX2,
                    ty = d3 ? emrkc_k::kTY3 * static_cast<cuuint32_t>(rmul) : 1;
   const bool halo = kind == kTmaHalo || kind == kTmaGhost;
   cuuint64_t dims[4];
@@ -750,6 +753,13 @@ int tma_map_box3(emrkc_handle* h, const void* ptr, cuuint32_t bx, cuuint32_t by,
   h->tmaps.push_back({ptr, key, m});
   *out = m;
   return EMRKC_OK;
+}
+
+// Pair-per-thread node kernel (k_node_pair): 3-D whole-grid handles on the
+// TMA path with HH proper (no aux rows); EMRKC_PAIR=0 keeps k_node_tma.
+bool use_pair(const emrkc_handle* h) {
+  return h->pair && h->fast && h->pipe == 3 && h->geom.dim == 3 && h->geom.naux == 0 &&
+         !h->partitioned && !h->level_hook;
 }
 
 // Temporally blocked inner stages (k_vin_tb) apply: 3-D handle on the TMA
@@ -942,7 +952,18 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         ++h->level;
         return EMRKC_OK;
       }
-      if (h->pipe == 3) {
+      const int pzc = use_pair(h) ? emrkc_k::pair_zc(h->geom, j == 1, h->pair == 2) : 0;
+      if (pzc > 0) {
+        // pair-per-thread node kernel (3-D whole grid, HH proper)
+        emrkc_k::TmaNode tm;
+        std::memset(&tm, 0, sizeof tm);
+        int rc = tma_map(h, f.g1, kTmaHalo, &tm.v, 1, emrkc_k::kPairXMul);
+        if (!rc) rc = tma_map(h, f.g1, kTmaGates, &tm.gates, 1, emrkc_k::kPairXMul);
+        if (!rc && f.g2) rc = tma_map(h, f.g2, kTmaAll, &tm.g2, 1, emrkc_k::kPairXMul);
+        if (rc) return rc;
+        f.zc = pzc;
+        CK(h, emrkc_k::launch_node_pair(h->geom, f, tm, pl.m >= 2, lstream(h)));
+      } else if (h->pipe == 3) {
         emrkc_k::TmaNode tm;
         int rc = tma_map(h, f.g1, kTmaHalo, &tm.v);
         if (!rc) rc = tma_map(h, f.g1, kTmaGates, &tm.gates);
@@ -1227,6 +1248,8 @@ int init_handle(emrkc_handle* h) {
   if (h->pipe != 3) h->zc = std::min(h->zc, emrkc_k::kMaxZcPipe);
   if (const char* tb = std::getenv("EMRKC_TB"))
     if (*tb) h->tb = std::atoi(tb) != 0;
+  if (const char* pr = std::getenv("EMRKC_PAIR"))
+    if (*pr) h->pair = std::max(0, std::min(2, std::atoi(pr)));  // 2: also on small grids (tests)
   if (const char* fu = std::getenv("EMRKC_FUSED"))
     if (*fu) h->fused = std::atoi(fu) != 0;
   if (const char* zp = std::getenv("EMRKC_ZPIPE"))

@@ -1485,6 +1485,265 @@ __global__ void __launch_bounds__(PipeTile<DIM>::NT, EMRKC_PIPE_MINBLOCKS)
 }
 
 // ---------------------------------------------------------------------------
+// k_node_pair<FIRST, ION>: k_node_tma's outer stage (3-D, HH proper, whole
+// grid) with an x-adjacent PAIR of nodes per thread: 64 x 4 tiles, 128
+// threads. k_node_tma spends ~140 of its ~340 warp instructions per node on
+// per-plane work that does not depend on the node count (ring and address
+// arithmetic, barrier, mbarrier wait, parameter loads, stimulus / range
+// tests); here that work serves two nodes, and
+//   * the z neighbours of a column are the thread's own registers (a
+//     (z - 1, z) window; one 128-bit shared load brings plane z + 1 of both
+//     nodes), the inner x neighbours are the pair's own values: 5 shared
+//     loads of V per pair (3 x 128 bit, 2 x 64 bit) instead of 14;
+//   * gates arrive with one 128-bit shared load per field and every output
+//     field leaves with one 128-bit global store per pair;
+//   * finite tests run on the integer pipe (max over hi | 0x800fffff).
+// Same node arithmetic (node_update_s) in the same order: bitwise equal to
+// k_node_tma (tests/test_gpu_kernel_families.py). No slab faces: partitioned
+// handles, aux rows and 2-D grids keep k_node_tma.
+// ---------------------------------------------------------------------------
+constexpr int kPairTX = 64, kPairTY = 4, kPairNT = 128;
+constexpr int kPairHX = kPairTX + 4, kPairHY = kPairTY + 2;  // V box 68 x 6 (x0 - 2, y0 - 1)
+constexpr int kPairVT = kPairHX * kPairHY;
+constexpr int kPairVS = (kPairVT + 15) & ~15;
+constexpr int kPairCS = kPairTX * kPairTY;  // cells of one centre field
+
+template <int FIRST>
+constexpr size_t pair_smem_bytes() {
+  return sizeof(double) * (kRV * kPairVS + kRG * 3 * kPairCS + (FIRST ? 0 : kRG * 4 * kPairCS)) +
+         128;
+}
+
+__device__ __forceinline__ unsigned nf_hi(double v) {
+  return (unsigned)__double2hiint(v) | 0x800fffffu;
+}
+
+template <int FIRST, int ION>
+__global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
+    k_node_pair(const Geom g, const FastArgs a, const __grid_constant__ TmaNode tm) {
+  constexpr int VS = kPairVS, CS = kPairCS, HXT = kPairHX;
+  extern __shared__ __align__(128) double smem_tma[];
+  double* vst = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;  // [kRV][VS]
+  double* gst = vst + kRV * VS;        // [kRG][3][CS]
+  double* g2s = gst + kRG * 3 * CS;    // [kRG][4][CS]
+  __shared__ double tab[256];
+  __shared__ __align__(8) unsigned long long bars[kRV];
+  __shared__ int skip;
+  const int t = threadIdx.x;
+  const int zb = a.z_lo + blockIdx.z * a.zc;
+  const int ze = min(a.z_hi, zb + a.zc);
+  pdl_launch_dependents();
+  if (t == 0) {  // prologue that reads nothing the previous kernel writes
+    for (int s = 0; s < kRV; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    mbar_fence_init();
+    prefetch_tensormap(&tm.v);
+    prefetch_tensormap(&tm.gates);
+    if (!FIRST) prefetch_tensormap(&tm.g2);
+  }
+  __syncthreads();
+  const int px = t & 31, ty = t >> 5;
+  const int x0 = blockIdx.x * kPairTX, y0 = blockIdx.y * kPairTY;
+  const int cx = x0 + 2 * px, cy = y0 + ty;  // cell 0; cell 1 = (cx + 1, cy)
+  const bool valid = cx < g.n0 && cy < g.n1;  // n0 is even: both cells or none
+  const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
+  const long long nn = g.nn, plane = g.plane;
+  const unsigned v0 = smem_u32(vst), gs0 = smem_u32(gst), qs0 = smem_u32(g2s);
+  const unsigned b0 = smem_u32(bars);
+  constexpr unsigned vbytes = 8u * kPairVT;
+  constexpr unsigned cbytes = 8u * CS * (3 + (FIRST ? 0 : 4));
+  auto issue_comp = [&](int zz) {  // thread 0: plane zz in [zb, ze)
+    const int q = zz - zb + 1;
+    const unsigned bar = b0 + 8u * (q & (kRV - 1));
+    const unsigned sg = (unsigned)((zz - zb) & (kRG - 1));
+    mbar_expect_tx(bar, vbytes + cbytes);
+    tma_load_3d(v0 + 8u * VS * (q & (kRV - 1)), &tm.v, bar, x0 - 2, y0 - 1, zz);
+    tma_load_4d(gs0 + 8u * 3 * CS * sg, &tm.gates, bar, x0, y0, zz, 1);
+    if (!FIRST) tma_load_4d(qs0 + 8u * 4 * CS * sg, &tm.g2, bar, x0, y0, zz, 0);
+  };
+  // halo plane zb - 1 or ze (V only; mirrored at the grid faces)
+  auto issue_edge = [&](int zz, unsigned extra) {
+    const int q = zz - zb + 1;
+    const unsigned bar = b0 + 8u * (q & (kRV - 1));
+    mbar_expect_tx(bar, vbytes + extra);
+    const int lz = zz < 0 ? 1 : (zz >= g.nzl ? g.nzl - 2 : zz);
+    tma_load_3d(v0 + 8u * VS * (q & (kRV - 1)), &tm.v, bar, x0 - 2, y0 - 1, lz);
+  };
+  pdl_wait();
+  if (t == 0) {
+    bulk_load(smem_u32(tab), kExp2Tab256, sizeof(double) * 256, b0);  // exp table
+    issue_edge(zb - 1, sizeof(double) * 256);
+    for (int i = 0; i < kTmaLA; ++i) {
+      if (zb + i < ze) issue_comp(zb + i);
+      else {
+        issue_edge(ze, 0);
+        break;
+      }
+    }
+  }
+  if (t == 32) skip = (*(volatile const unsigned long long*)a.event) < level_floor(a.code_base, a.j, a.m, 1);
+  __syncthreads();
+  if (skip != 0) {  // aborted earlier: drain the prologue copies
+    const int np = 1 + min(kTmaLA, ze - zb) + (ze - zb < kTmaLA ? 1 : 0);
+    for (int q = 0; q < np; ++q) mbar_wait(b0 + 8u * q, 0);
+    return;
+  }
+  // cell 0 of the pair in a V stage; mirrored in-plane neighbours at the
+  // grid edge (halo cells there are 0): x - 1 of cell 0, x + 1 of cell 1
+  const int cell = (ty + 1) * HXT + 2 * px + 2;
+  const int cxm = cell + (cx > 0 ? -1 : 1), cxp = cell + 1 + (cx + 1 < g.n0 - 1 ? 1 : -1);
+  const int cym = cell + (cy > 0 ? -HXT : HXT), cyp = cell + (cy < g.n1 - 1 ? HXT : -HXT);
+  const int gcell = ty * kPairTX + 2 * px;  // the pair in a centre field
+  int zs0 = 1, zs1 = 0;
+  const bool st0 = valid && stim_col_xy<3>(g, cx, cy), st1 = valid && stim_col_xy<3>(g, cx + 1, cy);
+  if (st0 || st1) {
+    zs0 = g.st_lo[2] - g.zoff;
+    zs1 = g.st_hi[2] - g.zoff;
+  }
+  bool guard = false;
+  unsigned nfacc = 0u;  // all ones once an output was non-finite
+  unsigned long long slow_mask = 0;  // planes z - zb (< kMaxZc = 64) left to the reference path
+  double glo = 2.0, ghi = -1.0;
+  double* po = a.out + ip + plane * zb;
+  double* pu = ION ? a.u1 + ip + plane * zb : nullptr;
+  mbar_wait(b0, 0);       // plane zb - 1
+  mbar_wait(b0 + 8u, 0);  // plane zb
+  // z window of the two columns: planes z - 1 and z
+  double2 wm = *reinterpret_cast<const double2*>(vst + cell);
+  double2 wc = *reinterpret_cast<const double2*>(vst + VS + cell);
+  for (int z = zb; z < ze; ++z) {
+    const int p = z - zb + 1;
+    if (t == 0) {
+      if (z + kTmaLA < ze) issue_comp(z + kTmaLA);
+      else if (z + kTmaLA == ze) issue_edge(ze, 0);
+    }
+    mbar_wait(b0 + 8u * ((p + 1) & (kRV - 1)), ((p + 1) >> 3) & 1);
+    const double* V0 = vst + (p & (kRV - 1)) * VS;
+    const double2 wp = *reinterpret_cast<const double2*>(vst + ((p + 1) & (kRV - 1)) * VS + cell);
+    const double2 ym = *reinterpret_cast<const double2*>(V0 + cym);
+    const double2 yp = *reinterpret_cast<const double2*>(V0 + cyp);
+    const double xm0 = V0[cxm], xp1 = V0[cxp];
+    const double* G0 = gst + ((z - zb) & (kRG - 1)) * 3 * CS + gcell;
+    const double* Q0 = g2s + ((z - zb) & (kRG - 1)) * 4 * CS + gcell;
+    const double2 za = *reinterpret_cast<const double2*>(G0);
+    const double2 zb2 = *reinterpret_cast<const double2*>(G0 + CS);
+    const double2 zc2 = *reinterpret_cast<const double2*>(G0 + 2 * CS);
+    const bool fast = fabs(wc.x - a.vmid) <= a.vfast && fabs(wc.y - a.vmid) <= a.vfast;
+    if (!fast) slow_mask |= 1ull << (z - zb);
+    NodeOut r0 = node_update_s<3, FIRST, ION, 0>(g, a, tab, wm.x, wc.x, wp.x, xm0 + wc.y,
+                                                 ym.x + yp.x, za.x, zb2.x, zc2.x, 0.0, Q0, CS);
+    NodeOut r1 = node_update_s<3, FIRST, ION, 0>(g, a, tab, wm.y, wc.y, wp.y, wc.x + xp1,
+                                                 ym.y + yp.y, za.y, zb2.y, zc2.y, 0.0, Q0 + 1, CS);
+    if (z >= zs0 && z <= zs1) {
+      const double sc = ION ? a.mue1 : a.cV;
+      if (st0) r0.o0 = fma(sc, a.stim, r0.o0);
+      if (st1) r1.o0 = fma(sc, a.stim, r1.o0);
+    }
+    if (valid && fast) {
+      *reinterpret_cast<double2*>(po + nn) = make_double2(r0.o1, r1.o1);
+      *reinterpret_cast<double2*>(po + 2 * nn) = make_double2(r0.o2, r1.o2);
+      *reinterpret_cast<double2*>(po + 3 * nn) = make_double2(r0.o3, r1.o3);
+      if (ION) {
+        *reinterpret_cast<double2*>(pu) = make_double2(r0.o0, r1.o0);
+      } else {
+        *reinterpret_cast<double2*>(po) = make_double2(r0.o0, r1.o0);
+        guard |= !(fabs(r0.o0) <= 1e6) || !(fabs(r1.o0) <= 1e6);  // also a non-finite V
+      }
+      nfacc = max(max(nfacc, max(nf_hi(r0.o0), nf_hi(r0.o1))), max(nf_hi(r0.o2), nf_hi(r0.o3)));
+      nfacc = max(max(nfacc, max(nf_hi(r1.o0), nf_hi(r1.o1))), max(nf_hi(r1.o2), nf_hi(r1.o3)));
+      if (a.last) {  // std::min / std::max per value (NaN skipped), select form
+        glo = r0.o1 < glo ? r0.o1 : glo;
+        ghi = ghi < r0.o1 ? r0.o1 : ghi;
+        glo = r0.o2 < glo ? r0.o2 : glo;
+        ghi = ghi < r0.o2 ? r0.o2 : ghi;
+        glo = r0.o3 < glo ? r0.o3 : glo;
+        ghi = ghi < r0.o3 ? r0.o3 : ghi;
+        glo = r1.o1 < glo ? r1.o1 : glo;
+        ghi = ghi < r1.o1 ? r1.o1 : ghi;
+        glo = r1.o2 < glo ? r1.o2 : glo;
+        ghi = ghi < r1.o2 ? r1.o2 : ghi;
+        glo = r1.o3 < glo ? r1.o3 : glo;
+        ghi = ghi < r1.o3 ? r1.o3 : ghi;
+      }
+    }
+    wm = wc;
+    wc = wp;
+    po += plane;
+    if (ION) pu += plane;
+    __syncthreads();  // stage (p - 5) may be refilled next iteration
+  }
+  bool bad = nfacc == 0xffffffffu;
+  if (valid && slow_mask) {  // planes with a node outside the fast window: reference-order path
+    const Halo h0{};
+    for (int c = 0; c < 2; ++c) {
+      const long long ipc = ip + c;
+      const Nbr<3> o = nbr_of<3>(g, Col<3>{cx + c, cy, ipc, zb, ze, true});
+      const double* G = a.g1;
+      const bool stc = c ? st1 : st0;
+      for (int z = zb; z < ze; ++z) {
+        if (!(slow_mask >> (z - zb) & 1ull)) continue;
+        const long long i = ipc + plane * z;
+        const double vc = __ldg(G + i);
+        const double vm = zval(G, g, ipc, z - 1, nullptr, nullptr);
+        const double vp = zval(G, g, ipc, z + 1, nullptr, nullptr);
+        const double xs = __ldg(G + i + o.xm) + __ldg(G + i + o.xp);
+        const double ys = __ldg(G + i + o.ym) + __ldg(G + i + o.yp);
+        const double stim = (stc && z >= zs0 && z <= zs1) ? a.stim : 0.0;
+        double q[4] = {0.0, 0.0, 0.0, 0.0};
+        if (!FIRST)
+          for (int f = 0; f < 4; ++f) q[f] = __ldg(a.g2 + f * nn + i);
+        // a node inside the window whose partner is not: the hot loop's form
+        // (stimulus added to the result), so both kernels agree bit for bit
+        NodeOut r;
+        if (fabs(vc - a.vmid) <= a.vfast) {
+          r = node_update_s<3, FIRST, ION, 0>(g, a, tab, vm, vc, vp, xs, ys, __ldg(G + nn + i),
+                                              __ldg(G + 2 * nn + i), __ldg(G + 3 * nn + i), 0.0,
+                                              q, 1);
+          if (stc && z >= zs0 && z <= zs1) r.o0 = fma(ION ? a.mue1 : a.cV, a.stim, r.o0);
+        } else {
+          r = node_update_s<3, FIRST, ION, 1>(g, a, tab, vm, vc, vp, xs, ys, __ldg(G + nn + i),
+                                              __ldg(G + 2 * nn + i), __ldg(G + 3 * nn + i), stim,
+                                              q, 1);
+        }
+        a.out[nn + i] = r.o1;
+        a.out[2 * nn + i] = r.o2;
+        a.out[3 * nn + i] = r.o3;
+        if (ION) {
+          a.u1[i] = r.o0;
+        } else {
+          a.out[i] = r.o0;
+          guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
+        }
+        bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
+        if (a.last) {
+          glo = fmin(glo, fmin(r.o1, fmin(r.o2, r.o3)));
+          ghi = fmax(ghi, fmax(r.o1, fmax(r.o2, r.o3)));
+        }
+      }
+    }
+    (void)h0;
+  }
+  if (bad && !a.exex) {  // EXEX-RL never throws NumericalAbort
+    const Halo h0{};
+    bool inner = false;
+    for (int c = 0; c < 2; ++c) {
+      Col<3> col;
+      col.c0 = cx + c;
+      col.c1 = cy;
+      col.ip = ip + c;
+      col.z0 = zb;
+      col.z1 = ze;
+      col.valid = true;
+      inner |= inner_nonfinite<3>(g, h0, a.g1, col, nbr_of<3>(g, col), a.eta);
+    }
+    atomicMin(a.event, a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1)) +
+                           (inner ? 1 : a.m + 1));
+  }
+  if (!ION && a.last && guard)
+    atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
+  if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, valid && ze > zb);
+}
+
+// ---------------------------------------------------------------------------
 // k_resident: a whole emrkc_run on a small grid in one cooperative launch
 // (s = m = 1). Config 1 (256^2) and the small sweep grids are launch- and
 // latency-bound one step per launch (~11 us for 65k nodes); here every
@@ -3155,6 +3414,41 @@ cudaError_t launch_node_tma(const Geom& g, const Halo& h, const FastArgs& a, con
   }
   if (ion) return first ? launch_node_tma_t<2, 1, 1>(g, h, a, tm, st) : launch_node_tma_t<2, 0, 1>(g, h, a, tm, st);
   return first ? launch_node_tma_t<2, 1, 0>(g, h, a, tm, st) : launch_node_tma_t<2, 0, 0>(g, h, a, tm, st);
+}
+
+// k_node_pair (3-D, whole grid, HH proper): z-chunk for 64 x 4 tiles at 4
+// (FIRST) / 2 resident blocks per SM, same 1.7-wave floor as fast_zc.
+int pair_zc(const Geom& g, bool first, bool force) {
+  const long long tiles = (long long)((g.n0 + kPairTX - 1) / kPairTX) * ((g.n1 + kPairTY - 1) / kPairTY);
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    sms = 148;
+  const long long want = (long long)(1.7 * sms * (first ? 4 : 2));
+  for (int zc = 48; zc >= 4; --zc)
+    if (tiles * ((g.nzl + zc - 1) / zc) >= want) return zc > g.nzl ? g.nzl : zc;
+  return force ? (g.nzl < 16 ? g.nzl : 16) : 0;  // too few blocks: the caller keeps k_node_tma
+}
+
+template <int F, int I>
+static cudaError_t launch_node_pair_t(const Geom& g, const FastArgs& a, const TmaNode& tm,
+                                      cudaStream_t st) {
+  constexpr size_t smem = pair_smem_bytes<F>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_node_pair<F, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int chunks = (a.z_hi - a.z_lo + a.zc - 1) / a.zc;
+  const dim3 grd((g.n0 + kPairTX - 1) / kPairTX, (g.n1 + kPairTY - 1) / kPairTY, chunks);
+  return launch_k(k_node_pair<F, I>, grd, dim3(kPairNT), smem, st, g, a, tm);
+}
+
+cudaError_t launch_node_pair(const Geom& g, const FastArgs& a, const TmaNode& tm, bool ion,
+                             cudaStream_t st) {
+  const bool first = a.j == 1;
+  if (ion) return first ? launch_node_pair_t<1, 1>(g, a, tm, st) : launch_node_pair_t<0, 1>(g, a, tm, st);
+  return first ? launch_node_pair_t<1, 0>(g, a, tm, st) : launch_node_pair_t<0, 0>(g, a, tm, st);
 }
 
 template <int D, int L, int F>
