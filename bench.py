@@ -91,7 +91,7 @@ KERNEL_ROLES = {"m1": ("node", "m = 1: whole outer stage"),
                 "zpipe_skip": ("zpipe", "timed with the step")}
 
 
-def kernel_name(kind: str, problem) -> str:
+def kernel_name(kind: str, problem, node_kernel: int = 0) -> str:
     """Kernel family the library selects (emrkc_capi.cpp init_handle):
     EMRKC_PIPE 3 (default; TMA, needs n0 even and dim >= 2), 1 (cp.async),
     2 (persistent node kernel), 0 (z-march)."""
@@ -108,6 +108,8 @@ def kernel_name(kind: str, problem) -> str:
     fam = {3: "tma", 1: "pipe", 2: "persist" if role == "node" else "pipe", 0: "fast"}[pipe]
     if kind.startswith("tb"):
         fam = "tb"
+    if role == "node" and node_kernel == 1:  # emrkc_node_kernel: pair-per-thread node kernel
+        fam = "pair"
     return f"k_{role}_{fam} ({what})"
 
 
@@ -476,6 +478,7 @@ def measure_device(w, device, warmup, steps, with_e2e=True, clocks=None, ramp_s=
                        ", best of 3, device time of the run, no L2 flush between steps"}
     out = {"op": op, "y0": y0, "rF": rF, "rS": rS, "s": rep.s, "m": rep.m, "run": run,
            "fused": int(lib.emrkc_fused_active(op.handle)),
+           "node_kernel": int(lib.emrkc_node_kernel(op.handle)),
            "launch_ms": launch_ms.reshape(steps, per), "res": results[-1], "steps": steps,
            "repeats": len(chunks), "aborted": any(r.aborted for r in results),
            "abort_at": kr if kr < w.n_steps else None}
@@ -599,7 +602,7 @@ def roofline_of(m, w, peak, peak_kind):
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "traffic": traffic,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-        "kernel": kernel_name(kinds[dom][0], w.problem),
+        "kernel": kernel_name(kinds[dom][0], w.problem, m.get("node_kernel", 0)),
         "alg_bytes_per_node": kb, "mean_launch_ms": float(per_pos[dom]),
         "share_of_step": float(per_pos[dom] / per_pos.sum()),
         "step_alg_bytes_per_node": 16 * nf, "step_achieved_gbs": step_gbs,

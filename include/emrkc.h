@@ -215,6 +215,11 @@ int emrkc_get_state(emrkc_handle* h, double* y, int64_t len);
  * stencil level. A diagnostic for benches and tests; no reference
  * counterpart. */
 int32_t emrkc_fused_active(emrkc_handle* h);
+/* Node kernel of the outer-stage level on this handle: 1 = k_node_pair (an
+ * x-adjacent pair of nodes per thread; 3-D whole grids with HH proper on the
+ * TMA path, EMRKC_PAIR=0 disables), 0 = k_node_tma or the family EMRKC_PIPE
+ * selects. A diagnostic for benches and tests; no reference counterpart. */
+int32_t emrkc_node_kernel(emrkc_handle* h);
 /* Device pointer of the current state (valid until the next step/run). */
 int emrkc_state_device_ptr(emrkc_handle* h, double** dptr);
 int emrkc_synchronize(emrkc_handle* h);

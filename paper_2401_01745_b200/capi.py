@@ -230,6 +230,7 @@ PROTOTYPES = {
     "emrkc_get_state": (C.c_int, [C.c_void_p, DP, C.c_int64]),
     "emrkc_state_device_ptr": (C.c_int, [C.c_void_p, C.POINTER(DP)]),
     "emrkc_fused_active": (C.c_int32, [C.c_void_p]),
+    "emrkc_node_kernel": (C.c_int32, [C.c_void_p]),
     "emrkc_synchronize": (C.c_int, [C.c_void_p]),
     "emrkc_eval_rhs": (C.c_int, [C.c_void_p, C.c_int32, C.c_double, DP, DP, C.c_int64]),
     "emrkc_exp_part": (C.c_int, [C.c_void_p, DP, DP, DP, C.c_int64]),

@@ -3124,6 +3124,11 @@ int emrkc_model_ionic_current(int32_t model, double V, const double* z_E, double
   return EMRKC_OK;
 }
 
+int32_t emrkc_node_kernel(emrkc_handle* h) {
+  if (!h) return 0;
+  return use_pair(h) && emrkc_k::pair_zc(h->geom, true, h->pair == 2) > 0 ? 1 : 0;
+}
+
 int32_t emrkc_fused_active(emrkc_handle* h) {
   if (!h || !h->plan_uploaded) return 0;
   if (use_fused(h, h->plan)) return 1;

@@ -27,6 +27,7 @@
 #include "fast_math.cuh"
 #include "hh.cuh"
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <type_traits>
 #include <utility>
@@ -3126,14 +3127,28 @@ __global__ void __launch_bounds__(kFuNT, 2)
 // Planes per block (z-chunk length): 16 amortises the block prologue (abort
 // word, exp table, the cp.async pipeline fill); halved while the grid would
 // give fewer than ~2 waves of 148 SMs x 5 resident blocks.
-int fast_zc(const Geom& g) {
-  if (g.dim == 1) return 1;
-  const long long tiles = (g.dim == 3) ? ((g.n0 + 31) / 32) * (long long)((g.n1 + 3) / 4)
-                                       : (g.n0 + 127) / 128;
-  // Longest z-chunk (<= 48, below the 64-bit deferred-node mask) that still gives
-  // >= 1.7 waves of resident node blocks (5 per SM): long chunks amortise
-  // the halo planes and the pipeline prologue, the wave floor keeps the
-  // tail short (measured on B200).
+// z-chunk of the staged 3-D node kernels. A launch of B = tiles x
+// ceil(nz / zc) blocks on S resident slots takes about
+//   W (1 + c0 / zc) + alpha (zc + c0),   W = tiles nz / S planes per slot:
+// every block pays a prologue worth c0 planes (barrier init, table, pipeline
+// fill), and the launch ends with a tail of about alpha blocks (the last
+// slots run part-empty). Measured on B200 (gpurun_out/ab_pair_zc*.log:
+// 128^3, 256x256x128, 512x512x256, sweep N = 100 / 200; r01 zc sweeps of
+// k_node_tma): c0 / alpha = 3.75 planes for k_node_pair and 7.5 for
+// k_node_tma (half the work per plane), i.e. zc* = sqrt(c0 W / alpha):
+// 128^3 -> 8 / 13, 256x256x128 -> 14, 512x512x256 -> 43-48. Chunks are
+// balanced (ceil(nz / chunks)) and at most 48 planes (the deferred-node mask
+// has 64 bits; longer chunks measured slower).
+static int zc_model(int nz, long long tiles, int slots, double k) {
+  const double W = (double)tiles * nz / slots;
+  const double zs = std::sqrt(k * W);
+  int chunks = (int)(nz / std::fmax(zs, 1.0) + 0.5);
+  chunks = std::max(chunks, (nz + 47) / 48);
+  chunks = std::max(1, std::min(chunks, std::max(1, nz / 4)));
+  return (nz + chunks - 1) / chunks;
+}
+
+static int sm_count() {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -3141,9 +3156,19 @@ int fast_zc(const Geom& g) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
       sms = 148;
   }
-  const long long want = (long long)(1.7 * sms * 5);
-  // longest chunk: 48 (config-4 step, B200, r02: zc 32 / 48 / 64 -> 1.205 /
-  // 1.186 / 1.200 ms)
+  return sms;
+}
+
+int fast_zc(const Geom& g) {
+  if (g.dim == 1) return 1;
+  if (const char* e = std::getenv("EMRKC_ZC"))  // experiments
+    if (*e) return std::max(1, std::min(std::atoi(e), std::min(g.nzl, 48)));
+  if (g.dim == 3)  // k_node_tma: 32 x 4 tiles, 5 resident blocks per SM
+    return zc_model(g.nzl, ((g.n0 + 31) / 32) * (long long)((g.n1 + 3) / 4), 5 * sm_count(), 7.5);
+  const long long tiles = (g.n0 + 127) / 128;
+  // 2-D (latency-bound launches): the longest chunk that
+  // still gives >= 1.7 waves of resident node blocks
+  const long long want = (long long)(1.7 * sm_count() * 5);
   for (int zc = 48; zc >= 4; --zc)
     if (tiles * ((g.nzl + zc - 1) / zc) >= want) return zc > g.nzl ? g.nzl : zc;
   int zc = 16;
@@ -3419,15 +3444,13 @@ cudaError_t launch_node_tma(const Geom& g, const Halo& h, const FastArgs& a, con
 // k_node_pair (3-D, whole grid, HH proper): z-chunk for 64 x 4 tiles at 4
 // (FIRST) / 2 resident blocks per SM, same 1.7-wave floor as fast_zc.
 int pair_zc(const Geom& g, bool first, bool force) {
+  if (const char* e = std::getenv("EMRKC_PAIR_ZC"))  // experiments
+    if (*e) return std::max(1, std::min(std::atoi(e), std::min(g.nzl, kMaxZc)));
   const long long tiles = (long long)((g.n0 + kPairTX - 1) / kPairTX) * ((g.n1 + kPairTY - 1) / kPairTY);
-  int sms = 148, dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    sms = 148;
-  const long long want = (long long)(1.7 * sms * (first ? 4 : 2));
-  for (int zc = 48; zc >= 4; --zc)
-    if (tiles * ((g.nzl + zc - 1) / zc) >= want) return zc > g.nzl ? g.nzl : zc;
-  return force ? (g.nzl < 16 ? g.nzl : 16) : 0;  // too few blocks: the caller keeps k_node_tma
+  const int slots = sm_count() * (first ? 4 : 2);
+  // fewer blocks than one wave of slots: k_node_tma's smaller tiles fill the GPU better
+  if (!force && tiles * ((g.nzl + 3) / 4) < slots) return 0;
+  return zc_model(g.nzl, tiles, slots, 3.75);
 }
 
 template <int F, int I>
