@@ -755,11 +755,11 @@ int tma_map_box3(emrkc_handle* h, const void* ptr, cuuint32_t bx, cuuint32_t by,
   return EMRKC_OK;
 }
 
-// Pair-per-thread node kernel (k_node_pair): 3-D whole-grid handles on the
-// TMA path with HH proper (no aux rows); EMRKC_PAIR=0 keeps k_node_tma.
+// Pair-per-thread node kernel (k_node_pair): 3-D handles (whole grid or
+// slab) on the TMA path with HH proper (no aux rows); EMRKC_PAIR=0 keeps
+// k_node_tma.
 bool use_pair(const emrkc_handle* h) {
-  return h->pair && h->fast && h->pipe == 3 && h->geom.dim == 3 && h->geom.naux == 0 &&
-         !h->partitioned && !h->level_hook;
+  return h->pair && h->fast && h->pipe == 3 && h->geom.dim == 3 && h->geom.naux == 0;
 }
 
 // Temporally blocked inner stages (k_vin_tb) apply: 3-D handle on the TMA
@@ -830,15 +830,16 @@ double* nbr_dghost(const emrkc_handle* h, int side, int par) {
   return nullptr;
 }
 
-int tma_ghosts(emrkc_handle* h, const Halo& hl, CUtensorMap* lo, CUtensorMap* hi, int rmul = 1) {
+int tma_ghosts(emrkc_handle* h, const Halo& hl, CUtensorMap* lo, CUtensorMap* hi, int rmul = 1,
+               int xmul = 1) {
   std::memset(lo, 0, sizeof *lo);
   std::memset(hi, 0, sizeof *hi);
   if (hl.lo) {
-    const int rc = tma_map(h, hl.lo, kTmaGhost, lo, rmul);
+    const int rc = tma_map(h, hl.lo, kTmaGhost, lo, rmul, xmul);
     if (rc) return rc;
   }
   if (hl.hi) {
-    const int rc = tma_map(h, hl.hi, kTmaGhost, hi, rmul);
+    const int rc = tma_map(h, hl.hi, kTmaGhost, hi, rmul, xmul);
     if (rc) return rc;
   }
   return EMRKC_OK;
@@ -953,16 +954,27 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         return EMRKC_OK;
       }
       const int pzc = use_pair(h) ? emrkc_k::pair_zc(h->geom, j == 1, h->pair == 2) : 0;
+      Halo hn = hl;
+      if (h->pipe == 3 && h->partitioned && use_tb(h, pl)) {
+        // wide halo: K planes of d_1 into the neighbours' d_1 ghosts
+        const int par = static_cast<int>(h->kstage & 1);
+        hn.put_lo = hn.put_hi = nullptr;
+        hn.kput = pl.m - 1;
+        hn.kput_lo = hl.put_lo ? nbr_dghost(h, 0, par) : nullptr;
+        hn.kput_hi = hl.put_hi ? nbr_dghost(h, 1, par) : nullptr;
+        signals = emrkc_k::halo_signals_pipe(h->geom) * hn.kput;
+      }
       if (pzc > 0) {
-        // pair-per-thread node kernel (3-D whole grid, HH proper)
+        // pair-per-thread node kernel (3-D, HH proper)
         emrkc_k::TmaNode tm;
         std::memset(&tm, 0, sizeof tm);
         int rc = tma_map(h, f.g1, kTmaHalo, &tm.v, 1, emrkc_k::kPairXMul);
         if (!rc) rc = tma_map(h, f.g1, kTmaGates, &tm.gates, 1, emrkc_k::kPairXMul);
         if (!rc && f.g2) rc = tma_map(h, f.g2, kTmaAll, &tm.g2, 1, emrkc_k::kPairXMul);
+        if (!rc) rc = tma_ghosts(h, hl, &tm.glo, &tm.ghi, 1, emrkc_k::kPairXMul);
         if (rc) return rc;
         f.zc = pzc;
-        CK(h, emrkc_k::launch_node_pair(h->geom, f, tm, pl.m >= 2, lstream(h)));
+        CK(h, emrkc_k::launch_node_pair(h->geom, hn, f, tm, pl.m >= 2, lstream(h)));
       } else if (h->pipe == 3) {
         emrkc_k::TmaNode tm;
         int rc = tma_map(h, f.g1, kTmaHalo, &tm.v);
@@ -971,16 +983,6 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         if (!f.g2) std::memset(&tm.g2, 0, sizeof tm.g2);
         if (!rc) rc = tma_ghosts(h, hl, &tm.glo, &tm.ghi);
         if (rc) return rc;
-        Halo hn = hl;
-        if (h->partitioned && use_tb(h, pl)) {
-          // wide halo: K planes of d_1 into the neighbours' d_1 ghosts
-          const int par = static_cast<int>(h->kstage & 1);
-          hn.put_lo = hn.put_hi = nullptr;
-          hn.kput = pl.m - 1;
-          hn.kput_lo = hl.put_lo ? nbr_dghost(h, 0, par) : nullptr;
-          hn.kput_hi = hl.put_hi ? nbr_dghost(h, 1, par) : nullptr;
-          signals = emrkc_k::halo_signals_pipe(h->geom) * hn.kput;
-        }
         CK(h, emrkc_k::launch_node_tma(h->geom, hn, f, tm, pl.m >= 2, lstream(h)));
       } else if (h->pipe == 2)
         CK(h, emrkc_k::launch_node_persist(h->geom, hl, f, pl.m >= 2, lstream(h)));

@@ -312,12 +312,12 @@ cudaError_t launch_node_tma(const Geom& g, const Halo& h, const FastArgs& a,
                             const TmaNode& tm, bool ion, cudaStream_t st);
 // Pair-per-thread node kernel (3-D whole grids, HH proper): TMA boxes of
 // 64 x 4 tiles (tm.v: (68, 6, 1), tm.gates: (64, 4, 1, 3), tm.g2: (64, 4, 1,
-// 4); no ghost maps). pair_zc: its z-chunk, 0 if the grid gives too few
+// 4), ghost planes (68, 6)). pair_zc: its z-chunk, 0 if the grid gives too few
 // blocks (the caller keeps k_node_tma) unless forced (tests).
 constexpr int kPairXMul = 2;  // tile width in units of kTX3
 int pair_zc(const Geom& g, bool first, bool force);
-cudaError_t launch_node_pair(const Geom& g, const FastArgs& a, const TmaNode& tm, bool ion,
-                             cudaStream_t st);
+cudaError_t launch_node_pair(const Geom& g, const Halo& h, const FastArgs& a, const TmaNode& tm,
+                             bool ion, cudaStream_t st);
 // Rows per thread of the 3-D inner-stage kernel (its TMA boxes are
 // (TX+4) x (4 rows + 2) and TX x 4 rows, rows = vin_rows); 1 in 2-D.
 int vin_rows(const Geom& g);

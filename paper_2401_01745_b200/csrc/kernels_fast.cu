@@ -1521,7 +1521,7 @@ __device__ __forceinline__ unsigned nf_hi(double v) {
 
 template <int FIRST, int ION>
 __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
-    k_node_pair(const Geom g, const FastArgs a, const __grid_constant__ TmaNode tm) {
+    k_node_pair(const Geom g, const Halo h, const FastArgs a, const __grid_constant__ TmaNode tm) {
   constexpr int VS = kPairVS, CS = kPairCS, HXT = kPairHX;
   extern __shared__ __align__(128) double smem_tma[];
   double* vst = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;  // [kRV][VS]
@@ -1561,16 +1561,23 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
     tma_load_4d(gs0 + 8u * 3 * CS * sg, &tm.gates, bar, x0, y0, zz, 1);
     if (!FIRST) tma_load_4d(qs0 + 8u * 4 * CS * sg, &tm.g2, bar, x0, y0, zz, 0);
   };
-  // halo plane zb - 1 or ze (V only; mirrored at the grid faces)
+  // halo plane zb - 1 or ze (V only; mirror or ghost at the slab edge)
   auto issue_edge = [&](int zz, unsigned extra) {
     const int q = zz - zb + 1;
     const unsigned bar = b0 + 8u * (q & (kRV - 1));
     mbar_expect_tx(bar, vbytes + extra);
-    const int lz = zz < 0 ? 1 : (zz >= g.nzl ? g.nzl - 2 : zz);
-    tma_load_3d(v0 + 8u * VS * (q & (kRV - 1)), &tm.v, bar, x0 - 2, y0 - 1, lz);
+    tma_vplane<3>(g, &tm.v, &tm.glo, &tm.ghi, h.lo != nullptr, h.hi != nullptr,
+                  v0 + 8u * VS * (q & (kRV - 1)), bar, x0, y0, zz);
   };
+  // a block stands for its 32-wide tiles in the neighbours' arrival counts
+  // (halo_signals_pipe counts 32 x 4 tiles whatever kernel stores the planes)
+  const int sigw = 1 + (x0 + kTX3 < g.n0 ? 1 : 0);
   pdl_wait();
+  halo_wait(h, zb == 0, ze >= g.nzl);
   if (t == 0) {
+    // ghost planes arrived through generic peer stores (acquired in
+    // halo_wait); order them before this thread's async-proxy reads
+    fence_proxy_async();
     bulk_load(smem_u32(tab), kExp2Tab256, sizeof(double) * 256, b0);  // exp table
     issue_edge(zb - 1, sizeof(double) * 256);
     for (int i = 0; i < kTmaLA; ++i) {
@@ -1586,6 +1593,8 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
   if (skip != 0) {  // aborted earlier: drain the prologue copies
     const int np = 1 + min(kTmaLA, ze - zb) + (ze - zb < kTmaLA ? 1 : 0);
     for (int q = 0; q < np; ++q) mbar_wait(b0 + 8u * q, 0);
+    const PutPlan pq = put_plan(h, g.nzl);  // release the neighbours
+    halo_signal_w(h, sigw * max(0, min(ze, pq.zl) - zb), sigw * max(0, ze - max(zb, pq.zh)));
     return;
   }
   // cell 0 of the pair in a V stage; mirrored in-plane neighbours at the
@@ -1611,6 +1620,9 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
   // z window of the two columns: planes z - 1 and z
   double2 wm = *reinterpret_cast<const double2*>(vst + cell);
   double2 wc = *reinterpret_cast<const double2*>(vst + VS + cell);
+  // halo puts: planes z < pp.zl / z >= pp.zh of this column go to the
+  // neighbours' ghosts (one plane, or K planes of d_1 for the wide halo)
+  const PutPlan pp = put_plan(h, g.nzl);
   for (int z = zb; z < ze; ++z) {
     const int p = z - zb + 1;
     if (t == 0) {
@@ -1649,6 +1661,9 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
         *reinterpret_cast<double2*>(po) = make_double2(r0.o0, r1.o0);
         guard |= !(fabs(r0.o0) <= 1e6) || !(fabs(r1.o0) <= 1e6);  // also a non-finite V
       }
+      if (z < pp.zl) *reinterpret_cast<double2*>(pp.plo + ip + plane * z) = make_double2(r0.o0, r1.o0);
+      if (z >= pp.zh)
+        *reinterpret_cast<double2*>(pp.phi + ip + plane * (z - pp.zh)) = make_double2(r0.o0, r1.o0);
       nfacc = max(max(nfacc, max(nf_hi(r0.o0), nf_hi(r0.o1))), max(nf_hi(r0.o2), nf_hi(r0.o3)));
       nfacc = max(max(nfacc, max(nf_hi(r1.o0), nf_hi(r1.o1))), max(nf_hi(r1.o2), nf_hi(r1.o3)));
       if (a.last) {  // std::min / std::max per value (NaN skipped), select form
@@ -1674,7 +1689,6 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
   }
   bool bad = nfacc == 0xffffffffu;
   if (valid && slow_mask) {  // planes with a node outside the fast window: reference-order path
-    const Halo h0{};
     for (int c = 0; c < 2; ++c) {
       const long long ipc = ip + c;
       const Nbr<3> o = nbr_of<3>(g, Col<3>{cx + c, cy, ipc, zb, ze, true});
@@ -1684,8 +1698,8 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
         if (!(slow_mask >> (z - zb) & 1ull)) continue;
         const long long i = ipc + plane * z;
         const double vc = __ldg(G + i);
-        const double vm = zval(G, g, ipc, z - 1, nullptr, nullptr);
-        const double vp = zval(G, g, ipc, z + 1, nullptr, nullptr);
+        const double vm = zval(G, g, ipc, z - 1, h.lo, h.hi);
+        const double vp = zval(G, g, ipc, z + 1, h.lo, h.hi);
         const double xs = __ldg(G + i + o.xm) + __ldg(G + i + o.xp);
         const double ys = __ldg(G + i + o.ym) + __ldg(G + i + o.yp);
         const double stim = (stc && z >= zs0 && z <= zs1) ? a.stim : 0.0;
@@ -1715,16 +1729,17 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
           guard |= !(fabs(r.o0) <= 1e6);  // also a non-finite V
         }
         bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
+        if (z < pp.zl) pp.plo[ipc + plane * z] = r.o0;
+        if (z >= pp.zh) pp.phi[ipc + plane * (z - pp.zh)] = r.o0;
         if (a.last) {
           glo = fmin(glo, fmin(r.o1, fmin(r.o2, r.o3)));
           ghi = fmax(ghi, fmax(r.o1, fmax(r.o2, r.o3)));
         }
       }
     }
-    (void)h0;
   }
+  halo_signal_w(h, sigw * max(0, min(ze, pp.zl) - zb), sigw * max(0, ze - max(zb, pp.zh)));
   if (bad && !a.exex) {  // EXEX-RL never throws NumericalAbort
-    const Halo h0{};
     bool inner = false;
     for (int c = 0; c < 2; ++c) {
       Col<3> col;
@@ -1734,7 +1749,7 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
       col.z0 = zb;
       col.z1 = ze;
       col.valid = true;
-      inner |= inner_nonfinite<3>(g, h0, a.g1, col, nbr_of<3>(g, col), a.eta);
+      inner |= inner_nonfinite<3>(g, h, a.g1, col, nbr_of<3>(g, col), a.eta);
     }
     atomicMin(a.event, a.code_base + (unsigned long long)((a.j - 1) * (a.m + 1)) +
                            (inner ? 1 : a.m + 1));
@@ -3454,8 +3469,8 @@ int pair_zc(const Geom& g, bool first, bool force) {
 }
 
 template <int F, int I>
-static cudaError_t launch_node_pair_t(const Geom& g, const FastArgs& a, const TmaNode& tm,
-                                      cudaStream_t st) {
+static cudaError_t launch_node_pair_t(const Geom& g, const Halo& h, const FastArgs& a,
+                                      const TmaNode& tm, cudaStream_t st) {
   constexpr size_t smem = pair_smem_bytes<F>();
   static bool attr = false;
   if (!attr) {
@@ -3464,14 +3479,15 @@ static cudaError_t launch_node_pair_t(const Geom& g, const FastArgs& a, const Tm
   }
   const int chunks = (a.z_hi - a.z_lo + a.zc - 1) / a.zc;
   const dim3 grd((g.n0 + kPairTX - 1) / kPairTX, (g.n1 + kPairTY - 1) / kPairTY, chunks);
-  return launch_k(k_node_pair<F, I>, grd, dim3(kPairNT), smem, st, g, a, tm);
+  return launch_k(k_node_pair<F, I>, grd, dim3(kPairNT), smem, st, g, h, a, tm);
 }
 
-cudaError_t launch_node_pair(const Geom& g, const FastArgs& a, const TmaNode& tm, bool ion,
-                             cudaStream_t st) {
+cudaError_t launch_node_pair(const Geom& g, const Halo& h, const FastArgs& a, const TmaNode& tm,
+                             bool ion, cudaStream_t st) {
   const bool first = a.j == 1;
-  if (ion) return first ? launch_node_pair_t<1, 1>(g, a, tm, st) : launch_node_pair_t<0, 1>(g, a, tm, st);
-  return first ? launch_node_pair_t<1, 0>(g, a, tm, st) : launch_node_pair_t<0, 0>(g, a, tm, st);
+  if (ion)
+    return first ? launch_node_pair_t<1, 1>(g, h, a, tm, st) : launch_node_pair_t<0, 1>(g, h, a, tm, st);
+  return first ? launch_node_pair_t<1, 0>(g, h, a, tm, st) : launch_node_pair_t<0, 0>(g, h, a, tm, st);
 }
 
 template <int D, int L, int F>

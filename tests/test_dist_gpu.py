@@ -56,9 +56,15 @@ def gather(p, ops):
 TB_CASES = {"3d_tb_m3": (3, 1), "3d_tb_m5": (5, 1), "3d_tb_s2m4": (4, 2)}
 
 
+# *@pair: the pair-per-thread node kernel forced on these small grids
+# (EMRKC_PAIR=2; it is the default on large 3-D grids): ghost planes, halo
+# puts and arrival counts of k_node_pair on slabs
 @pytest.mark.parametrize("nslab", [2, 3, 4])
-@pytest.mark.parametrize("case", ["3d_m2", "2d_m1", "3d_m1", *TB_CASES])
+@pytest.mark.parametrize("case", ["3d_m2", "2d_m1", "3d_m1", *TB_CASES, "3d_m2@pair",
+                                  "3d_m1@pair", "3d_tb_m3@pair", "3d_tb_s2m4@pair"])
 def test_dist_protocol_bitwise(case, nslab, monkeypatch):
+    monkeypatch.setenv("EMRKC_PAIR", "2" if case.endswith("@pair") else "0")
+    case = case.split("@")[0]
     if case in TB_CASES:
         monkeypatch.setenv("EMRKC_TB", "1")  # the default
     if case == "3d_m2":
