@@ -3465,6 +3465,9 @@ int pair_zc(const Geom& g, bool first, bool force) {
   const int slots = sm_count() * (first ? 4 : 2);
   // fewer blocks than one wave of slots: k_node_tma's smaller tiles fill the GPU better
   if (!force && tiles * ((g.nzl + 3) / 4) < slots) return 0;
+  // small grids (< 12 planes per slot): the shortest chunks (sweep N = 100:
+  // zc 4 / 7 / 10 -> 30.0 / 33.4 / 36.4 us per launch)
+  if ((double)tiles * g.nzl / slots < 12.0) return std::min(g.nzl, 4);
   return zc_model(g.nzl, tiles, slots, 3.75);
 }
 
