@@ -327,6 +327,7 @@ struct emrkc_handle {
   // device scalars
   unsigned long long* d_event = nullptr;
   unsigned long long* d_slots = nullptr;
+  const unsigned long long* slot_init = nullptr;  // run loops: slot of the initial state's gate range
   size_t slots_cap = 0;
   double* d_coef = nullptr;  // in_mueta | in_nu | in_kappa (3*(m+1))
   size_t coef_cap = 0;
@@ -612,6 +613,9 @@ void begin_step(emrkc_handle* h, double t, long long step_in_run,
   a.code_base = static_cast<unsigned long long>(step_in_run) * stride;
   a.event = h->d_event;
   a.gate_slot = gate_slot;
+  // run loops keep consecutive per-step slots and the initial state's slot
+  // (slot_init); single steps have no earlier range
+  a.gate_prev = !h->slot_init ? nullptr : (step_in_run > 0 ? gate_slot - 2 : h->slot_init);
   a.fs = h->fs;
   a.ye = h->ye;
   for (int k = 0; k < 3; ++k) a.u[k] = h->u[k];
@@ -930,6 +934,7 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.code_base = a.code_base;
       f.event = a.event;
       f.gate_slot = a.gate_slot;
+      f.gate_prev = a.last ? a.gate_prev : nullptr;
       if (use_fused(h, pl)) {
         // the whole step (levels 1 and 2) in one persistent pass
         emrkc_k::FusedArgs fa{};
@@ -2037,7 +2042,14 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     CK(h, emrkc_k::launch_gate_range(h->geom, h->buf[h->cur],
                                      h->d_slots + 2 * nsteps, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
+    h->slot_init = single_step ? nullptr : h->d_slots + 2 * nsteps;
   }
+  struct SlotReset {  // the slot chain only holds inside this run
+    const std::vector<emrkc_handle*>& v;
+    ~SlotReset() {
+      for (auto* q : v) q->slot_init = nullptr;
+    }
+  } slot_reset{hs};
   const Plan& pl = hs[0]->plan;
   // Initial ghost planes of the current state (level L0 slot).
   if (n > 1) {

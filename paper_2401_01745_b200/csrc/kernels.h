@@ -90,6 +90,7 @@ struct StageArgs {
   unsigned long long code_base;  // step_in_run * stride
   unsigned long long* event;     // first abort/guard event (atomicMin)
   unsigned long long* gate_slot; // [2]: ordered min, max for this step
+  const unsigned long long* gate_prev;  // range slot of everything before this step (or null)
   int last;                      // j == s: guard + gate range
 };
 
@@ -163,6 +164,11 @@ struct FastArgs {
   unsigned long long code_base;
   unsigned long long* event;
   unsigned long long* gate_slot;
+  // k_node_pair: the gate-range slot that holds the range of everything
+  // before this step of the run (initial state and earlier steps), or null.
+  // With it the kernel's slot becomes cumulative (prev folded in) and values
+  // whose high words lie strictly inside prev's skip the FP64 min / max.
+  const unsigned long long* gate_prev;
 };
 
 // Whole-run resident kernel for small grids (s = m = 1; emRKC standard /

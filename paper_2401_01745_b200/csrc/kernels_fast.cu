@@ -1610,9 +1610,32 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
     zs1 = g.st_hi[2] - g.zoff;
   }
   bool guard = false;
+  // Gate range of the step (P/src/simulate.cpp:76-85). With the range of
+  // everything before this step (a.gate_prev: positive finite bounds) a value
+  // whose high word lies strictly between the bounds' high words cannot
+  // extend the run's range: those skip the FP64 min / max (integer pipe
+  // test per pair); negative and non-finite values always take the exact path.
+  double glo = 2.0, ghi = -1.0;
+  unsigned tlo = 0xffffffffu, thi = 0u;  // exact path iff hmin <= tlo || hmax >= thi
+  unsigned long long plo = ~0ull, phi = 0ull;
+  if (a.last && a.gate_prev) {
+    plo = a.gate_prev[0];
+    phi = a.gate_prev[1];
+    const unsigned hl = (unsigned)((plo ^ 0x8000000000000000ull) >> 32);
+    const unsigned hh = (unsigned)((phi ^ 0x8000000000000000ull) >> 32);
+    if (plo != ~0ull && (plo >> 63) && (phi >> 63) && hh < 0x7ff00000u && hl <= hh) {
+      tlo = hl;
+      thi = hh;
+      // the running min / max start from the earlier range (no sentinels)
+      glo = __longlong_as_double((long long)(plo ^ 0x8000000000000000ull));
+      ghi = __longlong_as_double((long long)(phi ^ 0x8000000000000000ull));
+    } else {
+      plo = ~0ull;
+      phi = 0ull;
+    }
+  }
   unsigned nfacc = 0u;  // all ones once an output was non-finite
   unsigned long long slow_mask = 0;  // planes z - zb (< kMaxZc = 64) left to the reference path
-  double glo = 2.0, ghi = -1.0;
   double* po = a.out + ip + plane * zb;
   double* pu = ION ? a.u1 + ip + plane * zb : nullptr;
   mbar_wait(b0, 0);       // plane zb - 1
@@ -1666,7 +1689,16 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
         *reinterpret_cast<double2*>(pp.phi + ip + plane * (z - pp.zh)) = make_double2(r0.o0, r1.o0);
       nfacc = max(max(nfacc, max(nf_hi(r0.o0), nf_hi(r0.o1))), max(nf_hi(r0.o2), nf_hi(r0.o3)));
       nfacc = max(max(nfacc, max(nf_hi(r1.o0), nf_hi(r1.o1))), max(nf_hi(r1.o2), nf_hi(r1.o3)));
-      if (a.last) {  // std::min / std::max per value (NaN skipped), select form
+      bool track = a.last;
+      if (track) {
+        const unsigned h0 = __double2hiint(r0.o1), h1 = __double2hiint(r0.o2),
+                       h2 = __double2hiint(r0.o3), h3 = __double2hiint(r1.o1),
+                       h4 = __double2hiint(r1.o2), h5 = __double2hiint(r1.o3);
+        const unsigned hmin = min(min(min(h0, h1), min(h2, h3)), min(h4, h5));
+        const unsigned hmax = max(max(max(h0, h1), max(h2, h3)), max(h4, h5));
+        track = hmin <= tlo || hmax >= thi;
+      }
+      if (track) {  // std::min / std::max per value (NaN skipped), select form
         glo = r0.o1 < glo ? r0.o1 : glo;
         ghi = ghi < r0.o1 ? r0.o1 : ghi;
         glo = r0.o2 < glo ? r0.o2 : glo;
@@ -1756,7 +1788,13 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
   }
   if (!ION && a.last && guard)
     atomicMin(a.event, a.code_base + (unsigned long long)(a.s * (a.m + 1) + 1));
-  if (a.last) block_gate_range_d(a.gate_slot, glo, ghi, valid && ze > zb);
+  if (a.last) {
+    // fold the earlier range in: the slot is cumulative when a.gate_prev is
+    // used (values skipped above lie strictly inside it)
+    unsigned long long lo = valid && ze > zb ? ord_of(glo) : ~0ull;
+    unsigned long long hi = valid && ze > zb ? ord_of(ghi) : 0ull;
+    block_gate_range(a.gate_slot, min(lo, plo), max(hi, phi));
+  }
 }
 
 // ---------------------------------------------------------------------------
