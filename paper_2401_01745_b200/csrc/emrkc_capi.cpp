@@ -926,6 +926,20 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
       f.cA = pl.mudt[j] * pl.inner.c[pl.m];
       // fast ionic path only where its range analysis holds (fast_math.cuh)
       fast_window(pl.eta, &f.vmid, &f.vfast);
+      {
+        const double vlo = f.vmid - f.vfast, vhi = f.vmid + f.vfast;
+        auto hiword = [](double x) {
+          uint64_t b = 0;
+          std::memcpy(&b, &x, sizeof b);
+          return static_cast<uint32_t>(b >> 32);
+        };
+        f.vq_pos = 0;
+        f.vq_neg = 0;
+        if (vlo < 0.0 && vhi > 0.0 && std::isfinite(vlo) && std::isfinite(vhi)) {
+          f.vq_pos = static_cast<int>(hiword(vhi));
+          f.vq_neg = 0x80000000u + hiword(-vlo);
+        }
+      }
       f.j = j;
       f.m = pl.m;
       f.s = pl.s;

@@ -169,6 +169,12 @@ struct FastArgs {
   // With it the kernel's slot becomes cumulative (prev folded in) and values
   // whose high words lie strictly inside prev's skip the FP64 min / max.
   const unsigned long long* gate_prev;
+  // k_node_pair: integer-pipe form of the window test on V's high word hi:
+  // (int)hi < vq_pos && (unsigned)hi < vq_neg implies vlo < V < vhi. Nodes
+  // that fail it (including the few inside the window but past the high-word
+  // bounds) take the per-node path, which applies the exact test.
+  int vq_pos;
+  unsigned vq_neg;
 };
 
 // Whole-run resident kernel for small grids (s = m = 1; emRKC standard /

@@ -1663,7 +1663,11 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
     const double2 za = *reinterpret_cast<const double2*>(G0);
     const double2 zb2 = *reinterpret_cast<const double2*>(G0 + CS);
     const double2 zc2 = *reinterpret_cast<const double2*>(G0 + 2 * CS);
-    const bool fast = fabs(wc.x - a.vmid) <= a.vfast && fabs(wc.y - a.vmid) <= a.vfast;
+    // window test on the integer pipe (conservative; the per-node path below
+    // applies the exact test to the planes it defers)
+    const int hx = __double2hiint(wc.x), hy = __double2hiint(wc.y);
+    const bool fast = hx < a.vq_pos && (unsigned)hx < a.vq_neg && hy < a.vq_pos &&
+                      (unsigned)hy < a.vq_neg;
     if (!fast) slow_mask |= 1ull << (z - zb);
     NodeOut r0 = node_update_s<3, FIRST, ION, 0>(g, a, tab, wm.x, wc.x, wp.x, xm0 + wc.y,
                                                  ym.x + yp.x, za.x, zb2.x, zc2.x, 0.0, Q0, CS);
