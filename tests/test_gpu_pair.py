@@ -98,3 +98,31 @@ def test_pair_events(oracle, monkeypatch):
     b = run(p, yn, 4, 0, monkeypatch, rF, rS)
     assert a[1]["abort_kind"] == capi.EMRKC_ABORT_NONFINITE and a[1] == b[1]
     assert np.array_equal(a[0], b[0], equal_nan=True)
+
+
+def test_pair_gate_range_irregular(oracle, monkeypatch):
+    """Gate range with values outside (0, 1): a negative gate in the initial
+    state disables the high-word prefilter (the earlier range is not
+    positive); a gate that turns negative during the run must reach the
+    exact path. Records (gate_min / gate_max) bitwise k_node_tma's, and the
+    oracle's to rounding level."""
+    n, h, rF, rS, _ = CASES["m1"]
+    p = grid(n, h)
+    nn, plane = p.n_nodes, n[0] * n[1]
+    for tweak in ("neg_initial", "neg_later", "big_later"):
+        y0 = state(oracle, p, 9, slow=False)
+        if tweak == "neg_initial":
+            y0[nn + plane * 3 + 17] = -0.02
+        elif tweak == "neg_later":
+            y0[3 * nn + plane * 8 + n[0] * 5 + 9] = 1e-7  # n gate: relaxes through tiny values
+            y0[plane * 8 + n[0] * 5 + 9] = -95.0
+        else:
+            y0[2 * nn + plane * 12 + n[0] * 3 + 30] = 1.5
+        a = run(p, y0, 6, 2, monkeypatch, rF, rS)
+        b = run(p, y0, 6, 0, monkeypatch, rF, rS)
+        assert a[1] == b[1], tweak
+        assert np.array_equal(a[0], b[0])
+        _, ro, _ = oracle.run(p, y0, 0, 6, 0.05, 0.05, rF, rS)
+        # against the oracle: rounding-level differences of the fast path only
+        assert a[1]["gate_min"] == pytest.approx(ro.gate_min, rel=1e-9, abs=1e-12), tweak
+        assert a[1]["gate_max"] == pytest.approx(ro.gate_max, rel=1e-9, abs=1e-12), tweak
