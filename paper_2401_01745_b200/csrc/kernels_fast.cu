@@ -3585,10 +3585,12 @@ cudaError_t launch_vin_tma(const Geom& g, const Halo& h, const FastInnerArgs& a,
     return first ? launch_vin_tma_r_t<1, 1, R>(g, h, a, tm, st)
                  : launch_vin_tma_r_t<1, 0, R>(g, h, a, tm, st);
   }
+#if EMRKC_VIN_R <= 1  // 3-D one row per thread: measured slower than k_vin_tma_r
   if (g.dim == 3) {
     if (!last) return launch_vin_tma_t<3, 0, 0>(g, h, a, tm, st);
     return first ? launch_vin_tma_t<3, 1, 1>(g, h, a, tm, st) : launch_vin_tma_t<3, 1, 0>(g, h, a, tm, st);
   }
+#endif
   if (!last) return launch_vin_tma_t<2, 0, 0>(g, h, a, tm, st);
   return first ? launch_vin_tma_t<2, 1, 1>(g, h, a, tm, st) : launch_vin_tma_t<2, 1, 0>(g, h, a, tm, st);
 }
