@@ -73,6 +73,8 @@ KERNEL_BYTES = {
     ("last", "outer"): 48,
     ("fused", "first_outer"): 64,  # k_fused2: g_0 in (4 fields), g_1 out (4); d_1 stays on chip
     ("fused_skip", None): 0,       # level 2 ran inside the fused launch
+    ("xstep", "first_outer"): 64,  # k_step_x: inner stage 2 of step n + node update of step n + 1
+    ("x_first", "first_outer"): 0,  # the node level as its own launch: first step of a run only
     ("zpipe", "first_outer"): 64,  # the whole z-pipelined step (node + inner chunks, 2 streams)
     ("zpipe_skip", None): 0,       # timed inside the step's event pair
 }
@@ -88,7 +90,10 @@ KERNEL_ROLES = {"m1": ("node", "m = 1: whole outer stage"),
                 "fused_skip": ("fused2", "level 2 ran inside the fused launch"),
                 "zpipe": ("zpipe", "s = 1: node-kernel z-chunks overlapped with the inner-stage "
                                    "chunks on a second stream (one event pair per step)"),
-                "zpipe_skip": ("zpipe", "timed with the step")}
+                "zpipe_skip": ("zpipe", "timed with the step"),
+                "xstep": ("xstep", "s = 1, m = 2: inner stage 2 of step n + ionic update and inner "
+                                   "stage 1 of step n + 1 in one launch (cross-step fusion)"),
+                "x_first": ("node", "m >= 2: ionic + inner stage 1 (first step of the run only)")}
 
 
 def kernel_name(kind: str, problem, node_kernel: int = 0) -> str:
@@ -103,6 +108,8 @@ def kernel_name(kind: str, problem, node_kernel: int = 0) -> str:
     role, what = KERNEL_ROLES[kind]
     if role == "fused2":
         return f"k_fused2 ({what})"
+    if role == "xstep":
+        return f"k_step_x ({what})"
     if role == "zpipe":
         return f"k_node_tma + k_vin_tma_r z-pipelined step ({what})"
     fam = {3: "tma", 1: "pipe", 2: "persist" if role == "node" else "pipe", 0: "fast"}[pipe]
@@ -129,6 +136,8 @@ def launch_kinds(s: int, m: int, problem=None, fused: int = 0):
         return [("fused", "first_outer"), ("fused_skip", None)]
     if fused == 2:
         return [("zpipe", "first_outer")] + [("zpipe_skip", None)] * (s * m - 1)
+    if fused == 3:
+        return [("x_first", "first_outer"), ("xstep", "first_outer")]
     out = []
     tb = problem is not None and tb_active(problem, m)
     for j in range(1, s + 1):
@@ -575,6 +584,8 @@ def gpu_launches_per_step(m) -> int:
         return 1
     if m["fused"] == 2:
         return int(os.environ.get("EMRKC_ZPIPE") or 0) * m["m"]  # read at handle creation
+    if m["fused"] == 3:
+        return 1  # k_step_x (plus one node launch and one inner-stage launch per run)
     return m["s"] * m["m"]
 
 

@@ -342,6 +342,7 @@ struct emrkc_handle {
   int tb = 1;      // temporally blocked inner stages 2..m in one pass (k_vin_tb,
                    // 3 <= m <= 5; EMRKC_TB=0: one kernel per stage)
   int pair = 1;    // pair-per-thread node kernel on 3-D whole grids (EMRKC_PAIR=0: k_node_tma)
+  int xstep = 0;   // cross-step fusion of the s = 1, m = 2 step in run loops (EMRKC_XSTEP=1)
   int stiff = 1;   // mRKC stiff-gate split: gates in the fast part (bit 0 = m)
   double* mr_u[3] = {nullptr, nullptr, nullptr};  // mRKC inner stages (4 blocks each)
   double* mr_fs = nullptr;                        // mRKC frozen slow term
@@ -849,6 +850,55 @@ int tma_ghosts(emrkc_handle* h, const Halo& hl, CUtensorMap* lo, CUtensorMap* hi
   return EMRKC_OK;
 }
 
+// FastArgs of the node level (inner stage 1) of outer stage j: pointers and
+// coefficients from the step context.
+void fill_node_args(emrkc_handle* h, const Plan& pl, const StageArgs& a, int j,
+                    emrkc_k::FastArgs* f) {
+  const double cG = pl.mudt[j] / pl.eta;
+  f->g1 = a.g1;
+  f->g2 = a.g2;
+  f->out = a.out;
+  f->fs = h->fs;
+  f->u1 = h->u[3];
+  f->eta = pl.eta;
+  f->stim = a.stim;
+  f->cG = cG * pl.gate_c;  // gate rows (progressive: c_m (y_E - z))
+  f->cV = cG * pl.in_mueta[1];
+  f->mue1 = pl.in_mueta[1];
+  f->exex = pl.exex;
+  f->z_lo = h->zr_lo >= 0 ? h->zr_lo : 0;  // plane range (pipelined host step)
+  f->z_hi = h->zr_lo >= 0 ? h->zr_hi : h->geom.nzl;
+  f->nu = a.nu;
+  f->kappa = a.kappa;
+  // aux rows (EMRKC_MODEL_HH_AUX): the inner iterate is z + c_m eta g_S
+  f->cA = pl.mudt[j] * pl.inner.c[pl.m];
+  // fast ionic path only where its range analysis holds (fast_math.cuh)
+  fast_window(pl.eta, &f->vmid, &f->vfast);
+  {
+    const double vlo = f->vmid - f->vfast, vhi = f->vmid + f->vfast;
+    auto hiword = [](double x) {
+      uint64_t b = 0;
+      std::memcpy(&b, &x, sizeof b);
+      return static_cast<uint32_t>(b >> 32);
+    };
+    f->vq_pos = 0;
+    f->vq_neg = 0;
+    if (vlo < 0.0 && vhi > 0.0 && std::isfinite(vlo) && std::isfinite(vhi)) {
+      f->vq_pos = static_cast<int>(hiword(vhi));
+      f->vq_neg = 0x80000000u + hiword(-vlo);
+    }
+  }
+  f->j = j;
+  f->m = pl.m;
+  f->s = pl.s;
+  f->last = a.last;
+  f->zc = h->zc;
+  f->code_base = a.code_base;
+  f->event = a.event;
+  f->gate_slot = a.gate_slot;
+  f->gate_prev = a.last ? a.gate_prev : nullptr;
+}
+
 // Launches inner stage k (1..m) of outer stage j (1..s).
 int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
   const Plan& pl = h->plan;
@@ -907,48 +957,7 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
     if (k == 2 && use_fused(h, pl)) return EMRKC_OK;  // ran inside the k == 1 launch
     if (k == 1) {
       emrkc_k::FastArgs f{};
-      f.g1 = a.g1;
-      f.g2 = a.g2;
-      f.out = a.out;
-      f.fs = h->fs;
-      f.u1 = h->u[3];
-      f.eta = pl.eta;
-      f.stim = a.stim;
-      f.cG = cG * pl.gate_c;  // gate rows (progressive: c_m (y_E - z))
-      f.cV = cG * pl.in_mueta[1];
-      f.mue1 = pl.in_mueta[1];
-      f.exex = pl.exex;
-      f.z_lo = h->zr_lo >= 0 ? h->zr_lo : 0;  // plane range (pipelined host step)
-      f.z_hi = h->zr_lo >= 0 ? h->zr_hi : h->geom.nzl;
-      f.nu = a.nu;
-      f.kappa = a.kappa;
-      // aux rows (EMRKC_MODEL_HH_AUX): the inner iterate is z + c_m eta g_S
-      f.cA = pl.mudt[j] * pl.inner.c[pl.m];
-      // fast ionic path only where its range analysis holds (fast_math.cuh)
-      fast_window(pl.eta, &f.vmid, &f.vfast);
-      {
-        const double vlo = f.vmid - f.vfast, vhi = f.vmid + f.vfast;
-        auto hiword = [](double x) {
-          uint64_t b = 0;
-          std::memcpy(&b, &x, sizeof b);
-          return static_cast<uint32_t>(b >> 32);
-        };
-        f.vq_pos = 0;
-        f.vq_neg = 0;
-        if (vlo < 0.0 && vhi > 0.0 && std::isfinite(vlo) && std::isfinite(vhi)) {
-          f.vq_pos = static_cast<int>(hiword(vhi));
-          f.vq_neg = 0x80000000u + hiword(-vlo);
-        }
-      }
-      f.j = j;
-      f.m = pl.m;
-      f.s = pl.s;
-      f.last = a.last;
-      f.zc = h->zc;
-      f.code_base = a.code_base;
-      f.event = a.event;
-      f.gate_slot = a.gate_slot;
-      f.gate_prev = a.last ? a.gate_prev : nullptr;
+      fill_node_args(h, pl, a, j, &f);
       if (use_fused(h, pl)) {
         // the whole step (levels 1 and 2) in one persistent pass
         emrkc_k::FusedArgs fa{};
@@ -1178,6 +1187,56 @@ int enqueue_step_zpipe(emrkc_handle* h, double t, long long step_in_run,
   return EMRKC_OK;
 }
 
+// Cross-step fusion (k_step_x, EMRKC_XSTEP=1): in a run loop of a 3-D whole
+// grid with s = 1, m = 2 (emRKC standard), inner stage 2 of step r and the
+// node update of step r + 1 run as one launch. The state needs three
+// buffers (y_r stays intact for the abort rollback while y_{r+1} and the
+// gates of y_{r+2} are written) and d_1 two (u[3] / u[0], swapped per launch).
+bool use_xstep(emrkc_handle* h, const Plan& pl, int64_t nsteps) {
+  return h->xstep && use_pair(h) && !h->partitioned && !h->level_hook && h->zr_lo < 0 &&
+         pl.s == 1 && pl.m == 2 && pl.method != kMethodMrkc && !pl.exex && pl.gate_c == 1.0 &&
+         nsteps >= 2 && !use_fused(h, pl) && !use_zpipe(h, pl) &&
+         emrkc_k::pair_zc(h->geom, true, h->pair == 2) > 0;
+}
+
+// c: step r (its node level is done, its inner stage 2 runs here); cn: step
+// r + 1 after begin_step (cn->in == c->w[0]).
+int launch_xstep(emrkc_handle* h, const StepCtx* c, StepCtx* cn) {
+  const Plan& pl = h->plan;
+  StageArgs& a = cn->a;
+  a.j = 1;
+  a.last = 1;
+  a.out = h->buf[cn->w[0]];
+  a.g1 = h->buf[cn->in];
+  a.g2 = nullptr;
+  a.mudt = pl.mudt[1];
+  a.nu = pl.outer.nu[1];
+  a.kappa = pl.outer.kappa[1];
+  a.stim = stim_rate_at(&h->p, cn->t);
+  emrkc_k::XArgs x{};
+  fill_node_args(h, pl, a, 1, &x.f);
+  x.f.u1 = h->u[0];  // d_1 of step r + 1 (u[3] holds step r's until the swap below)
+  x.f.zc = emrkc_k::pair_zc(h->geom, true, h->pair == 2);
+  x.vn = h->buf[c->in];
+  x.d1 = h->u[3];
+  x.vout = h->buf[c->w[0]];
+  x.inv_mue1 = 1.0 / pl.in_mueta[1];
+  x.mueta2 = pl.in_mueta[2];
+  x.nu2 = pl.inner.nu[2];
+  x.cG2 = pl.mudt[1] / pl.eta;
+  x.code_prev = c->a.code_base;
+  emrkc_k::TmaX tm;
+  std::memset(&tm, 0, sizeof tm);
+  int rc = tma_map_box3(h, h->u[3], emrkc_k::kTX3 * emrkc_k::kPairXMul + 4, emrkc_k::kTY3 + 4, 150,
+                        &tm.d1);
+  if (!rc) rc = tma_map(h, a.g1, kTmaGates, &tm.gates, 1, emrkc_k::kPairXMul);
+  if (rc) return rc;
+  CK(h, emrkc_k::launch_step_x(h->geom, x, tm, lstream(h)));
+  std::swap(h->u[3], h->u[0]);
+  h->level += 2;
+  return EMRKC_OK;
+}
+
 int enqueue_step(emrkc_handle* h, double t, long long step_in_run,
                  unsigned long long* gate_slot, int* out_idx) {
   if (use_zpipe(h, h->plan)) return enqueue_step_zpipe(h, t, step_in_run, gate_slot, out_idx);
@@ -1269,6 +1328,8 @@ int init_handle(emrkc_handle* h) {
   if (h->pipe != 3) h->zc = std::min(h->zc, emrkc_k::kMaxZcPipe);
   if (const char* tb = std::getenv("EMRKC_TB"))
     if (*tb) h->tb = std::atoi(tb) != 0;
+  if (const char* xs = std::getenv("EMRKC_XSTEP"))
+    if (*xs) h->xstep = std::atoi(xs) != 0;
   if (const char* pr = std::getenv("EMRKC_PAIR"))
     if (*pr) h->pair = std::max(0, std::min(2, std::atoi(pr)));  // 2: also on small grids (tests)
   if (const char* fu = std::getenv("EMRKC_FUSED"))
@@ -2140,9 +2201,13 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     tev.resize(2 * nsteps * per);
     for (auto& e : tev) CK(h, cudaEventCreate(&e));
     int64_t li = 0;
+    const bool xs = use_xstep(h, pl, nsteps);
+    StepCtx xc;
+    if (xs && (rc = ensure_buffers(h, 3))) return rc;
     for (int64_t r = 0; r < nsteps; ++r) {
       const double t = static_cast<double>(step0 + r) * dt;
-      in_idx[0][r] = h->cur;
+      if (!xs || r == 0) in_idx[0][r] = h->cur;
+      if (xs && r + 1 < nsteps) in_idx[0][r + 1] = (h->cur + 1) % h->nbuf;
       if (scratch) {
         CK(h, cudaMemsetAsync(scratch, static_cast<int>(r & 0xff), flush_bytes, h->stream));
         CK(h, emrkc_k::launch_norm2_partial(static_cast<const double*>(scratch_rd),
@@ -2162,6 +2227,36 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
         }
         li += per;
         h->cur = outi;
+        continue;
+      }
+      if (xs) {
+        // entry 2r: the node level (a launch of its own only for r = 0),
+        // entry 2r + 1: inner(r) fused with node(r + 1), or inner(r) alone
+        // for the last step
+        if (r == 0) {
+          begin_step(h, t, 0, h->d_slots, &xc);
+          CK(h, cudaEventRecord(tev[0], h->stream));
+          if ((rc = launch_level(h, &xc, 1, 1))) return rc;
+          CK(h, cudaEventRecord(tev[1], h->stream));
+        } else {
+          CK(h, cudaEventRecord(tev[2 * li], h->stream));
+          CK(h, cudaEventRecord(tev[2 * li + 1], h->stream));
+        }
+        ++li;
+        CK(h, cudaEventRecord(tev[2 * li], h->stream));
+        if (r + 1 < nsteps) {
+          h->cur = end_step(h, &xc);
+          StepCtx cn;
+          begin_step(h, static_cast<double>(step0 + r + 1) * dt, r + 1,
+                     h->d_slots + 2 * (r + 1), &cn);
+          if ((rc = launch_xstep(h, &xc, &cn))) return rc;
+          xc = cn;
+        } else {
+          if ((rc = launch_level(h, &xc, 1, 2))) return rc;
+          h->cur = end_step(h, &xc);
+        }
+        CK(h, cudaEventRecord(tev[2 * li + 1], h->stream));
+        ++li;
         continue;
       }
       StepCtx c;
@@ -2192,6 +2287,27 @@ int run_slabs(const std::vector<emrkc_handle*>& hs, int64_t step0,
     emrkc_handle* h = hs[0];
     for (int64_t r = 0; r < nsteps; ++r) in_idx[0][r] = resident_out;  // rollback is in-kernel
     h->cur = resident_out;
+  } else if (n == 1 && use_xstep(hs[0], pl, nsteps)) {
+    // node(0), then inner(r) + node(r + 1) per launch, then inner(nsteps - 1)
+    emrkc_handle* h = hs[0];
+    if ((rc = ensure_buffers(h, 3))) return rc;
+    StepCtx c, cn;
+    in_idx[0][0] = h->cur;
+    begin_step(h, static_cast<double>(step0) * dt, 0, h->d_slots, &c);
+    if ((rc = launch_level(h, &c, 1, 1))) return rc;
+    for (int64_t r = 0; r < nsteps; ++r) {
+      if (r + 1 < nsteps) {
+        h->cur = end_step(h, &c);
+        in_idx[0][r + 1] = h->cur;
+        begin_step(h, static_cast<double>(step0 + r + 1) * dt, r + 1, h->d_slots + 2 * (r + 1),
+                   &cn);
+        if ((rc = launch_xstep(h, &c, &cn))) return rc;
+        c = cn;
+      } else {
+        if ((rc = launch_level(h, &c, 1, 2))) return rc;
+        h->cur = end_step(h, &c);
+      }
+    }
   } else if (n == 1) {
     emrkc_handle* h = hs[0];
     for (int64_t r = 0; r < nsteps; ++r) {
@@ -3160,7 +3276,8 @@ int32_t emrkc_node_kernel(emrkc_handle* h) {
 int32_t emrkc_fused_active(emrkc_handle* h) {
   if (!h || !h->plan_uploaded) return 0;
   if (use_fused(h, h->plan)) return 1;
-  return use_zpipe(h, h->plan) ? 2 : 0;
+  if (use_zpipe(h, h->plan)) return 2;
+  return use_xstep(h, h->plan, 2) ? 3 : 0;
 }
 
 // ---------------------------------------------------------------------------

@@ -330,6 +330,22 @@ constexpr int kPairXMul = 2;  // tile width in units of kTX3
 int pair_zc(const Geom& g, bool first, bool force);
 cudaError_t launch_node_pair(const Geom& g, const Halo& h, const FastArgs& a, const TmaNode& tm,
                              bool ion, cudaStream_t st);
+// Cross-step fusion of the s = 1, m = 2 step (k_step_x, EMRKC_XSTEP=1): inner
+// stage 2 of step n and the node update of step n + 1 in one launch.
+struct XArgs {
+  FastArgs f;           // update of step n + 1 (j = 1, ION): g1 = y_{n+1}'s buffer (its gate
+                        // fields are final), out = y_{n+2}'s buffer, u1 = d_1 of step n + 1
+  const double* vn;     // V of y_n
+  const double* d1;     // d_1 of step n
+  double* vout;         // V of y_{n+1} (field 0 of f.g1's buffer)
+  double inv_mue1, mueta2, nu2, cG2;  // 1/(mu'_1 eta), mu'_2 eta, nu'_2, mu_1 dt / eta
+  unsigned long long code_prev;       // abort-code base of step n
+};
+struct TmaX {
+  CUtensorMap d1;     // d_1 of step n, box (68, 8, 1) at (x0 - 2, y0 - 2)
+  CUtensorMap gates;  // fields of y_{n+1}'s buffer, box (64, 4, 1, 3) from field 1
+};
+cudaError_t launch_step_x(const Geom& g, const XArgs& a, const TmaX& tm, cudaStream_t st);
 // Rows per thread of the 3-D inner-stage kernel (its TMA boxes are
 // (TX+4) x (4 rows + 2) and TX x 4 rows, rows = vin_rows); 1 in 2-D.
 int vin_rows(const Geom& g);

@@ -1802,6 +1802,414 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
 }
 
 // ---------------------------------------------------------------------------
+// k_step_x: cross-step fusion of the s = 1, m = 2 step (EMRKC_XSTEP=1, 3-D
+// whole grids, HH proper). One launch does inner stage 2 of step n AND the
+// node update (exponential Euler + inner stage 1) of step n + 1:
+//   W = V_{n+1} = V_n + cG d_2,  d_2 = nu'_2 d_1 + mu'_2 eta (d_1 / (mu'_1 eta) + f_F(d_1))
+// is a 12-flop stencil of the complete fields d_1^n and V_n, so a block
+// computes it on its 64 x 4 tile plus a one-cell halo (the halo twice, by the
+// neighbouring blocks too: no exchange between blocks) straight into a
+// shared-memory plane, and k_node_pair's update of step n + 1 reads V from
+// there instead of from HBM. Per node the step moves 80 B instead of 88 B
+// and runs one kernel instead of two (V_{n+1} is never re-read, d_1 is read
+// once, with its halo, from L2).
+// March: iteration w produces W(w) (planes max(zb - 1, 0) .. min(ze, nz - 1);
+// the chunk's own planes go to global memory) and then updates the nodes of
+// plane z = w - 1 from W(z - 1), W(z), W(z + 1) (the thread's own column
+// window) and the in-plane neighbours of W(z) published one iteration
+// earlier (double-buffered plane, one __syncthreads per iteration).
+// Arithmetic and order are k_vin_tma_r's (producer) and k_node_pair's
+// (update): bitwise equal to the two-kernel step (tests/test_gpu_xstep.py).
+// ---------------------------------------------------------------------------
+constexpr int kXDX = kPairTX + 4, kXDY = kPairTY + 4;   // d_1 box 68 x 8 (x0 - 2, y0 - 2)
+constexpr int kXDT = kXDX * kXDY;
+constexpr int kXDS = (kXDT + 15) & ~15;
+constexpr int kXRD = 8;                                  // d_1 ring planes
+constexpr int kXLA = 3;                                  // groups in flight ahead
+constexpr int kXWS = kPairVS;                            // W plane (68 x 6)
+constexpr size_t xstep_smem_bytes() {
+  return sizeof(double) * (kXRD * kXDS + 2 * kXWS + kRG * 3 * kPairCS) + 128;
+}
+
+// A pair of x-adjacent cells of the producer: indices in a d_1 plane (cell 0
+// and its mirrored in-plane neighbours), offset of cell 0 in a global plane.
+struct XPairIdx {
+  int c, xm, xp, ym, yp;
+  long long gi;
+  bool on;  // inside the grid
+};
+__device__ __forceinline__ XPairIdx x_pair_idx(const Geom& g, int x0, int y0, int row, int pr) {
+  // row 0..5 of the W plane (gy = y0 - 1 + row), pair 0..33 (gx = x0 - 2 + 2 pr)
+  XPairIdx q;
+  const int gx = x0 - 2 + 2 * pr, gy = y0 - 1 + row;
+  q.on = gx >= 0 && gx < g.n0 && gy >= 0 && gy < g.n1;
+  q.c = (row + 1) * kXDX + 2 * pr;
+  q.xm = q.c + ((gx > 0 && pr > 0) ? -1 : 1);
+  q.xp = q.c + 1 + ((gx + 1 < g.n0 - 1 && pr < 33) ? 1 : -1);
+  q.ym = q.c + (gy > 0 ? -kXDX : kXDX);
+  q.yp = q.c + (gy < g.n1 - 1 ? kXDX : -kXDX);
+  q.gi = (long long)gx + (long long)g.n0 * gy;
+  return q;
+}
+
+// W of a pair at plane w from the d_1 planes (lower, centre, upper of the
+// pair's column; in-plane neighbours from the centre plane DC) and V_n.
+__device__ __forceinline__ void x_produce(const Geom& g, const XArgs& a, const double* DC,
+                                          const XPairIdx& q, double2 dm, double2 dc, double2 dp,
+                                          double2 vn, double2& dk, double2& o) {
+  const double2 ym = *reinterpret_cast<const double2*>(DC + q.ym);
+  const double2 yp = *reinterpret_cast<const double2*>(DC + q.yp);
+  const double xm0 = DC[q.xm], xp1 = DC[q.xp];
+  double L0 = fma(g.wc, dc.x, g.w[2] * (dm.x + dp.x));
+  double L1 = fma(g.wc, dc.y, g.w[2] * (dm.y + dp.y));
+  L0 = fma(g.w[0], xm0 + dc.y, L0);
+  L1 = fma(g.w[0], dc.x + xp1, L1);
+  L0 = fma(g.w[1], ym.x + yp.x, L0);
+  L1 = fma(g.w[1], ym.y + yp.y, L1);
+  dk.x = fma(a.mueta2, fma(dc.x, a.inv_mue1, L0), a.nu2 * dc.x);
+  dk.y = fma(a.mueta2, fma(dc.y, a.inv_mue1, L1), a.nu2 * dc.y);
+  o.x = fma(a.cG2, dk.x, vn.x);
+  o.y = fma(a.cG2, dk.y, vn.y);
+}
+
+// V_{n+1} at in-plane offset j of plane zz, from the complete fields d_1^n
+// and V_n (rare paths: deferred planes, abort ordinal).
+__device__ __noinline__ double x_w_at(const Geom& g, const XArgs& a, long long j, int zz) {
+  const int nz = g.nzl;
+  const double* Dn = a.d1;
+  const int gx = (int)(j % g.n0), gy = (int)(j / g.n0);
+  const long long xm = gx > 0 ? -1 : 1, xp = gx < g.n0 - 1 ? 1 : -1;
+  const long long ym = gy > 0 ? -(long long)g.n0 : (long long)g.n0;
+  const long long yp = gy < g.n1 - 1 ? (long long)g.n0 : -(long long)g.n0;
+  const int zm = zz > 0 ? zz - 1 : 1, zp = zz < nz - 1 ? zz + 1 : nz - 2;
+  const long long k0 = j + g.plane * zz;
+  const double dcv = __ldg(Dn + k0);
+  double L = fma(g.wc, dcv, g.w[2] * (__ldg(Dn + j + g.plane * zm) + __ldg(Dn + j + g.plane * zp)));
+  L = fma(g.w[0], __ldg(Dn + k0 + xm) + __ldg(Dn + k0 + xp), L);
+  L = fma(g.w[1], __ldg(Dn + k0 + ym) + __ldg(Dn + k0 + yp), L);
+  const double dkv = fma(a.mueta2, fma(dcv, a.inv_mue1, L), a.nu2 * dcv);
+  return fma(a.cG2, dkv, __ldg(a.vn + k0));
+}
+// Stencil inputs of the update at column offset j, plane z.
+struct XStencil {
+  double vm, vc, vp, xs, ys;
+};
+__device__ __forceinline__ XStencil x_stencil(const Geom& g, const XArgs& a, long long j, int z) {
+  const int nz = g.nzl;
+  const int gx = (int)(j % g.n0), gy = (int)(j / g.n0);
+  const long long xm = gx > 0 ? -1 : 1, xp = gx < g.n0 - 1 ? 1 : -1;
+  const long long ym = gy > 0 ? -(long long)g.n0 : (long long)g.n0;
+  const long long yp = gy < g.n1 - 1 ? (long long)g.n0 : -(long long)g.n0;
+  XStencil s;
+  s.vc = x_w_at(g, a, j, z);
+  s.vm = x_w_at(g, a, j, z > 0 ? z - 1 : 1);
+  s.vp = x_w_at(g, a, j, z < nz - 1 ? z + 1 : nz - 2);
+  s.xs = x_w_at(g, a, j + xm, z) + x_w_at(g, a, j + xp, z);
+  s.ys = x_w_at(g, a, j + ym, z) + x_w_at(g, a, j + yp, z);
+  return s;
+}
+// inner_nonfinite of a column (P/src/cheb.cpp:73-80, multirate.cpp:100-104)
+// with V of y_{n+1} recomputed (other blocks may still be writing theirs).
+__device__ __noinline__ bool x_inner_nonfinite(const Geom& g, const XArgs& a, long long j, int z0,
+                                               int z1) {
+  bool inner = false;
+  const double* G = a.f.g1;
+  for (int z = z0; z < z1; ++z) {
+    const XStencil s = x_stencil(g, a, j, z);
+    double D = fma(g.wc, s.vc, g.w[2] * (s.vm + s.vp));
+    D = fma(g.w[0], s.xs, D);
+    D = fma(g.w[1], s.ys, D);
+    const long long i = j + g.plane * z;
+    const double q0 = __ldg(G + g.nn + i), q1 = __ldg(G + 2 * g.nn + i), q2 = __ldg(G + 3 * g.nn + i);
+    const Dgate d = hh_expeuler_ref(s.vc, q0, q1, q2, a.f.eta);
+    const double y0 = q0 + d.d0, y1 = q1 + d.d1, y2 = q2 + d.d2;
+    const double fs = -current_fast(s.vc, y0, y1, y2) * g.inv_Cm;
+    inner |= !(finite_hi(D + fs) && finite_hi(y0) && finite_hi(y1) && finite_hi(y2));
+  }
+  return inner;
+}
+
+__global__ void __launch_bounds__(kPairNT, 3)
+    k_step_x(const Geom g, const XArgs a, const __grid_constant__ TmaX tm) {
+  constexpr int CS = kPairCS, HXT = kPairHX;
+  const FastArgs& f = a.f;
+  extern __shared__ __align__(128) double smem_tma[];
+  double* dst = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;  // [kXRD][kXDS]
+  double* wst = dst + kXRD * kXDS;   // [2][kXWS]
+  double* gst = wst + 2 * kXWS;      // [kRG][3][CS]
+  __shared__ double tab[256];
+  __shared__ __align__(8) unsigned long long bars[8];
+  __shared__ int skip;
+  const int t = threadIdx.x;
+  const int nz = g.nzl;
+  const int zb = blockIdx.z * f.zc;
+  const int ze = min(nz, zb + f.zc);
+  pdl_launch_dependents();
+  if (t == 0) {
+    for (int s = 0; s < 8; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    mbar_fence_init();
+    prefetch_tensormap(&tm.d1);
+    prefetch_tensormap(&tm.gates);
+  }
+  __syncthreads();
+  const int px = t & 31, ty = t >> 5;
+  const int x0 = blockIdx.x * kPairTX, y0 = blockIdx.y * kPairTY;
+  const int cx = x0 + 2 * px, cy = y0 + ty;
+  const bool valid = cx < g.n0 && cy < g.n1;
+  const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
+  const long long nn = g.nn, plane = g.plane;
+  const unsigned d0 = smem_u32(dst), gs0 = smem_u32(gst), b0 = smem_u32(bars);
+  const int w0 = zb > 0 ? zb - 1 : 0;          // first W plane produced
+  const int w1 = min(ze, nz - 1);              // last W plane produced
+  const int pbase = w0 - 1;                    // d_1 ring: slot (p - pbase) & 7
+  auto dslot = [&](int p) { return (p - pbase) & (kXRD - 1); };
+  // group of iteration w: d_1 of plane w + 1 (the producer's upper plane) and
+  // the gates of plane w - 1 (the update's plane)
+  auto group_bytes = [&](int w) {
+    unsigned b = 0;
+    if (w <= w1 && w + 1 <= nz - 1) b += 8u * kXDT;
+    if (w - 1 >= zb && w - 1 < ze) b += 8u * 3 * CS;
+    return b;
+  };
+  auto issue_group = [&](int w, unsigned extra) {  // thread 0
+    const unsigned bar = b0 + 8u * ((w - w0) & 7);
+    mbar_expect_tx(bar, group_bytes(w) + extra);
+    if (w <= w1 && w + 1 <= nz - 1)
+      tma_load_3d(d0 + 8u * kXDS * dslot(w + 1), &tm.d1, bar, x0 - 2, y0 - 2, w + 1);
+    if (w - 1 >= zb && w - 1 < ze)
+      tma_load_4d(gs0 + 8u * 3 * CS * ((w - 1 - zb) & (kRG - 1)), &tm.gates, bar, x0, y0, w - 1, 1);
+  };
+  pdl_wait();
+  if (t == 0) {
+    // first group: also d_1 of planes w0 - 1 (if any) and w0, and the exp table
+    unsigned extra = sizeof(double) * 256 + 8u * kXDT + (w0 >= 1 ? 8u * kXDT : 0u);
+    issue_group(w0, extra);
+    const unsigned bar = b0;
+    bulk_load(smem_u32(tab), kExp2Tab256, sizeof(double) * 256, bar);
+    tma_load_3d(d0 + 8u * kXDS * dslot(w0), &tm.d1, bar, x0 - 2, y0 - 2, w0);
+    if (w0 >= 1) tma_load_3d(d0 + 8u * kXDS * dslot(w0 - 1), &tm.d1, bar, x0 - 2, y0 - 2, w0 - 1);
+    for (int i = 1; i < kXLA && w0 + i <= ze; ++i) issue_group(w0 + i, 0);
+  }
+  if (t == 32) skip = (*(volatile const unsigned long long*)f.event) < a.code_prev + 2;
+  __syncthreads();
+  if (skip != 0) {  // an earlier step aborted: drain the prologue copies
+    for (int i = 0; i < kXLA && w0 + i <= ze; ++i) mbar_wait(b0 + 8u * i, 0);
+    return;
+  }
+  // producer pairs: the thread's own (interior) pair, row ty + 1, pair px + 1;
+  // threads 0..75 also take one pair of the one-cell halo ring
+  const XPairIdx qi = x_pair_idx(g, x0, y0, ty + 1, px + 1);
+  XPairIdx qe;
+  qe.on = false;
+  if (t < 76) {
+    const int row = t < 34 ? 0 : (t < 68 ? 5 : 1 + ((t - 68) >> 1));
+    const int pr = t < 34 ? t : (t < 68 ? t - 34 : (((t - 68) & 1) ? 33 : 0));
+    qe = x_pair_idx(g, x0, y0, row, pr);
+  }
+  // update: cell 0 of the pair in a W plane and its mirrored neighbours
+  const int cell = (ty + 1) * HXT + 2 * px + 2;
+  const int cxm = cell + (cx > 0 ? -1 : 1), cxp = cell + 1 + (cx + 1 < g.n0 - 1 ? 1 : -1);
+  const int cym = cell + (cy > 0 ? -HXT : HXT), cyp = cell + (cy < g.n1 - 1 ? HXT : -HXT);
+  const int gcell = ty * kPairTX + 2 * px;
+  int zs0 = 1, zs1 = 0;
+  const bool st0 = valid && stim_col_xy<3>(g, cx, cy), st1 = valid && stim_col_xy<3>(g, cx + 1, cy);
+  if (st0 || st1) {
+    zs0 = g.st_lo[2] - g.zoff;
+    zs1 = g.st_hi[2] - g.zoff;
+  }
+  // step n (producer) events; step n + 1 (update) events and gate range
+  bool p_bad_in = false, p_bad_out = false, p_guard = false;
+  double glo = 2.0, ghi = -1.0;
+  unsigned tlo = 0xffffffffu, thi = 0u;
+  unsigned long long plo = ~0ull, phi = 0ull;
+  if (f.last && f.gate_prev) {
+    plo = f.gate_prev[0];
+    phi = f.gate_prev[1];
+    const unsigned hl = (unsigned)((plo ^ 0x8000000000000000ull) >> 32);
+    const unsigned hh = (unsigned)((phi ^ 0x8000000000000000ull) >> 32);
+    if (plo != ~0ull && (plo >> 63) && (phi >> 63) && hh < 0x7ff00000u && hl <= hh) {
+      tlo = hl;
+      thi = hh;
+      glo = __longlong_as_double((long long)(plo ^ 0x8000000000000000ull));
+      ghi = __longlong_as_double((long long)(phi ^ 0x8000000000000000ull));
+    } else {
+      plo = ~0ull;
+      phi = 0ull;
+    }
+  }
+  unsigned nfacc = 0u;
+  unsigned long long slow_mask = 0;
+  mbar_wait(b0, 0);  // d_1 of w0 - 1, w0, w0 + 1, gates of w0 - 1, table
+  // d_1 window of the own pair: planes w - 1, w (w = w0)
+  double2 dm = make_double2(0.0, 0.0), dc;
+  if (w0 >= 1) dm = *reinterpret_cast<const double2*>(dst + dslot(w0 - 1) * kXDS + qi.c);
+  dc = *reinterpret_cast<const double2*>(dst + dslot(w0) * kXDS + qi.c);
+  double2 wm = make_double2(0.0, 0.0), wc = make_double2(0.0, 0.0);  // W(z - 1), W(z)
+  double* po = f.out + ip + plane * zb;   // gates of y_{n+2}
+  double* pu = f.u1 + ip + plane * zb;    // d_1 of step n + 1
+  // V_n of the pairs one plane ahead (global loads, a whole iteration of latency)
+  const double2 zero2 = make_double2(0.0, 0.0);
+  double2 vn = valid ? __ldg(reinterpret_cast<const double2*>(a.vn + ip + plane * w0)) : zero2;
+  double2 ev = (qe.on && w0 >= zb) ? __ldg(reinterpret_cast<const double2*>(a.vn + qe.gi + plane * w0)) : zero2;
+  for (int w = w0; w <= ze; ++w) {
+    const int it = w - w0;
+    if (t == 0 && w + kXLA <= ze) issue_group(w + kXLA, 0);
+    double2 vn_next = zero2, ev_next = zero2;
+    if (w + 1 <= w1) {
+      if (valid) vn_next = __ldg(reinterpret_cast<const double2*>(a.vn + ip + plane * (w + 1)));
+      if (qe.on && w + 1 >= zb && w + 1 < ze)
+        ev_next = __ldg(reinterpret_cast<const double2*>(a.vn + qe.gi + plane * (w + 1)));
+    }
+    if (it > 0) mbar_wait(b0 + 8u * (it & 7), (it >> 3) & 1);
+    // ---- producer: W(w) ----
+    double2 wp = make_double2(0.0, 0.0);
+    if (w <= w1) {
+      const double* DC = dst + dslot(w) * kXDS;
+      double2 dp;
+      if (w + 1 <= nz - 1) dp = *reinterpret_cast<const double2*>(dst + dslot(w + 1) * kXDS + qi.c);
+      else dp = dm;              // mirror at the top face
+      if (w == 0) dm = dp;       // mirror at the bottom face
+      const bool ownp = w >= zb && w < ze;
+      double2 dk;
+      x_produce(g, a, DC, qi, dm, dc, dp, vn, dk, wp);
+      *reinterpret_cast<double2*>(wst + (w & 1) * kXWS + qi.c - kXDX) = wp;
+      if (ownp && valid) {
+        *reinterpret_cast<double2*>(a.vout + ip + plane * w) = wp;
+        p_bad_in |= !finite_hi(dk.x) || !finite_hi(dk.y);
+        p_bad_out |= !finite_hi(wp.x) || !finite_hi(wp.y);
+        p_guard |= !(fabs(wp.x) <= 1e6) || !(fabs(wp.y) <= 1e6);
+      }
+      dm = dc;
+      dc = dp;
+      if (ownp && qe.on) {  // the halo ring of the chunk's own planes
+        const double* DM = dst + dslot(w == 0 ? 1 : w - 1) * kXDS;
+        const double* DP = dst + dslot(w + 1 <= nz - 1 ? w + 1 : w - 1) * kXDS;
+        const double2 em = *reinterpret_cast<const double2*>(DM + qe.c);
+        const double2 ec = *reinterpret_cast<const double2*>(DC + qe.c);
+        const double2 ep = *reinterpret_cast<const double2*>(DP + qe.c);
+        double2 ek, eo;
+        x_produce(g, a, DC, qe, em, ec, ep, ev, ek, eo);
+        *reinterpret_cast<double2*>(wst + (w & 1) * kXWS + qe.c - kXDX) = eo;
+      }
+    }
+    // ---- update of step n + 1: plane z = w - 1 ----
+    const int z = w - 1;
+    if (z >= zb) {
+      double2 um = wm, up = wp;
+      if (z == 0) um = wp;         // mirror at the bottom face
+      if (z == nz - 1) up = wm;    // mirror at the top face
+      const double* V0 = wst + (z & 1) * kXWS;
+      const double2 ym = *reinterpret_cast<const double2*>(V0 + cym);
+      const double2 yp = *reinterpret_cast<const double2*>(V0 + cyp);
+      const double xm0 = V0[cxm], xp1 = V0[cxp];
+      const double* G0 = gst + ((z - zb) & (kRG - 1)) * 3 * CS + gcell;
+      const double2 za = *reinterpret_cast<const double2*>(G0);
+      const double2 zb2 = *reinterpret_cast<const double2*>(G0 + CS);
+      const double2 zc2 = *reinterpret_cast<const double2*>(G0 + 2 * CS);
+      const int hx = __double2hiint(wc.x), hy = __double2hiint(wc.y);
+      const bool fast = hx < f.vq_pos && (unsigned)hx < f.vq_neg && hy < f.vq_pos &&
+                        (unsigned)hy < f.vq_neg;
+      if (!fast) slow_mask |= 1ull << (z - zb);
+      NodeOut r0 = node_update_s<3, 1, 1, 0>(g, f, tab, um.x, wc.x, up.x, xm0 + wc.y, ym.x + yp.x,
+                                             za.x, zb2.x, zc2.x, 0.0, nullptr, 0);
+      NodeOut r1 = node_update_s<3, 1, 1, 0>(g, f, tab, um.y, wc.y, up.y, wc.x + xp1, ym.y + yp.y,
+                                             za.y, zb2.y, zc2.y, 0.0, nullptr, 0);
+      if (z >= zs0 && z <= zs1) {
+        if (st0) r0.o0 = fma(f.mue1, f.stim, r0.o0);
+        if (st1) r1.o0 = fma(f.mue1, f.stim, r1.o0);
+      }
+      if (valid && fast) {
+        *reinterpret_cast<double2*>(po + nn) = make_double2(r0.o1, r1.o1);
+        *reinterpret_cast<double2*>(po + 2 * nn) = make_double2(r0.o2, r1.o2);
+        *reinterpret_cast<double2*>(po + 3 * nn) = make_double2(r0.o3, r1.o3);
+        *reinterpret_cast<double2*>(pu) = make_double2(r0.o0, r1.o0);
+        nfacc = max(max(nfacc, max(nf_hi(r0.o0), nf_hi(r0.o1))), max(nf_hi(r0.o2), nf_hi(r0.o3)));
+        nfacc = max(max(nfacc, max(nf_hi(r1.o0), nf_hi(r1.o1))), max(nf_hi(r1.o2), nf_hi(r1.o3)));
+        bool track = f.last;
+        if (track) {
+          const unsigned h0 = __double2hiint(r0.o1), h1 = __double2hiint(r0.o2),
+                         h2 = __double2hiint(r0.o3), h3 = __double2hiint(r1.o1),
+                         h4 = __double2hiint(r1.o2), h5 = __double2hiint(r1.o3);
+          const unsigned hmin = min(min(min(h0, h1), min(h2, h3)), min(h4, h5));
+          const unsigned hmax = max(max(max(h0, h1), max(h2, h3)), max(h4, h5));
+          track = hmin <= tlo || hmax >= thi;
+        }
+        if (track) {
+          glo = r0.o1 < glo ? r0.o1 : glo;
+          ghi = ghi < r0.o1 ? r0.o1 : ghi;
+          glo = r0.o2 < glo ? r0.o2 : glo;
+          ghi = ghi < r0.o2 ? r0.o2 : ghi;
+          glo = r0.o3 < glo ? r0.o3 : glo;
+          ghi = ghi < r0.o3 ? r0.o3 : ghi;
+          glo = r1.o1 < glo ? r1.o1 : glo;
+          ghi = ghi < r1.o1 ? r1.o1 : ghi;
+          glo = r1.o2 < glo ? r1.o2 : glo;
+          ghi = ghi < r1.o2 ? r1.o2 : ghi;
+          glo = r1.o3 < glo ? r1.o3 : glo;
+          ghi = ghi < r1.o3 ? r1.o3 : ghi;
+        }
+      }
+      po += plane;
+      pu += plane;
+    }
+    wm = wc;
+    wc = wp;
+    vn = vn_next;
+    ev = ev_next;
+    __syncthreads();
+  }
+  // ---- events of step n (inner stage 2, outer stage, norm guard) ----
+  if (p_bad_in) atomicMin(f.event, a.code_prev + 2ull);
+  if (p_bad_out) atomicMin(f.event, a.code_prev + 3ull);
+  if (p_guard) atomicMin(f.event, a.code_prev + 4ull);
+  // ---- step n + 1: deferred planes, events, gate range (as k_node_pair) ----
+  bool bad = nfacc == 0xffffffffu;
+  if (valid && slow_mask) {  // planes deferred by the window test: per-node path
+    for (int c = 0; c < 2; ++c) {
+      const long long ipc = ip + c;
+      const double* G = f.g1;
+      const bool stc = c ? st1 : st0;
+      for (int z = zb; z < ze; ++z) {
+        if (!(slow_mask >> (z - zb) & 1ull)) continue;
+        const long long i = ipc + plane * z;
+        const XStencil sx = x_stencil(g, a, ipc, z);
+        const double stim = (stc && z >= zs0 && z <= zs1) ? f.stim : 0.0;
+        double q[4] = {0.0, 0.0, 0.0, 0.0};
+        NodeOut r;
+        if (fabs(sx.vc - f.vmid) <= f.vfast) {  // the hot loop's form (stimulus added after)
+          r = node_update_s<3, 1, 1, 0>(g, f, tab, sx.vm, sx.vc, sx.vp, sx.xs, sx.ys,
+                                        __ldg(G + nn + i), __ldg(G + 2 * nn + i),
+                                        __ldg(G + 3 * nn + i), 0.0, q, 1);
+          if (stc && z >= zs0 && z <= zs1) r.o0 = fma(f.mue1, f.stim, r.o0);
+        } else {
+          r = node_update_s<3, 1, 1, 1>(g, f, tab, sx.vm, sx.vc, sx.vp, sx.xs, sx.ys,
+                                        __ldg(G + nn + i), __ldg(G + 2 * nn + i),
+                                        __ldg(G + 3 * nn + i), stim, q, 1);
+        }
+        f.out[nn + i] = r.o1;
+        f.out[2 * nn + i] = r.o2;
+        f.out[3 * nn + i] = r.o3;
+        f.u1[i] = r.o0;
+        bad |= !finite_hi((r.o0 + r.o1) + (r.o2 + r.o3));
+        if (f.last) {
+          glo = fmin(glo, fmin(r.o1, fmin(r.o2, r.o3)));
+          ghi = fmax(ghi, fmax(r.o1, fmax(r.o2, r.o3)));
+        }
+      }
+    }
+  }
+  if (bad && !f.exex) {  // exact ordinal: inner stage 1 before the outer stage
+    const bool inner = x_inner_nonfinite(g, a, ip, zb, ze) || x_inner_nonfinite(g, a, ip + 1, zb, ze);
+    atomicMin(f.event, f.code_base + (inner ? 1ull : (unsigned long long)(f.m + 1)));
+  }
+  if (f.last) {
+    unsigned long long lo = valid && ze > zb ? ord_of(glo) : ~0ull;
+    unsigned long long hi = valid && ze > zb ? ord_of(ghi) : 0ull;
+    block_gate_range(f.gate_slot, min(lo, plo), max(hi, phi));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k_resident: a whole emrkc_run on a small grid in one cooperative launch
 // (s = m = 1). Config 1 (256^2) and the small sweep grids are launch- and
 // latency-bound one step per launch (~11 us for 65k nodes); here every
@@ -3533,6 +3941,18 @@ cudaError_t launch_node_pair(const Geom& g, const Halo& h, const FastArgs& a, co
   if (ion)
     return first ? launch_node_pair_t<1, 1>(g, h, a, tm, st) : launch_node_pair_t<0, 1>(g, h, a, tm, st);
   return first ? launch_node_pair_t<1, 0>(g, h, a, tm, st) : launch_node_pair_t<0, 0>(g, h, a, tm, st);
+}
+
+cudaError_t launch_step_x(const Geom& g, const XArgs& a, const TmaX& tm, cudaStream_t st) {
+  constexpr size_t smem = xstep_smem_bytes();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_step_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const int chunks = (g.nzl + a.f.zc - 1) / a.f.zc;
+  const dim3 grd((g.n0 + kPairTX - 1) / kPairTX, (g.n1 + kPairTY - 1) / kPairTY, chunks);
+  return launch_k(k_step_x, grd, dim3(kPairNT), smem, st, g, a, tm);
 }
 
 template <int D, int L, int F>
