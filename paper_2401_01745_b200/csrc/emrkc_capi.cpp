@@ -773,7 +773,10 @@ bool use_pair(const emrkc_handle* h) {
 // least K planes deep (min_depth: emrkc_set_slab_min_depth, or the group).
 bool use_tb(const emrkc_handle* h, const Plan& pl) {
   const int K = pl.m - 1;
-  if (!(h->tb && h->pipe == 3 && h->geom.dim == 3 && K >= 2 && K <= emrkc_k::kTbMaxK))
+  // K = 1 (m = 2: the single inner stage through k_vin_tb's lean march instead of
+  // k_vin_tma_r) only with EMRKC_TB=2 (A/B)
+  if (!(h->tb && h->pipe == 3 && h->geom.dim == 3 && K >= (h->tb >= 2 ? 1 : 2) &&
+        K <= emrkc_k::kTbMaxK))
     return false;
   return !h->partitioned || h->min_depth >= K;
 }
@@ -1327,7 +1330,7 @@ int init_handle(emrkc_handle* h) {
   if (h->pipe == 3 && !tma_supported(h)) h->pipe = 1;
   if (h->pipe != 3) h->zc = std::min(h->zc, emrkc_k::kMaxZcPipe);
   if (const char* tb = std::getenv("EMRKC_TB"))
-    if (*tb) h->tb = std::atoi(tb) != 0;
+    if (*tb) h->tb = std::max(0, std::min(2, std::atoi(tb)));
   if (const char* xs = std::getenv("EMRKC_XSTEP"))
     if (*xs) h->xstep = std::atoi(xs) != 0;
   if (const char* pr = std::getenv("EMRKC_PAIR"))

@@ -2859,7 +2859,7 @@ static_assert(kTbTY % 2 == 0 && tb_hx(kTbMaxK) >= kTbMaxK, "k_vin_tb tile");
 template <int K>
 constexpr size_t tb_smem_bytes() { return sizeof(double) * TbTile<K>::total() + 128; }
 template <int K>
-constexpr int tb_min_blocks() { return K == 2 ? 3 : (K == 3 ? 2 : 1); }
+constexpr int tb_min_blocks() { return K == 1 ? 4 : (K == 2 ? 3 : (K == 3 ? 2 : 1)); }
 
 // Compile-time loop: f(integral_constant<int, i>) for i in [B, E).
 template <int B, int E, typename F>
@@ -2912,9 +2912,10 @@ struct TbCtx {
 };
 template <int K>
 struct TbState {
-  // column windows: D[c][i] = d_1 at plane s - K + i; W[c][k - 2][i] = stage k
-  // at plane (s - k + 1) - 2 + i, k = 2..K
-  double D[2][K + 1], W[2][K > 1 ? K - 1 : 1][3];
+  // column windows: D[c][i] = d_1 at plane s - (DW - 1) + i; W[c][k - 2][i] =
+  // stage k at plane (s - k + 1) - 2 + i, k = 2..K
+  static constexpr int DW = K + 1 > 3 ? K + 1 : 3;  // d_1 planes kept per column
+  double D[2][DW], W[2][K > 1 ? K - 1 : 1][3];
   unsigned acc[K + 2];  // per stage: all ones once an owned value was non-finite
   unsigned acc_o;
   bool guard;
@@ -2929,6 +2930,7 @@ __device__ __forceinline__ void tb_step(const Geom& g, const Halo& h, const TbAr
                                         const TbCtx& c, TbState<K>& st, const int s) {
   using T = TbTile<K>;
   constexpr int M = K + 1;
+  constexpr int DW = TbState<K>::DW;
   const int i = s - c.lo1;
   const int ph = EDGE ? (i & 3) : PH;
   // V of g_{j-1} / g_{j-2} for the final stage's plane, early
@@ -2944,8 +2946,9 @@ __device__ __forceinline__ void tb_step(const Geom& g, const Halo& h, const TbAr
 #pragma unroll
   for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-    for (int q = 0; q < K; ++q) st.D[cc][q] = st.D[cc][q + 1];
-  if (has_d) lds2<EDGE ? -1 : T::ring_off(PH)>(c.aC, T::ring_off(1) * ph, st.D[0][K], st.D[1][K]);
+    for (int q = 0; q < DW - 1; ++q) st.D[cc][q] = st.D[cc][q + 1];
+  if (has_d)
+    lds2<EDGE ? -1 : T::ring_off(PH)>(c.aC, T::ring_off(1) * ph, st.D[0][DW - 1], st.D[1][DW - 1]);
   // In-plane neighbours of stage k: d_1 of plane s - 1 (k = 2) or the plane
   // stage k - 1 published one step ago. The loads of stage k + 1 are issued
   // before stage k computes (every plane read here was published before the
@@ -2985,9 +2988,9 @@ __device__ __forceinline__ void tb_step(const Geom& g, const Halo& h, const TbAr
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
         if constexpr (k == 2) {
-          z0[cc] = st.D[cc][K - 2];
-          z1[cc] = st.D[cc][K - 1];
-          z2[cc] = st.D[cc][K];
+          z0[cc] = st.D[cc][DW - 3];
+          z1[cc] = st.D[cc][DW - 2];
+          z2[cc] = st.D[cc][DW - 1];
         } else {
           z0[cc] = st.W[cc][k - 3][0];
           z1[cc] = st.W[cc][k - 3][1];
@@ -3003,7 +3006,7 @@ __device__ __forceinline__ void tb_step(const Geom& g, const Halo& h, const TbAr
         double L = fma(g.wc, vc, g.w[2] * (z0[cc] + z2[cc]));
         L = fma(g.w[0], xs[cc], L);
         L = fma(g.w[1], n[cc] + n[2 + cc], L);
-        const double d1c = st.D[cc][K - (k - 1)];
+        const double d1c = st.D[cc][DW - k];
         double bs = nu * vc;
         if constexpr (k == 3) bs = fma(nu, vc, kappa * d1c);
         if constexpr (k >= 4) bs = fma(nu, vc, kappa * st.W[cc][k >= 4 ? k - 4 : 0][0]);
@@ -3132,7 +3135,7 @@ __global__ void __launch_bounds__(TbTile<K>::NT, tb_min_blocks<K>())
 #pragma unroll
   for (int cc = 0; cc < 2; ++cc) {
 #pragma unroll
-    for (int q = 0; q <= K; ++q) st.D[cc][q] = 0.0;
+    for (int q = 0; q < TbState<K>::DW; ++q) st.D[cc][q] = 0.0;
 #pragma unroll
     for (int k = 0; k < K - 1; ++k) st.W[cc][k][0] = st.W[cc][k][1] = st.W[cc][k][2] = 0.0;
   }
@@ -3842,6 +3845,7 @@ cudaError_t launch_vin_tb(const Geom& g, const Halo& h, const TbArgs& a, const T
                           cudaStream_t st) {
   const bool first = a.j == 1;
   switch (a.m - 1) {
+    case 1: return first ? launch_vin_tb_t<1, 1>(g, h, a, tm, st) : launch_vin_tb_t<1, 0>(g, h, a, tm, st);
     case 2: return first ? launch_vin_tb_t<2, 1>(g, h, a, tm, st) : launch_vin_tb_t<2, 0>(g, h, a, tm, st);
     case 3: return first ? launch_vin_tb_t<3, 1>(g, h, a, tm, st) : launch_vin_tb_t<3, 0>(g, h, a, tm, st);
     case 4: return first ? launch_vin_tb_t<4, 1>(g, h, a, tm, st) : launch_vin_tb_t<4, 0>(g, h, a, tm, st);
@@ -3872,7 +3876,7 @@ static int tb_slots() {
 }
 
 int tb_zc(const Geom& g, int K) {
-  const int slots = K == 2 ? tb_slots<2>() : (K == 3 ? tb_slots<3>() : tb_slots<4>());
+  const int slots = K == 1 ? tb_slots<1>() : (K == 2 ? tb_slots<2>() : (K == 3 ? tb_slots<3>() : tb_slots<4>()));
   const long long tiles = halo_signals_tb(g);
   const int nz = g.nzl;
   int best_zc = nz;
