@@ -2047,19 +2047,23 @@ __global__ void __launch_bounds__(kPairNT, 3)
   double2 wm = make_double2(0.0, 0.0), wc = make_double2(0.0, 0.0);  // W(z - 1), W(z)
   double* po = f.out + ip + plane * zb;   // gates of y_{n+2}
   double* pu = f.u1 + ip + plane * zb;    // d_1 of step n + 1
-  // V_n of the pairs one plane ahead (global loads, a whole iteration of latency)
+  // V_n of the pairs two planes ahead (global loads: under load their latency
+  // exceeds one iteration)
   const double2 zero2 = make_double2(0.0, 0.0);
-  double2 vn = valid ? __ldg(reinterpret_cast<const double2*>(a.vn + ip + plane * w0)) : zero2;
-  double2 ev = (qe.on && w0 >= zb) ? __ldg(reinterpret_cast<const double2*>(a.vn + qe.gi + plane * w0)) : zero2;
+  auto ld_vn = [&](int w) {
+    return (valid && w <= w1) ? __ldg(reinterpret_cast<const double2*>(a.vn + ip + plane * w)) : zero2;
+  };
+  auto ld_ev = [&](int w) {
+    return (qe.on && w >= zb && w < ze && w <= w1)
+               ? __ldg(reinterpret_cast<const double2*>(a.vn + qe.gi + plane * w))
+               : zero2;
+  };
+  double2 vn = ld_vn(w0), ev = ld_ev(w0);
+  double2 vn1 = ld_vn(w0 + 1), ev1 = ld_ev(w0 + 1);
   for (int w = w0; w <= ze; ++w) {
     const int it = w - w0;
     if (t == 0 && w + kXLA <= ze) issue_group(w + kXLA, 0);
-    double2 vn_next = zero2, ev_next = zero2;
-    if (w + 1 <= w1) {
-      if (valid) vn_next = __ldg(reinterpret_cast<const double2*>(a.vn + ip + plane * (w + 1)));
-      if (qe.on && w + 1 >= zb && w + 1 < ze)
-        ev_next = __ldg(reinterpret_cast<const double2*>(a.vn + qe.gi + plane * (w + 1)));
-    }
+    const double2 vn2 = ld_vn(w + 2), ev2 = ld_ev(w + 2);
     if (it > 0) mbar_wait(b0 + 8u * (it & 7), (it >> 3) & 1);
     // ---- producer: W(w) ----
     double2 wp = make_double2(0.0, 0.0);
@@ -2154,8 +2158,10 @@ __global__ void __launch_bounds__(kPairNT, 3)
     }
     wm = wc;
     wc = wp;
-    vn = vn_next;
-    ev = ev_next;
+    vn = vn1;
+    ev = ev1;
+    vn1 = vn2;
+    ev1 = ev2;
     __syncthreads();
   }
   // ---- events of step n (inner stage 2, outer stage, norm guard) ----
