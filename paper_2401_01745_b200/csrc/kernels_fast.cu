@@ -2926,6 +2926,7 @@ struct TbState {
   unsigned acc_o;
   bool guard;
   long long go;         // final-stage output offset of the step
+  double2 v1n, v2n;     // V of g_{j-1} / g_{j-2} of the NEXT step's output plane (prefetched)
 };
 
 // One march step at ring phase (s - lo1) & 3 (PH, compile time, when
@@ -2939,13 +2940,26 @@ __device__ __forceinline__ void tb_step(const Geom& g, const Halo& h, const TbAr
   constexpr int DW = TbState<K>::DW;
   const int i = s - c.lo1;
   const int ph = EDGE ? (i & 3) : PH;
-  // V of g_{j-1} / g_{j-2} for the final stage's plane, early
+  // V of g_{j-1} / g_{j-2} for the final stage's plane: loaded one step ahead
+  // (under load the global-load latency exceeds a step; K = 2: +3%, K = 4:
+  // +11%), except for K = 3, whose 72-register budget (two blocks per SM)
+  // has no room for the carried values (spills: -10%) and loads them at the
+  // start of the step they are used in.
   const int qo = s - K;
-  const bool outp = !EDGE || (qo >= c.zb && qo < c.ze);
-  double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
-  if (c.own && outp) {
-    v1 = __ldg(reinterpret_cast<const double2*>(a.g1v + st.go));
-    if (!FIRST) v2 = __ldg(reinterpret_cast<const double2*>(a.g2v + st.go));
+  double2 v1, v2;
+  if constexpr (K != 3) {
+    v1 = st.v1n;
+    v2 = st.v2n;
+    if (c.own && qo + 1 >= c.zb && qo + 1 < c.ze) {
+      st.v1n = __ldg(reinterpret_cast<const double2*>(a.g1v + st.go + c.plane));
+      if (!FIRST) st.v2n = __ldg(reinterpret_cast<const double2*>(a.g2v + st.go + c.plane));
+    }
+  } else {
+    v1 = v2 = make_double2(0.0, 0.0);
+    if (c.own && (!EDGE || (qo >= c.zb && qo < c.ze))) {
+      v1 = __ldg(reinterpret_cast<const double2*>(a.g1v + st.go));
+      if (!FIRST) v2 = __ldg(reinterpret_cast<const double2*>(a.g2v + st.go));
+    }
   }
   const bool has_d = !EDGE || s < c.hi1;
   if (has_d) mbar_wait(c.b0 + 8u * ph, (i >> 2) & 1);
@@ -3138,6 +3152,7 @@ __global__ void __launch_bounds__(TbTile<K>::NT, tb_min_blocks<K>())
   for (int k = 0; k <= M; ++k) st.acc[k] = 0u;
   st.acc_o = 0u;
   st.guard = false;
+  st.v1n = st.v2n = make_double2(0.0, 0.0);
 #pragma unroll
   for (int cc = 0; cc < 2; ++cc) {
 #pragma unroll
