@@ -999,10 +999,11 @@ int launch_level(emrkc_handle* h, StepCtx* c, int j, int k) {
         // pair-per-thread node kernel (3-D, HH proper)
         emrkc_k::TmaNode tm;
         std::memset(&tm, 0, sizeof tm);
-        int rc = tma_map(h, f.g1, kTmaHalo, &tm.v, 1, emrkc_k::kPairXMul);
-        if (!rc) rc = tma_map(h, f.g1, kTmaGates, &tm.gates, 1, emrkc_k::kPairXMul);
-        if (!rc && f.g2) rc = tma_map(h, f.g2, kTmaAll, &tm.g2, 1, emrkc_k::kPairXMul);
-        if (!rc) rc = tma_ghosts(h, hl, &tm.glo, &tm.ghi, 1, emrkc_k::kPairXMul);
+        const int xm = emrkc_k::pair_tx(h->geom) / emrkc_k::kTX3, rm = 2 / xm;  // 64 x 4 or 32 x 8
+        int rc = tma_map(h, f.g1, kTmaHalo, &tm.v, rm, xm);
+        if (!rc) rc = tma_map(h, f.g1, kTmaGates, &tm.gates, rm, xm);
+        if (!rc && f.g2) rc = tma_map(h, f.g2, kTmaAll, &tm.g2, rm, xm);
+        if (!rc) rc = tma_ghosts(h, hl, &tm.glo, &tm.ghi, rm, xm);
         if (rc) return rc;
         f.zc = pzc;
         CK(h, emrkc_k::launch_node_pair(h->geom, hn, f, tm, pl.m >= 2, lstream(h)));
@@ -1198,7 +1199,7 @@ int enqueue_step_zpipe(emrkc_handle* h, double t, long long step_in_run,
 bool use_xstep(emrkc_handle* h, const Plan& pl, int64_t nsteps) {
   return h->xstep && use_pair(h) && !h->partitioned && !h->level_hook && h->zr_lo < 0 &&
          pl.s == 1 && pl.m == 2 && pl.method != kMethodMrkc && !pl.exex && pl.gate_c == 1.0 &&
-         nsteps >= 2 && !use_fused(h, pl) && !use_zpipe(h, pl) &&
+         nsteps >= 2 && !use_fused(h, pl) && !use_zpipe(h, pl) && emrkc_k::pair_tx(h->geom) == 64 &&
          emrkc_k::pair_zc(h->geom, true, h->pair == 2) > 0;
 }
 

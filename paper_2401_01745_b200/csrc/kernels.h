@@ -326,7 +326,8 @@ cudaError_t launch_node_tma(const Geom& g, const Halo& h, const FastArgs& a,
 // 64 x 4 tiles (tm.v: (68, 6, 1), tm.gates: (64, 4, 1, 3), tm.g2: (64, 4, 1,
 // 4), ghost planes (68, 6)). pair_zc: its z-chunk, 0 if the grid gives too few
 // blocks (the caller keeps k_node_tma) unless forced (tests).
-constexpr int kPairXMul = 2;  // tile width in units of kTX3
+constexpr int kPairXMul = 2;  // k_step_x: tile width in units of kTX3
+int pair_tx(const Geom& g);    // k_node_pair tile width on this grid: 64 (x 4 rows) or 32 (x 8 rows)
 int pair_zc(const Geom& g, bool first, bool force);
 cudaError_t launch_node_pair(const Geom& g, const Halo& h, const FastArgs& a, const TmaNode& tm,
                              bool ion, cudaStream_t st);

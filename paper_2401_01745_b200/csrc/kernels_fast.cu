@@ -1509,20 +1509,30 @@ constexpr int kPairVT = kPairHX * kPairHY;
 constexpr int kPairVS = (kPairVT + 15) & ~15;
 constexpr int kPairCS = kPairTX * kPairTY;  // cells of one centre field
 
-template <int FIRST>
+// Tile shapes of k_node_pair: 64 x 4 (a warp per row) or 32 x 8 (half a warp
+// per row) for grids whose width wastes fewer lanes in 32-wide tiles
+// (n0 = 200: 224 / 200 against 256 / 200 columns).
+template <int TXW>
+struct PairTile {
+  static constexpr int TX = TXW, TY = kPairNT * 2 / TXW, PPR = TXW / 2;  // pairs per row
+  static constexpr int HX = TX + 4, HY = TY + 2;                         // V box (x0 - 2, y0 - 1)
+  static constexpr int VT = HX * HY, VS = (VT + 15) & ~15, CS = TX * TY;
+};
+template <int FIRST, int TXW>
 constexpr size_t pair_smem_bytes() {
-  return sizeof(double) * (kRV * kPairVS + kRG * 3 * kPairCS + (FIRST ? 0 : kRG * 4 * kPairCS)) +
-         128;
+  using P = PairTile<TXW>;
+  return sizeof(double) * (kRV * P::VS + kRG * 3 * P::CS + (FIRST ? 0 : kRG * 4 * P::CS)) + 128;
 }
 
 __device__ __forceinline__ unsigned nf_hi(double v) {
   return (unsigned)__double2hiint(v) | 0x800fffffu;
 }
 
-template <int FIRST, int ION>
+template <int FIRST, int ION, int TXW>
 __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
     k_node_pair(const Geom g, const Halo h, const FastArgs a, const __grid_constant__ TmaNode tm) {
-  constexpr int VS = kPairVS, CS = kPairCS, HXT = kPairHX;
+  using P = PairTile<TXW>;
+  constexpr int VS = P::VS, CS = P::CS, HXT = P::HX;
   extern __shared__ __align__(128) double smem_tma[];
   double* vst = smem_tma + ((128u - (smem_u32(smem_tma) & 127u)) & 127u) / 8;  // [kRV][VS]
   double* gst = vst + kRV * VS;        // [kRG][3][CS]
@@ -1542,15 +1552,15 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
     if (!FIRST) prefetch_tensormap(&tm.g2);
   }
   __syncthreads();
-  const int px = t & 31, ty = t >> 5;
-  const int x0 = blockIdx.x * kPairTX, y0 = blockIdx.y * kPairTY;
+  const int px = t % P::PPR, ty = t / P::PPR;
+  const int x0 = blockIdx.x * P::TX, y0 = blockIdx.y * P::TY;
   const int cx = x0 + 2 * px, cy = y0 + ty;  // cell 0; cell 1 = (cx + 1, cy)
   const bool valid = cx < g.n0 && cy < g.n1;  // n0 is even: both cells or none
   const long long ip = valid ? (long long)cx + (long long)g.n0 * cy : 0;
   const long long nn = g.nn, plane = g.plane;
   const unsigned v0 = smem_u32(vst), gs0 = smem_u32(gst), qs0 = smem_u32(g2s);
   const unsigned b0 = smem_u32(bars);
-  constexpr unsigned vbytes = 8u * kPairVT;
+  constexpr unsigned vbytes = 8u * P::VT;
   constexpr unsigned cbytes = 8u * CS * (3 + (FIRST ? 0 : 4));
   auto issue_comp = [&](int zz) {  // thread 0: plane zz in [zb, ze)
     const int q = zz - zb + 1;
@@ -1571,7 +1581,8 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
   };
   // a block stands for its 32-wide tiles in the neighbours' arrival counts
   // (halo_signals_pipe counts 32 x 4 tiles whatever kernel stores the planes)
-  const int sigw = 1 + (x0 + kTX3 < g.n0 ? 1 : 0);
+  const int sigw = (P::TX > kTX3 ? 1 + (x0 + kTX3 < g.n0 ? 1 : 0) : 1) *
+                   (P::TY > kTY3 ? 1 + (y0 + kTY3 < g.n1 ? 1 : 0) : 1);
   pdl_wait();
   halo_wait(h, zb == 0, ze >= g.nzl);
   if (t == 0) {
@@ -1602,7 +1613,7 @@ __global__ void __launch_bounds__(kPairNT, FIRST ? 4 : 2)
   const int cell = (ty + 1) * HXT + 2 * px + 2;
   const int cxm = cell + (cx > 0 ? -1 : 1), cxp = cell + 1 + (cx + 1 < g.n0 - 1 ? 1 : -1);
   const int cym = cell + (cy > 0 ? -HXT : HXT), cyp = cell + (cy < g.n1 - 1 ? HXT : -HXT);
-  const int gcell = ty * kPairTX + 2 * px;  // the pair in a centre field
+  const int gcell = ty * P::TX + 2 * px;  // the pair in a centre field
   int zs0 = 1, zs1 = 0;
   const bool st0 = valid && stim_col_xy<3>(g, cx, cy), st1 = valid && stim_col_xy<3>(g, cx + 1, cy);
   if (st0 || st1) {
@@ -3933,10 +3944,21 @@ cudaError_t launch_node_tma(const Geom& g, const Halo& h, const FastArgs& a, con
 
 // k_node_pair (3-D, whole grid, HH proper): z-chunk for 64 x 4 tiles at 4
 // (FIRST) / 2 resident blocks per SM, same 1.7-wave floor as fast_zc.
+// Tile width of k_node_pair on this grid: 32 x 8 tiles when they waste at
+// least 5% fewer lanes than 64 x 4 tiles (EMRKC_PAIR_TX: 32 / 64, experiments).
+int pair_tx(const Geom& g) {
+  if (const char* e = std::getenv("EMRKC_PAIR_TX"))
+    if (*e) return std::atoi(e) == 32 ? 32 : 64;
+  const double c64 = (double)((g.n0 + 63) / 64 * 64) * ((g.n1 + 3) / 4 * 4);
+  const double c32 = (double)((g.n0 + 31) / 32 * 32) * ((g.n1 + 7) / 8 * 8);
+  return c32 * 1.05 <= c64 ? 32 : 64;
+}
+
 int pair_zc(const Geom& g, bool first, bool force) {
   if (const char* e = std::getenv("EMRKC_PAIR_ZC"))  // experiments
     if (*e) return std::max(1, std::min(std::atoi(e), std::min(g.nzl, kMaxZc)));
-  const long long tiles = (long long)((g.n0 + kPairTX - 1) / kPairTX) * ((g.n1 + kPairTY - 1) / kPairTY);
+  const int tx = pair_tx(g), ty = kPairNT * 2 / tx;
+  const long long tiles = (long long)((g.n0 + tx - 1) / tx) * ((g.n1 + ty - 1) / ty);
   const int slots = sm_count() * (first ? 4 : 2);
   // fewer blocks than one wave of slots: k_node_tma's smaller tiles fill the GPU better
   if (!force && tiles * ((g.nzl + 3) / 4) < slots) return 0;
@@ -3946,26 +3968,37 @@ int pair_zc(const Geom& g, bool first, bool force) {
   return zc_model(g.nzl, tiles, slots, 3.75);
 }
 
-template <int F, int I>
+template <int F, int I, int TXW>
 static cudaError_t launch_node_pair_t(const Geom& g, const Halo& h, const FastArgs& a,
                                       const TmaNode& tm, cudaStream_t st) {
-  constexpr size_t smem = pair_smem_bytes<F>();
+  using P = PairTile<TXW>;
+  constexpr size_t smem = pair_smem_bytes<F, TXW>();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_node_pair<F, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_node_pair<F, I, TXW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = true;
   }
   const int chunks = (a.z_hi - a.z_lo + a.zc - 1) / a.zc;
-  const dim3 grd((g.n0 + kPairTX - 1) / kPairTX, (g.n1 + kPairTY - 1) / kPairTY, chunks);
-  return launch_k(k_node_pair<F, I>, grd, dim3(kPairNT), smem, st, g, h, a, tm);
+  const dim3 grd((g.n0 + P::TX - 1) / P::TX, (g.n1 + P::TY - 1) / P::TY, chunks);
+  return launch_k(k_node_pair<F, I, TXW>, grd, dim3(kPairNT), smem, st, g, h, a, tm);
+}
+
+template <int TXW>
+static cudaError_t launch_node_pair_w(const Geom& g, const Halo& h, const FastArgs& a,
+                                      const TmaNode& tm, bool ion, cudaStream_t st) {
+  const bool first = a.j == 1;
+  if (ion)
+    return first ? launch_node_pair_t<1, 1, TXW>(g, h, a, tm, st)
+                 : launch_node_pair_t<0, 1, TXW>(g, h, a, tm, st);
+  return first ? launch_node_pair_t<1, 0, TXW>(g, h, a, tm, st)
+               : launch_node_pair_t<0, 0, TXW>(g, h, a, tm, st);
 }
 
 cudaError_t launch_node_pair(const Geom& g, const Halo& h, const FastArgs& a, const TmaNode& tm,
                              bool ion, cudaStream_t st) {
-  const bool first = a.j == 1;
-  if (ion)
-    return first ? launch_node_pair_t<1, 1>(g, h, a, tm, st) : launch_node_pair_t<0, 1>(g, h, a, tm, st);
-  return first ? launch_node_pair_t<1, 0>(g, h, a, tm, st) : launch_node_pair_t<0, 0>(g, h, a, tm, st);
+  return pair_tx(g) == 32 ? launch_node_pair_w<32>(g, h, a, tm, ion, st)
+                          : launch_node_pair_w<64>(g, h, a, tm, ion, st);
 }
 
 cudaError_t launch_step_x(const Geom& g, const XArgs& a, const TmaX& tm, cudaStream_t st) {
