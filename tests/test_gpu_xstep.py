@@ -36,6 +36,7 @@ def state(oracle, p, seed=0, slow=True):
 def run(p, y0, n, xs, monkeypatch, rF, rS, follow=0):
     monkeypatch.setenv("EMRKC_XSTEP", str(xs))
     monkeypatch.setenv("EMRKC_PAIR", "2")
+    monkeypatch.setenv("EMRKC_PAIR_TX", "64")  # k_step_x works on 64 x 4 tiles
     op = MonodomainOperator(p)
     op.set_state(y0)
     res = op.run(0, n, 0.05, rF, rS).as_dict()
@@ -100,6 +101,7 @@ def test_xstep_timed_form(oracle, monkeypatch):
     y0 = state(oracle, p, 5)
     monkeypatch.setenv("EMRKC_XSTEP", "1")
     monkeypatch.setenv("EMRKC_PAIR", "2")
+    monkeypatch.setenv("EMRKC_PAIR_TX", "64")
     lib = capi.load()
     op = MonodomainOperator(p)
     op.set_state(y0)
