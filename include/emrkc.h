@@ -209,7 +209,7 @@ int emrkc_set_state(emrkc_handle* h, const double* y, int64_t len);
 int emrkc_get_state(emrkc_handle* h, double* y, int64_t len);
 /* Kernel plan of the handle's current step plan (after a step / run):
  * 1 when one step runs as the single fused pass (k_fused2: s = 1, m = 2,
- * 3-D whole grid, EMRKC_FUSED=1), 2 when it runs z-pipelined (node-kernel
+ * 3-D whole grid, EMRKC_FUSED=1 on a -DEMRKC_EXPERIMENTAL=1 build), 2 when it runs z-pipelined (node-kernel
  * chunks on the handle's stream, inner-stage chunks overlapping them on a
  * second stream, EMRKC_ZPIPE=K chunks), 3 when run loops fuse inner stage 2
  * of step n with the node update of step n + 1 (k_step_x, EMRKC_XSTEP=1), 0 when it runs as one launch per

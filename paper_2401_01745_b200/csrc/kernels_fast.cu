@@ -3276,6 +3276,7 @@ dim3 fgrid(const Geom& g, int zc) {
   return dim3((g.nzl + kFThreads - 1) / kFThreads, 1, 1);
 }
 
+#if EMRKC_EXPERIMENTAL  // k_fused2: measured slower than the two-kernel step
 // ---------------------------------------------------------------------------
 // k_fused2: a whole emRKC step with s = 1, m = 2 in ONE pass over HBM (3-D,
 // whole grid): the node update (exponential Euler of the gates, f_S(y_E),
@@ -3621,6 +3622,7 @@ __global__ void __launch_bounds__(kFuNT, 2)
     }
   }
 }
+#endif  // EMRKC_EXPERIMENTAL (k_fused2)
 
 }  // namespace
 
@@ -4133,6 +4135,7 @@ cudaError_t launch_vin_fast(const Geom& g, const Halo& h, const FastInnerArgs& a
 }
 
 
+#if EMRKC_EXPERIMENTAL
 // Fused s = 1, m = 2 step: resident blocks per SM of k_fused2 (0 if it
 // cannot run) and the cooperative launch.
 int fused_blocks_per_sm() {
@@ -4162,5 +4165,14 @@ cudaError_t launch_fused2(const Geom& g, const FusedArgs& a, const TmaFused& tm,
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_fused2, g, a, tm);
 }
+
+#else
+// k_fused2 is compiled only with -DEMRKC_EXPERIMENTAL=1 (EMRKC_FUSED=1 then
+// keeps the two-kernel step).
+int fused_blocks_per_sm() { return 0; }
+cudaError_t launch_fused2(const Geom&, const FusedArgs&, const TmaFused&, cudaStream_t) {
+  return cudaErrorNotSupported;
+}
+#endif
 
 }  // namespace emrkc_k

@@ -18,6 +18,33 @@ pytestmark = pytest.mark.gpu
 H = 0.1
 
 
+@pytest.fixture(scope="module", autouse=True)
+def _needs_k_fused2():
+    """k_fused2 is measured slower than the two-kernel step and compiled only
+    with -DEMRKC_EXPERIMENTAL=1 (tools/build_variant.sh exp
+    -DEMRKC_EXPERIMENTAL=1; EMRKC_LIB=build_var/lib_exp.so): skip without it."""
+    import os
+
+    old = os.environ.get("EMRKC_FUSED")
+    os.environ["EMRKC_FUSED"] = "1"
+    try:
+        lo, hi = [-0.05] * 3, [0.75] * 3
+        p = make_problem(3, [256, 192, 40], [H] * 3, [0.3, 0.1, 0.1], 140.0, 0.01, 70.0, lo, hi,
+                         0.0, 1.0)
+        op = MonodomainOperator(p)
+        op.set_state(op.initial_state())
+        op.run(0, 1, 0.05, 60.0, 0.7)
+        active = capi.load().emrkc_fused_active(op.handle)
+        op.close()
+    finally:
+        if old is None:
+            os.environ.pop("EMRKC_FUSED", None)
+        else:
+            os.environ["EMRKC_FUSED"] = old
+    if active != 1:
+        pytest.skip("k_fused2 not built (-DEMRKC_EXPERIMENTAL=1)")
+
+
 def grid(nx, ny, nz, sigma=(0.3, 0.1, 0.1), stim_lo=(10, 12, 3), stim_hi=(17, 19, 8)):
     lo = [(i - 0.5) * H for i in stim_lo]
     hi = [(i + 0.5) * H for i in stim_hi]
